@@ -1,0 +1,175 @@
+/*
+ * clomp_b200.h — C-ABI of the B200-native CLOMP reconstruction loop.
+ *
+ * Drop-in boundary for the reference's hot path.  The reference
+ * exposes a static C++ API, not an FFI; each entry point below says which
+ * reference function it replaces.  Plain pointers and sizes only: no torch, no
+ * C++ types.  The C++ shim (paper_2501_11592_b200/csrc/shim/cskit_clomp_shim.cpp)
+ * re-exposes these under the reference's own signatures, and INTEGRATION.md
+ * shows the bindings.
+ *
+ * Numeric contract
+ *   * Operands A and y are fp32 (north star).  Every product and reduction on
+ *     the learning path is carried in fp64; correlations run on the tensor
+ *     cores (3xTF32) and every selection whose top-2 gap is inside the error
+ *     bound of that GEMM is re-decided from fp64 scores.  Supports therefore
+ *     match the fp64 reference (clomp.cpp:211-292) and coefficients agree to
+ *     ~1e-12 relative.
+ *   * Priors (w_tv/w_lv > 0 after resolve_weights, clomp.cpp:131-140) are not
+ *     implemented: CL_ERR_UNSUPPORTED, never a CPU fallback.
+ *
+ * Threading: one context per host thread; calls on distinct contexts may run
+ * concurrently.  A context owns one device, one stream and its workspace.
+ */
+#ifndef CLOMP_B200_H
+#define CLOMP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_ABI_VERSION 1
+
+/* Status codes.  2/3/4 are the reference's CLI exit codes for ConfigError,
+ * DimensionError and NumericalError (errors.hpp:10-37, cskit.cpp:1074-1093). */
+typedef enum cl_status {
+  CL_OK = 0,
+  CL_ERR_INTERNAL = 1,
+  CL_ERR_CONFIG = 2,       /* cskit::ConfigError    (clomp.cpp:18-30)          */
+  CL_ERR_DIMENSION = 3,    /* cskit::DimensionError (clomp.cpp:215-218)        */
+  CL_ERR_NUMERICAL = 4,    /* cskit::NumericalError (clomp.cpp:255-256)        */
+  CL_ERR_UNSUPPORTED = 5,  /* priors on                                        */
+  CL_ERR_CUDA = 6,         /* CUDA runtime / no device / extension missing     */
+  CL_ERR_CAPACITY = 7      /* support grew past the per-signal capacity        */
+} cl_status;
+
+/* Optimizers (clomp.hpp:14, gradient_step clomp.cpp:171-209). */
+enum { CL_OPT_PLAIN = 0, CL_OPT_MOMENTUM = 1, CL_OPT_ADAM = 2 };
+
+/* Solve semantics.
+ *   JOINT      = clomp_solve_batch (clomp.cpp:211-292): batch-global eps test,
+ *                mask_changed, stall counter and best iterate.
+ *   PER_SIGNAL = clomp_solve (clomp.cpp:294-311) on every column: the CLI's
+ *                per-signal loop (cskit.cpp:543-551).  Columns never interact,
+ *                which is what lets batches shard across GPUs with no traffic. */
+enum { CL_MODE_JOINT = 0, CL_MODE_PER_SIGNAL = 1 };
+
+/* Layouts.  REF = the reference's la::Mat row-major (A: m x n, y: m x B,
+ * linalg.hpp:12-29).  T = transposed (A atom-major n x m, y signal-major B x m). */
+enum { CL_LAYOUT_REF = 0, CL_LAYOUT_T = 1 };
+
+/* ClompConfig (clomp.hpp:16-33), same field order and meaning. */
+typedef struct cl_config {
+  double th;                /* injection threshold in (0, 1]               */
+  uint64_t max_outer;       /* outer iterations                            */
+  double eps;               /* stop when ||r|| < eps                       */
+  uint64_t inner_steps;     /* optimizer steps per outer iteration         */
+  double lr;                /* step size; the gradient is 2 A^T r          */
+  int32_t opt;              /* CL_OPT_*                                    */
+  int32_t pad0;
+  double w_tv;              /* negative = auto 0.01*mean(y^2); 0 = off     */
+  double w_lv;
+  uint64_t lv_window;       /* LvParams (priors.hpp:22-25)                 */
+  uint64_t lv_stride;
+  double stall_tol;
+  uint64_t stall_patience;
+} cl_config;
+
+/* The reference defaults (clomp.hpp:16-33): th 0.7, max_outer 200, eps 1e-6,
+ * inner 50, lr 0.01, Adam, auto priors, LvParams{3,2}, stall 1e-4 x 2. */
+void cl_config_default(cl_config* cfg);
+
+/* Results, caller-owned host buffers.  NULL pointers are skipped.
+ * `cap` is the per-signal length of support/coef.  The support of signal b is
+ * support[b*cap .. b*cap+count[b]) in ascending atom order with coef aligned. */
+typedef struct cl_result {
+  int64_t cap;
+  int32_t* support;             /* [B][cap]                                */
+  double* coef;                 /* [B][cap]                                */
+  int32_t* count;               /* [B]                                     */
+  double* s;                    /* dense n x B, REF layout (BatchSolveResult::s)   */
+  uint8_t* mask;                /* dense n x B, REF layout (BatchSolveResult::mask) */
+  int64_t* iterations;          /* [B]  (JOINT: identical)                 */
+  double* final_residual_norm;  /* [B]  (JOINT: the batch Frobenius norm)  */
+  uint8_t* converged;           /* [B]                                     */
+  int32_t* status;              /* [B]  cl_status per signal               */
+} cl_result;
+
+typedef struct cl_ctx cl_ctx;
+
+/* Upload the dictionary once.  Replaces the per-call LossOps transpose
+ * (clomp.cpp:57-66, 224): A is stored atom-major fp32 in HBM.
+ * a: host pointer, m x n (CL_LAYOUT_REF) or n x m (CL_LAYOUT_T).
+ * Returns NULL on failure with *status set (cl_last_error(NULL) explains). */
+cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
+                  int a_layout, int* status);
+void cl_destroy(cl_ctx* ctx);
+
+/* Message of the last failing call on ctx (or of the last failing cl_create
+ * on this thread when ctx is NULL). */
+const char* cl_last_error(const cl_ctx* ctx);
+
+/* Replaces clomp_solve_batch (clomp.cpp:211-292) and, with batch == 1,
+ * clomp_solve (clomp.cpp:294-311).  Host buffers; blocking.
+ * y: m x B (CL_LAYOUT_REF) or B x m (CL_LAYOUT_T).
+ * Returns the call status: JOINT -> the exception the reference would throw;
+ * PER_SIGNAL -> CL_OK unless the call itself is invalid (per-signal failures
+ * are in out->status). */
+int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
+                   const cl_config* cfg, int mode, cl_result* out);
+
+/* Device-resident variant for throughput: d_y is a device pointer, signal-major
+ * B x m fp32 (leading dimension m).  Results are written to device buffers
+ * (any may be NULL): support/coef [B][cap], count/iterations(int32)/
+ * final_rn/converged/status [B].  Asynchronous on the context stream; call
+ * cl_synchronize before reading. */
+typedef struct cl_device_result {
+  int64_t cap;
+  int32_t* support;
+  double* coef;
+  int32_t* count;
+  int32_t* iterations;
+  double* final_residual_norm;
+  uint8_t* converged;
+  int32_t* status;
+} cl_device_result;
+int cl_solve_batch_device(cl_ctx* ctx, const float* d_y, int64_t batch,
+                          const cl_config* cfg, int mode,
+                          const cl_device_result* out);
+int cl_synchronize(cl_ctx* ctx);
+
+/* Replaces inject_support (clomp.cpp:142-154): mask |= { j : |a_j^T r| >= th *
+ * max_j |a_j^T r| } per column, skipping zero columns.
+ * r: host m x B fp64 (REF layout); mask: host n x B (REF layout), in/out. */
+int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
+                      uint8_t* mask);
+
+/* Introspection for tests and the bench. */
+typedef struct cl_stats {
+  int64_t kernel_launches;      /* kernels launched by the last solve       */
+  int64_t rescans;              /* selections re-decided in fp64            */
+  int64_t outer_iterations;     /* outer iterations executed (max over B)   */
+  double corr_ms;               /* device time of the correlation kernels   */
+  double learn_ms;              /* device time of the learning kernels      */
+  double total_ms;              /* device time of the whole solve           */
+  int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32            */
+  int32_t pad0;
+} cl_stats;
+int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
+
+/* Tuning / test knobs: 0 = auto, 1 = force fp64 SIMT correlation,
+ * 2 = force the tcgen05 3xTF32 correlation (th == 1 only). */
+int cl_set_corr_path(cl_ctx* ctx, int path);
+/* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
+int cl_set_profiling(cl_ctx* ctx, int on);
+
+int cl_abi_version(void);
+int cl_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CLOMP_B200_H */

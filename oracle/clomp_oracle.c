@@ -1,0 +1,550 @@
+/*
+ * clomp_oracle.c — fp64 CPU restatement of the reference CLOMP loop.
+ *
+ * TEST INFRASTRUCTURE ONLY (see clomp_oracle.h).  Never linked into, loaded by
+ * or called from the product library.
+ *
+ * What it restates, with the reference lines it follows:
+ *   validate                 clomp.cpp:18-30
+ *   inject_from_scores       clomp.cpp:41-53   (select_support twin, solvers.cpp:68-80)
+ *   loss_impl (priors off)   clomp.cpp:74-91, 120-127
+ *   resolve_weights          clomp.cpp:131-140
+ *   gradient_step            clomp.cpp:171-209
+ *   clomp_solve_batch        clomp.cpp:211-292
+ *   clomp_solve              clomp.cpp:294-311
+ * and the arithmetic of the kernels those call:
+ *   kern::gemm  avx2  kernels_avx2.cpp:164-236  (per output: sequential FMA over k)
+ *               scalar kernels_scalar.cpp:62-70 (per output: sequential mul+add over k)
+ *   kern::sum_sq avx2 kernels_avx2.cpp:30-58    (4x4 accumulators, hsum, FMA tail)
+ *               scalar kernels_scalar.cpp:16-20
+ *
+ * Why it is bit-identical although it is support-restricted: the reference
+ * residual A*(mask.*s) sums over all n atoms, but a term with s_j == 0 adds an
+ * exact zero to a sequential accumulation, so summing only the support in
+ * ascending index order gives the same bits.  Gradients are
+ * only needed on the mask (loss_impl zeroes the rest, clomp.cpp:120-122).
+ *
+ * Build flags matter: compiled with -mfma -ffp-contract=off so that every
+ * fused multiply-add below is an explicit fma() and nothing else is fused.
+ */
+#include "clomp_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- kernels */
+
+/* kern::dot / sum_sq, avx2 variant (kernels_avx2.cpp:30-58). */
+static double dot_avx2(const double* a, const double* b, int64_t n) {
+  double acc[4][4];
+  memset(acc, 0, sizeof(acc));
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16)
+    for (int k = 0; k < 4; ++k)
+      for (int l = 0; l < 4; ++l)
+        acc[k][l] = fma(a[i + 4 * k + l], b[i + 4 * k + l], acc[k][l]);
+  for (; i + 4 <= n; i += 4)
+    for (int l = 0; l < 4; ++l) acc[0][l] = fma(a[i + l], b[i + l], acc[0][l]);
+  double v[4];
+  for (int l = 0; l < 4; ++l) v[l] = (acc[0][l] + acc[1][l]) + (acc[2][l] + acc[3][l]);
+  /* hsum: lo = (v0+v2, v1+v3), then lo[0] + lo[1] (kernels_avx2.cpp:20-26). */
+  double total = (v[0] + v[2]) + (v[1] + v[3]);
+  for (; i < n; ++i) total = fma(a[i], b[i], total); /* contracted under -mfma */
+  return total;
+}
+
+/* kern::sum_sq, scalar variant (kernels_scalar.cpp:16-20). */
+static double dot_scalar(const double* a, const double* b, int64_t n) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+  return acc;
+}
+
+static double sum_sq(const double* a, int64_t n, int isa) {
+  return isa == ORC_ISA_AVX2 ? dot_avx2(a, a, n) : dot_scalar(a, a, n);
+}
+
+/* One gemm accumulation step c += a*b in the reference's per-ISA arithmetic. */
+static inline double mac(double acc, double a, double b, int isa) {
+  return isa == ORC_ISA_AVX2 ? fma(a, b, acc) : acc + a * b;
+}
+
+/* --------------------------------------------------------------- helpers */
+
+static void set_err(char* err, int errlen, const char* fmt, ...) {
+  if (!err || errlen <= 0) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(err, (size_t)errlen, fmt, ap);
+  va_end(ap);
+}
+
+static int validate(const orc_config* c, char* err, int errlen) {
+  if (!(c->th > 0.0) || c->th > 1.0) {
+    set_err(err, errlen, "clomp: th must be in (0, 1]");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->max_outer == 0) {
+    set_err(err, errlen, "clomp: max_outer must be >= 1");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->eps < 0.0) {
+    set_err(err, errlen, "clomp: eps must be non-negative");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->inner_steps == 0) {
+    set_err(err, errlen, "clomp: inner_steps must be >= 1");
+    return ORC_ERR_CONFIG;
+  }
+  if (!(c->lr > 0.0)) {
+    set_err(err, errlen, "clomp: lr must be positive");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->stall_tol < 0.0) {
+    set_err(err, errlen, "clomp: stall_tol must be non-negative");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->stall_patience == 0) {
+    set_err(err, errlen, "clomp: stall_patience must be >= 1");
+    return ORC_ERR_CONFIG;
+  }
+  if (c->opt < 0 || c->opt > 2) {
+    set_err(err, errlen, "clomp: unknown optimizer");
+    return ORC_ERR_CONFIG;
+  }
+  return ORC_OK;
+}
+
+/* resolve_weights (clomp.cpp:131-140). */
+static void resolve_weights(const orc_config* c, const double* y, int64_t count,
+                            int isa, double* w_tv, double* w_lv) {
+  const double mean_sq = sum_sq(y, count, isa) / (double)count;
+  const double auto_w = 0.01 * mean_sq;
+  *w_tv = c->w_tv < 0.0 ? auto_w : c->w_tv;
+  *w_lv = c->w_lv < 0.0 ? auto_w : c->w_lv;
+}
+
+/* Per-column ascending support list (the order the dense sum visits atoms). */
+typedef struct {
+  int64_t* idx;
+  int64_t count;
+} support_t;
+
+static void support_insert(support_t* s, int64_t j) {
+  int64_t pos = s->count;
+  while (pos > 0 && s->idx[pos - 1] > j) {
+    s->idx[pos] = s->idx[pos - 1];
+    --pos;
+  }
+  s->idx[pos] = j;
+  ++s->count;
+}
+
+typedef struct {
+  const double* a;   /* m x n */
+  const double* at;  /* n x m (LossOps::at, clomp.cpp:57-66) */
+  int64_t m, n, batch;
+  int isa;
+} problem_t;
+
+/* r = A*(mask.*s) - y  (clomp.cpp:83-84, 236-237, 285-286), support-restricted. */
+static void residual(const problem_t* p, const double* s, const support_t* sup,
+                     const double* y, double* r) {
+  const int64_t B = p->batch;
+  for (int64_t i = 0; i < p->m; ++i) {
+    const double* arow = p->a + i * p->n;
+    for (int64_t b = 0; b < B; ++b) {
+      double acc = 0.0;
+      const support_t* sb = &sup[b];
+      for (int64_t q = 0; q < sb->count; ++q) {
+        const int64_t j = sb->idx[q];
+        acc = mac(acc, arow[j], s[j * B + b], p->isa);
+      }
+      r[i * B + b] = acc - y[i * B + b];
+    }
+  }
+}
+
+/* (A^T r)[j, b] for one atom j: la::matmul(ops.at, r) element (clomp.cpp:89, 245). */
+static inline double corr(const problem_t* p, const double* r, int64_t j,
+                          int64_t b) {
+  const double* atrow = p->at + j * p->m;
+  const int64_t B = p->batch;
+  double acc = 0.0;
+  for (int64_t q = 0; q < p->m; ++q) acc = mac(acc, atrow[q], r[q * B + b], p->isa);
+  return acc;
+}
+
+/* inject_from_scores (clomp.cpp:41-53) on freshly computed scores.
+ * Returns 1 if any mask bit flipped; records the fp64 top-2 for tracing. */
+static int inject(const problem_t* p, const double* r, double th,
+                  uint8_t* mask, support_t* sup, double* scores,
+                  double* trace_row /* per column stride handled by caller */,
+                  int64_t trace_stride) {
+  const int64_t B = p->batch, n = p->n;
+  int changed = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    double cmax = 0.0, second = 0.0;
+    int64_t arg = -1;
+    for (int64_t j = 0; j < n; ++j) {
+      const double v = fabs(corr(p, r, j, b));
+      scores[j] = v;
+      if (v > cmax) {
+        second = cmax;
+        cmax = v;
+        arg = j;
+      } else if (v > second) {
+        second = v;
+      }
+    }
+    /* std::max semantics: cmax = max(cmax, |s|) keeps the first maximum. */
+    int64_t added = 0;
+    if (cmax != 0.0) {
+      const double cut = th * cmax;
+      for (int64_t j = 0; j < n; ++j)
+        if (scores[j] >= cut && !mask[j * B + b]) {
+          mask[j * B + b] = 1;
+          support_insert(&sup[b], j);
+          ++added;
+        }
+    }
+    if (added) changed = 1;
+    if (trace_row) {
+      double* t = trace_row + b * trace_stride;
+      t[0] = (double)arg;
+      t[1] = cmax;
+      t[2] = second;
+      t[3] = (double)added;
+    }
+  }
+  return changed;
+}
+
+/* gradient_step (clomp.cpp:171-209) restricted to the entries whose mask bit
+ * is set: unmasked entries have g == 0 and zero moments forever, so every
+ * update on them is an exact no-op. */
+static void step_support(double* s, double* m1, double* m2, const double* g,
+                         const support_t* sup, int64_t B,
+                         const orc_config* c, uint64_t* adam_steps) {
+  switch (c->opt) {
+    case 0:
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t q = 0; q < sup[b].count; ++q) {
+          const int64_t e = sup[b].idx[q] * B + b;
+          s[e] -= c->lr * g[e];
+        }
+      break;
+    case 1:
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t q = 0; q < sup[b].count; ++q) {
+          const int64_t e = sup[b].idx[q] * B + b;
+          m1[e] = 0.9 * m1[e] + g[e];
+          s[e] -= c->lr * m1[e];
+        }
+      break;
+    case 2: {
+      const double b1 = 0.9, b2 = 0.999, tiny = 1e-8;
+      ++*adam_steps;
+      const double bc1 = 1.0 - pow(b1, (double)*adam_steps);
+      const double bc2 = 1.0 - pow(b2, (double)*adam_steps);
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t q = 0; q < sup[b].count; ++q) {
+          const int64_t e = sup[b].idx[q] * B + b;
+          const double gg = g[e];
+          m1[e] = b1 * m1[e] + (1.0 - b1) * gg;
+          m2[e] = b2 * m2[e] + (1.0 - b2) * gg * gg;
+          const double mhat = m1[e] / bc1;
+          const double vhat = m2[e] / bc2;
+          s[e] -= c->lr * mhat / (sqrt(vhat) + tiny);
+        }
+      break;
+    }
+  }
+}
+
+/* ----------------------------------------------------------- batch solve */
+
+static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
+                       double* s_out, uint8_t* mask_out, int64_t* iters_out,
+                       double* rn_out, uint8_t* conv_out, double* trace,
+                       int64_t trace_col_stride, char* err, int errlen) {
+  const int64_t m = p->m, n = p->n, B = p->batch;
+  const int64_t nb = n * B, mb = m * B;
+  double* s = calloc((size_t)nb, sizeof(double));
+  double* m1 = calloc((size_t)nb, sizeof(double));
+  double* m2 = calloc((size_t)nb, sizeof(double));
+  double* g = calloc((size_t)nb, sizeof(double));
+  uint8_t* mask = calloc((size_t)nb, 1);
+  double* best_s = calloc((size_t)nb, sizeof(double));
+  uint8_t* best_mask = calloc((size_t)nb, 1);
+  double* r = calloc((size_t)mb, sizeof(double));
+  double* scores = calloc((size_t)n, sizeof(double));
+  support_t* sup = calloc((size_t)B, sizeof(support_t));
+  support_t* best_sup = calloc((size_t)B, sizeof(support_t));
+  int64_t* sup_mem = calloc((size_t)(2 * nb), sizeof(int64_t));
+  for (int64_t b = 0; b < B; ++b) {
+    sup[b].idx = sup_mem + b * n;
+    best_sup[b].idx = sup_mem + nb + b * n;
+  }
+  uint64_t adam_steps = 0;
+  double best_loss = INFINITY, prev_loss = INFINITY;
+  uint64_t stall = 0;
+  int converged = 0, status = ORC_OK, have_best = 0;
+  int64_t iterations = 0;
+
+  for (uint64_t outer = 1; outer <= c->max_outer; ++outer) {
+    residual(p, s, sup, y, r);
+    const double rn = sqrt(sum_sq(r, mb, p->isa));
+    if (rn < c->eps) {
+      converged = 1;
+      break;
+    }
+    double* trow = trace ? trace + (int64_t)(outer - 1) * 4 : NULL;
+    const int mask_changed = inject(p, r, c->th, mask, sup, scores, trow,
+                                    trace_col_stride);
+    for (uint64_t step = 0; step < c->inner_steps; ++step) {
+      /* loss_impl with grad (clomp.cpp:83-91, 120-123): the residual sum of
+       * squares is computed and discarded there; it does not feed the step. */
+      residual(p, s, sup, y, r);
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t q = 0; q < sup[b].count; ++q) {
+          const int64_t j = sup[b].idx[q];
+          g[j * B + b] = corr(p, r, j, b) * 2.0;
+        }
+      step_support(s, m1, m2, g, sup, B, c, &adam_steps);
+    }
+    residual(p, s, sup, y, r);
+    const double loss = sum_sq(r, mb, p->isa);
+    if (!isfinite(loss)) {
+      set_err(err, errlen, "clomp: loss diverged; reduce lr");
+      status = ORC_ERR_NUMERICAL;
+      goto done;
+    }
+    iterations = (int64_t)outer;
+    if (loss < best_loss) {
+      best_loss = loss;
+      memcpy(best_s, s, (size_t)nb * sizeof(double));
+      memcpy(best_mask, mask, (size_t)nb);
+      for (int64_t b = 0; b < B; ++b) {
+        best_sup[b].count = sup[b].count;
+        memcpy(best_sup[b].idx, sup[b].idx, (size_t)sup[b].count * sizeof(int64_t));
+      }
+      have_best = 1;
+    }
+    const double rel = isfinite(prev_loss)
+                           ? (prev_loss - loss) / fmax(fabs(prev_loss), 1e-300)
+                           : INFINITY;
+    if (!mask_changed && rel < c->stall_tol)
+      ++stall;
+    else
+      stall = 0;
+    prev_loss = loss;
+    if (stall >= c->stall_patience) break;
+  }
+
+  {
+    const double* so = s;
+    const uint8_t* mo = mask;
+    const support_t* su = sup;
+    if (!converged && isfinite(best_loss) && have_best) {
+      so = best_s;
+      mo = best_mask;
+      su = best_sup;
+    }
+    /* Final residual (clomp.cpp:285-288). */
+    residual(p, so, su, y, r);
+    const double frn = sqrt(sum_sq(r, mb, p->isa));
+    /* Unmasked entries of s are never written (gradient_step guards every
+     * update with the mask), so they are exactly 0 here as in the reference. */
+    memcpy(s_out, so, (size_t)nb * sizeof(double));
+    memcpy(mask_out, mo, (size_t)nb);
+    for (int64_t b = 0; b < B; ++b) {
+      iters_out[b] = iterations;
+      rn_out[b] = frn;
+      conv_out[b] = frn < c->eps;
+    }
+  }
+done:
+  free(s); free(m1); free(m2); free(g); free(mask); free(best_s);
+  free(best_mask); free(r); free(scores); free(sup); free(best_sup);
+  free(sup_mem);
+  return status;
+}
+
+static double* transpose(const double* a, int64_t m, int64_t n) {
+  double* t = malloc((size_t)(m * n) * sizeof(double));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) t[j * m + i] = a[i * n + j];
+  return t;
+}
+
+int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
+                          const double* y, int64_t batch,
+                          const orc_config* cfg, int isa, int mode,
+                          double* s_out, uint8_t* mask_out,
+                          int64_t* iterations, double* final_rn,
+                          uint8_t* converged, int32_t* status, double* trace,
+                          char* err, int errlen) {
+  int st = validate(cfg, err, errlen);
+  if (st) return st;
+  if (m <= 0 || n <= 0) {
+    set_err(err, errlen, "clomp: empty operator");
+    return ORC_ERR_DIMENSION;
+  }
+  if (batch <= 0) {
+    set_err(err, errlen, "clomp: empty batch");
+    return ORC_ERR_DIMENSION;
+  }
+  if (trace)
+    for (int64_t e = 0; e < batch * (int64_t)cfg->max_outer * 4; ++e) trace[e] = -1.0;
+
+  double* at = transpose(a, m, n);
+  if (mode == ORC_MODE_JOINT) {
+    double w_tv, w_lv;
+    resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
+    if (w_tv > 0.0 || w_lv > 0.0) {
+      free(at);
+      set_err(err, errlen, "clomp oracle: priors (w_tv/w_lv > 0) are not restated");
+      return ORC_ERR_UNSUPPORTED;
+    }
+    problem_t p = {a, at, m, n, batch, isa};
+    st = solve_joint(&p, y, cfg, s_out, mask_out, iterations, final_rn,
+                     converged, trace, (int64_t)cfg->max_outer * 4, err, errlen);
+    for (int64_t b = 0; b < batch; ++b) status[b] = st;
+    free(at);
+    return st;
+  }
+
+  /* PER_SIGNAL: clomp_solve on every column (clomp.cpp:294-311). */
+  double* yc = malloc((size_t)m * sizeof(double));
+  double* sc = malloc((size_t)n * sizeof(double));
+  uint8_t* mc = malloc((size_t)n);
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t i = 0; i < m; ++i) yc[i] = y[i * batch + b];
+    double w_tv, w_lv;
+    resolve_weights(cfg, yc, m, isa, &w_tv, &w_lv);
+    int sb;
+    int64_t it = 0;
+    double rn = 0.0;
+    uint8_t cv = 0;
+    if (w_tv > 0.0 || w_lv > 0.0) {
+      sb = ORC_ERR_UNSUPPORTED;
+    } else {
+      problem_t p = {a, at, m, n, 1, isa};
+      sb = solve_joint(&p, yc, cfg, sc, mc, &it, &rn, &cv,
+                       trace ? trace + b * (int64_t)cfg->max_outer * 4 : NULL,
+                       4, NULL, 0);
+    }
+    status[b] = sb;
+    if (sb != ORC_OK) {
+      for (int64_t j = 0; j < n; ++j) {
+        s_out[j * batch + b] = 0.0;
+        mask_out[j * batch + b] = 0;
+      }
+      iterations[b] = 0;
+      final_rn[b] = NAN;
+      converged[b] = 0;
+      continue;
+    }
+    for (int64_t j = 0; j < n; ++j) {
+      s_out[j * batch + b] = sc[j];
+      mask_out[j * batch + b] = mc[j];
+    }
+    iterations[b] = it;
+    final_rn[b] = rn;
+    converged[b] = cv;
+  }
+  free(yc); free(sc); free(mc); free(at);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------ unit entry points */
+
+int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
+                       int64_t batch, double th, int isa, uint8_t* mask) {
+  if (!(th > 0.0) || th > 1.0) return ORC_ERR_CONFIG;
+  double* at = transpose(a, m, n);
+  problem_t p = {a, at, m, n, batch, isa};
+  support_t* sup = calloc((size_t)batch, sizeof(support_t));
+  int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
+  for (int64_t b = 0; b < batch; ++b) {
+    sup[b].idx = mem + b * n;
+    for (int64_t j = 0; j < n; ++j)
+      if (mask[j * batch + b]) sup[b].idx[sup[b].count++] = j;
+  }
+  double* scores = malloc((size_t)n * sizeof(double));
+  inject(&p, r, th, mask, sup, scores, NULL, 0);
+  free(scores); free(mem); free(sup); free(at);
+  return ORC_OK;
+}
+
+int orc_clomp_loss(const double* a, int64_t m, int64_t n, const double* y,
+                   int64_t batch, const double* s, const uint8_t* mask,
+                   const orc_config* cfg, int isa, double* loss,
+                   double* grad) {
+  int st = validate(cfg, NULL, 0);
+  if (st) return st;
+  double w_tv, w_lv;
+  resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
+  if (w_tv > 0.0 || w_lv > 0.0) return ORC_ERR_UNSUPPORTED;
+  double* at = transpose(a, m, n);
+  problem_t p = {a, at, m, n, batch, isa};
+  support_t* sup = calloc((size_t)batch, sizeof(support_t));
+  int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
+  for (int64_t b = 0; b < batch; ++b) {
+    sup[b].idx = mem + b * n;
+    for (int64_t j = 0; j < n; ++j)
+      if (mask[j * batch + b]) sup[b].idx[sup[b].count++] = j;
+  }
+  double* r = malloc((size_t)(m * batch) * sizeof(double));
+  residual(&p, s, sup, y, r);
+  *loss = sum_sq(r, m * batch, isa);
+  if (grad) {
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t b = 0; b < batch; ++b)
+        grad[j * batch + b] = mask[j * batch + b] ? corr(&p, r, j, b) * 2.0 : 0.0;
+  }
+  free(r); free(mem); free(sup); free(at);
+  return ORC_OK;
+}
+
+int orc_gradient_step(double* s, const uint8_t* mask, double* m1, double* m2,
+                      uint64_t* adam_steps, const double* grad, int64_t total,
+                      const orc_config* cfg) {
+  if (!(cfg->lr > 0.0)) return ORC_ERR_CONFIG;
+  switch (cfg->opt) {
+    case 0:
+      for (int64_t i = 0; i < total; ++i)
+        if (mask[i]) s[i] -= cfg->lr * grad[i];
+      break;
+    case 1:
+      for (int64_t i = 0; i < total; ++i) {
+        m1[i] = 0.9 * m1[i] + grad[i];
+        if (mask[i]) s[i] -= cfg->lr * m1[i];
+      }
+      break;
+    case 2: {
+      const double b1 = 0.9, b2 = 0.999, tiny = 1e-8;
+      ++*adam_steps;
+      const double bc1 = 1.0 - pow(b1, (double)*adam_steps);
+      const double bc2 = 1.0 - pow(b2, (double)*adam_steps);
+      for (int64_t i = 0; i < total; ++i) {
+        const double g = grad[i];
+        m1[i] = b1 * m1[i] + (1.0 - b1) * g;
+        m2[i] = b2 * m2[i] + (1.0 - b2) * g * g;
+        if (mask[i]) {
+          const double mhat = m1[i] / bc1;
+          const double vhat = m2[i] / bc2;
+          s[i] -= cfg->lr * mhat / (sqrt(vhat) + tiny);
+        }
+      }
+      break;
+    }
+    default:
+      return ORC_ERR_CONFIG;
+  }
+  return ORC_OK;
+}

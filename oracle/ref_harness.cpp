@@ -1,0 +1,231 @@
+// ref_harness.cpp — C entry points over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled (by oracle/Makefile) together with the
+// reference sources where they lie under /root/reference/proj/src into
+// oracle/_ref/libcskit_ref.so.  It lets the Python tests and bench.py's
+// reference arm call cskit::clomp_solve_batch / clomp_solve (clomp.cpp:211-311)
+// and the unit-level entry points through ctypes.  Nothing here computes; it
+// marshals plain arrays into cskit types and maps the reference exceptions
+// (errors.hpp:10-37) onto the status codes of include/clomp_b200.h.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "cskit/clomp.hpp"
+#include "cskit/errors.hpp"
+#include "cskit/kernels.hpp"
+#include "cskit/rng.hpp"
+#include "cskit/sensing.hpp"
+
+extern "C" {
+// Same layout as cl_config (include/clomp_b200.h) and orc_config.
+struct ref_config {
+  double th;
+  uint64_t max_outer;
+  double eps;
+  uint64_t inner_steps;
+  double lr;
+  int32_t opt;
+  int32_t pad0;
+  double w_tv;
+  double w_lv;
+  uint64_t lv_window;
+  uint64_t lv_stride;
+  double stall_tol;
+  uint64_t stall_patience;
+};
+}
+
+namespace {
+
+cskit::ClompConfig to_cfg(const ref_config* c) {
+  cskit::ClompConfig cfg;
+  cfg.th = c->th;
+  cfg.max_outer = c->max_outer;
+  cfg.eps = c->eps;
+  cfg.inner_steps = c->inner_steps;
+  cfg.lr = c->lr;
+  cfg.opt = c->opt == 0   ? cskit::Optimizer::plain
+            : c->opt == 1 ? cskit::Optimizer::momentum
+                          : cskit::Optimizer::adam;
+  cfg.w_tv = c->w_tv;
+  cfg.w_lv = c->w_lv;
+  cfg.lv.window = c->lv_window;
+  cfg.lv.stride = c->lv_stride;
+  cfg.stall_tol = c->stall_tol;
+  cfg.stall_patience = c->stall_patience;
+  return cfg;
+}
+
+// MeasurementSetup with a 1 x n dummy basis: with priors off the
+// basis is read only for x_hat = basis * s_eff (clomp.cpp:289).
+cskit::MeasurementSetup to_setup(const double* a, int64_t m, int64_t n,
+                                 const double* basis) {
+  cskit::MeasurementSetup s;
+  s.n = static_cast<std::size_t>(n);
+  s.m = static_cast<std::size_t>(m);
+  s.a = cskit::la::Mat(s.m, s.n);
+  std::memcpy(s.a.data(), a, sizeof(double) * s.m * s.n);
+  if (basis) {
+    s.basis = cskit::la::Mat(s.n, s.n);
+    std::memcpy(s.basis.data(), basis, sizeof(double) * s.n * s.n);
+  } else {
+    s.basis = cskit::la::Mat(1, s.n);
+  }
+  return s;
+}
+
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const cskit::ConfigError*>(&e)) return 2;
+  if (dynamic_cast<const cskit::DimensionError*>(&e)) return 3;
+  if (dynamic_cast<const cskit::NumericalError*>(&e)) return 4;
+  return 1;
+}
+
+void put_err(char* err, int errlen, const char* what) {
+  if (err && errlen > 0) {
+    std::strncpy(err, what, static_cast<std::size_t>(errlen) - 1);
+    err[errlen - 1] = 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// isa: 0 scalar, 1 avx2 (kern::force, kernels.cpp:40-44).
+int ref_force_isa(int isa) {
+  try {
+    cskit::kern::force(isa ? cskit::kern::Isa::avx2 : cskit::kern::Isa::scalar);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_clomp_solve_batch(const double* a, int64_t m, int64_t n,
+                          const double* y, int64_t batch, const ref_config* c,
+                          double* s_out, uint8_t* mask_out, int64_t* iterations,
+                          double* final_rn, uint8_t* converged,
+                          double* wall_s, char* err, int errlen) {
+  try {
+    const auto setup = to_setup(a, m, n, nullptr);
+    cskit::la::Mat yc(static_cast<std::size_t>(m), static_cast<std::size_t>(batch));
+    if (batch > 0) std::memcpy(yc.data(), y, sizeof(double) * yc.a.size());
+    const auto res = cskit::clomp_solve_batch(setup, yc, to_cfg(c));
+    std::memcpy(s_out, res.s.data(), sizeof(double) * res.s.a.size());
+    std::memcpy(mask_out, res.mask.data(), res.mask.size());
+    *iterations = static_cast<int64_t>(res.iterations);
+    *final_rn = res.final_residual_norm;
+    *converged = res.converged ? 1 : 0;
+    if (wall_s) *wall_s = res.wall_time_s;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return code_of(e);
+  }
+}
+
+int ref_clomp_solve(const double* a, int64_t m, int64_t n, const double* y,
+                    const ref_config* c, double* s_out, uint8_t* mask_out,
+                    int64_t* iterations, double* final_rn, uint8_t* converged,
+                    double* wall_s, char* err, int errlen) {
+  try {
+    const auto setup = to_setup(a, m, n, nullptr);
+    cskit::la::Vec yv(y, y + m);
+    const auto res = cskit::clomp_solve(setup, yv, to_cfg(c));
+    std::memcpy(s_out, res.s.values.data(), sizeof(double) * res.s.values.size());
+    std::memcpy(mask_out, res.s.mask.data(), res.s.mask.size());
+    *iterations = static_cast<int64_t>(res.iterations);
+    *final_rn = res.final_residual_norm;
+    *converged = res.converged ? 1 : 0;
+    if (wall_s) *wall_s = res.wall_time_s;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return code_of(e);
+  }
+}
+
+int ref_inject_support(const double* a, int64_t m, int64_t n, const double* r,
+                       int64_t batch, double th, uint8_t* mask) {
+  try {
+    const auto setup = to_setup(a, m, n, nullptr);
+    cskit::la::Mat rc(static_cast<std::size_t>(m), static_cast<std::size_t>(batch));
+    std::memcpy(rc.data(), r, sizeof(double) * rc.a.size());
+    std::vector<std::uint8_t> mk(mask, mask + n * batch);
+    cskit::inject_support(setup, rc, th, mk);
+    std::memcpy(mask, mk.data(), mk.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_clomp_loss(const double* a, int64_t m, int64_t n, const double* y,
+                   int64_t batch, const double* s, const uint8_t* mask,
+                   const ref_config* c, double* loss, double* grad) {
+  try {
+    const auto setup = to_setup(a, m, n, nullptr);
+    cskit::la::Mat yc(static_cast<std::size_t>(m), static_cast<std::size_t>(batch));
+    std::memcpy(yc.data(), y, sizeof(double) * yc.a.size());
+    cskit::ClompState st(static_cast<std::size_t>(n), static_cast<std::size_t>(batch));
+    std::memcpy(st.s.data(), s, sizeof(double) * st.s.a.size());
+    std::memcpy(st.mask.data(), mask, st.mask.size());
+    cskit::la::Mat g;
+    const auto lb = cskit::clomp_loss(setup, yc, st, to_cfg(c), grad ? &g : nullptr);
+    *loss = lb.total;
+    if (grad) std::memcpy(grad, g.data(), sizeof(double) * g.a.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_gradient_step(double* s, const uint8_t* mask, double* m1, double* m2,
+                      uint64_t* adam_steps, const double* grad, int64_t total,
+                      const ref_config* c) {
+  try {
+    cskit::ClompState st(static_cast<std::size_t>(total), 1);
+    std::memcpy(st.s.data(), s, sizeof(double) * total);
+    std::memcpy(st.mask.data(), mask, total);
+    std::memcpy(st.m1.data(), m1, sizeof(double) * total);
+    std::memcpy(st.m2.data(), m2, sizeof(double) * total);
+    st.adam_steps = *adam_steps;
+    cskit::la::Mat g(static_cast<std::size_t>(total), 1);
+    std::memcpy(g.data(), grad, sizeof(double) * total);
+    cskit::gradient_step(st, g, to_cfg(c));
+    std::memcpy(s, st.s.data(), sizeof(double) * total);
+    std::memcpy(m1, st.m1.data(), sizeof(double) * total);
+    std::memcpy(m2, st.m2.data(), sizeof(double) * total);
+    *adam_steps = st.adam_steps;
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// Draws from cskit::Rng (rng.hpp:13-79): kind 0 next_u64 (as double bits via
+// out_u64), 1 uniform, 2 normal, 3 uniform_below(bound).
+void ref_rng_draws(uint64_t seed, int kind, uint64_t bound, int64_t count,
+                   double* out, uint64_t* out_u64) {
+  cskit::Rng rng(seed);
+  for (int64_t i = 0; i < count; ++i) {
+    switch (kind) {
+      case 0: out_u64[i] = rng.next_u64(); break;
+      case 1: out[i] = rng.uniform(); break;
+      case 2: out[i] = rng.normal(); break;
+      default: out_u64[i] = rng.uniform_below(bound); break;
+    }
+  }
+}
+
+// dct_basis (sensing.cpp:13-29), n x n row-major.
+void ref_dct_basis(int64_t n, double* out) {
+  const auto b = cskit::dct_basis(static_cast<std::size_t>(n));
+  std::memcpy(out, b.d.data(), sizeof(double) * b.d.a.size());
+}
+
+}  // extern "C"

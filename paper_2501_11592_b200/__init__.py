@@ -1,0 +1,398 @@
+"""B200-native CLOMP reconstruction loop (arXiv 2501.11592), host mirror.
+
+A thin ctypes layer over the C-ABI in include/clomp_b200.h
+(paper_2501_11592_b200/_build/libclomp_b200.so).  Names, argument meaning and
+error behaviour follow the reference library's public API
+(/root/reference/proj/include/cskit/clomp.hpp:16-101):
+
+    ClompConfig            <- cskit::ClompConfig          (clomp.hpp:16-33)
+    ClompContext           <- cskit::MeasurementSetup     (sensing.hpp:37-45),
+                              uploaded once (atom-major fp32 in HBM)
+    clomp_solve_batch()    <- cskit::clomp_solve_batch    (clomp.cpp:211-292)
+    clomp_solve()          <- cskit::clomp_solve          (clomp.cpp:294-311)
+    inject_support()       <- cskit::inject_support       (clomp.cpp:142-154)
+    ConfigError / DimensionError / NumericalError  <- errors.hpp:10-37
+
+There is no CPU path: if the CUDA library is missing or no B200 is visible the
+calls raise.  Numerics: fp32 operands, fp64 learning, tensor-core correlations
+with fp64 re-decision of near-tied selections.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_build" / "libclomp_b200.so"
+
+PLAIN, MOMENTUM, ADAM = 0, 1, 2
+MODE_JOINT, MODE_PER_SIGNAL = 0, 1
+LAYOUT_REF, LAYOUT_T = 0, 1
+
+CL_OK, CL_ERR_INTERNAL, CL_ERR_CONFIG, CL_ERR_DIMENSION = 0, 1, 2, 3
+CL_ERR_NUMERICAL, CL_ERR_UNSUPPORTED, CL_ERR_CUDA, CL_ERR_CAPACITY = 4, 5, 6, 7
+
+
+class Error(RuntimeError):
+    """cskit::Error (errors.hpp:10)."""
+
+
+class DimensionError(Error):
+    """cskit::DimensionError (errors.hpp:16)."""
+
+
+class ConfigError(Error):
+    """cskit::ConfigError (errors.hpp:22)."""
+
+
+class NumericalError(Error):
+    """cskit::NumericalError (errors.hpp:28)."""
+
+
+class UnsupportedError(Error):
+    """Priors requested: not implemented on the B200 path (no CPU fallback)."""
+
+
+class CudaError(Error):
+    """No device, wrong architecture, or a CUDA runtime failure."""
+
+
+class CapacityError(Error):
+    """The support outgrew the per-signal capacity."""
+
+
+_ERRORS = {
+    CL_ERR_INTERNAL: Error,
+    CL_ERR_CONFIG: ConfigError,
+    CL_ERR_DIMENSION: DimensionError,
+    CL_ERR_NUMERICAL: NumericalError,
+    CL_ERR_UNSUPPORTED: UnsupportedError,
+    CL_ERR_CUDA: CudaError,
+    CL_ERR_CAPACITY: CapacityError,
+}
+
+
+class CConfig(C.Structure):
+    """cl_config (include/clomp_b200.h), same layout as orc_config."""
+
+    _fields_ = [
+        ("th", C.c_double),
+        ("max_outer", C.c_uint64),
+        ("eps", C.c_double),
+        ("inner_steps", C.c_uint64),
+        ("lr", C.c_double),
+        ("opt", C.c_int32),
+        ("pad0", C.c_int32),
+        ("w_tv", C.c_double),
+        ("w_lv", C.c_double),
+        ("lv_window", C.c_uint64),
+        ("lv_stride", C.c_uint64),
+        ("stall_tol", C.c_double),
+        ("stall_patience", C.c_uint64),
+    ]
+
+
+class CResult(C.Structure):
+    _fields_ = [
+        ("cap", C.c_int64),
+        ("support", C.c_void_p),
+        ("coef", C.c_void_p),
+        ("count", C.c_void_p),
+        ("s", C.c_void_p),
+        ("mask", C.c_void_p),
+        ("iterations", C.c_void_p),
+        ("final_residual_norm", C.c_void_p),
+        ("converged", C.c_void_p),
+        ("status", C.c_void_p),
+    ]
+
+
+class CDeviceResult(C.Structure):
+    _fields_ = [
+        ("cap", C.c_int64),
+        ("support", C.c_void_p),
+        ("coef", C.c_void_p),
+        ("count", C.c_void_p),
+        ("iterations", C.c_void_p),
+        ("final_residual_norm", C.c_void_p),
+        ("converged", C.c_void_p),
+        ("status", C.c_void_p),
+    ]
+
+
+class CStats(C.Structure):
+    _fields_ = [
+        ("kernel_launches", C.c_int64),
+        ("rescans", C.c_int64),
+        ("outer_iterations", C.c_int64),
+        ("corr_ms", C.c_double),
+        ("learn_ms", C.c_double),
+        ("total_ms", C.c_double),
+        ("corr_path", C.c_int32),
+        ("pad0", C.c_int32),
+    ]
+
+
+# Every symbol include/clomp_b200.h declares (tests check the .so exports them).
+EXPORTED = [
+    "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
+    "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
+    "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
+    "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
+]
+
+_lib_handle = None
+
+
+def lib() -> C.CDLL:
+    """Load libclomp_b200.so; raises if it was not built (no fallback)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not LIB_PATH.exists():
+            raise CudaError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                "(python -m paper_2501_11592_b200.build)")
+        h = C.CDLL(str(LIB_PATH))
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        h.cl_create.restype = vp
+        h.cl_create.argtypes = [i32, vp, i64, i64, i32, C.POINTER(C.c_int)]
+        h.cl_destroy.argtypes = [vp]
+        h.cl_last_error.restype = C.c_char_p
+        h.cl_last_error.argtypes = [vp]
+        h.cl_solve_batch.argtypes = [vp, vp, i64, i32, C.POINTER(CConfig), i32, C.POINTER(CResult)]
+        h.cl_solve_batch_device.argtypes = [vp, vp, i64, C.POINTER(CConfig), i32, C.POINTER(CDeviceResult)]
+        h.cl_synchronize.argtypes = [vp]
+        h.cl_inject_support.argtypes = [vp, vp, i64, C.c_double, vp]
+        h.cl_get_stats.argtypes = [vp, C.POINTER(CStats)]
+        h.cl_set_corr_path.argtypes = [vp, i32]
+        h.cl_set_profiling.argtypes = [vp, i32]
+        h.cl_config_default.argtypes = [C.POINTER(CConfig)]
+        h.cl_rng_draws.argtypes = [C.c_uint64, i32, C.c_uint64, i64, vp, vp]
+        h.cl_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, i32, i32, C.c_double, vp, vp, vp, vp]
+        _lib_handle = h
+    return _lib_handle
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclasses.dataclass
+class ClompConfig:
+    """cskit::ClompConfig with the reference defaults (clomp.hpp:16-33)."""
+
+    th: float = 0.7
+    max_outer: int = 200
+    eps: float = 1e-6
+    inner_steps: int = 50
+    lr: float = 0.01
+    opt: int = ADAM
+    w_tv: float = -1.0
+    w_lv: float = -1.0
+    lv_window: int = 3
+    lv_stride: int = 2
+    stall_tol: float = 1e-4
+    stall_patience: int = 2
+
+    @classmethod
+    def baseline(cls, k: int, lr: float = 0.1, epochs: int = 200) -> "ClompConfig":
+        """BASELINE.json mapping: sparsity K -> th=1,
+        max_outer=K; plain gradient descent; priors off."""
+        return cls(th=1.0, max_outer=k, inner_steps=epochs, lr=lr, opt=PLAIN,
+                   w_tv=0.0, w_lv=0.0)
+
+    def to_c(self) -> CConfig:
+        def u64(v):
+            return max(0, int(v)) if int(v) >= 0 else 0
+        return CConfig(float(self.th), u64(self.max_outer), float(self.eps),
+                       u64(self.inner_steps), float(self.lr), int(self.opt), 0,
+                       float(self.w_tv), float(self.w_lv), u64(self.lv_window),
+                       u64(self.lv_stride), float(self.stall_tol),
+                       u64(self.stall_patience))
+
+
+@dataclasses.dataclass
+class BatchSolveResult:
+    """cskit::BatchSolveResult (clomp.hpp:82-90) plus the compact support."""
+
+    s: np.ndarray                 # n x B fp64 (reference layout)
+    mask: np.ndarray              # n x B uint8
+    iterations: np.ndarray        # [B]
+    final_residual_norm: np.ndarray
+    converged: np.ndarray
+    status: np.ndarray
+    support: list                 # per signal, ascending atom indices
+    coef: list                    # per signal, aligned with support
+
+
+@dataclasses.dataclass
+class SolveResult:
+    """cskit::SolveResult (solvers.hpp:12-19), without x_hat."""
+
+    values: np.ndarray
+    mask: np.ndarray
+    iterations: int
+    final_residual_norm: float
+    converged: bool
+
+
+def _raise(code: int, handle=None):
+    if code == CL_OK:
+        return
+    msg = lib().cl_last_error(handle)
+    msg = msg.decode() if msg else f"status {code}"
+    raise _ERRORS.get(code, Error)(msg)
+
+
+class ClompContext:
+    """A dictionary resident on one B200 (replaces MeasurementSetup.a).
+
+    a: m x n (layout='ref', the reference la::Mat layout) or n x m ('t').
+    Values are rounded to fp32 (north-star operand precision)."""
+
+    def __init__(self, a, device: int = 0, layout: str = "ref"):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        if a.ndim != 2:
+            raise DimensionError("dictionary must be 2-D")
+        if layout == "ref":
+            self.m, self.n = a.shape
+            lay = LAYOUT_REF
+        else:
+            self.n, self.m = a.shape
+            lay = LAYOUT_T
+        st = C.c_int(0)
+        h = lib().cl_create(int(device), _ptr(a), self.m, self.n, lay, C.byref(st))
+        if not h:
+            _raise(st.value or CL_ERR_CUDA, None)
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().cl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_corr_path(self, path: int):
+        _raise(lib().cl_set_corr_path(self._h, int(path)), self._h)
+
+    def set_profiling(self, on: bool):
+        _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)
+
+    def stats(self) -> dict:
+        s = CStats()
+        _raise(lib().cl_get_stats(self._h, C.byref(s)), self._h)
+        return {f: getattr(s, f) for f, _ in CStats._fields_ if f != "pad0"}
+
+
+def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
+                      mode: int = MODE_JOINT, layout: str = "ref") -> BatchSolveResult:
+    """Reconstruct a batch; y_cols is m x B (reference layout) or B x m ('t')."""
+    cfg = cfg or ClompConfig()
+    y = np.ascontiguousarray(y_cols, dtype=np.float32)
+    if y.ndim == 1:
+        y = y.reshape(-1, 1) if layout == "ref" else y.reshape(1, -1)
+    if layout == "ref":
+        if y.shape[0] != ctx.m:
+            raise DimensionError(f"clomp: y rows {y.shape[0]} vs m={ctx.m}")
+        B = y.shape[1]
+        lay = LAYOUT_REF
+    else:
+        if y.shape[1] != ctx.m:
+            raise DimensionError(f"clomp: y cols {y.shape[1]} vs m={ctx.m}")
+        B = y.shape[0]
+        lay = LAYOUT_T
+    n = ctx.n
+    cap = max(1, n if cfg.th < 1.0 else min(n, max(1, int(cfg.max_outer))))
+    sup = np.zeros((max(B, 1), cap), np.int32)
+    coef = np.zeros((max(B, 1), cap), np.float64)
+    cnt = np.zeros(max(B, 1), np.int32)
+    s = np.zeros((n, max(B, 1)), np.float64)
+    mask = np.zeros((n, max(B, 1)), np.uint8)
+    it = np.zeros(max(B, 1), np.int64)
+    rn = np.zeros(max(B, 1), np.float64)
+    cv = np.zeros(max(B, 1), np.uint8)
+    st = np.zeros(max(B, 1), np.int32)
+    res = CResult(cap, _ptr(sup), _ptr(coef), _ptr(cnt), _ptr(s), _ptr(mask),
+                  _ptr(it), _ptr(rn), _ptr(cv), _ptr(st))
+    c = cfg.to_c()
+    code = lib().cl_solve_batch(ctx.handle, _ptr(y), B, lay, C.byref(c), int(mode), C.byref(res))
+    _raise(code, ctx.handle)
+    supports = [sup[b, :min(cnt[b], cap)].copy() for b in range(B)]
+    coefs = [coef[b, :min(cnt[b], cap)].copy() for b in range(B)]
+    return BatchSolveResult(s[:, :B], mask[:, :B], it[:B], rn[:B], cv[:B].astype(bool),
+                            st[:B], supports, coefs)
+
+
+def clomp_solve(ctx: ClompContext, y, cfg: ClompConfig | None = None) -> SolveResult:
+    """Single-signal wrapper: exactly a one-column batch (clomp.cpp:294-311)."""
+    y = np.asarray(y, dtype=np.float32).reshape(-1)
+    if y.shape[0] != ctx.m:
+        raise DimensionError(f"clomp: y has {y.shape[0]} entries, setup expects {ctx.m}")
+    r = clomp_solve_batch(ctx, y.reshape(-1, 1), cfg, MODE_JOINT)
+    return SolveResult(r.s[:, 0].copy(), r.mask[:, 0].copy(), int(r.iterations[0]),
+                       float(r.final_residual_norm[0]), bool(r.converged[0]))
+
+
+def inject_support(ctx: ClompContext, r_cols, th: float, mask) -> np.ndarray:
+    """mask |= thresholded |A^T r| per column (clomp.cpp:142-154); returns mask."""
+    r = np.ascontiguousarray(r_cols, dtype=np.float64)
+    if r.ndim == 1:
+        r = r.reshape(-1, 1)
+    if r.shape[0] != ctx.m:
+        raise DimensionError(f"inject_support: residual rows {r.shape[0]} vs m={ctx.m}")
+    B = r.shape[1]
+    mk = np.ascontiguousarray(mask, dtype=np.uint8)
+    if mk.size != ctx.n * B:
+        raise DimensionError("inject_support: mask size mismatch")
+    mk = mk.reshape(ctx.n, B).copy()
+    _raise(lib().cl_inject_support(ctx.handle, _ptr(r), B, float(th), _ptr(mk)), ctx.handle)
+    return mk
+
+
+# ------------------------------------------------------------- datagen
+def rng_draws(seed: int, kind: str, count: int, bound: int = 0) -> np.ndarray:
+    """Draws of the restated cskit::Rng (rng.hpp:13-79)."""
+    k = {"u64": 0, "uniform": 1, "normal": 2, "below": 3}[kind]
+    out = np.zeros(count, np.float64)
+    out64 = np.zeros(count, np.uint64)
+    lib().cl_rng_draws(seed, k, bound, count, _ptr(out), _ptr(out64))
+    return out64 if k in (0, 3) else out
+
+
+def gen_problem_1d(seed: int, m: int, n: int, k: int, batch: int,
+                   normalize: bool = True, value_law: int = 0,
+                   snr_db: float = -1.0):
+    """Seeded synthetic problem.  Returns (A m x n fp32,
+    X n x B fp64, Y m x B fp32, supports B x k int32)."""
+    A = np.zeros((m, n), np.float32)
+    X = np.zeros((n, batch), np.float64)
+    Y = np.zeros((m, batch), np.float32)
+    S = np.zeros((batch, k), np.int32)
+    code = lib().cl_gen_problem_1d(seed, m, n, k, batch, int(normalize), int(value_law),
+                                   float(snr_db), _ptr(A), _ptr(X), _ptr(Y), _ptr(S))
+    if code:
+        raise DimensionError("gen_problem_1d: bad sizes")
+    return A, X, Y, S
+
+
+# BASELINE.json configs.  lr / epochs for configs 2-5 are not
+# stated there; config 1's are used and recorded.
+CONFIGS = {
+    1: dict(name="cfg1_1d_single", m=128, n=256, k=10, batch=1, value_law=0, snr_db=-1.0, seed=0),
+    2: dict(name="cfg2_1d_batched", m=512, n=1024, k=32, batch=4096, value_law=0, snr_db=40.0, seed=1),
+    3: dict(name="cfg3_1d_long", m=4096, n=16384, k=256, batch=256, value_law=1, snr_db=-1.0, seed=2),
+}

@@ -1,0 +1,90 @@
+"""Build libclomp_b200.so in-tree (sm_100a only).
+
+    python -m paper_2501_11592_b200.build        # or __graft_entry__.build()
+
+Every .cu / .cpp under csrc/ (except csrc/shim/, built separately) is compiled
+with nvcc for `-gencode arch=compute_100a,code=sm_100a -lineinfo` and linked
+into paper_2501_11592_b200/_build/libclomp_b200.so with the CUDA runtime
+linked statically, so the library loads on a CPU-only host (for the ABI
+tests) and needs only the driver on the GPU box.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_build"
+INCLUDE = PKG.parent / "include"
+LIB = OUT / "libclomp_b200.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", "-Xptxas", "-v",
+    f"-I{INCLUDE}", f"-I{CSRC}",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _sources() -> list[Path]:
+    return sorted(p for p in CSRC.glob("*") if p.suffix in (".cu", ".cpp"))
+
+
+def _digest(paths: list[Path]) -> str:
+    h = hashlib.sha256()
+    for p in paths:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()
+
+
+def _compile(src: Path) -> tuple[Path, str]:
+    obj = OUT / (src.stem + ".o")
+    cmd = [nvcc()] + NVCC_FLAGS + ["-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":
+        cmd = [nvcc(), "-x", "cu"] + NVCC_FLAGS + ["-c", str(src), "-o", str(obj)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stdout}\n{res.stderr}")
+    return obj, res.stderr
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    OUT.mkdir(parents=True, exist_ok=True)
+    srcs = _sources()
+    headers = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
+    stamp = OUT / "build.stamp"
+    digest = _digest(srcs + headers)
+    if LIB.exists() and stamp.exists() and stamp.read_text() == digest and not force:
+        return LIB
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        results = list(ex.map(_compile, srcs))
+    log = "\n".join(f"== {o.name}\n{err}" for o, err in results)
+    (OUT / "ptxas.log").write_text(log)
+    if verbose:
+        print(log)
+    objs = [str(o) for o, _ in results]
+    cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", str(LIB)] + objs + ["-lpthread", "-ldl", "-lrt"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    stamp.write_text(digest)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,0 +1,691 @@
+// clomp_api.cu — host side of the C-ABI (include/clomp_b200.h).
+//
+// Owns the device copy of the dictionary, the batch workspace and the outer
+// loop that sequences the kernels of one CLOMP solve:
+//
+//   init -> [ corr (K1) -> select (K1c) -> rescan -> learn (K2) -> control ]*
+//        -> finalize
+//
+// Validation, error classes and messages follow the reference
+// (clomp.cpp:18-30, 131-140, 211-218); there is no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/clomp_b200.h"
+#include "clomp_internal.cuh"
+
+using namespace clb;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+struct cl_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t m = 0, n = 0, ldm = 0;
+  float* at32 = nullptr;
+  float* at_hi = nullptr;
+  float* at_lo = nullptr;
+  double colnorm_max = 0.0;
+  std::string err;
+  // batch workspace
+  void* wbuf = nullptr;
+  size_t wbytes = 0;
+  Work w;
+  // Adam bias-correction tables
+  double* bc = nullptr;
+  size_t bc_len = 0;
+  // host-call staging
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  int32_t* h_counters = nullptr;  // pinned
+  int corr_force = 0;
+  bool profiling = false;
+  cl_stats stats{};
+  int sms = 148;
+  bool tc_ok = false;
+};
+
+namespace {
+
+int fail(cl_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where) {
+  std::string msg = std::string("CUDA error in ") + where + ": " +
+                    cudaGetErrorString(e);
+  cudaGetLastError();
+  return fail(ctx, CL_ERR_CUDA, msg);
+}
+
+#define CL_CUDA(ctx, call)                                   \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+int validate(cl_ctx* ctx, const cl_config* c) {
+  if (!c) return fail(ctx, CL_ERR_CONFIG, "clomp: null config");
+  if (!(c->th > 0.0) || c->th > 1.0)
+    return fail(ctx, CL_ERR_CONFIG, "clomp: th must be in (0, 1]");
+  if (c->max_outer == 0) return fail(ctx, CL_ERR_CONFIG, "clomp: max_outer must be >= 1");
+  if (c->eps < 0.0) return fail(ctx, CL_ERR_CONFIG, "clomp: eps must be non-negative");
+  if (c->inner_steps == 0)
+    return fail(ctx, CL_ERR_CONFIG, "clomp: inner_steps must be >= 1");
+  if (!(c->lr > 0.0)) return fail(ctx, CL_ERR_CONFIG, "clomp: lr must be positive");
+  if (c->stall_tol < 0.0)
+    return fail(ctx, CL_ERR_CONFIG, "clomp: stall_tol must be non-negative");
+  if (c->stall_patience == 0)
+    return fail(ctx, CL_ERR_CONFIG, "clomp: stall_patience must be >= 1");
+  if (c->opt < 0 || c->opt > 2) return fail(ctx, CL_ERR_CONFIG, "clomp: unknown optimizer");
+  if (c->max_outer > (1u << 30) || c->inner_steps > (1u << 30))
+    return fail(ctx, CL_ERR_CONFIG, "clomp: iteration counts out of range");
+  return CL_OK;
+}
+
+// resolve_weights (clomp.cpp:131-140) and whether loss_impl would run a prior
+// (clomp.cpp:93-94: LV only when the batch fits its window).
+bool priors_active(const cl_config* c, double mean_sq, int64_t batch, int64_t n) {
+  const double auto_w = 0.01 * mean_sq;
+  const double w_tv = c->w_tv < 0.0 ? auto_w : c->w_tv;
+  const double w_lv = c->w_lv < 0.0 ? auto_w : c->w_lv;
+  const bool lv_fits = (uint64_t)batch >= c->lv_window && (uint64_t)n >= c->lv_window;
+  return w_tv > 0.0 || (w_lv > 0.0 && lv_fits);
+}
+
+int64_t support_cap(const cl_ctx* ctx, const cl_config* c) {
+  if (c->th >= 1.0) return std::min<int64_t>(ctx->n, (int64_t)c->max_outer);
+  return ctx->n;
+}
+
+// Carve the workspace for (B, cap); reallocate only when it grows.
+int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
+                     bool need_split, int64_t ntile) {
+  const int64_t ldm = ctx->ldm;
+  const int64_t mwords = (ctx->n + 31) / 32;
+  auto carve = [&](Carver& cv, Work& w) {
+    w.y32 = cv.take<float>(B * ldm);
+    w.y64 = cv.take<double>(B * ldm);
+    w.r64 = cv.take<double>(B * ldm);
+    w.r_hi = need_split ? cv.take<float>(B * ldm) : nullptr;
+    w.r_lo = need_split ? cv.take<float>(B * ldm) : nullptr;
+    w.cand_v1 = cv.take<double>(B * ntile);
+    w.cand_v2 = cv.take<double>(B * ntile);
+    w.cand_i1 = cv.take<int32_t>(B * ntile);
+    w.scores = need_scores ? cv.take<double>(B * ctx->n) : nullptr;
+    w.sup = cv.take<int32_t>(B * cap);
+    w.cnt = cv.take<int32_t>(B);
+    w.gcnt = cv.take<int32_t>(B);
+    w.coef = cv.take<double>(B * cap);
+    w.mom1 = cv.take<double>(B * cap);
+    w.mom2 = cv.take<double>(B * cap);
+    w.gram = cv.take<double>(B * cap * cap);
+    w.bvec = cv.take<double>(B * cap);
+    w.maskbits = cv.take<uint32_t>(B * mwords);
+    w.best_coef = cv.take<double>(B * cap);
+    w.best_cnt = cv.take<int32_t>(B);
+    w.best_L = cv.take<double>(B);
+    w.prev_L = cv.take<double>(B);
+    w.loss = cv.take<double>(B);
+    w.stall = cv.take<int32_t>(B);
+    w.iters = cv.take<int32_t>(B);
+    w.active = cv.take<int32_t>(B);
+    w.conv = cv.take<uint8_t>(B);
+    w.status = cv.take<int32_t>(B);
+    w.changed = cv.take<int32_t>(B);
+    w.rescan_list = cv.take<int32_t>(2 * B);
+    w.counters = cv.take<int32_t>(kNumCounters);
+    w.joint = cv.take<double>(kNumJoint);
+  };
+  Carver probe{nullptr};
+  Work tmp;
+  carve(probe, tmp);
+  const size_t need = probe.off + 256;
+  if (need > ctx->wbytes) {
+    if (ctx->wbuf) cudaFree(ctx->wbuf);
+    ctx->wbuf = nullptr;
+    ctx->wbytes = 0;
+    cudaError_t e = cudaMalloc(&ctx->wbuf, need);
+    if (e != cudaSuccess) {
+      return cuda_fail(ctx, e, "workspace allocation");
+    }
+    ctx->wbytes = need;
+  }
+  Carver real{static_cast<char*>(ctx->wbuf)};
+  Work w;
+  carve(real, w);
+  w.at32 = ctx->at32;
+  w.at_hi = ctx->at_hi;
+  w.at_lo = ctx->at_lo;
+  ctx->w = w;
+  return CL_OK;
+}
+
+int ensure_adam_tables(cl_ctx* ctx, const cl_config* c) {
+  if (c->opt != CL_OPT_ADAM) return CL_OK;
+  const size_t len = (size_t)c->max_outer * (size_t)c->inner_steps;
+  if (len > ctx->bc_len) {
+    if (ctx->bc) cudaFree(ctx->bc);
+    ctx->bc = nullptr;
+    CL_CUDA(ctx, cudaMalloc(&ctx->bc, 2 * len * sizeof(double)));
+    ctx->bc_len = len;
+  }
+  // bc1/bc2 exactly as gradient_step computes them (clomp.cpp:191-195).
+  std::vector<double> h(2 * len);
+  for (size_t s = 0; s < len; ++s) {
+    h[s] = 1.0 - std::pow(0.9, (double)(s + 1));
+    h[len + s] = 1.0 - std::pow(0.999, (double)(s + 1));
+  }
+  CL_CUDA(ctx, cudaMemcpy(ctx->bc, h.data(), 2 * len * sizeof(double),
+                          cudaMemcpyHostToDevice));
+  return CL_OK;
+}
+
+bool use_tensor_path(const cl_ctx* ctx, const cl_config* c) {
+  if (c->th < 1.0) return false;
+  if (ctx->corr_force == 1) return false;
+  return ctx->tc_ok;
+}
+
+// Correlation error bound relative to max||a_j|| * ||r||.  fp64 SIMT: a few
+// hundred ulps of the dot length covers summation-order differences with the
+// reference's sequential FMA (kernels_avx2.cpp:164-236).  3xTF32: see
+// DESIGN.md §4 (measured worst error x safety factor).
+double delta_for(bool tensor) { return tensor ? 4e-5 : 1e-12; }
+
+struct OutPtrs {
+  int64_t cap;
+  int32_t* sup;
+  double* coef;
+  int32_t* cnt;
+  int32_t* iters;
+  double* rn;
+  uint8_t* conv;
+  int32_t* status;
+};
+
+// The outer loop shared by the host-buffer and device-buffer entry points.
+// y_dev: device pointer, layout_ref ? m x B : B x m.
+int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
+               const cl_config* c, int mode, const OutPtrs& out) {
+  const bool tensor = use_tensor_path(ctx, c);
+  const bool full_scores = c->th < 1.0;
+  const int64_t cap = support_cap(ctx, c);
+  if (cap > 1024)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "clomp: support capacity above 1024 atoms per signal is not "
+                "supported (th < 1 with n > 1024)");
+  const int64_t tile_atoms = tensor ? 128 : kCorrTileAtoms;
+  const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
+  int st = ensure_workspace(ctx, B, cap, full_scores, tensor, ntile);
+  if (st) return st;
+  st = ensure_adam_tables(ctx, c);
+  if (st) return st;
+
+  SolveParams p{};
+  p.B = B;
+  p.n = ctx->n;
+  p.m = ctx->m;
+  p.ldm = ctx->ldm;
+  p.cap = cap;
+  p.ntile = ntile;
+  p.mwords = (ctx->n + 31) / 32;
+  p.th = c->th;
+  p.eps = c->eps;
+  p.lr = c->lr;
+  p.stall_tol = c->stall_tol;
+  p.stall_patience = (int32_t)std::min<uint64_t>(c->stall_patience, 1u << 30);
+  p.opt = c->opt;
+  p.inner = (int32_t)c->inner_steps;
+  p.max_outer = (int32_t)c->max_outer;
+  p.mode = mode;
+  p.bc1 = ctx->bc;
+  p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
+  p.delta_rel = delta_for(tensor);
+  p.colnorm_max = ctx->colnorm_max;
+
+  const Work& w = ctx->w;
+  cudaStream_t s = ctx->stream;
+  cl_stats stats{};
+  stats.corr_path = tensor ? 1 : 0;
+  int64_t launches = 0;
+  cudaEvent_t ev[4] = {};
+  if (ctx->profiling)
+    for (auto& e : ev) cudaEventCreate(&e);
+
+  CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
+  if (ctx->profiling) cudaEventRecord(ev[0], s);
+  launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
+  ++launches;
+  if (mode == CL_MODE_JOINT) {
+    launch_joint_control(p, w, 0, true, s);
+    ++launches;
+  }
+  const int rescan_grid = (int)std::min<int64_t>(B, ctx->sms);
+  int outer = 1;
+  for (; outer <= p.max_outer; ++outer) {
+    CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s));
+    if (ctx->profiling) cudaEventRecord(ev[1], s);
+    if (tensor)
+      launch_corr_tc(p, w, s);
+    else
+      launch_corr_f64(p, w, full_scores, s);
+    launch_select(p, w, full_scores, s);
+    launch_rescan(p, w, rescan_grid, s);
+    launches += 3;
+    if (ctx->profiling) cudaEventRecord(ev[2], s);
+    launch_learn(p, w, outer, (int)cap, s);
+    launches += cap > kWarpCap ? 2 : 1;
+    if (mode == CL_MODE_JOINT) {
+      launch_joint_control(p, w, outer, false, s);
+      launch_joint_snapshot(p, w, s);
+      launches += 2;
+    }
+    if (ctx->profiling) cudaEventRecord(ev[3], s);
+    CL_CUDA(ctx, cudaGetLastError());
+    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters,
+                                 kNumCounters * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
+    if (ctx->profiling) {
+      float a = 0.f, b2 = 0.f;
+      cudaEventElapsedTime(&a, ev[1], ev[2]);
+      cudaEventElapsedTime(&b2, ev[2], ev[3]);
+      stats.corr_ms += a;
+      stats.learn_ms += b2;
+    }
+    if (ctx->h_counters[kActiveCount] == 0) break;
+  }
+  launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
+                  out.conv, out.status, s);
+  ++launches;
+  CL_CUDA(ctx, cudaGetLastError());
+  CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters,
+                               kNumCounters * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, s));
+  if (ctx->profiling) cudaEventRecord(ev[3], s);
+  CL_CUDA(ctx, cudaStreamSynchronize(s));
+  if (ctx->profiling) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[0], ev[3]);
+    stats.total_ms = t;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  stats.kernel_launches = launches;
+  stats.rescans = ctx->h_counters[kRescanTotal];
+  stats.outer_iterations = std::min(outer, p.max_outer);
+  ctx->stats = stats;
+  return CL_OK;
+}
+
+void* stage_bytes(cl_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->stage_bytes) {
+    if (ctx->stage) cudaFree(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    if (cudaMalloc(&ctx->stage, bytes) != cudaSuccess) return nullptr;
+    ctx->stage_bytes = bytes;
+  }
+  return ctx->stage;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cl_abi_version(void) { return CL_ABI_VERSION; }
+
+int cl_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void cl_config_default(cl_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->th = 0.7;
+  c->max_outer = 200;
+  c->eps = 1e-6;
+  c->inner_steps = 50;
+  c->lr = 0.01;
+  c->opt = CL_OPT_ADAM;
+  c->w_tv = -1.0;
+  c->w_lv = -1.0;
+  c->lv_window = 3;
+  c->lv_stride = 2;
+  c->stall_tol = 1e-4;
+  c->stall_patience = 2;
+}
+
+const char* cl_last_error(const cl_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
+                  int a_layout, int* status) {
+  auto bail = [&](int code, const std::string& msg) -> cl_ctx* {
+    g_create_error = msg;
+    if (status) *status = code;
+    return nullptr;
+  };
+  if (!a || m <= 0 || n <= 0)
+    return bail(CL_ERR_DIMENSION, "cl_create: empty or null dictionary");
+  if (n > (1LL << 30) || m > (1LL << 30))
+    return bail(CL_ERR_DIMENSION, "cl_create: dictionary too large");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return bail(CL_ERR_CUDA, std::string("cl_create: no CUDA device: ") +
+                                 cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= ndev)
+    return bail(CL_ERR_CUDA, "cl_create: device index out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess)
+    return bail(CL_ERR_CUDA, std::string("cl_create: ") + cudaGetErrorString(e));
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10)
+    return bail(CL_ERR_CUDA, "cl_create: this build targets sm_100a (B200) only");
+
+  auto* ctx = new cl_ctx();
+  ctx->device = device;
+  ctx->m = m;
+  ctx->n = n;
+  ctx->ldm = (m + 31) / 32 * 32;
+  ctx->sms = prop.multiProcessorCount;
+  // Atom-major fp32 copy (the reference's LossOps transpose, clomp.cpp:57-66,
+  // done once per dictionary instead of once per call).
+  std::vector<float> at((size_t)(n * ctx->ldm), 0.f);
+  double cmax = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    double ss = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      const float v = a_layout == CL_LAYOUT_REF ? a[i * n + j] : a[j * m + i];
+      at[(size_t)(j * ctx->ldm + i)] = v;
+      ss += (double)v * (double)v;
+    }
+    cmax = std::max(cmax, std::sqrt(ss));
+  }
+  ctx->colnorm_max = cmax;
+  const size_t bytes = at.size() * sizeof(float);
+  ctx->tc_ok = corr_tc_available();
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->at32, bytes) != cudaSuccess ||
+      cudaMemcpy(ctx->at32, at.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_counters, kNumCounters * sizeof(int32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    cl_destroy(ctx);
+    return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
+  }
+  if (ctx->tc_ok) {
+    if (cudaMalloc(&ctx->at_hi, bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->at_lo, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      cl_destroy(ctx);
+      return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
+    }
+    launch_split_tf32(ctx->at32, ctx->at_hi, ctx->at_lo, (int64_t)at.size(), ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cl_destroy(ctx);
+      return bail(CL_ERR_CUDA, "cl_create: tf32 split failed");
+    }
+  }
+  if (status) *status = CL_OK;
+  return ctx;
+}
+
+void cl_destroy(cl_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->at32);
+  cudaFree(ctx->at_hi);
+  cudaFree(ctx->at_lo);
+  cudaFree(ctx->wbuf);
+  cudaFree(ctx->bc);
+  cudaFree(ctx->stage);
+  if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int cl_set_corr_path(cl_ctx* ctx, int path) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (path < 0 || path > 2) return fail(ctx, CL_ERR_CONFIG, "cl_set_corr_path: 0, 1 or 2");
+  if (path == 2 && !corr_tc_available())
+    return fail(ctx, CL_ERR_UNSUPPORTED, "tcgen05 correlation kernel not available");
+  ctx->corr_force = path;
+  return CL_OK;
+}
+
+int cl_set_profiling(cl_ctx* ctx, int on) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  ctx->profiling = on != 0;
+  return CL_OK;
+}
+
+int cl_get_stats(const cl_ctx* ctx, cl_stats* out) {
+  if (!ctx || !out) return CL_ERR_INTERNAL;
+  *out = ctx->stats;
+  return CL_OK;
+}
+
+int cl_synchronize(cl_ctx* ctx) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  CL_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return CL_OK;
+}
+
+static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode,
+                      double mean_sq_all, const std::vector<double>* col_ms) {
+  int st = validate(ctx, cfg);
+  if (st) return st;
+  if (batch <= 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: empty batch");
+  if (mode != CL_MODE_JOINT && mode != CL_MODE_PER_SIGNAL)
+    return fail(ctx, CL_ERR_CONFIG, "clomp: unknown solve mode");
+  bool pri = false;
+  if (mode == CL_MODE_JOINT) {
+    pri = priors_active(cfg, mean_sq_all, batch, ctx->n);
+  } else if (col_ms) {
+    for (double ms : *col_ms) pri = pri || priors_active(cfg, ms, 1, ctx->n);
+  }
+  if (pri)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "clomp: TV/LV priors are not implemented on the B200 path; set "
+                "w_tv = w_lv = 0");
+  return CL_OK;
+}
+
+int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
+                   const cl_config* cfg, int mode, cl_result* out) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (!y && batch > 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: null y");
+  cudaSetDevice(ctx->device);
+  const int64_t m = ctx->m, n = ctx->n;
+  // mean(y^2) for resolve_weights (clomp.cpp:134-136), per batch and per column.
+  std::vector<double> col_ms;
+  double all = 0.0;
+  if (batch > 0) {
+    col_ms.assign((size_t)batch, 0.0);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t b = 0; b < batch; ++b) {
+        const double v = y_layout == CL_LAYOUT_REF ? y[i * batch + b] : y[b * m + i];
+        col_ms[(size_t)b] += v * v;
+      }
+    for (double& v : col_ms) {
+      all += v;
+      v /= (double)m;
+    }
+    all /= (double)(m * batch);
+  }
+  int st = check_call(ctx, batch, cfg, mode, all, &col_ms);
+  if (st) return st;
+
+  const int64_t cap = support_cap(ctx, cfg);
+  const size_t ybytes = (size_t)(m * batch) * sizeof(float);
+  const size_t obytes = align_up((size_t)(batch * cap) * 4, 256) +
+                        align_up((size_t)(batch * cap) * 8, 256) +
+                        4 * align_up((size_t)batch * 8, 256) + 256;
+  char* stg = static_cast<char*>(stage_bytes(ctx, align_up(ybytes, 256) + obytes));
+  if (!stg) return fail(ctx, CL_ERR_CUDA, "clomp: staging allocation failed");
+  float* d_y = reinterpret_cast<float*>(stg);
+  Carver cv{stg + align_up(ybytes, 256)};
+  OutPtrs o{};
+  o.cap = cap;
+  o.sup = cv.take<int32_t>(batch * cap);
+  o.coef = cv.take<double>(batch * cap);
+  o.cnt = cv.take<int32_t>(batch);
+  o.iters = cv.take<int32_t>(batch);
+  o.rn = cv.take<double>(batch);
+  o.conv = cv.take<uint8_t>(batch);
+  o.status = cv.take<int32_t>(batch);
+  CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, ctx->stream));
+  st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o);
+  if (st) return st;
+
+  std::vector<int32_t> h_sup((size_t)(batch * cap)), h_cnt((size_t)batch),
+      h_it((size_t)batch), h_st((size_t)batch);
+  std::vector<double> h_coef((size_t)(batch * cap)), h_rn((size_t)batch);
+  std::vector<uint8_t> h_cv((size_t)batch);
+  CL_CUDA(ctx, cudaMemcpy(h_sup.data(), o.sup, h_sup.size() * 4, cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_coef.data(), o.coef, h_coef.size() * 8, cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_cnt.data(), o.cnt, h_cnt.size() * 4, cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_it.data(), o.iters, h_it.size() * 4, cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_rn.data(), o.rn, h_rn.size() * 8, cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_cv.data(), o.conv, h_cv.size(), cudaMemcpyDeviceToHost));
+  CL_CUDA(ctx, cudaMemcpy(h_st.data(), o.status, h_st.size() * 4, cudaMemcpyDeviceToHost));
+
+  if (out) {
+    if (out->s) std::memset(out->s, 0, sizeof(double) * (size_t)(n * batch));
+    if (out->mask) std::memset(out->mask, 0, (size_t)(n * batch));
+    for (int64_t b = 0; b < batch; ++b) {
+      const int cnt = h_cnt[(size_t)b];
+      for (int k = 0; k < cnt; ++k) {
+        const int32_t j = h_sup[(size_t)(b * cap + k)];
+        const double v = h_coef[(size_t)(b * cap + k)];
+        if (k < out->cap) {
+          if (out->support) out->support[b * out->cap + k] = j;
+          if (out->coef) out->coef[b * out->cap + k] = v;
+        }
+        if (out->s) out->s[(int64_t)j * batch + b] = v;
+        if (out->mask) out->mask[(int64_t)j * batch + b] = 1;
+      }
+      if (out->count) out->count[b] = cnt;
+      if (out->iterations) out->iterations[b] = h_it[(size_t)b];
+      if (out->final_residual_norm) out->final_residual_norm[b] = h_rn[(size_t)b];
+      if (out->converged) out->converged[b] = h_cv[(size_t)b];
+      if (out->status) out->status[b] = h_st[(size_t)b];
+    }
+  }
+  if (mode == CL_MODE_JOINT && batch > 0 && h_st[0] != CL_OK) {
+    return fail(ctx, h_st[0],
+                h_st[0] == CL_ERR_NUMERICAL ? "clomp: loss diverged; reduce lr"
+                                            : "clomp: support capacity exceeded");
+  }
+  return CL_OK;
+}
+
+int cl_solve_batch_device(cl_ctx* ctx, const float* d_y, int64_t batch,
+                          const cl_config* cfg, int mode,
+                          const cl_device_result* out) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  // Prior weights need mean(y^2); the device path requires them off explicitly
+  // (w_tv == w_lv == 0), which is what every BASELINE config uses.
+  if (cfg && (cfg->w_tv != 0.0 || cfg->w_lv != 0.0))
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_solve_batch_device: set w_tv = w_lv = 0 (priors unsupported)");
+  int st = check_call(ctx, batch, cfg, mode, 0.0, nullptr);
+  if (st) return st;
+  if (!out) return fail(ctx, CL_ERR_DIMENSION, "cl_solve_batch_device: null result");
+  OutPtrs o{out->cap,  out->support, out->coef, out->count, out->iterations,
+            out->final_residual_norm, out->converged, out->status};
+  return solve_core(ctx, d_y, 0, batch, cfg, mode, o);
+}
+
+int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
+                      uint8_t* mask) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (!(th > 0.0) || th > 1.0)
+    return fail(ctx, CL_ERR_CONFIG, "inject_support: th must be in (0, 1]");
+  if (batch <= 0 || !r || !mask)
+    return fail(ctx, CL_ERR_DIMENSION, "inject_support: mask size mismatch");
+  cudaSetDevice(ctx->device);
+  const int64_t m = ctx->m, n = ctx->n, ldm = ctx->ldm;
+  const bool full = th < 1.0;
+  const int64_t ntile = (n + kCorrTileAtoms - 1) / kCorrTileAtoms;
+  int st = ensure_workspace(ctx, batch, n, full, false, ntile);
+  if (st) return st;
+  SolveParams p{};
+  p.B = batch;
+  p.n = n;
+  p.m = m;
+  p.ldm = ldm;
+  p.cap = n;
+  p.ntile = ntile;
+  p.mwords = (n + 31) / 32;
+  p.th = th;
+  p.delta_rel = delta_for(false);
+  p.colnorm_max = ctx->colnorm_max;
+  Work w = ctx->w;
+  w.r_hi = w.r_lo = nullptr;
+  std::vector<double> rt((size_t)(batch * ldm), 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t b = 0; b < batch; ++b) rt[(size_t)(b * ldm + i)] = r[i * batch + b];
+  std::vector<uint32_t> bits((size_t)(batch * p.mwords), 0u);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t b = 0; b < batch; ++b)
+      if (mask[j * batch + b]) bits[(size_t)(b * p.mwords + j / 32)] |= 1u << (j % 32);
+  cudaStream_t s = ctx->stream;
+  CL_CUDA(ctx, cudaMemcpyAsync(w.r64, rt.data(), rt.size() * 8, cudaMemcpyHostToDevice, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(w.maskbits, bits.data(), bits.size() * 4,
+                               cudaMemcpyHostToDevice, s));
+  CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
+  launch_inject_finish(p, w, s);
+  launch_corr_f64(p, w, full, s);
+  launch_select(p, w, full, s);
+  launch_rescan(p, w, (int)std::min<int64_t>(batch, ctx->sms), s);
+  CL_CUDA(ctx, cudaGetLastError());
+  CL_CUDA(ctx, cudaMemcpyAsync(bits.data(), w.maskbits, bits.size() * 4,
+                               cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaStreamSynchronize(s));
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t b = 0; b < batch; ++b)
+      mask[j * batch + b] = (bits[(size_t)(b * p.mwords + j / 32)] >> (j % 32)) & 1u;
+  return CL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// clomp_internal.cuh — device-side data layout and kernel launchers shared by
+// the CUDA translation units of libclomp_b200.so.  Not a public header.
+//
+// HBM layout:
+//   at32   [n][ldm] fp32   dictionary, atom-major (K-major GEMM operand); the
+//                          reference keeps A row-major m x n plus a transposed
+//                          copy per call (clomp.cpp:57-66).
+//   y32/y64, r32/r64 [B][ldm]   measurements and residuals, signal-major.
+//   per-signal state: support list in insertion order, coefficients, Gram
+//   G = A_S^T A_S (fp64, cap x cap), b = A_S^T y, optimizer moments, best
+//   snapshot, loss/stall bookkeeping (clomp.cpp:226-273).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace clb {
+
+constexpr int kCorrTileAtoms = 64;    // fp64 SIMT correlation tile (atoms)
+constexpr int kCorrTileSignals = 64;  // fp64 SIMT correlation tile (signals)
+constexpr int kWarpCap = 32;          // register-resident learning kernel limit
+
+struct SolveParams {
+  int64_t B, n, m, ldm, cap, ntile;
+  int64_t mwords;           // 32-bit words per signal in the mask bitmap
+  double th, eps, lr, stall_tol;
+  int32_t stall_patience, opt, inner, max_outer, mode;
+  const double* bc1;        // Adam bias corrections per global step (1-based)
+  const double* bc2;
+  double delta_rel;         // correlation error bound / (||a||max * ||r||)
+  double colnorm_max;
+};
+
+struct Work {
+  // operands
+  const float* at32 = nullptr;   // [n][ldm]
+  const float* at_hi = nullptr;  // [n][ldm] tf32 split (tensor path)
+  const float* at_lo = nullptr;
+  float* y32 = nullptr;          // [B][ldm]
+  double* y64 = nullptr;
+  double* r64 = nullptr;
+  float* r_hi = nullptr;         // [B][ldm] tf32 split of the residual
+  float* r_lo = nullptr;
+  // correlation candidates, [B][ntile]
+  double* cand_v1 = nullptr;
+  double* cand_v2 = nullptr;
+  int32_t* cand_i1 = nullptr;
+  double* scores = nullptr;      // [B][n] |A^T r| (th < 1 path)
+  // per-signal state
+  int32_t* sup = nullptr;        // [B][cap] insertion order
+  int32_t* cnt = nullptr;        // [B]
+  int32_t* gcnt = nullptr;       // [B] atoms whose Gram row/col is built
+  double* coef = nullptr;        // [B][cap]
+  double* mom1 = nullptr;        // [B][cap]
+  double* mom2 = nullptr;        // [B][cap]
+  double* gram = nullptr;        // [B][cap][cap]
+  double* bvec = nullptr;        // [B][cap]
+  uint32_t* maskbits = nullptr;  // [B][mwords]
+  double* best_coef = nullptr;   // [B][cap]
+  int32_t* best_cnt = nullptr;
+  double* best_L = nullptr;
+  double* prev_L = nullptr;
+  double* loss = nullptr;        // [B] current loss ||A_S c - y||^2
+  int32_t* stall = nullptr;
+  int32_t* iters = nullptr;
+  int32_t* active = nullptr;
+  uint8_t* conv = nullptr;       // eps break happened
+  int32_t* status = nullptr;
+  int32_t* changed = nullptr;
+  int32_t* rescan_list = nullptr;  // [B]
+  int32_t* counters = nullptr;     // see Counter
+  double* joint = nullptr;         // see Joint
+};
+
+enum Counter {
+  kRescanCount = 0,   // entries in rescan_list this outer iteration
+  kActiveCount = 1,   // signals still iterating after this outer iteration
+  kMaxCount = 2,      // max support size over the batch
+  kRescanTotal = 3,   // rescans over the whole solve
+  kNumCounters = 8
+};
+
+enum Joint {
+  kJBest = 0, kJPrev = 1, kJTotal = 2, kJStall = 3, kJImproved = 4,
+  kJStop = 5, kJConv = 6, kJStatus = 7, kJIters = 8, kJFinalRn = 9,
+  kNumJoint = 16
+};
+
+// ---- launchers (k_corr.cu) ----
+// fp64 SIMT correlation with fused top-2 epilogue (th == 1) or full |scores|.
+void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
+                     cudaStream_t s);
+// tcgen05 3xTF32 correlation with fused top-2 epilogue (th == 1).
+bool corr_tc_available();
+void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
+void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
+                       cudaStream_t s);
+
+// ---- launchers (k_solve.cu) ----
+void launch_init(const SolveParams& p, const Work& w, const float* y_in,
+                 int y_layout, bool y_on_device_signal_major, cudaStream_t s);
+void launch_select(const SolveParams& p, const Work& w, bool full_scores,
+                   cudaStream_t s);
+void launch_rescan(const SolveParams& p, const Work& w, int grid,
+                   cudaStream_t s);
+void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
+                  cudaStream_t s);
+void launch_joint_control(const SolveParams& p, const Work& w, int outer,
+                          bool init, cudaStream_t s);
+void launch_joint_snapshot(const SolveParams& p, const Work& w,
+                           cudaStream_t s);
+void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
+                     int32_t* sup_out, double* coef_out, int32_t* cnt_out,
+                     int32_t* iters_out, double* rn_out, uint8_t* conv_out,
+                     int32_t* status_out, cudaStream_t s);
+// inject_support unit path: residual already in w.r64 (and split), mask in
+// w.maskbits; appends nothing to the learning state.
+void launch_inject_finish(const SolveParams& p, const Work& w, cudaStream_t s);
+
+}  // namespace clb

@@ -1,0 +1,130 @@
+"""ctypes bindings to the test-side checkers (oracle/ and oracle/_ref/).
+
+TEST INFRASTRUCTURE ONLY: used by tests/, __graft_entry__.smoke() and the CPU
+legs of bench.py, never by the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_2501_11592_b200 import CConfig, ClompConfig
+
+ROOT = Path(__file__).resolve().parents[1]
+ORACLE_SO = ROOT / "oracle" / "_build" / "libclomp_oracle.so"
+REF_SO = ROOT / "oracle" / "_ref" / "libcskit_ref.so"
+
+ISA_SCALAR, ISA_AVX2 = 0, 1
+MODE_JOINT, MODE_PER_SIGNAL = 0, 1
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def build_oracle() -> None:
+    if not ORACLE_SO.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+
+
+_orc = None
+_ref = None
+
+
+def oracle() -> C.CDLL:
+    global _orc
+    if _orc is None:
+        build_oracle()
+        h = C.CDLL(str(ORACLE_SO))
+        vp, i64 = C.c_void_p, C.c_int64
+        h.orc_clomp_solve_batch.argtypes = [vp, i64, i64, vp, i64, C.POINTER(CConfig), C.c_int,
+                                            C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_char_p, C.c_int]
+        h.orc_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, C.c_int, vp]
+        h.orc_clomp_loss.argtypes = [vp, i64, i64, vp, i64, vp, vp, C.POINTER(CConfig), C.c_int, vp, vp]
+        h.orc_gradient_step.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(CConfig)]
+        _orc = h
+    return _orc
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        h = C.CDLL(str(REF_SO))
+        vp, i64 = C.c_void_p, C.c_int64
+        h.ref_clomp_solve_batch.argtypes = [vp, i64, i64, vp, i64, C.POINTER(CConfig), vp, vp, vp,
+                                            vp, vp, vp, C.c_char_p, C.c_int]
+        h.ref_clomp_solve.argtypes = [vp, i64, i64, vp, C.POINTER(CConfig), vp, vp, vp, vp, vp, vp,
+                                      C.c_char_p, C.c_int]
+        h.ref_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, vp]
+        h.ref_rng_draws.argtypes = [C.c_uint64, C.c_int, C.c_uint64, i64, vp, vp]
+        h.ref_dct_basis.argtypes = [i64, vp]
+        h.ref_force_isa.argtypes = [C.c_int]
+        _ref = h
+    return _ref
+
+
+def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False):
+    """Oracle restatement. A m x n, Y m x B (fp64 arrays of fp32 values)."""
+    A = np.ascontiguousarray(A, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    if Y.ndim == 1:
+        Y = Y.reshape(-1, 1)
+    m, n = A.shape
+    B = Y.shape[1]
+    s = np.zeros((n, B))
+    mk = np.zeros((n, B), np.uint8)
+    it = np.zeros(B, np.int64)
+    rn = np.zeros(B)
+    cv = np.zeros(B, np.uint8)
+    st = np.zeros(B, np.int32)
+    tr = np.zeros((B, max(1, cfg.max_outer), 4)) if trace else None
+    err = C.create_string_buffer(256)
+    c = cfg.to_c()
+    code = oracle().orc_clomp_solve_batch(_p(A), m, n, _p(Y), B, C.byref(c), isa, mode, _p(s),
+                                          _p(mk), _p(it), _p(rn), _p(cv), _p(st), _p(tr), err, 256)
+    return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
+                final_residual_norm=rn, converged=cv.astype(bool), status=st, trace=tr)
+
+
+def ref_solve_batch(A, Y, cfg: ClompConfig):
+    """The unmodified reference clomp_solve_batch."""
+    A = np.ascontiguousarray(A, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    if Y.ndim == 1:
+        Y = Y.reshape(-1, 1)
+    m, n = A.shape
+    B = Y.shape[1]
+    s = np.zeros((n, B))
+    mk = np.zeros((n, B), np.uint8)
+    it = np.zeros(1, np.int64)
+    rn = np.zeros(1)
+    cv = np.zeros(1, np.uint8)
+    wall = np.zeros(1)
+    err = C.create_string_buffer(256)
+    c = cfg.to_c()
+    code = ref().ref_clomp_solve_batch(_p(A), m, n, _p(Y), B, C.byref(c), _p(s), _p(mk), _p(it),
+                                       _p(rn), _p(cv), _p(wall), err, 256)
+    return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=int(it[0]),
+                final_residual_norm=float(rn[0]), converged=bool(cv[0]), wall_s=float(wall[0]))
+
+
+def orc_inject(A, R, th, mask, isa=ISA_AVX2):
+    A = np.ascontiguousarray(A, np.float64)
+    R = np.ascontiguousarray(R, np.float64)
+    if R.ndim == 1:
+        R = R.reshape(-1, 1)
+    mk = np.ascontiguousarray(mask, np.uint8).copy()
+    code = oracle().orc_inject_support(_p(A), A.shape[0], A.shape[1], _p(R), R.shape[1],
+                                       float(th), isa, _p(mk))
+    return code, mk
+
+
+def support_sets(mask):
+    return [tuple(np.flatnonzero(mask[:, b])) for b in range(mask.shape[1])]

@@ -1,0 +1,55 @@
+"""The C-ABI library loads and exports every symbol include/clomp_b200.h
+declares; host-side logic that needs no GPU (CPU-only)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2501_11592_b200 as cl
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "clomp_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:[\w\*]+\s+\**)+\**(cl_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_what_python_binds():
+    syms = declared_symbols()
+    assert "cl_solve_batch" in syms and "cl_create" in syms
+    for s in syms:
+        assert s in cl.EXPORTED, s
+
+
+def test_library_exports_every_declared_symbol(built_lib):
+    h = C.CDLL(str(built_lib))
+    for s in declared_symbols() + ["cl_rng_draws", "cl_gen_problem_1d"]:
+        assert hasattr(h, s), f"missing export {s}"
+    assert h.cl_abi_version() == 1
+
+
+def test_default_config_matches_reference(built_lib):
+    c = cl.CConfig()
+    cl.lib().cl_config_default(C.byref(c))
+    d = cl.ClompConfig()
+    for f, _ in cl.CConfig._fields_:
+        if f == "pad0":
+            continue
+        assert getattr(c, f) == getattr(d, f), f
+    # clomp.hpp:16-33
+    assert (d.th, d.max_outer, d.eps, d.inner_steps, d.lr, d.opt) == (0.7, 200, 1e-6, 50, 0.01, cl.ADAM)
+
+
+def test_no_device_fails_loudly(built_lib):
+    if cl.lib().cl_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(cl.CudaError):
+        cl.ClompContext(np.ones((4, 8), np.float32))
+
+
+def test_baseline_mapping():
+    c = cl.ClompConfig.baseline(32)
+    assert (c.th, c.max_outer, c.inner_steps, c.lr, c.opt, c.w_tv, c.w_lv) == (1.0, 32, 200, 0.1, cl.PLAIN, 0.0, 0.0)

@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference's golden outputs.
+
+Bar (north star): identical support sets, identical iteration
+counts and converged flags, coefficients within 1e-4 relative
+(max|c - c_ref| / max|c_ref|), reconstruction SNR within 0.1 dB.  The learning
+path is fp64, so the tests also hold a much tighter 1e-9 on the small cases.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2501_11592_b200 as cl
+import refbind
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+CASES = json.loads((GOLD / "cases.json").read_text())
+ARR = np.load(GOLD / "golden.npz")
+
+COEF_RTOL = 1e-4     # north-star tolerance
+TIGHT_RTOL = 1e-9    # what fp64 learning actually achieves on small cases
+
+
+def rel_coef_err(s, s_ref):
+    den = np.max(np.abs(s_ref)) if np.any(s_ref) else 1.0
+    return float(np.max(np.abs(s - s_ref)) / den)
+
+
+def snr_db(x, xh):
+    e = np.sum((x - xh) ** 2)
+    return np.inf if e == 0 else 10 * np.log10(np.sum(x ** 2) / e)
+
+
+@pytest.fixture(scope="module", params=["f64", "auto"])
+def corr_path(request, gpu_available):
+    return request.param
+
+
+def make_ctx(A, path="auto"):
+    ctx = cl.ClompContext(np.asarray(A, np.float32))
+    if path == "f64":
+        ctx.set_corr_path(1)
+    return ctx
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "solve"], ids=lambda c: c["name"])
+def test_solve_matches_reference_golden(case, corr_path):
+    name = case["name"]
+    A = ARR[f"{name}/A"]
+    Y = ARR[f"{name}/Y"]
+    cfg = cl.ClompConfig(**case["cfg"])
+    ctx = make_ctx(A, corr_path)
+    mode = cl.MODE_JOINT if case["api"] == "batch" else cl.MODE_PER_SIGNAL
+    if case["code"] != 0:
+        exc = {2: cl.ConfigError, 3: cl.DimensionError, 4: cl.NumericalError}[case["code"]]
+        with pytest.raises(exc):
+            cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
+        return
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
+    assert np.array_equal(r.mask, ARR[f"{name}/mask"]), "support sets differ"
+    assert np.array_equal(r.iterations, ARR[f"{name}/iterations"])
+    assert np.array_equal(r.converged, ARR[f"{name}/converged"].astype(bool))
+    s_ref = ARR[f"{name}/s"]
+    assert rel_coef_err(r.s, s_ref) <= TIGHT_RTOL
+    np.testing.assert_allclose(r.final_residual_norm, ARR[f"{name}/final_residual_norm"],
+                               rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "inject"], ids=lambda c: c["name"])
+def test_inject_support_matches_reference(case, gpu_available):
+    name = case["name"]
+    ctx = make_ctx(ARR[f"{name}/A"])
+    out = cl.inject_support(ctx, ARR[f"{name}/R"], case["th"], ARR[f"{name}/mask_in"])
+    assert np.array_equal(out, ARR[f"{name}/mask_out"])
+    with pytest.raises(cl.ConfigError):
+        cl.inject_support(ctx, ARR[f"{name}/R"], 0.0, ARR[f"{name}/mask_in"])
+    with pytest.raises(cl.DimensionError):
+        cl.inject_support(ctx, ARR[f"{name}/R"], 0.7, np.zeros(3, np.uint8))
+
+
+def test_config1_full_vs_reference(gpu_available):
+    """BASELINE config 1 (N=256, M=128, K=10, seed 0) against the reference's
+    own output, plus truth recovery and SNR."""
+    A = ARR["cfg1_full/A"]
+    Y = ARR["cfg1_full/Y"]
+    X = ARR["cfg1_full/X"]
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(10)
+    r = cl.clomp_solve(ctx, Y[:, 0], cfg)
+    assert np.array_equal(r.mask, ARR["cfg1_full/mask"][:, 0])
+    assert set(np.flatnonzero(r.mask)) == set(np.flatnonzero(X[:, 0]))
+    assert r.iterations == 10 and r.converged
+    s_ref = ARR["cfg1_full/s"][:, 0]
+    assert rel_coef_err(r.values, s_ref) <= COEF_RTOL
+    assert abs(snr_db(X[:, 0], r.values) - snr_db(X[:, 0], s_ref)) < 0.1
+
+
+def _subset_parity(A, Y, cfg, idx, gpu_res, X=None):
+    ref = refbind.orc_solve(A.astype(np.float64), Y[:, idx].astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL, trace=True)
+    assert np.all(ref["status"] == 0)
+    for q, b in enumerate(idx):
+        ms = np.flatnonzero(gpu_res.mask[:, b])
+        mr = np.flatnonzero(ref["mask"][:, q])
+        assert np.array_equal(ms, mr), f"signal {b}: support differs"
+        assert gpu_res.iterations[b] == ref["iterations"][q]
+        assert gpu_res.converged[b] == ref["converged"][q]
+        assert rel_coef_err(gpu_res.s[:, b], ref["s"][:, q]) <= COEF_RTOL
+        if X is not None:
+            assert abs(snr_db(X[:, b], gpu_res.s[:, b]) - snr_db(X[:, b], ref["s"][:, q])) < 0.1
+
+
+def test_config2_full_batch_subset_parity(gpu_available):
+    """Config 2 (N=1024, M=512, K=32, B=4096, 40 dB) solved as one batch on
+    the GPU; 24 signals spread over the batch are re-solved by the oracle
+    (per-signal semantics make each column independent of the others)."""
+    c = cl.CONFIGS[2]
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(c["k"])
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.all(r.status == 0)
+    assert np.all(r.iterations == c["k"])
+    idx = np.linspace(0, c["batch"] - 1, 24).astype(int)
+    _subset_parity(A, Y, cfg, idx, r, X)
+    # whole-batch properties: K atoms each, high SNR recovery
+    assert np.all(r.mask.sum(0) == c["k"])
+    snrs = np.array([snr_db(X[:, b], r.s[:, b]) for b in range(0, c["batch"], 64)])
+    assert np.median(snrs) > 30.0
+
+
+def test_joint_mode_batch_of_nine_matches_reference(gpu_available):
+    name = "small_th1_plain_b9_tile"
+    ctx = make_ctx(ARR[f"{name}/A"])
+    cfg = cl.ClompConfig.baseline(6)
+    r = cl.clomp_solve_batch(ctx, ARR[f"{name}/Y"], cfg, mode=cl.MODE_JOINT)
+    assert np.array_equal(r.mask, ARR[f"{name}/mask"])
+    assert rel_coef_err(r.s, ARR[f"{name}/s"]) <= TIGHT_RTOL
+
+
+def test_wrapper_equals_one_column_batch_and_determinism(gpu_available):
+    name = "small_th1_plain_b3_noisy"
+    A, Y = ARR[f"{name}/A"], ARR[f"{name}/Y"]
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig(max_outer=6, inner_steps=12, w_tv=0.0, w_lv=0.0)
+    one = cl.clomp_solve(ctx, Y[:, 0], cfg)
+    bat = cl.clomp_solve_batch(ctx, Y[:, :1], cfg)
+    assert np.array_equal(one.values, bat.s[:, 0])
+    assert np.array_equal(one.mask, bat.mask[:, 0])
+    assert one.iterations == bat.iterations[0]
+    r1 = cl.clomp_solve_batch(ctx, Y, cl.ClompConfig.baseline(5), mode=cl.MODE_PER_SIGNAL)
+    r2 = cl.clomp_solve_batch(ctx, Y, cl.ClompConfig.baseline(5), mode=cl.MODE_PER_SIGNAL)
+    assert np.array_equal(r1.s, r2.s) and np.array_equal(r1.mask, r2.mask)
+
+
+def test_errors_map_to_reference_exceptions(gpu_available):
+    A = ARR["small_th1_plain_b1/A"]
+    ctx = make_ctx(A)
+    y = ARR["small_th1_plain_b1/Y"]
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_solve_batch(ctx, y, cl.ClompConfig(th=1.5, w_tv=0, w_lv=0))
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_solve_batch(ctx, y, cl.ClompConfig(lr=0.0, w_tv=0, w_lv=0))
+    with pytest.raises(cl.DimensionError):
+        cl.clomp_solve_batch(ctx, np.zeros((3, 1), np.float32), cl.ClompConfig(w_tv=0, w_lv=0))
+    with pytest.raises(cl.DimensionError):
+        cl.clomp_solve_batch(ctx, np.zeros((A.shape[0], 0), np.float32), cl.ClompConfig(w_tv=0, w_lv=0))
+    with pytest.raises(cl.UnsupportedError):
+        cl.clomp_solve_batch(ctx, y, cl.ClompConfig())  # default auto priors
+    with pytest.raises(cl.NumericalError):
+        cl.clomp_solve_batch(ctx, y, cl.ClompConfig(th=1.0, opt=cl.PLAIN, lr=1e6, w_tv=0, w_lv=0))
+    # per-signal mode reports divergence per signal instead of aborting the batch
+    r = cl.clomp_solve_batch(ctx, y, cl.ClompConfig(th=1.0, opt=cl.PLAIN, lr=1e6, w_tv=0, w_lv=0),
+                             mode=cl.MODE_PER_SIGNAL)
+    assert r.status[0] == cl.CL_ERR_NUMERICAL
+
+
+def test_large_support_block_kernel(gpu_available):
+    """Supports beyond 32 atoms run on the block-per-signal learning kernel."""
+    A, X, Y, _ = cl.gen_problem_1d(11, 256, 512, 48, 4, snr_db=50.0)
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(48)
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    _subset_parity(A, Y, cfg, np.arange(4), r, X)
+
+
+def test_config3_law_reduced(gpu_available):
+    """Config-3 value law (+-(1+U), noiseless) at reduced size, with supports
+    up to 96 atoms (block kernel, G in shared memory)."""
+    A, X, Y, _ = cl.gen_problem_1d(12, 512, 2048, 96, 3, value_law=1)
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(96)
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    _subset_parity(A, Y, cfg, np.arange(3), r, X)
+    for b in range(3):
+        assert set(np.flatnonzero(r.mask[:, b])) == set(np.flatnonzero(X[:, b]))
