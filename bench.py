@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py — CLOMP reconstruction throughput on B200.
+
+Metric (BASELINE.json): signals reconstructed per second at fixed (N, M, K),
+plus the roofline fraction of the dominant kernel.  Default workload is
+BASELINE config 2 (configs[1]): N=1024, M=512, K=32, 4096 signals per GPU,
+40 dB, lr 0.1, 200 epochs, th=1 / max_outer=K / plain GD / priors off
+(SURVEY.md §8d mapping).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one full CLOMP solve (K outer iterations x 200 epochs) of one batch
+of 4096 signals already resident in HBM.  Multi-GPU: every rank solves its own
+4096-signal batch (per-signal semantics: no data-path collective), so scaling
+is weak; value = all ranks' signals / max-over-ranks step time.
+
+--impl reference times the unmodified reference library (oracle/_ref,
+compiled from /root/reference/proj/src) on the host cores: P single-threaded
+workers (the library has no threads), each solving a contiguous chunk of 8
+signals with clomp_solve_batch (its AVX2 4x8 GEMM tile path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "signals reconstructed/sec at fixed (N,M,K)"
+UNIT = "signals/s"
+CHUNK = 8  # signals per reference worker call (AVX2 tile width)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05")
+    return ap.parse_args()
+
+
+def workload(cfg_id: int, rank: int):
+    import paper_2501_11592_b200 as cl
+
+    c = dict(cl.CONFIGS[cfg_id])
+    c["seed"] = c["seed"] + 1000 * rank
+    return c
+
+
+def config_block(c, n_gpus):
+    return {
+        "workload": f"{c['name']}: N={c['n']} M={c['m']} K={c['k']} batch={c['batch']}/GPU "
+                    f"{'noiseless' if c['snr_db'] < 0 else str(c['snr_db']) + ' dB'}",
+        "n": c["n"], "m": c["m"], "k": c["k"], "batch_per_gpu": c["batch"],
+        "global_batch": c["batch"] * n_gpus, "lr": 0.1, "epochs": 200,
+        "th": 1.0, "max_outer": c["k"], "optimizer": "plain", "priors": "off",
+        "mode": "per_signal (clomp_solve per column)", "seed": c["seed"],
+        "parallelism": f"signal-shard x{n_gpus}, no collectives",
+        "l2": "flushed between timed steps (256 MiB write)",
+    }
+
+
+# ----------------------------------------------------------- reference arm
+def _ref_worker(args):
+    core, A, Ychunk, cfgd = args
+    try:
+        os.sched_setaffinity(0, {core})
+    except Exception:
+        pass
+    sys.path.insert(0, str(ROOT / "tests"))
+    import refbind
+    from paper_2501_11592_b200 import ClompConfig
+
+    cfg = ClompConfig(**cfgd)
+    t0 = time.perf_counter()
+    r = refbind.ref_solve_batch(A, Ychunk, cfg)
+    return time.perf_counter() - t0, r["code"], Ychunk.shape[1]
+
+
+def reference_round(A64, Y64, cfg, workers: int):
+    """One bounded sample: `workers` processes x CHUNK signals, in parallel."""
+    import multiprocessing as mp
+    import dataclasses
+
+    cfgd = dataclasses.asdict(cfg)
+    B = Y64.shape[1]
+    jobs = []
+    for w in range(workers):
+        lo = (w * CHUNK) % B
+        jobs.append((w % (os.cpu_count() or 1), A64, np.ascontiguousarray(Y64[:, lo:lo + CHUNK]), cfgd))
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_ref_worker, jobs)
+    wall = time.perf_counter() - t0
+    if any(code != 0 for _, code, _ in res):
+        raise RuntimeError("reference solve failed")
+    sig = sum(n for _, _, n in res)
+    return sig / wall, wall, sig
+
+
+def cpu_info():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_workers():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import paper_2501_11592_b200 as cl
+    sys.path.insert(0, str(ROOT / "tests"))
+    import refbind
+
+    c = workload(args.config, 0)
+    if not refbind.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcskit_ref.so not built"}))
+        return
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    A64, Y64 = A.astype(np.float64), Y.astype(np.float64)
+    cfg = cl.ClompConfig.baseline(c["k"])
+    P = host_workers()
+    for _ in range(args.warmup):
+        reference_round(A64, Y64, cfg, min(P, 2))
+    vals, walls = [], []
+    for _ in range(args.steps):
+        v, wall, sig = reference_round(A64, Y64, cfg, P)
+        vals.append(v)
+        walls.append(wall)
+    value = statistics.mean(vals)
+    sample = f"{P} workers x {CHUNK} signals per step (clomp_solve_batch, AVX2), {sig} signals/step"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(c, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "reference",
+                         "sample": sample, "cpu": cpu_info()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+    import torch
+    import paper_2501_11592_b200 as cl
+
+    dist = world > 1
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = workload(args.config, rank)
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    B, m, n = c["batch"], c["m"], c["n"]
+    cfg = cl.ClompConfig.baseline(c["k"])
+    ctx = cl.ClompContext(A, device=local_rank)
+    if args.corr_path:
+        ctx.set_corr_path(args.corr_path)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    d_y = torch.from_numpy(np.ascontiguousarray(Y.T)).to(dev)  # signal-major B x m
+    cap = min(n, c["k"] + 16)
+    o_sup = torch.zeros((B, cap), dtype=torch.int32, device=dev)
+    o_coef = torch.zeros((B, cap), dtype=torch.float64, device=dev)
+    o_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+    o_it = torch.zeros(B, dtype=torch.int32, device=dev)
+    o_rn = torch.zeros(B, dtype=torch.float64, device=dev)
+    o_cv = torch.zeros(B, dtype=torch.uint8, device=dev)
+    o_st = torch.zeros(B, dtype=torch.int32, device=dev)
+    dres = cl.CDeviceResult(cap, o_sup.data_ptr(), o_coef.data_ptr(), o_cnt.data_ptr(),
+                            o_it.data_ptr(), o_rn.data_ptr(), o_cv.data_ptr(), o_st.data_ptr())
+    ccfg = cfg.to_c()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        code = cl.lib().cl_solve_batch_device(ctx.handle, C.c_void_p(d_y.data_ptr()), B,
+                                              C.byref(ccfg), cl.MODE_PER_SIGNAL, C.byref(dres))
+        if code:
+            cl._raise(code, ctx.handle)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(o_st.max()) == 0, "solve reported a failing signal"
+    launches_per_step = ctx.stats()["kernel_launches"]
+
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    evs = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    times = [a.elapsed_time(b) for a, b in evs]
+    ms = statistics.mean(times)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = B * world / (ms_max / 1000.0)
+
+    # Per-phase breakdown of one solve (profiling events, outside the timed region).
+    ctx.set_profiling(True)
+    with torch.cuda.stream(stream):
+        flush.fill_(2)
+    step()
+    torch.cuda.synchronize()
+    prof = ctx.stats()
+    ctx.set_profiling(False)
+
+    # End to end through the public API: host y in, host results out.
+    e2e_ms = []
+    for _ in range(min(args.steps, 3)):
+        with torch.cuda.stream(stream):
+            flush.fill_(3)
+        torch.cuda.synchronize()
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        st = ctx.stats()
+        e2e_ms.append(st["e2e_ms"])
+    assert np.all(r.status == 0)
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if dist:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = B * world / (float(te.item()) / 1000.0)
+
+    if rank != 0:
+        return
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    outers = prof["outer_iterations"]
+    corr_flops = 2.0 * n * m * B  # one launch: A^T R over the batch
+    corr_ms_launch = prof["corr_ms"] / max(outers, 1)
+    if prof["corr_path"] == 1:
+        # 3xTF32: 3 tf32 MMAs per product; the useful rate is compared with
+        # the measured bf16 peak / 2 (tf32 rate) / 3 (three MMAs).
+        peak = peaks.get("bf16_tflops", 1590.0) / 2.0 / 3.0
+        bound, punit = "tensor", "TFLOP/s (fp32-equivalent 3xTF32)"
+        peak_src = "MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (3xTF32), derived"
+    else:
+        clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        peak = 148 * 64 * 2 * clk / 1e12
+        bound, punit = "fp64", "TFLOP/s"
+        peak_src = "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x measured SM clock"
+    achieved = corr_flops / (corr_ms_launch / 1000.0) / 1e12
+    roofline = {
+        "kernel": "K1 correlation A^T R + top-2 epilogue",
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": punit,
+        "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "algorithmic_per_launch": f"2*N*M*B = {corr_flops:.3e} FLOP",
+        "avg_launch_ms": corr_ms_launch,
+        "phase_ms_per_step": {"corr": prof["corr_ms"], "select_rescan": prof["select_ms"],
+                              "learn": prof["learn_ms"], "total": prof["total_ms"]},
+        "rescans_per_step": prof["rescans"],
+    }
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded cskit::Rng restatement, BASELINE config laws)",
+        "config": config_block(c, world),
+        "roofline": roofline,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
+                "d2h_bytes_per_step": st["d2h_bytes"],
+                "path": "clomp_solve_batch (host numpy y in, host results out)"},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import refbind
+        if refbind.ref_available():
+            P = host_workers()
+            v, wall, sig = reference_round(A.astype(np.float64), Y.astype(np.float64), cfg, P)
+            out["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": P, "kind": "reference",
+                "sample": f"{P} workers x {CHUNK} signals of this workload, one round ({wall:.1f} s)",
+                "cpu": cpu_info()}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

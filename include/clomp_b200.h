@@ -156,6 +156,10 @@ typedef struct cl_stats {
   double total_ms;              /* device time of the whole solve           */
   int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32            */
   int32_t pad0;
+  double e2e_ms;                /* cl_solve_batch: H2D + solve + D2H, events */
+  double select_ms;             /* device time of select + fp64 rescans     */
+  int64_t h2d_bytes;            /* bytes copied host->device by that call   */
+  int64_t d2h_bytes;            /* bytes copied device->host by that call   */
 } cl_stats;
 int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 
@@ -164,6 +168,10 @@ int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 int cl_set_corr_path(cl_ctx* ctx, int path);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);
+/* Run this context's work on a caller-owned cudaStream_t (NULL restores the
+ * context's own stream).  Lets a caller order the solve with its own work and
+ * time it with events on that stream. */
+int cl_set_stream(cl_ctx* ctx, void* stream);
 
 int cl_abi_version(void);
 int cl_device_count(void);

@@ -134,6 +134,10 @@ class CStats(C.Structure):
         ("total_ms", C.c_double),
         ("corr_path", C.c_int32),
         ("pad0", C.c_int32),
+        ("e2e_ms", C.c_double),
+        ("select_ms", C.c_double),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
     ]
 
 
@@ -142,6 +146,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
+    "cl_set_stream",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
 
@@ -170,6 +175,7 @@ def lib() -> C.CDLL:
         h.cl_get_stats.argtypes = [vp, C.POINTER(CStats)]
         h.cl_set_corr_path.argtypes = [vp, i32]
         h.cl_set_profiling.argtypes = [vp, i32]
+        h.cl_set_stream.argtypes = [vp, vp]
         h.cl_config_default.argtypes = [C.POINTER(CConfig)]
         h.cl_rng_draws.argtypes = [C.c_uint64, i32, C.c_uint64, i64, vp, vp]
         h.cl_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, i32, i32, C.c_double, vp, vp, vp, vp]
@@ -292,6 +298,12 @@ class ClompContext:
     def set_profiling(self, on: bool):
         _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)
 
+    def set_stream(self, stream_handle: int | None):
+        """Issue work on a caller-owned cudaStream_t (e.g. torch's
+        stream.cuda_stream); None restores the context's own stream."""
+        _raise(lib().cl_set_stream(self._h, C.c_void_p(stream_handle) if stream_handle else None),
+               self._h)
+
     def stats(self) -> dict:
         s = CStats()
         _raise(lib().cl_get_stats(self._h, C.byref(s)), self._h)
@@ -316,7 +328,7 @@ def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
         B = y.shape[0]
         lay = LAYOUT_T
     n = ctx.n
-    cap = max(1, n if cfg.th < 1.0 else min(n, max(1, int(cfg.max_outer))))
+    cap = max(1, n if cfg.th < 1.0 else min(n, max(1, int(cfg.max_outer)) + 16))
     sup = np.zeros((max(B, 1), cap), np.int32)
     coef = np.zeros((max(B, 1), cap), np.float64)
     cnt = np.zeros(max(B, 1), np.int32)

@@ -26,6 +26,8 @@ namespace {
 
 thread_local std::string g_create_error;
 
+constexpr int64_t kTieSlack = 16;
+
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carver {
@@ -44,7 +46,8 @@ struct Carver {
 
 struct cl_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream all work is issued on
+  cudaStream_t own_stream = nullptr;  // created by cl_create
   int64_t m = 0, n = 0, ldm = 0;
   float* at32 = nullptr;
   float* at_hi = nullptr;
@@ -118,8 +121,10 @@ bool priors_active(const cl_config* c, double mean_sq, int64_t batch, int64_t n)
   return w_tv > 0.0 || (w_lv > 0.0 && lv_fits);
 }
 
+// Per-signal support capacity.  th == 1 adds one atom per outer iteration
+// except on exact ties (clomp.cpp:49-51 injects every tie), hence the slack.
 int64_t support_cap(const cl_ctx* ctx, const cl_config* c) {
-  if (c->th >= 1.0) return std::min<int64_t>(ctx->n, (int64_t)c->max_outer);
+  if (c->th >= 1.0) return std::min<int64_t>(ctx->n, (int64_t)c->max_outer + kTieSlack);
   return ctx->n;
 }
 
@@ -274,7 +279,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   cl_stats stats{};
   stats.corr_path = tensor ? 1 : 0;
   int64_t launches = 0;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[5] = {};
   if (ctx->profiling)
     for (auto& e : ev) cudaEventCreate(&e);
 
@@ -295,6 +300,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       launch_corr_tc(p, w, s);
     else
       launch_corr_f64(p, w, full_scores, s);
+    if (ctx->profiling) cudaEventRecord(ev[4], s);
     launch_select(p, w, full_scores, s);
     launch_rescan(p, w, rescan_grid, s);
     launches += 3;
@@ -313,10 +319,12 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                                  cudaMemcpyDeviceToHost, s));
     CL_CUDA(ctx, cudaStreamSynchronize(s));
     if (ctx->profiling) {
-      float a = 0.f, b2 = 0.f;
-      cudaEventElapsedTime(&a, ev[1], ev[2]);
+      float a = 0.f, b2 = 0.f, c2 = 0.f;
+      cudaEventElapsedTime(&a, ev[1], ev[4]);
+      cudaEventElapsedTime(&c2, ev[4], ev[2]);
       cudaEventElapsedTime(&b2, ev[2], ev[3]);
       stats.corr_ms += a;
+      stats.select_ms += c2;
       stats.learn_ms += b2;
     }
     if (ctx->h_counters[kActiveCount] == 0) break;
@@ -440,8 +448,10 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
   ctx->colnorm_max = cmax;
   const size_t bytes = at.size() * sizeof(float);
   ctx->tc_ok = corr_tc_available();
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&ctx->at32, bytes) != cudaSuccess ||
+  ctx->stream = nullptr;
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) == cudaSuccess)
+    ctx->stream = ctx->own_stream;
+  if (!ctx->stream || cudaMalloc(&ctx->at32, bytes) != cudaSuccess ||
       cudaMemcpy(ctx->at32, at.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMallocHost(&ctx->h_counters, kNumCounters * sizeof(int32_t)) != cudaSuccess) {
     cudaGetLastError();
@@ -477,7 +487,7 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->bc);
   cudaFree(ctx->stage);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
 
@@ -487,6 +497,14 @@ int cl_set_corr_path(cl_ctx* ctx, int path) {
   if (path == 2 && !corr_tc_available())
     return fail(ctx, CL_ERR_UNSUPPORTED, "tcgen05 correlation kernel not available");
   ctx->corr_force = path;
+  return CL_OK;
+}
+
+int cl_set_stream(cl_ctx* ctx, void* stream) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
   return CL_OK;
 }
 
@@ -572,21 +590,42 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   o.rn = cv.take<double>(batch);
   o.conv = cv.take<uint8_t>(batch);
   o.status = cv.take<int32_t>(batch);
+  cudaEvent_t e2e[2];
+  cudaEventCreate(&e2e[0]);
+  cudaEventCreate(&e2e[1]);
+  cudaEventRecord(e2e[0], ctx->stream);
   CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, ctx->stream));
   st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o);
-  if (st) return st;
+  if (st) {
+    cudaEventDestroy(e2e[0]);
+    cudaEventDestroy(e2e[1]);
+    return st;
+  }
 
   std::vector<int32_t> h_sup((size_t)(batch * cap)), h_cnt((size_t)batch),
       h_it((size_t)batch), h_st((size_t)batch);
   std::vector<double> h_coef((size_t)(batch * cap)), h_rn((size_t)batch);
   std::vector<uint8_t> h_cv((size_t)batch);
-  CL_CUDA(ctx, cudaMemcpy(h_sup.data(), o.sup, h_sup.size() * 4, cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_coef.data(), o.coef, h_coef.size() * 8, cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_cnt.data(), o.cnt, h_cnt.size() * 4, cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_it.data(), o.iters, h_it.size() * 4, cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_rn.data(), o.rn, h_rn.size() * 8, cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_cv.data(), o.conv, h_cv.size(), cudaMemcpyDeviceToHost));
-  CL_CUDA(ctx, cudaMemcpy(h_st.data(), o.status, h_st.size() * 4, cudaMemcpyDeviceToHost));
+  cudaStream_t s = ctx->stream;
+  CL_CUDA(ctx, cudaMemcpyAsync(h_sup.data(), o.sup, h_sup.size() * 4, cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_coef.data(), o.coef, h_coef.size() * 8, cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_cnt.data(), o.cnt, h_cnt.size() * 4, cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_it.data(), o.iters, h_it.size() * 4, cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_rn.data(), o.rn, h_rn.size() * 8, cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_cv.data(), o.conv, h_cv.size(), cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(h_st.data(), o.status, h_st.size() * 4, cudaMemcpyDeviceToHost, s));
+  cudaEventRecord(e2e[1], s);
+  CL_CUDA(ctx, cudaStreamSynchronize(s));
+  {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e2e[0], e2e[1]);
+    ctx->stats.e2e_ms = ms;
+    ctx->stats.h2d_bytes = (int64_t)ybytes;
+    ctx->stats.d2h_bytes = (int64_t)(h_sup.size() * 4 + h_coef.size() * 8 + h_cnt.size() * 4 +
+                                     h_it.size() * 4 + h_rn.size() * 8 + h_cv.size() + h_st.size() * 4);
+    cudaEventDestroy(e2e[0]);
+    cudaEventDestroy(e2e[1]);
+  }
 
   if (out) {
     if (out->s) std::memset(out->s, 0, sizeof(double) * (size_t)(n * batch));
