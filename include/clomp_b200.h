@@ -173,6 +173,12 @@ int cl_set_profiling(cl_ctx* ctx, int on);
  * time it with events on that stream. */
 int cl_set_stream(cl_ctx* ctx, void* stream);
 
+/* Test hook: correlation scores A^T r for a batch of fp32 residuals
+ * r (B x m, signal-major host) through the fp64 SIMT kernel (path 1, |scores|)
+ * or the tcgen05 3xTF32 kernel (path 2, signed scores); scores: host B x n. */
+int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
+                    double* scores);
+
 int cl_abi_version(void);
 int cl_device_count(void);
 

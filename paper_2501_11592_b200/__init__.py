@@ -146,7 +146,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream",
+    "cl_set_stream", "cl_debug_scores",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
 
@@ -176,6 +176,7 @@ def lib() -> C.CDLL:
         h.cl_set_corr_path.argtypes = [vp, i32]
         h.cl_set_profiling.argtypes = [vp, i32]
         h.cl_set_stream.argtypes = [vp, vp]
+        h.cl_debug_scores.argtypes = [vp, vp, i64, i32, vp]
         h.cl_config_default.argtypes = [C.POINTER(CConfig)]
         h.cl_rng_draws.argtypes = [C.c_uint64, i32, C.c_uint64, i64, vp, vp]
         h.cl_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, i32, i32, C.c_double, vp, vp, vp, vp]
@@ -303,6 +304,13 @@ class ClompContext:
         stream.cuda_stream); None restores the context's own stream."""
         _raise(lib().cl_set_stream(self._h, C.c_void_p(stream_handle) if stream_handle else None),
                self._h)
+
+    def debug_scores(self, r_signal_major, path: int) -> np.ndarray:
+        """A^T r for B x m fp32 residuals via path 1 (fp64 SIMT) or 2 (tcgen05)."""
+        r = np.ascontiguousarray(r_signal_major, dtype=np.float32)
+        out = np.zeros((r.shape[0], self.n), np.float64)
+        _raise(lib().cl_debug_scores(self._h, _ptr(r), r.shape[0], int(path), _ptr(out)), self._h)
+        return out
 
     def stats(self) -> dict:
         s = CStats()

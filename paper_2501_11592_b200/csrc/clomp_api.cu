@@ -221,7 +221,13 @@ bool use_tensor_path(const cl_ctx* ctx, const cl_config* c) {
 // hundred ulps of the dot length covers summation-order differences with the
 // reference's sequential FMA (kernels_avx2.cpp:164-236).  3xTF32: see
 // DESIGN.md §4 (measured worst error x safety factor).
-double delta_for(bool tensor) { return tensor ? 4e-5 : 1e-12; }
+double delta_for(bool tensor, int64_t ldm) {
+  if (!tensor) return 1e-12;
+  // 3xTF32: per-product split error ~3*2^-20, plus fp32 accumulation in TMEM
+  // (one rounding per 8-wide MMA K step).  Worst-case style bound, checked
+  // against measured errors by tests/test_gpu_corr.py.
+  return 1e-5 + (double)(ldm / 8) * 1.2e-7;
+}
 
 struct OutPtrs {
   int64_t cap;
@@ -245,7 +251,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     return fail(ctx, CL_ERR_UNSUPPORTED,
                 "clomp: support capacity above 1024 atoms per signal is not "
                 "supported (th < 1 with n > 1024)");
-  const int64_t tile_atoms = tensor ? 128 : kCorrTileAtoms;
+  const int64_t tile_atoms = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
   int st = ensure_workspace(ctx, B, cap, full_scores, tensor, ntile);
   if (st) return st;
@@ -271,7 +277,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.mode = mode;
   p.bc1 = ctx->bc;
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
-  p.delta_rel = delta_for(tensor);
+  p.delta_rel = delta_for(tensor, ctx->ldm);
   p.colnorm_max = ctx->colnorm_max;
 
   const Work& w = ctx->w;
@@ -697,7 +703,7 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   p.ntile = ntile;
   p.mwords = (n + 31) / 32;
   p.th = th;
-  p.delta_rel = delta_for(false);
+  p.delta_rel = delta_for(false, ldm);
   p.colnorm_max = ctx->colnorm_max;
   Work w = ctx->w;
   w.r_hi = w.r_lo = nullptr;
@@ -724,6 +730,66 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   for (int64_t j = 0; j < n; ++j)
     for (int64_t b = 0; b < batch; ++b)
       mask[j * batch + b] = (bits[(size_t)(b * p.mwords + j / 32)] >> (j % 32)) & 1u;
+  return CL_OK;
+}
+
+int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
+                    double* scores) {
+  if (!ctx || !r || !scores || batch <= 0) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  if (path == 2 && !ctx->tc_ok)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "tcgen05 correlation kernel not available");
+  const int64_t m = ctx->m, n = ctx->n, ldm = ctx->ldm;
+  const bool tc = path == 2;
+  const int64_t ntile = tc ? (n + corr_tc_tile_atoms() - 1) / corr_tc_tile_atoms()
+                           : (n + kCorrTileAtoms - 1) / kCorrTileAtoms;
+  int st = ensure_workspace(ctx, batch, 1, true, true, ntile);
+  if (st) return st;
+  SolveParams p{};
+  p.B = batch;
+  p.n = n;
+  p.m = m;
+  p.ldm = ldm;
+  p.cap = 1;
+  p.ntile = ntile;
+  p.mwords = (n + 31) / 32;
+  const Work& w = ctx->w;
+  std::vector<double> r64((size_t)(batch * ldm), 0.0);
+  std::vector<float> hi((size_t)(batch * ldm), 0.f), lo((size_t)(batch * ldm), 0.f);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < m; ++i) {
+      const float x = r[b * m + i];
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u &= 0xFFFFE000u;
+      float h;
+      std::memcpy(&h, &u, 4);
+      r64[(size_t)(b * ldm + i)] = x;
+      hi[(size_t)(b * ldm + i)] = h;
+      lo[(size_t)(b * ldm + i)] = x - h;
+    }
+  std::vector<int32_t> ones((size_t)batch, 1);
+  cudaStream_t s = ctx->stream;
+  CL_CUDA(ctx, cudaMemcpyAsync(w.r64, r64.data(), r64.size() * 8, cudaMemcpyHostToDevice, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(w.r_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(w.r_lo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice, s));
+  CL_CUDA(ctx, cudaMemcpyAsync(w.active, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice, s));
+  if (tc) {
+    float* d = nullptr;
+    CL_CUDA(ctx, cudaMalloc(&d, (size_t)(batch * n) * 4));
+    launch_corr_tc_debug(p, w, d, s);
+    std::vector<float> h((size_t)(batch * n));
+    CL_CUDA(ctx, cudaMemcpyAsync(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
+    cudaFree(d);
+    for (size_t e = 0; e < h.size(); ++e) scores[e] = h[e];
+  } else {
+    launch_corr_f64(p, w, true, s);
+    CL_CUDA(ctx, cudaMemcpyAsync(scores, w.scores, (size_t)(batch * n) * 8,
+                                 cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  CL_CUDA(ctx, cudaGetLastError());
   return CL_OK;
 }
 

@@ -92,7 +92,11 @@ void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
                      cudaStream_t s);
 // tcgen05 3xTF32 correlation with fused top-2 epilogue (th == 1).
 bool corr_tc_available();
+int64_t corr_tc_tile_atoms();
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
+// Same kernel, additionally writing the signed fp32 scores [B][n] (tests).
+void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
+                          cudaStream_t s);
 void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
                        cudaStream_t s);
 

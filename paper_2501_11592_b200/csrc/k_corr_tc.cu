@@ -1,27 +1,374 @@
-// k_corr_tc.cu — K1 on the tcgen05 tensor cores (3xTF32).  Placeholder until
-// the kernel lands; the fp64 SIMT path in k_corr_f64.cu serves meanwhile.
+// k_corr_tc.cu — K1 on the 5th-generation tensor cores: scores = R A^T in
+// 3xTF32 with the argmax selection fused into the TMEM epilogue.
+//
+// Replaces la::matmul(ops.at, r) (clomp.cpp:245) and the max scan of
+// inject_from_scores (clomp.cpp:45-47) on the th == 1 path.
+//
+// Shape: one CTA per 128-signal x 256-atom tile.  UMMA M = signals (TMEM
+// lanes), N = atoms (TMEM columns), K = measurements, both operands K-major in
+// shared memory with the 128-byte swizzle that TMA writes.  Every fp32 operand
+// x is split once into tf32 hi = trunc(x) and lo = x - hi (exact), and the
+// product is accumulated as hi*hi + hi*lo + lo*hi in fp32 in TMEM (3xTF32,
+// ~fp32 accuracy; the dropped lo*lo term is < 2^-20 |a||r|).
+//
+// Roles (128 threads): warp 0 lane 0 issues TMA into a 2-stage ring,
+// warp 1 lane 0 issues tcgen05.mma (single thread per CTA), warp 2 owns the
+// TMEM allocation.  After the last commit all four warps drain TMEM with
+// tcgen05.ld: thread = signal (its TMEM lane), so the per-signal top-2 over the
+// tile's 256 atoms is a register scan with no shuffles.  Only (top1, argmax,
+// top2) per (signal, atom tile) reaches HBM; the selection kernel merges tiles
+// and sends near-ties (gap inside the 3xTF32 error bound) to an fp64 rescan.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
 #include "clomp_internal.cuh"
 
 namespace clb {
-
 namespace {
+
+constexpr int TM = 128;  // signals per tile  (UMMA M, TMEM lanes)
+constexpr int TN = 256;  // atoms per tile    (UMMA N, TMEM columns)
+constexpr int BK = 32;   // fp32 K elements per stage: one 128-byte swizzle row
+constexpr int STAGES = 2;
+constexpr int R_BYTES = TM * BK * 4;  // 16 KB
+constexpr int A_BYTES = TN * BK * 4;  // 32 KB
+constexpr int STAGE_BYTES = 2 * R_BYTES + 2 * A_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t TMEM_COLS = 256;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 bytes apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4)           // D format f32
+                            | (2u << 7)         // A format tf32
+                            | (2u << 10)        // B format tf32
+                            | ((TN >> 3) << 17) // N
+                            | ((TM >> 4) << 24);// M
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(128, 1)
+k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
+          const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+          int64_t n, int64_t B, int kblocks, int64_t ntile, const int32_t* __restrict__ active,
+          double* __restrict__ cand_v1, double* __restrict__ cand_v2,
+          int32_t* __restrict__ cand_i1, float* __restrict__ scores_dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * TM;  // first signal
+  const int64_t n0 = (int64_t)blockIdx.x * TN;  // first atom
+
+  // Whole tile finished?  (uniform per CTA)
+  int mine = 0;
+  {
+    const int64_t b = m0 + threadIdx.x;
+    mine = (b < B) ? active[b] : 0;
+  }
+  if (!__syncthreads_or(mine)) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rhi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rlo)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)));
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* st = smem + s * STAGE_BYTES;
+      mbar_expect_tx(&full[s], STAGE_BYTES);
+      const int k0 = kb * BK;
+      tma_load_2d(st, &tm_rhi, &full[s], k0, (int)m0);
+      tma_load_2d(st + R_BYTES, &tm_rlo, &full[s], k0, (int)m0);
+      tma_load_2d(st + 2 * R_BYTES, &tm_ahi, &full[s], k0, (int)n0);
+      tma_load_2d(st + 2 * R_BYTES + A_BYTES, &tm_alo, &full[s], k0, (int)n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (one thread for the CTA)
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint8_t* st = smem + s * STAGE_BYTES;
+      const uint64_t d_rhi = sw128_desc(smem_u32(st));
+      const uint64_t d_rlo = sw128_desc(smem_u32(st + R_BYTES));
+      const uint64_t d_ahi = sw128_desc(smem_u32(st + 2 * R_BYTES));
+      const uint64_t d_alo = sw128_desc(smem_u32(st + 2 * R_BYTES + A_BYTES));
+#pragma unroll
+      for (int j = 0; j < BK / 8; ++j) {  // 8 tf32 (32 bytes) per MMA K step
+        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+        mma_tf32(tmem, d_rhi + adv, d_alo + adv, (kb | j) != 0);
+        mma_tf32(tmem, d_rlo + adv, d_ahi + adv, 1);
+        mma_tf32(tmem, d_rhi + adv, d_ahi + adv, 1);
+      }
+      mma_commit(&empty[s]);  // stage free once these MMAs retire
+    }
+    mma_commit(accum);        // accumulator complete
+  }
+
+  // ---------------- epilogue: thread = signal, scan its 256 atom columns
+  __syncwarp();
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int64_t b = m0 + warp * 32 + lane;
+  float v1 = -1.f, v2 = -1.f;
+  int i1 = 0x7fffffff;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll 1
+  for (int c = 0; c < TN / 32; ++c) {
+    float v[32];
+    tmem_ld_32(tmem + lane_base + (uint32_t)(c * 32), v);
+    const int64_t a0 = n0 + c * 32;
+    if (scores_dbg && b < B) {
+      for (int q = 0; q < 32; ++q)
+        if (a0 + q < n) scores_dbg[b * n + a0 + q] = v[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const float x = fabsf(v[q]);
+      const bool ok = a0 + q < n;
+      if (ok && x > v1) {
+        v2 = v1;
+        v1 = x;
+        i1 = (int)(a0 + q);
+      } else if (ok && x > v2) {
+        v2 = x;
+      }
+    }
+  }
+  if (b < B) {
+    const int64_t o = b * ntile + blockIdx.x;
+    cand_v1[o] = (double)v1;
+    cand_v2[o] = (double)v2;
+    cand_i1[o] = i1;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// Exact tf32 split: hi = x with the 13 low mantissa bits cleared (what a tf32
+// operand can hold), lo = x - hi (exact in fp32).
 __global__ void k_split_tf32(const float* __restrict__ src, float* __restrict__ hi,
                              float* __restrict__ lo, int64_t count) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const float x = src[i];
-  uint32_t h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  const float hf = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hf));
-  hi[i] = hf;
-  lo[i] = __uint_as_float(l);
+  const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  hi[i] = h;
+  lo[i] = x - h;
 }
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major [rows][ld], box [box_rows][32], 128-byte swizzle.
+bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ld, int box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct MapCache {
+  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t rows[4] = {0, 0, 0, 0};
+  CUtensorMap map[4];
+};
+thread_local MapCache g_maps;
+
+const CUtensorMap* cached_map(int slot, const float* base, int64_t rows, int64_t ld,
+                              int box_rows) {
+  if (g_maps.key[slot] != base || g_maps.rows[slot] != rows) {
+    if (!make_map(&g_maps.map[slot], base, rows, ld, box_rows)) return nullptr;
+    g_maps.key[slot] = base;
+    g_maps.rows[slot] = rows;
+  }
+  return &g_maps.map[slot];
+}
+
 }  // namespace
 
-bool corr_tc_available() { return false; }
+bool corr_tc_available() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return prop.major == 10 && encode_fn() != nullptr;
+}
 
-void launch_corr_tc(const SolveParams&, const Work&, cudaStream_t) {}
+int64_t corr_tc_tile_atoms() { return TN; }
+
+static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_dbg,
+                           cudaStream_t s) {
+  const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
+  const CUtensorMap* rlo = cached_map(1, w.r_lo, p.B, p.ldm, TM);
+  const CUtensorMap* ahi = cached_map(2, w.at_hi, p.n, p.ldm, TN);
+  const CUtensorMap* alo = cached_map(3, w.at_lo, p.n, p.ldm, TN);
+  if (!rhi || !rlo || !ahi || !alo) return false;
+  cudaFuncSetAttribute(k_corr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  dim3 grid((unsigned)((p.n + TN - 1) / TN), (unsigned)((p.B + TM - 1) / TM));
+  k_corr_tc<<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n, p.B,
+                                          (int)(p.ldm / BK), p.ntile, w.active, w.cand_v1,
+                                          w.cand_v2, w.cand_i1, scores_dbg);
+  return true;
+}
+
+void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
+  launch_tc_impl(p, w, nullptr, s);
+}
+
+void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
+                          cudaStream_t s) {
+  launch_tc_impl(p, w, scores, s);
+}
 
 void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
                        cudaStream_t s) {

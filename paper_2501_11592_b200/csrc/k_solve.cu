@@ -46,13 +46,11 @@ __device__ __forceinline__ bool mask_test(const uint32_t* mb, int j) {
   return (mb[j >> 5] >> (j & 31)) & 1u;
 }
 
-// tf32 split of an fp32 value: hi = rna(x), lo = rna(x - hi).
+// Exact tf32 split of an fp32 value: hi = x with the 13 low mantissa bits
+// cleared, lo = x - hi (exact).  Must match k_split_tf32 in k_corr_tc.cu.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
-  lo = __uint_as_float(l);
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
 }
 
 __device__ __forceinline__ void store_residual(const Work& w, int64_t o,

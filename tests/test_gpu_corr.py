@@ -1,0 +1,48 @@
+"""K1 correlation kernels on the GPU: the tcgen05 3xTF32 scores against fp64
+scores, and the measured error against the bound the selection step uses to
+decide when a near-tie must be re-decided in fp64 (clomp_api.cu delta_for)."""
+import numpy as np
+import pytest
+
+import paper_2501_11592_b200 as cl
+
+pytestmark = pytest.mark.gpu
+
+
+def delta_rel(m):
+    ldm = (m + 31) // 32 * 32
+    return 1e-5 + (ldm // 8) * 1.2e-7
+
+
+@pytest.mark.parametrize("m,n,B", [(128, 256, 5), (512, 1024, 300), (1000, 700, 129), (4096, 4096, 64)])
+def test_tc_scores_within_bound(gpu_available, m, n, B):
+    rng = np.random.default_rng(m + n)
+    A = (rng.standard_normal((m, n)) / np.sqrt(m)).astype(np.float32)
+    A /= np.linalg.norm(A.astype(np.float64), axis=0).astype(np.float32)
+    R = rng.standard_normal((B, m)).astype(np.float32)
+    ctx = cl.ClompContext(A)
+    s64 = ctx.debug_scores(R, 1)                 # |A^T r| fp64
+    stc = np.abs(ctx.debug_scores(R, 2))         # 3xTF32 on tcgen05
+    exact = np.abs(R.astype(np.float64) @ A.astype(np.float64))
+    assert np.max(np.abs(s64 - exact)) <= 1e-12 * np.max(exact)
+    colmax = np.max(np.linalg.norm(A.astype(np.float64), axis=0))
+    rn = np.linalg.norm(R.astype(np.float64), axis=1, keepdims=True)
+    err = np.abs(stc - exact) / (colmax * rn)
+    worst = float(err.max())
+    print(f"m={m} n={n} B={B}: max 3xTF32 error {worst:.3e} of ||a||*||r||, bound {delta_rel(m):.3e}")
+    assert worst <= delta_rel(m) / 4, "3xTF32 error too close to the rescan bound"
+
+
+def test_tc_argmax_matches_fp64(gpu_available):
+    rng = np.random.default_rng(5)
+    m, n, B = 512, 1024, 512
+    A = (rng.standard_normal((m, n)) / np.sqrt(m)).astype(np.float32)
+    R = rng.standard_normal((B, m)).astype(np.float32)
+    ctx = cl.ClompContext(A)
+    s64 = ctx.debug_scores(R, 1)
+    stc = np.abs(ctx.debug_scores(R, 2))
+    top = np.sort(s64, axis=1)
+    gap = (top[:, -1] - top[:, -2]) / np.linalg.norm(R, axis=1)
+    clear = gap > 2 * delta_rel(m)
+    assert clear.mean() > 0.9
+    assert np.array_equal(np.argmax(stc, 1)[clear], np.argmax(s64, 1)[clear])
