@@ -166,6 +166,11 @@ int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 /* Tuning / test knobs: 0 = auto, 1 = force fp64 SIMT correlation,
  * 2 = force the tcgen05 3xTF32 correlation (th == 1 only). */
 int cl_set_corr_path(cl_ctx* ctx, int path);
+/* Dictionary Gram cache G = A^T A (fp64, n x n) used to extend each signal's
+ * support Gram matrix by a gather instead of re-streaming atoms:
+ * 1 = build, 0 = drop, -1 = auto (built by cl_create when n*n*8 <= min(8 GiB,
+ * free/4)). */
+int cl_set_gram_cache(cl_ctx* ctx, int mode);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);
 /* Run this context's work on a caller-owned cudaStream_t (NULL restores the

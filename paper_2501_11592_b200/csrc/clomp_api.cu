@@ -42,6 +42,21 @@ struct Carver {
   }
 };
 
+constexpr int kChunkIters = 8;
+
+struct GraphKey {
+  SolveParams p{};
+  Work w{};  // every device pointer a captured kernel reads
+  const void* wbuf = nullptr;
+  bool tensor = false, full = false;
+  cudaStream_t stream = nullptr;
+  bool operator==(const GraphKey& o) const {
+    return std::memcmp(&p, &o.p, sizeof(p)) == 0 && std::memcmp(&w, &o.w, sizeof(w)) == 0 &&
+           wbuf == o.wbuf && tensor == o.tensor &&
+           full == o.full && stream == o.stream;
+  }
+};
+
 }  // namespace
 
 struct cl_ctx {
@@ -52,6 +67,8 @@ struct cl_ctx {
   float* at32 = nullptr;
   float* at_hi = nullptr;
   float* at_lo = nullptr;
+  double* gfull = nullptr;  // A^T A fp64 [n][n], built once (k_gram.cu)
+  double* at64 = nullptr;   // fp64 copy of the atom-major dictionary
   double colnorm_max = 0.0;
   std::string err;
   // batch workspace
@@ -65,6 +82,10 @@ struct cl_ctx {
   void* stage = nullptr;
   size_t stage_bytes = 0;
   int32_t* h_counters = nullptr;  // pinned
+  int32_t* h_chunk = nullptr;     // pinned, 2 x kNumCounters (graph chunks)
+  cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
+  GraphKey gkey;
+  std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool profiling = false;
   cl_stats stats{};
@@ -143,6 +164,12 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.cand_v2 = cv.take<double>(B * ntile);
     w.cand_i1 = cv.take<int32_t>(B * ntile);
     w.scores = need_scores ? cv.take<double>(B * ctx->n) : nullptr;
+    const int64_t nchunk = (ctx->n + 256 + 63) / 64;  // tiles cover <= n + 256 atoms
+    w.rs_top = cv.take<double>(B);
+    w.rs_delta = cv.take<double>(B);
+    w.rs_done = cv.take<int32_t>(B);
+    w.rs_cmax = cv.take<double>(B * nchunk);
+    w.rs_ids = cv.take<int32_t>(B * nchunk * 5);
     w.sup = cv.take<int32_t>(B * cap);
     w.cnt = cv.take<int32_t>(B);
     w.gcnt = cv.take<int32_t>(B);
@@ -187,6 +214,8 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
   w.at32 = ctx->at32;
   w.at_hi = ctx->at_hi;
   w.at_lo = ctx->at_lo;
+  w.gfull = ctx->gfull;
+  w.at64 = ctx->at64;
   ctx->w = w;
   return CL_OK;
 }
@@ -229,6 +258,12 @@ double delta_for(bool tensor, int64_t ldm) {
   return 1e-5 + (double)(ldm / 8) * 1.2e-7;
 }
 
+void enqueue_count(const SolveParams&, const cl_config* c, int mode, int64_t cap,
+                   int64_t* per_iter) {
+  (void)c;
+  *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0);
+}
+
 struct OutPtrs {
   int64_t cap;
   int32_t* sup;
@@ -265,6 +300,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.ldm = ctx->ldm;
   p.cap = cap;
   p.ntile = ntile;
+  p.tile_atoms = tile_atoms;
   p.mwords = (ctx->n + 31) / 32;
   p.th = c->th;
   p.eps = c->eps;
@@ -284,47 +320,68 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   cudaStream_t s = ctx->stream;
   cl_stats stats{};
   stats.corr_path = tensor ? 1 : 0;
-  int64_t launches = 0;
-  cudaEvent_t ev[5] = {};
-  if (ctx->profiling)
-    for (auto& e : ev) cudaEventCreate(&e);
+  const int rescan_grid = 2 * ctx->sms;
+
+  // One outer iteration (clomp.cpp:235-274): counters reset, K1, K1c, fp64
+  // rescans, learning + residual + stopping rules.  th == 1 adds one atom per
+  // iteration, so the learning kernel's support bucket follows `outer`
+  // (signals grown past it by ties are finished by the block kernel).
+  auto enqueue_iteration = [&](int outer, int64_t* launches) {
+    cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
+    if (tensor)
+      launch_corr_tc(p, w, s);
+    else
+      launch_corr_f64(p, w, full_scores, s);
+    launch_select(p, w, full_scores, s);
+    launch_rescan(p, w, rescan_grid, s);
+    const int bound = c->th >= 1.0 ? outer : (int)cap;
+    launch_learn(p, w, outer, bound, s);
+    *launches += 3 + (cap > 8 ? 3 : 2);
+    if (mode == CL_MODE_JOINT) {
+      launch_joint_control(p, w, outer, false, s);
+      launch_joint_snapshot(p, w, s);
+      *launches += 2;
+    }
+  };
 
   CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
-  if (ctx->profiling) cudaEventRecord(ev[0], s);
+  std::memset(ctx->h_counters, 0, kNumCounters * sizeof(int32_t));
+  int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
   ++launches;
   if (mode == CL_MODE_JOINT) {
     launch_joint_control(p, w, 0, true, s);
     ++launches;
   }
-  const int rescan_grid = (int)std::min<int64_t>(B, ctx->sms);
-  int outer = 1;
-  for (; outer <= p.max_outer; ++outer) {
-    CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s));
-    if (ctx->profiling) cudaEventRecord(ev[1], s);
-    if (tensor)
-      launch_corr_tc(p, w, s);
-    else
-      launch_corr_f64(p, w, full_scores, s);
-    if (ctx->profiling) cudaEventRecord(ev[4], s);
-    launch_select(p, w, full_scores, s);
-    launch_rescan(p, w, rescan_grid, s);
-    launches += 3;
-    if (ctx->profiling) cudaEventRecord(ev[2], s);
-    launch_learn(p, w, outer, (int)cap, s);
-    launches += cap > kWarpCap ? 2 : 1;
-    if (mode == CL_MODE_JOINT) {
-      launch_joint_control(p, w, outer, false, s);
-      launch_joint_snapshot(p, w, s);
-      launches += 2;
-    }
-    if (ctx->profiling) cudaEventRecord(ev[3], s);
-    CL_CUDA(ctx, cudaGetLastError());
-    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters,
-                                 kNumCounters * sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost, s));
-    CL_CUDA(ctx, cudaStreamSynchronize(s));
-    if (ctx->profiling) {
+  int outer_done = 0;
+  if (ctx->profiling) {
+    // Per-phase CUDA-event timing: one iteration at a time, synchronised.
+    cudaEvent_t ev[5];
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[0], s);
+    for (int outer = 1; outer <= p.max_outer; ++outer) {
+      cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
+      cudaEventRecord(ev[1], s);
+      if (tensor)
+        launch_corr_tc(p, w, s);
+      else
+        launch_corr_f64(p, w, full_scores, s);
+      cudaEventRecord(ev[4], s);
+      launch_select(p, w, full_scores, s);
+      launch_rescan(p, w, rescan_grid, s);
+      cudaEventRecord(ev[2], s);
+      launch_learn(p, w, outer, c->th >= 1.0 ? outer : (int)cap, s);
+      launches += 3 + (cap > 8 ? 3 : 2);
+      if (mode == CL_MODE_JOINT) {
+        launch_joint_control(p, w, outer, false, s);
+        launch_joint_snapshot(p, w, s);
+        launches += 2;
+      }
+      cudaEventRecord(ev[3], s);
+      CL_CUDA(ctx, cudaGetLastError());
+      CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, s));
+      CL_CUDA(ctx, cudaStreamSynchronize(s));
       float a = 0.f, b2 = 0.f, c2 = 0.f;
       cudaEventElapsedTime(&a, ev[1], ev[4]);
       cudaEventElapsedTime(&c2, ev[4], ev[2]);
@@ -332,27 +389,81 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       stats.corr_ms += a;
       stats.select_ms += c2;
       stats.learn_ms += b2;
+      outer_done = outer;
+      if (ctx->h_counters[kActiveCount] == 0) break;
     }
-    if (ctx->h_counters[kActiveCount] == 0) break;
-  }
-  launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
-                  out.conv, out.status, s);
-  ++launches;
-  CL_CUDA(ctx, cudaGetLastError());
-  CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters,
-                               kNumCounters * sizeof(int32_t),
-                               cudaMemcpyDeviceToHost, s));
-  if (ctx->profiling) cudaEventRecord(ev[3], s);
-  CL_CUDA(ctx, cudaStreamSynchronize(s));
-  if (ctx->profiling) {
+    launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
+                    out.conv, out.status, s);
+    ++launches;
+    cudaEventRecord(ev[3], s);
+    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
     float t = 0.f;
     cudaEventElapsedTime(&t, ev[0], ev[3]);
     stats.total_ms = t;
     for (auto& e : ev) cudaEventDestroy(e);
+  } else {
+    // Graph path: the iterations are captured in chunks of kChunkIters into
+    // CUDA graphs (cached per launch configuration) and replayed back to back.
+    // After each chunk the active-signal count is copied to pinned memory; the
+    // host checks it one chunk behind, so the GPU never waits for the host.
+    GraphKey key{};
+    key.p = p;
+    key.w = w;
+    key.wbuf = ctx->wbuf;
+    key.tensor = tensor;
+    key.full = full_scores;
+    key.stream = s;
+    if (!(key == ctx->gkey)) {
+      for (auto& g : ctx->graphs)
+        if (g) cudaGraphExecDestroy(g);
+      ctx->graphs.assign(0, nullptr);
+      ctx->gkey = key;
+    }
+    const int nchunks = (p.max_outer + kChunkIters - 1) / kChunkIters;
+    if ((int)ctx->graphs.size() < nchunks) ctx->graphs.resize((size_t)nchunks, nullptr);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      if (!ctx->graphs[(size_t)ch]) {
+        const int o0 = ch * kChunkIters + 1;
+        const int o1 = std::min(p.max_outer, o0 + kChunkIters - 1);
+        int64_t dummy = 0;
+        cudaGraph_t g = nullptr;
+        CL_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        for (int o = o0; o <= o1; ++o) enqueue_iteration(o, &dummy);
+        cudaMemcpyAsync(ctx->h_chunk + (ch & 1) * kNumCounters, w.counters,
+                        kNumCounters * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        CL_CUDA(ctx, cudaStreamEndCapture(s, &g));
+        cudaGraphExec_t ge = nullptr;
+        CL_CUDA(ctx, cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        ctx->graphs[(size_t)ch] = ge;
+      }
+    }
+    int64_t per_iter = 0;
+    enqueue_count(p, c, mode, cap, &per_iter);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      CL_CUDA(ctx, cudaGraphLaunch(ctx->graphs[(size_t)ch], s));
+      cudaEventRecord(ctx->chunk_ev[ch & 1], s);
+      const int o1 = std::min(p.max_outer, (ch + 1) * kChunkIters);
+      launches += per_iter * (o1 - ch * kChunkIters);
+      outer_done = o1;
+      if (ch >= 1) {
+        CL_CUDA(ctx, cudaEventSynchronize(ctx->chunk_ev[(ch - 1) & 1]));
+        if (ctx->h_chunk[((ch - 1) & 1) * kNumCounters + kActiveCount] == 0) break;
+      }
+    }
+    launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
+                    out.conv, out.status, s);
+    ++launches;
+    CL_CUDA(ctx, cudaGetLastError());
+    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
   }
   stats.kernel_launches = launches;
   stats.rescans = ctx->h_counters[kRescanTotal];
-  stats.outer_iterations = std::min(outer, p.max_outer);
+  stats.outer_iterations = outer_done;
   ctx->stats = stats;
   return CL_OK;
 }
@@ -436,7 +547,7 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
   ctx->device = device;
   ctx->m = m;
   ctx->n = n;
-  ctx->ldm = (m + 31) / 32 * 32;
+  ctx->ldm = (m + 127) / 128 * 128;  // float4 x 32 lanes per row chunk
   ctx->sms = prop.multiProcessorCount;
   // Atom-major fp32 copy (the reference's LossOps transpose, clomp.cpp:57-66,
   // done once per dictionary instead of once per call).
@@ -459,10 +570,23 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
     ctx->stream = ctx->own_stream;
   if (!ctx->stream || cudaMalloc(&ctx->at32, bytes) != cudaSuccess ||
       cudaMemcpy(ctx->at32, at.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_counters, kNumCounters * sizeof(int32_t)) != cudaSuccess) {
+      cudaMallocHost(&ctx->h_counters, kNumCounters * sizeof(int32_t)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_chunk, 2 * kNumCounters * sizeof(int32_t)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     cl_destroy(ctx);
     return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
+  }
+  {
+    std::vector<double> at64(at.begin(), at.end());
+    if (cudaMalloc(&ctx->at64, at64.size() * sizeof(double)) != cudaSuccess ||
+        cudaMemcpy(ctx->at64, at64.data(), at64.size() * sizeof(double),
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      cl_destroy(ctx);
+      return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
+    }
   }
   if (ctx->tc_ok) {
     if (cudaMalloc(&ctx->at_hi, bytes) != cudaSuccess ||
@@ -478,8 +602,41 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
       return bail(CL_ERR_CUDA, "cl_create: tf32 split failed");
     }
   }
+  cl_set_gram_cache(ctx, -1);
   if (status) *status = CL_OK;
   return ctx;
+}
+
+int cl_set_gram_cache(cl_ctx* ctx, int mode) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  const size_t bytes = (size_t)ctx->n * (size_t)ctx->n * sizeof(double);
+  bool want = mode > 0;
+  if (mode < 0) {  // auto: when it fits comfortably
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    want = bytes <= (size_t)8 << 30 && bytes <= free_b / 4;
+  }
+  if (!want) {
+    if (ctx->gfull) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->gfull);
+  cudaFree(ctx->at64);
+      ctx->gfull = nullptr;
+    }
+    ctx->w.gfull = nullptr;
+    return CL_OK;
+  }
+  if (ctx->gfull) return CL_OK;
+  if (cudaMalloc(&ctx->gfull, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->gfull = nullptr;
+    return mode > 0 ? fail(ctx, CL_ERR_CUDA, "cl_set_gram_cache: allocation failed") : CL_OK;
+  }
+  launch_gram_full(ctx->at32, ctx->n, ctx->ldm, ctx->gfull, ctx->stream);
+  CL_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->w.gfull = ctx->gfull;
+  return CL_OK;
 }
 
 void cl_destroy(cl_ctx* ctx) {
@@ -489,10 +646,17 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->at32);
   cudaFree(ctx->at_hi);
   cudaFree(ctx->at_lo);
+  cudaFree(ctx->gfull);
+  cudaFree(ctx->at64);
   cudaFree(ctx->wbuf);
   cudaFree(ctx->bc);
   cudaFree(ctx->stage);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  if (ctx->h_chunk) cudaFreeHost(ctx->h_chunk);
+  for (auto& e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& g : ctx->graphs)
+    if (g) cudaGraphExecDestroy(g);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -701,6 +865,7 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   p.ldm = ldm;
   p.cap = n;
   p.ntile = ntile;
+  p.tile_atoms = kCorrTileAtoms;
   p.mwords = (n + 31) / 32;
   p.th = th;
   p.delta_rel = delta_for(false, ldm);
@@ -722,7 +887,7 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   launch_inject_finish(p, w, s);
   launch_corr_f64(p, w, full, s);
   launch_select(p, w, full, s);
-  launch_rescan(p, w, (int)std::min<int64_t>(batch, ctx->sms), s);
+  launch_rescan(p, w, 2 * ctx->sms, s);
   CL_CUDA(ctx, cudaGetLastError());
   CL_CUDA(ctx, cudaMemcpyAsync(bits.data(), w.maskbits, bits.size() * 4,
                                cudaMemcpyDeviceToHost, s));

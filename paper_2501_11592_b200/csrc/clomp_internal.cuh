@@ -22,6 +22,7 @@ constexpr int kWarpCap = 32;          // register-resident learning kernel limit
 
 struct SolveParams {
   int64_t B, n, m, ldm, cap, ntile;
+  int64_t tile_atoms;       // atoms per correlation tile (candidate granularity)
   int64_t mwords;           // 32-bit words per signal in the mask bitmap
   double th, eps, lr, stall_tol;
   int32_t stall_patience, opt, inner, max_outer, mode;
@@ -36,6 +37,9 @@ struct Work {
   const float* at32 = nullptr;   // [n][ldm]
   const float* at_hi = nullptr;  // [n][ldm] tf32 split (tensor path)
   const float* at_lo = nullptr;
+  const double* gfull = nullptr; // [n][n] fp64 A^T A (optional, per context)
+  const double* at64 = nullptr;  // [n][ldm] fp64 copy of at32 (exact): the
+                                 // fp64 gathers read it, no conversions
   float* y32 = nullptr;          // [B][ldm]
   double* y64 = nullptr;
   double* r64 = nullptr;
@@ -46,6 +50,12 @@ struct Work {
   double* cand_v2 = nullptr;
   int32_t* cand_i1 = nullptr;
   double* scores = nullptr;      // [B][n] |A^T r| (th < 1 path)
+  // fp64 rescans of near-tied selections, indexed by rescan-list slot
+  double* rs_top = nullptr;      // [B] correlation-kernel top1
+  double* rs_delta = nullptr;    // [B] error bound used for that signal
+  int32_t* rs_done = nullptr;    // [B] chunks finished
+  double* rs_cmax = nullptr;     // [B][nchunk] exact max per 64-atom chunk
+  int32_t* rs_ids = nullptr;     // [B][nchunk][1 + 4] atoms attaining it
   // per-signal state
   int32_t* sup = nullptr;        // [B][cap] insertion order
   int32_t* cnt = nullptr;        // [B]
@@ -77,6 +87,7 @@ enum Counter {
   kActiveCount = 1,   // signals still iterating after this outer iteration
   kMaxCount = 2,      // max support size over the batch
   kRescanTotal = 3,   // rescans over the whole solve
+  kBigCount = 4,      // signals queued for the block learning kernel
   kNumCounters = 8
 };
 
@@ -99,6 +110,24 @@ void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
                           cudaStream_t s);
 void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
                        cudaStream_t s);
+// ---- launchers (k_gram.cu) ----
+void launch_gram_full(const float* at, int64_t n, int64_t ldm, double* g,
+                      cudaStream_t s);
+
+// fp32 -> fp64 with integer ops (ALU pipe) instead of F2F.F64.F32: exact for
+// zeros, normals, infinities and NaNs; fp32 subnormals flush to signed zero.
+__device__ __forceinline__ double f2d(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t sign = u & 0x80000000u;
+  const uint32_t e = (u >> 23) & 0xffu;
+  const uint32_t man_hi = (u >> 3) & 0x000FFFFFu;
+  uint32_t hi = sign | ((e + 896u) << 20) | man_hi;
+  uint32_t lo = u << 29;
+  hi = (e == 0u) ? sign : hi;
+  lo = (e == 0u) ? 0u : lo;
+  hi = (e == 0xffu) ? (sign | 0x7FF00000u | man_hi) : hi;
+  return __hiloint2double((int)hi, (int)lo);
+}
 
 // ---- launchers (k_solve.cu) ----
 void launch_init(const SolveParams& p, const Work& w, const float* y_in,

@@ -18,6 +18,7 @@
 
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "clomp_internal.cuh"
 
@@ -133,6 +134,9 @@ __global__ void k_select_top(SolveParams p, Work w) {
   if (v1 - v2 <= delta) {
     const int slot = atomicAdd(&w.counters[kRescanCount], 1);
     w.rescan_list[slot] = (int32_t)b;
+    w.rs_top[slot] = v1;
+    w.rs_delta[slot] = delta;
+    w.rs_done[slot] = 0;
     return;
   }
   uint32_t* mb = w.maskbits + b * p.mwords;
@@ -202,80 +206,142 @@ __global__ void k_select_thresh(SolveParams p, Work w) {
   warp_threshold_append(p, w, b, cut, [&](int64_t j) { return sc[j]; }, lane);
 }
 
-// fp64 score of atom j against the fp64 residual of signal b (one warp).
-__device__ __forceinline__ double warp_score64(const SolveParams& p,
-                                               const Work& w, int64_t b,
-                                               int64_t j, int lane) {
-  const float* a = w.at32 + j * p.ldm;
-  const double* r = w.r64 + b * p.ldm;
-  double acc = 0.0;
-  for (int64_t i = lane; i < p.ldm; i += 32) acc = fma((double)a[i], r[i], acc);
-  return fabs(warp_sum(acc));
-}
+// Re-decide a near-tied th == 1 selection from fp64 scores.  Only atom tiles
+// whose correlation-kernel top1 lies within 2*delta of the best tile's top1
+// can hold the exact maximum or a tie with it, so only those are rescored:
+// exact fp64 dot products of the fp32 atoms with the fp64 residual.  Work
+// items are (queued signal, 64-atom chunk) spread over the whole grid; each
+// chunk records its exact max and the atoms attaining it, and the block that
+// completes a signal's last chunk applies inject_from_scores (clomp.cpp:45-51)
+// with every tie.
+constexpr int kChunk = 64;
+constexpr int kChunkTies = 4;
 
-// Re-decide a near-tied selection from fp64 scores over all atoms: the exact
-// inject_from_scores rule, including every tie.  One block per queued signal.
 __global__ void __launch_bounds__(256) k_rescan(SolveParams p, Work w) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  __shared__ double red[32];
-  __shared__ double sc[32];
-  __shared__ int s_t, s_added, s_over;
+  __shared__ double wmax[8];
+  __shared__ int32_t wids[8][kChunkTies];
+  __shared__ int wnid[8];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int count = w.counters[kRescanCount];
-  for (int li = blockIdx.x; li < count; li += gridDim.x) {
+  const int nchunk = (int)((p.ntile * p.tile_atoms + kChunk - 1) / kChunk);
+  const int64_t items = (int64_t)count * nchunk;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int li = (int)(it / nchunk), ch = (int)(it % nchunk);
     const int64_t b = w.rescan_list[li];
-    double cmax = 0.0;
-    for (int64_t j = warp; j < p.n; j += nw) {
-      const double v = warp_score64(p, w, b, j, lane);
-      cmax = fmax(cmax, v);
-    }
-    if (lane == 0) red[warp] = cmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
-      red[0] = m;
-      s_t = w.cnt[b];
-      s_added = 0;
-      s_over = 0;
-    }
-    __syncthreads();
-    cmax = red[0];
-    if (cmax > 0.0) {
-      const double cut = p.th * cmax;
-      uint32_t* mb = w.maskbits + b * p.mwords;
-      for (int64_t j0 = 0; j0 < p.n; j0 += nw) {
-        const int64_t j = j0 + warp;
-        double v = -1.0;
-        if (j < p.n) v = warp_score64(p, w, b, j, lane);
-        if (lane == 0) sc[warp] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          for (int q = 0; q < nw && j0 + q < p.n; ++q) {
-            const int jj = (int)(j0 + q);
-            if (sc[q] >= cut && !mask_test(mb, jj)) {
-              if (s_t < p.cap) {
-                w.sup[b * p.cap + s_t] = jj;
-                mb[jj >> 5] |= 1u << (jj & 31);
-                ++s_t;
-                ++s_added;
-              } else {
-                s_over = 1;
-              }
-            }
+    const int64_t tile = (int64_t)ch * kChunk / p.tile_atoms;
+    const double cut_tile = w.rs_top[li] - 2.0 * w.rs_delta[li];
+    double* cm = w.rs_cmax + (int64_t)li * nchunk;
+    int32_t* cids = w.rs_ids + ((int64_t)li * nchunk + ch) * (kChunkTies + 1);
+    if (w.cand_v1[b * p.ntile + tile] >= cut_tile) {
+      // 8 warps x 8 atoms, 8 independent dot products per warp.
+      const int64_t j0 = (int64_t)ch * kChunk + warp * 8;
+      const double* r = w.r64 + b * p.ldm;
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 2
+      for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
+        const double2 r01 = *reinterpret_cast<const double2*>(r + i);
+        const double2 r23 = *reinterpret_cast<const double2*>(r + i + 2);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (j0 + u < p.n) {
+            const double* a = w.at64 + (j0 + u) * p.ldm + i;
+            const double2 a01 = *reinterpret_cast<const double2*>(a);
+            const double2 a23 = *reinterpret_cast<const double2*>(a + 2);
+            acc[u] = fma(a01.x, r01.x, acc[u]);
+            acc[u] = fma(a01.y, r01.y, acc[u]);
+            acc[u] = fma(a23.x, r23.x, acc[u]);
+            acc[u] = fma(a23.y, r23.y, acc[u]);
           }
         }
-        __syncthreads();
       }
+      double best = -1.0;
+      int nid = 0;
+      int32_t ids[kChunkTies];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double v = fabs(warp_sum(acc[u]));
+        if (j0 + u < p.n) {
+          if (v > best) {
+            best = v;
+            nid = 0;
+          }
+          if (v == best && nid < kChunkTies) ids[nid++] = (int32_t)(j0 + u);
+          else if (v == best) nid = kChunkTies + 1;  // overflow marker
+        }
+      }
+      if (lane == 0) {
+        wmax[warp] = best;
+        wnid[warp] = nid;
+        for (int q = 0; q < kChunkTies && q < nid; ++q) wids[warp][q] = ids[q];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double m = -1.0;
+        for (int q = 0; q < 8; ++q) m = fmax(m, wmax[q]);
+        int n = 0;
+        for (int q = 0; q < 8; ++q)
+          if (wmax[q] == m) {
+            if (wnid[q] > kChunkTies) n = kChunkTies + 1;
+            for (int e = 0; e < wnid[q] && e < kChunkTies; ++e) {
+              if (n < kChunkTies) cids[1 + n] = wids[q][e];
+              ++n;
+            }
+          }
+        cm[ch] = m;
+        cids[0] = n;
+      }
+    } else if (tid == 0) {
+      cm[ch] = -1.0;  // cannot hold the maximum
+      cids[0] = 0;
     }
-    if (threadIdx.x == 0) {
-      w.cnt[b] = s_t;
-      w.changed[b] = s_added > 0;
-      if (s_over) {
+    // The block completing the last chunk of this signal finalises it.
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(&w.rs_done[li], 1) == nchunk - 1;
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {
+      __threadfence();
+      double m = 0.0;
+      for (int q = 0; q < nchunk; ++q) m = fmax(m, cm[q]);
+      int32_t picks[kChunkTies * 4];
+      int np = 0, over = 0;
+      uint32_t* mb = w.maskbits + b * p.mwords;
+      if (m > 0.0) {
+        for (int q = 0; q < nchunk; ++q) {
+          if (cm[q] != m) continue;  // th == 1: only exact ties with the max
+          const int32_t* ci = w.rs_ids + ((int64_t)li * nchunk + q) * (kChunkTies + 1);
+          if (ci[0] > kChunkTies) over = 1;
+          for (int e = 0; e < ci[0] && e < kChunkTies; ++e) {
+            const int32_t j = ci[1 + e];
+            if (mask_test(mb, j)) continue;
+            if (np < kChunkTies * 4) picks[np++] = j;
+            else over = 1;
+          }
+        }
+      }
+      // picks arrive in ascending chunk / atom order already
+      int t = w.cnt[b];
+      for (int a = 0; a < np; ++a) {
+        if (t < p.cap) {
+          const int32_t j = picks[a];
+          w.sup[b * p.cap + t] = j;
+          mb[j >> 5] |= 1u << (j & 31);
+          ++t;
+        } else {
+          over = 1;
+        }
+      }
+      w.cnt[b] = t;
+      w.changed[b] = np > 0;
+      if (over) {
         w.status[b] = kStatusCapacity;
         w.active[b] = 0;
       }
-      if (s_added) atomicMax(&w.counters[kMaxCount], s_t);
+      if (np) atomicMax(&w.counters[kMaxCount], t);
       atomicAdd(&w.counters[kRescanTotal], 1);
     }
     __syncthreads();
@@ -341,79 +407,281 @@ __device__ __forceinline__ void opt_step(double& c, double g, double& m1,
 // ------------------------------------------ learning, warp per signal
 // All epochs of one outer iteration with G's row `lane` in registers (zero
 // padded to T columns, which is exact) and c broadcast through shared memory.
-template <int T, int OPT>
-__device__ __forceinline__ void epochs_warp(const double (&g)[kWarpCap],
+// All epochs of one outer iteration, one warp per signal, lane i owning row i
+// of the support Gram system (rows beyond t are zero, which is exact), c
+// broadcast through a double-buffered shared-memory vector (one __syncwarp per
+// epoch).
+//   plain GD (OPT 0): the step is affine, c <- (I - 2 lr G) c + 2 lr b, so
+//     `g` holds the row of T = I - 2 lr G and `bi` holds 2 lr b_i: an epoch is
+//     T FMAs into accumulators seeded with 2 lr b_i, nothing else.  Equal to
+//     s -= lr * 2 A^T (A s - y) (clomp.cpp:87-90, 178-181) in exact arithmetic.
+//   momentum / Adam: g = 2 (G c - b), then gradient_step's update
+//     (clomp.cpp:182-206).
+template <int T, int TB, int OPT>
+__device__ __forceinline__ void epochs_warp(const double (&g)[TB],
                                             double& c, double bi, double& m1,
                                             double& m2, double* cs,
                                             const SolveParams& p, int step0,
                                             int lane, int t) {
+  constexpr int NA = T >= 16 ? 8 : 4;
   for (int e = 0; e < p.inner; ++e) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* cr = cs + (e & 1) * kWarpCap;
+    double a[NA];
+    a[0] = OPT == 0 ? bi : 0.0;
 #pragma unroll
-    for (int j = 0; j < T; j += 4) {
-      const double2 c01 = *reinterpret_cast<const double2*>(cs + j);
-      const double2 c23 = *reinterpret_cast<const double2*>(cs + j + 2);
-      a0 = fma(g[j + 0], c01.x, a0);
-      a1 = fma(g[j + 1], c01.y, a1);
-      a2 = fma(g[j + 2], c23.x, a2);
-      a3 = fma(g[j + 3], c23.y, a3);
+    for (int q = 1; q < NA; ++q) a[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < T; j += NA) {
+#pragma unroll
+      for (int q = 0; q < NA; q += 2) {
+        const double2 cv = *reinterpret_cast<const double2*>(cr + j + q);
+        a[q] = fma(g[j + q], cv.x, a[q]);
+        a[q + 1] = fma(g[j + q + 1], cv.y, a[q + 1]);
+      }
     }
-    const double grad = 2.0 * (((a0 + a1) + (a2 + a3)) - bi);
-    double bc1 = 1.0, bc2 = 1.0;
-    if (OPT == 2) {
-      bc1 = p.bc1[step0 + e];
-      bc2 = p.bc2[step0 + e];
+    double acc;
+    if constexpr (NA == 8)
+      acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    else
+      acc = (a[0] + a[1]) + (a[2] + a[3]);
+    if constexpr (OPT == 0) {
+      c = acc;
+    } else {
+      const double grad = 2.0 * (acc - bi);
+      double bc1 = 1.0, bc2 = 1.0;
+      if (OPT == 2) {
+        bc1 = p.bc1[step0 + e];
+        bc2 = p.bc2[step0 + e];
+      }
+      if (lane < t) opt_step<OPT>(c, grad, m1, m2, p.lr, bc1, bc2);
     }
-    if (lane < t) opt_step<OPT>(c, grad, m1, m2, p.lr, bc1, bc2);
-    __syncwarp();
-    cs[lane] = c;
+    cs[((e + 1) & 1) * kWarpCap + lane] = c;
     __syncwarp();
   }
 }
 
-template <int OPT>
-__device__ __forceinline__ void epochs_dispatch(const double (&g)[kWarpCap],
-                                                double& c, double bi,
-                                                double& m1, double& m2,
-                                                double* cs,
-                                                const SolveParams& p,
-                                                int step0, int lane, int t) {
-  if (t <= 8)
-    epochs_warp<8, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
-  else if (t <= 16)
-    epochs_warp<16, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
-  else if (t <= 24)
-    epochs_warp<24, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
-  else
-    epochs_warp<32, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
-}
-
-// Gram row/column and b entry for every atom added since the last call
-// (one warp).  G[k][i] = a_k . a_i and b_k = a_k . y in fp64.
-__device__ void warp_extend_gram(const SolveParams& p, const Work& w,
-                                 int64_t b, int t0, int t, int lane) {
-  const int64_t cap = p.cap;
-  double* G = w.gram + b * cap * cap;
-  const int32_t* sup = w.sup + b * cap;
-  const double* y = w.y64 + b * p.ldm;
-  for (int k = t0; k < t; ++k) {
-    const float* ak = w.at32 + (int64_t)sup[k] * p.ldm;
-    for (int i = 0; i <= k; ++i) {
-      const float* ai = w.at32 + (int64_t)sup[i] * p.ldm;
-      double acc = 0.0;
-      for (int64_t q = lane; q < p.ldm; q += 32)
-        acc = fma((double)ak[q], (double)ai[q], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        G[(int64_t)k * cap + i] = acc;
-        G[(int64_t)i * cap + k] = acc;
+// c <- M c + d, `steps` times: M's row `lane` in registers (T columns live),
+// c broadcast through the double-buffered cs (parity continues from *ep).
+template <int T, int TB>
+__device__ __forceinline__ void affine_steps(const double (&m)[TB], double& c, double d,
+                                             double* cs, int steps, int* ep) {
+  constexpr int NA = T >= 16 ? 8 : 4;
+  for (int e = 0; e < steps; ++e, ++*ep) {
+    const double* cr = cs + (*ep & 1) * kWarpCap;
+    double a[NA];
+    a[0] = d;
+#pragma unroll
+    for (int q = 1; q < NA; ++q) a[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < T; j += NA) {
+#pragma unroll
+      for (int q = 0; q < NA; q += 2) {
+        const double2 cv = *reinterpret_cast<const double2*>(cr + j + q);
+        a[q] = fma(m[j + q], cv.x, a[q]);
+        a[q + 1] = fma(m[j + q + 1], cv.y, a[q + 1]);
       }
     }
-    double acc = 0.0;
-    for (int64_t q = lane; q < p.ldm; q += 32) acc = fma((double)ak[q], y[q], acc);
-    acc = warp_sum(acc);
+    if constexpr (NA == 8)
+      c = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    else
+      c = (a[0] + a[1]) + (a[2] + a[3]);
+    cs[((*ep + 1) & 1) * kWarpCap + threadIdx.x % 32] = c;
+    __syncwarp();
+  }
+}
+
+// res <- row `lane` of P*P, P symmetric and stored as T x T rows in smem.
+// Row k of P is read by broadcast (LDS.128); the lane's own factor P[lane][k]
+// is read as P[k][lane] (exact by symmetry; consecutive lanes hit consecutive
+// words, so no bank conflicts).  Nothing but the result row lives in registers.
+template <int T, int TB>
+__device__ __forceinline__ void square_row(double (&res)[TB], const double* src, int lane) {
+#pragma unroll
+  for (int j = 0; j < T; ++j) res[j] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < T; ++k) {
+    const double* row = src + k * T;
+    const double own = lane < T ? row[lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < T; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(row + j);
+      res[j] = fma(own, v.x, res[j]);
+      res[j + 1] = fma(own, v.y, res[j + 1]);
+    }
+  }
+}
+
+template <int T, int TB>
+__device__ __forceinline__ void store_rows(const double (&g)[TB], double* dst, int lane) {
+  if (lane < T) {
+#pragma unroll
+    for (int j = 0; j < T; j += 2)
+      *reinterpret_cast<double2*>(dst + lane * T + j) = make_double2(g[j], g[j + 1]);
+  }
+}
+
+// Plain gradient descent, E = inner_steps epochs of c <- T c + d with
+// T = I - 2 lr G and d = 2 lr b (clomp.cpp:87-90, 178-181).  With E = 4q + r:
+// r single steps, then q steps of c <- T^4 c + (I + T + T^2 + T^3) d, the same
+// iterate in exact arithmetic (T^4 c_k + sum_{i<4} T^i d = c_{k+4}) at a
+// quarter of the broadcast traffic; T^2 and T^4 are formed once per outer
+// iteration by two warp-level squarings in shared memory.
+template <int T, int TB>
+__device__ void epochs_plain(double (&g)[TB], double& c, double d, double* cs,
+                             double* s1, const SolveParams& p, int lane) {
+  const int E = p.inner;
+  const int q = E / 4, r = E % 4;
+  int ep = 0;
+  if (q < 2) {  // too few epochs for the powers to pay off
+    affine_steps<T, TB>(g, c, d, cs, E, &ep);
+    return;
+  }
+  affine_steps<T, TB>(g, c, d, cs, r, &ep);
+  // d4 = (I + T + T^2 + T^3) d by Horner: v <- T v + d, three times from v = d.
+  double v = d;
+  cs[(ep & 1) * kWarpCap + lane] = v;  // stage v in the slot affine_steps reads
+  __syncwarp();
+  {
+    int ev = ep;
+    affine_steps<T, TB>(g, v, d, cs, 3, &ev);
+    // restore c in the slot the next affine step reads
+    cs[(ev & 1) * kWarpCap + lane] = c;
+    ep = ev;
+    __syncwarp();
+  }
+  const double d4 = v;
+  // T is exactly symmetric (G is stored mirrored), hence so are T^2 and T^4,
+  // which square_row relies on.  One T x T buffer: T, then T^2.
+  store_rows<T, TB>(g, s1, lane);
+  __syncwarp();
+  square_row<T, TB>(g, s1, lane);  // g <- row of T^2
+  __syncwarp();
+  store_rows<T, TB>(g, s1, lane);
+  __syncwarp();
+  square_row<T, TB>(g, s1, lane);  // g <- row of T^4
+  affine_steps<T, TB>(g, c, d4, cs, q, &ep);
+}
+
+template <int TB, int OPT>
+__device__ __forceinline__ void epochs_dispatch(const double (&g)[TB], double& c,
+                                                double bi, double& m1, double& m2,
+                                                double* cs, const SolveParams& p,
+                                                int step0, int lane, int t) {
+  if constexpr (TB == 8) {
+    epochs_warp<8, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+  } else if constexpr (TB == 16) {
+    if (t <= 8)
+      epochs_warp<8, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+    else
+      epochs_warp<16, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+  } else {
+    if (t <= 16)
+      epochs_warp<16, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+    else if (t <= 24)
+      epochs_warp<24, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+    else
+      epochs_warp<32, TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+  }
+}
+
+// Sum of per-lane vectors acc[0..N) over the warp: afterwards lane L holds
+// sum over all 32 lanes of acc[L % N].  Recursive halving inside each group of
+// N lanes (N-1 shuffles), then a butterfly across the 32/N groups; all array
+// indices are compile-time so acc stays in registers.
+template <int N>
+__device__ __forceinline__ double transpose_reduce(double (&acc)[N], int lane) {
+#pragma unroll
+  for (int sft = N / 2; sft >= 1; sft >>= 1) {
+    const bool upper = (lane & sft) != 0;
+#pragma unroll
+    for (int j = 0; j < sft; ++j) {
+      const double send = upper ? acc[j] : acc[j + sft];
+      const double keep = upper ? acc[j + sft] : acc[j];
+      acc[j] = keep + __shfl_xor_sync(kFull, send, sft);
+    }
+  }
+  double v = acc[0];
+#pragma unroll
+  for (int sft = N; sft < 32; sft <<= 1) v += __shfl_xor_sync(kFull, v, sft);
+  return v;
+}
+
+// Gram row/column and b entry of every atom added since the last call
+// (one warp, t <= 32): G[k][i] = a_k . a_i, b_k = a_k . y, fp64 sums of the
+// fp32 products.  All k+1 dot products run at once (float4 loads, lanes over
+// the measurements) and are reduced together by transpose_reduce32.
+template <int TB>
+__device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
+                                 int t0, int t, int lane, const int32_t* sups) {
+  const int64_t cap = p.cap, ldm = p.ldm;
+  double* G = w.gram + b * cap * cap;
+  const double* y = w.y64 + b * ldm;
+  if (w.gfull) {
+    // Gather from the context's A^T A; b_k = a_k . y on demand.
+    for (int k = t0; k < t; ++k) {
+      const int64_t jk = sups[k];
+      if (lane <= k) {
+        const double v = w.gfull[jk * p.n + sups[lane]];
+        G[(int64_t)k * cap + lane] = v;
+        G[(int64_t)lane * cap + k] = v;
+      }
+      const double* ak = w.at64 + jk * ldm;
+      double accb = 0.0;
+      for (int64_t i0 = 4 * lane; i0 < ldm; i0 += 128) {
+        const double2 a01 = *reinterpret_cast<const double2*>(ak + i0);
+        const double2 a23 = *reinterpret_cast<const double2*>(ak + i0 + 2);
+        const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
+        const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+        accb = fma(a01.x, y01.x, accb);
+        accb = fma(a01.y, y01.y, accb);
+        accb = fma(a23.x, y23.x, accb);
+        accb = fma(a23.y, y23.y, accb);
+      }
+      accb = warp_sum(accb);
+      if (lane == 0) {
+        w.bvec[b * cap + k] = accb;
+        w.coef[b * cap + k] = 0.0;  // new atoms start at 0 (clomp.hpp:53-54)
+        w.mom1[b * cap + k] = 0.0;
+        w.mom2[b * cap + k] = 0.0;
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  for (int k = t0; k < t; ++k) {
+    const float* ak = w.at32 + (int64_t)sups[k] * ldm;
+    double acc[TB];
+#pragma unroll
+    for (int i = 0; i < TB; ++i) acc[i] = 0.0;
+    double accb = 0.0;
+    for (int64_t i0 = 4 * lane; i0 < ldm; i0 += 128) {
+      const float4 av = *reinterpret_cast<const float4*>(ak + i0);
+      const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
+      const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+      const double ax = f2d(av.x), ay = f2d(av.y), az = f2d(av.z), aw = f2d(av.w);
+      accb = fma(ax, y01.x, accb);
+      accb = fma(ay, y01.y, accb);
+      accb = fma(az, y23.x, accb);
+      accb = fma(aw, y23.y, accb);
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        if (i <= k) {
+          const float4 ai = *reinterpret_cast<const float4*>(w.at32 + (int64_t)sups[i] * ldm + i0);
+          acc[i] = fma(ax, f2d(ai.x), acc[i]);
+          acc[i] = fma(ay, f2d(ai.y), acc[i]);
+          acc[i] = fma(az, f2d(ai.z), acc[i]);
+          acc[i] = fma(aw, f2d(ai.w), acc[i]);
+        }
+      }
+    }
+    const double gk = transpose_reduce<TB>(acc, lane);
+    if (lane <= k) {
+      G[(int64_t)k * cap + lane] = gk;
+      G[(int64_t)lane * cap + k] = gk;
+    }
+    accb = warp_sum(accb);
     if (lane == 0) {
-      w.bvec[b * cap + k] = acc;
+      w.bvec[b * cap + k] = accb;
       w.coef[b * cap + k] = 0.0;  // new atoms start at 0 (clomp.hpp:53-54)
       w.mom1[b * cap + k] = 0.0;
       w.mom2[b * cap + k] = 0.0;
@@ -422,56 +690,151 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w,
   __syncwarp();
 }
 
-// Residual r = A_S c - y (fp64), stored for the next correlation, and its
-// sum of squares.  c is read from shared memory (cs[k] for support slot k).
+// Residual r = A_S c - y (fp64), stored for the next correlation (fp64 and the
+// tf32 split), and its sum of squares.  Each lane owns 16 measurements per
+// 512-row pass (float4 atom loads); c and the support come from shared memory.
 __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
                                 const double* cs, const int32_t* sups, int t,
                                 int lane) {
+  const int64_t ldm = p.ldm;
+  const double* y = w.y64 + b * ldm;
   double lacc = 0.0;
-  const double* y = w.y64 + b * p.ldm;
-  for (int64_t i = lane; i < p.ldm; i += 32) {
-    double acc = 0.0;
-    for (int k = 0; k < t; ++k)
-      acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
-    const double rv = acc - y[i];
-    store_residual(w, b * p.ldm + i, rv);
-    lacc = fma(rv, rv, lacc);
+  for (int64_t base = 0; base < ldm; base += 512) {
+    double r[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) r[q] = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < t; ++k) {
+      const double ck = cs[k];
+      const double* row = w.at64 + (int64_t)sups[k] * ldm + base + 4 * lane;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (base + 128 * q < ldm) {
+          const double2 v01 = *reinterpret_cast<const double2*>(row + 128 * q);
+          const double2 v23 = *reinterpret_cast<const double2*>(row + 128 * q + 2);
+          r[4 * q + 0] = fma(v01.x, ck, r[4 * q + 0]);
+          r[4 * q + 1] = fma(v01.y, ck, r[4 * q + 1]);
+          r[4 * q + 2] = fma(v23.x, ck, r[4 * q + 2]);
+          r[4 * q + 3] = fma(v23.y, ck, r[4 * q + 3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i0 = base + 128 * q + 4 * lane;
+      if (base + 128 * q < ldm) {
+        const int64_t o = b * ldm + i0;
+        const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
+        const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+        const double v0 = r[4 * q + 0] - y01.x, v1 = r[4 * q + 1] - y01.y;
+        const double v2 = r[4 * q + 2] - y23.x, v3 = r[4 * q + 3] - y23.y;
+        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(v0, v1);
+        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(v2, v3);
+        if (w.r_hi) {
+          float h0, h1, h2, h3, l0, l1, l2, l3;
+          split_tf32((float)v0, h0, l0);
+          split_tf32((float)v1, h1, l1);
+          split_tf32((float)v2, h2, l2);
+          split_tf32((float)v3, h3, l3);
+          *reinterpret_cast<float4*>(w.r_hi + o) = make_float4(h0, h1, h2, h3);
+          *reinterpret_cast<float4*>(w.r_lo + o) = make_float4(l0, l1, l2, l3);
+        }
+        lacc = fma(v0, v0, lacc);
+        lacc = fma(v1, v1, lacc);
+        lacc = fma(v2, v2, lacc);
+        lacc = fma(v3, v3, lacc);
+      }
+    }
   }
   return warp_sum(lacc);
 }
 
-template <int OPT>
+template <int TB, int OPT>
 __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
-                                int outer, double* cs, int32_t* sups,
-                                int lane) {
+                                int outer, double* cs, int32_t* sups, double* s1,
+                                double* s2, int lane) {
   const int t = w.cnt[b];
   const int t0 = w.gcnt[b];
   const int64_t cap = p.cap;
-  warp_extend_gram(p, w, b, t0, t, lane);
+  if (lane < t) sups[lane] = w.sup[b * cap + lane];
+  __syncwarp();
+  warp_extend_gram<TB>(p, w, b, t0, t, lane, sups);
   if (lane == 0) w.gcnt[b] = t;
 
-  double g[kWarpCap];
+  double g[TB];
   const double* G = w.gram + b * cap * cap;
+  const double twolr = 2.0 * p.lr;
 #pragma unroll
-  for (int j = 0; j < kWarpCap; ++j)
-    g[j] = (lane < t && j < t) ? G[(int64_t)lane * cap + j] : 0.0;
+  for (int j = 0; j < TB; ++j) {
+    const double gij = (lane < t && j < t) ? G[(int64_t)lane * cap + j] : 0.0;
+    if (OPT == 0)
+      g[j] = (lane < t && j == lane) ? 1.0 - twolr * gij : -(twolr * gij);
+    else
+      g[j] = gij;
+  }
   double c = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
   if (lane < t) {
     c = w.coef[b * cap + lane];
     bi = w.bvec[b * cap + lane];
+    if (OPT == 0) bi = twolr * bi;
     m1 = w.mom1[b * cap + lane];
     m2 = w.mom2[b * cap + lane];
-    sups[lane] = w.sup[b * cap + lane];
   }
   cs[lane] = c;
   __syncwarp();
   const int step0 = (outer - 1) * p.inner;
-  epochs_dispatch<OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+  if constexpr (OPT == 0) {
+    if constexpr (TB == 8) {
+      epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
+    } else if constexpr (TB == 16) {
+      if (t <= 8)
+        epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
+      else
+        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
+    } else {
+      if (t <= 16)
+        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
+      else if (t <= 24)
+        epochs_plain<24, TB>(g, c, bi, cs, s1, p, lane);
+      else
+        epochs_plain<32, TB>(g, c, bi, cs, s1, p, lane);
+    }
+  } else {
+    epochs_dispatch<TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
+  }
   if (lane < t) {
     w.coef[b * cap + lane] = c;
-    w.mom1[b * cap + lane] = m1;
-    w.mom2[b * cap + lane] = m2;
+    if (OPT != 0) {
+      w.mom1[b * cap + lane] = m1;
+      w.mom2[b * cap + lane] = m2;
+    }
   }
+}
+
+// Residual, loss and stopping rules after the learning phase: one warp per
+// signal, few registers, so enough warps are resident to hide the L2 latency
+// of the support-atom gathers.  Signals whose support outgrew the learning
+// bucket TB were finished by the block kernel and are skipped.
+template <int TB>
+__global__ void __launch_bounds__(256)
+k_resid_warp(SolveParams p, Work w, int outer) {
+  __shared__ __align__(16) double cs_all[8][kWarpCap];
+  __shared__ int32_t sup_all[8][kWarpCap];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 8 + warp;
+  if (b >= p.B || !w.active[b]) return;
+  const int t = w.cnt[b];
+  if (t > TB) return;
+  double* cs = cs_all[warp];
+  int32_t* sups = sup_all[warp];
+  const int64_t cap = p.cap;
+  double c = 0.0;
+  if (lane < t) {
+    c = w.coef[b * cap + lane];
+    sups[lane] = w.sup[b * cap + lane];
+  }
+  cs[lane] = c;
+  __syncwarp();
   const double L = warp_residual(p, w, b, cs, sups, t, lane);
   if (p.mode == kModePerSignal) {
     bool snap = false;
@@ -483,27 +846,37 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   }
 }
 
-__global__ void __launch_bounds__(128)
+// TB: support-size bucket this launch is compiled for (8, 16 or 32).  Signals
+// whose support outgrew it (possible only through ties) are queued for the
+// block kernel.
+template <int TB>
+constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
+
+template <int TB>
+constexpr int learn_min_blocks() { return TB == 32 ? 6 : 4; }
+
+template <int TB, int OPT>
+__global__ void __launch_bounds__(32 * learn_warps<TB>(), learn_min_blocks<TB>())
 k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
-  __shared__ __align__(16) double cs_all[4][kWarpCap];
-  __shared__ int32_t sup_all[4][kWarpCap];
+  constexpr int NW = learn_warps<TB>();
+  __shared__ __align__(16) double cs_all[NW][2 * kWarpCap];
+  __shared__ int32_t sup_all[NW][kWarpCap];
+  __shared__ __align__(16) double sq_all[NW][TB * TB];  // T / T^2 scratch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  const int64_t b = (int64_t)blockIdx.x * NW + warp;
   if (b >= p.B || !w.active[b]) return;
-  if (w.cnt[b] > kWarpCap) {  // handled by the block kernel
+  if (w.cnt[b] > TB) {
     if (lane == 0) {
-      const int slot = atomicAdd(&w.counters[kRescanCount + 4], 1);
+      const int slot = atomicAdd(&w.counters[kBigCount], 1);
       big_list[slot] = (int32_t)b;
     }
     return;
   }
   double* cs = cs_all[warp];
   int32_t* sups = sup_all[warp];
-  switch (p.opt) {
-    case 0: learn_warp_body<0>(p, w, b, outer, cs, sups, lane); break;
-    case 1: learn_warp_body<1>(p, w, b, outer, cs, sups, lane); break;
-    default: learn_warp_body<2>(p, w, b, outer, cs, sups, lane); break;
-  }
+  double* s1 = sq_all[warp];
+  double* s2 = nullptr;
+  learn_warp_body<TB, OPT>(p, w, b, outer, cs, sups, s1, s2, lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -524,7 +897,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
   __shared__ int snap_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kBlockThreads / 32;
-  const int count = w.counters[kRescanCount + 4];
+  const int count = w.counters[kBigCount];
   const int64_t cap = p.cap;
   for (int li = blockIdx.x; li < count; li += gridDim.x) {
     const int64_t b = big_list[li];
@@ -534,23 +907,33 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     const double* y = w.y64 + b * p.ldm;
     for (int k = tid; k < t; k += kBlockThreads) sups[k] = w.sup[b * cap + k];
     __syncthreads();
-    // Gram extension: warps over (k, i) pairs, lanes over m.
+    // Gram extension: gathered from the context's A^T A when present, else
+    // warps over (k, i) pairs with lanes over m.
     for (int k = t0; k < t; ++k) {
       const float* ak = w.at32 + (int64_t)sups[k] * p.ldm;
-      for (int i = warp; i <= k; i += nw) {
-        const float* ai = w.at32 + (int64_t)sups[i] * p.ldm;
-        double acc = 0.0;
-        for (int64_t q = lane; q < p.ldm; q += 32)
-          acc = fma((double)ak[q], (double)ai[q], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-          G[(int64_t)k * cap + i] = acc;
-          G[(int64_t)i * cap + k] = acc;
+      if (w.gfull) {
+        for (int i = tid; i <= k; i += kBlockThreads) {
+          const double v = w.gfull[(int64_t)sups[k] * p.n + sups[i]];
+          G[(int64_t)k * cap + i] = v;
+          G[(int64_t)i * cap + k] = v;
+        }
+      } else {
+        for (int i = warp; i <= k; i += nw) {
+          const float* ai = w.at32 + (int64_t)sups[i] * p.ldm;
+          double acc = 0.0;
+          for (int64_t q = lane; q < p.ldm; q += 32)
+            acc = fma(w.at64[(int64_t)sups[k] * p.ldm + q], w.at64[(int64_t)sups[i] * p.ldm + q], acc);
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            G[(int64_t)k * cap + i] = acc;
+            G[(int64_t)i * cap + k] = acc;
+          }
         }
       }
-      if (warp == 0) {
+      if (warp == nw - 1) {
         double acc = 0.0;
-        for (int64_t q = lane; q < p.ldm; q += 32) acc = fma((double)ak[q], y[q], acc);
+        for (int64_t q = lane; q < p.ldm; q += 32)
+          acc = fma(w.at64[(int64_t)sups[k] * p.ldm + q], y[q], acc);
         acc = warp_sum(acc);
         if (lane == 0) {
           w.bvec[b * cap + k] = acc;
@@ -632,7 +1015,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     for (int64_t i = tid; i < p.ldm; i += kBlockThreads) {
       double acc = 0.0;
       for (int k = 0; k < t; ++k)
-        acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
+        acc = fma(w.at64[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
       const double rv = acc - y[i];
       store_residual(w, b * p.ldm + i, rv);
       lacc = fma(rv, rv, lacc);
@@ -861,11 +1244,28 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                   cudaStream_t s) {
   int32_t* big_list = w.rescan_list + p.B;  // second half of the list buffer
-  cudaMemsetAsync(&w.counters[kRescanCount + 4], 0, sizeof(int32_t), s);
-  const int64_t blocks = (p.B + 3) / 4;
-  k_learn_warp<<<(unsigned)blocks, 128, 0, s>>>(p, w, outer, big_list);
-  (void)max_cnt;
-  if (p.cap > kWarpCap) {
+  cudaMemsetAsync(&w.counters[kBigCount], 0, sizeof(int32_t), s);
+  // max_cnt: upper bound on the support size after this iteration's select
+  // (ties can exceed it; those signals fall through to the block kernel).
+  const int64_t rblocks = (p.B + 7) / 8;
+  auto blocks_for = [&](int nw) { return (unsigned)((p.B + nw - 1) / nw); };
+  auto learn = [&](auto tb) {
+    constexpr int TB = decltype(tb)::value;
+    constexpr int NW = learn_warps<TB>();
+    switch (p.opt) {
+      case 0: k_learn_warp<TB, 0><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
+      case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
+      default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
+    }
+    k_resid_warp<TB><<<(unsigned)rblocks, 256, 0, s>>>(p, w, outer);
+  };
+  if (max_cnt <= 8)
+    learn(std::integral_constant<int, 8>());
+  else if (max_cnt <= 16)
+    learn(std::integral_constant<int, 16>());
+  else
+    learn(std::integral_constant<int, 32>());
+  if (p.cap > 8) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -197,3 +197,17 @@ def test_config3_law_reduced(gpu_available):
     cfg = cl.ClompConfig.baseline(96)
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
     _subset_parity(A, Y, cfg, np.arange(3), r, X)
+
+
+def test_gram_cache_on_off_identical(gpu_available):
+    """Support-Gram rows gathered from the context's A^T A equal the on-demand
+    dot products (same fp64 values up to summation order)."""
+    A, X, Y, _ = cl.gen_problem_1d(21, 256, 640, 24, 64, snr_db=30.0)
+    cfg = cl.ClompConfig.baseline(24)
+    ctx = make_ctx(A)
+    ctx.set_gram_cache(1)
+    r1 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    ctx.set_gram_cache(0)
+    r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.array_equal(r1.mask, r0.mask)
+    assert rel_coef_err(r1.s, r0.s) <= 1e-10
