@@ -811,39 +811,82 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   }
 }
 
-// Residual, loss and stopping rules after the learning phase: one warp per
-// signal, few registers, so enough warps are resident to hide the L2 latency
-// of the support-atom gathers.  Signals whose support outgrew the learning
-// bucket TB were finished by the block kernel and are skipped.
+// Residual, loss and stopping rules after the learning phase.  One block per
+// signal; each warp owns 128-row chunks of the measurement vector (4 rows per
+// lane, fp64 atom rows read as 16-byte loads), so a signal's residual is
+// spread over several warps and many signals are resident per SM to hide the
+// L2 latency of the support-atom gathers.  Signals whose support outgrew the
+// learning bucket TB were finished by the block learning kernel.
+constexpr int kResidWarps = 4;
+
 template <int TB>
-__global__ void __launch_bounds__(256)
-k_resid_warp(SolveParams p, Work w, int outer) {
-  __shared__ __align__(16) double cs_all[8][kWarpCap];
-  __shared__ int32_t sup_all[8][kWarpCap];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * 8 + warp;
-  if (b >= p.B || !w.active[b]) return;
+__global__ void __launch_bounds__(32 * kResidWarps)
+k_resid(SolveParams p, Work w, int outer) {
+  __shared__ __align__(16) double cs[kWarpCap];
+  __shared__ int32_t sups[kWarpCap];
+  __shared__ double red[kResidWarps];
+  __shared__ int snap_s;
+  const int64_t b = blockIdx.x;
+  if (!w.active[b]) return;
   const int t = w.cnt[b];
   if (t > TB) return;
-  double* cs = cs_all[warp];
-  int32_t* sups = sup_all[warp];
-  const int64_t cap = p.cap;
-  double c = 0.0;
-  if (lane < t) {
-    c = w.coef[b * cap + lane];
-    sups[lane] = w.sup[b * cap + lane];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t cap = p.cap, ldm = p.ldm;
+  if (tid < t) {
+    cs[tid] = w.coef[b * cap + tid];
+    sups[tid] = w.sup[b * cap + tid];
   }
-  cs[lane] = c;
-  __syncwarp();
-  const double L = warp_residual(p, w, b, cs, sups, t, lane);
-  if (p.mode == kModePerSignal) {
-    bool snap = false;
-    if (lane == 0) snap = control_signal(p, w, b, outer, L);
-    snap = __shfl_sync(kFull, snap, 0);
-    if (snap && lane < t) w.best_coef[b * cap + lane] = c;
-  } else if (lane == 0) {
-    w.loss[b] = L;
+  __syncthreads();
+  const double* y = w.y64 + b * ldm;
+  double lacc = 0.0;
+  for (int64_t q = warp; q * 128 < ldm; q += kResidWarps) {
+    const int64_t i0 = q * 128 + 4 * lane;
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < t; ++k) {
+      const double ck = cs[k];
+      const double* row = w.at64 + (int64_t)sups[k] * ldm + i0;
+      const double2 v01 = *reinterpret_cast<const double2*>(row);
+      const double2 v23 = *reinterpret_cast<const double2*>(row + 2);
+      r0 = fma(v01.x, ck, r0);
+      r1 = fma(v01.y, ck, r1);
+      r2 = fma(v23.x, ck, r2);
+      r3 = fma(v23.y, ck, r3);
+    }
+    const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
+    const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+    const double v0 = r0 - y01.x, v1 = r1 - y01.y, v2 = r2 - y23.x, v3 = r3 - y23.y;
+    const int64_t o = b * ldm + i0;
+    *reinterpret_cast<double2*>(w.r64 + o) = make_double2(v0, v1);
+    *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(v2, v3);
+    if (w.r_hi) {
+      float h0, h1, h2, h3, l0, l1, l2, l3;
+      split_tf32((float)v0, h0, l0);
+      split_tf32((float)v1, h1, l1);
+      split_tf32((float)v2, h2, l2);
+      split_tf32((float)v3, h3, l3);
+      *reinterpret_cast<float4*>(w.r_hi + o) = make_float4(h0, h1, h2, h3);
+      *reinterpret_cast<float4*>(w.r_lo + o) = make_float4(l0, l1, l2, l3);
+    }
+    lacc = fma(v0, v0, lacc);
+    lacc = fma(v1, v1, lacc);
+    lacc = fma(v2, v2, lacc);
+    lacc = fma(v3, v3, lacc);
   }
+  lacc = warp_sum(lacc);
+  if (lane == 0) red[warp] = lacc;
+  __syncthreads();
+  if (tid == 0) {
+    double L = 0.0;
+    for (int q = 0; q < kResidWarps; ++q) L += red[q];
+    snap_s = 0;
+    if (p.mode == kModePerSignal)
+      snap_s = control_signal(p, w, b, outer, L);
+    else
+      w.loss[b] = L;
+  }
+  __syncthreads();
+  if (snap_s && tid < t) w.best_coef[b * cap + tid] = cs[tid];
 }
 
 // TB: support-size bucket this launch is compiled for (8, 16 or 32).  Signals
@@ -1045,6 +1088,14 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
 __global__ void __launch_bounds__(1024)
 k_joint_control(SolveParams p, Work w, int outer, int init) {
   __shared__ double red[1024];
+  // Once the batch has stopped, later (graph-replayed) iterations are no-ops.
+  if (!init && w.joint[kJStop] != 0.0) {
+    if (threadIdx.x == 0) {
+      w.joint[kJImproved] = 0.0;
+      w.counters[kActiveCount] = 0;
+    }
+    return;
+  }
   __shared__ int chg[32];
   const int tid = threadIdx.x;
   double s = 0.0;
@@ -1247,7 +1298,6 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
   cudaMemsetAsync(&w.counters[kBigCount], 0, sizeof(int32_t), s);
   // max_cnt: upper bound on the support size after this iteration's select
   // (ties can exceed it; those signals fall through to the block kernel).
-  const int64_t rblocks = (p.B + 7) / 8;
   auto blocks_for = [&](int nw) { return (unsigned)((p.B + nw - 1) / nw); };
   auto learn = [&](auto tb) {
     constexpr int TB = decltype(tb)::value;
@@ -1257,7 +1307,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
       default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
     }
-    k_resid_warp<TB><<<(unsigned)rblocks, 256, 0, s>>>(p, w, outer);
+    k_resid<TB><<<(unsigned)p.B, 32 * kResidWarps, 0, s>>>(p, w, outer);
   };
   if (max_cnt <= 8)
     learn(std::integral_constant<int, 8>());

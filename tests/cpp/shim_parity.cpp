@@ -1,0 +1,103 @@
+// shim_parity.cpp — the reference's own C++ API, served by the B200 shim.
+//
+// TEST INFRASTRUCTURE.  Linked (oracle/Makefile, target shim) from: this file,
+// paper_2501_11592_b200/csrc/shim/cskit_clomp_shim.cpp (first, so its
+// cskit::clomp_solve / clomp_solve_batch win), the unmodified reference
+// objects (everything incl. clomp.o, via --allow-multiple-definition), the
+// oracle restatement, and libclomp_b200.so.  Solves reference-style problems
+// (make_setup: Gaussian sensing composed with the DCT basis, sensing.cpp:77-79)
+// through cskit::clomp_solve and compares with the oracle: identical supports
+// and iteration counts, coefficients within 1e-9, x_hat within 1e-9.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "cskit/clomp.hpp"
+#include "cskit/errors.hpp"
+#include "cskit/rng.hpp"
+#include "cskit/sensing.hpp"
+
+extern "C" {
+#include "clomp_oracle.h"
+}
+
+using namespace cskit;
+
+static la::Mat round32(const la::Mat& m) {
+  la::Mat r = m;
+  for (double& v : r.a) v = static_cast<double>(static_cast<float>(v));
+  return r;
+}
+
+int main() {
+  int failures = 0;
+  for (int seed = 1; seed <= 6; ++seed) {
+    MeasurementSetup setup = make_setup(64, 0.5, 100 + seed);
+    setup.a = round32(setup.a);  // the GPU's fp32 operands, seen by both sides
+    Rng rng(static_cast<uint64_t>(seed));
+    la::Vec x(setup.n, 0.0);
+    for (int k = 0; k < 4; ++k) x[rng.uniform_below(setup.n)] = rng.normal();
+    la::Vec y = la::matvec(setup.a, x);
+    for (double& v : y) v = static_cast<double>(static_cast<float>(v));
+    ClompConfig cfg;
+    cfg.th = seed % 2 ? 1.0 : 0.7;
+    cfg.opt = seed % 3 == 0 ? Optimizer::adam : Optimizer::plain;
+    cfg.lr = cfg.opt == Optimizer::adam ? 0.02 : 0.1;
+    cfg.max_outer = 8;
+    cfg.inner_steps = 60;
+    cfg.w_tv = 0.0;
+    cfg.w_lv = 0.0;
+    const SolveResult got = clomp_solve(setup, y, cfg);  // -> shim -> GPU
+
+    orc_config oc{cfg.th, cfg.max_outer, cfg.eps, cfg.inner_steps, cfg.lr,
+                  static_cast<int32_t>(cfg.opt == Optimizer::plain ? 0 : cfg.opt == Optimizer::momentum ? 1 : 2),
+                  0, 0.0, 0.0, cfg.lv.window, cfg.lv.stride, cfg.stall_tol, cfg.stall_patience};
+    std::vector<double> s(setup.n);
+    std::vector<uint8_t> mk(setup.n);
+    int64_t it = 0;
+    double rn = 0.0;
+    uint8_t cv = 0;
+    int32_t st = 0;
+    orc_clomp_solve_batch(setup.a.data(), setup.m, setup.n, y.data(), 1, &oc, ORC_ISA_AVX2,
+                          ORC_MODE_JOINT, s.data(), mk.data(), &it, &rn, &cv, &st, nullptr,
+                          nullptr, 0);
+    double cmax = 0.0, err = 0.0, xerr = 0.0;
+    bool same_mask = true;
+    for (std::size_t j = 0; j < setup.n; ++j) {
+      same_mask = same_mask && (got.s.mask[j] == mk[j]);
+      cmax = std::fmax(cmax, std::fabs(s[j]));
+      err = std::fmax(err, std::fabs(got.s.values[j] - s[j]));
+    }
+    // x_hat = basis * s_eff (clomp.cpp:289) from the oracle's coefficients
+    for (std::size_t i = 0; i < setup.n; ++i) {
+      double acc = 0.0;
+      for (std::size_t j = 0; j < setup.n; ++j) acc += setup.basis(i, j) * (mk[j] ? s[j] : 0.0);
+      xerr = std::fmax(xerr, std::fabs(acc - got.x_hat[i]));
+    }
+    const bool ok = st == 0 && same_mask && got.iterations == static_cast<std::size_t>(it) &&
+                    err <= 1e-9 * std::fmax(cmax, 1.0) && xerr <= 1e-9 &&
+                    got.converged == (cv != 0);
+    std::printf("seed %d th %.1f opt %d: mask %s iters %zu/%lld coef err %.2e x_hat err %.2e %s\n",
+                seed, cfg.th, oc.opt, same_mask ? "same" : "DIFF", got.iterations,
+                static_cast<long long>(it), err, xerr, ok ? "ok" : "FAIL");
+    failures += ok ? 0 : 1;
+  }
+  // Error mapping: a diverging lr raises cskit::NumericalError through the shim.
+  try {
+    MeasurementSetup setup = make_setup(32, 0.5, 7);
+    setup.a = round32(setup.a);
+    la::Vec y(setup.m, 0.25);
+    ClompConfig cfg;
+    cfg.th = 1.0;
+    cfg.opt = Optimizer::plain;
+    cfg.lr = 1e6;
+    cfg.w_tv = cfg.w_lv = 0.0;
+    clomp_solve(setup, y, cfg);
+    std::printf("divergence: no exception FAIL\n");
+    ++failures;
+  } catch (const NumericalError&) {
+    std::printf("divergence: NumericalError ok\n");
+  }
+  std::printf("%s\n", failures ? "SHIM PARITY FAILED" : "SHIM PARITY OK");
+  return failures ? 1 : 0;
+}

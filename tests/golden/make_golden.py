@@ -129,6 +129,12 @@ def main():
     add_solve("diverging_lr", A, Y[:, :1], ClompConfig(th=1.0, opt=PLAIN, lr=1e6, w_tv=0.0,
                                                        w_lv=0.0, max_outer=5), "batch")
     add_solve("eps_at_start", A, np.zeros((32, 1)), base(5), "single")
+    # Joint early stops: noiseless batch that converges before max_outer (eps
+    # break, clomp.cpp:238-242) and a stalled batch (clomp.cpp:264-273).
+    A2, Y2 = rand_problem(7, 40, 80, 3, 4)
+    add_solve("joint_eps_break", A2, Y2, base(9), "batch")
+    add_solve("joint_stall", A2, Y2, ClompConfig(th=1.0, opt=PLAIN, lr=1e-6, inner_steps=1,
+                                                max_outer=40, w_tv=0.0, w_lv=0.0), "batch")
     add_solve("stall_small_lr", A, Y[:, :1], ClompConfig(th=1.0, opt=PLAIN, lr=1e-6,
                                                          inner_steps=1, max_outer=50,
                                                          w_tv=0.0, w_lv=0.0), "single")
