@@ -107,6 +107,16 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
                   int a_layout, int* status);
 void cl_destroy(cl_ctx* ctx);
 
+/* Separable 2D operator Y = A_r S A_c^T (north star "2D mode"):
+ * the dictionary is A = A_c (x) A_r with column-major vec, i.e. atom
+ * p = i + n_r*j (S[i][j]) and measurement q = qr + m_r*qc (Y[qr][qc]); y
+ * passed to cl_solve_batch is vec(Y) per signal (m = m_r*m_c rows).  The
+ * Kronecker matrix is never formed.  a_r: m_r x n_r, a_c: m_c x n_c
+ * (CL_LAYOUT_REF) or their transposes (CL_LAYOUT_T). */
+cl_ctx* cl_create_sep(int device, const float* a_r, int64_t m_r, int64_t n_r,
+                      const float* a_c, int64_t m_c, int64_t n_c, int layout,
+                      int* status);
+
 /* Message of the last failing call on ctx (or of the last failing cl_create
  * on this thread when ctx is NULL). */
 const char* cl_last_error(const cl_ctx* ctx);

@@ -144,24 +144,35 @@ static void support_insert(support_t* s, int64_t j) {
 }
 
 typedef struct {
-  const double* a;   /* m x n */
+  const double* a;   /* m x n (NULL for the separable operator) */
   const double* at;  /* n x m (LossOps::at, clomp.cpp:57-66) */
   int64_t m, n, batch;
   int isa;
+  /* Separable operator A = A_c (x) A_r, column-major vec: atom p = i + n_r j,
+   * measurement q = qr + m_r qc, A[q][p] = A_c[qc][j] * A_r[qr][i] (the entry
+   * an explicit np.kron / dense Kronecker matrix would hold). */
+  const double* ar;  /* m_r x n_r */
+  const double* ac;  /* m_c x n_c */
+  int64_t mr, nr, mc, nc;
 } problem_t;
+
+static inline double entry(const problem_t* p, int64_t q, int64_t j) {
+  if (p->a) return p->a[q * p->n + j];
+  const int64_t qr = q % p->mr, qc = q / p->mr, i = j % p->nr, jc = j / p->nr;
+  return p->ac[qc * p->nc + jc] * p->ar[qr * p->nr + i];
+}
 
 /* r = A*(mask.*s) - y  (clomp.cpp:83-84, 236-237, 285-286), support-restricted. */
 static void residual(const problem_t* p, const double* s, const support_t* sup,
                      const double* y, double* r) {
   const int64_t B = p->batch;
   for (int64_t i = 0; i < p->m; ++i) {
-    const double* arow = p->a + i * p->n;
     for (int64_t b = 0; b < B; ++b) {
       double acc = 0.0;
       const support_t* sb = &sup[b];
       for (int64_t q = 0; q < sb->count; ++q) {
         const int64_t j = sb->idx[q];
-        acc = mac(acc, arow[j], s[j * B + b], p->isa);
+        acc = mac(acc, entry(p, i, j), s[j * B + b], p->isa);
       }
       r[i * B + b] = acc - y[i * B + b];
     }
@@ -171,10 +182,14 @@ static void residual(const problem_t* p, const double* s, const support_t* sup,
 /* (A^T r)[j, b] for one atom j: la::matmul(ops.at, r) element (clomp.cpp:89, 245). */
 static inline double corr(const problem_t* p, const double* r, int64_t j,
                           int64_t b) {
-  const double* atrow = p->at + j * p->m;
   const int64_t B = p->batch;
   double acc = 0.0;
-  for (int64_t q = 0; q < p->m; ++q) acc = mac(acc, atrow[q], r[q * B + b], p->isa);
+  if (p->at) {
+    const double* atrow = p->at + j * p->m;
+    for (int64_t q = 0; q < p->m; ++q) acc = mac(acc, atrow[q], r[q * B + b], p->isa);
+  } else {
+    for (int64_t q = 0; q < p->m; ++q) acc = mac(acc, entry(p, q, j), r[q * B + b], p->isa);
+  }
   return acc;
 }
 
@@ -381,13 +396,14 @@ static double* transpose(const double* a, int64_t m, int64_t n) {
   return t;
 }
 
-int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
-                          const double* y, int64_t batch,
-                          const orc_config* cfg, int isa, int mode,
-                          double* s_out, uint8_t* mask_out,
-                          int64_t* iterations, double* final_rn,
-                          uint8_t* converged, int32_t* status, double* trace,
-                          char* err, int errlen) {
+/* Shared driver: `proto` carries the operator (dense or separable). */
+static int solve_driver(problem_t proto, const double* y, int64_t batch,
+                        const orc_config* cfg, int mode, double* s_out,
+                        uint8_t* mask_out, int64_t* iterations, double* final_rn,
+                        uint8_t* converged, int32_t* status, double* trace,
+                        char* err, int errlen) {
+  const int64_t m = proto.m, n = proto.n;
+  const int isa = proto.isa;
   int st = validate(cfg, err, errlen);
   if (st) return st;
   if (m <= 0 || n <= 0) {
@@ -401,20 +417,18 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
   if (trace)
     for (int64_t e = 0; e < batch * (int64_t)cfg->max_outer * 4; ++e) trace[e] = -1.0;
 
-  double* at = transpose(a, m, n);
   if (mode == ORC_MODE_JOINT) {
     double w_tv, w_lv;
     resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
     if (w_tv > 0.0 || w_lv > 0.0) {
-      free(at);
       set_err(err, errlen, "clomp oracle: priors (w_tv/w_lv > 0) are not restated");
       return ORC_ERR_UNSUPPORTED;
     }
-    problem_t p = {a, at, m, n, batch, isa};
+    problem_t p = proto;
+    p.batch = batch;
     st = solve_joint(&p, y, cfg, s_out, mask_out, iterations, final_rn,
                      converged, trace, (int64_t)cfg->max_outer * 4, err, errlen);
     for (int64_t b = 0; b < batch; ++b) status[b] = st;
-    free(at);
     return st;
   }
 
@@ -433,7 +447,8 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
     if (w_tv > 0.0 || w_lv > 0.0) {
       sb = ORC_ERR_UNSUPPORTED;
     } else {
-      problem_t p = {a, at, m, n, 1, isa};
+      problem_t p = proto;
+      p.batch = 1;
       sb = solve_joint(&p, yc, cfg, sc, mc, &it, &rn, &cv,
                        trace ? trace + b * (int64_t)cfg->max_outer * 4 : NULL,
                        4, NULL, 0);
@@ -457,8 +472,38 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
     final_rn[b] = rn;
     converged[b] = cv;
   }
-  free(yc); free(sc); free(mc); free(at);
+  free(yc); free(sc); free(mc);
   return ORC_OK;
+}
+
+int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
+                          const double* y, int64_t batch,
+                          const orc_config* cfg, int isa, int mode,
+                          double* s_out, uint8_t* mask_out,
+                          int64_t* iterations, double* final_rn,
+                          uint8_t* converged, int32_t* status, double* trace,
+                          char* err, int errlen) {
+  if (m <= 0 || n <= 0) {
+    set_err(err, errlen, "clomp: empty operator");
+    return ORC_ERR_DIMENSION;
+  }
+  double* at = transpose(a, m, n);
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
+  const int st = solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations,
+                              final_rn, converged, status, trace, err, errlen);
+  free(at);
+  return st;
+}
+
+int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
+                        const double* ac, int64_t mc, int64_t nc,
+                        const double* y, int64_t batch, const orc_config* cfg,
+                        int isa, int mode, double* s_out, uint8_t* mask_out,
+                        int64_t* iterations, double* final_rn, uint8_t* converged,
+                        int32_t* status, double* trace, char* err, int errlen) {
+  problem_t p = {NULL, NULL, mr * mc, nr * nc, batch, isa, ar, ac, mr, nr, mc, nc};
+  return solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations, final_rn,
+                      converged, status, trace, err, errlen);
 }
 
 /* ------------------------------------------------------ unit entry points */
@@ -467,7 +512,7 @@ int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
                        int64_t batch, double th, int isa, uint8_t* mask) {
   if (!(th > 0.0) || th > 1.0) return ORC_ERR_CONFIG;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {
@@ -491,7 +536,7 @@ int orc_clomp_loss(const double* a, int64_t m, int64_t n, const double* y,
   resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
   if (w_tv > 0.0 || w_lv > 0.0) return ORC_ERR_UNSUPPORTED;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {

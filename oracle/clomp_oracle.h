@@ -73,6 +73,18 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           uint8_t* converged, int32_t* status, double* trace,
                           char* err, int errlen);
 
+/* Separable 2D operator A = A_c (x) A_r with column-major vec (atom
+ * p = i + n_r j, measurement q = qr + m_r qc): exactly clomp_solve(_batch) run
+ * on the explicit Kronecker matrix with entries A_c[qc][j] * A_r[qr][i]
+ * (the reference has no separable mode).  ar: m_r x n_r,
+ * ac: m_c x n_c row-major; y: (m_r m_c) x B. */
+int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
+                        const double* ac, int64_t mc, int64_t nc,
+                        const double* y, int64_t batch, const orc_config* cfg,
+                        int isa, int mode, double* s_out, uint8_t* mask_out,
+                        int64_t* iterations, double* final_rn, uint8_t* converged,
+                        int32_t* status, double* trace, char* err, int errlen);
+
 /* inject_support (clomp.cpp:142-154): mask |= thresholded |A^T r| per column. */
 int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
                        int64_t batch, double th, int isa, uint8_t* mask);

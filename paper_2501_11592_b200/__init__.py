@@ -146,7 +146,8 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep",
+    "cl_gen_problem_2d",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
 
@@ -178,6 +179,9 @@ def lib() -> C.CDLL:
         h.cl_set_stream.argtypes = [vp, vp]
         h.cl_debug_scores.argtypes = [vp, vp, i64, i32, vp]
         h.cl_set_gram_cache.argtypes = [vp, i32]
+        h.cl_create_sep.restype = vp
+        h.cl_create_sep.argtypes = [i32, vp, i64, i64, vp, i64, i64, i32, C.POINTER(C.c_int)]
+        h.cl_gen_problem_2d.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]
         h.cl_config_default.argtypes = [C.POINTER(CConfig)]
         h.cl_rng_draws.argtypes = [C.c_uint64, i32, C.c_uint64, i64, vp, vp]
         h.cl_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, i32, i32, C.c_double, vp, vp, vp, vp]
@@ -278,6 +282,26 @@ class ClompContext:
             _raise(st.value or CL_ERR_CUDA, None)
         self._h = h
         self.device = device
+
+    @classmethod
+    def separable(cls, a_r, a_c, device: int = 0) -> "ClompContext":
+        """Separable 2D operator A = A_c (x) A_r (Y = A_r S A_c^T), column-major
+        vec: atom p = i + n_r*j, measurement q = qr + m_r*qc.  The Kronecker
+        matrix is never formed."""
+        ar = np.ascontiguousarray(a_r, dtype=np.float32)
+        ac = np.ascontiguousarray(a_c, dtype=np.float32)
+        self = cls.__new__(cls)
+        st = C.c_int(0)
+        h = lib().cl_create_sep(int(device), _ptr(ar), ar.shape[0], ar.shape[1], _ptr(ac),
+                                ac.shape[0], ac.shape[1], LAYOUT_REF, C.byref(st))
+        if not h:
+            _raise(st.value or CL_ERR_CUDA, None)
+        self._h = h
+        self.device = device
+        self.m = ar.shape[0] * ac.shape[0]
+        self.n = ar.shape[1] * ac.shape[1]
+        self.shape2d = (ar.shape, ac.shape)
+        return self
 
     @property
     def handle(self):
@@ -414,10 +438,28 @@ def gen_problem_1d(seed: int, m: int, n: int, k: int, batch: int,
     return A, X, Y, S
 
 
+def gen_problem_2d(seed: int, n_r: int, n_c: int, m_r: int, m_c: int, k: int, batch: int):
+    """Separable 2D problem.  Returns (A_r m_r x n_r fp32,
+    A_c m_c x n_c fp32, S (n_r n_c) x B fp64 vec'd coefficients, Y (m_r m_c) x B
+    fp32 vec'd measurements), column-major vec."""
+    Ar = np.zeros((m_r, n_r), np.float32)
+    Ac = np.zeros((m_c, n_c), np.float32)
+    S = np.zeros((n_r * n_c, batch), np.float64)
+    Y = np.zeros((m_r * m_c, batch), np.float32)
+    code = lib().cl_gen_problem_2d(seed, n_r, n_c, m_r, m_c, k, batch, _ptr(Ar), _ptr(Ac),
+                                   _ptr(S), _ptr(Y))
+    if code:
+        raise DimensionError("gen_problem_2d: bad sizes")
+    return Ar, Ac, S, Y
+
+
 # BASELINE.json configs (SURVEY.md §8d).  lr / epochs for configs 2-5 are not
 # stated there; config 1's are used and recorded.
 CONFIGS = {
     1: dict(name="cfg1_1d_single", m=128, n=256, k=10, batch=1, value_law=0, snr_db=-1.0, seed=0),
     2: dict(name="cfg2_1d_batched", m=512, n=1024, k=32, batch=4096, value_law=0, snr_db=40.0, seed=1),
     3: dict(name="cfg3_1d_long", m=4096, n=16384, k=256, batch=256, value_law=1, snr_db=-1.0, seed=2),
+    4: dict(name="cfg4_2d_sep", n_r=256, n_c=256, m_r=128, m_c=128, k=1500, batch=64, seed=3),
+    5: dict(name="cfg5_2d_sweep_r025", n_r=512, n_c=512, m_r=128, m_c=128, k=13107, batch=1024, seed=4),
+    6: dict(name="cfg5_2d_sweep_r05", n_r=512, n_c=512, m_r=256, m_c=256, k=13107, batch=1024, seed=5),
 }

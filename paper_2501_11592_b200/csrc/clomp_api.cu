@@ -69,6 +69,15 @@ struct cl_ctx {
   float* at_lo = nullptr;
   double* gfull = nullptr;  // A^T A fp64 [n][n], built once (k_gram.cu)
   double* at64 = nullptr;   // fp64 copy of the atom-major dictionary
+  // separable 2D contexts (cl_create_sep)
+  bool sep = false;
+  int64_t mr = 0, nr = 0, mc = 0, nc = 0, ldr = 0, ldc = 0;
+  float* at_r32 = nullptr;
+  float* at_c32 = nullptr;
+  double* at_r64 = nullptr;
+  double* at_c64 = nullptr;
+  double* gr = nullptr;
+  double* gc = nullptr;
   double colnorm_max = 0.0;
   std::string err;
   // batch workspace
@@ -165,6 +174,11 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.cand_i1 = cv.take<int32_t>(B * ntile);
     w.scores = need_scores ? cv.take<double>(B * ctx->n) : nullptr;
     const int64_t nchunk = (ctx->n + 256 + 63) / 64;  // tiles cover <= n + 256 atoms
+    if (ctx->sep) {
+      w.zb = cv.take<double>(B * ctx->n);
+      w.sep_scratch = cv.take<double>(B * ctx->nc * ctx->mr);
+      w.lpart = cv.take<double>(B * (((ctx->mr + 63) / 64) * ((ctx->mc + 63) / 64)));
+    }
     w.rs_top = cv.take<double>(B);
     w.rs_delta = cv.take<double>(B);
     w.rs_done = cv.take<int32_t>(B);
@@ -216,6 +230,10 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
   w.at_lo = ctx->at_lo;
   w.gfull = ctx->gfull;
   w.at64 = ctx->at64;
+  w.at_r64 = ctx->at_r64;
+  w.at_c64 = ctx->at_c64;
+  w.gr = ctx->gr;
+  w.gc = ctx->gc;
   ctx->w = w;
   return CL_OK;
 }
@@ -258,10 +276,13 @@ double delta_for(bool tensor, int64_t ldm) {
   return 1e-5 + (double)(ldm / 8) * 1.2e-7;
 }
 
-void enqueue_count(const SolveParams&, const cl_config* c, int mode, int64_t cap,
+void enqueue_count(const SolveParams& p, const cl_config* c, int mode, int64_t cap,
                    int64_t* per_iter) {
   (void)c;
-  *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0);
+  if (p.sep)
+    *per_iter = 3 + 2 + (cap > 8 ? 2 : 1) + 3 + (mode == CL_MODE_JOINT ? 2 : 0);
+  else
+    *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0);
 }
 
 struct OutPtrs {
@@ -279,13 +300,13 @@ struct OutPtrs {
 // y_dev: device pointer, layout_ref ? m x B : B x m.
 int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                const cl_config* c, int mode, const OutPtrs& out) {
-  const bool tensor = use_tensor_path(ctx, c);
-  const bool full_scores = c->th < 1.0;
+  const bool tensor = !ctx->sep && use_tensor_path(ctx, c);
+  const bool full_scores = c->th < 1.0 || ctx->sep;
   const int64_t cap = support_cap(ctx, c);
-  if (cap > 1024)
+  if (cap > 2048)
     return fail(ctx, CL_ERR_UNSUPPORTED,
-                "clomp: support capacity above 1024 atoms per signal is not "
-                "supported (th < 1 with n > 1024)");
+                "clomp: support capacity above 2048 atoms per signal is not "
+                "supported (lower max_outer, or th < 1 with n > 2048)");
   const int64_t tile_atoms = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
   int st = ensure_workspace(ctx, B, cap, full_scores, tensor, ntile);
@@ -315,6 +336,13 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
   p.delta_rel = delta_for(tensor, ctx->ldm);
   p.colnorm_max = ctx->colnorm_max;
+  p.sep = ctx->sep ? 1 : 0;
+  p.nr = ctx->nr;
+  p.nc = ctx->nc;
+  p.mr = ctx->mr;
+  p.mc = ctx->mc;
+  p.ldr = ctx->ldr;
+  p.ldc = ctx->ldc;
 
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
@@ -328,6 +356,20 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // (signals grown past it by ties are finished by the block kernel).
   auto enqueue_iteration = [&](int outer, int64_t* launches) {
     cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
+    if (p.sep) {
+      launch_sep_corr(p, w, w.r64, w.scores, true, s);
+      launch_select(p, w, true, s);
+      const int bound = c->th >= 1.0 ? outer : (int)cap;
+      launch_learn(p, w, outer, bound, s);
+      launch_sep_resid(p, w, outer, bound, s);
+      *launches += 3 + 2 + (cap > 8 ? 2 : 1) + 3;
+      if (mode == CL_MODE_JOINT) {
+        launch_joint_control(p, w, outer, false, s);
+        launch_joint_snapshot(p, w, s);
+        *launches += 2;
+      }
+      return;
+    }
     if (tensor)
       launch_corr_tc(p, w, s);
     else
@@ -349,6 +391,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
   ++launches;
+  if (p.sep) {  // b values of every atom: Z = A_r^T Y A_c
+    launch_sep_corr(p, w, w.y64, w.zb, false, s);
+    launches += 2;
+  }
   if (mode == CL_MODE_JOINT) {
     launch_joint_control(p, w, 0, true, s);
     ++launches;
@@ -360,6 +406,15 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     for (auto& e : ev) cudaEventCreate(&e);
     cudaEventRecord(ev[0], s);
     for (int outer = 1; outer <= p.max_outer; ++outer) {
+      if (p.sep) {
+        enqueue_iteration(outer, &launches);
+        CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, s));
+        CL_CUDA(ctx, cudaStreamSynchronize(s));
+        outer_done = outer;
+        if (ctx->h_counters[kActiveCount] == 0) break;
+        continue;
+      }
       cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
       cudaEventRecord(ev[1], s);
       if (tensor)
@@ -607,8 +662,98 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
   return ctx;
 }
 
+cl_ctx* cl_create_sep(int device, const float* a_r, int64_t m_r, int64_t n_r,
+                      const float* a_c, int64_t m_c, int64_t n_c, int layout,
+                      int* status) {
+  auto bail = [&](int code, const std::string& msg) -> cl_ctx* {
+    g_create_error = msg;
+    if (status) *status = code;
+    return nullptr;
+  };
+  if (!a_r || !a_c || m_r <= 0 || n_r <= 0 || m_c <= 0 || n_c <= 0)
+    return bail(CL_ERR_DIMENSION, "cl_create_sep: empty or null operator");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return bail(CL_ERR_CUDA, std::string("cl_create_sep: no CUDA device: ") +
+                                 cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= ndev) return bail(CL_ERR_CUDA, "cl_create_sep: bad device");
+  cudaSetDevice(device);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10)
+    return bail(CL_ERR_CUDA, "cl_create_sep: this build targets sm_100a (B200) only");
+  auto* ctx = new cl_ctx();
+  ctx->device = device;
+  ctx->sep = true;
+  ctx->mr = m_r;
+  ctx->nr = n_r;
+  ctx->mc = m_c;
+  ctx->nc = n_c;
+  ctx->m = m_r * m_c;
+  ctx->n = n_r * n_c;
+  ctx->ldm = (ctx->m + 127) / 128 * 128;
+  ctx->ldr = (m_r + 127) / 128 * 128;
+  ctx->ldc = (m_c + 127) / 128 * 128;
+  ctx->sms = prop.multiProcessorCount;
+  ctx->tc_ok = false;
+  auto atom_major = [&](const float* a, int64_t m, int64_t n, int64_t ld,
+                        std::vector<float>& f, std::vector<double>& d, double& cmax) {
+    f.assign((size_t)(n * ld), 0.f);
+    d.assign((size_t)(n * ld), 0.0);
+    for (int64_t j = 0; j < n; ++j) {
+      double ss = 0.0;
+      for (int64_t i = 0; i < m; ++i) {
+        const float v = layout == CL_LAYOUT_REF ? a[i * n + j] : a[j * m + i];
+        f[(size_t)(j * ld + i)] = v;
+        d[(size_t)(j * ld + i)] = v;
+        ss += (double)v * v;
+      }
+      cmax = std::max(cmax, std::sqrt(ss));
+    }
+  };
+  std::vector<float> fr, fc;
+  std::vector<double> dr, dc;
+  double cr = 0.0, cc = 0.0;
+  atom_major(a_r, m_r, n_r, ctx->ldr, fr, dr, cr);
+  atom_major(a_c, m_c, n_c, ctx->ldc, fc, dc, cc);
+  ctx->colnorm_max = cr * cc;
+  bool ok = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) == cudaSuccess;
+  ctx->stream = ctx->own_stream;
+  ok = ok && cudaMalloc(&ctx->at_r32, fr.size() * 4) == cudaSuccess &&
+       cudaMalloc(&ctx->at_c32, fc.size() * 4) == cudaSuccess &&
+       cudaMalloc(&ctx->at_r64, dr.size() * 8) == cudaSuccess &&
+       cudaMalloc(&ctx->at_c64, dc.size() * 8) == cudaSuccess &&
+       cudaMalloc(&ctx->gr, (size_t)(n_r * n_r) * 8) == cudaSuccess &&
+       cudaMalloc(&ctx->gc, (size_t)(n_c * n_c) * 8) == cudaSuccess &&
+       cudaMemcpy(ctx->at_r32, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(ctx->at_c32, fc.data(), fc.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(ctx->at_r64, dr.data(), dr.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(ctx->at_c64, dc.data(), dc.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMallocHost(&ctx->h_counters, kNumCounters * sizeof(int32_t)) == cudaSuccess &&
+       cudaMallocHost(&ctx->h_chunk, 2 * kNumCounters * sizeof(int32_t)) == cudaSuccess &&
+       cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming) == cudaSuccess &&
+       cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming) == cudaSuccess;
+  if (ok) {
+    // Factor Grams in fp64 on the device (k_gram.cu): Gr = A_r^T A_r, Gc = A_c^T A_c.
+    launch_gram_full(ctx->at_r32, n_r, ctx->ldr, ctx->gr, ctx->stream);
+    launch_gram_full(ctx->at_c32, n_c, ctx->ldc, ctx->gc, ctx->stream);
+    ok = cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    cl_destroy(ctx);
+    return bail(CL_ERR_CUDA, "cl_create_sep: device allocation failed");
+  }
+  if (status) *status = CL_OK;
+  return ctx;
+}
+
 int cl_set_gram_cache(cl_ctx* ctx, int mode) {
   if (!ctx) return CL_ERR_INTERNAL;
+  if (ctx->sep) return CL_OK;  // separable contexts use the factor Grams
   cudaSetDevice(ctx->device);
   const size_t bytes = (size_t)ctx->n * (size_t)ctx->n * sizeof(double);
   bool want = mode > 0;
@@ -622,6 +767,12 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->gfull);
   cudaFree(ctx->at64);
+  cudaFree(ctx->at_r32);
+  cudaFree(ctx->at_c32);
+  cudaFree(ctx->at_r64);
+  cudaFree(ctx->at_c64);
+  cudaFree(ctx->gr);
+  cudaFree(ctx->gc);
       ctx->gfull = nullptr;
     }
     ctx->w.gfull = nullptr;
@@ -648,6 +799,12 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->at_lo);
   cudaFree(ctx->gfull);
   cudaFree(ctx->at64);
+  cudaFree(ctx->at_r32);
+  cudaFree(ctx->at_c32);
+  cudaFree(ctx->at_r64);
+  cudaFree(ctx->at_c64);
+  cudaFree(ctx->gr);
+  cudaFree(ctx->gc);
   cudaFree(ctx->wbuf);
   cudaFree(ctx->bc);
   cudaFree(ctx->stage);
@@ -848,6 +1005,8 @@ int cl_solve_batch_device(cl_ctx* ctx, const float* d_y, int64_t batch,
 int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
                       uint8_t* mask) {
   if (!ctx) return CL_ERR_INTERNAL;
+  if (ctx->sep)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "inject_support: not available on separable contexts");
   if (!(th > 0.0) || th > 1.0)
     return fail(ctx, CL_ERR_CONFIG, "inject_support: th must be in (0, 1]");
   if (batch <= 0 || !r || !mask)

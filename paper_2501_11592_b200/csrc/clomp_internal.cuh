@@ -30,6 +30,9 @@ struct SolveParams {
   const double* bc2;
   double delta_rel;         // correlation error bound / (||a||max * ||r||)
   double colnorm_max;
+  // separable 2D operator A = A_c (x) A_r (atom p = i + nr*j, row q = qr + mr*qc)
+  int32_t sep;
+  int64_t nr, nc, mr, mc, ldr, ldc;
 };
 
 struct Work {
@@ -45,6 +48,14 @@ struct Work {
   double* r64 = nullptr;
   float* r_hi = nullptr;         // [B][ldm] tf32 split of the residual
   float* r_lo = nullptr;
+  // separable 2D mode
+  const double* at_r64 = nullptr;  // [nr][ldr] A_r atom-major
+  const double* at_c64 = nullptr;  // [nc][ldc] A_c atom-major
+  const double* gr = nullptr;      // [nr][nr] A_r^T A_r
+  const double* gc = nullptr;      // [nc][nc] A_c^T A_c
+  double* zb = nullptr;            // [B][n] A_r^T Y A_c (b values of every atom)
+  double* sep_scratch = nullptr;   // [B][nc][mr] U = R A_c  /  V = A_r C
+  double* lpart = nullptr;         // [B][tiles] residual sum-of-squares partials
   // correlation candidates, [B][ntile]
   double* cand_v1 = nullptr;
   double* cand_v2 = nullptr;
@@ -110,6 +121,13 @@ void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
                           cudaStream_t s);
 void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
                        cudaStream_t s);
+// ---- launchers (k_sep.cu) ----
+void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
+                     double* dst, bool abs_scores, cudaStream_t s);
+void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
+                      cudaStream_t s);
+int64_t sep_resid_tiles(const SolveParams& p);
+
 // ---- launchers (k_gram.cu) ----
 void launch_gram_full(const float* at, int64_t n, int64_t ldm, double* g,
                       cudaStream_t s);

@@ -174,4 +174,80 @@ int cl_gen_problem_1d(uint64_t seed, int64_t m, int64_t n, int64_t k,
   return 0;
 }
 
+// dct_basis (sensing.cpp:13-29): orthonormal DCT-II, d[j][k] = c_k cos(pi(2j+1)k/(2n)).
+static void dct(int64_t n, std::vector<double>& d) {
+  d.assign(static_cast<size_t>(n * n), 0.0);
+  const double c0 = std::sqrt(1.0 / static_cast<double>(n));
+  const double ck = std::sqrt(2.0 / static_cast<double>(n));
+  const double base = 3.14159265358979323846 / (2.0 * static_cast<double>(n));
+  for (int64_t j = 0; j < n; ++j) {
+    const double phase = static_cast<double>(2 * j + 1) * base;
+    for (int64_t k = 0; k < n; ++k)
+      d[j * n + k] = (k == 0 ? c0 : ck) * std::cos(phase * static_cast<double>(k));
+  }
+}
+
+// Separable 2D problem (BASELINE configs 4-5):
+//   Phi_r (m_r x n_r), Phi_c (m_c x n_c) i.i.d. normal()/sqrt(m), row-major;
+//   A_r = fp32(Phi_r D_r), A_c = fp32(Phi_c D_c) with D the orthonormal DCT;
+//   per image: k positions of the n_r x n_c coefficient grid by partial
+//   Fisher-Yates, values normal() / (1 + i + j) at frequency (i, j);
+//   Y = A_r S A_c^T in fp64, rounded to fp32.
+// Column-major vec: p = i + n_r j (S), q = qr + m_r qc (Y).
+// Outputs: Ar m_r x n_r, Ac m_c x n_c (fp32 row-major), S (n_r n_c) x B fp64
+// (may be NULL), Y (m_r m_c) x B fp32.
+int cl_gen_problem_2d(uint64_t seed, int64_t n_r, int64_t n_c, int64_t m_r, int64_t m_c,
+                      int64_t k, int64_t batch, float* Ar, float* Ac, double* S, float* Y) {
+  const int64_t N = n_r * n_c, M = m_r * m_c;
+  if (n_r <= 0 || n_c <= 0 || m_r <= 0 || m_c <= 0 || batch <= 0 || k < 0 || k > N) return 3;
+  Rng rng(seed);
+  std::vector<double> phr(static_cast<size_t>(m_r * n_r)), phc(static_cast<size_t>(m_c * n_c));
+  for (auto& e : phr) e = rng.normal() / std::sqrt(static_cast<double>(m_r));
+  for (auto& e : phc) e = rng.normal() / std::sqrt(static_cast<double>(m_c));
+  std::vector<double> dr, dc;
+  dct(n_r, dr);
+  dct(n_c, dc);
+  std::vector<double> ar(static_cast<size_t>(m_r * n_r)), ac(static_cast<size_t>(m_c * n_c));
+  for (int64_t i = 0; i < m_r; ++i)
+    for (int64_t j = 0; j < n_r; ++j) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < n_r; ++t) acc += phr[i * n_r + t] * dr[t * n_r + j];
+      Ar[i * n_r + j] = static_cast<float>(acc);
+      ar[i * n_r + j] = Ar[i * n_r + j];
+    }
+  for (int64_t i = 0; i < m_c; ++i)
+    for (int64_t j = 0; j < n_c; ++j) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < n_c; ++t) acc += phc[i * n_c + t] * dc[t * n_c + j];
+      Ac[i * n_c + j] = static_cast<float>(acc);
+      ac[i * n_c + j] = Ac[i * n_c + j];
+    }
+  if (S) std::memset(S, 0, sizeof(double) * N * batch);
+  std::vector<int64_t> perm(static_cast<size_t>(N));
+  std::vector<double> v(static_cast<size_t>(m_r * n_c));
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t p = 0; p < N; ++p) perm[p] = p;
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t r = q + static_cast<int64_t>(rng.uniform_below(static_cast<uint64_t>(N - q)));
+      const int64_t tmp = perm[q];
+      perm[q] = perm[r];
+      perm[r] = tmp;
+    }
+    std::fill(v.begin(), v.end(), 0.0);  // V = A_r S  (m_r x n_c)
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t p = perm[q], i = p % n_r, j = p / n_r;
+      const double val = rng.normal() / (1.0 + static_cast<double>(i + j));
+      if (S) S[p * batch + b] = val;
+      for (int64_t qr = 0; qr < m_r; ++qr) v[qr * n_c + j] += ar[qr * n_r + i] * val;
+    }
+    for (int64_t qc = 0; qc < m_c; ++qc)
+      for (int64_t qr = 0; qr < m_r; ++qr) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < n_c; ++j) acc += v[qr * n_c + j] * ac[qc * n_c + j];
+        Y[(qr + m_r * qc) * batch + b] = static_cast<float>(acc);
+      }
+  }
+  return 0;
+}
+
 }  // extern "C"

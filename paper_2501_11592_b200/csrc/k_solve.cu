@@ -616,6 +616,27 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
   const int64_t cap = p.cap, ldm = p.ldm;
   double* G = w.gram + b * cap * cap;
   const double* y = w.y64 + b * ldm;
+  if (p.sep) {
+    // Separable atoms: G[(i,j),(i',j')] = Gr[i][i'] * Gc[j][j']; b_k = Z[p_k]
+    // with Z = A_r^T Y A_c (fp64, once per solve).
+    for (int k = t0; k < t; ++k) {
+      const int64_t pk = sups[k], ik = pk % p.nr, jk = pk / p.nr;
+      if (lane <= k) {
+        const int64_t pl = sups[lane], il = pl % p.nr, jl = pl / p.nr;
+        const double v = w.gr[ik * p.nr + il] * w.gc[jk * p.nc + jl];
+        G[(int64_t)k * cap + lane] = v;
+        G[(int64_t)lane * cap + k] = v;
+      }
+      if (lane == 0) {
+        w.bvec[b * cap + k] = w.zb[b * p.n + pk];
+        w.coef[b * cap + k] = 0.0;
+        w.mom1[b * cap + k] = 0.0;
+        w.mom2[b * cap + k] = 0.0;
+      }
+    }
+    __syncwarp();
+    return;
+  }
   if (w.gfull) {
     // Gather from the context's A^T A; b_k = a_k . y on demand.
     for (int k = t0; k < t; ++k) {
@@ -927,7 +948,7 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
 // when it fits, else it is streamed from L2 every epoch (symmetric G is read
 // column-wise so the threads of a warp touch consecutive addresses).
 constexpr int kBlockThreads = 256;
-constexpr int kBlockRows = 4;
+constexpr int kBlockRows = 8;
 
 template <int OPT, bool SMEM_G>
 __global__ void __launch_bounds__(kBlockThreads)
@@ -953,7 +974,23 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     // Gram extension: gathered from the context's A^T A when present, else
     // warps over (k, i) pairs with lanes over m.
     for (int k = t0; k < t; ++k) {
-      const float* ak = w.at32 + (int64_t)sups[k] * p.ldm;
+      if (p.sep) {
+        // Separable atoms: G[(i,j),(i',j')] = Gr[i][i'] * Gc[j][j'], b from Z.
+        const int64_t pk = sups[k], ik = pk % p.nr, jk = pk / p.nr;
+        for (int i = tid; i <= k; i += kBlockThreads) {
+          const int64_t pi = sups[i], ii = pi % p.nr, ji = pi / p.nr;
+          const double v = w.gr[ik * p.nr + ii] * w.gc[jk * p.nc + ji];
+          G[(int64_t)k * cap + i] = v;
+          G[(int64_t)i * cap + k] = v;
+        }
+        if (tid == 0) {
+          w.bvec[b * cap + k] = w.zb[b * p.n + pk];
+          w.coef[b * cap + k] = 0.0;
+          w.mom1[b * cap + k] = 0.0;
+          w.mom2[b * cap + k] = 0.0;
+        }
+        continue;
+      }
       if (w.gfull) {
         for (int i = tid; i <= k; i += kBlockThreads) {
           const double v = w.gfull[(int64_t)sups[k] * p.n + sups[i]];
@@ -1053,6 +1090,11 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
         w.mom2[b * cap + i] = m2[q];
       }
     }
+    if (p.sep) {  // the separable residual pipeline (k_sep.cu) takes over
+      for (int i = tid; i < t; i += kBlockThreads) w.coef[b * cap + i] = cs[i];
+      __syncthreads();
+      continue;
+    }
     // Residual + loss.
     double lacc = 0.0;
     for (int64_t i = tid; i < p.ldm; i += kBlockThreads) {
@@ -1079,6 +1121,24 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     if (snap_s)
       for (int i = tid; i < t; i += kBlockThreads) w.best_coef[b * cap + i] = cs[i];
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ separable mode
+// Loss of the separable residual (tile partials in fixed order) and the
+// per-signal stopping rules; the snapshot copies the learned coefficients.
+__global__ void k_sep_control(SolveParams p, Work w, int outer, int64_t tiles) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= p.B || !w.active[b]) return;
+  double L = 0.0;
+  for (int64_t t = 0; t < tiles; ++t) L += w.lpart[b * tiles + t];
+  if (p.mode == kModePerSignal) {
+    if (control_signal(p, w, b, outer, L)) {
+      const int t = w.cnt[b];
+      for (int k = 0; k < t; ++k) w.best_coef[b * p.cap + k] = w.coef[b * p.cap + k];
+    }
+  } else {
+    w.loss[b] = L;
   }
 }
 
@@ -1307,7 +1367,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
       default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
     }
-    k_resid<TB><<<(unsigned)p.B, 32 * kResidWarps, 0, s>>>(p, w, outer);
+    if (!p.sep) k_resid<TB><<<(unsigned)p.B, 32 * kResidWarps, 0, s>>>(p, w, outer);
   };
   if (max_cnt <= 8)
     learn(std::integral_constant<int, 8>());
@@ -1347,6 +1407,11 @@ void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
   k_finalize<<<(unsigned)blocks, 256, 0, s>>>(p, w, out_cap, sup_out, coef_out,
                                              cnt_out, iters_out, rn_out,
                                              conv_out, status_out);
+}
+
+void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
+  const int64_t blocks = (p.B + 127) / 128;
+  k_sep_control<<<(unsigned)blocks, 128, 0, s>>>(p, w, outer, sep_resid_tiles(p));
 }
 
 void launch_inject_finish(const SolveParams& p, const Work& w,

@@ -58,9 +58,9 @@ def main():
     arrays = {}
     cases = []
 
-    def add_solve(name, A, Y, cfg, api):
+    def add_solve(name, A, Y, cfg, api, round_a=True):
         """api: 'batch' (clomp_solve_batch) or 'single' (clomp_solve per column)."""
-        A = f32(A)
+        A = f32(A) if round_a else np.asarray(A, np.float64)
         Y = f32(Y)
         if Y.ndim == 1:
             Y = Y.reshape(-1, 1)
@@ -146,6 +146,23 @@ def main():
     A1, X1, Y1, _ = cl.gen_problem_1d(c1["seed"], c1["m"], c1["n"], c1["k"], 1)
     add_solve("cfg1_full", A1, Y1, base(c1["k"]), "single")
     arrays["cfg1_full/X"] = X1
+    # Separable 2D operator (north-star 2D mode): the reference
+    # has no separable mode, so its semantics are clomp_solve on the explicit
+    # Kronecker matrix A = A_c (x) A_r (column-major vec), built here with
+    # np.kron (fp64 products of the fp32 factors).
+    for name, (nr, nc, mr, mc, kk, B), cfg, api in [
+        ("sep_small_single", (12, 10, 6, 8, 5, 3), base(6), "single"),
+        ("sep_small_joint_adam", (10, 8, 6, 5, 4, 2),
+         ClompConfig(max_outer=8, lr=0.02, w_tv=0.0, w_lv=0.0), "batch"),
+    ]:
+        Ar, Ac, S2, Y2 = cl.gen_problem_2d(100 + nr, nr, nc, mr, mc, kk, B)
+        Kr = np.kron(Ac.astype(np.float64), Ar.astype(np.float64))
+        add_solve(name, Kr, Y2, cfg, api, round_a=False)
+        cases[-1]["kind"] = "sep"
+        arrays[f"{name}/Ar"] = Ar
+        arrays[f"{name}/Ac"] = Ac
+        arrays[f"{name}/S"] = S2
+        del arrays[f"{name}/A"]
     # config validation (test_clomp.cpp:328-343)
     add_solve("bad_th", A, Y[:, :1], ClompConfig(th=0.0), "batch")
     add_solve("bad_inner", A, Y[:, :1], ClompConfig(inner_steps=0), "batch")

@@ -42,6 +42,9 @@ def oracle() -> C.CDLL:
         vp, i64 = C.c_void_p, C.c_int64
         h.orc_clomp_solve_batch.argtypes = [vp, i64, i64, vp, i64, C.POINTER(CConfig), C.c_int,
                                             C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_char_p, C.c_int]
+        h.orc_clomp_solve_sep.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, C.POINTER(CConfig),
+                                          C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp,
+                                          C.c_char_p, C.c_int]
         h.orc_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, C.c_int, vp]
         h.orc_clomp_loss.argtypes = [vp, i64, i64, vp, i64, vp, vp, C.POINTER(CConfig), C.c_int, vp, vp]
         h.orc_gradient_step.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(CConfig)]
@@ -91,6 +94,30 @@ def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False
                                           _p(mk), _p(it), _p(rn), _p(cv), _p(st), _p(tr), err, 256)
     return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
                 final_residual_norm=rn, converged=cv.astype(bool), status=st, trace=tr)
+
+
+def orc_solve_sep(Ar, Ac, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2):
+    """Oracle restatement with the separable operator A = A_c (x) A_r."""
+    Ar = np.ascontiguousarray(Ar, np.float64)
+    Ac = np.ascontiguousarray(Ac, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    if Y.ndim == 1:
+        Y = Y.reshape(-1, 1)
+    n = Ar.shape[1] * Ac.shape[1]
+    B = Y.shape[1]
+    s = np.zeros((n, B))
+    mk = np.zeros((n, B), np.uint8)
+    it = np.zeros(B, np.int64)
+    rn = np.zeros(B)
+    cv = np.zeros(B, np.uint8)
+    st = np.zeros(B, np.int32)
+    err = C.create_string_buffer(256)
+    c = cfg.to_c()
+    code = oracle().orc_clomp_solve_sep(_p(Ar), Ar.shape[0], Ar.shape[1], _p(Ac), Ac.shape[0],
+                                        Ac.shape[1], _p(Y), B, C.byref(c), isa, mode, _p(s), _p(mk),
+                                        _p(it), _p(rn), _p(cv), _p(st), None, err, 256)
+    return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
+                final_residual_norm=rn, converged=cv.astype(bool), status=st)
 
 
 def ref_solve_batch(A, Y, cfg: ClompConfig):
