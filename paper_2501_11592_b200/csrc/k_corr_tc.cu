@@ -32,8 +32,12 @@ namespace {
 
 constexpr int TM = 128;  // signals per tile  (UMMA M, TMEM lanes)
 constexpr int TN = 256;  // atoms per tile    (UMMA N, TMEM columns)
-constexpr int BK = 32;   // fp32 K elements per stage: one 128-byte swizzle row
-constexpr int STAGES = 2;
+// K slice per pipeline stage: 16 fp32 = one 64-byte swizzle row, so a stage
+// (R hi/lo + A hi/lo) is 48 KB and four stages fit beside the epilogue.
+constexpr int BK = 16;
+constexpr int STAGES = 4;
+constexpr int ROW_BYTES = BK * 4;             // bytes per operand row in smem
+constexpr uint64_t kSwizzleMode = 4;          // UMMA layout type: SWIZZLE_64B
 constexpr int R_BYTES = TM * BK * 4;  // 16 KB
 constexpr int A_BYTES = TN * BK * 4;  // 32 KB
 constexpr int STAGE_BYTES = 2 * R_BYTES + 2 * A_BYTES;
@@ -77,15 +81,37 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
-// 1024 bytes apart (SBO), version 1 (sm_100).
+// Multicast variant: the box lands at the same smem offset in every CTA of
+// `mask` and completes `bytes` on each destination CTA's mbarrier.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, ROW_BYTES swizzle, 8-row groups
+// 8 * ROW_BYTES apart (SBO), version 1 (sm_100).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
-  d |= (uint64_t)1 << 46;            // descriptor version
-  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((8 * ROW_BYTES) >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;                        // descriptor version
+  d |= kSwizzleMode << 61;                       // swizzle mode
   return d;
 }
 
@@ -105,6 +131,14 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -133,6 +167,11 @@ __device__ __forceinline__ void tmem_ld_32(uint32_t taddr, float (&v)[32]) {
 }
 
 // ---------------------------------------------------------------- the kernel
+// CL: CTAs per cluster along the signal dimension.  With CL > 1 the atom tile
+// (the operand every CTA of the cluster shares) is fetched once per cluster:
+// CTA r loads rows [r*TN/CL, (r+1)*TN/CL) of A_hi/A_lo and multicasts them, and
+// a stage is refilled only after all CL MMA issuers released it.
+template <int CL>
 __global__ void __launch_bounds__(128, 1)
 k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
           const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
@@ -151,18 +190,20 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   const int64_t m0 = (int64_t)blockIdx.y * TM;  // first signal
   const int64_t n0 = (int64_t)blockIdx.x * TN;  // first atom
 
-  // Whole tile finished?  (uniform per CTA)
-  int mine = 0;
-  {
+  // Whole tile finished?  (uniform per CTA; a cluster must stay together)
+  if (CL == 1) {
+    int mine = 0;
     const int64_t b = m0 + threadIdx.x;
     mine = (b < B) ? active[b] : 0;
+    if (!__syncthreads_or(mine)) return;
   }
-  if (!__syncthreads_or(mine)) return;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     mbar_init(accum, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -179,6 +220,7 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CL > 1) cluster_sync();  // peers' barriers exist before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -193,8 +235,16 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
       const int k0 = kb * BK;
       tma_load_2d(st, &tm_rhi, &full[s], k0, (int)m0);
       tma_load_2d(st + R_BYTES, &tm_rlo, &full[s], k0, (int)m0);
-      tma_load_2d(st + 2 * R_BYTES, &tm_ahi, &full[s], k0, (int)n0);
-      tma_load_2d(st + 2 * R_BYTES + A_BYTES, &tm_alo, &full[s], k0, (int)n0);
+      if (CL == 1) {
+        tma_load_2d(st + 2 * R_BYTES, &tm_ahi, &full[s], k0, (int)n0);
+        tma_load_2d(st + 2 * R_BYTES + A_BYTES, &tm_alo, &full[s], k0, (int)n0);
+      } else {
+        constexpr int rows = TN / CL;
+        const uint32_t off = crank * rows * BK * 4;
+        const int a_row = (int)n0 + (int)crank * rows;
+        tma_load_2d_mc(st + 2 * R_BYTES + off, &tm_ahi, &full[s], k0, a_row, kMask);
+        tma_load_2d_mc(st + 2 * R_BYTES + A_BYTES + off, &tm_alo, &full[s], k0, a_row, kMask);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (one thread for the CTA)
@@ -215,7 +265,14 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
         mma_tf32(tmem, d_rlo + adv, d_ahi + adv, 1);
         mma_tf32(tmem, d_rhi + adv, d_ahi + adv, 1);
       }
-      mma_commit(&empty[s]);  // stage free once these MMAs retire
+      // Stage free once these MMAs retire (in every CTA of the cluster that
+      // multicasts into it).  The last STAGES releases are never waited for.
+      if (kb < kblocks - STAGES) {
+        if (CL == 1)
+          mma_commit(&empty[s]);
+        else
+          mma_commit_mc(&empty[s], kMask);
+      }
     }
     mma_commit(accum);        // accumulator complete
   }
@@ -258,6 +315,7 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still write into it
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
@@ -306,7 +364,8 @@ bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ld, int
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            ROW_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -314,16 +373,21 @@ bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ld, int
 struct MapCache {
   const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t rows[4] = {0, 0, 0, 0};
+  int box[4] = {0, 0, 0, 0};
+  int64_t ld[4] = {0, 0, 0, 0};
   CUtensorMap map[4];
 };
 thread_local MapCache g_maps;
 
 const CUtensorMap* cached_map(int slot, const float* base, int64_t rows, int64_t ld,
                               int box_rows) {
-  if (g_maps.key[slot] != base || g_maps.rows[slot] != rows) {
+  if (g_maps.key[slot] != base || g_maps.rows[slot] != rows || g_maps.box[slot] != box_rows ||
+      g_maps.ld[slot] != ld) {
     if (!make_map(&g_maps.map[slot], base, rows, ld, box_rows)) return nullptr;
     g_maps.key[slot] = base;
     g_maps.rows[slot] = rows;
+    g_maps.box[slot] = box_rows;
+    g_maps.ld[slot] = ld;
   }
   return &g_maps.map[slot];
 }
@@ -346,19 +410,45 @@ bool corr_tc_available() {
 
 int64_t corr_tc_tile_atoms() { return TN; }
 
+constexpr int kCluster = 4;
+
 static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_dbg,
                            cudaStream_t s) {
+  const int64_t mtiles = (p.B + TM - 1) / TM;
+  const bool clustered = mtiles >= kCluster;
+  const int arows = clustered ? TN / kCluster : TN;
   const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
   const CUtensorMap* rlo = cached_map(1, w.r_lo, p.B, p.ldm, TM);
-  const CUtensorMap* ahi = cached_map(2, w.at_hi, p.n, p.ldm, TN);
-  const CUtensorMap* alo = cached_map(3, w.at_lo, p.n, p.ldm, TN);
+  const CUtensorMap* ahi = cached_map(2, w.at_hi, p.n, p.ldm, arows);
+  const CUtensorMap* alo = cached_map(3, w.at_lo, p.n, p.ldm, arows);
   if (!rhi || !rlo || !ahi || !alo) return false;
-  cudaFuncSetAttribute(k_corr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  dim3 grid((unsigned)((p.n + TN - 1) / TN), (unsigned)((p.B + TM - 1) / TM));
-  k_corr_tc<<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n, p.B,
-                                          (int)(p.ldm / BK), p.ntile, w.active, w.cand_v1,
-                                          w.cand_v2, w.cand_i1, scores_dbg);
-  return true;
+  const int kblocks = (int)(p.ldm / BK);
+  if (!clustered) {
+    cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    dim3 grid((unsigned)((p.n + TN - 1) / TN), (unsigned)mtiles);
+    k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n, p.B, kblocks, p.ntile,
+                                               w.active, w.cand_v1, w.cand_v2, w.cand_i1,
+                                               scores_dbg);
+    return true;
+  }
+  cudaFuncSetAttribute(k_corr_tc<kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       SMEM_BYTES);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)((p.n + TN - 1) / TN),
+                     (unsigned)((mtiles + kCluster - 1) / kCluster * kCluster));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = kCluster;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n, p.B, kblocks,
+                            p.ntile, w.active, w.cand_v1, w.cand_v2, w.cand_i1,
+                            scores_dbg) == cudaSuccess;
 }
 
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {

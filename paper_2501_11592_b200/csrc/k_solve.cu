@@ -511,12 +511,14 @@ __device__ __forceinline__ void square_row(double (&res)[TB], const double* src,
   }
 }
 
+// Write the lane's row of a symmetric T x T matrix as its column: for fixed j
+// the lanes hit consecutive words (conflict-free), and by symmetry the stored
+// matrix is the same.
 template <int T, int TB>
 __device__ __forceinline__ void store_rows(const double (&g)[TB], double* dst, int lane) {
   if (lane < T) {
 #pragma unroll
-    for (int j = 0; j < T; j += 2)
-      *reinterpret_cast<double2*>(dst + lane * T + j) = make_double2(g[j], g[j + 1]);
+    for (int j = 0; j < T; ++j) dst[j * T + lane] = g[j];
   }
 }
 
