@@ -164,7 +164,7 @@ typedef struct cl_stats {
   double corr_ms;               /* device time of the correlation kernels   */
   double learn_ms;              /* device time of the learning kernels      */
   double total_ms;              /* device time of the whole solve           */
-  int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32            */
+  int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32, 2 fused   */
   int32_t pad0;
   double e2e_ms;                /* cl_solve_batch: H2D + solve + D2H, events */
   double select_ms;             /* device time of select + fp64 rescans     */
@@ -181,6 +181,10 @@ int cl_set_corr_path(cl_ctx* ctx, int path);
  * 1 = build, 0 = drop, -1 = auto (built by cl_create when n*n*8 <= min(8 GiB,
  * free/4)). */
 int cl_set_gram_cache(cl_ctx* ctx, int mode);
+/* Small problems (n*m <= 4M words, supports <= 32 atoms, per-signal
+ * semantics) run the whole solve in one persistent block per signal; 0
+ * forces the batched kernel pipeline instead (tests compare the two). */
+int cl_set_fused(cl_ctx* ctx, int on);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);
 /* Run this context's work on a caller-owned cudaStream_t (NULL restores the

@@ -146,7 +146,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused",
     "cl_gen_problem_2d",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
@@ -179,6 +179,7 @@ def lib() -> C.CDLL:
         h.cl_set_stream.argtypes = [vp, vp]
         h.cl_debug_scores.argtypes = [vp, vp, i64, i32, vp]
         h.cl_set_gram_cache.argtypes = [vp, i32]
+        h.cl_set_fused.argtypes = [vp, i32]
         h.cl_create_sep.restype = vp
         h.cl_create_sep.argtypes = [i32, vp, i64, i64, vp, i64, i64, i32, C.POINTER(C.c_int)]
         h.cl_gen_problem_2d.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]
@@ -324,6 +325,10 @@ class ClompContext:
     def set_gram_cache(self, mode: int):
         """1 build / 0 drop / -1 auto the fp64 A^T A cache."""
         _raise(lib().cl_set_gram_cache(self._h, int(mode)), self._h)
+
+    def set_fused(self, on: bool):
+        """Allow (default) or forbid the one-block-per-signal latency path."""
+        _raise(lib().cl_set_fused(self._h, int(bool(on))), self._h)
 
     def set_profiling(self, on: bool):
         _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)

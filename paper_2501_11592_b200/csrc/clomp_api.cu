@@ -96,6 +96,7 @@ struct cl_ctx {
   GraphKey gkey;
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
+  bool fused_ok = true;  // small problems: one persistent block per signal
   bool profiling = false;
   cl_stats stats{};
   int sms = 148;
@@ -307,9 +308,14 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     return fail(ctx, CL_ERR_UNSUPPORTED,
                 "clomp: support capacity above 2048 atoms per signal is not "
                 "supported (lower max_outer, or th < 1 with n > 2048)");
+  // Latency path: the whole solve in one persistent block per signal when the
+  // dictionary is small (config 1) and supports stay register-resident.
+  const bool fused = ctx->fused_ok && !ctx->sep && (mode == CL_MODE_PER_SIGNAL || B == 1) &&
+                     cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
+                     B <= 4 * (int64_t)ctx->sms;
   const int64_t tile_atoms = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
-  int st = ensure_workspace(ctx, B, cap, full_scores, tensor, ntile);
+  int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile);
   if (st) return st;
   st = ensure_adam_tables(ctx, c);
   if (st) return st;
@@ -331,7 +337,9 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.opt = c->opt;
   p.inner = (int32_t)c->inner_steps;
   p.max_outer = (int32_t)c->max_outer;
-  p.mode = mode;
+  // A one-column joint solve is exactly clomp_solve (clomp.cpp:294-311), so
+  // the fused path runs everything with per-signal state.
+  p.mode = fused ? CL_MODE_PER_SIGNAL : mode;
   p.bc1 = ctx->bc;
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
   p.delta_rel = delta_for(tensor, ctx->ldm);
@@ -395,11 +403,27 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     launch_sep_corr(p, w, w.y64, w.zb, false, s);
     launches += 2;
   }
-  if (mode == CL_MODE_JOINT) {
+  if (p.mode == CL_MODE_JOINT) {
     launch_joint_control(p, w, 0, true, s);
     ++launches;
   }
   int outer_done = 0;
+  if (fused) {
+    launch_solve_fused(p, w, s);
+    launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
+                    out.conv, out.status, s);
+    launches += 2;
+    CL_CUDA(ctx, cudaGetLastError());
+    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+    CL_CUDA(ctx, cudaStreamSynchronize(s));
+    stats.kernel_launches = launches;
+    stats.rescans = 0;
+    stats.outer_iterations = p.max_outer;
+    stats.corr_path = 2;
+    ctx->stats = stats;
+    return CL_OK;
+  }
   if (ctx->profiling) {
     // Per-phase CUDA-event timing: one iteration at a time, synchronised.
     cudaEvent_t ev[5];
@@ -832,6 +856,12 @@ int cl_set_stream(cl_ctx* ctx, void* stream) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return CL_OK;
+}
+
+int cl_set_fused(cl_ctx* ctx, int on) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  ctx->fused_ok = on != 0;
   return CL_OK;
 }
 

@@ -164,6 +164,8 @@ void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
                      int32_t* sup_out, double* coef_out, int32_t* cnt_out,
                      int32_t* iters_out, double* rn_out, uint8_t* conv_out,
                      int32_t* status_out, cudaStream_t s);
+// Whole per-signal solve in one persistent block per signal (small problems).
+void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);
 // inject_support unit path: residual already in w.r64 (and split), mask in
 // w.maskbits; appends nothing to the learning state.
 void launch_inject_finish(const SolveParams& p, const Work& w, cudaStream_t s);

@@ -1126,6 +1126,109 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
   }
 }
 
+// ------------------------------------------------------ fused small solve
+// Whole clomp_solve (clomp.cpp:294-311, i.e. clomp_solve_batch on one column)
+// in one persistent block per signal for small dictionaries (config 1 and
+// other latency-bound cases): exact fp64 correlation of every atom (warps over
+// atoms, lanes over measurements), the inject_from_scores rule with ties, the
+// warp learning routine of the batched path, the fp64 residual and the
+// stopping rules, with no kernel boundary between outer iterations.
+constexpr int kFusedThreads = 256;
+
+template <int OPT>
+__global__ void __launch_bounds__(kFusedThreads)
+k_solve_fused(SolveParams p, Work w) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  double* rs = reinterpret_cast<double*>(fsm);                 // [ldm] residual
+  __shared__ __align__(16) double cs[2 * kWarpCap];
+  __shared__ int32_t sups[kWarpCap];
+  __shared__ __align__(16) double sq[kWarpCap * kWarpCap];
+  __shared__ double red[kFusedThreads / 32];
+  __shared__ int s_active;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = kFusedThreads / 32;
+  const int64_t b = blockIdx.x;
+  if (!w.active[b]) return;
+  for (int64_t i = tid; i < p.ldm; i += kFusedThreads) rs[i] = w.r64[b * p.ldm + i];
+  __syncthreads();
+  double* sc = w.scores + b * p.n;
+  for (int outer = 1; outer <= p.max_outer; ++outer) {
+    // K1: exact fp64 scores |a_j . r|, 8 atoms per warp pass (8 independent
+    // dot products keep enough loads in flight to hide L2 latency).
+    double cmax = 0.0;
+    for (int64_t j0 = warp * 8; j0 < p.n; j0 += nw * 8) {
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+      for (int64_t i = 2 * lane; i < p.ldm; i += 64) {
+        const double2 r01 = *reinterpret_cast<const double2*>(rs + i);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (j0 + u < p.n) {
+            const double2 a = *reinterpret_cast<const double2*>(w.at64 + (j0 + u) * p.ldm + i);
+            acc[u] = fma(a.x, r01.x, acc[u]);
+            acc[u] = fma(a.y, r01.y, acc[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double v = fabs(warp_sum(acc[u]));
+        if (j0 + u < p.n) {
+          if (lane == 0) sc[j0 + u] = v;
+          cmax = fmax(cmax, v);
+        }
+      }
+    }
+    if (lane == 0) red[warp] = cmax;
+    __syncthreads();
+    // K1c: inject_from_scores (clomp.cpp:41-53), ties included; K2 learning.
+    if (warp == 0) {
+      double m = 0.0;
+      for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
+      if (lane == 0) w.changed[b] = 0;
+      if (m > 0.0)
+        warp_threshold_append(p, w, b, p.th * m, [&](int64_t j) { return sc[j]; }, lane);
+      __syncwarp();
+      if (w.active[b] && w.cnt[b] <= kWarpCap)
+        learn_warp_body<kWarpCap, OPT>(p, w, b, outer, cs, sups, sq, nullptr, lane);
+      else if (lane == 0 && w.active[b])
+        w.status[b] = 7, w.active[b] = 0;  // capacity: larger supports use the batched path
+    }
+    __syncthreads();
+    if (!w.active[b]) break;
+    // residual r = A_S c - y (fp64) and the stopping rules
+    const int t = w.cnt[b];
+    if (tid < t) {
+      cs[tid] = w.coef[b * p.cap + tid];
+      sups[tid] = w.sup[b * p.cap + tid];
+    }
+    __syncthreads();
+    double lacc = 0.0;
+    for (int64_t i = tid; i < p.ldm; i += kFusedThreads) {
+      double acc = 0.0;
+      for (int k = 0; k < t; ++k) acc = fma(w.at64[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
+      const double rv = acc - w.y64[b * p.ldm + i];
+      rs[i] = rv;
+      lacc = fma(rv, rv, lacc);
+    }
+    lacc = warp_sum(lacc);
+    if (lane == 0) red[warp] = lacc;
+    __syncthreads();
+    if (tid == 0) {
+      double L = 0.0;
+      for (int q = 0; q < nw; ++q) L += red[q];
+      s_active = 0;
+      if (control_signal(p, w, b, outer, L)) {
+        for (int k = 0; k < t; ++k) w.best_coef[b * p.cap + k] = cs[k];
+      }
+      s_active = w.active[b];
+    }
+    __syncthreads();
+    if (!s_active) break;
+  }
+}
+
 // ------------------------------------------------------ separable mode
 // Loss of the separable residual (tile partials in fixed order) and the
 // per-signal stopping rules; the snapshot copies the learned coefficients.
@@ -1414,6 +1517,20 @@ void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
 void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
   const int64_t blocks = (p.B + 127) / 128;
   k_sep_control<<<(unsigned)blocks, 128, 0, s>>>(p, w, outer, sep_resid_tiles(p));
+}
+
+void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s) {
+  const size_t smem = (size_t)p.ldm * 8;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w);
+  };
+  switch (p.opt) {
+    case 0: go(k_solve_fused<0>); break;
+    case 1: go(k_solve_fused<1>); break;
+    default: go(k_solve_fused<2>); break;
+  }
 }
 
 void launch_inject_finish(const SolveParams& p, const Work& w,

@@ -35,15 +35,20 @@ def snr_db(x, xh):
     return np.inf if e == 0 else 10 * np.log10(np.sum(x ** 2) / e)
 
 
-@pytest.fixture(scope="module", params=["f64", "auto"])
+@pytest.fixture(scope="module", params=["f64", "tc", "auto"])
 def corr_path(request, gpu_available):
     return request.param
 
 
 def make_ctx(A, path="auto"):
+    """path: 'f64' batched pipeline with fp64 SIMT correlation, 'tc' batched
+    pipeline with the tcgen05 correlation, 'auto' library choice (the fused
+    one-block-per-signal solve for small per-signal problems)."""
     ctx = cl.ClompContext(np.asarray(A, np.float32))
     if path == "f64":
         ctx.set_corr_path(1)
+    if path in ("f64", "tc"):
+        ctx.set_fused(False)
     return ctx
 
 
