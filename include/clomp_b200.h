@@ -117,6 +117,24 @@ cl_ctx* cl_create_sep(int device, const float* a_r, int64_t m_r, int64_t n_r,
                       const float* a_c, int64_t m_c, int64_t n_c, int layout,
                       int* status);
 
+/* Column-sharded dictionary over `world` GPUs (one process per GPU, SURVEY.md
+ * §8e): every rank passes the whole dictionary and the same batch; rank r runs
+ * the correlation GEMM on atoms [r n/world, (r+1) n/world) for all signals and
+ * learns signals [r B/world, (r+1) B/world).  Per outer iteration the ranks
+ * exchange the per-(signal, atom tile) correlation candidates and the new
+ * residual rows with ncclAllGather and sum the active-signal count with
+ * ncclAllReduce; every rank returns the results of the whole batch.
+ * Per-signal mode with th = 1; n divisible by world * 256.  nccl_id: the
+ * 128-byte ncclUniqueId from cl_nccl_unique_id on rank 0, shared by the caller
+ * (e.g. torch.distributed.broadcast_object_list).  world == 1 needs no id. */
+int cl_nccl_unique_id(void* id_out);
+cl_ctx* cl_create_colshard(int device, const float* a, int64_t m, int64_t n,
+                           int a_layout, int rank, int world,
+                           const void* nccl_id, int* status);
+/* Test hook: run the column-sharded algorithm with `shards` virtual shards on
+ * this one GPU (the exchange is a local copy instead of NCCL). */
+int cl_set_virtual_shards(cl_ctx* ctx, int shards);
+
 /* Message of the last failing call on ctx (or of the last failing cl_create
  * on this thread when ctx is NULL). */
 const char* cl_last_error(const cl_ctx* ctx);

@@ -147,6 +147,7 @@ EXPORTED = [
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
     "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused",
+    "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
     "cl_gen_problem_2d",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
@@ -180,6 +181,10 @@ def lib() -> C.CDLL:
         h.cl_debug_scores.argtypes = [vp, vp, i64, i32, vp]
         h.cl_set_gram_cache.argtypes = [vp, i32]
         h.cl_set_fused.argtypes = [vp, i32]
+        h.cl_nccl_unique_id.argtypes = [vp]
+        h.cl_create_colshard.restype = vp
+        h.cl_create_colshard.argtypes = [i32, vp, i64, i64, i32, i32, i32, vp, C.POINTER(C.c_int)]
+        h.cl_set_virtual_shards.argtypes = [vp, i32]
         h.cl_create_sep.restype = vp
         h.cl_create_sep.argtypes = [i32, vp, i64, i64, vp, i64, i64, i32, C.POINTER(C.c_int)]
         h.cl_gen_problem_2d.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]
@@ -304,6 +309,27 @@ class ClompContext:
         self.shape2d = (ar.shape, ac.shape)
         return self
 
+    @classmethod
+    def colshard(cls, a, rank: int, world: int, nccl_id: bytes | None,
+                 device: int = 0) -> "ClompContext":
+        """Column-sharded dictionary over `world` GPUs (cl_create_colshard)."""
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        self = cls.__new__(cls)
+        self.m, self.n = a.shape
+        st = C.c_int(0)
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id else None
+        h = lib().cl_create_colshard(int(device), _ptr(a), self.m, self.n, LAYOUT_REF, int(rank),
+                                     int(world), idbuf, C.byref(st))
+        if not h:
+            _raise(st.value or CL_ERR_CUDA, None)
+        self._h = h
+        self.device = device
+        return self
+
+    def set_virtual_shards(self, shards: int):
+        """Emulate `shards` column shards on this GPU (tests the sharded math)."""
+        _raise(lib().cl_set_virtual_shards(self._h, int(shards)), self._h)
+
     @property
     def handle(self):
         return self._h
@@ -350,6 +376,13 @@ class ClompContext:
         s = CStats()
         _raise(lib().cl_get_stats(self._h, C.byref(s)), self._h)
         return {f: getattr(s, f) for f, _ in CStats._fields_ if f != "pad0"}
+
+
+def nccl_unique_id() -> bytes:
+    """ncclUniqueId (128 bytes) for cl_create_colshard, created on rank 0."""
+    buf = C.create_string_buffer(128)
+    _raise(lib().cl_nccl_unique_id(buf), None)
+    return buf.raw
 
 
 def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,

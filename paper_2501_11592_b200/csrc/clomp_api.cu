@@ -97,6 +97,9 @@ struct cl_ctx {
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool fused_ok = true;  // small problems: one persistent block per signal
+  // column sharding (cl_create_colshard); vshards emulates W shards on one GPU
+  int rank = 0, world = 1, vshards = 1;
+  void* comm = nullptr;
   bool profiling = false;
   cl_stats stats{};
   int sms = 148;
@@ -179,6 +182,11 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
       w.zb = cv.take<double>(B * ctx->n);
       w.sep_scratch = cv.take<double>(B * ctx->nc * ctx->mr);
       w.lpart = cv.take<double>(B * (((ctx->mr + 63) / 64) * ((ctx->mc + 63) / 64)));
+    }
+    if (ctx->world > 1 || ctx->vshards > 1) {
+      w.xg_v1 = cv.take<double>(B * ntile);
+      w.xg_v2 = cv.take<double>(B * ntile);
+      w.xg_i1 = cv.take<int32_t>(B * ntile);
     }
     w.rs_top = cv.take<double>(B);
     w.rs_delta = cv.take<double>(B);
@@ -304,13 +312,27 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   const bool tensor = !ctx->sep && use_tensor_path(ctx, c);
   const bool full_scores = c->th < 1.0 || ctx->sep;
   const int64_t cap = support_cap(ctx, c);
+  const int W = ctx->world > 1 ? ctx->world : ctx->vshards;
+  const bool colshard = W > 1;
+  if (colshard) {
+    const int64_t tile = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
+    if (ctx->sep || c->th < 1.0 || mode != CL_MODE_PER_SIGNAL)
+      return fail(ctx, CL_ERR_UNSUPPORTED,
+                  "column sharding: per-signal mode with th = 1 on 1D dictionaries only");
+    if (ctx->n % (W * tile) != 0)
+      return fail(ctx, CL_ERR_DIMENSION, "column sharding: n must be a multiple of shards x " +
+                                             std::to_string(tile));
+    if (ctx->world > 1 && B % ctx->world != 0)
+      return fail(ctx, CL_ERR_DIMENSION, "column sharding: batch must divide by the world size");
+  }
   if (cap > 2048)
     return fail(ctx, CL_ERR_UNSUPPORTED,
                 "clomp: support capacity above 2048 atoms per signal is not "
                 "supported (lower max_outer, or th < 1 with n > 2048)");
   // Latency path: the whole solve in one persistent block per signal when the
   // dictionary is small (config 1) and supports stay register-resident.
-  const bool fused = ctx->fused_ok && !ctx->sep && (mode == CL_MODE_PER_SIGNAL || B == 1) &&
+  const bool fused = ctx->fused_ok && !ctx->sep && !colshard &&
+                     (mode == CL_MODE_PER_SIGNAL || B == 1) &&
                      cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
                      B <= 4 * (int64_t)ctx->sms;
   const int64_t tile_atoms = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
@@ -328,6 +350,19 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.cap = cap;
   p.ntile = ntile;
   p.tile_atoms = tile_atoms;
+  p.sig_lo = 0;
+  p.sig_hi = B;
+  p.atom0 = 0;
+  p.n_corr = ctx->n;
+  p.ntl = ntile;
+  if (colshard) {
+    p.n_corr = ctx->n / W;
+    p.ntl = p.n_corr / tile_atoms;
+    if (ctx->world > 1) {
+      p.sig_lo = (int64_t)ctx->rank * (B / ctx->world);
+      p.sig_hi = p.sig_lo + B / ctx->world;
+    }
+  }
   p.mwords = (ctx->n + 31) / 32;
   p.th = c->th;
   p.eps = c->eps;
@@ -375,6 +410,46 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         launch_joint_control(p, w, outer, false, s);
         launch_joint_snapshot(p, w, s);
         *launches += 2;
+      }
+      return;
+    }
+    if (colshard) {
+      // K1 per column shard into [W][B][ntl], exchange, then global tiles.
+      const int r0 = ctx->world > 1 ? ctx->rank : 0, r1 = ctx->world > 1 ? ctx->rank + 1 : W;
+      for (int r = r0; r < r1; ++r) {
+        SolveParams pk = p;
+        pk.atom0 = (int64_t)r * p.n_corr;
+        Work wk = w;
+        wk.cand_v1 = w.xg_v1 + (int64_t)r * B * p.ntl;
+        wk.cand_v2 = w.xg_v2 + (int64_t)r * B * p.ntl;
+        wk.cand_i1 = w.xg_i1 + (int64_t)r * B * p.ntl;
+        if (tensor)
+          launch_corr_tc(pk, wk, s);
+        else
+          launch_corr_f64(pk, wk, false, s);
+        ++*launches;
+      }
+      if (ctx->world > 1) {
+        const size_t cnt = (size_t)(B * p.ntl);
+        nccl_allgather_inplace(ctx->comm, w.xg_v1, cnt, 8, ctx->rank, s);
+        nccl_allgather_inplace(ctx->comm, w.xg_v2, cnt, 8, ctx->rank, s);
+        nccl_allgather_inplace(ctx->comm, w.xg_i1, cnt, 4, ctx->rank, s);
+      }
+      launch_cand_exchange(w.xg_v1, w.xg_v2, w.xg_i1, w.cand_v1, w.cand_v2, w.cand_i1, B, p.ntl,
+                           W, p.n_corr, s);
+      launch_select(p, w, false, s);
+      launch_rescan(p, w, rescan_grid, s);
+      launch_learn(p, w, outer, outer, s);
+      *launches += 3 + (cap > 8 ? 3 : 2);
+      if (ctx->world > 1) {
+        const size_t rows = (size_t)((p.sig_hi - p.sig_lo) * p.ldm);
+        if (w.r_hi) {
+          nccl_allgather_inplace(ctx->comm, w.r_hi, rows, 4, ctx->rank, s);
+          nccl_allgather_inplace(ctx->comm, w.r_lo, rows, 4, ctx->rank, s);
+        } else {
+          nccl_allgather_inplace(ctx->comm, w.r64, rows, 8, ctx->rank, s);
+        }
+        nccl_allreduce_sum_i32(ctx->comm, &w.counters[kActiveCount], 1, s);
       }
       return;
     }
@@ -502,7 +577,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     }
     const int nchunks = (p.max_outer + kChunkIters - 1) / kChunkIters;
     if ((int)ctx->graphs.size() < nchunks) ctx->graphs.resize((size_t)nchunks, nullptr);
-    for (int ch = 0; ch < nchunks; ++ch) {
+    for (int ch = 0; ch < nchunks && !colshard; ++ch) {
       if (!ctx->graphs[(size_t)ch]) {
         const int o0 = ch * kChunkIters + 1;
         const int o1 = std::min(p.max_outer, o0 + kChunkIters - 1);
@@ -522,7 +597,16 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     int64_t per_iter = 0;
     enqueue_count(p, c, mode, cap, &per_iter);
     for (int ch = 0; ch < nchunks; ++ch) {
-      CL_CUDA(ctx, cudaGraphLaunch(ctx->graphs[(size_t)ch], s));
+      if (colshard) {  // NCCL inside: enqueue directly (not captured)
+        const int o0 = ch * kChunkIters + 1;
+        const int o1c = std::min(p.max_outer, o0 + kChunkIters - 1);
+        int64_t dummy = 0;
+        for (int o = o0; o <= o1c; ++o) enqueue_iteration(o, &dummy);
+        cudaMemcpyAsync(ctx->h_chunk + (ch & 1) * kNumCounters, w.counters,
+                        kNumCounters * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      } else {
+        CL_CUDA(ctx, cudaGraphLaunch(ctx->graphs[(size_t)ch], s));
+      }
       cudaEventRecord(ctx->chunk_ev[ch & 1], s);
       const int o1 = std::min(p.max_outer, (ch + 1) * kChunkIters);
       launches += per_iter * (o1 - ch * kChunkIters);
@@ -535,6 +619,16 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
                     out.conv, out.status, s);
     ++launches;
+    if (colshard && ctx->world > 1) {  // every rank returns the whole batch
+      const size_t ns = (size_t)(p.sig_hi - p.sig_lo);
+      if (out.sup) nccl_allgather_inplace(ctx->comm, out.sup, ns * out.cap, 4, ctx->rank, s);
+      if (out.coef) nccl_allgather_inplace(ctx->comm, out.coef, ns * out.cap, 8, ctx->rank, s);
+      if (out.cnt) nccl_allgather_inplace(ctx->comm, out.cnt, ns, 4, ctx->rank, s);
+      if (out.iters) nccl_allgather_inplace(ctx->comm, out.iters, ns, 4, ctx->rank, s);
+      if (out.rn) nccl_allgather_inplace(ctx->comm, out.rn, ns, 8, ctx->rank, s);
+      if (out.conv) nccl_allgather_inplace(ctx->comm, out.conv, ns, 1, ctx->rank, s);
+      if (out.status) nccl_allgather_inplace(ctx->comm, out.status, ns, 4, ctx->rank, s);
+    }
     CL_CUDA(ctx, cudaGetLastError());
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, s));
@@ -834,6 +928,7 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->stage);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   if (ctx->h_chunk) cudaFreeHost(ctx->h_chunk);
+  if (ctx->comm) nccl_comm_destroy(ctx->comm);
   for (auto& e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
   for (auto& g : ctx->graphs)
@@ -856,6 +951,44 @@ int cl_set_stream(cl_ctx* ctx, void* stream) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return CL_OK;
+}
+
+int cl_nccl_unique_id(void* id_out) {
+  if (!id_out) return CL_ERR_INTERNAL;
+  return nccl_unique_id(id_out) == 0 ? CL_OK : CL_ERR_CUDA;
+}
+
+cl_ctx* cl_create_colshard(int device, const float* a, int64_t m, int64_t n, int a_layout,
+                           int rank, int world, const void* nccl_id, int* status) {
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) {
+    g_create_error = "cl_create_colshard: bad rank / world / id";
+    if (status) *status = CL_ERR_CONFIG;
+    return nullptr;
+  }
+  cl_ctx* ctx = cl_create(device, a, m, n, a_layout, status);
+  if (!ctx || world == 1) return ctx;
+  std::string err;
+  cudaSetDevice(device);
+  ctx->comm = nccl_comm_init(world, rank, nccl_id, &err);
+  if (!ctx->comm) {
+    cl_destroy(ctx);
+    g_create_error = "cl_create_colshard: " + err;
+    if (status) *status = CL_ERR_CUDA;
+    return nullptr;
+  }
+  ctx->rank = rank;
+  ctx->world = world;
+  return ctx;
+}
+
+int cl_set_virtual_shards(cl_ctx* ctx, int shards) {
+  if (!ctx || shards < 1) return CL_ERR_INTERNAL;
+  if (ctx->world > 1) return fail(ctx, CL_ERR_CONFIG, "context is already column-sharded");
+  ctx->vshards = shards;
+  ctx->wbytes = 0;  // force a fresh workspace carve with the shard buffers
+  cudaFree(ctx->wbuf);
+  ctx->wbuf = nullptr;
   return CL_OK;
 }
 
@@ -1055,6 +1188,11 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   p.cap = n;
   p.ntile = ntile;
   p.tile_atoms = kCorrTileAtoms;
+  p.sig_lo = 0;
+  p.sig_hi = batch;
+  p.atom0 = 0;
+  p.n_corr = n;
+  p.ntl = ntile;
   p.mwords = (n + 31) / 32;
   p.th = th;
   p.delta_rel = delta_for(false, ldm);
@@ -1106,6 +1244,11 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
   p.ldm = ldm;
   p.cap = 1;
   p.ntile = ntile;
+  p.sig_lo = 0;
+  p.sig_hi = batch;
+  p.atom0 = 0;
+  p.n_corr = n;
+  p.ntl = ntile;
   p.mwords = (n + 31) / 32;
   const Work& w = ctx->w;
   std::vector<double> r64((size_t)(batch * ldm), 0.0);

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace clb {
 
 constexpr int kCorrTileAtoms = 64;    // fp64 SIMT correlation tile (atoms)
@@ -23,6 +25,10 @@ constexpr int kWarpCap = 32;          // register-resident learning kernel limit
 struct SolveParams {
   int64_t B, n, m, ldm, cap, ntile;
   int64_t tile_atoms;       // atoms per correlation tile (candidate granularity)
+  // Column-sharded contexts (cl_create_colshard): this rank learns signals
+  // [sig_lo, sig_hi) and correlates atoms [atom0, atom0 + n_corr) for every
+  // signal into ntl local tiles.  Single-GPU: 0, B, 0, n, ntile.
+  int64_t sig_lo, sig_hi, atom0, n_corr, ntl;
   int64_t mwords;           // 32-bit words per signal in the mask bitmap
   double th, eps, lr, stall_tol;
   int32_t stall_patience, opt, inner, max_outer, mode;
@@ -56,6 +62,10 @@ struct Work {
   double* zb = nullptr;            // [B][n] A_r^T Y A_c (b values of every atom)
   double* sep_scratch = nullptr;   // [B][nc][mr] U = R A_c  /  V = A_r C
   double* lpart = nullptr;         // [B][tiles] residual sum-of-squares partials
+  // column sharding: per-shard candidates, [W][B][ntl]
+  double* xg_v1 = nullptr;
+  double* xg_v2 = nullptr;
+  int32_t* xg_i1 = nullptr;
   // correlation candidates, [B][ntile]
   double* cand_v1 = nullptr;
   double* cand_v2 = nullptr;
@@ -164,6 +174,18 @@ void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
                      int32_t* sup_out, double* coef_out, int32_t* cnt_out,
                      int32_t* iters_out, double* rn_out, uint8_t* conv_out,
                      int32_t* status_out, cudaStream_t s);
+// ---- colshard.cu ----
+bool nccl_available();
+int nccl_unique_id(void* out);
+void* nccl_comm_init(int world, int rank, const void* id, std::string* err);
+void nccl_comm_destroy(void* comm);
+bool nccl_allgather_inplace(void* comm, void* buf, size_t count_per_rank, int bytes_per_elem,
+                            int rank, cudaStream_t s);
+bool nccl_allreduce_sum_i32(void* comm, int32_t* buf, size_t count, cudaStream_t s);
+void launch_cand_exchange(const double* g1, const double* g2, const int32_t* gi, double* v1,
+                          double* v2, int32_t* i1, int64_t B, int64_t ntl, int world,
+                          int64_t atoms_per_rank, cudaStream_t s);
+
 // Whole per-signal solve in one persistent block per signal (small problems).
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);
 // inject_support unit path: residual already in w.r64 (and split), mask in

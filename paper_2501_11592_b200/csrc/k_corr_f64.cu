@@ -149,9 +149,12 @@ k_corr_f64(const float* __restrict__ at, const double* __restrict__ r,
 
 void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
                      cudaStream_t s) {
-  dim3 grid((unsigned)((p.n + BM - 1) / BM), (unsigned)((p.B + BN - 1) / BN));
-  k_corr_f64<<<grid, 256, 0, s>>>(w.at32, w.r64, w.active, p.n, p.B, p.ldm,
-                                  p.ntile, w.cand_v1, w.cand_v2, w.cand_i1,
+  // Column shard: atoms [atom0, atom0 + n_corr) into ntl local tiles (the
+  // candidate indices are shifted back to global atom numbers by the caller's
+  // exchange; single-GPU: atom0 = 0, n_corr = n, ntl = ntile).
+  dim3 grid((unsigned)((p.n_corr + BM - 1) / BM), (unsigned)((p.B + BN - 1) / BN));
+  k_corr_f64<<<grid, 256, 0, s>>>(w.at32 + p.atom0 * p.ldm, w.r64, w.active, p.n_corr, p.B,
+                                  p.ldm, p.ntl, w.cand_v1, w.cand_v2, w.cand_i1,
                                   full_scores ? w.scores : nullptr);
 }
 

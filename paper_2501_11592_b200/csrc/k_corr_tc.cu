@@ -419,14 +419,14 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   const int arows = clustered ? TN / kCluster : TN;
   const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
   const CUtensorMap* rlo = cached_map(1, w.r_lo, p.B, p.ldm, TM);
-  const CUtensorMap* ahi = cached_map(2, w.at_hi, p.n, p.ldm, arows);
-  const CUtensorMap* alo = cached_map(3, w.at_lo, p.n, p.ldm, arows);
+  const CUtensorMap* ahi = cached_map(2, w.at_hi + p.atom0 * p.ldm, p.n_corr, p.ldm, arows);
+  const CUtensorMap* alo = cached_map(3, w.at_lo + p.atom0 * p.ldm, p.n_corr, p.ldm, arows);
   if (!rhi || !rlo || !ahi || !alo) return false;
   const int kblocks = (int)(p.ldm / BK);
   if (!clustered) {
     cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    dim3 grid((unsigned)((p.n + TN - 1) / TN), (unsigned)mtiles);
-    k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n, p.B, kblocks, p.ntile,
+    dim3 grid((unsigned)((p.n_corr + TN - 1) / TN), (unsigned)mtiles);
+    k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n_corr, p.B, kblocks, p.ntl,
                                                w.active, w.cand_v1, w.cand_v2, w.cand_i1,
                                                scores_dbg);
     return true;
@@ -434,7 +434,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   cudaFuncSetAttribute(k_corr_tc<kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        SMEM_BYTES);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)((p.n + TN - 1) / TN),
+  cfg.gridDim = dim3((unsigned)((p.n_corr + TN - 1) / TN),
                      (unsigned)((mtiles + kCluster - 1) / kCluster * kCluster));
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = SMEM_BYTES;
@@ -446,8 +446,8 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n, p.B, kblocks,
-                            p.ntile, w.active, w.cand_v1, w.cand_v2, w.cand_i1,
+  return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
+                            kblocks, p.ntl, w.active, w.cand_v1, w.cand_v2, w.cand_i1,
                             scores_dbg) == cudaSuccess;
 }
 

@@ -112,8 +112,8 @@ __global__ void k_init(SolveParams p, Work w, const float* __restrict__ y_in,
 // queue the signal for an fp64 rescan when the top-2 gap is inside the
 // correlation error bound (or tied: all ties must be injected).
 __global__ void k_select_top(SolveParams p, Work w) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= p.B || !w.active[b]) return;
+  const int64_t b = p.sig_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= p.sig_hi || !w.active[b]) return;
   double v1 = -1.0, v2 = -1.0;
   int i1 = 0x7fffffff;
   const int64_t base = b * p.ntile;
@@ -194,8 +194,8 @@ __device__ void warp_threshold_append(const SolveParams& p, const Work& w,
 // K1c for th < 1: threshold pass over the materialised |scores|.
 __global__ void k_select_thresh(SolveParams p, Work w) {
   const int lane = threadIdx.x & 31;
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (b >= p.B || !w.active[b]) return;
+  const int64_t b = p.sig_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= p.sig_hi || !w.active[b]) return;
   const double* sc = w.scores + b * p.n;
   double cmax = 0.0;
   for (int64_t j = lane; j < p.n; j += 32) cmax = fmax(cmax, sc[j]);
@@ -849,7 +849,7 @@ k_resid(SolveParams p, Work w, int outer) {
   __shared__ int32_t sups[kWarpCap];
   __shared__ double red[kResidWarps];
   __shared__ int snap_s;
-  const int64_t b = blockIdx.x;
+  const int64_t b = p.sig_lo + blockIdx.x;
   if (!w.active[b]) return;
   const int t = w.cnt[b];
   if (t > TB) return;
@@ -929,8 +929,8 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   __shared__ int32_t sup_all[NW][kWarpCap];
   __shared__ __align__(16) double sq_all[NW][TB * TB];  // T / T^2 scratch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * NW + warp;
-  if (b >= p.B || !w.active[b]) return;
+  const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
+  if (b >= p.sig_hi || !w.active[b]) return;
   if (w.cnt[b] > TB) {
     if (lane == 0) {
       const int slot = atomicAdd(&w.counters[kBigCount], 1);
@@ -1349,8 +1349,8 @@ __global__ void k_finalize(SolveParams p, Work w, int64_t out_cap,
                            int32_t* iters_out, double* rn_out,
                            uint8_t* conv_out, int32_t* status_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (b >= p.B) return;
+  const int64_t b = p.sig_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= p.sig_hi) return;
   const int64_t cap = p.cap;
   int status, iters, use_best;
   double rn;
@@ -1421,11 +1421,12 @@ void launch_init(const SolveParams& p, const Work& w, const float* y_in,
 
 void launch_select(const SolveParams& p, const Work& w, bool full_scores,
                    cudaStream_t s) {
+  const int64_t nsig = p.sig_hi - p.sig_lo;
   if (full_scores) {
-    const int64_t blocks = (p.B * 32 + 255) / 256;
+    const int64_t blocks = (nsig * 32 + 255) / 256;
     k_select_thresh<<<(unsigned)blocks, 256, 0, s>>>(p, w);
   } else {
-    const int64_t blocks = (p.B + 255) / 256;
+    const int64_t blocks = (nsig + 255) / 256;
     k_select_top<<<(unsigned)blocks, 256, 0, s>>>(p, w);
   }
 }
@@ -1463,7 +1464,8 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
   cudaMemsetAsync(&w.counters[kBigCount], 0, sizeof(int32_t), s);
   // max_cnt: upper bound on the support size after this iteration's select
   // (ties can exceed it; those signals fall through to the block kernel).
-  auto blocks_for = [&](int nw) { return (unsigned)((p.B + nw - 1) / nw); };
+  const int64_t nsig = p.sig_hi - p.sig_lo;
+  auto blocks_for = [&](int nw) { return (unsigned)((nsig + nw - 1) / nw); };
   auto learn = [&](auto tb) {
     constexpr int TB = decltype(tb)::value;
     constexpr int NW = learn_warps<TB>();
@@ -1472,7 +1474,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
       default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
     }
-    if (!p.sep) k_resid<TB><<<(unsigned)p.B, 32 * kResidWarps, 0, s>>>(p, w, outer);
+    if (!p.sep) k_resid<TB><<<(unsigned)nsig, 32 * kResidWarps, 0, s>>>(p, w, outer);
   };
   if (max_cnt <= 8)
     learn(std::integral_constant<int, 8>());
@@ -1484,7 +1486,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)(p.B < 2 * sms ? p.B : 2 * sms);
+    const int grid = (int)(nsig < 2 * sms ? nsig : 2 * sms);
     switch (p.opt) {
       case 0: launch_block_variant<0>(p, w, outer, big_list, grid, s); break;
       case 1: launch_block_variant<1>(p, w, outer, big_list, grid, s); break;
@@ -1508,7 +1510,7 @@ void launch_finalize(const SolveParams& p, const Work& w, int64_t out_cap,
                      int32_t* sup_out, double* coef_out, int32_t* cnt_out,
                      int32_t* iters_out, double* rn_out, uint8_t* conv_out,
                      int32_t* status_out, cudaStream_t s) {
-  const int64_t blocks = (p.B * 32 + 255) / 256;
+  const int64_t blocks = ((p.sig_hi - p.sig_lo) * 32 + 255) / 256;
   k_finalize<<<(unsigned)blocks, 256, 0, s>>>(p, w, out_cap, sup_out, coef_out,
                                              cnt_out, iters_out, rn_out,
                                              conv_out, status_out);
