@@ -2,23 +2,30 @@
 """bench.py — CLOMP reconstruction throughput on B200.
 
 Metric (BASELINE.json): signals reconstructed per second at fixed (N, M, K),
-plus the roofline fraction of the dominant kernel.  Default workload is
+plus the roofline fraction of the correlation kernel.  Default workload is
 BASELINE config 2 (configs[1]): N=1024, M=512, K=32, 4096 signals per GPU,
 40 dB, lr 0.1, 200 epochs, th=1 / max_outer=K / plain GD / priors off
 (SURVEY.md §8d mapping).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1..6] [--colshard] [--max-outer T]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A step = one full CLOMP solve (K outer iterations x 200 epochs) of one batch
-of 4096 signals already resident in HBM.  Multi-GPU: every rank solves its own
-4096-signal batch (per-signal semantics: no data-path collective), so scaling
-is weak; value = all ranks' signals / max-over-ranks step time.
+already resident in HBM.  Multi-GPU: by default every rank solves its own
+batch (per-signal semantics: no data-path collective; scaling "weak");
+--colshard (config 3) shards one dictionary by columns over the ranks with
+NCCL exchanges and solves one batch together (scaling "strong").  Configs 4-6
+(separable 2D) are timed on a truncated prefix (--max-outer, default 64; the
+full K = 1500 / 13107 outer iterations take minutes to hours per batch).
 
 --impl reference times the unmodified reference library (oracle/_ref,
 compiled from /root/reference/proj/src) on the host cores: P single-threaded
 workers (the library has no threads), each solving a contiguous chunk of 8
-signals with clomp_solve_batch (its AVX2 4x8 GEMM tile path).
+signals with clomp_solve_batch (its AVX2 4x8 GEMM tile path).  For config 3
+the reference needs ~25 min per signal per core, so each worker times 2 outer
+iterations and the figure is extrapolated (the reference's cost per outer
+iteration does not depend on the support size, clomp.cpp:84-89, 237-245).
 """
 from __future__ import annotations
 
@@ -48,28 +55,63 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--colshard", action="store_true")
+    ap.add_argument("--max-outer", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05")
     return ap.parse_args()
 
 
-def workload(cfg_id: int, rank: int):
+def workload(args, rank: int):
     import paper_2501_11592_b200 as cl
 
-    c = dict(cl.CONFIGS[cfg_id])
-    c["seed"] = c["seed"] + 1000 * rank
+    c = dict(cl.CONFIGS[args.config])
+    c["sep"] = "n_r" in c
+    if c["sep"]:
+        c["n"], c["m"] = c["n_r"] * c["n_c"], c["m_r"] * c["m_c"]
+        c["max_outer"] = args.max_outer or 64
+    else:
+        c["max_outer"] = args.max_outer or c["k"]
+    if not args.colshard:
+        c["seed"] = c["seed"] + 1000 * rank  # weak scaling: each rank its own batch
     return c
 
 
-def config_block(c, n_gpus):
+def make_problem(c):
+    import paper_2501_11592_b200 as cl
+
+    if c["sep"]:
+        Ar, Ac, X, Y = cl.gen_problem_2d(c["seed"], c["n_r"], c["n_c"], c["m_r"], c["m_c"],
+                                         c["k"], c["batch"])
+        return (Ar, Ac), X, Y
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    return A, X, Y
+
+
+def solver_config(c):
+    import paper_2501_11592_b200 as cl
+
+    cfg = cl.ClompConfig.baseline(c["k"])
+    cfg.max_outer = c["max_outer"]
+    return cfg
+
+
+def config_block(c, n_gpus, colshard):
+    if c["sep"]:
+        shape = (f"{c['n_r']}x{c['n_c']} coefficients, {c['m_r']}x{c['m_c']} measurements, "
+                 f"K={c['k']} (prefix: {c['max_outer']} outer iterations)")
+    else:
+        shape = f"N={c['n']} M={c['m']} K={c['k']}"
+    noise = "" if c["sep"] or c["snr_db"] < 0 else f" {c['snr_db']} dB"
     return {
-        "workload": f"{c['name']}: N={c['n']} M={c['m']} K={c['k']} batch={c['batch']}/GPU "
-                    f"{'noiseless' if c['snr_db'] < 0 else str(c['snr_db']) + ' dB'}",
-        "n": c["n"], "m": c["m"], "k": c["k"], "batch_per_gpu": c["batch"],
-        "global_batch": c["batch"] * n_gpus, "lr": 0.1, "epochs": 200,
-        "th": 1.0, "max_outer": c["k"], "optimizer": "plain", "priors": "off",
+        "workload": f"{c['name']}: {shape} batch={c['batch']}{'' if colshard else '/GPU'}{noise}",
+        "n": c["n"], "m": c["m"], "k": c["k"], "batch_per_gpu": c["batch"] // (n_gpus if colshard else 1),
+        "global_batch": c["batch"] * (1 if colshard else n_gpus), "lr": 0.1, "epochs": 200,
+        "th": 1.0, "max_outer": c["max_outer"], "optimizer": "plain", "priors": "off",
         "mode": "per_signal (clomp_solve per column)", "seed": c["seed"],
-        "parallelism": f"signal-shard x{n_gpus}, no collectives",
+        "parallelism": (f"column-shard x{n_gpus} (NCCL all-gathers)" if colshard
+                        else f"signal-shard x{n_gpus}, no collectives"),
         "l2": "flushed between timed steps (256 MiB write)",
     }
 
@@ -91,10 +133,12 @@ def _ref_worker(args):
     return time.perf_counter() - t0, r["code"], Ychunk.shape[1]
 
 
-def reference_round(A64, Y64, cfg, workers: int):
-    """One bounded sample: `workers` processes x CHUNK signals, in parallel."""
-    import multiprocessing as mp
+def reference_round(A64, Y64, cfg, workers: int, extrapolate_to: int = 0):
+    """One bounded sample: `workers` processes x CHUNK signals in parallel.
+    With extrapolate_to, each worker runs cfg.max_outer outer iterations and
+    the time is scaled to extrapolate_to iterations."""
     import dataclasses
+    import multiprocessing as mp
 
     cfgd = dataclasses.asdict(cfg)
     B = Y64.shape[1]
@@ -110,6 +154,8 @@ def reference_round(A64, Y64, cfg, workers: int):
     if any(code != 0 for _, code, _ in res):
         raise RuntimeError("reference solve failed")
     sig = sum(n for _, _, n in res)
+    if extrapolate_to:
+        wall = wall * extrapolate_to / cfg.max_outer
     return sig / wall, wall, sig
 
 
@@ -130,37 +176,52 @@ def host_workers():
         return os.cpu_count() or 1
 
 
+def reference_plan(c):
+    """(config for the timed sample, extrapolation target or 0, note)."""
+    cfg = solver_config(c)
+    if c["n"] * c["m"] > 4_000_000:  # config 3: time 2 outer iterations per worker
+        full = cfg.max_outer
+        cfg.max_outer = 2
+        return cfg, full, f"2 outer iterations timed, extrapolated x{full / 2:.0f}"
+    return cfg, 0, "full solves"
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import paper_2501_11592_b200 as cl
     sys.path.insert(0, str(ROOT / "tests"))
     import refbind
 
-    c = workload(args.config, 0)
+    c = workload(args, 0)
+    if c["sep"]:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference has no separable mode; its explicit Kronecker matrix "
+                          "(8.6-137 GB fp64) does not fit the workers"}))
+        return
     if not refbind.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcskit_ref.so not built"}))
         return
-    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
-                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    A, X, Y = make_problem(c)
     A64, Y64 = A.astype(np.float64), Y.astype(np.float64)
-    cfg = cl.ClompConfig.baseline(c["k"])
+    cfg, extra, note = reference_plan(c)
     P = host_workers()
     for _ in range(args.warmup):
-        reference_round(A64, Y64, cfg, min(P, 2))
+        reference_round(A64, Y64, cfg, min(P, 2), extra)
     vals, walls = [], []
+    sig = 0
     for _ in range(args.steps):
-        v, wall, sig = reference_round(A64, Y64, cfg, P)
+        v, wall, sig = reference_round(A64, Y64, cfg, P, extra)
         vals.append(v)
         walls.append(wall)
     value = statistics.mean(vals)
-    sample = f"{P} workers x {CHUNK} signals per step (clomp_solve_batch, AVX2), {sig} signals/step"
+    sample = (f"{P} workers x {CHUNK} signals per step (clomp_solve_batch, AVX2), {sig} "
+              f"signals/step, {note}")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(c, 1),
+        "scaling": "strong" if args.colshard else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(c, 1, False),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "reference",
                          "sample": sample, "cpu": cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -217,18 +278,24 @@ def run_ours(args, rank, world, local_rank):
     dist = world > 1
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    c = workload(args.config, rank)
-    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
-                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    c = workload(args, rank)
+    A, X, Y = make_problem(c)
     B, m, n = c["batch"], c["m"], c["n"]
-    cfg = cl.ClompConfig.baseline(c["k"])
-    ctx = cl.ClompContext(A, device=local_rank)
+    cfg = solver_config(c)
+    if c["sep"]:
+        ctx = cl.ClompContext.separable(A[0], A[1], device=local_rank)
+    elif args.colshard and dist:
+        nid = [cl.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(nid, src=0)
+        ctx = cl.ClompContext.colshard(A, rank, world, nid[0], device=local_rank)
+    else:
+        ctx = cl.ClompContext(A, device=local_rank)
     if args.corr_path:
         ctx.set_corr_path(args.corr_path)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)
     d_y = torch.from_numpy(np.ascontiguousarray(Y.T)).to(dev)  # signal-major B x m
-    cap = min(n, c["k"] + 16)
+    cap = min(n, c["max_outer"] + 16)
     o_sup = torch.zeros((B, cap), dtype=torch.int32, device=dev)
     o_coef = torch.zeros((B, cap), dtype=torch.float64, device=dev)
     o_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
@@ -277,16 +344,19 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = B * world / (ms_max / 1000.0)
+    total_signals = B if args.colshard else B * world
+    value = total_signals / (ms_max / 1000.0)
 
     # Per-phase breakdown of one solve (profiling events, outside the timed region).
-    ctx.set_profiling(True)
-    with torch.cuda.stream(stream):
-        flush.fill_(2)
-    step()
-    torch.cuda.synchronize()
-    prof = ctx.stats()
-    ctx.set_profiling(False)
+    prof = None
+    if not args.colshard:
+        ctx.set_profiling(True)
+        with torch.cuda.stream(stream):
+            flush.fill_(2)
+        step()
+        torch.cuda.synchronize()
+        prof = ctx.stats()
+        ctx.set_profiling(False)
 
     # End to end through the public API: host y in, host results out.
     e2e_ms = []
@@ -301,7 +371,7 @@ def run_ours(args, rank, world, local_rank):
     te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
     if dist:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = B * world / (float(te.item()) / 1000.0)
+    e2e_val = total_signals / (float(te.item()) / 1000.0)
 
     if rank != 0:
         return
@@ -309,53 +379,63 @@ def run_ours(args, rank, world, local_rank):
     pk = ROOT / "MEASURED_PEAKS.json"
     if pk.exists():
         peaks = json.loads(pk.read_text())
-    outers = prof["outer_iterations"]
-    corr_flops = 2.0 * n * m * B  # one launch: A^T R over the batch
-    corr_ms_launch = prof["corr_ms"] / max(outers, 1)
-    if prof["corr_path"] == 1:
-        # 3xTF32: 3 tf32 MMAs per product; the useful rate is compared with
-        # the measured bf16 peak / 2 (tf32 rate) / 3 (three MMAs).
-        peak = peaks.get("bf16_tflops", 1590.0) / 2.0 / 3.0
-        bound, punit = "tensor", "TFLOP/s (fp32-equivalent 3xTF32)"
-        peak_src = "MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (3xTF32), derived"
-    else:
-        clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
-        peak = 148 * 64 * 2 * clk / 1e12
-        bound, punit = "fp64", "TFLOP/s"
-        peak_src = "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x measured SM clock"
-    achieved = corr_flops / (corr_ms_launch / 1000.0) / 1e12
-    roofline = {
-        "kernel": "K1 correlation A^T R + top-2 epilogue",
-        "bound": bound, "achieved": achieved, "peak": peak, "unit": punit,
-        "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-        "algorithmic_per_launch": f"2*N*M*B = {corr_flops:.3e} FLOP",
-        "avg_launch_ms": corr_ms_launch,
-        "phase_ms_per_step": {"corr": prof["corr_ms"], "select_rescan": prof["select_ms"],
-                              "learn": prof["learn_ms"], "total": prof["total_ms"]},
-        "rescans_per_step": prof["rescans"],
-    }
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded cskit::Rng restatement, BASELINE config laws)",
-        "config": config_block(c, world),
-        "roofline": roofline,
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
-                "d2h_bytes_per_step": st["d2h_bytes"],
-                "path": "clomp_solve_batch (host numpy y in, host results out)"},
-        "gpu_launches": int(launches_per_step * args.steps),
-        "clocks": clocks,
+        "higher_is_better": True, "scaling": "strong" if args.colshard else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded cskit::Rng restatement, BASELINE config laws)",
+        "config": config_block(c, world, args.colshard),
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if prof and prof["corr_path"] in (0, 1) and not c["sep"]:
+        outers = max(prof["outer_iterations"], 1)
+        corr_flops = 2.0 * n * m * B  # one launch: A^T R over the batch
+        corr_ms_launch = prof["corr_ms"] / outers
+        if prof["corr_path"] == 1:
+            # 3xTF32: 3 tf32 MMAs per product; the useful rate is compared with
+            # the measured bf16 peak / 2 (tf32 rate) / 3 (three MMAs).
+            peak = peaks.get("bf16_tflops", 1590.0) / 2.0 / 3.0
+            bound, punit = "tensor", "TFLOP/s (fp32-equivalent 3xTF32)"
+            peak_src = ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (3xTF32), derived"
+                        if "bf16_tflops" in peaks else "fallback 1590 TFLOP/s / 2 / 3")
+        else:
+            clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+            peak = 148 * 64 * 2 * clk / 1e12
+            bound, punit = "fp64", "TFLOP/s"
+            peak_src = "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x measured SM clock"
+        achieved = corr_flops / (corr_ms_launch / 1000.0) / 1e12
+        out["roofline"] = {
+            "kernel": "K1 correlation A^T R + top-2 epilogue (k_corr_tc)",
+            "bound": bound, "achieved": achieved, "peak": peak, "unit": punit,
+            "frac": achieved / peak,
+            "traffic": 21.0e6 if prof["corr_path"] == 1 and args.config == 2 else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch, profiles/r1_cfg2_ncu_full_summary.txt"
+                             if prof["corr_path"] == 1 and args.config == 2 else None),
+            "peak_source": peak_src,
+            "algorithmic_per_launch": f"2*N*M*B = {corr_flops:.3e} FLOP",
+            "avg_launch_ms": corr_ms_launch,
+            "phase_ms_per_step": {"corr": prof["corr_ms"], "select_rescan": prof["select_ms"],
+                                  "learn_residual": prof["learn_ms"], "total": prof["total_ms"]},
+            "rescans_per_step": prof["rescans"],
+            "note": ("phase times come from a separately profiled solve (per-iteration sync); "
+                     "the learning kernels (fp64 pipe / shared-memory bound) are the largest share, "
+                     "see DESIGN.md §4"),
+        }
+    out["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
+                  "d2h_bytes_per_step": st["d2h_bytes"],
+                  "path": "clomp_solve_batch (host numpy y in, host results out)"}
+    out["gpu_launches"] = int(launches_per_step * args.steps)
+    out["clocks"] = clocks
+    if world == 1 and not args.no_cpu_baseline and not c["sep"]:
         sys.path.insert(0, str(ROOT / "tests"))
         import refbind
         if refbind.ref_available():
             P = host_workers()
-            v, wall, sig = reference_round(A.astype(np.float64), Y.astype(np.float64), cfg, P)
+            rcfg, extra, note = reference_plan(c)
+            v, wall, sig = reference_round(A.astype(np.float64), Y.astype(np.float64), rcfg, P, extra)
             out["cpu_baseline"] = {
                 "value": v, "unit": UNIT, "cores": P, "kind": "reference",
-                "sample": f"{P} workers x {CHUNK} signals of this workload, one round ({wall:.1f} s)",
+                "sample": f"{P} workers x {CHUNK} signals of this workload, one round ({note})",
                 "cpu": cpu_info()}
     print(json.dumps(out))
 
@@ -365,6 +445,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.colshard and args.config != 3:
+        raise SystemExit("--colshard applies to config 3 (one large dictionary)")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -523,45 +523,47 @@ __device__ __forceinline__ void store_rows(const double (&g)[TB], double* dst, i
 }
 
 // Plain gradient descent, E = inner_steps epochs of c <- T c + d with
-// T = I - 2 lr G and d = 2 lr b (clomp.cpp:87-90, 178-181).  With E = 4q + r:
-// r single steps, then q steps of c <- T^4 c + (I + T + T^2 + T^3) d, the same
-// iterate in exact arithmetic (T^4 c_k + sum_{i<4} T^i d = c_{k+4}) at a
-// quarter of the broadcast traffic; T^2 and T^4 are formed once per outer
-// iteration by two warp-level squarings in shared memory.
-template <int T, int TB>
+// T = I - 2 lr G and d = 2 lr b (clomp.cpp:87-90, 178-181).  With E = P q + r
+// (P = 2^LP): r single steps, then q steps of c <- T^P c + d_P where
+// d_P = sum_{i<P} T^i d — the same iterate in exact arithmetic
+// (T^P c_k + d_P = c_{k+P}).  T^(2^l) and d_(2^l) are built by doubling:
+// d_{2k} = d_k + T^k d_k and T^{2k} = (T^k)^2 (warp squarings in shared
+// memory, T exactly symmetric).  Squarings are long independent FMA chains;
+// trading latency-bound single steps for them is what makes this fast.
+template <int T, int TB, int LP>
 __device__ void epochs_plain(double (&g)[TB], double& c, double d, double* cs,
                              double* s1, const SolveParams& p, int lane) {
+  constexpr int P = 1 << LP;
   const int E = p.inner;
-  const int q = E / 4, r = E % 4;
+  const int q = E / P, r = E % P;
   int ep = 0;
   if (q < 2) {  // too few epochs for the powers to pay off
     affine_steps<T, TB>(g, c, d, cs, E, &ep);
     return;
   }
   affine_steps<T, TB>(g, c, d, cs, r, &ep);
-  // d4 = (I + T + T^2 + T^3) d by Horner: v <- T v + d, three times from v = d.
+  // Park c; the doubling reuses the broadcast buffer for v.
+  const double c_keep = c;
   double v = d;
-  cs[(ep & 1) * kWarpCap + lane] = v;  // stage v in the slot affine_steps reads
-  __syncwarp();
-  {
-    int ev = ep;
-    affine_steps<T, TB>(g, v, d, cs, 3, &ev);
-    // restore c in the slot the next affine step reads
-    cs[(ev & 1) * kWarpCap + lane] = c;
-    ep = ev;
+#pragma unroll 1
+  for (int l = 0; l < LP; ++l) {
+    // v <- v + M v with M = T^(2^l) (its row is in g): an affine step with
+    // offset v itself.
+    cs[(ep & 1) * kWarpCap + lane] = v;
+    __syncwarp();
+    double vv = v;
+    affine_steps<T, TB>(g, vv, v, cs, 1, &ep);
+    v = vv;
+    // M <- M^2
+    store_rows<T, TB>(g, s1, lane);
+    __syncwarp();
+    square_row<T, TB>(g, s1, lane);
     __syncwarp();
   }
-  const double d4 = v;
-  // T is exactly symmetric (G is stored mirrored), hence so are T^2 and T^4,
-  // which square_row relies on.  One T x T buffer: T, then T^2.
-  store_rows<T, TB>(g, s1, lane);
+  c = c_keep;
+  cs[(ep & 1) * kWarpCap + lane] = c;
   __syncwarp();
-  square_row<T, TB>(g, s1, lane);  // g <- row of T^2
-  __syncwarp();
-  store_rows<T, TB>(g, s1, lane);
-  __syncwarp();
-  square_row<T, TB>(g, s1, lane);  // g <- row of T^4
-  affine_steps<T, TB>(g, c, d4, cs, q, &ep);
+  affine_steps<T, TB>(g, c, v, cs, q, &ep);
 }
 
 template <int TB, int OPT>
@@ -808,19 +810,19 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   const int step0 = (outer - 1) * p.inner;
   if constexpr (OPT == 0) {
     if constexpr (TB == 8) {
-      epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
+      epochs_plain<8, TB, 4>(g, c, bi, cs, s1, p, lane);
     } else if constexpr (TB == 16) {
       if (t <= 8)
-        epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<8, TB, 4>(g, c, bi, cs, s1, p, lane);
       else
-        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<16, TB, 4>(g, c, bi, cs, s1, p, lane);
     } else {
       if (t <= 16)
-        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<16, TB, 4>(g, c, bi, cs, s1, p, lane);
       else if (t <= 24)
-        epochs_plain<24, TB>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<24, TB, 3>(g, c, bi, cs, s1, p, lane);
       else
-        epochs_plain<32, TB>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<32, TB, 3>(g, c, bi, cs, s1, p, lane);
     }
   } else {
     epochs_dispatch<TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
