@@ -32,6 +32,10 @@ NVCC_FLAGS = ARCH + [
 ]
 
 
+# Experiment hook: extra -D flags (e.g. CL_NVCC_EXTRA="-DCL_SQ_COST=2").
+NVCC_FLAGS += os.environ.get("CL_NVCC_EXTRA", "").split()
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and Path(cand).exists():

@@ -68,7 +68,6 @@ struct cl_ctx {
   float* at_hi = nullptr;
   float* at_lo = nullptr;
   double* gfull = nullptr;  // A^T A fp64 [n][n], built once (k_gram.cu)
-  double* at64 = nullptr;   // fp64 copy of the atom-major dictionary
   // separable 2D contexts (cl_create_sep)
   bool sep = false;
   int64_t mr = 0, nr = 0, mc = 0, nc = 0, ldr = 0, ldc = 0;
@@ -238,7 +237,6 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
   w.at_hi = ctx->at_hi;
   w.at_lo = ctx->at_lo;
   w.gfull = ctx->gfull;
-  w.at64 = ctx->at64;
   w.at_r64 = ctx->at_r64;
   w.at_c64 = ctx->at_c64;
   w.gr = ctx->gr;
@@ -751,16 +749,6 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
     cl_destroy(ctx);
     return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
   }
-  {
-    std::vector<double> at64(at.begin(), at.end());
-    if (cudaMalloc(&ctx->at64, at64.size() * sizeof(double)) != cudaSuccess ||
-        cudaMemcpy(ctx->at64, at64.data(), at64.size() * sizeof(double),
-                   cudaMemcpyHostToDevice) != cudaSuccess) {
-      cudaGetLastError();
-      cl_destroy(ctx);
-      return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
-    }
-  }
   if (ctx->tc_ok) {
     if (cudaMalloc(&ctx->at_hi, bytes) != cudaSuccess ||
         cudaMalloc(&ctx->at_lo, bytes) != cudaSuccess) {
@@ -884,7 +872,6 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode) {
     if (ctx->gfull) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->gfull);
-  cudaFree(ctx->at64);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);
@@ -916,7 +903,6 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->at_hi);
   cudaFree(ctx->at_lo);
   cudaFree(ctx->gfull);
-  cudaFree(ctx->at64);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);

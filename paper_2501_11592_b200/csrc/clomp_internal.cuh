@@ -47,8 +47,6 @@ struct Work {
   const float* at_hi = nullptr;  // [n][ldm] tf32 split (tensor path)
   const float* at_lo = nullptr;
   const double* gfull = nullptr; // [n][n] fp64 A^T A (optional, per context)
-  const double* at64 = nullptr;  // [n][ldm] fp64 copy of at32 (exact): the
-                                 // fp64 gathers read it, no conversions
   float* y32 = nullptr;          // [B][ldm]
   double* y64 = nullptr;
   double* r64 = nullptr;
@@ -142,20 +140,10 @@ int64_t sep_resid_tiles(const SolveParams& p);
 void launch_gram_full(const float* at, int64_t n, int64_t ldm, double* g,
                       cudaStream_t s);
 
-// fp32 -> fp64 with integer ops (ALU pipe) instead of F2F.F64.F32: exact for
-// zeros, normals, infinities and NaNs; fp32 subnormals flush to signed zero.
-__device__ __forceinline__ double f2d(float f) {
-  const uint32_t u = __float_as_uint(f);
-  const uint32_t sign = u & 0x80000000u;
-  const uint32_t e = (u >> 23) & 0xffu;
-  const uint32_t man_hi = (u >> 3) & 0x000FFFFFu;
-  uint32_t hi = sign | ((e + 896u) << 20) | man_hi;
-  uint32_t lo = u << 29;
-  hi = (e == 0u) ? sign : hi;
-  lo = (e == 0u) ? 0u : lo;
-  hi = (e == 0xffu) ? (sign | 0x7FF00000u | man_hi) : hi;
-  return __hiloint2double((int)hi, (int)lo);
-}
+// fp32 -> fp64 (exact).  The hardware F2F.F64.F32 keeps pace with DFMA on
+// sm_100a (tools/micro/cvt.cu: ~61 conversions per SM-cycle); integer
+// bit-assembly with special-case selects measured 10x slower.
+__device__ __forceinline__ double f2d(float f) { return (double)f; }
 
 // ---- launchers (k_solve.cu) ----
 void launch_init(const SolveParams& p, const Work& w, const float* y_in,

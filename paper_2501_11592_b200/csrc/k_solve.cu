@@ -247,13 +247,11 @@ __global__ void __launch_bounds__(256) k_rescan(SolveParams p, Work w) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (j0 + u < p.n) {
-            const double* a = w.at64 + (j0 + u) * p.ldm + i;
-            const double2 a01 = *reinterpret_cast<const double2*>(a);
-            const double2 a23 = *reinterpret_cast<const double2*>(a + 2);
-            acc[u] = fma(a01.x, r01.x, acc[u]);
-            acc[u] = fma(a01.y, r01.y, acc[u]);
-            acc[u] = fma(a23.x, r23.x, acc[u]);
-            acc[u] = fma(a23.y, r23.y, acc[u]);
+            const float4 a = *reinterpret_cast<const float4*>(w.at32 + (j0 + u) * p.ldm + i);
+            acc[u] = fma(f2d(a.x), r01.x, acc[u]);
+            acc[u] = fma(f2d(a.y), r01.y, acc[u]);
+            acc[u] = fma(f2d(a.z), r23.x, acc[u]);
+            acc[u] = fma(f2d(a.w), r23.y, acc[u]);
           }
         }
       }
@@ -490,77 +488,134 @@ __device__ __forceinline__ void affine_steps(const double (&m)[TB], double& c, d
   }
 }
 
-// res <- row `lane` of P*P, P symmetric and stored as T x T rows in smem.
-// Row k of P is read by broadcast (LDS.128); the lane's own factor P[lane][k]
-// is read as P[k][lane] (exact by symmetry; consecutive lanes hit consecutive
-// words, so no bank conflicts).  Nothing but the result row lives in registers.
-template <int T, int TB>
-__device__ __forceinline__ void square_row(double (&res)[TB], const double* src, int lane) {
+// P <- P * P in place for a symmetric T x T matrix stored with row stride
+// T + 4 (bank-conflict-free fragment loads), on the fp64 tensor cores
+// (mma.sync m8n8k4 f64 -> DMMA).  By symmetry the B fragment of block (K, J)
+// equals the A fragment of block (J, K), so every lane loads its T*T/32 share
+// of P once (A-layout fragments F(I, K) = P[8I + lane/4][4K + lane%4]) and the
+// whole product runs from registers; the shared-memory broadcast traffic of
+// the SIMT squaring disappears.
+#ifndef CL_SQ_ILP
+#define CL_SQ_ILP 0
+#endif
+template <int T>
+__device__ __forceinline__ void square_dmma(double* buf, int lane) {
+  constexpr int NI = T / 8, NK = T / 4, LD = T + 4;
+  const int r = lane >> 2, c = lane & 3;
+  double f[NI][NK];
 #pragma unroll
-  for (int j = 0; j < T; ++j) res[j] = 0.0;
-#pragma unroll 2
-  for (int k = 0; k < T; ++k) {
-    const double* row = src + k * T;
-    const double own = lane < T ? row[lane] : 0.0;
+  for (int I = 0; I < NI; ++I)
 #pragma unroll
-    for (int j = 0; j < T; j += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(row + j);
-      res[j] = fma(own, v.x, res[j]);
-      res[j + 1] = fma(own, v.y, res[j + 1]);
-    }
+    for (int K = 0; K < NK; ++K) f[I][K] = buf[(8 * I + r) * LD + 4 * K + c];
+  __syncwarp();
+#if CL_SQ_ILP
+  double acc[NI][NI][2];
+#pragma unroll
+  for (int I = 0; I < NI; ++I)
+#pragma unroll
+    for (int J = 0; J < NI; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+#pragma unroll
+  for (int K = 0; K < NK; ++K)
+#pragma unroll
+    for (int I = 0; I < NI; ++I)
+#pragma unroll
+      for (int J = 0; J < NI; ++J)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(acc[I][J][0]), "+d"(acc[I][J][1])
+            : "d"(f[I][K]), "d"(f[J][K]));
+#pragma unroll
+  for (int I = 0; I < NI; ++I)
+#pragma unroll
+    for (int J = 0; J < NI; ++J)
+      *reinterpret_cast<double2*>(buf + (8 * I + r) * LD + 8 * J + 2 * c) =
+          make_double2(acc[I][J][0], acc[I][J][1]);
+#else
+#pragma unroll
+  for (int I = 0; I < NI; ++I) {
+    double acc[NI][2];
+#pragma unroll
+    for (int J = 0; J < NI; ++J) acc[J][0] = acc[J][1] = 0.0;
+#pragma unroll
+    for (int K = 0; K < NK; ++K)
+#pragma unroll
+      for (int J = 0; J < NI; ++J)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(acc[J][0]), "+d"(acc[J][1])
+            : "d"(f[I][K]), "d"(f[J][K]));
+#pragma unroll
+    for (int J = 0; J < NI; ++J)
+      *reinterpret_cast<double2*>(buf + (8 * I + r) * LD + 8 * J + 2 * c) =
+          make_double2(acc[J][0], acc[J][1]);
   }
-}
-
-// Write the lane's row of a symmetric T x T matrix as its column: for fixed j
-// the lanes hit consecutive words (conflict-free), and by symmetry the stored
-// matrix is the same.
-template <int T, int TB>
-__device__ __forceinline__ void store_rows(const double (&g)[TB], double* dst, int lane) {
-  if (lane < T) {
-#pragma unroll
-    for (int j = 0; j < T; ++j) dst[j * T + lane] = g[j];
-  }
+#endif
+  __syncwarp();
 }
 
 // Plain gradient descent, E = inner_steps epochs of c <- T c + d with
-// T = I - 2 lr G and d = 2 lr b (clomp.cpp:87-90, 178-181).  With E = P q + r
-// (P = 2^LP): r single steps, then q steps of c <- T^P c + d_P where
-// d_P = sum_{i<P} T^i d — the same iterate in exact arithmetic
-// (T^P c_k + d_P = c_{k+P}).  T^(2^l) and d_(2^l) are built by doubling:
-// d_{2k} = d_k + T^k d_k and T^{2k} = (T^k)^2 (warp squarings in shared
-// memory, T exactly symmetric).  Squarings are long independent FMA chains;
-// trading latency-bound single steps for them is what makes this fast.
-template <int T, int TB, int LP>
+// T = I - 2 lr G and d = 2 lr b (clomp.cpp:87-90, 178-181).  Write
+// E = P q + r with P = 2^L.  Powers T^(2^l) and offsets d_(2^l) =
+// sum_{i<2^l} T^i d are built by doubling (d_{2k} = d_k + T^k d_k,
+// T^{2k} = (T^k)^2, squarings on the fp64 tensor cores); on the way up, every
+// set bit l of r applies c <- T^(2^l) c + d_(2^l), then q steps of
+// c <- T^P c + d_P finish — the same iterate as E single steps in exact
+// arithmetic (c_{k+a} = T^a c_k + d_a composes in any order).  L minimises
+// popcount(r) + L + q dependent matvecs plus L squarings.
+#ifndef CL_SQ_COST
+#define CL_SQ_COST 5
+#endif
+__device__ __forceinline__ int power_levels(int E) {
+  int best_l = 0, best = E;
+  for (int l = 1; l <= 8; ++l) {
+    const int cost = __popc(E & ((1 << l) - 1)) + (1 + CL_SQ_COST) * l + (E >> l);
+    if ((E >> l) >= 1 && cost < best) {
+      best = cost;
+      best_l = l;
+    }
+  }
+  return best_l;
+}
+
+template <int T, int TB>
 __device__ void epochs_plain(double (&g)[TB], double& c, double d, double* cs,
                              double* s1, const SolveParams& p, int lane) {
-  constexpr int P = 1 << LP;
   const int E = p.inner;
-  const int q = E / P, r = E % P;
+  const int L = power_levels(E);
   int ep = 0;
-  if (q < 2) {  // too few epochs for the powers to pay off
+  if (L == 0) {
     affine_steps<T, TB>(g, c, d, cs, E, &ep);
     return;
   }
-  affine_steps<T, TB>(g, c, d, cs, r, &ep);
-  // Park c; the doubling reuses the broadcast buffer for v.
-  const double c_keep = c;
+  const int q = E >> L, r = E & ((1 << L) - 1);
   double v = d;
+  constexpr int LD = T + 4;
 #pragma unroll 1
-  for (int l = 0; l < LP; ++l) {
-    // v <- v + M v with M = T^(2^l) (its row is in g): an affine step with
-    // offset v itself.
+  for (int l = 0; l < L; ++l) {
+    // here g = row `lane` of M = T^(2^l), v = d_(2^l)
+    if ((r >> l) & 1) {
+      cs[(ep & 1) * kWarpCap + lane] = c;
+      __syncwarp();
+      affine_steps<T, TB>(g, c, v, cs, 1, &ep);
+    }
+    // v <- v + M v: an affine step with offset v itself.
     cs[(ep & 1) * kWarpCap + lane] = v;
     __syncwarp();
     double vv = v;
     affine_steps<T, TB>(g, vv, v, cs, 1, &ep);
     v = vv;
-    // M <- M^2
-    store_rows<T, TB>(g, s1, lane);
+    // M <- M^2; g <- row `lane` of M (read as a column, conflict-free, exact
+    // by symmetry).
+    if (lane < T) {
+#pragma unroll
+      for (int j = 0; j < T; ++j) s1[j * LD + lane] = g[j];
+    }
     __syncwarp();
-    square_row<T, TB>(g, s1, lane);
+    square_dmma<T>(s1, lane);
+#pragma unroll
+    for (int j = 0; j < T; ++j) g[j] = lane < T ? s1[j * LD + lane] : 0.0;
     __syncwarp();
   }
-  c = c_keep;
   cs[(ep & 1) * kWarpCap + lane] = c;
   __syncwarp();
   affine_steps<T, TB>(g, c, v, cs, q, &ep);
@@ -650,17 +705,16 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
         G[(int64_t)k * cap + lane] = v;
         G[(int64_t)lane * cap + k] = v;
       }
-      const double* ak = w.at64 + jk * ldm;
+      const float* ak = w.at32 + jk * ldm;
       double accb = 0.0;
       for (int64_t i0 = 4 * lane; i0 < ldm; i0 += 128) {
-        const double2 a01 = *reinterpret_cast<const double2*>(ak + i0);
-        const double2 a23 = *reinterpret_cast<const double2*>(ak + i0 + 2);
+        const float4 a = *reinterpret_cast<const float4*>(ak + i0);
         const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
         const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
-        accb = fma(a01.x, y01.x, accb);
-        accb = fma(a01.y, y01.y, accb);
-        accb = fma(a23.x, y23.x, accb);
-        accb = fma(a23.y, y23.y, accb);
+        accb = fma(f2d(a.x), y01.x, accb);
+        accb = fma(f2d(a.y), y01.y, accb);
+        accb = fma(f2d(a.z), y23.x, accb);
+        accb = fma(f2d(a.w), y23.y, accb);
       }
       accb = warp_sum(accb);
       if (lane == 0) {
@@ -731,16 +785,15 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
 #pragma unroll 2
     for (int k = 0; k < t; ++k) {
       const double ck = cs[k];
-      const double* row = w.at64 + (int64_t)sups[k] * ldm + base + 4 * lane;
+      const float* row = w.at32 + (int64_t)sups[k] * ldm + base + 4 * lane;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (base + 128 * q < ldm) {
-          const double2 v01 = *reinterpret_cast<const double2*>(row + 128 * q);
-          const double2 v23 = *reinterpret_cast<const double2*>(row + 128 * q + 2);
-          r[4 * q + 0] = fma(v01.x, ck, r[4 * q + 0]);
-          r[4 * q + 1] = fma(v01.y, ck, r[4 * q + 1]);
-          r[4 * q + 2] = fma(v23.x, ck, r[4 * q + 2]);
-          r[4 * q + 3] = fma(v23.y, ck, r[4 * q + 3]);
+          const float4 v = *reinterpret_cast<const float4*>(row + 128 * q);
+          r[4 * q + 0] = fma(f2d(v.x), ck, r[4 * q + 0]);
+          r[4 * q + 1] = fma(f2d(v.y), ck, r[4 * q + 1]);
+          r[4 * q + 2] = fma(f2d(v.z), ck, r[4 * q + 2]);
+          r[4 * q + 3] = fma(f2d(v.w), ck, r[4 * q + 3]);
         }
       }
     }
@@ -810,19 +863,19 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   const int step0 = (outer - 1) * p.inner;
   if constexpr (OPT == 0) {
     if constexpr (TB == 8) {
-      epochs_plain<8, TB, 4>(g, c, bi, cs, s1, p, lane);
+      epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
     } else if constexpr (TB == 16) {
       if (t <= 8)
-        epochs_plain<8, TB, 4>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
       else
-        epochs_plain<16, TB, 4>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
     } else {
       if (t <= 16)
-        epochs_plain<16, TB, 4>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
       else if (t <= 24)
-        epochs_plain<24, TB, 3>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<24, TB>(g, c, bi, cs, s1, p, lane);
       else
-        epochs_plain<32, TB, 3>(g, c, bi, cs, s1, p, lane);
+        epochs_plain<32, TB>(g, c, bi, cs, s1, p, lane);
     }
   } else {
     epochs_dispatch<TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
@@ -838,7 +891,7 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
 
 // Residual, loss and stopping rules after the learning phase.  One block per
 // signal; each warp owns 128-row chunks of the measurement vector (4 rows per
-// lane, fp64 atom rows read as 16-byte loads), so a signal's residual is
+// lane, fp32 atom rows read as float4), so a signal's residual is
 // spread over several warps and many signals are resident per SM to hide the
 // L2 latency of the support-atom gathers.  Signals whose support outgrew the
 // learning bucket TB were finished by the block learning kernel.
@@ -870,13 +923,12 @@ k_resid(SolveParams p, Work w, int outer) {
 #pragma unroll 4
     for (int k = 0; k < t; ++k) {
       const double ck = cs[k];
-      const double* row = w.at64 + (int64_t)sups[k] * ldm + i0;
-      const double2 v01 = *reinterpret_cast<const double2*>(row);
-      const double2 v23 = *reinterpret_cast<const double2*>(row + 2);
-      r0 = fma(v01.x, ck, r0);
-      r1 = fma(v01.y, ck, r1);
-      r2 = fma(v23.x, ck, r2);
-      r3 = fma(v23.y, ck, r3);
+      // fp32 atom rows (exact in fp64, half the L2 bytes of the fp64 copy)
+      const float4 v = *reinterpret_cast<const float4*>(w.at32 + (int64_t)sups[k] * ldm + i0);
+      r0 = fma(f2d(v.x), ck, r0);
+      r1 = fma(f2d(v.y), ck, r1);
+      r2 = fma(f2d(v.z), ck, r2);
+      r3 = fma(f2d(v.w), ck, r3);
     }
     const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
     const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
@@ -929,7 +981,7 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   constexpr int NW = learn_warps<TB>();
   __shared__ __align__(16) double cs_all[NW][2 * kWarpCap];
   __shared__ int32_t sup_all[NW][kWarpCap];
-  __shared__ __align__(16) double sq_all[NW][TB * TB];  // T / T^2 scratch
+  __shared__ __align__(16) double sq_all[NW][TB * (TB + 4)];  // powers of T (padded rows)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi || !w.active[b]) return;
@@ -1006,7 +1058,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
           const float* ai = w.at32 + (int64_t)sups[i] * p.ldm;
           double acc = 0.0;
           for (int64_t q = lane; q < p.ldm; q += 32)
-            acc = fma(w.at64[(int64_t)sups[k] * p.ldm + q], w.at64[(int64_t)sups[i] * p.ldm + q], acc);
+            acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + q], (double)w.at32[(int64_t)sups[i] * p.ldm + q], acc);
           acc = warp_sum(acc);
           if (lane == 0) {
             G[(int64_t)k * cap + i] = acc;
@@ -1017,7 +1069,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
       if (warp == nw - 1) {
         double acc = 0.0;
         for (int64_t q = lane; q < p.ldm; q += 32)
-          acc = fma(w.at64[(int64_t)sups[k] * p.ldm + q], y[q], acc);
+          acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + q], y[q], acc);
         acc = warp_sum(acc);
         if (lane == 0) {
           w.bvec[b * cap + k] = acc;
@@ -1104,7 +1156,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     for (int64_t i = tid; i < p.ldm; i += kBlockThreads) {
       double acc = 0.0;
       for (int k = 0; k < t; ++k)
-        acc = fma(w.at64[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
+        acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
       const double rv = acc - y[i];
       store_residual(w, b * p.ldm + i, rv);
       lacc = fma(rv, rv, lacc);
@@ -1144,7 +1196,7 @@ k_solve_fused(SolveParams p, Work w) {
   double* rs = reinterpret_cast<double*>(fsm);                 // [ldm] residual
   __shared__ __align__(16) double cs[2 * kWarpCap];
   __shared__ int32_t sups[kWarpCap];
-  __shared__ __align__(16) double sq[kWarpCap * kWarpCap];
+  __shared__ __align__(16) double sq[kWarpCap * (kWarpCap + 4)];
   __shared__ double red[kFusedThreads / 32];
   __shared__ int s_active;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1167,9 +1219,9 @@ k_solve_fused(SolveParams p, Work w) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (j0 + u < p.n) {
-            const double2 a = *reinterpret_cast<const double2*>(w.at64 + (j0 + u) * p.ldm + i);
-            acc[u] = fma(a.x, r01.x, acc[u]);
-            acc[u] = fma(a.y, r01.y, acc[u]);
+            const float2 a = *reinterpret_cast<const float2*>(w.at32 + (j0 + u) * p.ldm + i);
+            acc[u] = fma(f2d(a.x), r01.x, acc[u]);
+            acc[u] = fma(f2d(a.y), r01.y, acc[u]);
           }
         }
       }
@@ -1209,7 +1261,7 @@ k_solve_fused(SolveParams p, Work w) {
     double lacc = 0.0;
     for (int64_t i = tid; i < p.ldm; i += kFusedThreads) {
       double acc = 0.0;
-      for (int k = 0; k < t; ++k) acc = fma(w.at64[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
+      for (int k = 0; k < t; ++k) acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
       const double rv = acc - w.y64[b * p.ldm + i];
       rs[i] = rv;
       lacc = fma(rv, rv, lacc);
