@@ -350,8 +350,25 @@ __global__ void __launch_bounds__(256) k_rescan(SolveParams p, Work w) {
 // Per-signal bookkeeping after the learning phase of outer iteration `outer`
 // (clomp.cpp:253-273), plus the eps test that opens the next iteration
 // (clomp.cpp:238-242).  Returns true when the best snapshot must be taken.
+// Per-signal control state read before the residual pass, so its load
+// latency overlaps the atom gathers instead of following the loss reduction.
+struct CtlState {
+  double best_L, prev_L;
+  int cnt, changed, stall;
+};
+
+__device__ __forceinline__ CtlState load_ctl(const Work& w, int64_t b) {
+  CtlState c;
+  c.best_L = w.best_L[b];
+  c.prev_L = w.prev_L[b];
+  c.cnt = w.cnt[b];
+  c.changed = w.changed[b];
+  c.stall = w.stall[b];
+  return c;
+}
+
 __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
-                               int outer, double L) {
+                               int outer, double L, const CtlState& st) {
   w.loss[b] = L;
   if (!isfinite(L)) {
     w.status[b] = kStatusNumerical;
@@ -360,15 +377,15 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
   }
   w.iters[b] = outer;
   bool snap = false;
-  if (L < w.best_L[b]) {
+  if (L < st.best_L) {
     w.best_L[b] = L;
-    w.best_cnt[b] = w.cnt[b];
+    w.best_cnt[b] = st.cnt;
     snap = true;
   }
-  const double prev = w.prev_L[b];
+  const double prev = st.prev_L;
   const double rel = isfinite(prev) ? (prev - L) / fmax(fabs(prev), 1e-300)
                                     : CUDART_INF;
-  int stall = (!w.changed[b] && rel < p.stall_tol) ? w.stall[b] + 1 : 0;
+  const int stall = (!st.changed && rel < p.stall_tol) ? st.stall + 1 : 0;
   w.stall[b] = stall;
   w.prev_L[b] = L;
   if (stall >= p.stall_patience || outer >= p.max_outer) {
@@ -380,6 +397,11 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
     atomicAdd(&w.counters[kActiveCount], 1);
   }
   return snap;
+}
+
+__device__ __forceinline__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
+                                               int outer, double L) {
+  return control_signal(p, w, b, outer, L, load_ctl(w, b));
 }
 
 // ----------------------------------------------------- optimizer steps
@@ -772,6 +794,11 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
 // Residual r = A_S c - y (fp64), stored for the next correlation (fp64 and the
 // tf32 split), and its sum of squares.  Each lane owns 16 measurements per
 // 512-row pass (float4 atom loads); c and the support come from shared memory.
+#ifndef CL_RESIDW_UNROLL
+#define CL_RESIDW_UNROLL 4
+#endif
+constexpr int kResidUnroll = CL_RESIDW_UNROLL;
+
 __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
                                 const double* cs, const int32_t* sups, int t,
                                 int lane) {
@@ -782,7 +809,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
     double r[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) r[q] = 0.0;
-#pragma unroll 2
+#pragma unroll kResidUnroll
     for (int k = 0; k < t; ++k) {
       const double ck = cs[k];
       const float* row = w.at32 + (int64_t)sups[k] * ldm + base + 4 * lane;
@@ -896,9 +923,16 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
 // L2 latency of the support-atom gathers.  Signals whose support outgrew the
 // learning bucket TB were finished by the block learning kernel.
 constexpr int kResidWarps = 4;
+#ifndef CL_RESID_BATCH
+#define CL_RESID_BATCH 4
+#endif
+constexpr int kResidBatch = CL_RESID_BATCH;
 
+#ifndef CL_RESID_MINB
+#define CL_RESID_MINB 1
+#endif
 template <int TB>
-__global__ void __launch_bounds__(32 * kResidWarps)
+__global__ void __launch_bounds__(32 * kResidWarps, CL_RESID_MINB)
 k_resid(SolveParams p, Work w, int outer) {
   __shared__ __align__(16) double cs[kWarpCap];
   __shared__ int32_t sups[kWarpCap];
@@ -910,25 +944,34 @@ k_resid(SolveParams p, Work w, int outer) {
   if (t > TB) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t cap = p.cap, ldm = p.ldm;
-  if (tid < t) {
-    cs[tid] = w.coef[b * cap + tid];
-    sups[tid] = w.sup[b * cap + tid];
+  if (tid < kWarpCap) {  // zero tail: batched loops read cs up to a batch edge
+    cs[tid] = tid < t ? w.coef[b * cap + tid] : 0.0;
+    sups[tid] = tid < t ? w.sup[b * cap + tid] : 0;
   }
+  CtlState ctl{};
+  if (tid == 0 && p.mode == kModePerSignal) ctl = load_ctl(w, b);
   __syncthreads();
   const double* y = w.y64 + b * ldm;
   double lacc = 0.0;
   for (int64_t q = warp; q * 128 < ldm; q += kResidWarps) {
     const int64_t i0 = q * 128 + 4 * lane;
     double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < t; ++k) {
-      const double ck = cs[k];
-      // fp32 atom rows (exact in fp64, half the L2 bytes of the fp64 copy)
-      const float4 v = *reinterpret_cast<const float4*>(w.at32 + (int64_t)sups[k] * ldm + i0);
-      r0 = fma(f2d(v.x), ck, r0);
-      r1 = fma(f2d(v.y), ck, r1);
-      r2 = fma(f2d(v.z), ck, r2);
-      r3 = fma(f2d(v.w), ck, r3);
+    // fp32 atom rows (exact in fp64, half the L2 bytes of an fp64 copy),
+    // kResidBatch independent gathers in flight per lane.
+    for (int k0 = 0; k0 < t; k0 += kResidBatch) {
+      float4 v[kResidBatch];
+#pragma unroll
+      for (int u = 0; u < kResidBatch; ++u)
+        v[u] = k0 + u < t ? *reinterpret_cast<const float4*>(w.at32 + (int64_t)sups[k0 + u] * ldm + i0)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kResidBatch; ++u) {
+        const double ck = cs[k0 + u];
+        r0 = fma(f2d(v[u].x), ck, r0);
+        r1 = fma(f2d(v[u].y), ck, r1);
+        r2 = fma(f2d(v[u].z), ck, r2);
+        r3 = fma(f2d(v[u].w), ck, r3);
+      }
     }
     const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
     const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
@@ -958,12 +1001,51 @@ k_resid(SolveParams p, Work w, int outer) {
     for (int q = 0; q < kResidWarps; ++q) L += red[q];
     snap_s = 0;
     if (p.mode == kModePerSignal)
-      snap_s = control_signal(p, w, b, outer, L);
+      snap_s = control_signal(p, w, b, outer, L, ctl);
     else
       w.loss[b] = L;
   }
   __syncthreads();
   if (snap_s && tid < t) w.best_coef[b * cap + tid] = cs[tid];
+}
+
+// Warp-per-signal variant: no block barriers, the whole signal's gathers
+// (16 rows per lane per 512-row pass) issued by one warp, many signals
+// resident per SM.
+#ifndef CL_RESID_WARP
+#define CL_RESID_WARP 1
+#endif
+#ifndef CL_RESIDW_MINB
+#define CL_RESIDW_MINB 4
+#endif
+template <int TB>
+__global__ void __launch_bounds__(128, CL_RESIDW_MINB)
+k_resid_w(SolveParams p, Work w, int outer) {
+  __shared__ __align__(16) double cs_all[4][kWarpCap];
+  __shared__ int32_t sup_all[4][kWarpCap];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = p.sig_lo + (int64_t)blockIdx.x * 4 + warp;
+  if (b >= p.sig_hi || !w.active[b]) return;
+  const int t = w.cnt[b];
+  if (t > TB) return;
+  const int64_t cap = p.cap;
+  double* cs = cs_all[warp];
+  int32_t* sups = sup_all[warp];
+  cs[lane] = lane < t ? w.coef[b * cap + lane] : 0.0;
+  sups[lane] = lane < t ? w.sup[b * cap + lane] : 0;
+  CtlState ctl{};
+  if (lane == 0 && p.mode == kModePerSignal) ctl = load_ctl(w, b);
+  __syncwarp();
+  const double L = warp_residual(p, w, b, cs, sups, t, lane);
+  int snap = 0;
+  if (lane == 0) {
+    if (p.mode == kModePerSignal)
+      snap = control_signal(p, w, b, outer, L, ctl);
+    else
+      w.loss[b] = L;
+  }
+  snap = __shfl_sync(kFull, snap, 0);
+  if (snap && lane < t) w.best_coef[b * cap + lane] = cs[lane];
 }
 
 // TB: support-size bucket this launch is compiled for (8, 16 or 32).  Signals
@@ -1528,7 +1610,13 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
       default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
     }
-    if (!p.sep) k_resid<TB><<<(unsigned)nsig, 32 * kResidWarps, 0, s>>>(p, w, outer);
+    if (!p.sep) {
+#if CL_RESID_WARP
+      k_resid_w<TB><<<(unsigned)((nsig + 3) / 4), 128, 0, s>>>(p, w, outer);
+#else
+      k_resid<TB><<<(unsigned)nsig, 32 * kResidWarps, 0, s>>>(p, w, outer);
+#endif
+    }
   };
   if (max_cnt <= 8)
     learn(std::integral_constant<int, 8>());
