@@ -3,7 +3,8 @@
 // Owns the device copy of the dictionary, the batch workspace and the outer
 // loop that sequences the kernels of one CLOMP solve:
 //
-//   init -> [ corr (K1) -> select (K1c) -> rescan -> learn (K2) -> control ]*
+//   init -> [ corr (K1) -> select (K1c, exact near-tie rescoring) + learn (K2)
+//             -> residual + control ]*
 //        -> finalize
 //
 // Validation, error classes and messages follow the reference
@@ -172,26 +173,16 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.r64 = cv.take<double>(B * ldm);
     w.r_hi = need_split ? cv.take<float>(B * ldm) : nullptr;
     w.r_lo = need_split ? cv.take<float>(B * ldm) : nullptr;
-    w.cand_v1 = cv.take<double>(B * ntile);
-    w.cand_v2 = cv.take<double>(B * ntile);
-    w.cand_i1 = cv.take<int32_t>(B * ntile);
+    w.cand = cv.take<Cand>(B * ntile);
     w.scores = need_scores ? cv.take<double>(B * ctx->n) : nullptr;
-    const int64_t nchunk = (ctx->n + 256 + 63) / 64;  // tiles cover <= n + 256 atoms
     if (ctx->sep) {
       w.zb = cv.take<double>(B * ctx->n);
       w.sep_scratch = cv.take<double>(B * ctx->nc * ctx->mr);
       w.lpart = cv.take<double>(B * (((ctx->mr + 63) / 64) * ((ctx->mc + 63) / 64)));
     }
     if (ctx->world > 1 || ctx->vshards > 1) {
-      w.xg_v1 = cv.take<double>(B * ntile);
-      w.xg_v2 = cv.take<double>(B * ntile);
-      w.xg_i1 = cv.take<int32_t>(B * ntile);
+      w.xg = cv.take<Cand>(B * ntile);
     }
-    w.rs_top = cv.take<double>(B);
-    w.rs_delta = cv.take<double>(B);
-    w.rs_done = cv.take<int32_t>(B);
-    w.rs_cmax = cv.take<double>(B * nchunk);
-    w.rs_ids = cv.take<int32_t>(B * nchunk * 5);
     w.sup = cv.take<int32_t>(B * cap);
     w.cnt = cv.take<int32_t>(B);
     w.gcnt = cv.take<int32_t>(B);
@@ -212,7 +203,7 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.conv = cv.take<uint8_t>(B);
     w.status = cv.take<int32_t>(B);
     w.changed = cv.take<int32_t>(B);
-    w.rescan_list = cv.take<int32_t>(2 * B);
+    w.big_list = cv.take<int32_t>(B);
     w.counters = cv.take<int32_t>(kNumCounters);
     w.joint = cv.take<double>(kNumJoint);
   };
@@ -384,15 +375,18 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.mc = ctx->mc;
   p.ldr = ctx->ldr;
   p.ldc = ctx->ldc;
+  // th == 1: the selection (K1c, near-tie rescoring included) runs at the top
+  // of the learning kernel, one warp per signal, instead of its own launch.
+  p.fuse_select = (!full_scores && !p.sep) ? 1 : 0;
 
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
   cl_stats stats{};
   stats.corr_path = tensor ? 1 : 0;
-  const int rescan_grid = 2 * ctx->sms;
 
-  // One outer iteration (clomp.cpp:235-274): counters reset, K1, K1c, fp64
-  // rescans, learning + residual + stopping rules.  th == 1 adds one atom per
+  // One outer iteration (clomp.cpp:235-274): counters reset, K1, K1c (with
+  // exact fp64 rescoring of near-ties; fused into the learning kernel when
+  // th == 1), learning + residual + stopping rules.  th == 1 adds one atom per
   // iteration, so the learning kernel's support bucket follows `outer`
   // (signals grown past it by ties are finished by the block kernel).
   auto enqueue_iteration = [&](int outer, int64_t* launches) {
@@ -418,9 +412,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         SolveParams pk = p;
         pk.atom0 = (int64_t)r * p.n_corr;
         Work wk = w;
-        wk.cand_v1 = w.xg_v1 + (int64_t)r * B * p.ntl;
-        wk.cand_v2 = w.xg_v2 + (int64_t)r * B * p.ntl;
-        wk.cand_i1 = w.xg_i1 + (int64_t)r * B * p.ntl;
+        wk.cand = w.xg + (int64_t)r * B * p.ntl;
         if (tensor)
           launch_corr_tc(pk, wk, s);
         else
@@ -429,16 +421,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       }
       if (ctx->world > 1) {
         const size_t cnt = (size_t)(B * p.ntl);
-        nccl_allgather_inplace(ctx->comm, w.xg_v1, cnt, 8, ctx->rank, s);
-        nccl_allgather_inplace(ctx->comm, w.xg_v2, cnt, 8, ctx->rank, s);
-        nccl_allgather_inplace(ctx->comm, w.xg_i1, cnt, 4, ctx->rank, s);
+        nccl_allgather_inplace(ctx->comm, w.xg, cnt * sizeof(Cand), 1, ctx->rank, s);
       }
-      launch_cand_exchange(w.xg_v1, w.xg_v2, w.xg_i1, w.cand_v1, w.cand_v2, w.cand_i1, B, p.ntl,
-                           W, p.n_corr, s);
-      launch_select(p, w, false, s);
-      launch_rescan(p, w, rescan_grid, s);
-      launch_learn(p, w, outer, outer, s);
-      *launches += 3 + (cap > 8 ? 3 : 2);
+      launch_cand_exchange(w.xg, w.cand, B, p.ntl, W, p.n_corr, s);
+      launch_learn(p, w, outer, outer, s);  // selection fused (p.fuse_select)
+      *launches += 1 + (cap > 8 ? 3 : 2);
       if (ctx->world > 1) {
         const size_t rows = (size_t)((p.sig_hi - p.sig_lo) * p.ldm);
         if (w.r_hi) {
@@ -455,11 +442,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       launch_corr_tc(p, w, s);
     else
       launch_corr_f64(p, w, full_scores, s);
-    launch_select(p, w, full_scores, s);
-    launch_rescan(p, w, rescan_grid, s);
+    if (!p.fuse_select) launch_select(p, w, full_scores, s);
     const int bound = c->th >= 1.0 ? outer : (int)cap;
     launch_learn(p, w, outer, bound, s);
-    *launches += 3 + (cap > 8 ? 3 : 2);
+    *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
     if (mode == CL_MODE_JOINT) {
       launch_joint_control(p, w, outer, false, s);
       launch_joint_snapshot(p, w, s);
@@ -519,11 +505,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       else
         launch_corr_f64(p, w, full_scores, s);
       cudaEventRecord(ev[4], s);
-      launch_select(p, w, full_scores, s);
-      launch_rescan(p, w, rescan_grid, s);
+      if (!p.fuse_select) launch_select(p, w, full_scores, s);
       cudaEventRecord(ev[2], s);
       launch_learn(p, w, outer, c->th >= 1.0 ? outer : (int)cap, s);
-      launches += 3 + (cap > 8 ? 3 : 2);
+      launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
       if (mode == CL_MODE_JOINT) {
         launch_joint_control(p, w, outer, false, s);
         launch_joint_snapshot(p, w, s);
@@ -1200,7 +1185,6 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   launch_inject_finish(p, w, s);
   launch_corr_f64(p, w, full, s);
   launch_select(p, w, full, s);
-  launch_rescan(p, w, 2 * ctx->sms, s);
   CL_CUDA(ctx, cudaGetLastError());
   CL_CUDA(ctx, cudaMemcpyAsync(bits.data(), w.maskbits, bits.size() * 4,
                                cudaMemcpyDeviceToHost, s));

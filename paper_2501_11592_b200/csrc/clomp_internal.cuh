@@ -22,6 +22,49 @@ constexpr int kCorrTileAtoms = 64;    // fp64 SIMT correlation tile (atoms)
 constexpr int kCorrTileSignals = 64;  // fp64 SIMT correlation tile (signals)
 constexpr int kWarpCap = 32;          // register-resident learning kernel limit
 
+// Correlation summary of one (signal, atom tile): the two largest |scores|
+// with their atoms (the lowest atom wins an exact tie) and the third largest
+// value.  A near-tied selection is re-decided exactly from these alone unless
+// a third atom of the tile also lies inside the error band.
+struct __align__(16) Cand {
+  double v1, v2, v3;
+  int32_t i1, i2;
+};
+
+// Insert score x of atom k into a descending (v1,i1) (v2,i2) v3 summary.
+__host__ __device__ __forceinline__ void cand_insert(double& v1, int& i1, double& v2, int& i2,
+                                                     double& v3, double x, int k) {
+  if (x > v1 || (x == v1 && k < i1)) {
+    v3 = v2;
+    v2 = v1;
+    i2 = i1;
+    v1 = x;
+    i1 = k;
+  } else if (x > v2 || (x == v2 && k < i2)) {
+    v3 = v2;
+    v2 = x;
+    i2 = k;
+  } else if (x > v3) {
+    v3 = x;
+  }
+}
+
+__host__ __device__ __forceinline__ void cand_merge(Cand& a, const Cand& b) {
+  double v1 = a.v1, v2 = a.v2, v3 = a.v3;
+  int i1 = a.i1, i2 = a.i2;
+  cand_insert(v1, i1, v2, i2, v3, b.v1, b.i1);
+  cand_insert(v1, i1, v2, i2, v3, b.v2, b.i2);
+  v3 = v3 > b.v3 ? v3 : b.v3;
+  a.v1 = v1; a.v2 = v2; a.v3 = v3; a.i1 = i1; a.i2 = i2;
+}
+
+__host__ __device__ __forceinline__ Cand cand_empty() {
+  Cand c;
+  c.v1 = c.v2 = c.v3 = -1.0;
+  c.i1 = c.i2 = 0x7fffffff;
+  return c;
+}
+
 struct SolveParams {
   int64_t B, n, m, ldm, cap, ntile;
   int64_t tile_atoms;       // atoms per correlation tile (candidate granularity)
@@ -39,6 +82,8 @@ struct SolveParams {
   // separable 2D operator A = A_c (x) A_r (atom p = i + nr*j, row q = qr + mr*qc)
   int32_t sep;
   int64_t nr, nc, mr, mc, ldr, ldc;
+  // th == 1 selection runs inside the learning kernel (warp per signal)
+  int32_t fuse_select;
 };
 
 struct Work {
@@ -60,21 +105,9 @@ struct Work {
   double* zb = nullptr;            // [B][n] A_r^T Y A_c (b values of every atom)
   double* sep_scratch = nullptr;   // [B][nc][mr] U = R A_c  /  V = A_r C
   double* lpart = nullptr;         // [B][tiles] residual sum-of-squares partials
-  // column sharding: per-shard candidates, [W][B][ntl]
-  double* xg_v1 = nullptr;
-  double* xg_v2 = nullptr;
-  int32_t* xg_i1 = nullptr;
-  // correlation candidates, [B][ntile]
-  double* cand_v1 = nullptr;
-  double* cand_v2 = nullptr;
-  int32_t* cand_i1 = nullptr;
+  Cand* xg = nullptr;            // column sharding: per-shard candidates [W][B][ntl]
+  Cand* cand = nullptr;          // correlation candidates [B][ntile]
   double* scores = nullptr;      // [B][n] |A^T r| (th < 1 path)
-  // fp64 rescans of near-tied selections, indexed by rescan-list slot
-  double* rs_top = nullptr;      // [B] correlation-kernel top1
-  double* rs_delta = nullptr;    // [B] error bound used for that signal
-  int32_t* rs_done = nullptr;    // [B] chunks finished
-  double* rs_cmax = nullptr;     // [B][nchunk] exact max per 64-atom chunk
-  int32_t* rs_ids = nullptr;     // [B][nchunk][1 + 4] atoms attaining it
   // per-signal state
   int32_t* sup = nullptr;        // [B][cap] insertion order
   int32_t* cnt = nullptr;        // [B]
@@ -96,13 +129,13 @@ struct Work {
   uint8_t* conv = nullptr;       // eps break happened
   int32_t* status = nullptr;
   int32_t* changed = nullptr;
-  int32_t* rescan_list = nullptr;  // [B]
+  int32_t* big_list = nullptr;     // [B] signals queued for the block learner
   int32_t* counters = nullptr;     // see Counter
   double* joint = nullptr;         // see Joint
 };
 
 enum Counter {
-  kRescanCount = 0,   // entries in rescan_list this outer iteration
+  kCounter0 = 0,      // (unused)
   kActiveCount = 1,   // signals still iterating after this outer iteration
   kMaxCount = 2,      // max support size over the batch
   kRescanTotal = 3,   // rescans over the whole solve
@@ -150,8 +183,6 @@ void launch_init(const SolveParams& p, const Work& w, const float* y_in,
                  int y_layout, bool y_on_device_signal_major, cudaStream_t s);
 void launch_select(const SolveParams& p, const Work& w, bool full_scores,
                    cudaStream_t s);
-void launch_rescan(const SolveParams& p, const Work& w, int grid,
-                   cudaStream_t s);
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                   cudaStream_t s);
 void launch_joint_control(const SolveParams& p, const Work& w, int outer,
@@ -170,8 +201,7 @@ void nccl_comm_destroy(void* comm);
 bool nccl_allgather_inplace(void* comm, void* buf, size_t count_per_rank, int bytes_per_elem,
                             int rank, cudaStream_t s);
 bool nccl_allreduce_sum_i32(void* comm, int32_t* buf, size_t count, cudaStream_t s);
-void launch_cand_exchange(const double* g1, const double* g2, const int32_t* gi, double* v1,
-                          double* v2, int32_t* i1, int64_t B, int64_t ntl, int world,
+void launch_cand_exchange(const Cand* g, Cand* cand, int64_t B, int64_t ntl, int world,
                           int64_t atoms_per_rank, cudaStream_t s);
 
 // Whole per-signal solve in one persistent block per signal (small problems).

@@ -5,8 +5,8 @@
 // learns signals [r B/W, (r+1) B/W); every rank keeps the whole dictionary for
 // the support gathers (256 MB fp32 at config 3).  Per outer iteration:
 //   K1 on the local atom shard for all B residuals -> per (signal, tile)
-//   (top1, argmax, top2);  ncclAllGather of those candidates (B x tiles x
-//   20 bytes: ~330 KB at config 3, W = 8);  the selection rule then runs on the
+//   candidate records (Cand: top-2 atoms + third value);  ncclAllGather of
+//   those (B x tiles x 32 bytes: ~0.5 MB at config 3, W = 8);  the selection rule then runs on the
 //   owner rank over the complete candidate table exactly as on one GPU (the
 //   per-signal (max, index) reduction plus the top-2 gap that decides whether
 //   the fp64 rescan is needed);  learning on the owner;  ncclAllGather of the
@@ -58,20 +58,18 @@ NcclApi& nccl() {
   return api;
 }
 
-// cand[b][r*ntl + tl] <- gathered[r][b][tl], argmax shifted to global atoms.
-__global__ void k_cand_exchange(const double* __restrict__ g1, const double* __restrict__ g2,
-                                const int32_t* __restrict__ gi, double* __restrict__ v1,
-                                double* __restrict__ v2, int32_t* __restrict__ i1, int64_t B,
+// cand[b][r*ntl + tl] <- gathered[r][b][tl], atoms shifted to global numbers.
+__global__ void k_cand_exchange(const Cand* __restrict__ g, Cand* __restrict__ cand, int64_t B,
                                 int64_t ntl, int world, int64_t atoms_per_rank) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)world * B * ntl;
   if (e >= total) return;
   const int64_t r = e / (B * ntl), rem = e % (B * ntl), b = rem / ntl, tl = rem % ntl;
-  const int64_t o = b * (world * ntl) + r * ntl + tl;
-  v1[o] = g1[e];
-  v2[o] = g2[e];
-  const int32_t k = gi[e];
-  i1[o] = (k >= 0 && k != 0x7fffffff) ? (int32_t)(k + r * atoms_per_rank) : k;
+  Cand c = g[e];
+  const int32_t sh = (int32_t)(r * atoms_per_rank);
+  if (c.i1 >= 0 && c.i1 != 0x7fffffff) c.i1 += sh;
+  if (c.i2 >= 0 && c.i2 != 0x7fffffff) c.i2 += sh;
+  cand[b * (world * ntl) + r * ntl + tl] = c;
 }
 
 }  // namespace
@@ -116,7 +114,8 @@ void nccl_comm_destroy(void* comm) {
 bool nccl_allgather_inplace(void* comm, void* buf, size_t count_per_rank, int bytes_per_elem,
                             int rank, cudaStream_t s) {
   NcclApi& a = nccl();
-  ncclDataType_t t = bytes_per_elem == 8 ? ncclFloat64 : (bytes_per_elem == 4 ? ncclInt32 : ncclUint8);
+  const ncclDataType_t t =
+      bytes_per_elem == 8 ? ncclFloat64 : (bytes_per_elem == 4 ? ncclInt32 : ncclUint8);
   char* base = static_cast<char*>(buf);
   return a.allGather(base + (size_t)rank * count_per_rank * bytes_per_elem, buf, count_per_rank,
                      t, static_cast<ncclComm_t>(comm), s) == ncclSuccess;
@@ -135,12 +134,11 @@ bool nccl_allreduce_sum_i32(void* comm, int32_t* buf, size_t count, cudaStream_t
          ncclSuccess;
 }
 
-void launch_cand_exchange(const double* g1, const double* g2, const int32_t* gi, double* v1,
-                          double* v2, int32_t* i1, int64_t B, int64_t ntl, int world,
+void launch_cand_exchange(const Cand* g, Cand* cand, int64_t B, int64_t ntl, int world,
                           int64_t atoms_per_rank, cudaStream_t s) {
   const int64_t total = (int64_t)world * B * ntl;
-  k_cand_exchange<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g1, g2, gi, v1, v2, i1, B, ntl,
-                                                                   world, atoms_per_rank);
+  k_cand_exchange<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g, cand, B, ntl, world,
+                                                                   atoms_per_rank);
 }
 
 }  // namespace clb

@@ -20,30 +20,14 @@ constexpr int BM = kCorrTileAtoms;
 constexpr int BN = kCorrTileSignals;
 constexpr int BK = 16;
 
-__device__ __forceinline__ void top2_merge(double& v1, int& i1, double& v2,
-                                           double w1, int k1, double w2) {
-  // Lowest index wins an exact tie; the loser's value becomes the runner-up,
-  // which makes the gap 0 and sends the signal to the fp64 rescan.
-  if (w1 > v1 || (w1 == v1 && k1 < i1)) {
-    v2 = fmax(v1, w2);
-    v1 = w1;
-    i1 = k1;
-  } else {
-    v2 = fmax(v2, w1);
-  }
-}
-
 __global__ void __launch_bounds__(256)
 k_corr_f64(const float* __restrict__ at, const double* __restrict__ r,
            const int32_t* __restrict__ active, int64_t n, int64_t B,
-           int64_t ldm, int64_t ntile, double* __restrict__ cand_v1,
-           double* __restrict__ cand_v2, int32_t* __restrict__ cand_i1,
+           int64_t ldm, int64_t ntile, Cand* __restrict__ cand,
            double* __restrict__ scores) {
   __shared__ double As[BK][BM + 2];
   __shared__ double Rs[BK][BN + 2];
-  __shared__ double red_v1[16][BN];
-  __shared__ double red_v2[16][BN];
-  __shared__ int red_i1[16][BN];
+  __shared__ Cand red[8][BN];
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -115,32 +99,36 @@ k_corr_f64(const float* __restrict__ at, const double* __restrict__ r,
     }
   }
 
-  // Per-signal top-2 over this thread's 4 atoms, then across the 16 ty rows.
+  // Per-signal candidate record over this thread's 4 atoms (ascending, so the
+  // lowest atom wins an exact tie), then across the 16 ty rows (two rounds
+  // through an 8-row shared buffer).
+  Cand c[4];
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) {
-    double v1 = -1.0, v2 = -1.0;
-    int i1 = 0x7fffffff;
+    c[jj] = cand_empty();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t j = j0 + ty * 4 + i;
-      if (j < n) top2_merge(v1, i1, v2, fabs(acc[i][jj]), (int)j, -1.0);
+      if (j < n) cand_insert(c[jj].v1, c[jj].i1, c[jj].v2, c[jj].i2, c[jj].v3, fabs(acc[i][jj]), (int)j);
     }
-    red_v1[ty][tx * 4 + jj] = v1;
-    red_v2[ty][tx * 4 + jj] = v2;
-    red_i1[ty][tx * 4 + jj] = i1;
   }
+  if (ty >= 8)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) red[ty - 8][tx * 4 + jj] = c[jj];
+  __syncthreads();
+  if (ty < 8)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      cand_merge(c[jj], red[ty][tx * 4 + jj]);
+      red[ty][tx * 4 + jj] = c[jj];
+    }
   __syncthreads();
   if (tid < BN) {
     const int64_t b = b0 + tid;
     if (b < B) {
-      double v1 = red_v1[0][tid], v2 = red_v2[0][tid];
-      int i1 = red_i1[0][tid];
-      for (int t = 1; t < 16; ++t)
-        top2_merge(v1, i1, v2, red_v1[t][tid], red_i1[t][tid], red_v2[t][tid]);
-      const int64_t o = b * ntile + blockIdx.x;
-      cand_v1[o] = v1;
-      cand_v2[o] = v2;
-      cand_i1[o] = i1;
+      Cand m = red[0][tid];
+      for (int t = 1; t < 8; ++t) cand_merge(m, red[t][tid]);
+      cand[b * ntile + blockIdx.x] = m;
     }
   }
 }
@@ -154,8 +142,7 @@ void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
   // exchange; single-GPU: atom0 = 0, n_corr = n, ntl = ntile).
   dim3 grid((unsigned)((p.n_corr + BM - 1) / BM), (unsigned)((p.B + BN - 1) / BN));
   k_corr_f64<<<grid, 256, 0, s>>>(w.at32 + p.atom0 * p.ldm, w.r64, w.active, p.n_corr, p.B,
-                                  p.ldm, p.ntl, w.cand_v1, w.cand_v2, w.cand_i1,
-                                  full_scores ? w.scores : nullptr);
+                                  p.ldm, p.ntl, w.cand, full_scores ? w.scores : nullptr);
 }
 
 }  // namespace clb

@@ -11,13 +11,14 @@
 // product is accumulated as hi*hi + hi*lo + lo*hi in fp32 in TMEM (3xTF32,
 // ~fp32 accuracy; the dropped lo*lo term is < 2^-20 |a||r|).
 //
-// Roles (128 threads): warp 0 lane 0 issues TMA into a 2-stage ring,
+// Roles (128 threads): warp 0 lane 0 issues TMA into a 4-stage ring,
 // warp 1 lane 0 issues tcgen05.mma (single thread per CTA), warp 2 owns the
 // TMEM allocation.  After the last commit all four warps drain TMEM with
-// tcgen05.ld: thread = signal (its TMEM lane), so the per-signal top-2 over the
-// tile's 256 atoms is a register scan with no shuffles.  Only (top1, argmax,
-// top2) per (signal, atom tile) reaches HBM; the selection kernel merges tiles
-// and sends near-ties (gap inside the 3xTF32 error bound) to an fp64 rescan.
+// tcgen05.ld: thread = signal (its TMEM lane), so the per-signal candidate
+// record over the tile's 256 atoms (top-2 atoms + third value, Cand) is a
+// register scan with no shuffles.  Only that record per (signal, atom tile)
+// reaches HBM; the selection merges tiles and re-decides near-ties (gap inside
+// the 3xTF32 error bound) from exact fp64 scores of the few atoms in the band.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -167,6 +168,26 @@ __device__ __forceinline__ void tmem_ld_32(uint32_t taddr, float (&v)[32]) {
 }
 
 // ---------------------------------------------------------------- the kernel
+// Insert 32 consecutive scores (atoms ka, ka+1, ...) into a signal's
+// candidate summary.  Branch-free because the lanes hold different signals:
+// sorted insert of the values by min/max, indices by two predicates on the old
+// values; ascending atoms with strict compares keep the lowest atom on ties.
+template <bool CHECK>
+__device__ __forceinline__ void cand_scan32(const float (&v)[32], int ka, int lim, float& v1,
+                                            int& i1, float& v2, int& i2, float& v3) {
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const float x = (!CHECK || q < lim) ? fabsf(v[q]) : -1.f;
+    const int k = ka + q;
+    const bool g1 = x > v1, g2 = x > v2;
+    i2 = g1 ? i1 : (g2 ? k : i2);
+    i1 = g1 ? k : i1;
+    v3 = fmaxf(v3, fminf(x, v2));
+    v2 = fmaxf(v2, fminf(x, v1));
+    v1 = fmaxf(v1, x);
+  }
+}
+
 // CL: CTAs per cluster along the signal dimension.  With CL > 1 the atom tile
 // (the operand every CTA of the cluster shares) is fetched once per cluster:
 // CTA r loads rows [r*TN/CL, (r+1)*TN/CL) of A_hi/A_lo and multicasts them, and
@@ -176,8 +197,7 @@ __global__ void __launch_bounds__(128, 1)
 k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
           const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
           int64_t n, int64_t B, int kblocks, int64_t ntile, const int32_t* __restrict__ active,
-          double* __restrict__ cand_v1, double* __restrict__ cand_v2,
-          int32_t* __restrict__ cand_i1, float* __restrict__ scores_dbg) {
+          Cand* __restrict__ cand, float* __restrict__ scores_dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -282,8 +302,10 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   mbar_wait(accum, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int64_t b = m0 + warp * 32 + lane;
-  float v1 = -1.f, v2 = -1.f;
-  int i1 = 0x7fffffff;
+  // Candidate record (Cand) of this signal over the tile's atoms, scanned in
+  // ascending order so strict comparisons give the lowest atom on ties.
+  float v1 = -1.f, v2 = -1.f, v3 = -1.f;
+  int i1 = 0x7fffffff, i2 = 0x7fffffff;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
 #pragma unroll 1
   for (int c = 0; c < TN / 32; ++c) {
@@ -294,24 +316,19 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
       for (int q = 0; q < 32; ++q)
         if (a0 + q < n) scores_dbg[b * n + a0 + q] = v[q];
     }
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const float x = fabsf(v[q]);
-      const bool ok = a0 + q < n;
-      if (ok && x > v1) {
-        v2 = v1;
-        v1 = x;
-        i1 = (int)(a0 + q);
-      } else if (ok && x > v2) {
-        v2 = x;
-      }
-    }
+    if (a0 + 32 <= n)
+      cand_scan32<false>(v, (int)a0, 32, v1, i1, v2, i2, v3);
+    else  // ragged last tile: atoms past n never enter
+      cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
   }
   if (b < B) {
-    const int64_t o = b * ntile + blockIdx.x;
-    cand_v1[o] = (double)v1;
-    cand_v2[o] = (double)v2;
-    cand_i1[o] = i1;
+    Cand r;
+    r.v1 = (double)v1;
+    r.v2 = (double)v2;
+    r.v3 = (double)v3;
+    r.i1 = i1;
+    r.i2 = i2;
+    cand[b * ntile + blockIdx.x] = r;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -427,8 +444,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
     cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     dim3 grid((unsigned)((p.n_corr + TN - 1) / TN), (unsigned)mtiles);
     k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n_corr, p.B, kblocks, p.ntl,
-                                               w.active, w.cand_v1, w.cand_v2, w.cand_i1,
-                                               scores_dbg);
+                                               w.active, w.cand, scores_dbg);
     return true;
   }
   cudaFuncSetAttribute(k_corr_tc<kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -447,8 +463,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
-                            kblocks, p.ntl, w.active, w.cand_v1, w.cand_v2, w.cand_i1,
-                            scores_dbg) == cudaSuccess;
+                            kblocks, p.ntl, w.active, w.cand, scores_dbg) == cudaSuccess;
 }
 
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {

@@ -108,50 +108,180 @@ __global__ void k_init(SolveParams p, Work w, const float* __restrict__ y_in,
 }
 
 // --------------------------------------------------------------- select
-// K1c for th == 1: merge the per-tile top-2 candidates, accept a clear winner,
-// queue the signal for an fp64 rescan when the top-2 gap is inside the
-// correlation error bound (or tied: all ties must be injected).
-__global__ void k_select_top(SolveParams p, Work w) {
-  const int64_t b = p.sig_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= p.sig_hi || !w.active[b]) return;
-  double v1 = -1.0, v2 = -1.0;
-  int i1 = 0x7fffffff;
-  const int64_t base = b * p.ntile;
-  for (int64_t t = 0; t < p.ntile; ++t) {
-    const double c1 = w.cand_v1[base + t], c2 = w.cand_v2[base + t];
-    const int k1 = w.cand_i1[base + t];
-    if (c1 > v1 || (c1 == v1 && k1 < i1)) {
-      v2 = fmax(v1, c2);
-      v1 = c1;
-      i1 = k1;
-    } else {
-      v2 = fmax(v2, c1);
+// K1c for th == 1, one warp per signal: merge the per-tile candidate records,
+// accept a clear winner, and re-decide a near-tie (top-2 gap inside the
+// correlation error bound, or tied) from exact fp64 scores of every atom whose
+// approximate score lies within 2*delta of the top: an atom outside that band
+// cannot reach the exact maximum.  The records name the tile's two best atoms
+// and bound the rest by the third value, so normally only those atoms are
+// rescored; a tile whose third value is in the band too is rescored whole.
+// Every tie with the exact maximum is injected in ascending atom order
+// (inject_from_scores, clomp.cpp:41-53).
+
+// Exact |a_j . r| for up to 8 consecutive atoms j0 .. j0+cnt-1 (fp64 products
+// of the fp32 atoms with the fp64 residual, one fixed summation order for
+// every atom, so identical atoms score bitwise identically).  All lanes get
+// every value.
+__device__ __forceinline__ void exact_scores8(const SolveParams& p, const Work& w,
+                                              const double* r, int64_t j0, int cnt,
+                                              double (&out)[8], int lane) {
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 2
+  for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
+    const double2 r01 = *reinterpret_cast<const double2*>(r + i);
+    const double2 r23 = *reinterpret_cast<const double2*>(r + i + 2);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (u < cnt) {
+        const float4 a = *reinterpret_cast<const float4*>(w.at32 + (j0 + u) * p.ldm + i);
+        acc[u] = fma(f2d(a.x), r01.x, acc[u]);
+        acc[u] = fma(f2d(a.y), r01.y, acc[u]);
+        acc[u] = fma(f2d(a.z), r23.x, acc[u]);
+        acc[u] = fma(f2d(a.w), r23.y, acc[u]);
+      }
     }
   }
-  w.changed[b] = 0;
-  if (!(v1 > 0.0)) return;  // zero column: inject nothing (clomp.cpp:48)
-  const double delta = p.delta_rel * p.colnorm_max * sqrt(w.loss[b]);
-  if (v1 - v2 <= delta) {
-    const int slot = atomicAdd(&w.counters[kRescanCount], 1);
-    w.rescan_list[slot] = (int32_t)b;
-    w.rs_top[slot] = v1;
-    w.rs_delta[slot] = delta;
-    w.rs_done[slot] = 0;
-    return;
-  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) out[u] = u < cnt ? fabs(warp_sum(acc[u])) : -1.0;
+}
+
+__device__ __forceinline__ double exact_score(const SolveParams& p, const Work& w,
+                                              const double* r, int64_t j, int lane) {
+  double v[8];
+  exact_scores8(p, w, r, j, 1, v, lane);
+  return v[0];
+}
+
+// Support update of one picked atom (lane 0): skip atoms already selected,
+// stop the signal with kStatusCapacity when the support is full.
+struct PickState {
+  int t, added, over;
+};
+
+__device__ __forceinline__ void pick_atom(const SolveParams& p, const Work& w, int64_t b,
+                                          int32_t j, PickState& ps) {
   uint32_t* mb = w.maskbits + b * p.mwords;
-  if (mask_test(mb, i1)) return;  // argmax already selected: mask unchanged
-  const int t = w.cnt[b];
-  if (t >= p.cap) {
+  if (mask_test(mb, j)) return;  // already in the support: mask unchanged
+  if (ps.t < p.cap) {
+    w.sup[b * p.cap + ps.t] = j;
+    mb[j >> 5] |= 1u << (j & 31);
+    ++ps.t;
+    ++ps.added;
+  } else {
+    ps.over = 1;
+  }
+}
+
+__device__ __forceinline__ void pick_finish(const SolveParams& p, const Work& w, int64_t b,
+                                            const PickState& ps) {
+  w.cnt[b] = ps.t;
+  w.changed[b] = ps.added > 0;
+  if (ps.over) {
     w.status[b] = kStatusCapacity;
     w.active[b] = 0;
-    return;
   }
-  mb[i1 >> 5] |= 1u << (i1 & 31);
-  w.sup[b * p.cap + t] = i1;
-  w.cnt[b] = t + 1;
-  w.changed[b] = 1;
-  atomicMax(&w.counters[kMaxCount], t + 1);
+  if (ps.added) atomicMax(&w.counters[kMaxCount], ps.t);
+}
+
+// One pass over the atoms inside the band (ascending atom order).  Pass 0
+// returns the exact maximum; pass 1 picks every atom attaining M.
+__device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, double cut,
+                            const double* r, int pass, double M, PickState& ps, int lane) {
+  const Cand* cd = w.cand + b * p.ntile;
+  for (int64_t t0 = 0; t0 < p.ntile; t0 += 32) {
+    const int64_t tl = t0 + lane;
+    const Cand c = tl < p.ntile ? cd[tl] : cand_empty();
+    unsigned any = __ballot_sync(kFull, c.v1 >= cut);
+    while (any) {
+      const int src = __ffs(any) - 1;
+      any &= any - 1;
+      const double cv2 = __shfl_sync(kFull, c.v2, src), cv3 = __shfl_sync(kFull, c.v3, src);
+      const int ci1 = __shfl_sync(kFull, c.i1, src), ci2 = __shfl_sync(kFull, c.i2, src);
+      if (cv3 >= cut) {  // a third atom of this tile is in the band: whole tile
+        const int64_t a0 = (t0 + src) * p.tile_atoms;
+        const int64_t a1 = a0 + p.tile_atoms < p.n ? a0 + p.tile_atoms : p.n;
+        for (int64_t j0 = a0; j0 < a1; j0 += 8) {
+          const int cnt = (int)(a1 - j0 < 8 ? a1 - j0 : 8);
+          double v[8];
+          exact_scores8(p, w, r, j0, cnt, v, lane);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (u >= cnt) continue;
+            if (pass == 0) M = fmax(M, v[u]);
+            else if (v[u] == M && lane == 0) pick_atom(p, w, b, (int32_t)(j0 + u), ps);
+          }
+        }
+      } else {
+        int ja = ci1, jb = cv2 >= cut ? ci2 : -1;
+        if (jb >= 0 && jb < ja) {
+          const int tmp = ja;
+          ja = jb;
+          jb = tmp;
+        }
+        const double va = exact_score(p, w, r, ja, lane);
+        const double vb = jb >= 0 ? exact_score(p, w, r, jb, lane) : -1.0;
+        if (pass == 0) {
+          M = fmax(M, fmax(va, vb));
+        } else if (lane == 0) {
+          if (va == M) pick_atom(p, w, b, ja, ps);
+          if (jb >= 0 && vb == M) pick_atom(p, w, b, jb, ps);
+        }
+      }
+    }
+  }
+  return M;
+}
+
+__device__ void select_top_warp(const SolveParams& p, const Work& w, int64_t b, int lane) {
+  const Cand* cd = w.cand + b * p.ntile;
+  double v1 = -1.0, v2 = -1.0;
+  int i1 = 0x7fffffff;
+  for (int64_t t = lane; t < p.ntile; t += 32) {
+    const Cand c = cd[t];
+    if (c.v1 > v1 || (c.v1 == v1 && c.i1 < i1)) {
+      v2 = fmax(v1, c.v2);
+      v1 = c.v1;
+      i1 = c.i1;
+    } else {
+      v2 = fmax(v2, c.v1);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov1 = __shfl_xor_sync(kFull, v1, o), ov2 = __shfl_xor_sync(kFull, v2, o);
+    const int oi1 = __shfl_xor_sync(kFull, i1, o);
+    if (ov1 > v1 || (ov1 == v1 && oi1 < i1)) {
+      v2 = fmax(v1, ov2);
+      v1 = ov1;
+      i1 = oi1;
+    } else {
+      v2 = fmax(v2, ov1);
+    }
+  }
+  PickState ps{w.cnt[b], 0, 0};
+  if (v1 > 0.0) {  // else zero column: inject nothing (clomp.cpp:48)
+    const double delta = p.delta_rel * p.colnorm_max * sqrt(w.loss[b]);
+    if (v1 - v2 > delta) {
+      if (lane == 0) pick_atom(p, w, b, i1, ps);
+    } else {
+      if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
+      const double cut = v1 - 2.0 * delta;
+      const double* r = w.r64 + b * p.ldm;
+      const double M = band_pass(p, w, b, cut, r, 0, -1.0, ps, lane);
+      if (M > 0.0) band_pass(p, w, b, cut, r, 1, M, ps, lane);
+    }
+  }
+  if (lane == 0) pick_finish(p, w, b, ps);
+  __syncwarp();
+}
+
+__global__ void k_select_top(SolveParams p, Work w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = p.sig_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= p.sig_hi || !w.active[b]) return;
+  select_top_warp(p, w, b, lane);
 }
 
 // Ordered append of every j with score(j) >= cut that is not yet in the mask
@@ -204,146 +334,6 @@ __global__ void k_select_thresh(SolveParams p, Work w) {
   if (cmax == 0.0) return;
   const double cut = p.th * cmax;
   warp_threshold_append(p, w, b, cut, [&](int64_t j) { return sc[j]; }, lane);
-}
-
-// Re-decide a near-tied th == 1 selection from fp64 scores.  Only atom tiles
-// whose correlation-kernel top1 lies within 2*delta of the best tile's top1
-// can hold the exact maximum or a tie with it, so only those are rescored:
-// exact fp64 dot products of the fp32 atoms with the fp64 residual.  Work
-// items are (queued signal, 64-atom chunk) spread over the whole grid; each
-// chunk records its exact max and the atoms attaining it, and the block that
-// completes a signal's last chunk applies inject_from_scores (clomp.cpp:45-51)
-// with every tie.
-constexpr int kChunk = 64;
-constexpr int kChunkTies = 4;
-
-__global__ void __launch_bounds__(256) k_rescan(SolveParams p, Work w) {
-  __shared__ double wmax[8];
-  __shared__ int32_t wids[8][kChunkTies];
-  __shared__ int wnid[8];
-  __shared__ int s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int count = w.counters[kRescanCount];
-  const int nchunk = (int)((p.ntile * p.tile_atoms + kChunk - 1) / kChunk);
-  const int64_t items = (int64_t)count * nchunk;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int li = (int)(it / nchunk), ch = (int)(it % nchunk);
-    const int64_t b = w.rescan_list[li];
-    const int64_t tile = (int64_t)ch * kChunk / p.tile_atoms;
-    const double cut_tile = w.rs_top[li] - 2.0 * w.rs_delta[li];
-    double* cm = w.rs_cmax + (int64_t)li * nchunk;
-    int32_t* cids = w.rs_ids + ((int64_t)li * nchunk + ch) * (kChunkTies + 1);
-    if (w.cand_v1[b * p.ntile + tile] >= cut_tile) {
-      // 8 warps x 8 atoms, 8 independent dot products per warp.
-      const int64_t j0 = (int64_t)ch * kChunk + warp * 8;
-      const double* r = w.r64 + b * p.ldm;
-      double acc[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-#pragma unroll 2
-      for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
-        const double2 r01 = *reinterpret_cast<const double2*>(r + i);
-        const double2 r23 = *reinterpret_cast<const double2*>(r + i + 2);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (j0 + u < p.n) {
-            const float4 a = *reinterpret_cast<const float4*>(w.at32 + (j0 + u) * p.ldm + i);
-            acc[u] = fma(f2d(a.x), r01.x, acc[u]);
-            acc[u] = fma(f2d(a.y), r01.y, acc[u]);
-            acc[u] = fma(f2d(a.z), r23.x, acc[u]);
-            acc[u] = fma(f2d(a.w), r23.y, acc[u]);
-          }
-        }
-      }
-      double best = -1.0;
-      int nid = 0;
-      int32_t ids[kChunkTies];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double v = fabs(warp_sum(acc[u]));
-        if (j0 + u < p.n) {
-          if (v > best) {
-            best = v;
-            nid = 0;
-          }
-          if (v == best && nid < kChunkTies) ids[nid++] = (int32_t)(j0 + u);
-          else if (v == best) nid = kChunkTies + 1;  // overflow marker
-        }
-      }
-      if (lane == 0) {
-        wmax[warp] = best;
-        wnid[warp] = nid;
-        for (int q = 0; q < kChunkTies && q < nid; ++q) wids[warp][q] = ids[q];
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double m = -1.0;
-        for (int q = 0; q < 8; ++q) m = fmax(m, wmax[q]);
-        int n = 0;
-        for (int q = 0; q < 8; ++q)
-          if (wmax[q] == m) {
-            if (wnid[q] > kChunkTies) n = kChunkTies + 1;
-            for (int e = 0; e < wnid[q] && e < kChunkTies; ++e) {
-              if (n < kChunkTies) cids[1 + n] = wids[q][e];
-              ++n;
-            }
-          }
-        cm[ch] = m;
-        cids[0] = n;
-      }
-    } else if (tid == 0) {
-      cm[ch] = -1.0;  // cannot hold the maximum
-      cids[0] = 0;
-    }
-    // The block completing the last chunk of this signal finalises it.
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(&w.rs_done[li], 1) == nchunk - 1;
-    }
-    __syncthreads();
-    if (s_last && tid == 0) {
-      __threadfence();
-      double m = 0.0;
-      for (int q = 0; q < nchunk; ++q) m = fmax(m, cm[q]);
-      int32_t picks[kChunkTies * 4];
-      int np = 0, over = 0;
-      uint32_t* mb = w.maskbits + b * p.mwords;
-      if (m > 0.0) {
-        for (int q = 0; q < nchunk; ++q) {
-          if (cm[q] != m) continue;  // th == 1: only exact ties with the max
-          const int32_t* ci = w.rs_ids + ((int64_t)li * nchunk + q) * (kChunkTies + 1);
-          if (ci[0] > kChunkTies) over = 1;
-          for (int e = 0; e < ci[0] && e < kChunkTies; ++e) {
-            const int32_t j = ci[1 + e];
-            if (mask_test(mb, j)) continue;
-            if (np < kChunkTies * 4) picks[np++] = j;
-            else over = 1;
-          }
-        }
-      }
-      // picks arrive in ascending chunk / atom order already
-      int t = w.cnt[b];
-      for (int a = 0; a < np; ++a) {
-        if (t < p.cap) {
-          const int32_t j = picks[a];
-          w.sup[b * p.cap + t] = j;
-          mb[j >> 5] |= 1u << (j & 31);
-          ++t;
-        } else {
-          over = 1;
-        }
-      }
-      w.cnt[b] = t;
-      w.changed[b] = np > 0;
-      if (over) {
-        w.status[b] = kStatusCapacity;
-        w.active[b] = 0;
-      }
-      if (np) atomicMax(&w.counters[kMaxCount], t);
-      atomicAdd(&w.counters[kRescanTotal], 1);
-    }
-    __syncthreads();
-  }
 }
 
 // ------------------------------------------------------ stopping rules
@@ -531,17 +521,19 @@ __device__ __forceinline__ void square_dmma(double* buf, int lane) {
     for (int K = 0; K < NK; ++K) f[I][K] = buf[(8 * I + r) * LD + 4 * K + c];
   __syncwarp();
 #if CL_SQ_ILP
+  // Upper block triangle only (J >= I), all blocks' accumulators live at once
+  // (independent DMMA chains); off-diagonal blocks also written transposed.
   double acc[NI][NI][2];
 #pragma unroll
   for (int I = 0; I < NI; ++I)
 #pragma unroll
-    for (int J = 0; J < NI; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+    for (int J = I; J < NI; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
 #pragma unroll
   for (int K = 0; K < NK; ++K)
 #pragma unroll
     for (int I = 0; I < NI; ++I)
 #pragma unroll
-      for (int J = 0; J < NI; ++J)
+      for (int J = I; J < NI; ++J)
         asm volatile(
             "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(acc[I][J][0]), "+d"(acc[I][J][1])
@@ -549,27 +541,40 @@ __device__ __forceinline__ void square_dmma(double* buf, int lane) {
 #pragma unroll
   for (int I = 0; I < NI; ++I)
 #pragma unroll
-    for (int J = 0; J < NI; ++J)
+    for (int J = I; J < NI; ++J) {
       *reinterpret_cast<double2*>(buf + (8 * I + r) * LD + 8 * J + 2 * c) =
           make_double2(acc[I][J][0], acc[I][J][1]);
+      if (J != I) {
+        buf[(8 * J + 2 * c) * LD + 8 * I + r] = acc[I][J][0];
+        buf[(8 * J + 2 * c + 1) * LD + 8 * I + r] = acc[I][J][1];
+      }
+    }
 #else
+  // Upper block triangle only (J >= I): the product is symmetric, so each
+  // off-diagonal 8x8 block is also written transposed (NI(NI+1)/2 of NI^2
+  // blocks computed: 10 of 16 at T = 32).
 #pragma unroll
   for (int I = 0; I < NI; ++I) {
     double acc[NI][2];
 #pragma unroll
-    for (int J = 0; J < NI; ++J) acc[J][0] = acc[J][1] = 0.0;
+    for (int J = I; J < NI; ++J) acc[J][0] = acc[J][1] = 0.0;
 #pragma unroll
     for (int K = 0; K < NK; ++K)
 #pragma unroll
-      for (int J = 0; J < NI; ++J)
+      for (int J = I; J < NI; ++J)
         asm volatile(
             "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(acc[J][0]), "+d"(acc[J][1])
             : "d"(f[I][K]), "d"(f[J][K]));
 #pragma unroll
-    for (int J = 0; J < NI; ++J)
+    for (int J = I; J < NI; ++J) {
       *reinterpret_cast<double2*>(buf + (8 * I + r) * LD + 8 * J + 2 * c) =
           make_double2(acc[J][0], acc[J][1]);
+      if (J != I) {
+        buf[(8 * J + 2 * c) * LD + 8 * I + r] = acc[J][0];
+        buf[(8 * J + 2 * c + 1) * LD + 8 * I + r] = acc[J][1];
+      }
+    }
   }
 #endif
   __syncwarp();
@@ -628,7 +633,7 @@ __device__ void epochs_plain(double (&g)[TB], double& c, double d, double* cs,
     v = vv;
     // M <- M^2; g <- row `lane` of M (read as a column, conflict-free, exact
     // by symmetry).
-    if (lane < T) {
+    if (l == 0 && lane < T) {  // later levels: s1 already holds M (last square)
 #pragma unroll
       for (int j = 0; j < T; ++j) s1[j * LD + lane] = g[j];
     }
@@ -871,7 +876,8 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   const double twolr = 2.0 * p.lr;
 #pragma unroll
   for (int j = 0; j < TB; ++j) {
-    const double gij = (lane < t && j < t) ? G[(int64_t)lane * cap + j] : 0.0;
+    // G[lane][j] read as G[j][lane] (G is stored symmetric): coalesced
+    const double gij = (lane < t && j < t) ? G[(int64_t)j * cap + lane] : 0.0;
     if (OPT == 0)
       g[j] = (lane < t && j == lane) ? 1.0 - twolr * gij : -(twolr * gij);
     else
@@ -882,8 +888,10 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
     c = w.coef[b * cap + lane];
     bi = w.bvec[b * cap + lane];
     if (OPT == 0) bi = twolr * bi;
-    m1 = w.mom1[b * cap + lane];
-    m2 = w.mom2[b * cap + lane];
+    if (OPT != 0) {
+      m1 = w.mom1[b * cap + lane];
+      m2 = w.mom2[b * cap + lane];
+    }
   }
   cs[lane] = c;
   __syncwarp();
@@ -1067,6 +1075,10 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi || !w.active[b]) return;
+  if (p.fuse_select) {  // this iteration's th == 1 selection (K1c) first
+    select_top_warp(p, w, b, lane);
+    if (!w.active[b]) return;
+  }
   if (w.cnt[b] > TB) {
     if (lane == 0) {
       const int slot = atomicAdd(&w.counters[kBigCount], 1);
@@ -1562,14 +1574,9 @@ void launch_select(const SolveParams& p, const Work& w, bool full_scores,
     const int64_t blocks = (nsig * 32 + 255) / 256;
     k_select_thresh<<<(unsigned)blocks, 256, 0, s>>>(p, w);
   } else {
-    const int64_t blocks = (nsig + 255) / 256;
+    const int64_t blocks = (nsig * 32 + 255) / 256;
     k_select_top<<<(unsigned)blocks, 256, 0, s>>>(p, w);
   }
-}
-
-void launch_rescan(const SolveParams& p, const Work& w, int grid,
-                   cudaStream_t s) {
-  k_rescan<<<grid, 256, 0, s>>>(p, w);
 }
 
 static size_t block_smem_bytes(int64_t cap, bool smem_g) {
@@ -1596,7 +1603,7 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
 
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                   cudaStream_t s) {
-  int32_t* big_list = w.rescan_list + p.B;  // second half of the list buffer
+  int32_t* big_list = w.big_list;
   cudaMemsetAsync(&w.counters[kBigCount], 0, sizeof(int32_t), s);
   // max_cnt: upper bound on the support size after this iteration's select
   // (ties can exceed it; those signals fall through to the block kernel).
