@@ -1062,8 +1062,14 @@ k_resid_w(SolveParams p, Work w, int outer) {
 template <int TB>
 constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
 
+#ifndef CL_LEARN32_MINB
+#define CL_LEARN32_MINB 8
+#endif
+#ifndef CL_LEARN16_MINB
+#define CL_LEARN16_MINB 4
+#endif
 template <int TB>
-constexpr int learn_min_blocks() { return TB == 32 ? 6 : 4; }
+constexpr int learn_min_blocks() { return TB == 32 ? CL_LEARN32_MINB : CL_LEARN16_MINB; }
 
 template <int TB, int OPT>
 __global__ void __launch_bounds__(32 * learn_warps<TB>(), learn_min_blocks<TB>())
