@@ -698,7 +698,8 @@ __device__ __forceinline__ double transpose_reduce(double (&acc)[N], int lane) {
 // the measurements) and are reduced together by transpose_reduce32.
 template <int TB>
 __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
-                                 int t0, int t, int lane, const int32_t* sups) {
+                                 int t0, int t, int lane, const int32_t* sups,
+                                 double* sG, int lds) {
   const int64_t cap = p.cap, ldm = p.ldm;
   double* G = w.gram + b * cap * cap;
   const double* y = w.y64 + b * ldm;
@@ -712,6 +713,8 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
         const double v = w.gr[ik * p.nr + il] * w.gc[jk * p.nc + jl];
         G[(int64_t)k * cap + lane] = v;
         G[(int64_t)lane * cap + k] = v;
+        sG[k * lds + lane] = v;
+        sG[lane * lds + k] = v;
       }
       if (lane == 0) {
         w.bvec[b * cap + k] = w.zb[b * p.n + pk];
@@ -731,6 +734,8 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
         const double v = w.gfull[jk * p.n + sups[lane]];
         G[(int64_t)k * cap + lane] = v;
         G[(int64_t)lane * cap + k] = v;
+        sG[k * lds + lane] = v;
+        sG[lane * lds + k] = v;
       }
       const float* ak = w.at32 + jk * ldm;
       double accb = 0.0;
@@ -784,6 +789,8 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
     if (lane <= k) {
       G[(int64_t)k * cap + lane] = gk;
       G[(int64_t)lane * cap + k] = gk;
+      sG[k * lds + lane] = gk;
+      sG[lane * lds + k] = gk;
     }
     accb = warp_sum(accb);
     if (lane == 0) {
@@ -859,6 +866,24 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
   return warp_sum(lacc);
 }
 
+// Asynchronous copy (LDGSTS, no registers held) of the Gram rows built in
+// earlier iterations, G[j][i] for i, j < t0, into the warp's shared buffer
+// (row stride lds), issued before the selection and the Gram extension so its
+// latency overlaps theirs.  learn_warp_body waits for it.
+__device__ __forceinline__ void stage_gram_async(const SolveParams& p, const Work& w, int64_t b,
+                                                 int t0, double* sG, int lds, int lane) {
+  if (lane < t0) {
+    const double* G = w.gram + b * p.cap * p.cap;
+    for (int j = 0; j < t0; ++j) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sG + j * lds + lane);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                   "l"(G + (int64_t)j * p.cap + lane)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int TB, int OPT>
 __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
                                 int outer, double* cs, int32_t* sups, double* s1,
@@ -868,16 +893,18 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   const int64_t cap = p.cap;
   if (lane < t) sups[lane] = w.sup[b * cap + lane];
   __syncwarp();
-  warp_extend_gram<TB>(p, w, b, t0, t, lane, sups);
+  constexpr int LDS = TB + 4;  // staged Gram (s1, see stage_gram_async)
+  warp_extend_gram<TB>(p, w, b, t0, t, lane, sups, s1, LDS);
   if (lane == 0) w.gcnt[b] = t;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
 
   double g[TB];
-  const double* G = w.gram + b * cap * cap;
   const double twolr = 2.0 * p.lr;
 #pragma unroll
   for (int j = 0; j < TB; ++j) {
-    // G[lane][j] read as G[j][lane] (G is stored symmetric): coalesced
-    const double gij = (lane < t && j < t) ? G[(int64_t)j * cap + lane] : 0.0;
+    // G[lane][j] read as G[j][lane] (G is symmetric): conflict-free
+    const double gij = (lane < t && j < t) ? s1[j * LDS + lane] : 0.0;
     if (OPT == 0)
       g[j] = (lane < t && j == lane) ? 1.0 - twolr * gij : -(twolr * gij);
     else
@@ -1081,20 +1108,26 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi || !w.active[b]) return;
+  double* s1 = sq_all[warp];
+  const int t0 = w.gcnt[b];
+  if (t0 <= TB) stage_gram_async(p, w, b, t0, s1, TB + 4, lane);
   if (p.fuse_select) {  // this iteration's th == 1 selection (K1c) first
     select_top_warp(p, w, b, lane);
-    if (!w.active[b]) return;
+    if (!w.active[b]) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      return;
+    }
   }
   if (w.cnt[b] > TB) {
     if (lane == 0) {
       const int slot = atomicAdd(&w.counters[kBigCount], 1);
       big_list[slot] = (int32_t)b;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
   double* cs = cs_all[warp];
   int32_t* sups = sup_all[warp];
-  double* s1 = sq_all[warp];
   double* s2 = nullptr;
   learn_warp_body<TB, OPT>(p, w, b, outer, cs, sups, s1, s2, lane);
 }
@@ -1344,8 +1377,10 @@ k_solve_fused(SolveParams p, Work w) {
       if (m > 0.0)
         warp_threshold_append(p, w, b, p.th * m, [&](int64_t j) { return sc[j]; }, lane);
       __syncwarp();
-      if (w.active[b] && w.cnt[b] <= kWarpCap)
+      if (w.active[b] && w.cnt[b] <= kWarpCap) {
+        stage_gram_async(p, w, b, w.gcnt[b], sq, kWarpCap + 4, lane);
         learn_warp_body<kWarpCap, OPT>(p, w, b, outer, cs, sups, sq, nullptr, lane);
+      }
       else if (lane == 0 && w.active[b])
         w.status[b] = 7, w.active[b] = 0;  // capacity: larger supports use the batched path
     }
