@@ -66,8 +66,9 @@ struct cl_ctx {
   cudaStream_t own_stream = nullptr;  // created by cl_create
   int64_t m = 0, n = 0, ldm = 0;
   float* at32 = nullptr;
-  float* at_hi = nullptr;
-  float* at_lo = nullptr;
+  __half* at_hi = nullptr;   // scaled fp16 split of at32 (tensor path)
+  __half* at_lo = nullptr;
+  float a_scale = 1.0f;      // its power-of-two scale
   double* gfull = nullptr;  // A^T A fp64 [n][n], built once (k_gram.cu)
   // separable 2D contexts (cl_create_sep)
   bool sep = false;
@@ -171,8 +172,9 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.y32 = cv.take<float>(B * ldm);
     w.y64 = cv.take<double>(B * ldm);
     w.r64 = cv.take<double>(B * ldm);
-    w.r_hi = need_split ? cv.take<float>(B * ldm) : nullptr;
-    w.r_lo = need_split ? cv.take<float>(B * ldm) : nullptr;
+    w.r_hi = need_split ? cv.take<__half>(B * ldm) : nullptr;
+    w.r_lo = need_split ? cv.take<__half>(B * ldm) : nullptr;
+    w.r_scale = need_split ? cv.take<float>(B) : nullptr;
     w.cand = cv.take<Cand>(B * ntile);
     w.scores = need_scores ? cv.take<double>(B * ctx->n) : nullptr;
     if (ctx->sep) {
@@ -368,6 +370,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
   p.delta_rel = delta_for(tensor, ctx->ldm);
   p.colnorm_max = ctx->colnorm_max;
+  p.a_inv_scale = 1.0 / (double)ctx->a_scale;
   p.sep = ctx->sep ? 1 : 0;
   p.nr = ctx->nr;
   p.nc = ctx->nc;
@@ -429,8 +432,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       if (ctx->world > 1) {
         const size_t rows = (size_t)((p.sig_hi - p.sig_lo) * p.ldm);
         if (w.r_hi) {
-          nccl_allgather_inplace(ctx->comm, w.r_hi, rows, 4, ctx->rank, s);
-          nccl_allgather_inplace(ctx->comm, w.r_lo, rows, 4, ctx->rank, s);
+          nccl_allgather_inplace(ctx->comm, w.r_hi, rows * sizeof(__half), 1, ctx->rank, s);
+          nccl_allgather_inplace(ctx->comm, w.r_lo, rows * sizeof(__half), 1, ctx->rank, s);
+          nccl_allgather_inplace(ctx->comm, w.r_scale, (size_t)(p.sig_hi - p.sig_lo), 4,
+                                 ctx->rank, s);
         } else {
           nccl_allgather_inplace(ctx->comm, w.r64, rows, 8, ctx->rank, s);
         }
@@ -735,13 +740,16 @@ cl_ctx* cl_create(int device, const float* a, int64_t m, int64_t n,
     return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
   }
   if (ctx->tc_ok) {
-    if (cudaMalloc(&ctx->at_hi, bytes) != cudaSuccess ||
-        cudaMalloc(&ctx->at_lo, bytes) != cudaSuccess) {
+    if (cudaMalloc(&ctx->at_hi, at.size() * sizeof(__half)) != cudaSuccess ||
+        cudaMalloc(&ctx->at_lo, at.size() * sizeof(__half)) != cudaSuccess) {
       cudaGetLastError();
       cl_destroy(ctx);
       return bail(CL_ERR_CUDA, "cl_create: device allocation failed");
     }
-    launch_split_tf32(ctx->at32, ctx->at_hi, ctx->at_lo, (int64_t)at.size(), ctx->stream);
+    // |scale * a| < 2^14 for every entry (max |a| <= ||a||_2 <= colnorm_max)
+    ctx->a_scale = split_scale(ctx->colnorm_max * ctx->colnorm_max);
+    launch_split_dict(ctx->at32, ctx->at_hi, ctx->at_lo, (int64_t)at.size(), ctx->a_scale,
+                      ctx->stream);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
       cudaGetLastError();
       cl_destroy(ctx);
@@ -1220,27 +1228,16 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
   p.n_corr = n;
   p.ntl = ntile;
   p.mwords = (n + 31) / 32;
+  p.a_inv_scale = 1.0 / (double)ctx->a_scale;
   const Work& w = ctx->w;
   std::vector<double> r64((size_t)(batch * ldm), 0.0);
-  std::vector<float> hi((size_t)(batch * ldm), 0.f), lo((size_t)(batch * ldm), 0.f);
   for (int64_t b = 0; b < batch; ++b)
-    for (int64_t i = 0; i < m; ++i) {
-      const float x = r[b * m + i];
-      uint32_t u;
-      std::memcpy(&u, &x, 4);
-      u &= 0xFFFFE000u;
-      float h;
-      std::memcpy(&h, &u, 4);
-      r64[(size_t)(b * ldm + i)] = x;
-      hi[(size_t)(b * ldm + i)] = h;
-      lo[(size_t)(b * ldm + i)] = x - h;
-    }
+    for (int64_t i = 0; i < m; ++i) r64[(size_t)(b * ldm + i)] = r[b * m + i];
   std::vector<int32_t> ones((size_t)batch, 1);
   cudaStream_t s = ctx->stream;
   CL_CUDA(ctx, cudaMemcpyAsync(w.r64, r64.data(), r64.size() * 8, cudaMemcpyHostToDevice, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(w.r_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(w.r_lo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice, s));
   CL_CUDA(ctx, cudaMemcpyAsync(w.active, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice, s));
+  if (tc) launch_split_resid(p, w, s);
   if (tc) {
     float* d = nullptr;
     CL_CUDA(ctx, cudaMalloc(&d, (size_t)(batch * n) * 4));

@@ -11,6 +11,7 @@
 //   snapshot, loss/stall bookkeeping (clomp.cpp:226-273).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -65,6 +66,24 @@ __host__ __device__ __forceinline__ Cand cand_empty() {
   return c;
 }
 
+// Power-of-two scale for the fp16 split of a vector of 2-norm sqrt(L): every
+// entry of the scaled vector is below 2^14 (fp16 max 65504), typical entries
+// ~2^14/sqrt(m) keep the lo halves well above the fp16 subnormal range.
+__host__ __device__ __forceinline__ float split_scale(double L) {
+  if (!(L > 0.0) || !(L < 1e300)) return 1.0f;
+  int k = 0;
+  (void)frexp(sqrt(L), &k);  // sqrt(L) = f 2^k, f in [0.5, 1)
+  k = k < -100 ? -100 : (k > 100 ? 100 : k);
+  return ldexpf(1.0f, 14 - k);
+}
+
+// s*x = hi + lo + O(2^-22 |s x|), both fp16 (s = 2^e, exact).
+__device__ __forceinline__ void split_f16(double x, float s, __half& hi, __half& lo) {
+  const float f = (float)x * s;
+  hi = __float2half_rn(f);
+  lo = __float2half_rn(f - __half2float(hi));
+}
+
 struct SolveParams {
   int64_t B, n, m, ldm, cap, ntile;
   int64_t tile_atoms;       // atoms per correlation tile (candidate granularity)
@@ -84,19 +103,21 @@ struct SolveParams {
   int64_t nr, nc, mr, mc, ldr, ldc;
   // th == 1 selection runs inside the learning kernel (warp per signal)
   int32_t fuse_select;
+  double a_inv_scale;       // 1 / (power-of-two scale of the fp16 dictionary split)
 };
 
 struct Work {
   // operands
   const float* at32 = nullptr;   // [n][ldm]
-  const float* at_hi = nullptr;  // [n][ldm] tf32 split (tensor path)
-  const float* at_lo = nullptr;
+  const __half* at_hi = nullptr;  // [n][ldm] scaled fp16 split (tensor path)
+  const __half* at_lo = nullptr;
   const double* gfull = nullptr; // [n][n] fp64 A^T A (optional, per context)
   float* y32 = nullptr;          // [B][ldm]
   double* y64 = nullptr;
   double* r64 = nullptr;
-  float* r_hi = nullptr;         // [B][ldm] tf32 split of the residual
-  float* r_lo = nullptr;
+  __half* r_hi = nullptr;        // [B][ldm] scaled fp16 split of the residual
+  __half* r_lo = nullptr;
+  float* r_scale = nullptr;      // [B] 1 / (its power-of-two scale)
   // separable 2D mode
   const double* at_r64 = nullptr;  // [nr][ldr] A_r atom-major
   const double* at_c64 = nullptr;  // [nc][ldc] A_c atom-major
@@ -160,8 +181,10 @@ void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
 // Same kernel, additionally writing the signed fp32 scores [B][n] (tests).
 void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
                           cudaStream_t s);
-void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
+void launch_split_dict(const float* src, __half* hi, __half* lo, int64_t count, float scale,
                        cudaStream_t s);
+// Residual fp16 split from r64 (warp per signal; init / unit paths).
+void launch_split_resid(const SolveParams& p, const Work& w, cudaStream_t s);
 // ---- launchers (k_sep.cu) ----
 void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
                      double* dst, bool abs_scores, cudaStream_t s);

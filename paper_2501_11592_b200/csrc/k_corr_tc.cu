@@ -1,15 +1,19 @@
 // k_corr_tc.cu — K1 on the 5th-generation tensor cores: scores = R A^T in
-// 3xTF32 with the argmax selection fused into the TMEM epilogue.
+// 3xFP16 (split fp16 operands, fp32 accumulation) with the argmax selection
+// fused into the TMEM epilogue.
 //
 // Replaces la::matmul(ops.at, r) (clomp.cpp:245) and the max scan of
 // inject_from_scores (clomp.cpp:45-47) on the th == 1 path.
 //
 // Shape: one CTA per 128-signal x 256-atom tile.  UMMA M = signals (TMEM
 // lanes), N = atoms (TMEM columns), K = measurements, both operands K-major in
-// shared memory with the 128-byte swizzle that TMA writes.  Every fp32 operand
-// x is split once into tf32 hi = trunc(x) and lo = x - hi (exact), and the
-// product is accumulated as hi*hi + hi*lo + lo*hi in fp32 in TMEM (3xTF32,
-// ~fp32 accuracy; the dropped lo*lo term is < 2^-20 |a||r|).
+// shared memory with the 64-byte swizzle that TMA writes.  Every operand x is
+// scaled by an exact power of two (per signal for the residual, from its norm;
+// once for the dictionary) so |s x| < 2^14, and split into fp16
+// hi = fp16(s x), lo = fp16(s x - hi); the product is accumulated as
+// hi*hi + hi*lo + lo*hi in fp32 in TMEM (~fp32 accuracy; the dropped lo*lo
+// term is ~2^-22 |a||r|) at twice the tf32 tensor rate, and the epilogue
+// divides the scales back out exactly.
 //
 // Roles (128 threads): warp 0 lane 0 issues TMA into a 4-stage ring,
 // warp 1 lane 0 issues tcgen05.mma (single thread per CTA), warp 2 owns the
@@ -18,7 +22,7 @@
 // record over the tile's 256 atoms (top-2 atoms + third value, Cand) is a
 // register scan with no shuffles.  Only that record per (signal, atom tile)
 // reaches HBM; the selection merges tiles and re-decides near-ties (gap inside
-// the 3xTF32 error bound) from exact fp64 scores of the few atoms in the band.
+// the split-fp16 error bound) from exact fp64 scores of the few atoms in the band.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -35,12 +39,12 @@ constexpr int TM = 128;  // signals per tile  (UMMA M, TMEM lanes)
 constexpr int TN = 256;  // atoms per tile    (UMMA N, TMEM columns)
 // K slice per pipeline stage: 16 fp32 = one 64-byte swizzle row, so a stage
 // (R hi/lo + A hi/lo) is 48 KB and four stages fit beside the epilogue.
-constexpr int BK = 16;
+constexpr int BK = 32;  // fp16 elements per operand row per stage (64 bytes)
 constexpr int STAGES = 4;
-constexpr int ROW_BYTES = BK * 4;             // bytes per operand row in smem
+constexpr int ROW_BYTES = BK * 2;             // bytes per operand row in smem
 constexpr uint64_t kSwizzleMode = 4;          // UMMA layout type: SWIZZLE_64B
-constexpr int R_BYTES = TM * BK * 4;  // 16 KB
-constexpr int A_BYTES = TN * BK * 4;  // 32 KB
+constexpr int R_BYTES = TM * BK * 2;  // 8 KB
+constexpr int A_BYTES = TN * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = 2 * R_BYTES + 2 * A_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t TMEM_COLS = 256;
@@ -116,20 +120,21 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256.
+// Instruction descriptor (kind::f16): D f32, A/B f16, both K-major,
+// M = 128, N = 256.
 constexpr uint32_t kIdesc = (1u << 4)           // D format f32
-                            | (2u << 7)         // A format tf32
-                            | (2u << 10)        // B format tf32
+                            | (0u << 7)         // A format f16
+                            | (0u << 10)        // B format f16
                             | ((TN >> 3) << 17) // N
                             | ((TM >> 4) << 24);// M
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
 }
@@ -197,7 +202,8 @@ __global__ void __launch_bounds__(128, 1)
 k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
           const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
           int64_t n, int64_t B, int kblocks, int64_t ntile, const int32_t* __restrict__ active,
-          Cand* __restrict__ cand, float* __restrict__ scores_dbg) {
+          const float* __restrict__ r_scale, double a_inv_scale, Cand* __restrict__ cand,
+          float* __restrict__ scores_dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -260,7 +266,7 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
         tma_load_2d(st + 2 * R_BYTES + A_BYTES, &tm_alo, &full[s], k0, (int)n0);
       } else {
         constexpr int rows = TN / CL;
-        const uint32_t off = crank * rows * BK * 4;
+        const uint32_t off = crank * rows * BK * 2;
         const int a_row = (int)n0 + (int)crank * rows;
         tma_load_2d_mc(st + 2 * R_BYTES + off, &tm_ahi, &full[s], k0, a_row, kMask);
         tma_load_2d_mc(st + 2 * R_BYTES + A_BYTES + off, &tm_alo, &full[s], k0, a_row, kMask);
@@ -279,11 +285,11 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
       const uint64_t d_ahi = sw128_desc(smem_u32(st + 2 * R_BYTES));
       const uint64_t d_alo = sw128_desc(smem_u32(st + 2 * R_BYTES + A_BYTES));
 #pragma unroll
-      for (int j = 0; j < BK / 8; ++j) {  // 8 tf32 (32 bytes) per MMA K step
+      for (int j = 0; j < BK / 16; ++j) {  // 16 fp16 (32 bytes) per MMA K step
         const uint64_t adv = (uint64_t)(j * 32) >> 4;
-        mma_tf32(tmem, d_rhi + adv, d_alo + adv, (kb | j) != 0);
-        mma_tf32(tmem, d_rlo + adv, d_ahi + adv, 1);
-        mma_tf32(tmem, d_rhi + adv, d_ahi + adv, 1);
+        mma_f16(tmem, d_rhi + adv, d_alo + adv, (kb | j) != 0);
+        mma_f16(tmem, d_rlo + adv, d_ahi + adv, 1);
+        mma_f16(tmem, d_rhi + adv, d_ahi + adv, 1);
       }
       // Stage free once these MMAs retire (in every CTA of the cluster that
       // multicasts into it).  The last STAGES releases are never waited for.
@@ -313,8 +319,9 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
     tmem_ld_32(tmem + lane_base + (uint32_t)(c * 32), v);
     const int64_t a0 = n0 + c * 32;
     if (scores_dbg && b < B) {
+      const double u = (double)r_scale[b] * a_inv_scale;
       for (int q = 0; q < 32; ++q)
-        if (a0 + q < n) scores_dbg[b * n + a0 + q] = v[q];
+        if (a0 + q < n) scores_dbg[b * n + a0 + q] = (float)((double)v[q] * u);
     }
     if (a0 + 32 <= n)
       cand_scan32<false>(v, (int)a0, 32, v1, i1, v2, i2, v3);
@@ -322,10 +329,12 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
       cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
   }
   if (b < B) {
+    // back to true units: both operand scales are exact powers of two
+    const double u = (double)r_scale[b] * a_inv_scale;
     Cand r;
-    r.v1 = (double)v1;
-    r.v2 = (double)v2;
-    r.v3 = (double)v3;
+    r.v1 = v1 >= 0.f ? (double)v1 * u : -1.0;
+    r.v2 = v2 >= 0.f ? (double)v2 * u : -1.0;
+    r.v3 = v3 >= 0.f ? (double)v3 * u : -1.0;
     r.i1 = i1;
     r.i2 = i2;
     cand[b * ntile + blockIdx.x] = r;
@@ -339,16 +348,13 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   }
 }
 
-// Exact tf32 split: hi = x with the 13 low mantissa bits cleared (what a tf32
-// operand can hold), lo = x - hi (exact in fp32).
-__global__ void k_split_tf32(const float* __restrict__ src, float* __restrict__ hi,
-                             float* __restrict__ lo, int64_t count) {
+// fp16 split of the dictionary: scale*x = hi + lo with scale = 2^e chosen by
+// the host so that |scale*x| < 2^14; hi = fp16(scale*x), lo = fp16(rest).
+__global__ void k_split_dict(const float* __restrict__ src, __half* __restrict__ hi,
+                             __half* __restrict__ lo, int64_t count, float scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const float x = src[i];
-  const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  hi[i] = h;
-  lo[i] = x - h;
+  split_f16(src[i], scale, hi[i], lo[i]);
 }
 
 // ---------------------------------------------------------------- host side
@@ -372,15 +378,15 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 row-major [rows][ld], box [box_rows][32], 128-byte swizzle.
-bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ld, int box_rows) {
+// 2-D fp16 row-major [rows][ld], box [box_rows][BK] (64 bytes), 64-byte swizzle.
+bool make_map(CUtensorMap* map, const __half* base, int64_t rows, int64_t ld, int box_rows) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides,
             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             ROW_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -396,7 +402,7 @@ struct MapCache {
 };
 thread_local MapCache g_maps;
 
-const CUtensorMap* cached_map(int slot, const float* base, int64_t rows, int64_t ld,
+const CUtensorMap* cached_map(int slot, const __half* base, int64_t rows, int64_t ld,
                               int box_rows) {
   if (g_maps.key[slot] != base || g_maps.rows[slot] != rows || g_maps.box[slot] != box_rows ||
       g_maps.ld[slot] != ld) {
@@ -444,7 +450,8 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
     cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     dim3 grid((unsigned)((p.n_corr + TN - 1) / TN), (unsigned)mtiles);
     k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n_corr, p.B, kblocks, p.ntl,
-                                               w.active, w.cand, scores_dbg);
+                                               w.active, w.r_scale, p.a_inv_scale, w.cand,
+                                               scores_dbg);
     return true;
   }
   cudaFuncSetAttribute(k_corr_tc<kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -463,7 +470,8 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
-                            kblocks, p.ntl, w.active, w.cand, scores_dbg) == cudaSuccess;
+                            kblocks, p.ntl, w.active, w.r_scale, p.a_inv_scale, w.cand,
+                            scores_dbg) == cudaSuccess;
 }
 
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
@@ -475,10 +483,10 @@ void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
   launch_tc_impl(p, w, scores, s);
 }
 
-void launch_split_tf32(const float* src, float* hi, float* lo, int64_t count,
+void launch_split_dict(const float* src, __half* hi, __half* lo, int64_t count, float scale,
                        cudaStream_t s) {
   const int64_t blocks = (count + 255) / 256;
-  k_split_tf32<<<(unsigned)blocks, 256, 0, s>>>(src, hi, lo, count);
+  k_split_dict<<<(unsigned)blocks, 256, 0, s>>>(src, hi, lo, count, scale);
 }
 
 }  // namespace clb

@@ -28,8 +28,6 @@ struct Gemm {
   int64_t X, Y, K;
   int mode;  // 0 store, 1 |.|, 2 residual (acc - yref), split + sum of squares
   const double* yref;
-  float* r_hi;
-  float* r_lo;
   double* lpart;
   int64_t tiles;  // tiles per batch entry (lpart stride)
   const int32_t* active;
@@ -100,12 +98,6 @@ __global__ void __launch_bounds__(256) k_gemm_sep(Gemm g) {
       } else if (g.mode == 2) {
         v -= g.yref[b * g.csb + o];
         ss = fma(v, v, ss);
-        if (g.r_hi) {
-          const float f = (float)v;
-          const float h = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
-          g.r_hi[b * g.csb + o] = h;
-          g.r_lo[b * g.csb + o] = f - h;
-        }
       }
       C[o] = v;
     }
@@ -218,8 +210,6 @@ void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
   g.K = p.nc;
   g.mode = 2;
   g.yref = w.y64;
-  g.r_hi = w.r_hi;
-  g.r_lo = w.r_lo;
   g.lpart = w.lpart;
   g.tiles = sep_resid_tiles(p);
   g.active = w.active;

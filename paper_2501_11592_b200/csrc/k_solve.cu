@@ -49,20 +49,14 @@ __device__ __forceinline__ bool mask_test(const uint32_t* mb, int j) {
 
 // Exact tf32 split of an fp32 value: hi = x with the 13 low mantissa bits
 // cleared, lo = x - hi (exact).  Must match k_split_tf32 in k_corr_tc.cu.
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
-}
-
-__device__ __forceinline__ void store_residual(const Work& w, int64_t o,
-                                               double rv) {
-  w.r64[o] = rv;
-  if (w.r_hi) {
-    float hi, lo;
-    split_tf32((float)rv, hi, lo);
-    w.r_hi[o] = hi;
-    w.r_lo[o] = lo;
-  }
+// fp16 split of residual row b (already in r64) with the scale of its
+// norm^2 L; lanes/threads stride over the row.
+__device__ __forceinline__ void split_row(const Work& w, int64_t b, int64_t ldm, double L,
+                                          int64_t start, int64_t stride) {
+  const float sc = split_scale(L);
+  if (start == 0) w.r_scale[b] = 1.0f / sc;
+  for (int64_t i = start; i < ldm; i += stride)
+    split_f16(w.r64[b * ldm + i], sc, w.r_hi[b * ldm + i], w.r_lo[b * ldm + i]);
 }
 
 // ------------------------------------------------------------------ init
@@ -80,11 +74,12 @@ __global__ void k_init(SolveParams p, Work w, const float* __restrict__ y_in,
     const int64_t o = b * p.ldm + i;
     w.y32[o] = v;
     w.y64[o] = (double)v;
-    store_residual(w, o, -(double)v);
+    w.r64[o] = -(double)v;
     acc = fma((double)v, (double)v, acc);
   }
   for (int64_t q = lane; q < p.mwords; q += 32) w.maskbits[b * p.mwords + q] = 0u;
   const double L = warp_sum(acc);
+  if (w.r_hi) split_row(w, b, p.ldm, L, lane, 32);
   if (lane == 0) {
     w.loss[b] = L;
     w.cnt[b] = 0;
@@ -817,6 +812,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
   const int64_t ldm = p.ldm;
   const double* y = w.y64 + b * ldm;
   double lacc = 0.0;
+  double rr[16];  // the last 512-row pass stays in registers for the split
   for (int64_t base = 0; base < ldm; base += 512) {
     double r[16];
 #pragma unroll
@@ -843,27 +839,41 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
         const int64_t o = b * ldm + i0;
         const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
         const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
-        const double v0 = r[4 * q + 0] - y01.x, v1 = r[4 * q + 1] - y01.y;
-        const double v2 = r[4 * q + 2] - y23.x, v3 = r[4 * q + 3] - y23.y;
-        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(v0, v1);
-        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(v2, v3);
-        if (w.r_hi) {
-          float h0, h1, h2, h3, l0, l1, l2, l3;
-          split_tf32((float)v0, h0, l0);
-          split_tf32((float)v1, h1, l1);
-          split_tf32((float)v2, h2, l2);
-          split_tf32((float)v3, h3, l3);
-          *reinterpret_cast<float4*>(w.r_hi + o) = make_float4(h0, h1, h2, h3);
-          *reinterpret_cast<float4*>(w.r_lo + o) = make_float4(l0, l1, l2, l3);
-        }
-        lacc = fma(v0, v0, lacc);
-        lacc = fma(v1, v1, lacc);
-        lacc = fma(v2, v2, lacc);
-        lacc = fma(v3, v3, lacc);
+        r[4 * q + 0] -= y01.x;
+        r[4 * q + 1] -= y01.y;
+        r[4 * q + 2] -= y23.x;
+        r[4 * q + 3] -= y23.y;
+        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
+        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lacc = fma(r[4 * q + e], r[4 * q + e], lacc);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) rr[q] = r[q];
   }
-  return warp_sum(lacc);
+  const double L = warp_sum(lacc);
+  if (w.r_hi) {
+    if (ldm <= 512) {  // single pass: split straight from registers
+      const float sc = split_scale(L);
+      if (lane == 0) w.r_scale[b] = 1.0f / sc;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i0 = 128 * q + 4 * lane;
+        if (128 * q < ldm) {
+          __align__(8) __half h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) split_f16(rr[4 * q + e], sc, h[e], l[e]);
+          *reinterpret_cast<uint2*>(w.r_hi + b * ldm + i0) = *reinterpret_cast<const uint2*>(h);
+          *reinterpret_cast<uint2*>(w.r_lo + b * ldm + i0) = *reinterpret_cast<const uint2*>(l);
+        }
+      }
+    } else {
+      __syncwarp();
+      split_row(w, b, ldm, L, lane, 32);
+    }
+  }
+  return L;
 }
 
 // Asynchronous copy (LDGSTS, no registers held) of the Gram rows built in
@@ -951,105 +961,11 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   }
 }
 
-// Residual, loss and stopping rules after the learning phase.  One block per
-// signal; each warp owns 128-row chunks of the measurement vector (4 rows per
-// lane, fp32 atom rows read as float4), so a signal's residual is
-// spread over several warps and many signals are resident per SM to hide the
-// L2 latency of the support-atom gathers.  Signals whose support outgrew the
-// learning bucket TB were finished by the block learning kernel.
-constexpr int kResidWarps = 4;
-#ifndef CL_RESID_BATCH
-#define CL_RESID_BATCH 4
-#endif
-constexpr int kResidBatch = CL_RESID_BATCH;
-
-#ifndef CL_RESID_MINB
-#define CL_RESID_MINB 1
-#endif
-template <int TB>
-__global__ void __launch_bounds__(32 * kResidWarps, CL_RESID_MINB)
-k_resid(SolveParams p, Work w, int outer) {
-  __shared__ __align__(16) double cs[kWarpCap];
-  __shared__ int32_t sups[kWarpCap];
-  __shared__ double red[kResidWarps];
-  __shared__ int snap_s;
-  const int64_t b = p.sig_lo + blockIdx.x;
-  if (!w.active[b]) return;
-  const int t = w.cnt[b];
-  if (t > TB) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t cap = p.cap, ldm = p.ldm;
-  if (tid < kWarpCap) {  // zero tail: batched loops read cs up to a batch edge
-    cs[tid] = tid < t ? w.coef[b * cap + tid] : 0.0;
-    sups[tid] = tid < t ? w.sup[b * cap + tid] : 0;
-  }
-  CtlState ctl{};
-  if (tid == 0 && p.mode == kModePerSignal) ctl = load_ctl(w, b);
-  __syncthreads();
-  const double* y = w.y64 + b * ldm;
-  double lacc = 0.0;
-  for (int64_t q = warp; q * 128 < ldm; q += kResidWarps) {
-    const int64_t i0 = q * 128 + 4 * lane;
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-    // fp32 atom rows (exact in fp64, half the L2 bytes of an fp64 copy),
-    // kResidBatch independent gathers in flight per lane.
-    for (int k0 = 0; k0 < t; k0 += kResidBatch) {
-      float4 v[kResidBatch];
-#pragma unroll
-      for (int u = 0; u < kResidBatch; ++u)
-        v[u] = k0 + u < t ? *reinterpret_cast<const float4*>(w.at32 + (int64_t)sups[k0 + u] * ldm + i0)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int u = 0; u < kResidBatch; ++u) {
-        const double ck = cs[k0 + u];
-        r0 = fma(f2d(v[u].x), ck, r0);
-        r1 = fma(f2d(v[u].y), ck, r1);
-        r2 = fma(f2d(v[u].z), ck, r2);
-        r3 = fma(f2d(v[u].w), ck, r3);
-      }
-    }
-    const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
-    const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
-    const double v0 = r0 - y01.x, v1 = r1 - y01.y, v2 = r2 - y23.x, v3 = r3 - y23.y;
-    const int64_t o = b * ldm + i0;
-    *reinterpret_cast<double2*>(w.r64 + o) = make_double2(v0, v1);
-    *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(v2, v3);
-    if (w.r_hi) {
-      float h0, h1, h2, h3, l0, l1, l2, l3;
-      split_tf32((float)v0, h0, l0);
-      split_tf32((float)v1, h1, l1);
-      split_tf32((float)v2, h2, l2);
-      split_tf32((float)v3, h3, l3);
-      *reinterpret_cast<float4*>(w.r_hi + o) = make_float4(h0, h1, h2, h3);
-      *reinterpret_cast<float4*>(w.r_lo + o) = make_float4(l0, l1, l2, l3);
-    }
-    lacc = fma(v0, v0, lacc);
-    lacc = fma(v1, v1, lacc);
-    lacc = fma(v2, v2, lacc);
-    lacc = fma(v3, v3, lacc);
-  }
-  lacc = warp_sum(lacc);
-  if (lane == 0) red[warp] = lacc;
-  __syncthreads();
-  if (tid == 0) {
-    double L = 0.0;
-    for (int q = 0; q < kResidWarps; ++q) L += red[q];
-    snap_s = 0;
-    if (p.mode == kModePerSignal)
-      snap_s = control_signal(p, w, b, outer, L, ctl);
-    else
-      w.loss[b] = L;
-  }
-  __syncthreads();
-  if (snap_s && tid < t) w.best_coef[b * cap + tid] = cs[tid];
-}
-
-// Warp-per-signal variant: no block barriers, the whole signal's gathers
-// (16 rows per lane per 512-row pass) issued by one warp, many signals
-// resident per SM.
-#ifndef CL_RESID_WARP
-#define CL_RESID_WARP 1
-#endif
+// Residual, loss and stopping rules after the learning phase, one warp per
+// signal: no block barriers, the whole signal's gathers (16 rows per lane per
+// 512-row pass) issued by one warp, many signals resident per SM.  Signals
+// whose support outgrew the learning bucket TB were finished by the block
+// learning kernel.
 #ifndef CL_RESIDW_MINB
 #define CL_RESIDW_MINB 4
 #endif
@@ -1148,6 +1064,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
   double* Gs = reinterpret_cast<double*>(sups + ((p.cap + 1) & ~1LL));  // [cap*cap]
   __shared__ double red[kBlockThreads / 32];
   __shared__ int snap_s;
+  __shared__ double s_L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kBlockThreads / 32;
   const int count = w.counters[kBigCount];
@@ -1291,7 +1208,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
       for (int k = 0; k < t; ++k)
         acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
       const double rv = acc - y[i];
-      store_residual(w, b * p.ldm + i, rv);
+      w.r64[b * p.ldm + i] = rv;
       lacc = fma(rv, rv, lacc);
     }
     lacc = warp_sum(lacc);
@@ -1300,6 +1217,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     if (tid == 0) {
       double L = 0.0;
       for (int q = 0; q < nw; ++q) L += red[q];
+      s_L = L;
       snap_s = 0;
       if (p.mode == kModePerSignal)
         snap_s = control_signal(p, w, b, outer, L);
@@ -1307,6 +1225,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
         w.loss[b] = L;
     }
     __syncthreads();
+    if (w.r_hi) split_row(w, b, p.ldm, s_L, tid, kBlockThreads);  // own r64 entries
     if (snap_s)
       for (int i = tid; i < t; i += kBlockThreads) w.best_coef[b * cap + i] = cs[i];
     __syncthreads();
@@ -1579,6 +1498,19 @@ __global__ void k_finalize(SolveParams p, Work w, int64_t out_cap,
   }
 }
 
+// fp16 split of residual rows already in r64 (warp per signal).
+__global__ void k_split_resid(SolveParams p, Work w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (b >= p.B) return;
+  double acc = 0.0;
+  for (int64_t i = lane; i < p.ldm; i += 32) {
+    const double v = w.r64[b * p.ldm + i];
+    acc = fma(v, v, acc);
+  }
+  split_row(w, b, p.ldm, warp_sum(acc), lane, 32);
+}
+
 // inject_support unit path: ||r||^2 per column and a clean support list.
 __global__ void k_inject_prep(SolveParams p, Work w) {
   const int lane = threadIdx.x & 31;
@@ -1588,9 +1520,9 @@ __global__ void k_inject_prep(SolveParams p, Work w) {
   for (int64_t i = lane; i < p.ldm; i += 32) {
     const double v = w.r64[b * p.ldm + i];
     acc = fma(v, v, acc);
-    if (w.r_hi) store_residual(w, b * p.ldm + i, v);
   }
   acc = warp_sum(acc);
+  if (w.r_hi) split_row(w, b, p.ldm, acc, lane, 32);
   if (lane == 0) {
     w.loss[b] = acc;
     w.cnt[b] = 0;
@@ -1606,6 +1538,10 @@ void launch_init(const SolveParams& p, const Work& w, const float* y_in,
   const int threads = 256;
   const int64_t blocks = (p.B * 32 + threads - 1) / threads;
   k_init<<<(unsigned)blocks, threads, 0, s>>>(p, w, y_in, y_layout == 0);
+}
+
+void launch_split_resid(const SolveParams& p, const Work& w, cudaStream_t s) {
+  k_split_resid<<<(unsigned)((p.B * 32 + 255) / 256), 256, 0, s>>>(p, w);
 }
 
 void launch_select(const SolveParams& p, const Work& w, bool full_scores,
@@ -1659,11 +1595,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
     }
     if (!p.sep) {
-#if CL_RESID_WARP
       k_resid_w<TB><<<(unsigned)((nsig + 3) / 4), 128, 0, s>>>(p, w, outer);
-#else
-      k_resid<TB><<<(unsigned)nsig, 32 * kResidWarps, 0, s>>>(p, w, outer);
-#endif
     }
   };
   if (max_cnt <= 8)

@@ -1,4 +1,4 @@
-"""K1 correlation kernels on the GPU: the tcgen05 3xTF32 scores against fp64
+"""K1 correlation kernels on the GPU: the tcgen05 split-fp16 (3 MMA) scores against fp64
 scores, and the measured error against the bound the selection step uses to
 decide when a near-tie must be re-decided in fp64 (clomp_api.cu delta_for)."""
 import numpy as np
@@ -22,15 +22,15 @@ def test_tc_scores_within_bound(gpu_available, m, n, B):
     R = rng.standard_normal((B, m)).astype(np.float32)
     ctx = cl.ClompContext(A)
     s64 = ctx.debug_scores(R, 1)                 # |A^T r| fp64
-    stc = np.abs(ctx.debug_scores(R, 2))         # 3xTF32 on tcgen05
+    stc = np.abs(ctx.debug_scores(R, 2))         # split fp16 on tcgen05
     exact = np.abs(R.astype(np.float64) @ A.astype(np.float64))
     assert np.max(np.abs(s64 - exact)) <= 1e-12 * np.max(exact)
     colmax = np.max(np.linalg.norm(A.astype(np.float64), axis=0))
     rn = np.linalg.norm(R.astype(np.float64), axis=1, keepdims=True)
     err = np.abs(stc - exact) / (colmax * rn)
     worst = float(err.max())
-    print(f"m={m} n={n} B={B}: max 3xTF32 error {worst:.3e} of ||a||*||r||, bound {delta_rel(m):.3e}")
-    assert worst <= delta_rel(m) / 4, "3xTF32 error too close to the rescan bound"
+    print(f"m={m} n={n} B={B}: max split-fp16 error {worst:.3e} of ||a||*||r||, bound {delta_rel(m):.3e}")
+    assert worst <= delta_rel(m) / 4, "split-fp16 error too close to the rescan bound"
 
 
 def test_tc_argmax_matches_fp64(gpu_available):
