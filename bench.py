@@ -358,15 +358,21 @@ def run_ours(args, rank, world, local_rank):
         prof = ctx.stats()
         ctx.set_profiling(False)
 
-    # End to end through the public API: host y in, host results out.
+    # End to end through the public API: y from pinned host memory in, the
+    # compact per-signal results (supports, coefficients, norms, flags) back in
+    # host memory; wall clock of the whole library call (ctx.stats e2e_ms).
+    Y_pin = torch.empty(Y.shape, dtype=torch.float32, pin_memory=True).numpy()
+    Y_pin[...] = Y
+    cl.clomp_solve_batch(ctx, Y_pin, cfg, mode=cl.MODE_PER_SIGNAL, dense=False)  # warm-up
     e2e_ms = []
     for _ in range(min(args.steps, 3)):
         with torch.cuda.stream(stream):
             flush.fill_(3)
         torch.cuda.synchronize()
-        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        t0 = time.perf_counter()
+        r = cl.clomp_solve_batch(ctx, Y_pin, cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
         st = ctx.stats()
-        e2e_ms.append(st["e2e_ms"])
     assert np.all(r.status == 0)
     te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
     if dist:
@@ -423,7 +429,8 @@ def run_ours(args, rank, world, local_rank):
         }
     out["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
                   "d2h_bytes_per_step": st["d2h_bytes"],
-                  "path": "clomp_solve_batch (host numpy y in, host results out)"}
+                  "path": ("clomp_solve_batch(dense=False): y from pinned host memory, compact "
+                           "results (supports, coefficients, norms, flags) to host; host wall clock around the Python call")}
     out["gpu_launches"] = int(launches_per_step * args.steps)
     out["clocks"] = clocks
     if world == 1 and not args.no_cpu_baseline and not c["sep"]:

@@ -184,7 +184,7 @@ typedef struct cl_stats {
   double total_ms;              /* device time of the whole solve           */
   int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32, 2 fused   */
   int32_t pad0;
-  double e2e_ms;                /* cl_solve_batch: H2D + solve + D2H, events */
+  double e2e_ms;                /* cl_solve_batch: wall clock of the whole call  */
   double select_ms;             /* device time of select + fp64 rescans     */
   int64_t h2d_bytes;            /* bytes copied host->device by that call   */
   int64_t d2h_bytes;            /* bytes copied device->host by that call   */

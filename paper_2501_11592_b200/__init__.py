@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+from collections.abc import Sequence
 from pathlib import Path
 
 import numpy as np
@@ -233,6 +234,24 @@ class ClompConfig:
                        u64(self.stall_patience))
 
 
+
+
+class Ragged(Sequence):
+    """Per-signal rows of a [B][cap] array cut at counts[b] (views, built on
+    access): the compact support / coefficient lists of a batch."""
+
+    def __init__(self, data: np.ndarray, counts: np.ndarray):
+        self.data, self.counts = data, counts
+
+    def __len__(self) -> int:
+        return len(self.counts)
+
+    def __getitem__(self, b):
+        if isinstance(b, slice):
+            return [self[i] for i in range(*b.indices(len(self)))]
+        return self.data[b, :self.counts[b]]
+
+
 @dataclasses.dataclass
 class BatchSolveResult:
     """cskit::BatchSolveResult (clomp.hpp:82-90) plus the compact support."""
@@ -243,8 +262,8 @@ class BatchSolveResult:
     final_residual_norm: np.ndarray
     converged: np.ndarray
     status: np.ndarray
-    support: list                 # per signal, ascending atom indices
-    coef: list                    # per signal, aligned with support
+    support: Ragged               # per signal, ascending atom indices
+    coef: Ragged                  # per signal, aligned with support
 
 
 @dataclasses.dataclass
@@ -386,8 +405,14 @@ def nccl_unique_id() -> bytes:
 
 
 def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
-                      mode: int = MODE_JOINT, layout: str = "ref") -> BatchSolveResult:
-    """Reconstruct a batch; y_cols is m x B (reference layout) or B x m ('t')."""
+                      mode: int = MODE_JOINT, layout: str = "ref",
+                      dense: bool = True) -> BatchSolveResult:
+    """Reconstruct a batch; y_cols is m x B (reference layout) or B x m ('t').
+
+    dense=False skips materialising the n x B `s` / `mask` matrices (they are
+    None in the result); supports and coefficients are always returned.  A y
+    in page-locked memory (e.g. a pinned torch tensor's numpy view) is copied
+    to the GPU directly, pageable y through the context's pinned staging."""
     cfg = cfg or ClompConfig()
     y = np.ascontiguousarray(y_cols, dtype=np.float32)
     if y.ndim == 1:
@@ -407,8 +432,8 @@ def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
     sup = np.zeros((max(B, 1), cap), np.int32)
     coef = np.zeros((max(B, 1), cap), np.float64)
     cnt = np.zeros(max(B, 1), np.int32)
-    s = np.zeros((n, max(B, 1)), np.float64)
-    mask = np.zeros((n, max(B, 1)), np.uint8)
+    s = np.zeros((n, max(B, 1)), np.float64) if dense else None
+    mask = np.zeros((n, max(B, 1)), np.uint8) if dense else None
     it = np.zeros(max(B, 1), np.int64)
     rn = np.zeros(max(B, 1), np.float64)
     cv = np.zeros(max(B, 1), np.uint8)
@@ -418,10 +443,11 @@ def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
     c = cfg.to_c()
     code = lib().cl_solve_batch(ctx.handle, _ptr(y), B, lay, C.byref(c), int(mode), C.byref(res))
     _raise(code, ctx.handle)
-    supports = [sup[b, :min(cnt[b], cap)].copy() for b in range(B)]
-    coefs = [coef[b, :min(cnt[b], cap)].copy() for b in range(B)]
-    return BatchSolveResult(s[:, :B], mask[:, :B], it[:B], rn[:B], cv[:B].astype(bool),
-                            st[:B], supports, coefs)
+    counts = np.minimum(cnt[:B], cap)
+    supports = Ragged(sup, counts)
+    coefs = Ragged(coef, counts)
+    return BatchSolveResult(s[:, :B] if dense else None, mask[:, :B] if dense else None,
+                            it[:B], rn[:B], cv[:B].astype(bool), st[:B], supports, coefs)
 
 
 def clomp_solve(ctx: ClompContext, y, cfg: ClompConfig | None = None) -> SolveResult:

@@ -11,6 +11,8 @@
 // (clomp.cpp:18-30, 131-140, 211-218); there is no CPU compute path.
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -92,6 +94,8 @@ struct cl_ctx {
   void* stage = nullptr;
   size_t stage_bytes = 0;
   int32_t* h_counters = nullptr;  // pinned
+  char* h_io = nullptr;           // pinned host staging (pageable y in, results out)
+  size_t h_io_bytes = 0;
   int32_t* h_chunk = nullptr;     // pinned, 2 x kNumCounters (graph chunks)
   cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
   GraphKey gkey;
@@ -906,6 +910,7 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->bc);
   cudaFree(ctx->stage);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  if (ctx->h_io) cudaFreeHost(ctx->h_io);
   if (ctx->h_chunk) cudaFreeHost(ctx->h_chunk);
   if (ctx->comm) nccl_comm_destroy(ctx->comm);
   for (auto& e : ctx->chunk_ev)
@@ -1016,16 +1021,39 @@ static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode
   return CL_OK;
 }
 
+static char* host_io(cl_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->h_io_bytes) {
+    if (ctx->h_io) cudaFreeHost(ctx->h_io);
+    ctx->h_io = nullptr;
+    ctx->h_io_bytes = 0;
+    if (cudaMallocHost(&ctx->h_io, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ctx->h_io_bytes = bytes;
+  }
+  return ctx->h_io;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess;
+  cudaGetLastError();
+  return ok && at.type == cudaMemoryTypeHost;
+}
+
 int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
                    const cl_config* cfg, int mode, cl_result* out) {
   if (!ctx) return CL_ERR_INTERNAL;
   if (!y && batch > 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: null y");
+  const auto t_start = std::chrono::steady_clock::now();
   cudaSetDevice(ctx->device);
   const int64_t m = ctx->m, n = ctx->n;
-  // mean(y^2) for resolve_weights (clomp.cpp:134-136), per batch and per column.
+  // mean(y^2) for resolve_weights (clomp.cpp:134-136), per batch and per
+  // column; only automatic prior weights (w < 0) depend on it.
   std::vector<double> col_ms;
   double all = 0.0;
-  if (batch > 0) {
+  if (batch > 0 && cfg && (cfg->w_tv < 0.0 || cfg->w_lv < 0.0)) {
     col_ms.assign((size_t)batch, 0.0);
     for (int64_t i = 0; i < m; ++i)
       for (int64_t b = 0; b < batch; ++b) {
@@ -1038,7 +1066,7 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
     }
     all /= (double)(m * batch);
   }
-  int st = check_call(ctx, batch, cfg, mode, all, &col_ms);
+  int st = check_call(ctx, batch, cfg, mode, all, col_ms.empty() ? nullptr : &col_ms);
   if (st) return st;
 
   const int64_t cap = support_cap(ctx, cfg);
@@ -1059,51 +1087,45 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   o.rn = cv.take<double>(batch);
   o.conv = cv.take<uint8_t>(batch);
   o.status = cv.take<int32_t>(batch);
-  cudaEvent_t e2e[2];
-  cudaEventCreate(&e2e[0]);
-  cudaEventCreate(&e2e[1]);
-  cudaEventRecord(e2e[0], ctx->stream);
-  CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, ctx->stream));
-  st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o);
-  if (st) {
-    cudaEventDestroy(e2e[0]);
-    cudaEventDestroy(e2e[1]);
-    return st;
-  }
+  const size_t out_bytes = cv.off;  // the compact results, one D2H copy
 
-  std::vector<int32_t> h_sup((size_t)(batch * cap)), h_cnt((size_t)batch),
-      h_it((size_t)batch), h_st((size_t)batch);
-  std::vector<double> h_coef((size_t)(batch * cap)), h_rn((size_t)batch);
-  std::vector<uint8_t> h_cv((size_t)batch);
+  // Host side: pinned caller buffers go straight to the DMA engine; pageable
+  // ones are staged through the context's pinned buffer, which also receives
+  // the compact results.
+  const bool y_pinned = is_pinned(y);
+  char* hio = host_io(ctx, out_bytes + (y_pinned ? 0 : align_up(ybytes, 256)));
+  if (!hio) return fail(ctx, CL_ERR_CUDA, "clomp: pinned host staging allocation failed");
   cudaStream_t s = ctx->stream;
-  CL_CUDA(ctx, cudaMemcpyAsync(h_sup.data(), o.sup, h_sup.size() * 4, cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_coef.data(), o.coef, h_coef.size() * 8, cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_cnt.data(), o.cnt, h_cnt.size() * 4, cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_it.data(), o.iters, h_it.size() * 4, cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_rn.data(), o.rn, h_rn.size() * 8, cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_cv.data(), o.conv, h_cv.size(), cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaMemcpyAsync(h_st.data(), o.status, h_st.size() * 4, cudaMemcpyDeviceToHost, s));
-  cudaEventRecord(e2e[1], s);
-  CL_CUDA(ctx, cudaStreamSynchronize(s));
-  {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e2e[0], e2e[1]);
-    ctx->stats.e2e_ms = ms;
-    ctx->stats.h2d_bytes = (int64_t)ybytes;
-    ctx->stats.d2h_bytes = (int64_t)(h_sup.size() * 4 + h_coef.size() * 8 + h_cnt.size() * 4 +
-                                     h_it.size() * 4 + h_rn.size() * 8 + h_cv.size() + h_st.size() * 4);
-    cudaEventDestroy(e2e[0]);
-    cudaEventDestroy(e2e[1]);
+  if (y_pinned) {
+    CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, s));
+  } else {
+    char* hy = hio + out_bytes;
+    std::memcpy(hy, y, ybytes);
+    CL_CUDA(ctx, cudaMemcpyAsync(d_y, hy, ybytes, cudaMemcpyHostToDevice, s));
   }
+  st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o);
+  if (st) return st;
+  CL_CUDA(ctx, cudaMemcpyAsync(hio, stg + align_up(ybytes, 256), out_bytes,
+                               cudaMemcpyDeviceToHost, s));
+  CL_CUDA(ctx, cudaStreamSynchronize(s));
+  // host views of the compact results (same carving as the device side)
+  Carver hv{hio};
+  const int32_t* h_sup = hv.take<int32_t>(batch * cap);
+  const double* h_coef = hv.take<double>(batch * cap);
+  const int32_t* h_cnt = hv.take<int32_t>(batch);
+  const int32_t* h_it = hv.take<int32_t>(batch);
+  const double* h_rn = hv.take<double>(batch);
+  const uint8_t* h_cv = hv.take<uint8_t>(batch);
+  const int32_t* h_st = hv.take<int32_t>(batch);
 
   if (out) {
     if (out->s) std::memset(out->s, 0, sizeof(double) * (size_t)(n * batch));
     if (out->mask) std::memset(out->mask, 0, (size_t)(n * batch));
     for (int64_t b = 0; b < batch; ++b) {
-      const int cnt = h_cnt[(size_t)b];
+      const int cnt = h_cnt[b];
       for (int k = 0; k < cnt; ++k) {
-        const int32_t j = h_sup[(size_t)(b * cap + k)];
-        const double v = h_coef[(size_t)(b * cap + k)];
+        const int32_t j = h_sup[b * cap + k];
+        const double v = h_coef[b * cap + k];
         if (k < out->cap) {
           if (out->support) out->support[b * out->cap + k] = j;
           if (out->coef) out->coef[b * out->cap + k] = v;
@@ -1112,12 +1134,18 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
         if (out->mask) out->mask[(int64_t)j * batch + b] = 1;
       }
       if (out->count) out->count[b] = cnt;
-      if (out->iterations) out->iterations[b] = h_it[(size_t)b];
-      if (out->final_residual_norm) out->final_residual_norm[b] = h_rn[(size_t)b];
-      if (out->converged) out->converged[b] = h_cv[(size_t)b];
-      if (out->status) out->status[b] = h_st[(size_t)b];
+      if (out->iterations) out->iterations[b] = h_it[b];
+      if (out->final_residual_norm) out->final_residual_norm[b] = h_rn[b];
+      if (out->converged) out->converged[b] = h_cv[b];
+      if (out->status) out->status[b] = h_st[b];
     }
   }
+  // End to end through this call: host y in, host results out (wall clock).
+  ctx->stats.e2e_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start)
+          .count();
+  ctx->stats.h2d_bytes = (int64_t)ybytes;
+  ctx->stats.d2h_bytes = (int64_t)out_bytes;
   if (mode == CL_MODE_JOINT && batch > 0 && h_st[0] != CL_OK) {
     return fail(ctx, h_st[0],
                 h_st[0] == CL_ERR_NUMERICAL ? "clomp: loss diverged; reduce lr"

@@ -53,3 +53,14 @@ def test_no_device_fails_loudly(built_lib):
 def test_baseline_mapping():
     c = cl.ClompConfig.baseline(32)
     assert (c.th, c.max_outer, c.inner_steps, c.lr, c.opt, c.w_tv, c.w_lv) == (1.0, 32, 200, 0.1, cl.PLAIN, 0.0, 0.0)
+
+
+def test_ragged_rows_view_counts():
+    import paper_2501_11592_b200 as cl
+    r = cl.Ragged(np.arange(12, dtype=np.int32).reshape(3, 4), np.array([1, 4, 0]))
+    assert len(r) == 3
+    assert r[0].tolist() == [0] and r[1].tolist() == [4, 5, 6, 7] and r[2].size == 0
+    assert [x.tolist() for x in r[0:2]] == [[0], [4, 5, 6, 7]]
+    res = cl.BatchSolveResult(None, None, np.zeros(3), np.zeros(3), np.zeros(3, bool),
+                              np.zeros(3, np.int32), r, r)
+    assert res.support[1].tolist() == [4, 5, 6, 7]
