@@ -397,7 +397,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // iteration, so the learning kernel's support bucket follows `outer`
   // (signals grown past it by ties are finished by the block kernel).
   auto enqueue_iteration = [&](int outer, int64_t* launches) {
-    cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
+    // (the active count is cleared by the learning kernel, see k_learn_warp)
     if (p.sep) {
       launch_sep_corr(p, w, w.r64, w.scores, true, s);
       launch_select(p, w, true, s);
@@ -507,7 +507,6 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         if (ctx->h_counters[kActiveCount] == 0) break;
         continue;
       }
-      cudaMemsetAsync(w.counters, 0, 2 * sizeof(int32_t), s);
       cudaEventRecord(ev[1], s);
       if (tensor)
         launch_corr_tc(p, w, s);

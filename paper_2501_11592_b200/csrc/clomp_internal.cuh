@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace clb {
 
@@ -160,7 +161,8 @@ enum Counter {
   kActiveCount = 1,   // signals still iterating after this outer iteration
   kMaxCount = 2,      // max support size over the batch
   kRescanTotal = 3,   // rescans over the whole solve
-  kBigCount = 4,      // signals queued for the block learning kernel
+  kBigCount = 4,      // signals queued for the block learning kernel; slots
+                      // 4 + (outer & 1), the block kernel clears the other one
   kNumCounters = 8
 };
 
@@ -169,6 +171,33 @@ enum Joint {
   kJStop = 5, kJConv = 6, kJStatus = 7, kJIters = 8, kJFinalRn = 9,
   kNumJoint = 16
 };
+
+// Programmatic dependent launch (PDL): kernels of the per-iteration chain are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization, let their
+// successor start launching as soon as every CTA is resident (pdl_trigger),
+// and wait for their predecessor's completion and memory (pdl_wait) before
+// touching its outputs, so launch latency and prologues overlap the previous
+// kernel's tail.  Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- launchers (k_corr.cu) ----
 // fp64 SIMT correlation with fused top-2 epilogue (th == 1) or full |scores|.

@@ -216,6 +216,8 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   const int64_t m0 = (int64_t)blockIdx.y * TM;  // first signal
   const int64_t n0 = (int64_t)blockIdx.x * TN;  // first atom
 
+  pdl_wait();  // the residual split of the previous kernel
+  pdl_trigger();
   // Whole tile finished?  (uniform per CTA; a cluster must stay together)
   if (CL == 1) {
     int mine = 0;
@@ -449,10 +451,9 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   if (!clustered) {
     cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     dim3 grid((unsigned)((p.n_corr + TN - 1) / TN), (unsigned)mtiles);
-    k_corr_tc<1><<<grid, 128, SMEM_BYTES, s>>>(*rhi, *rlo, *ahi, *alo, p.n_corr, p.B, kblocks, p.ntl,
-                                               w.active, w.r_scale, p.a_inv_scale, w.cand,
-                                               scores_dbg);
-    return true;
+    return launch_pdl(k_corr_tc<1>, grid, dim3(128), (size_t)SMEM_BYTES, s, *rhi, *rlo, *ahi, *alo,
+                      p.n_corr, p.B, kblocks, p.ntl, (const int32_t*)w.active,
+                      (const float*)w.r_scale, p.a_inv_scale, w.cand, scores_dbg) == cudaSuccess;
   }
   cudaFuncSetAttribute(k_corr_tc<kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        SMEM_BYTES);
@@ -462,13 +463,15 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = kCluster;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_wait
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
                             kblocks, p.ntl, w.active, w.r_scale, p.a_inv_scale, w.cand,
                             scores_dbg) == cudaSuccess;

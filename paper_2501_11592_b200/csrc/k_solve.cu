@@ -975,6 +975,8 @@ k_resid_w(SolveParams p, Work w, int outer) {
   __shared__ __align__(16) double cs_all[4][kWarpCap];
   __shared__ int32_t sup_all[4][kWarpCap];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();
+  pdl_trigger();
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * 4 + warp;
   if (b >= p.sig_hi || !w.active[b]) return;
   const int t = w.cnt[b];
@@ -1022,6 +1024,11 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   __shared__ int32_t sup_all[NW][kWarpCap];
   __shared__ __align__(16) double sq_all[NW][TB * (TB + 4)];  // powers of T (padded rows)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();
+  pdl_trigger();
+  // this iteration's active count starts here (incremented by the stopping
+  // rules after learning; read by the host one graph chunk later)
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi || !w.active[b]) return;
   double* s1 = sq_all[warp];
@@ -1036,7 +1043,7 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   }
   if (w.cnt[b] > TB) {
     if (lane == 0) {
-      const int slot = atomicAdd(&w.counters[kBigCount], 1);
+      const int slot = atomicAdd(&w.counters[kBigCount + (outer & 1)], 1);
       big_list[slot] = (int32_t)b;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1067,7 +1074,10 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
   __shared__ double s_L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kBlockThreads / 32;
-  const int count = w.counters[kBigCount];
+  pdl_wait();
+  pdl_trigger();
+  const int count = w.counters[kBigCount + (outer & 1)];
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kBigCount + ((outer + 1) & 1)] = 0;
   const int64_t cap = p.cap;
   for (int li = blockIdx.x; li < count; li += gridDim.x) {
     const int64_t b = big_list[li];
@@ -1569,19 +1579,20 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
   if (smem_g <= 200 * 1024) {
     cudaFuncSetAttribute(k_learn_block<OPT, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g);
-    k_learn_block<OPT, true><<<grid, kBlockThreads, smem_g, s>>>(p, w, outer, big_list);
+    launch_pdl(k_learn_block<OPT, true>, dim3(grid), dim3(kBlockThreads), smem_g, s, p, w,
+               outer, (const int32_t*)big_list);
   } else {
     const size_t sm = block_smem_bytes(p.cap, false);
     cudaFuncSetAttribute(k_learn_block<OPT, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_learn_block<OPT, false><<<grid, kBlockThreads, sm, s>>>(p, w, outer, big_list);
+    launch_pdl(k_learn_block<OPT, false>, dim3(grid), dim3(kBlockThreads), sm, s, p, w, outer,
+               (const int32_t*)big_list);
   }
 }
 
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                   cudaStream_t s) {
   int32_t* big_list = w.big_list;
-  cudaMemsetAsync(&w.counters[kBigCount], 0, sizeof(int32_t), s);
   // max_cnt: upper bound on the support size after this iteration's select
   // (ties can exceed it; those signals fall through to the block kernel).
   const int64_t nsig = p.sig_hi - p.sig_lo;
@@ -1589,14 +1600,14 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
   auto learn = [&](auto tb) {
     constexpr int TB = decltype(tb)::value;
     constexpr int NW = learn_warps<TB>();
+    const dim3 lg(blocks_for(NW)), lb(32 * NW);
     switch (p.opt) {
-      case 0: k_learn_warp<TB, 0><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
-      case 1: k_learn_warp<TB, 1><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
-      default: k_learn_warp<TB, 2><<<blocks_for(NW), 32 * NW, 0, s>>>(p, w, outer, big_list); break;
+      case 0: launch_pdl(k_learn_warp<TB, 0>, lg, lb, 0, s, p, w, outer, big_list); break;
+      case 1: launch_pdl(k_learn_warp<TB, 1>, lg, lb, 0, s, p, w, outer, big_list); break;
+      default: launch_pdl(k_learn_warp<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
     }
-    if (!p.sep) {
-      k_resid_w<TB><<<(unsigned)((nsig + 3) / 4), 128, 0, s>>>(p, w, outer);
-    }
+    if (!p.sep)
+      launch_pdl(k_resid_w<TB>, dim3((unsigned)((nsig + 3) / 4)), dim3(128), 0, s, p, w, outer);
   };
   if (max_cnt <= 8)
     learn(std::integral_constant<int, 8>());
