@@ -229,11 +229,30 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
   return M;
 }
 
-__device__ void select_top_warp(const SolveParams& p, const Work& w, int64_t b, int lane) {
+// Near-tied th == 1 selection: exact rescoring of the band, every tie with the
+// exact maximum injected (see above).  Updates sup / cnt / mask / changed.
+__device__ void select_near_tie(const SolveParams& p, const Work& w, int64_t b, double v1,
+                                double delta, int t_old, int lane) {
+  PickState ps{t_old, 0, 0};
+  if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
+  const double cut = v1 - 2.0 * delta;
+  const double* r = w.r64 + b * p.ldm;
+  const double M = band_pass(p, w, b, cut, r, 0, -1.0, ps, lane);
+  if (M > 0.0) band_pass(p, w, b, cut, r, 1, M, ps, lane);
+  if (lane == 0) pick_finish(p, w, b, ps);
+  __syncwarp();
+}
+
+// Merge of one signal's candidate records: best (v1, i1) over all tiles (the
+// lowest atom wins an exact tie) and the runner-up value v2.
+__device__ __forceinline__ void cand_merge_warp(const SolveParams& p, const Work& w, int64_t b,
+                                                Cand first, double& v1, int& i1, double& v2,
+                                                int lane) {
+  v1 = first.v1;
+  v2 = first.v2;
+  i1 = first.i1;
   const Cand* cd = w.cand + b * p.ntile;
-  double v1 = -1.0, v2 = -1.0;
-  int i1 = 0x7fffffff;
-  for (int64_t t = lane; t < p.ntile; t += 32) {
+  for (int64_t t = lane + 32; t < p.ntile; t += 32) {
     const Cand c = cd[t];
     if (c.v1 > v1 || (c.v1 == v1 && c.i1 < i1)) {
       v2 = fmax(v1, c.v2);
@@ -255,21 +274,31 @@ __device__ void select_top_warp(const SolveParams& p, const Work& w, int64_t b, 
       v2 = fmax(v2, ov1);
     }
   }
-  PickState ps{w.cnt[b], 0, 0};
+}
+
+__device__ void select_top_warp(const SolveParams& p, const Work& w, int64_t b, int lane) {
+  double v1, v2;
+  int i1;
+  cand_merge_warp(p, w, b, lane < p.ntile ? w.cand[b * p.ntile + lane] : cand_empty(), v1, i1,
+                  v2, lane);
+  const int t_old = w.cnt[b];
   if (v1 > 0.0) {  // else zero column: inject nothing (clomp.cpp:48)
     const double delta = p.delta_rel * p.colnorm_max * sqrt(w.loss[b]);
     if (v1 - v2 > delta) {
-      if (lane == 0) pick_atom(p, w, b, i1, ps);
+      PickState ps{t_old, 0, 0};
+      if (lane == 0) {
+        pick_atom(p, w, b, i1, ps);
+        pick_finish(p, w, b, ps);
+      }
+      __syncwarp();
     } else {
-      if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
-      const double cut = v1 - 2.0 * delta;
-      const double* r = w.r64 + b * p.ldm;
-      const double M = band_pass(p, w, b, cut, r, 0, -1.0, ps, lane);
-      if (M > 0.0) band_pass(p, w, b, cut, r, 1, M, ps, lane);
+      select_near_tie(p, w, b, v1, delta, t_old, lane);
     }
+  } else {
+    PickState ps{t_old, 0, 0};
+    if (lane == 0) pick_finish(p, w, b, ps);
+    __syncwarp();
   }
-  if (lane == 0) pick_finish(p, w, b, ps);
-  __syncwarp();
 }
 
 __global__ void k_select_top(SolveParams p, Work w) {
@@ -894,21 +923,15 @@ __device__ __forceinline__ void stage_gram_async(const SolveParams& p, const Wor
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// Epochs of one outer iteration on a support of t atoms whose Gram matrix is
+// staged in s1 (row stride TB + 4, symmetric): c, b (and the optimizer moments)
+// of this lane's atom come in registers; the learned coefficients (and
+// moments) are stored.
 template <int TB, int OPT>
-__device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
-                                int outer, double* cs, int32_t* sups, double* s1,
-                                double* s2, int lane) {
-  const int t = w.cnt[b];
-  const int t0 = w.gcnt[b];
-  const int64_t cap = p.cap;
-  if (lane < t) sups[lane] = w.sup[b * cap + lane];
-  __syncwarp();
-  constexpr int LDS = TB + 4;  // staged Gram (s1, see stage_gram_async)
-  warp_extend_gram<TB>(p, w, b, t0, t, lane, sups, s1, LDS);
-  if (lane == 0) w.gcnt[b] = t;
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-
+__device__ __forceinline__ void learn_epochs(const SolveParams& p, const Work& w, int64_t b,
+                                             int outer, double* cs, double* s1, int lane, int t,
+                                             double c, double bi, double m1, double m2) {
+  constexpr int LDS = TB + 4;
   double g[TB];
   const double twolr = 2.0 * p.lr;
 #pragma unroll
@@ -920,16 +943,8 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
     else
       g[j] = gij;
   }
-  double c = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
-  if (lane < t) {
-    c = w.coef[b * cap + lane];
-    bi = w.bvec[b * cap + lane];
-    if (OPT == 0) bi = twolr * bi;
-    if (OPT != 0) {
-      m1 = w.mom1[b * cap + lane];
-      m2 = w.mom2[b * cap + lane];
-    }
-  }
+  if (lane >= t) c = bi = m1 = m2 = 0.0;
+  if (OPT == 0) bi = twolr * bi;
   cs[lane] = c;
   __syncwarp();
   const int step0 = (outer - 1) * p.inner;
@@ -952,6 +967,7 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
   } else {
     epochs_dispatch<TB, OPT>(g, c, bi, m1, m2, cs, p, step0, lane, t);
   }
+  const int64_t cap = p.cap;
   if (lane < t) {
     w.coef[b * cap + lane] = c;
     if (OPT != 0) {
@@ -959,6 +975,35 @@ __device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
       w.mom2[b * cap + lane] = m2;
     }
   }
+}
+
+// General entry (every path): state from global memory, Gram extension by
+// warp_extend_gram, then learn_epochs.  The caller staged the old Gram rows.
+template <int TB, int OPT>
+__device__ void learn_warp_body(const SolveParams& p, const Work& w, int64_t b,
+                                int outer, double* cs, int32_t* sups, double* s1,
+                                double* s2, int lane) {
+  (void)s2;
+  const int t = w.cnt[b];
+  const int t0 = w.gcnt[b];
+  const int64_t cap = p.cap;
+  if (lane < t) sups[lane] = w.sup[b * cap + lane];
+  __syncwarp();
+  constexpr int LDS = TB + 4;  // staged Gram (s1, see stage_gram_async)
+  warp_extend_gram<TB>(p, w, b, t0, t, lane, sups, s1, LDS);
+  if (lane == 0) w.gcnt[b] = t;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  double c = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
+  if (lane < t) {
+    c = w.coef[b * cap + lane];
+    bi = w.bvec[b * cap + lane];
+    if (OPT != 0) {
+      m1 = w.mom1[b * cap + lane];
+      m2 = w.mom2[b * cap + lane];
+    }
+  }
+  learn_epochs<TB, OPT>(p, w, b, outer, cs, s1, lane, t, c, bi, m1, m2);
 }
 
 // Residual, loss and stopping rules after the learning phase, one warp per
@@ -1004,6 +1049,169 @@ k_resid_w(SolveParams p, Work w, int outer) {
 // TB: support-size bucket this launch is compiled for (8, 16 or 32).  Signals
 // whose support outgrew it (possible only through ties) are queued for the
 // block kernel.
+// Bulk variant of stage_gram_async for learn_fast: one TMA bulk copy per
+// Gram row (cp.async.bulk, completion on the warp's mbarrier) instead of one
+// 8-byte cp.async per element, so the LSU queue stays free for the selection
+// and extension loads.  Rows are copied in 16-byte units (t0 & ~1 entries); an
+// odd last column comes from row t0-1 by symmetry with ordinary loads.
+__device__ __forceinline__ void stage_gram_bulk(const SolveParams& p, const Work& w, int64_t b,
+                                                int t0, double* sG, int lds, uint64_t* bar,
+                                                int lane) {
+  const double* G = w.gram + b * p.cap * p.cap;
+  const int ne = t0 & ~1;
+  const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(bar);
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
+                 "r"((uint32_t)(t0 * ne * 8))
+                 : "memory");
+  __syncwarp();
+  if (lane < t0 && ne > 0) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sG + lane * lds);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(G + (int64_t)lane * p.cap), "r"((uint32_t)(ne * 8)), "r"(bar_a)
+        : "memory");
+  }
+  if ((t0 & 1) && lane < t0) sG[lane * lds + t0 - 1] = G[(int64_t)(t0 - 1) * p.cap + lane];
+}
+
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
+      "@!P bra W_%=;\n"
+      "}\n" ::"r"(a)
+      : "memory");
+}
+
+// The batched th == 1 path with the context's A^T A (config 2): selection,
+// Gram extension and learning for one signal with the fewest dependent
+// memory round trips.  Every piece of the signal's state is loaded at once
+// (round trip 1, overlapping the asynchronous Gram staging), the selection
+// works on registers (support membership by ballot instead of the mask), the
+// new Gram row comes from gfull and b_k = a_k . y (round trip 2), and the
+// epochs start with everything in registers / shared memory.
+template <int TB, int OPT>
+__device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, int64_t b,
+                                           int outer, int32_t* big_list, double* cs,
+                                           double* s1, uint64_t* bar, int lane) {
+  const int64_t cap = p.cap;  // >= 32
+  constexpr int LDS = TB + 4;
+  // round trip 1: all independent loads (garbage beyond cnt is never used)
+  const int act = w.active[b];
+  const int t_old = w.cnt[b];
+  const int t0 = w.gcnt[b];
+  const double Lb = w.loss[b];
+  int32_t sup_l = w.sup[b * cap + lane];
+  double c_l = w.coef[b * cap + lane];
+  double b_l = w.bvec[b * cap + lane];
+  double m1 = 0.0, m2 = 0.0;
+  if (OPT != 0) {
+    m1 = w.mom1[b * cap + lane];
+    m2 = w.mom2[b * cap + lane];
+  }
+  const Cand first = lane < p.ntile ? w.cand[b * p.ntile + lane] : cand_empty();
+  if (!act) return;
+  const bool staged = t0 <= TB;
+  if (staged) stage_gram_bulk(p, w, b, t0, s1, LDS, bar, lane);
+
+  // K1c (th == 1): clear winner from the records, near-ties rescored exactly
+  double v1, v2;
+  int i1;
+  cand_merge_warp(p, w, b, first, v1, i1, v2, lane);
+  int t = t_old;
+  if (t_old >= 32) {  // support wider than the warp: mask-based general path
+    select_top_warp(p, w, b, lane);
+    if (!w.active[b]) {
+      if (staged) mbar_wait0(bar);
+      return;
+    }
+    t = w.cnt[b];
+  } else if (v1 > 0.0) {  // else zero column: inject nothing (clomp.cpp:48)
+    const double delta = p.delta_rel * p.colnorm_max * sqrt(Lb);
+    if (v1 - v2 > delta) {
+      const bool dup = __any_sync(kFull, lane < t_old && sup_l == i1);
+      if (!dup) {
+        if (t_old >= cap) {  // support full: kStatusCapacity
+          if (lane == 0) {
+            w.status[b] = kStatusCapacity;
+            w.active[b] = 0;
+            w.changed[b] = 0;
+          }
+          if (staged) mbar_wait0(bar);
+          return;
+        }
+        if (lane == t_old) sup_l = i1;
+        if (lane == 0) {
+          w.sup[b * cap + t_old] = i1;
+          atomicOr(&w.maskbits[b * p.mwords + (i1 >> 5)], 1u << (i1 & 31));
+          w.cnt[b] = t_old + 1;
+          atomicMax(&w.counters[kMaxCount], t_old + 1);
+        }
+        t = t_old + 1;
+      }
+      if (lane == 0) w.changed[b] = dup ? 0 : 1;
+    } else {
+      select_near_tie(p, w, b, v1, delta, t_old, lane);
+      if (!w.active[b]) {
+        if (staged) mbar_wait0(bar);
+        return;
+      }
+      t = w.cnt[b];
+      sup_l = w.sup[b * cap + lane];
+    }
+  } else if (lane == 0) {
+    w.changed[b] = 0;
+  }
+  if (t > TB || t0 > TB) {  // outgrew this bucket: the block kernel learns it
+    if (lane == 0) {
+      const int slot = atomicAdd(&w.counters[kBigCount + (outer & 1)], 1);
+      big_list[slot] = (int32_t)b;
+    }
+    if (staged) mbar_wait0(bar);
+    return;
+  }
+
+  // round trip 2: Gram row / column of the new atoms from gfull, b_k = a_k . y
+  double* G = w.gram + b * cap * cap;
+  const double* y = w.y64 + b * p.ldm;
+  for (int k = t0; k < t; ++k) {
+    const int64_t jk = __shfl_sync(kFull, sup_l, k);
+    if (lane <= k) {
+      const double v = w.gfull[jk * p.n + sup_l];
+      G[(int64_t)k * cap + lane] = v;
+      G[(int64_t)lane * cap + k] = v;
+      s1[k * LDS + lane] = v;
+      s1[lane * LDS + k] = v;
+    }
+    const float* ak = w.at32 + jk * p.ldm;
+    double accb = 0.0;
+#pragma unroll 4
+    for (int64_t i0 = 4 * lane; i0 < p.ldm; i0 += 128) {
+      const float4 a = *reinterpret_cast<const float4*>(ak + i0);
+      const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
+      const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+      accb = fma(f2d(a.x), y01.x, accb);
+      accb = fma(f2d(a.y), y01.y, accb);
+      accb = fma(f2d(a.z), y23.x, accb);
+      accb = fma(f2d(a.w), y23.y, accb);
+    }
+    accb = warp_sum(accb);
+    if (lane == k) {  // new atoms start at 0 (clomp.hpp:53-54)
+      b_l = accb;
+      c_l = m1 = m2 = 0.0;
+    }
+    if (lane == 0) w.bvec[b * cap + k] = accb;
+  }
+  if (lane == 0) w.gcnt[b] = t;
+  mbar_wait0(bar);
+  __syncwarp();
+  learn_epochs<TB, OPT>(p, w, b, outer, cs, s1, lane, t, c_l, b_l, m1, m2);
+}
+
 template <int TB>
 constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
 
@@ -1030,8 +1238,9 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   // rules after learning; read by the host one graph chunk later)
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
-  if (b >= p.sig_hi || !w.active[b]) return;
+  if (b >= p.sig_hi) return;
   double* s1 = sq_all[warp];
+  if (!w.active[b]) return;
   const int t0 = w.gcnt[b];
   if (t0 <= TB) stage_gram_async(p, w, b, t0, s1, TB + 4, lane);
   if (p.fuse_select) {  // this iteration's th == 1 selection (K1c) first
@@ -1053,6 +1262,30 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   int32_t* sups = sup_all[warp];
   double* s2 = nullptr;
   learn_warp_body<TB, OPT>(p, w, b, outer, cs, sups, s1, s2, lane);
+}
+
+// Same bucket, the fast path (learn_fast): batched th == 1 with gfull.
+template <int TB, int OPT>
+__global__ void __launch_bounds__(32 * learn_warps<TB>(), learn_min_blocks<TB>())
+k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
+  constexpr int NW = learn_warps<TB>();
+  __shared__ __align__(16) double cs_all[NW][2 * kWarpCap];
+  __shared__ __align__(16) double sq_all[NW][TB * (TB + 4)];
+  __shared__ __align__(8) uint64_t bar_all[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&bar_all[warp]))
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
+  const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
+  if (b >= p.sig_hi) return;
+  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sq_all[warp], &bar_all[warp], lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -1601,10 +1834,19 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     constexpr int TB = decltype(tb)::value;
     constexpr int NW = learn_warps<TB>();
     const dim3 lg(blocks_for(NW)), lb(32 * NW);
-    switch (p.opt) {
-      case 0: launch_pdl(k_learn_warp<TB, 0>, lg, lb, 0, s, p, w, outer, big_list); break;
-      case 1: launch_pdl(k_learn_warp<TB, 1>, lg, lb, 0, s, p, w, outer, big_list); break;
-      default: launch_pdl(k_learn_warp<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
+    const bool fast = p.fuse_select && w.gfull && !p.sep && p.cap >= 32 && (p.cap & 1) == 0;
+    if (fast) {
+      switch (p.opt) {
+        case 0: launch_pdl(k_learn_fast<TB, 0>, lg, lb, 0, s, p, w, outer, big_list); break;
+        case 1: launch_pdl(k_learn_fast<TB, 1>, lg, lb, 0, s, p, w, outer, big_list); break;
+        default: launch_pdl(k_learn_fast<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
+      }
+    } else {
+      switch (p.opt) {
+        case 0: launch_pdl(k_learn_warp<TB, 0>, lg, lb, 0, s, p, w, outer, big_list); break;
+        case 1: launch_pdl(k_learn_warp<TB, 1>, lg, lb, 0, s, p, w, outer, big_list); break;
+        default: launch_pdl(k_learn_warp<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
+      }
     }
     if (!p.sep)
       launch_pdl(k_resid_w<TB>, dim3((unsigned)((nsig + 3) / 4)), dim3(128), 0, s, p, w, outer);
