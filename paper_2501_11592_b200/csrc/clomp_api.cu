@@ -385,6 +385,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // th == 1: the selection (K1c, near-tie rescoring included) runs at the top
   // of the learning kernel, one warp per signal, instead of its own launch.
   p.fuse_select = (!full_scores && !p.sep) ? 1 : 0;
+  p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
 
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;

@@ -104,6 +104,9 @@ struct SolveParams {
   int64_t nr, nc, mr, mc, ldr, ldc;
   // th == 1 selection runs inside the learning kernel (warp per signal)
   int32_t fuse_select;
+  // r64 is not stored by the residual kernel; the rare near-tie rescoring
+  // recomputes the row it needs (tensor path, th == 1, ldm <= 512)
+  int32_t lazy_r64;
   double a_inv_scale;       // 1 / (power-of-two scale of the fp16 dictionary split)
 };
 

@@ -231,8 +231,42 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
 
 // Near-tied th == 1 selection: exact rescoring of the band, every tie with the
 // exact maximum injected (see above).  Updates sup / cnt / mask / changed.
+// r64 row of signal b from its current support and coefficients (same
+// per-element operation order as warp_residual), for lazy_r64 contexts.
+__device__ void recompute_r64_row(const SolveParams& p, const Work& w, int64_t b, int t,
+                                  int lane) {
+  const int64_t cap = p.cap;
+  const float* y = w.y32 + b * p.ldm;
+  for (int64_t i0 = 0; i0 < p.ldm; i0 += 128) {  // lane owns rows i0 + lane + 32 q
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < t; k0 += 32) {  // support in warp-sized pieces
+      const int kk = k0 + lane;
+      const int32_t sk = kk < t ? w.sup[b * cap + kk] : 0;
+      const double ck = kk < t ? w.coef[b * cap + kk] : 0.0;
+      const int kn = t - k0 < 32 ? t - k0 : 32;
+#pragma unroll 4
+      for (int k = 0; k < kn; ++k) {
+        const int64_t a = (int64_t)__shfl_sync(kFull, sk, k) * p.ldm;
+        const double c = __shfl_sync(kFull, ck, k);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t i = i0 + lane + 32 * q;
+          if (i < p.ldm) acc[q] = fma(f2d(w.at32[a + i]), c, acc[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + lane + 32 * q;
+      if (i < p.ldm) w.r64[b * p.ldm + i] = acc[q] - f2d(y[i]);
+    }
+  }
+  __syncwarp();
+}
+
 __device__ void select_near_tie(const SolveParams& p, const Work& w, int64_t b, double v1,
                                 double delta, int t_old, int lane) {
+  if (p.lazy_r64) recompute_r64_row(p, w, b, t_old, lane);
   PickState ps{t_old, 0, 0};
   if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
   const double cut = v1 - 2.0 * delta;
@@ -726,7 +760,7 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
                                  double* sG, int lds) {
   const int64_t cap = p.cap, ldm = p.ldm;
   double* G = w.gram + b * cap * cap;
-  const double* y = w.y64 + b * ldm;
+  const float* y = w.y32 + b * ldm;  // y is fp32 data: exact in fp64 on load
   if (p.sep) {
     // Separable atoms: G[(i,j),(i',j')] = Gr[i][i'] * Gc[j][j']; b_k = Z[p_k]
     // with Z = A_r^T Y A_c (fp64, once per solve).
@@ -765,8 +799,9 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
       double accb = 0.0;
       for (int64_t i0 = 4 * lane; i0 < ldm; i0 += 128) {
         const float4 a = *reinterpret_cast<const float4*>(ak + i0);
-        const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
-        const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+        const float4 yv = *reinterpret_cast<const float4*>(y + i0);
+        const double2 y01 = make_double2(f2d(yv.x), f2d(yv.y));
+        const double2 y23 = make_double2(f2d(yv.z), f2d(yv.w));
         accb = fma(f2d(a.x), y01.x, accb);
         accb = fma(f2d(a.y), y01.y, accb);
         accb = fma(f2d(a.z), y23.x, accb);
@@ -791,8 +826,9 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
     double accb = 0.0;
     for (int64_t i0 = 4 * lane; i0 < ldm; i0 += 128) {
       const float4 av = *reinterpret_cast<const float4*>(ak + i0);
-      const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
-      const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+      const float4 yv = *reinterpret_cast<const float4*>(y + i0);
+      const double2 y01 = make_double2(f2d(yv.x), f2d(yv.y));
+      const double2 y23 = make_double2(f2d(yv.z), f2d(yv.w));
       const double ax = f2d(av.x), ay = f2d(av.y), az = f2d(av.z), aw = f2d(av.w);
       accb = fma(ax, y01.x, accb);
       accb = fma(ay, y01.y, accb);
@@ -839,7 +875,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
                                 const double* cs, const int32_t* sups, int t,
                                 int lane) {
   const int64_t ldm = p.ldm;
-  const double* y = w.y64 + b * ldm;
+  const float* y = w.y32 + b * ldm;  // fp32 data, exact in fp64
   double lacc = 0.0;
   double rr[16];  // the last 512-row pass stays in registers for the split
   for (int64_t base = 0; base < ldm; base += 512) {
@@ -866,14 +902,17 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
       const int64_t i0 = base + 128 * q + 4 * lane;
       if (base + 128 * q < ldm) {
         const int64_t o = b * ldm + i0;
-        const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
-        const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+        const float4 yv = *reinterpret_cast<const float4*>(y + i0);
+        const double2 y01 = make_double2(f2d(yv.x), f2d(yv.y));
+        const double2 y23 = make_double2(f2d(yv.z), f2d(yv.w));
         r[4 * q + 0] -= y01.x;
         r[4 * q + 1] -= y01.y;
         r[4 * q + 2] -= y23.x;
         r[4 * q + 3] -= y23.y;
-        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
-        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
+        if (!p.lazy_r64) {
+          *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
+          *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) lacc = fma(r[4 * q + e], r[4 * q + e], lacc);
       }
@@ -1177,7 +1216,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
 
   // round trip 2: Gram row / column of the new atoms from gfull, b_k = a_k . y
   double* G = w.gram + b * cap * cap;
-  const double* y = w.y64 + b * p.ldm;
+  const float* y = w.y32 + b * p.ldm;  // fp32 data, exact in fp64
   for (int k = t0; k < t; ++k) {
     const int64_t jk = __shfl_sync(kFull, sup_l, k);
     if (lane <= k) {
@@ -1192,8 +1231,9 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
 #pragma unroll 4
     for (int64_t i0 = 4 * lane; i0 < p.ldm; i0 += 128) {
       const float4 a = *reinterpret_cast<const float4*>(ak + i0);
-      const double2 y01 = *reinterpret_cast<const double2*>(y + i0);
-      const double2 y23 = *reinterpret_cast<const double2*>(y + i0 + 2);
+      const float4 yv = *reinterpret_cast<const float4*>(y + i0);
+      const double2 y01 = make_double2(f2d(yv.x), f2d(yv.y));
+      const double2 y23 = make_double2(f2d(yv.z), f2d(yv.w));
       accb = fma(f2d(a.x), y01.x, accb);
       accb = fma(f2d(a.y), y01.y, accb);
       accb = fma(f2d(a.z), y23.x, accb);
@@ -1221,8 +1261,13 @@ constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
 #ifndef CL_LEARN16_MINB
 #define CL_LEARN16_MINB 4
 #endif
+#ifndef CL_LEARN8_MINB
+#define CL_LEARN8_MINB 4
+#endif
 template <int TB>
-constexpr int learn_min_blocks() { return TB == 32 ? CL_LEARN32_MINB : CL_LEARN16_MINB; }
+constexpr int learn_min_blocks() {
+  return TB == 32 ? CL_LEARN32_MINB : (TB == 16 ? CL_LEARN16_MINB : CL_LEARN8_MINB);
+}
 
 template <int TB, int OPT>
 __global__ void __launch_bounds__(32 * learn_warps<TB>(), learn_min_blocks<TB>())
