@@ -967,9 +967,9 @@ __device__ __forceinline__ void stage_gram_async(const SolveParams& p, const Wor
 // of this lane's atom come in registers; the learned coefficients (and
 // moments) are stored.
 template <int TB, int OPT>
-__device__ __forceinline__ void learn_epochs(const SolveParams& p, const Work& w, int64_t b,
-                                             int outer, double* cs, double* s1, int lane, int t,
-                                             double c, double bi, double m1, double m2) {
+__device__ __forceinline__ double learn_epochs(const SolveParams& p, const Work& w, int64_t b,
+                                               int outer, double* cs, double* s1, int lane, int t,
+                                               double c, double bi, double m1, double m2) {
   constexpr int LDS = TB + 4;
   double g[TB];
   const double twolr = 2.0 * p.lr;
@@ -1014,6 +1014,7 @@ __device__ __forceinline__ void learn_epochs(const SolveParams& p, const Work& w
       w.mom2[b * cap + lane] = m2;
     }
   }
+  return c;
 }
 
 // General entry (every path): state from global memory, Gram extension by
@@ -1136,7 +1137,7 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
 template <int TB, int OPT>
 __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, int64_t b,
                                            int outer, int32_t* big_list, double* cs,
-                                           double* s1, uint64_t* bar, int lane) {
+                                           int32_t* sups, double* s1, uint64_t* bar, int lane) {
   const int64_t cap = p.cap;  // >= 32
   constexpr int LDS = TB + 4;
   // round trip 1: all independent loads (garbage beyond cnt is never used)
@@ -1153,6 +1154,12 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
     m2 = w.mom2[b * cap + lane];
   }
   const Cand first = lane < p.ntile ? w.cand[b * p.ntile + lane] : cand_empty();
+  CtlState ctl{};  // stopping-rule state for the residual tail
+  if (p.mode == kModePerSignal) {
+    ctl.best_L = w.best_L[b];
+    ctl.prev_L = w.prev_L[b];
+    ctl.stall = w.stall[b];
+  }
   if (!act) return;
   const bool staged = t0 <= TB;
   if (staged) stage_gram_bulk(p, w, b, t0, s1, LDS, bar, lane);
@@ -1162,6 +1169,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
   int i1;
   cand_merge_warp(p, w, b, first, v1, i1, v2, lane);
   int t = t_old;
+  int chg = 0;  // mask changed this iteration (stall rule)
   if (t_old >= 32) {  // support wider than the warp: mask-based general path
     select_top_warp(p, w, b, lane);
     if (!w.active[b]) {
@@ -1169,6 +1177,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
       return;
     }
     t = w.cnt[b];
+    chg = w.changed[b];
   } else if (v1 > 0.0) {  // else zero column: inject nothing (clomp.cpp:48)
     const double delta = p.delta_rel * p.colnorm_max * sqrt(Lb);
     if (v1 - v2 > delta) {
@@ -1192,7 +1201,8 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
         }
         t = t_old + 1;
       }
-      if (lane == 0) w.changed[b] = dup ? 0 : 1;
+      chg = dup ? 0 : 1;
+      if (lane == 0) w.changed[b] = chg;
     } else {
       select_near_tie(p, w, b, v1, delta, t_old, lane);
       if (!w.active[b]) {
@@ -1200,6 +1210,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
         return;
       }
       t = w.cnt[b];
+      chg = w.changed[b];
       sup_l = w.sup[b * cap + lane];
     }
   } else if (lane == 0) {
@@ -1249,7 +1260,33 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
   if (lane == 0) w.gcnt[b] = t;
   mbar_wait0(bar);
   __syncwarp();
-  learn_epochs<TB, OPT>(p, w, b, outer, cs, s1, lane, t, c_l, b_l, m1, m2);
+  const double c = learn_epochs<TB, OPT>(p, w, b, outer, cs, s1, lane, t, c_l, b_l, m1, m2);
+
+  // residual r = A_S c - y, its fp16 split for the next K1, the loss and the
+  // stopping rules (clomp.cpp:236-242, 253-273) in the same warp: the L2-bound
+  // gathers of some warps overlap the epochs of others.
+  __syncwarp();
+  if (lane < t) {
+    cs[lane] = c;
+    sups[lane] = sup_l;
+  } else if (lane < kWarpCap) {
+    cs[lane] = 0.0;
+    sups[lane] = 0;
+  }
+  __syncwarp();
+  const double L = warp_residual(p, w, b, cs, sups, t, lane);
+  int snap = 0;
+  if (lane == 0) {
+    if (p.mode == kModePerSignal) {
+      ctl.cnt = t;
+      ctl.changed = chg;
+      snap = control_signal(p, w, b, outer, L, ctl);
+    } else {
+      w.loss[b] = L;
+    }
+  }
+  snap = __shfl_sync(kFull, snap, 0);
+  if (snap && lane < t) w.best_coef[b * p.cap + lane] = c;
 }
 
 template <int TB>
@@ -1317,6 +1354,7 @@ k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   __shared__ __align__(16) double cs_all[NW][2 * kWarpCap];
   __shared__ __align__(16) double sq_all[NW][TB * (TB + 4)];
   __shared__ __align__(8) uint64_t bar_all[NW];
+  __shared__ int32_t sup_all[NW][kWarpCap];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -1330,7 +1368,8 @@ k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi) return;
-  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sq_all[warp], &bar_all[warp], lane);
+  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp], sq_all[warp],
+                      &bar_all[warp], lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -1893,7 +1932,7 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
         default: launch_pdl(k_learn_warp<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
       }
     }
-    if (!p.sep)
+    if (!p.sep && !fast)  // the fast kernel finishes its signals' residuals itself
       launch_pdl(k_resid_w<TB>, dim3((unsigned)((nsig + 3) / 4)), dim3(128), 0, s, p, w, outer);
   };
   if (max_cnt <= 8)
