@@ -8,7 +8,7 @@ BASELINE config 2 (configs[1]): N=1024, M=512, K=32, 4096 signals per GPU,
 (SURVEY.md §8d mapping).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1..6] [--colshard] [--max-outer T]
+                    [--config 1..7] [--colshard] [--max-outer T]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A step = one full CLOMP solve (K outer iterations x 200 epochs) of one batch
@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--colshard", action="store_true")
     ap.add_argument("--max-outer", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05")
+    ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05, 3 GEMV")
     return ap.parse_args()
 
 
@@ -133,10 +133,10 @@ def _ref_worker(args):
     return time.perf_counter() - t0, r["code"], Ychunk.shape[1]
 
 
-def reference_round(A64, Y64, cfg, workers: int, extrapolate_to: int = 0):
+def reference_round(A64, Y64, cfg, workers: int, scale: float = 0.0):
     """One bounded sample: `workers` processes x CHUNK signals in parallel.
-    With extrapolate_to, each worker runs cfg.max_outer outer iterations and
-    the time is scaled to extrapolate_to iterations."""
+    With scale, the sample is a truncated solve (reference_plan) and its wall
+    time is multiplied by scale to extrapolate to the full one."""
     import dataclasses
     import multiprocessing as mp
 
@@ -154,8 +154,8 @@ def reference_round(A64, Y64, cfg, workers: int, extrapolate_to: int = 0):
     if any(code != 0 for _, code, _ in res):
         raise RuntimeError("reference solve failed")
     sig = sum(n for _, _, n in res)
-    if extrapolate_to:
-        wall = wall * extrapolate_to / cfg.max_outer
+    if scale:
+        wall = wall * scale
     return sig / wall, wall, sig
 
 
@@ -177,12 +177,26 @@ def host_workers():
 
 
 def reference_plan(c):
-    """(config for the timed sample, extrapolation target or 0, note)."""
+    """(config for the timed sample, wall-time scale factor or 0, note).
+
+    The reference's cost per outer iteration does not depend on the support
+    (every product is dense over N: clomp.cpp:84, 89, 237, 245) and is
+    2*inner_steps + 3 dense products (residual, correlation, inner_steps x
+    (forward, transposed), final loss), so truncated samples extrapolate
+    linearly."""
     cfg = solver_config(c)
+    if c["n"] * c["m"] > 4_000_000 and c["batch"] == 1:
+        # one signal per worker: ~100 s per full outer iteration per core, so
+        # time one outer iteration with 8 inner steps
+        full_outer, full_inner = cfg.max_outer, cfg.inner_steps
+        cfg.max_outer, cfg.inner_steps = 1, 8
+        scale = full_outer * (2 * full_inner + 3) / (2 * cfg.inner_steps + 3)
+        return cfg, scale, (f"1 outer iteration with 8 inner steps timed, extrapolated "
+                            f"x{scale:.0f} (cost per outer iteration = 2*inner+3 dense products)")
     if c["n"] * c["m"] > 4_000_000:  # config 3: time 2 outer iterations per worker
         full = cfg.max_outer
         cfg.max_outer = 2
-        return cfg, full, f"2 outer iterations timed, extrapolated x{full / 2:.0f}"
+        return cfg, full / 2, f"2 outer iterations timed, extrapolated x{full / 2:.0f}"
     return cfg, 0, "full solves"
 
 
@@ -230,6 +244,71 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ clocks
+class NvmlClockSampler:
+    """Polls SM clocks and clock-event reasons through NVML from a thread for
+    the duration of the timed region (a config-2 step is ~2 ms, far shorter than
+    nvidia-smi's sampling period, so the subprocess sampler saw nothing)."""
+
+    NAMES = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self, device: int):
+        import threading
+        import pynvml as nv
+        import torch
+
+        self.nv = nv
+        nv.nvmlInit()
+        pr = torch.cuda.get_device_properties(device)
+        try:
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+        self.smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        self.samples = []  # (t, sm_mhz, reasons bitmask)
+        self.stop_flag = False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.0005)
+
+    def stop(self, t0: float, t1: float):
+        self.stop_flag = True
+        self.t.join()
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        used = inside or self.samples
+        reasons = set()
+        for _, _, rs in used:
+            for name, attr in self.NAMES:
+                if rs & getattr(self.nv, attr, 0):
+                    reasons.add(name)
+        sm = [s[1] for s in used]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(reasons), "samples": len(inside),
+                "source": "NVML polled every ~0.5 ms during the timed region"
+                          + ("" if inside else " (no sample inside it: whole-run samples)")}
+
+
+def clock_sampler(device: int):
+    try:
+        return NvmlClockSampler(device)
+    except Exception:
+        return ClockSampler(device)
+
+
 class ClockSampler:
     def __init__(self, index: int):
         self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
@@ -244,7 +323,7 @@ class ClockSampler:
         except Exception:
             self.p = None
 
-    def stop(self):
+    def stop(self, t0: float = 0.0, t1: float = 0.0):
         if not self.p:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -323,8 +402,10 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local_rank)
+    sampler = clock_sampler(local_rank)
+    time.sleep(0.01)
     evs = []
+    t_region0 = time.perf_counter()
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(1)
@@ -335,9 +416,10 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
+    t_region1 = time.perf_counter()
     if dist:
         torch.distributed.barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop(t_region0, t_region1)
     times = [a.elapsed_time(b) for a, b in evs]
     ms = statistics.mean(times)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -393,6 +475,28 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (seeded cskit::Rng restatement, BASELINE config laws)",
         "config": config_block(c, world, args.colshard),
     }
+    if prof and prof["corr_path"] == 3 and not c["sep"]:
+        # K1b GEMV: HBM-bound; algorithmic bytes per launch = the fp32
+        # dictionary (n x ldm) + the fp64 residuals read + 32-byte candidate
+        # records written.
+        outers = max(prof["outer_iterations"], 1)
+        ldm = (m + 127) // 128 * 128
+        gemv_bytes = 4.0 * n * ldm + 8.0 * B * ldm + 32.0 * B * ((n + 63) // 64)
+        t_launch = prof["corr_ms"] / outers
+        achieved = gemv_bytes / (t_launch / 1000.0) / 1e9
+        peak = peaks.get("hbm_gbs", 7700.0)
+        out["roofline"] = {
+            "kernel": "K1b correlation GEMV A^T r + top-2 epilogue (k_corr_gemv)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "peak_source": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if "hbm_gbs" in peaks
+                            else "fallback 7700 GB/s (B200_PROFILING.md)"),
+            "algorithmic_per_launch": f"4*n*ldm + 8*B*ldm + 32*B*tiles = {gemv_bytes:.4e} B",
+            "avg_launch_ms": t_launch,
+            "phase_ms_per_step": {"corr": prof["corr_ms"], "select_rescan": prof["select_ms"],
+                                  "learn_residual": prof["learn_ms"], "total": prof["total_ms"]},
+            "note": "phase times come from a separately profiled solve (per-iteration sync)",
+        }
     if prof and prof["corr_path"] in (0, 1) and not c["sep"]:
         outers = max(prof["outer_iterations"], 1)
         corr_flops = 2.0 * n * m * B  # one launch: A^T R over the batch

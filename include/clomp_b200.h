@@ -182,7 +182,7 @@ typedef struct cl_stats {
   double corr_ms;               /* device time of the correlation kernels   */
   double learn_ms;              /* device time of the learning kernels      */
   double total_ms;              /* device time of the whole solve           */
-  int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 3xTF32, 2 fused   */
+  int32_t corr_path;            /* 0 fp64 SIMT, 1 tcgen05 split-f16, 2 fused, 3 GEMV */
   int32_t pad0;
   double e2e_ms;                /* cl_solve_batch: wall clock of the whole call  */
   double select_ms;             /* device time of select + fp64 rescans     */
@@ -191,8 +191,10 @@ typedef struct cl_stats {
 } cl_stats;
 int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 
-/* Tuning / test knobs: 0 = auto, 1 = force fp64 SIMT correlation,
- * 2 = force the tcgen05 3xTF32 correlation (th == 1 only). */
+/* Tuning / test knobs: 0 = auto (GEMV for B <= 8, else tcgen05 at th == 1,
+ * else fp64 SIMT), 1 = force fp64 SIMT correlation, 2 = force the tcgen05
+ * split-fp16 correlation (th == 1 only), 3 = force the HBM-bound GEMV
+ * (1 <= B <= 8). */
 int cl_set_corr_path(cl_ctx* ctx, int path);
 /* Dictionary Gram cache G = A^T A (fp64, n x n) used to extend each signal's
  * support Gram matrix by a gather instead of re-streaming atoms:
@@ -211,8 +213,9 @@ int cl_set_profiling(cl_ctx* ctx, int on);
 int cl_set_stream(cl_ctx* ctx, void* stream);
 
 /* Test hook: correlation scores A^T r for a batch of fp32 residuals
- * r (B x m, signal-major host) through the fp64 SIMT kernel (path 1, |scores|)
- * or the tcgen05 3xTF32 kernel (path 2, signed scores); scores: host B x n. */
+ * r (B x m, signal-major host) through the fp64 SIMT kernel (path 1, |scores|),
+ * the tcgen05 split-fp16 kernel (path 2, signed scores) or the GEMV (path 3,
+ * |scores|, B <= 4); scores: host B x n. */
 int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
                     double* scores);
 

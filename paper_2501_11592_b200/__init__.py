@@ -385,7 +385,8 @@ class ClompContext:
                self._h)
 
     def debug_scores(self, r_signal_major, path: int) -> np.ndarray:
-        """A^T r for B x m fp32 residuals via path 1 (fp64 SIMT) or 2 (tcgen05)."""
+        """A^T r for B x m fp32 residuals via path 1 (fp64 SIMT, |.|), 2 (tcgen05,
+        signed) or 3 (the B <= 4 GEMV, |.|)."""
         r = np.ascontiguousarray(r_signal_major, dtype=np.float32)
         out = np.zeros((r.shape[0], self.n), np.float64)
         _raise(lib().cl_debug_scores(self._h, _ptr(r), r.shape[0], int(path), _ptr(out)), self._h)
@@ -526,4 +527,7 @@ CONFIGS = {
     4: dict(name="cfg4_2d_sep", n_r=256, n_c=256, m_r=128, m_c=128, k=1500, batch=64, seed=3),
     5: dict(name="cfg5_2d_sweep_r025", n_r=512, n_c=512, m_r=128, m_c=128, k=13107, batch=1024, seed=4),
     6: dict(name="cfg5_2d_sweep_r05", n_r=512, n_c=512, m_r=256, m_c=256, k=13107, batch=1024, seed=5),
+    # config 3's dictionary solved one signal at a time (the CLI's per-signal
+    # clomp_solve loop, cskit.cpp:543-551): the correlation is the B = 1 GEMV
+    7: dict(name="cfg3_1d_long_single", m=4096, n=16384, k=256, batch=1, value_law=1, snr_db=-1.0, seed=2),
 }

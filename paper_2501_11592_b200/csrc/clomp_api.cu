@@ -51,11 +51,11 @@ struct GraphKey {
   SolveParams p{};
   Work w{};  // every device pointer a captured kernel reads
   const void* wbuf = nullptr;
-  bool tensor = false, full = false;
+  bool tensor = false, full = false, gemv = false;
   cudaStream_t stream = nullptr;
   bool operator==(const GraphKey& o) const {
     return std::memcmp(&p, &o.p, sizeof(p)) == 0 && std::memcmp(&w, &o.w, sizeof(w)) == 0 &&
-           wbuf == o.wbuf && tensor == o.tensor &&
+           wbuf == o.wbuf && tensor == o.tensor && gemv == o.gemv &&
            full == o.full && stream == o.stream;
   }
 };
@@ -304,7 +304,14 @@ struct OutPtrs {
 // y_dev: device pointer, layout_ref ? m x B : B x m.
 int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                const cl_config* c, int mode, const OutPtrs& out) {
-  const bool tensor = !ctx->sep && use_tensor_path(ctx, c);
+  // K1b: a handful of residuals (the CLI's one-signal-at-a-time path) makes
+  // the correlation an HBM-bound GEMV; auto below 9 signals, or forced (3).
+  const bool gemv_fit = !ctx->sep && corr_gemv_supported(ctx->ldm, B);
+  if (ctx->corr_force == 3 && !gemv_fit)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_set_corr_path(3): the GEMV correlation needs 1 <= B <= 8 on a 1D dictionary");
+  const bool gemv = gemv_fit && (ctx->corr_force == 0 || ctx->corr_force == 3);
+  const bool tensor = !ctx->sep && !gemv && use_tensor_path(ctx, c);
   const bool full_scores = c->th < 1.0 || ctx->sep;
   const int64_t cap = support_cap(ctx, c);
   const int W = ctx->world > 1 ? ctx->world : ctx->vshards;
@@ -390,7 +397,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
   cl_stats stats{};
-  stats.corr_path = tensor ? 1 : 0;
+  stats.corr_path = tensor ? 1 : gemv ? 3 : 0;
 
   // One outer iteration (clomp.cpp:235-274): counters reset, K1, K1c (with
   // exact fp64 rescoring of near-ties; fused into the learning kernel when
@@ -423,6 +430,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         wk.cand = w.xg + (int64_t)r * B * p.ntl;
         if (tensor)
           launch_corr_tc(pk, wk, s);
+        else if (gemv)
+          launch_corr_gemv(pk, wk, false, s);
         else
           launch_corr_f64(pk, wk, false, s);
         ++*launches;
@@ -450,6 +459,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     }
     if (tensor)
       launch_corr_tc(p, w, s);
+    else if (gemv)
+      launch_corr_gemv(p, w, full_scores, s);
     else
       launch_corr_f64(p, w, full_scores, s);
     if (!p.fuse_select) launch_select(p, w, full_scores, s);
@@ -511,6 +522,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       cudaEventRecord(ev[1], s);
       if (tensor)
         launch_corr_tc(p, w, s);
+      else if (gemv)
+        launch_corr_gemv(p, w, full_scores, s);
       else
         launch_corr_f64(p, w, full_scores, s);
       cudaEventRecord(ev[4], s);
@@ -559,6 +572,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     key.w = w;
     key.wbuf = ctx->wbuf;
     key.tensor = tensor;
+    key.gemv = gemv;
     key.full = full_scores;
     key.stream = s;
     if (!(key == ctx->gkey)) {
@@ -923,7 +937,7 @@ void cl_destroy(cl_ctx* ctx) {
 
 int cl_set_corr_path(cl_ctx* ctx, int path) {
   if (!ctx) return CL_ERR_INTERNAL;
-  if (path < 0 || path > 2) return fail(ctx, CL_ERR_CONFIG, "cl_set_corr_path: 0, 1 or 2");
+  if (path < 0 || path > 3) return fail(ctx, CL_ERR_CONFIG, "cl_set_corr_path: 0, 1, 2 or 3");
   if (path == 2 && !corr_tc_available())
     return fail(ctx, CL_ERR_UNSUPPORTED, "tcgen05 correlation kernel not available");
   ctx->corr_force = path;
@@ -1237,6 +1251,8 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
   cudaSetDevice(ctx->device);
   if (path == 2 && !ctx->tc_ok)
     return fail(ctx, CL_ERR_UNSUPPORTED, "tcgen05 correlation kernel not available");
+  if (path == 3 && !corr_gemv_supported(ctx->ldm, batch))
+    return fail(ctx, CL_ERR_UNSUPPORTED, "GEMV correlation: 1 <= batch <= 4");
   const int64_t m = ctx->m, n = ctx->n, ldm = ctx->ldm;
   const bool tc = path == 2;
   const int64_t ntile = tc ? (n + corr_tc_tile_atoms() - 1) / corr_tc_tile_atoms()
@@ -1276,7 +1292,10 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
     cudaFree(d);
     for (size_t e = 0; e < h.size(); ++e) scores[e] = h[e];
   } else {
-    launch_corr_f64(p, w, true, s);
+    if (path == 3)
+      launch_corr_gemv(p, w, true, s);
+    else
+      launch_corr_f64(p, w, true, s);
     CL_CUDA(ctx, cudaMemcpyAsync(scores, w.scores, (size_t)(batch * n) * 8,
                                  cudaMemcpyDeviceToHost, s));
     CL_CUDA(ctx, cudaStreamSynchronize(s));

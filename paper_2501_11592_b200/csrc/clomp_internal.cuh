@@ -206,6 +206,11 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // fp64 SIMT correlation with fused top-2 epilogue (th == 1) or full |scores|.
 void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
                      cudaStream_t s);
+// K1b (k_corr_gemv.cu): HBM-bound fp64-accumulating GEMV for B <= 8 residuals,
+// the same candidate records (and optional |scores|) as launch_corr_f64.
+bool corr_gemv_supported(int64_t ldm, int64_t B);
+void launch_corr_gemv(const SolveParams& p, const Work& w, bool full_scores,
+                      cudaStream_t s);
 // tcgen05 3xTF32 correlation with fused top-2 epilogue (th == 1).
 bool corr_tc_available();
 int64_t corr_tc_tile_atoms();

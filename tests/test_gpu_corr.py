@@ -46,3 +46,21 @@ def test_tc_argmax_matches_fp64(gpu_available):
     clear = gap > 2 * delta_rel(m)
     assert clear.mean() > 0.9
     assert np.array_equal(np.argmax(stc, 1)[clear], np.argmax(s64, 1)[clear])
+
+
+@pytest.mark.parametrize("m,n,B", [(128, 256, 1), (512, 1024, 3), (1000, 700, 4), (384, 130, 2),
+                                   (4096, 16384, 1)])
+def test_gemv_scores_fp64_exact(gpu_available, m, n, B):
+    """K1b (the B <= 4 GEMV): fp64 accumulation of fp32 atoms, the same error
+    class as the fp64 SIMT kernel (the selection's 1e-12 bound), ragged n
+    (partial candidate tiles) and m not a multiple of 128."""
+    rng = np.random.default_rng(m * 7 + n + B)
+    A = (rng.standard_normal((m, n)) / np.sqrt(m)).astype(np.float32)
+    R = rng.standard_normal((B, m)).astype(np.float32)
+    ctx = cl.ClompContext(A)
+    sg = ctx.debug_scores(R, 3)
+    exact = np.abs(R.astype(np.float64) @ A.astype(np.float64))
+    rn = np.linalg.norm(R.astype(np.float64), axis=1, keepdims=True)
+    err = np.abs(sg - exact) / rn
+    assert float(err.max()) <= 1e-13, f"max GEMV error {err.max():.3e} of ||a||*||r||"
+    assert np.array_equal(np.argmax(sg, 1), np.argmax(exact, 1))

@@ -35,19 +35,22 @@ def snr_db(x, xh):
     return np.inf if e == 0 else 10 * np.log10(np.sum(x ** 2) / e)
 
 
-@pytest.fixture(scope="module", params=["f64", "tc", "auto"])
+@pytest.fixture(scope="module", params=["f64", "tc", "gemv", "auto"])
 def corr_path(request, gpu_available):
     return request.param
 
 
 def make_ctx(A, path="auto"):
     """path: 'f64' batched pipeline with fp64 SIMT correlation, 'tc' batched
-    pipeline with the tcgen05 correlation, 'auto' library choice (the fused
+    pipeline with the tcgen05 correlation, 'gemv' batched pipeline with the
+    B <= 4 GEMV correlation, 'auto' library choice (the fused
     one-block-per-signal solve for small per-signal problems)."""
     ctx = cl.ClompContext(np.asarray(A, np.float32))
     if path == "f64":
         ctx.set_corr_path(1)
-    if path in ("f64", "tc"):
+    if path == "gemv":
+        ctx.set_corr_path(3)
+    if path in ("f64", "tc", "gemv"):
         ctx.set_fused(False)
     return ctx
 
@@ -58,6 +61,8 @@ def test_solve_matches_reference_golden(case, corr_path):
     A = ARR[f"{name}/A"]
     Y = ARR[f"{name}/Y"]
     cfg = cl.ClompConfig(**case["cfg"])
+    if corr_path == "gemv" and Y.shape[1] > 4:
+        pytest.skip("the GEMV correlation serves batches of at most 4 signals")
     ctx = make_ctx(A, corr_path)
     mode = cl.MODE_JOINT if case["api"] == "batch" else cl.MODE_PER_SIGNAL
     if case["code"] != 0:
@@ -216,3 +221,25 @@ def test_gram_cache_on_off_identical(gpu_available):
     r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
     assert np.array_equal(r1.mask, r0.mask)
     assert rel_coef_err(r1.s, r0.s) <= 1e-10
+
+
+def test_config3_shape_one_signal_gemv_prefix(gpu_available):
+    """The CLI's one-signal-at-a-time path (clomp_solve, cskit.cpp:543-551) at
+    the config-3 shape (N=16384, M=4096, K=256, +-(1+U), noiseless): the
+    correlation is the HBM-bound GEMV (K1b), learning the block kernel.  The
+    first 40 outer iterations are compared with the oracle (the solve is
+    deterministic, so a prefix of it must agree exactly)."""
+    c = cl.CONFIGS[3]
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], 2,
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(c["k"])
+    cfg.max_outer = 40
+    for b in range(2):
+        r = cl.clomp_solve_batch(ctx, Y[:, b:b + 1], cfg, mode=cl.MODE_PER_SIGNAL)
+        assert ctx.stats()["corr_path"] == 3
+        assert np.all(r.status == 0) and r.iterations[0] == 40
+        ref = refbind.orc_solve(A.astype(np.float64), Y[:, b:b + 1].astype(np.float64), cfg,
+                                mode=refbind.MODE_PER_SIGNAL)
+        assert np.array_equal(np.flatnonzero(r.mask[:, 0]), np.flatnonzero(ref["mask"][:, 0]))
+        assert rel_coef_err(r.s[:, 0], ref["s"][:, 0]) <= COEF_RTOL
