@@ -317,7 +317,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   const int W = ctx->world > 1 ? ctx->world : ctx->vshards;
   const bool colshard = W > 1;
   if (colshard) {
-    const int64_t tile = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
+    const int64_t tile = tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
     if (ctx->sep || c->th < 1.0 || mode != CL_MODE_PER_SIGNAL)
       return fail(ctx, CL_ERR_UNSUPPORTED,
                   "column sharding: per-signal mode with th = 1 on 1D dictionaries only");
@@ -337,7 +337,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                      (mode == CL_MODE_PER_SIGNAL || B == 1) &&
                      cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
                      B <= 4 * (int64_t)ctx->sms;
-  const int64_t tile_atoms = tensor ? corr_tc_tile_atoms() : kCorrTileAtoms;
+  const int64_t tile_atoms =
+      tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
   int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile);
   if (st) return st;
@@ -505,7 +506,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     return CL_OK;
   }
   if (ctx->profiling) {
-    // Per-phase CUDA-event timing: one iteration at a time, synchronised.
+    // Per-phase CUDA-event timing (outside the graph path).
     cudaEvent_t ev[5];
     for (auto& e : ev) cudaEventCreate(&e);
     cudaEventRecord(ev[0], s);
@@ -519,36 +520,50 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         if (ctx->h_counters[kActiveCount] == 0) break;
         continue;
       }
-      cudaEventRecord(ev[1], s);
-      if (tensor)
-        launch_corr_tc(p, w, s);
-      else if (gemv)
-        launch_corr_gemv(p, w, full_scores, s);
-      else
-        launch_corr_f64(p, w, full_scores, s);
-      cudaEventRecord(ev[4], s);
-      if (!p.fuse_select) launch_select(p, w, full_scores, s);
-      cudaEventRecord(ev[2], s);
-      launch_learn(p, w, outer, c->th >= 1.0 ? outer : (int)cap, s);
-      launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
-      if (mode == CL_MODE_JOINT) {
-        launch_joint_control(p, w, outer, false, s);
-        launch_joint_snapshot(p, w, s);
-        launches += 2;
+      // 1D: events around every phase, the stream synchronised once per
+      // chunk of kChunkIters iterations (the active count is checked there),
+      // so the kernels run back to back as in the timed graph path.
+      const int o1 = std::min(p.max_outer, outer + kChunkIters - 1);
+      std::vector<cudaEvent_t> pe((size_t)(4 * (o1 - outer + 1)));
+      for (auto& e : pe) cudaEventCreate(&e);
+      for (int o = outer; o <= o1; ++o) {
+        cudaEvent_t* e = &pe[(size_t)(4 * (o - outer))];
+        cudaEventRecord(e[0], s);
+        if (tensor)
+          launch_corr_tc(p, w, s);
+        else if (gemv)
+          launch_corr_gemv(p, w, full_scores, s);
+        else
+          launch_corr_f64(p, w, full_scores, s);
+        cudaEventRecord(e[1], s);
+        if (!p.fuse_select) launch_select(p, w, full_scores, s);
+        cudaEventRecord(e[2], s);
+        launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
+        launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
+        if (mode == CL_MODE_JOINT) {
+          launch_joint_control(p, w, o, false, s);
+          launch_joint_snapshot(p, w, s);
+          launches += 2;
+        }
+        cudaEventRecord(e[3], s);
       }
-      cudaEventRecord(ev[3], s);
       CL_CUDA(ctx, cudaGetLastError());
       CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
                                    cudaMemcpyDeviceToHost, s));
       CL_CUDA(ctx, cudaStreamSynchronize(s));
-      float a = 0.f, b2 = 0.f, c2 = 0.f;
-      cudaEventElapsedTime(&a, ev[1], ev[4]);
-      cudaEventElapsedTime(&c2, ev[4], ev[2]);
-      cudaEventElapsedTime(&b2, ev[2], ev[3]);
-      stats.corr_ms += a;
-      stats.select_ms += c2;
-      stats.learn_ms += b2;
-      outer_done = outer;
+      for (int o = outer; o <= o1; ++o) {
+        cudaEvent_t* e = &pe[(size_t)(4 * (o - outer))];
+        float a = 0.f, b2 = 0.f, c2 = 0.f;
+        cudaEventElapsedTime(&a, e[0], e[1]);
+        cudaEventElapsedTime(&c2, e[1], e[2]);
+        cudaEventElapsedTime(&b2, e[2], e[3]);
+        stats.corr_ms += a;
+        stats.select_ms += c2;
+        stats.learn_ms += b2;
+      }
+      for (auto& e : pe) cudaEventDestroy(e);
+      outer_done = o1;
+      outer = o1;
       if (ctx->h_counters[kActiveCount] == 0) break;
     }
     launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
@@ -1255,8 +1270,8 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
     return fail(ctx, CL_ERR_UNSUPPORTED, "GEMV correlation: 1 <= batch <= 4");
   const int64_t m = ctx->m, n = ctx->n, ldm = ctx->ldm;
   const bool tc = path == 2;
-  const int64_t ntile = tc ? (n + corr_tc_tile_atoms() - 1) / corr_tc_tile_atoms()
-                           : (n + kCorrTileAtoms - 1) / kCorrTileAtoms;
+  const int64_t tile = tc ? corr_tc_tile_atoms() : path == 3 ? corr_gemv_tile_atoms() : kCorrTileAtoms;
+  const int64_t ntile = (n + tile - 1) / tile;
   int st = ensure_workspace(ctx, batch, 1, true, true, ntile);
   if (st) return st;
   SolveParams p{};

@@ -209,6 +209,7 @@ void launch_corr_f64(const SolveParams& p, const Work& w, bool full_scores,
 // K1b (k_corr_gemv.cu): HBM-bound fp64-accumulating GEMV for B <= 8 residuals,
 // the same candidate records (and optional |scores|) as launch_corr_f64.
 bool corr_gemv_supported(int64_t ldm, int64_t B);
+int64_t corr_gemv_tile_atoms();
 void launch_corr_gemv(const SolveParams& p, const Work& w, bool full_scores,
                       cudaStream_t s);
 // tcgen05 3xTF32 correlation with fused top-2 epilogue (th == 1).

@@ -16,6 +16,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--events", action="store_true", help="profiling mode: plain launches, no graphs")
 a = ap.parse_args()
 c = dict(cl.CONFIGS[a.config])
 B = a.batch or c["batch"]
@@ -24,6 +25,8 @@ A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], B,
 ctx = cl.ClompContext(A)
 if a.path:
     ctx.set_corr_path(a.path)
+if a.events:
+    ctx.set_profiling(True)
 cfg = cl.ClompConfig.baseline(c["k"])
 for _ in range(1 + a.reps):
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
