@@ -205,6 +205,10 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode);
  * semantics) run the whole solve in one persistent block per signal; 0
  * forces the batched kernel pipeline instead (tests compare the two). */
 int cl_set_fused(cl_ctx* ctx, int on);
+/* Supports of 33..256 atoms learn on CTA clusters with the support Gram
+ * matrix in registers (default 1); 0 keeps them on the block-per-signal
+ * kernel (tests compare the two). */
+int cl_set_cluster_learn(cl_ctx* ctx, int on);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);
 /* Run this context's work on a caller-owned cudaStream_t (NULL restores the

@@ -147,7 +147,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
     "cl_gen_problem_2d",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
@@ -182,6 +182,7 @@ def lib() -> C.CDLL:
         h.cl_debug_scores.argtypes = [vp, vp, i64, i32, vp]
         h.cl_set_gram_cache.argtypes = [vp, i32]
         h.cl_set_fused.argtypes = [vp, i32]
+        h.cl_set_cluster_learn.argtypes = [vp, i32]
         h.cl_nccl_unique_id.argtypes = [vp]
         h.cl_create_colshard.restype = vp
         h.cl_create_colshard.argtypes = [i32, vp, i64, i64, i32, i32, i32, vp, C.POINTER(C.c_int)]
@@ -374,6 +375,11 @@ class ClompContext:
     def set_fused(self, on: bool):
         """Allow (default) or forbid the one-block-per-signal latency path."""
         _raise(lib().cl_set_fused(self._h, int(bool(on))), self._h)
+
+    def set_cluster_learn(self, on: bool):
+        """Learn supports of 33..256 atoms on CTA clusters with register-resident
+        Gram blocks (default) or on the block-per-signal kernel."""
+        _raise(lib().cl_set_cluster_learn(self._h, int(bool(on))), self._h)
 
     def set_profiling(self, on: bool):
         _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)

@@ -102,6 +102,7 @@ struct cl_ctx {
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool fused_ok = true;  // small problems: one persistent block per signal
+  bool cluster_learn = true;  // supports of 33..256 atoms on CTA clusters
   // column sharding (cl_create_colshard); vshards emulates W shards on one GPU
   int rank = 0, world = 1, vshards = 1;
   void* comm = nullptr;
@@ -393,6 +394,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // th == 1: the selection (K1c, near-tie rescoring included) runs at the top
   // of the learning kernel, one warp per signal, instead of its own launch.
   p.fuse_select = (!full_scores && !p.sep) ? 1 : 0;
+  p.cluster_learn = ctx->cluster_learn ? 1 : 0;
   p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
 
   const Work& w = ctx->w;
@@ -1008,6 +1010,12 @@ int cl_set_virtual_shards(cl_ctx* ctx, int shards) {
 int cl_set_fused(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
   ctx->fused_ok = on != 0;
+  return CL_OK;
+}
+
+int cl_set_cluster_learn(cl_ctx* ctx, int on) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  ctx->cluster_learn = on != 0;
   return CL_OK;
 }
 

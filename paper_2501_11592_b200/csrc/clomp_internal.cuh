@@ -108,6 +108,9 @@ struct SolveParams {
   // recomputes the row it needs (tensor path, th == 1, ldm <= 512)
   int32_t lazy_r64;
   double a_inv_scale;       // 1 / (power-of-two scale of the fp16 dictionary split)
+  // supports of 33..256 atoms learn on CTA clusters with register-resident
+  // Gram blocks (k_learn_cluster); 0 keeps them on k_learn_block (tests)
+  int32_t cluster_learn;
 };
 
 struct Work {

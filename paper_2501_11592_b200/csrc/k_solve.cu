@@ -14,8 +14,10 @@
 // A_S^T (A_S c - y) = G c - b, G = A_S^T A_S, b = A_S^T y, both accumulated in
 // fp64 from the fp32 atoms.  This is the reference gradient in exact
 // arithmetic; it costs t^2 per epoch instead of the reference's dense 2*m*n.
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
@@ -1381,7 +1383,7 @@ constexpr int kBlockRows = 8;
 
 template <int OPT, bool SMEM_G>
 __global__ void __launch_bounds__(kBlockThreads)
-k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
+k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int skip_le) {
   extern __shared__ __align__(16) unsigned char dsm[];
   double* cs = reinterpret_cast<double*>(dsm);                 // [cap]
   int32_t* sups = reinterpret_cast<int32_t*>(cs + p.cap);      // [cap]
@@ -1399,6 +1401,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
   for (int li = blockIdx.x; li < count; li += gridDim.x) {
     const int64_t b = big_list[li];
     const int t = w.cnt[b];
+    if (t <= skip_le) continue;  // learned by k_learn_cluster this iteration
     const int t0 = w.gcnt[b];
     double* G = w.gram + b * cap * cap;
     const double* y = w.y64 + b * p.ldm;
@@ -1556,6 +1559,221 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list) {
     if (snap_s)
       for (int i = tid; i < t; i += kBlockThreads) w.best_coef[b * cap + i] = cs[i];
     __syncthreads();
+  }
+}
+
+// ------------------------------------- learning, CTA cluster per signal
+// Supports of 33..256 atoms (config 3 and the one-signal path): the support
+// Gram matrix lives in REGISTERS, spread over a cluster of Q CTAs (Q = 1, 2, 4
+// for t <= 64, 128, 256).  CTA q, warp w owns rows [64q + 8w, 64q + 8w + 8),
+// lane l owns columns [8l, 8l + 8): an 8 x 8 fp64 block per thread, loaded
+// once per outer iteration.  An epoch is then 64 register FMAs per thread on
+// the 8 coefficients of its columns (read from a shared-memory copy of c that
+// every CTA of the cluster holds), a transposed butterfly across the warp that
+// leaves each row's G c in lane 4i, the optimizer step of that row
+// (gradient_step, clomp.cpp:171-209, g = 2 (G c - b)) and a store of the new
+// coefficient into the next c buffer of every CTA of the cluster (distributed
+// shared memory), closed by one cluster barrier.  The FMAs run from registers
+// at the fp64 pipe's rate instead of 8 bytes of shared memory or L2 per FMA
+// (k_learn_block), the rest of the outer iteration (Gram extension, residual,
+// loss, stopping rules, snapshot) is split over the whole cluster.
+constexpr int kClThreads = 256;
+
+__device__ __forceinline__ double warp_reduce8_t(double (&v)[8], int lane) {
+#pragma unroll
+  for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  double x = v[0];
+  x += __shfl_xor_sync(kFull, x, 2);
+  x += __shfl_xor_sync(kFull, x, 1);
+  return x;  // lanes 4i..4i+3: row i of the warp's 8 rows
+}
+
+template <int Q>
+__device__ __forceinline__ void cl_sync() {
+  if (Q > 1)
+    cooperative_groups::this_cluster().sync();
+  else
+    __syncthreads();
+}
+
+template <int Q, class T>
+__device__ __forceinline__ T* cl_map(T* ptr, int rank) {
+  if (Q > 1) return cooperative_groups::this_cluster().map_shared_rank(ptr, rank);
+  return ptr;
+}
+
+template <int Q, int OPT>
+__global__ void __launch_bounds__(kClThreads, 1)
+k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
+  __shared__ __align__(16) double cbuf[2][256];
+  __shared__ int32_t sups[256];
+  __shared__ double red[kClThreads / 32];
+  __shared__ double lpart[4];  // rank 0: per-CTA loss partials
+  __shared__ double s_L;
+  __shared__ int s_snap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kClThreads / 32;
+  const int q = Q > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int gt = q * kClThreads + tid;  // thread index within the cluster
+  constexpr int GS = Q * kClThreads;    // cluster size in threads
+  pdl_wait();
+  pdl_trigger();
+  const int count = w.counters[kBigCount + (outer & 1)];
+  const int64_t cap = p.cap;
+  const int R0 = 64 * q + 8 * warp, C0 = 8 * lane;
+  const int my_row = R0 + (lane >> 2);
+  for (int li = blockIdx.y; li < count; li += gridDim.y) {
+    const int64_t b = big_list[li];
+    const int t = w.cnt[b];
+    if (t > 64 * Q) continue;  // uniform over the cluster: left to k_learn_block
+    const int t0 = w.gcnt[b];
+    double* G = w.gram + b * cap * cap;
+    const float* y = w.y32 + b * p.ldm;
+    for (int k = tid; k < t; k += kClThreads) sups[k] = w.sup[b * cap + k];
+    __syncthreads();
+    // Gram extension for the atoms injected this iteration, over the cluster.
+    for (int k = t0; k < t; ++k) {
+      if (w.gfull) {
+        for (int i = gt; i <= k; i += GS) {
+          const double v = w.gfull[(int64_t)sups[k] * p.n + sups[i]];
+          G[(int64_t)k * cap + i] = v;
+          G[(int64_t)i * cap + k] = v;
+        }
+      } else {
+        const float* ak = w.at32 + (int64_t)sups[k] * p.ldm;
+        for (int i = q * nw + warp; i <= k; i += Q * nw) {
+          const float* ai = w.at32 + (int64_t)sups[i] * p.ldm;
+          double acc = 0.0;
+          for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(ai[m]), acc);
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            G[(int64_t)k * cap + i] = acc;
+            G[(int64_t)i * cap + k] = acc;
+          }
+        }
+      }
+      if (q == Q - 1 && warp == nw - 1) {
+        const float* ak = w.at32 + (int64_t)sups[k] * p.ldm;
+        double acc = 0.0;
+        for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(y[m]), acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          w.bvec[b * cap + k] = acc;
+          w.coef[b * cap + k] = 0.0;
+          w.mom1[b * cap + k] = 0.0;
+          w.mom2[b * cap + k] = 0.0;
+        }
+      }
+    }
+    for (int k = tid; k < 256; k += kClThreads) {
+      cbuf[1][k] = 0.0;  // padding rows stay exactly zero
+      cbuf[0][k] = 0.0;
+    }
+    __threadfence();
+    cl_sync<Q>();  // G, b, fresh coefficients visible to the whole cluster
+    if (q == 0 && tid == 0) w.gcnt[b] = t;
+    double g[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        g[i][j] = (R0 + i < t && C0 + j < t) ? G[(int64_t)(R0 + i) * cap + C0 + j] : 0.0;
+    for (int k = tid; k < t; k += kClThreads) cbuf[0][k] = w.coef[b * cap + k];
+    const bool owner = (lane & 3) == 0 && my_row < t;
+    double cr = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
+    if (my_row < t) {
+      cr = w.coef[b * cap + my_row];
+      bi = w.bvec[b * cap + my_row];
+      m1 = w.mom1[b * cap + my_row];
+      m2 = w.mom2[b * cap + my_row];
+    }
+    double* dst[Q];
+#pragma unroll
+    for (int r = 0; r < Q; ++r) dst[r] = cl_map<Q>(&cbuf[0][0], r);
+    __syncthreads();
+    const int step0 = (outer - 1) * p.inner;
+    int cur = 0;
+    for (int e = 0; e < p.inner; ++e) {
+      double cv[8];
+      const double2* cp2 = reinterpret_cast<const double2*>(&cbuf[cur][C0]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 x = cp2[j];
+        cv[2 * j] = x.x;
+        cv[2 * j + 1] = x.y;
+      }
+      double acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a = fma(g[i][j], cv[j], a);
+        acc[i] = a;
+      }
+      const double gc = warp_reduce8_t(acc, lane);
+      if (owner) {
+        double bc1 = 1.0, bc2 = 1.0;
+        if (OPT == 2) {
+          bc1 = p.bc1[step0 + e];
+          bc2 = p.bc2[step0 + e];
+        }
+        opt_step<OPT>(cr, 2.0 * (gc - bi), m1, m2, p.lr, bc1, bc2);
+#pragma unroll
+        for (int r = 0; r < Q; ++r) dst[r][(cur ^ 1) * 256 + my_row] = cr;
+      }
+      cl_sync<Q>();
+      cur ^= 1;
+    }
+    if (owner) {
+      w.coef[b * cap + my_row] = cr;
+      w.mom1[b * cap + my_row] = m1;
+      w.mom2[b * cap + my_row] = m2;
+    }
+    // Residual r = A_S c - y (fp64, rows over the cluster) and its loss.
+    const double* cs = cbuf[cur];
+    double lacc = 0.0;
+    for (int64_t i = gt; i < p.ldm; i += GS) {
+      double acc = 0.0;
+      for (int k = 0; k < t; ++k) acc = fma(f2d(w.at32[(int64_t)sups[k] * p.ldm + i]), cs[k], acc);
+      const double rv = acc - f2d(y[i]);
+      w.r64[b * p.ldm + i] = rv;
+      lacc = fma(rv, rv, lacc);
+    }
+    lacc = warp_sum(lacc);
+    if (lane == 0) red[warp] = lacc;
+    __syncthreads();
+    if (tid == 0) {
+      double L = 0.0;
+      for (int k = 0; k < nw; ++k) L += red[k];
+      cl_map<Q>(lpart, 0)[q] = L;
+    }
+    cl_sync<Q>();
+    if (q == 0 && tid == 0) {
+      double L = 0.0;
+      for (int r = 0; r < Q; ++r) L += lpart[r];
+      int snap = 0;
+      if (p.mode == kModePerSignal)
+        snap = control_signal(p, w, b, outer, L);
+      else
+        w.loss[b] = L;
+      for (int r = 0; r < Q; ++r) {
+        *cl_map<Q>(&s_L, r) = L;
+        *cl_map<Q>(&s_snap, r) = snap;
+      }
+    }
+    cl_sync<Q>();
+    if (w.r_hi) split_row(w, b, p.ldm, s_L, gt, GS);  // rows this thread wrote
+    if (s_snap)
+      for (int k = gt; k < t; k += GS) w.best_coef[b * cap + k] = cs[k];
+    cl_sync<Q>();  // smem (sups, cbuf, lpart) free for the next signal
   }
 }
 
@@ -1891,20 +2109,66 @@ static size_t block_smem_bytes(int64_t cap, bool smem_g) {
 
 template <int OPT>
 static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
-                                 int32_t* big_list, int grid, cudaStream_t s) {
+                                 int32_t* big_list, int grid, int skip_le, cudaStream_t s) {
   const size_t smem_g = block_smem_bytes(p.cap, true);
   if (smem_g <= 200 * 1024) {
     cudaFuncSetAttribute(k_learn_block<OPT, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g);
     launch_pdl(k_learn_block<OPT, true>, dim3(grid), dim3(kBlockThreads), smem_g, s, p, w,
-               outer, (const int32_t*)big_list);
+               outer, (const int32_t*)big_list, skip_le);
   } else {
     const size_t sm = block_smem_bytes(p.cap, false);
     cudaFuncSetAttribute(k_learn_block<OPT, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k_learn_block<OPT, false>, dim3(grid), dim3(kBlockThreads), sm, s, p, w, outer,
-               (const int32_t*)big_list);
+               (const int32_t*)big_list, skip_le);
   }
+}
+
+template <int Q>
+static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int32_t* big_list,
+                             int nclusters, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(Q, (unsigned)nclusters);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (Q > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = Q;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const int32_t* bl = big_list;
+  switch (p.opt) {
+    case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 0>, p, w, outer, bl); break;
+    case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 1>, p, w, outer, bl); break;
+    default: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 2>, p, w, outer, bl); break;
+  }
+}
+
+// Cluster learning for supports of 33..256 atoms: returns the support size
+// up to which it learns this iteration (0 when not launched).
+static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
+                                int64_t nsig, int sms, cudaStream_t s) {
+  if (p.sep || max_cnt <= kWarpCap || p.cluster_learn == 0) return 0;
+  const int Q = max_cnt <= 64 ? 1 : max_cnt <= 128 ? 2 : 4;
+  const int nclusters = (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / Q));
+  if (Q == 1)
+    launch_cluster_q<1>(p, w, outer, w.big_list, nclusters, s);
+  else if (Q == 2)
+    launch_cluster_q<2>(p, w, outer, w.big_list, nclusters, s);
+  else
+    launch_cluster_q<4>(p, w, outer, w.big_list, nclusters, s);
+  return 64 * Q;
 }
 
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
@@ -1946,10 +2210,11 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(nsig < 2 * sms ? nsig : 2 * sms);
+    const int skip_le = launch_cluster_learn(p, w, outer, max_cnt, nsig, sms, s);
     switch (p.opt) {
-      case 0: launch_block_variant<0>(p, w, outer, big_list, grid, s); break;
-      case 1: launch_block_variant<1>(p, w, outer, big_list, grid, s); break;
-      default: launch_block_variant<2>(p, w, outer, big_list, grid, s); break;
+      case 0: launch_block_variant<0>(p, w, outer, big_list, grid, skip_le, s); break;
+      case 1: launch_block_variant<1>(p, w, outer, big_list, grid, skip_le, s); break;
+      default: launch_block_variant<2>(p, w, outer, big_list, grid, skip_le, s); break;
     }
   }
 }

@@ -243,3 +243,26 @@ def test_config3_shape_one_signal_gemv_prefix(gpu_available):
                                 mode=refbind.MODE_PER_SIGNAL)
         assert np.array_equal(np.flatnonzero(r.mask[:, 0]), np.flatnonzero(ref["mask"][:, 0]))
         assert rel_coef_err(r.s[:, 0], ref["s"][:, 0]) <= COEF_RTOL
+
+
+@pytest.mark.parametrize("K,opt", [(60, cl.PLAIN), (120, cl.PLAIN), (200, cl.PLAIN),
+                                   (70, cl.MOMENTUM), (70, cl.ADAM)])
+def test_cluster_learning_vs_oracle_and_block_kernel(gpu_available, K, opt):
+    """Supports of 33..256 atoms learn on CTA clusters (Q = 1, 2, 4 CTAs for
+    t <= 64, 128, 256) with register-resident Gram blocks; the result matches
+    the oracle and the block-per-signal kernel."""
+    m, n, B = 1024, 2048, 3
+    A, X, Y, _ = cl.gen_problem_1d(30 + K, m, n, K, B, value_law=1)
+    cfg = cl.ClompConfig.baseline(K)
+    cfg.opt = opt
+    if opt == cl.ADAM:
+        cfg.lr = 0.01
+    ctx = make_ctx(A, "tc")
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.all(r.status == 0)
+    _subset_parity(A, Y, cfg, np.arange(min(B, 2)), r, X if opt == cl.PLAIN else None)
+    ctx.set_cluster_learn(False)
+    r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.array_equal(r.mask, r0.mask)
+    assert np.array_equal(r.iterations, r0.iterations)
+    assert rel_coef_err(r.s, r0.s) <= 1e-9
