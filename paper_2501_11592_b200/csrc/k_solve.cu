@@ -1610,10 +1610,90 @@ __device__ __forceinline__ T* cl_map(T* ptr, int rank) {
   return ptr;
 }
 
+__device__ __forceinline__ uint32_t cl_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared::cluster address of the same variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cl_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra W_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Residual rows r_i = sum_k a_{S_k, i} c_k - y_i (sequential k, fp64) for
+// rows i = i0, i0 + stride, ...: RPT rows and 8 atoms per step, so 8 RPT
+// independent gathers are in flight per thread instead of one.
+template <int RPT>
+__device__ __forceinline__ double resid_rows(const SolveParams& p, const Work& w, int64_t b,
+                                             const int32_t* sups, const double* cs, int t,
+                                             int64_t i0, int64_t stride) {
+  const float* y = w.y32 + b * p.ldm;
+  double lacc = 0.0;
+  for (int64_t ib = i0; ib < p.ldm; ib += RPT * stride) {
+    double acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u] = 0.0;
+    int k = 0;
+    for (; k + 8 <= t; k += 8) {
+      float v[8][RPT];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const float* ap = w.at32 + (int64_t)sups[k + z] * p.ldm;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int64_t i = ib + u * stride;
+          v[z][u] = i < p.ldm ? ap[i] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int z = 0; z < 8; ++z)
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) acc[u] = fma(f2d(v[z][u]), cs[k + z], acc[u]);
+    }
+    for (; k < t; ++k) {
+      const float* ap = w.at32 + (int64_t)sups[k] * p.ldm;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t i = ib + u * stride;
+        if (i < p.ldm) acc[u] = fma(f2d(ap[i]), cs[k], acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t i = ib + u * stride;
+      if (i < p.ldm) {
+        const double rv = acc[u] - f2d(y[i]);
+        w.r64[b * p.ldm + i] = rv;
+        lacc = fma(rv, rv, lacc);
+      }
+    }
+  }
+  return lacc;
+}
+
+// Row blocks of 8 are dealt round-robin over the cluster (block rb -> CTA
+// rb % Q, warp rb / Q), so every CTA owns rows whenever t > 8 (Q - 1): each
+// CTA then has a warp that waits on every exchange phase, which keeps the
+// phases of its barriers in order (see the epoch loop).
 template <int Q, int OPT>
 __global__ void __launch_bounds__(kClThreads, 1)
 k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   __shared__ __align__(16) double cbuf[2][256];
+  __shared__ __align__(8) uint64_t fullb[2];  // c buffer b complete (t * 8 bytes)
+  __shared__ uint32_t s_phase[2];            // phases of fullb[] completed so far
   __shared__ int32_t sups[256];
   __shared__ double red[kClThreads / 32];
   __shared__ double lpart[4];  // rank 0: per-CTA loss partials
@@ -1624,12 +1704,27 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   const int q = Q > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
   const int gt = q * kClThreads + tid;  // thread index within the cluster
   constexpr int GS = Q * kClThreads;    // cluster size in threads
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cl_smem_u32(&fullb[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cl_smem_u32(&fullb[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_phase[0] = s_phase[1] = 0;
+  }
   pdl_wait();
   pdl_trigger();
   const int count = w.counters[kBigCount + (outer & 1)];
   const int64_t cap = p.cap;
-  const int R0 = 64 * q + 8 * warp, C0 = 8 * lane;
+  const int R0 = 8 * (warp * Q + q), C0 = 8 * lane;
   const int my_row = R0 + (lane >> 2);
+  // remote addresses: c buffers and their barriers in every CTA of the cluster
+  uint32_t dst_c[Q], dst_b0[Q], dst_b1[Q];
+#pragma unroll
+  for (int r = 0; r < Q; ++r) {
+    dst_c[r] = cl_mapa(cl_smem_u32(&cbuf[0][0]), r);
+    dst_b0[r] = cl_mapa(cl_smem_u32(&fullb[0]), r);
+    dst_b1[r] = cl_mapa(cl_smem_u32(&fullb[1]), r);
+  }
+  cl_sync<Q>();  // barriers initialised cluster-wide before any exchange
   for (int li = blockIdx.y; li < count; li += gridDim.y) {
     const int64_t b = big_list[li];
     const int t = w.cnt[b];
@@ -1687,6 +1782,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       for (int j = 0; j < 8; ++j)
         g[i][j] = (R0 + i < t && C0 + j < t) ? G[(int64_t)(R0 + i) * cap + C0 + j] : 0.0;
     for (int k = tid; k < t; k += kClThreads) cbuf[0][k] = w.coef[b * cap + k];
+    const bool producing = R0 < t;
     const bool owner = (lane & 3) == 0 && my_row < t;
     double cr = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
     if (my_row < t) {
@@ -1695,42 +1791,73 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       m1 = w.mom1[b * cap + my_row];
       m2 = w.mom2[b * cap + my_row];
     }
-    double* dst[Q];
-#pragma unroll
-    for (int r = 0; r < Q; ++r) dst[r] = cl_map<Q>(&cbuf[0][0], r);
+    uint32_t pc0 = s_phase[0], pc1 = s_phase[1];
     __syncthreads();
     const int step0 = (outer - 1) * p.inner;
-    int cur = 0;
-    for (int e = 0; e < p.inner; ++e) {
-      double cv[8];
-      const double2* cp2 = reinterpret_cast<const double2*>(&cbuf[cur][C0]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double2 x = cp2[j];
-        cv[2 * j] = x.x;
-        cv[2 * j + 1] = x.y;
-      }
-      double acc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double a = 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a = fma(g[i][j], cv[j], a);
-        acc[i] = a;
-      }
-      const double gc = warp_reduce8_t(acc, lane);
-      if (owner) {
-        double bc1 = 1.0, bc2 = 1.0;
-        if (OPT == 2) {
-          bc1 = p.bc1[step0 + e];
-          bc2 = p.bc2[step0 + e];
+    const int E = p.inner;
+    // Epoch e reads buffer e & 1 and sends its rows' new coefficients into
+    // buffer (e + 1) & 1 of every CTA (st.async, completing t * 8 bytes on
+    // that CTA's barrier).  A sender has received every row of epoch e's
+    // input, produced by warps that had themselves waited for the phase of
+    // the buffer being overwritten, so a phase never receives bytes early.
+    if (producing) {
+      for (int e = 0; e < E; ++e) {
+        const int cur = e & 1, nxt = cur ^ 1;
+        if (e > 0) {
+          if (cur) {
+            cl_mbar_wait(cl_smem_u32(&fullb[1]), pc1 & 1);
+            ++pc1;
+          } else {
+            cl_mbar_wait(cl_smem_u32(&fullb[0]), pc0 & 1);
+            ++pc0;
+          }
         }
-        opt_step<OPT>(cr, 2.0 * (gc - bi), m1, m2, p.lr, bc1, bc2);
+        if (tid == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           cl_smem_u32(&fullb[nxt])),
+                       "r"((uint32_t)(t * 8))
+                       : "memory");
+        double cv[8];
+        const double2* cp2 = reinterpret_cast<const double2*>(&cbuf[cur][C0]);
 #pragma unroll
-        for (int r = 0; r < Q; ++r) dst[r][(cur ^ 1) * 256 + my_row] = cr;
+        for (int j = 0; j < 4; ++j) {
+          const double2 x = cp2[j];
+          cv[2 * j] = x.x;
+          cv[2 * j + 1] = x.y;
+        }
+        double acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          double a = 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a = fma(g[i][j], cv[j], a);
+          acc[i] = a;
+        }
+        const double gc = warp_reduce8_t(acc, lane);
+        if (owner) {
+          double bc1 = 1.0, bc2 = 1.0;
+          if (OPT == 2) {
+            bc1 = p.bc1[step0 + e];
+            bc2 = p.bc2[step0 + e];
+          }
+          opt_step<OPT>(cr, 2.0 * (gc - bi), m1, m2, p.lr, bc1, bc2);
+          const uint32_t off = (uint32_t)((nxt * 256 + my_row) * 8);
+#pragma unroll
+          for (int r = 0; r < Q; ++r)
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                    dst_c[r] + off),
+                "d"(cr), "r"(nxt ? dst_b1[r] : dst_b0[r])
+                : "memory");
+        }
       }
-      cl_sync<Q>();
-      cur ^= 1;
+      const int fin = E & 1;
+      cl_mbar_wait(cl_smem_u32(&fullb[fin]), (fin ? pc1 : pc0) & 1);
+    }
+    cl_sync<Q>();  // the final coefficients are in every CTA's buffer E & 1
+    if (tid == 0) {
+      s_phase[1] += (uint32_t)((E + 1) / 2);
+      s_phase[0] += (uint32_t)(E / 2);
     }
     if (owner) {
       w.coef[b * cap + my_row] = cr;
@@ -1738,22 +1865,15 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       w.mom2[b * cap + my_row] = m2;
     }
     // Residual r = A_S c - y (fp64, rows over the cluster) and its loss.
-    const double* cs = cbuf[cur];
-    double lacc = 0.0;
-    for (int64_t i = gt; i < p.ldm; i += GS) {
-      double acc = 0.0;
-      for (int k = 0; k < t; ++k) acc = fma(f2d(w.at32[(int64_t)sups[k] * p.ldm + i]), cs[k], acc);
-      const double rv = acc - f2d(y[i]);
-      w.r64[b * p.ldm + i] = rv;
-      lacc = fma(rv, rv, lacc);
-    }
+    const double* cs = cbuf[E & 1];
+    double lacc = resid_rows<4>(p, w, b, sups, cs, t, gt, GS);
     lacc = warp_sum(lacc);
     if (lane == 0) red[warp] = lacc;
     __syncthreads();
     if (tid == 0) {
       double L = 0.0;
       for (int k = 0; k < nw; ++k) L += red[k];
-      cl_map<Q>(lpart, 0)[q] = L;
+      *cl_map<Q>(&lpart[q], 0) = L;
     }
     cl_sync<Q>();
     if (q == 0 && tid == 0) {
@@ -2138,13 +2258,12 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
-  if (Q > 1) {
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = Q;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
+  // explicit cluster launch even for Q = 1: st.async / mapa need one
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = Q;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
   cfg.attrs = at;
   cfg.numAttrs = na;
   const int32_t* bl = big_list;
