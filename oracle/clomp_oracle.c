@@ -7,7 +7,9 @@
  * What it restates, with the reference lines it follows:
  *   validate                 clomp.cpp:18-30
  *   inject_from_scores       clomp.cpp:41-53   (select_support twin, solvers.cpp:68-80)
- *   loss_impl (priors off)   clomp.cpp:74-91, 120-127
+ *   loss_impl                clomp.cpp:74-127 (priors: TV-1D on single-column
+ *                            solves, the only prior a column of clomp_solve sees)
+ *   tv_1d                    priors.cpp:11-26
  *   resolve_weights          clomp.cpp:131-140
  *   gradient_step            clomp.cpp:171-209
  *   clomp_solve_batch        clomp.cpp:211-292
@@ -154,6 +156,12 @@ typedef struct {
   const double* ar;  /* m_r x n_r */
   const double* ac;  /* m_c x n_c */
   int64_t mr, nr, mc, nc;
+  /* Priors (single-column solves): synthesis basis D (n x n row-major,
+   * x = D s), its transpose (LossOps::dt, clomp.cpp:63-65) and the resolved
+   * TV weight (0 = prior branch skipped, clomp.cpp:94). */
+  const double* basis;
+  const double* dt;
+  double w_tv;
 } problem_t;
 
 static inline double entry(const problem_t* p, int64_t q, int64_t j) {
@@ -177,6 +185,58 @@ static void residual(const problem_t* p, const double* s, const support_t* sup,
       r[i * B + b] = acc - y[i * B + b];
     }
   }
+}
+
+/* x = basis * s_eff (clomp.cpp:95) for a single column, support-restricted
+ * like residual() (exact zeros add nothing to the sequential sums). */
+static void synth(const problem_t* p, const double* s, const support_t* sup, double* x) {
+  const int64_t n = p->n;
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int64_t q = 0; q < sup[0].count; ++q) {
+      const int64_t j = sup[0].idx[q];
+      acc = mac(acc, p->basis[i * n + j], s[j], p->isa);
+    }
+    x[i] = acc;
+  }
+}
+
+/* tv_1d (priors.cpp:11-26): mean squared forward difference and its gradient. */
+static double tv_1d(const double* x, int64_t n, double* grad) {
+  if (grad)
+    for (int64_t i = 0; i < n; ++i) grad[i] = 0.0;
+  if (n < 2) return 0.0;
+  const double inv_n = 1.0 / (double)n;
+  double acc = 0.0;
+  for (int64_t j = 0; j + 1 < n; ++j) {
+    const double d = x[j] - x[j + 1];
+    acc += d * d;
+    if (grad) {
+      grad[j] += 2.0 * inv_n * d;
+      grad[j + 1] -= 2.0 * inv_n * d;
+    }
+  }
+  return acc * inv_n;
+}
+
+/* The TV-1D part of loss_impl (clomp.cpp:93-119) for a single column: returns
+ * tv; with g != NULL adds the chained gradient D^T (w_tv * dtv/dx) to g on the
+ * support (clomp.cpp:100-102, 114-117).  x, gv, gx: n-entry scratch. */
+static double prior_tv(const problem_t* p, const double* s, const support_t* sup, double* g,
+                       double* x, double* gv, double* gx) {
+  const int64_t n = p->n;
+  synth(p, s, sup, x);
+  const double tv = tv_1d(x, n, g ? gv : NULL);
+  if (g) {
+    for (int64_t i = 0; i < n; ++i) gx[i] = 0.0 + p->w_tv * gv[i];
+    for (int64_t q = 0; q < sup[0].count; ++q) {
+      const int64_t j = sup[0].idx[q];
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc = mac(acc, p->dt[j * n + i], gx[i], p->isa);
+      g[j] += acc;
+    }
+  }
+  return tv;
 }
 
 /* (A^T r)[j, b] for one atom j: la::matmul(ops.at, r) element (clomp.cpp:89, 245). */
@@ -304,6 +364,8 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
     sup[b].idx = sup_mem + b * n;
     best_sup[b].idx = sup_mem + nb + b * n;
   }
+  const int prior = p->w_tv > 0.0;  /* single-column solves only (solve_driver) */
+  double* px = prior ? calloc((size_t)(3 * n), sizeof(double)) : NULL;
   uint64_t adam_steps = 0;
   double best_loss = INFINITY, prev_loss = INFINITY;
   uint64_t stall = 0;
@@ -329,10 +391,13 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
           const int64_t j = sup[b].idx[q];
           g[j * B + b] = corr(p, r, j, b) * 2.0;
         }
+      if (prior) prior_tv(p, s, sup, g, px, px + n, px + 2 * n);
       step_support(s, m1, m2, g, sup, B, c, &adam_steps);
     }
     residual(p, s, sup, y, r);
-    const double loss = sum_sq(r, mb, p->isa);
+    double loss = sum_sq(r, mb, p->isa);
+    if (prior) /* lb.total = residual + w_tv tv (+ w_lv * 0: no LV on one column) */
+      loss = loss + p->w_tv * prior_tv(p, s, sup, NULL, px, NULL, NULL);
     if (!isfinite(loss)) {
       set_err(err, errlen, "clomp: loss diverged; reduce lr");
       status = ORC_ERR_NUMERICAL;
@@ -385,7 +450,7 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
 done:
   free(s); free(m1); free(m2); free(g); free(mask); free(best_s);
   free(best_mask); free(r); free(scores); free(sup); free(best_sup);
-  free(sup_mem);
+  free(sup_mem); free(px);
   return status;
 }
 
@@ -394,6 +459,33 @@ static double* transpose(const double* a, int64_t m, int64_t n) {
   for (int64_t i = 0; i < m; ++i)
     for (int64_t j = 0; j < n; ++j) t[j * m + i] = a[i * n + j];
   return t;
+}
+
+/* Which priors loss_impl evaluates for this solve (clomp.cpp:93-119): TV-1D
+ * on single-column solves (clomp_solve, or a one-column batch); local
+ * variance only when batch >= window (never for one column, except the
+ * window < 2 configuration error local_variance raises, priors.cpp:77-79).
+ * TV-2D / LV on multi-column batches are not restated. */
+static int prior_setup(problem_t* p, const orc_config* c, double w_tv, double w_lv,
+                       int64_t batch, char* err, int errlen) {
+  p->w_tv = 0.0;
+  const int lv_fits = batch >= (int64_t)c->lv_window && p->n >= (int64_t)c->lv_window;
+  if (!(w_tv > 0.0) && !(w_lv > 0.0 && lv_fits)) return ORC_OK;
+  if (batch > 1) {
+    set_err(err, errlen, "clomp oracle: TV-2D / local-variance priors on multi-column "
+                         "batches are not restated");
+    return ORC_ERR_UNSUPPORTED;
+  }
+  if (w_lv > 0.0 && lv_fits) {
+    set_err(err, errlen, "local_variance: window must be >= 2");
+    return ORC_ERR_CONFIG;
+  }
+  if (!p->basis) {
+    set_err(err, errlen, "clomp oracle: priors need the synthesis basis");
+    return ORC_ERR_UNSUPPORTED;
+  }
+  p->w_tv = w_tv;
+  return ORC_OK;
 }
 
 /* Shared driver: `proto` carries the operator (dense or separable). */
@@ -420,14 +512,12 @@ static int solve_driver(problem_t proto, const double* y, int64_t batch,
   if (mode == ORC_MODE_JOINT) {
     double w_tv, w_lv;
     resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
-    if (w_tv > 0.0 || w_lv > 0.0) {
-      set_err(err, errlen, "clomp oracle: priors (w_tv/w_lv > 0) are not restated");
-      return ORC_ERR_UNSUPPORTED;
-    }
     problem_t p = proto;
     p.batch = batch;
-    st = solve_joint(&p, y, cfg, s_out, mask_out, iterations, final_rn,
-                     converged, trace, (int64_t)cfg->max_outer * 4, err, errlen);
+    st = prior_setup(&p, cfg, w_tv, w_lv, batch, err, errlen);
+    if (st == ORC_OK)
+      st = solve_joint(&p, y, cfg, s_out, mask_out, iterations, final_rn,
+                       converged, trace, (int64_t)cfg->max_outer * 4, err, errlen);
     for (int64_t b = 0; b < batch; ++b) status[b] = st;
     return st;
   }
@@ -444,15 +534,13 @@ static int solve_driver(problem_t proto, const double* y, int64_t batch,
     int64_t it = 0;
     double rn = 0.0;
     uint8_t cv = 0;
-    if (w_tv > 0.0 || w_lv > 0.0) {
-      sb = ORC_ERR_UNSUPPORTED;
-    } else {
-      problem_t p = proto;
-      p.batch = 1;
+    problem_t p = proto;
+    p.batch = 1;
+    sb = prior_setup(&p, cfg, w_tv, w_lv, 1, NULL, 0);
+    if (sb == ORC_OK)
       sb = solve_joint(&p, yc, cfg, sc, mc, &it, &rn, &cv,
                        trace ? trace + b * (int64_t)cfg->max_outer * 4 : NULL,
                        4, NULL, 0);
-    }
     status[b] = sb;
     if (sb != ORC_OK) {
       for (int64_t j = 0; j < n; ++j) {
@@ -476,6 +564,27 @@ static int solve_driver(problem_t proto, const double* y, int64_t batch,
   return ORC_OK;
 }
 
+int orc_clomp_solve_batch_basis(const double* a, int64_t m, int64_t n,
+                                const double* basis, const double* y, int64_t batch,
+                                const orc_config* cfg, int isa, int mode,
+                                double* s_out, uint8_t* mask_out,
+                                int64_t* iterations, double* final_rn,
+                                uint8_t* converged, int32_t* status, double* trace,
+                                char* err, int errlen) {
+  if (m <= 0 || n <= 0) {
+    set_err(err, errlen, "clomp: empty operator");
+    return ORC_ERR_DIMENSION;
+  }
+  double* at = transpose(a, m, n);
+  double* dt = basis ? transpose(basis, n, n) : NULL;
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, basis, dt, 0.0};
+  const int st = solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations,
+                              final_rn, converged, status, trace, err, errlen);
+  free(at);
+  free(dt);
+  return st;
+}
+
 int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           const double* y, int64_t batch,
                           const orc_config* cfg, int isa, int mode,
@@ -483,16 +592,9 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           int64_t* iterations, double* final_rn,
                           uint8_t* converged, int32_t* status, double* trace,
                           char* err, int errlen) {
-  if (m <= 0 || n <= 0) {
-    set_err(err, errlen, "clomp: empty operator");
-    return ORC_ERR_DIMENSION;
-  }
-  double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
-  const int st = solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations,
-                              final_rn, converged, status, trace, err, errlen);
-  free(at);
-  return st;
+  return orc_clomp_solve_batch_basis(a, m, n, NULL, y, batch, cfg, isa, mode, s_out,
+                                     mask_out, iterations, final_rn, converged, status,
+                                     trace, err, errlen);
 }
 
 int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
@@ -501,7 +603,8 @@ int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
                         int isa, int mode, double* s_out, uint8_t* mask_out,
                         int64_t* iterations, double* final_rn, uint8_t* converged,
                         int32_t* status, double* trace, char* err, int errlen) {
-  problem_t p = {NULL, NULL, mr * mc, nr * nc, batch, isa, ar, ac, mr, nr, mc, nc};
+  problem_t p = {NULL, NULL, mr * mc, nr * nc, batch, isa, ar, ac, mr, nr, mc, nc,
+                 NULL, NULL, 0.0};
   return solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations, final_rn,
                       converged, status, trace, err, errlen);
 }
@@ -512,7 +615,7 @@ int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
                        int64_t batch, double th, int isa, uint8_t* mask) {
   if (!(th > 0.0) || th > 1.0) return ORC_ERR_CONFIG;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {
@@ -536,7 +639,7 @@ int orc_clomp_loss(const double* a, int64_t m, int64_t n, const double* y,
   resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
   if (w_tv > 0.0 || w_lv > 0.0) return ORC_ERR_UNSUPPORTED;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {

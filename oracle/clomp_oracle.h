@@ -43,7 +43,7 @@ enum {
   ORC_ERR_CONFIG = 2,      /* cskit::ConfigError    (errors.hpp:22) */
   ORC_ERR_DIMENSION = 3,   /* cskit::DimensionError (errors.hpp:16) */
   ORC_ERR_NUMERICAL = 4,   /* cskit::NumericalError (errors.hpp:28) */
-  ORC_ERR_UNSUPPORTED = 5  /* priors (w_tv/w_lv > 0) are not restated */
+  ORC_ERR_UNSUPPORTED = 5  /* multi-column priors (TV-2D / LV), or priors without a basis */
 };
 
 /* Kernel semantics to reproduce: 1 = kernels_avx2.cpp (FMA), 0 = kernels_scalar.cpp. */
@@ -72,6 +72,17 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           int64_t* iterations, double* final_rn,
                           uint8_t* converged, int32_t* status, double* trace,
                           char* err, int errlen);
+
+/* Same with the synthesis basis D (n x n row-major, x = D s; NULL = none), which
+ * the priors need: TV-1D (priors.cpp:11-26) chained through D^T on
+ * single-column solves (PER_SIGNAL, or JOINT with one column). */
+int orc_clomp_solve_batch_basis(const double* a, int64_t m, int64_t n,
+                                const double* basis, const double* y, int64_t batch,
+                                const orc_config* cfg, int isa, int mode,
+                                double* s_out, uint8_t* mask_out,
+                                int64_t* iterations, double* final_rn,
+                                uint8_t* converged, int32_t* status, double* trace,
+                                char* err, int errlen);
 
 /* Separable 2D operator A = A_c (x) A_r with column-major vec (atom
  * p = i + n_r j, measurement q = qr + m_r qc): exactly clomp_solve(_batch) run

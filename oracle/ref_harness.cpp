@@ -105,6 +105,32 @@ int ref_force_isa(int isa) {
   }
 }
 
+// basis: n x n row-major synthesis matrix (x = basis * s) or NULL for the
+// 1 x n dummy; the priors (w_tv / w_lv) need the real one.
+int ref_clomp_solve_batch_b(const double* a, int64_t m, int64_t n, const double* basis,
+                            const double* y, int64_t batch, const ref_config* c,
+                            double* s_out, uint8_t* mask_out, int64_t* iterations,
+                            double* final_rn, uint8_t* converged, double* x_hat,
+                            double* wall_s, char* err, int errlen) {
+  try {
+    const auto setup = to_setup(a, m, n, basis);
+    cskit::la::Mat yc(static_cast<std::size_t>(m), static_cast<std::size_t>(batch));
+    if (batch > 0) std::memcpy(yc.data(), y, sizeof(double) * yc.a.size());
+    const auto res = cskit::clomp_solve_batch(setup, yc, to_cfg(c));
+    std::memcpy(s_out, res.s.data(), sizeof(double) * res.s.a.size());
+    std::memcpy(mask_out, res.mask.data(), res.mask.size());
+    *iterations = static_cast<int64_t>(res.iterations);
+    *final_rn = res.final_residual_norm;
+    *converged = res.converged ? 1 : 0;
+    if (x_hat && basis) std::memcpy(x_hat, res.x_hat.data(), sizeof(double) * res.x_hat.a.size());
+    if (wall_s) *wall_s = res.wall_time_s;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return code_of(e);
+  }
+}
+
 int ref_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           const double* y, int64_t batch, const ref_config* c,
                           double* s_out, uint8_t* mask_out, int64_t* iterations,

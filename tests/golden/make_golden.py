@@ -58,8 +58,11 @@ def main():
     arrays = {}
     cases = []
 
-    def add_solve(name, A, Y, cfg, api, round_a=True):
-        """api: 'batch' (clomp_solve_batch) or 'single' (clomp_solve per column)."""
+    def add_solve(name, A, Y, cfg, api, round_a=True, basis=None, gpu_code=None):
+        """api: 'batch' (clomp_solve_batch) or 'single' (clomp_solve per column).
+        basis: synthesis matrix D (x = D s) handed to the reference, which its
+        priors need; gpu_code: the status the B200 library is expected to give
+        where it differs from the reference's (unsupported configurations)."""
         A = f32(A) if round_a else np.asarray(A, np.float64)
         Y = f32(Y)
         if Y.ndim == 1:
@@ -67,7 +70,7 @@ def main():
         m, n = A.shape
         B = Y.shape[1]
         if api == "batch":
-            r = refbind.ref_solve_batch(A, Y, cfg)
+            r = refbind.ref_solve_batch(A, Y, cfg, basis=basis)
             out = dict(code=r["code"], s=r["s"], mask=r["mask"],
                        iterations=np.full(B, r["iterations"]),
                        final_residual_norm=np.full(B, r["final_residual_norm"]),
@@ -80,7 +83,7 @@ def main():
             cvs = np.zeros(B, bool)
             code = 0
             for b in range(B):
-                r = refbind.ref_solve_batch(A, Y[:, b:b + 1], cfg)  # wrapper == batch of one
+                r = refbind.ref_solve_batch(A, Y[:, b:b + 1], cfg, basis=basis)  # == clomp_solve
                 code = code or r["code"]
                 s[:, b] = r["s"][:, 0]
                 mk[:, b] = r["mask"][:, 0]
@@ -93,8 +96,14 @@ def main():
         arrays[f"{name}/Y"] = Y.astype(np.float32)
         for k in ("s", "mask", "iterations", "final_residual_norm", "converged"):
             arrays[f"{name}/{k}"] = np.asarray(out[k])
-        cases.append(dict(name=name, kind="solve", api=api, code=int(out["code"]),
-                          cfg={f: getattr(cfg, f) for f in cfg.__dataclass_fields__}))
+        if basis is not None:
+            arrays[f"{name}/D"] = np.asarray(basis, np.float64)
+        case = dict(name=name, kind="solve", api=api, code=int(out["code"]),
+                    cfg={f: getattr(cfg, f) for f in cfg.__dataclass_fields__},
+                    basis=basis is not None)
+        if gpu_code is not None:
+            case["gpu_code"] = gpu_code
+        cases.append(case)
         print(f"{name:34s} code={out['code']} iters={np.asarray(out['iterations'])[:4]} "
               f"rn={np.asarray(out['final_residual_norm'])[:2]}")
 
@@ -163,6 +172,36 @@ def main():
         arrays[f"{name}/Ac"] = Ac
         arrays[f"{name}/S"] = S2
         del arrays[f"{name}/A"]
+    # Priors (clomp.cpp:93-119): the reference's default configuration (Adam,
+    # th = 0.7, auto TV / LV weights) on a make_setup-style problem A = Phi D
+    # with the DCT synthesis basis (sensing.cpp:13-29, 60-79).  A column solved
+    # alone sees TV-1D only (LV needs batch >= window); a multi-column batch
+    # runs TV-2D + LV, which the B200 library rejects (gpu_code 5).
+    nP, mP = 64, 32
+    DP = np.zeros((nP, nP))
+    refbind.ref().ref_dct_basis(nP, refbind._p(DP))
+    rngp = np.random.default_rng(77)
+    AP = f32(rngp.standard_normal((mP, nP)) / np.sqrt(mP) @ DP)
+    XP = np.zeros((nP, 3))
+    for b in range(3):
+        XP[rngp.choice(nP, 5, replace=False), b] = rngp.standard_normal(5)
+    YP = f32(AP @ XP + 0.01 * rngp.standard_normal((mP, 3)))
+    add_solve("prior_default_single", AP, YP, ClompConfig(max_outer=15), "single", basis=DP)
+    add_solve("prior_plain_th1_single", AP, YP, ClompConfig(th=1.0, opt=PLAIN, lr=0.1, max_outer=6,
+                                                            w_tv=0.05), "single", basis=DP)
+    add_solve("prior_momentum_auto_single", AP, YP, ClompConfig(th=1.0, opt=MOMENTUM, lr=0.05,
+                                                                max_outer=6, inner_steps=40,
+                                                                w_tv=-1.0), "single", basis=DP)
+    add_solve("prior_joint_b1", AP, YP[:, :1], ClompConfig(max_outer=12), "batch", basis=DP)
+    add_solve("prior_joint_b3_tv2d", AP, YP, ClompConfig(max_outer=8), "batch", basis=DP,
+              gpu_code=5)
+    # identity basis: TV of the coefficients themselves
+    Ai, Yi = rand_problem(8, 32, 64, 5, 2, snr_db=30)
+    add_solve("prior_identity_basis_single", Ai, Yi, ClompConfig(th=1.0, opt=ADAM, lr=0.02,
+                                                               max_outer=8, inner_steps=60,
+                                                               w_tv=0.2), "single",
+              basis=np.eye(64))
+
     # config validation (test_clomp.cpp:328-343)
     add_solve("bad_th", A, Y[:, :1], ClompConfig(th=0.0), "batch")
     add_solve("bad_inner", A, Y[:, :1], ClompConfig(inner_steps=0), "batch")

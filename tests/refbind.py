@@ -42,6 +42,9 @@ def oracle() -> C.CDLL:
         vp, i64 = C.c_void_p, C.c_int64
         h.orc_clomp_solve_batch.argtypes = [vp, i64, i64, vp, i64, C.POINTER(CConfig), C.c_int,
                                             C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_char_p, C.c_int]
+        h.orc_clomp_solve_batch_basis.argtypes = [vp, i64, i64, vp, vp, i64, C.POINTER(CConfig),
+                                                  C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp,
+                                                  C.c_char_p, C.c_int]
         h.orc_clomp_solve_sep.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, C.POINTER(CConfig),
                                           C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp,
                                           C.c_char_p, C.c_int]
@@ -63,6 +66,8 @@ def ref() -> C.CDLL:
         vp, i64 = C.c_void_p, C.c_int64
         h.ref_clomp_solve_batch.argtypes = [vp, i64, i64, vp, i64, C.POINTER(CConfig), vp, vp, vp,
                                             vp, vp, vp, C.c_char_p, C.c_int]
+        h.ref_clomp_solve_batch_b.argtypes = [vp, i64, i64, vp, vp, i64, C.POINTER(CConfig), vp,
+                                              vp, vp, vp, vp, vp, vp, C.c_char_p, C.c_int]
         h.ref_clomp_solve.argtypes = [vp, i64, i64, vp, C.POINTER(CConfig), vp, vp, vp, vp, vp, vp,
                                       C.c_char_p, C.c_int]
         h.ref_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, vp]
@@ -73,9 +78,11 @@ def ref() -> C.CDLL:
     return _ref
 
 
-def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False):
-    """Oracle restatement. A m x n, Y m x B (fp64 arrays of fp32 values)."""
+def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False, basis=None):
+    """Oracle restatement. A m x n, Y m x B (fp64 arrays of fp32 values);
+    basis: n x n synthesis matrix for the priors (None: no basis)."""
     A = np.ascontiguousarray(A, np.float64)
+    D = None if basis is None else np.ascontiguousarray(basis, np.float64)
     Y = np.ascontiguousarray(Y, np.float64)
     if Y.ndim == 1:
         Y = Y.reshape(-1, 1)
@@ -90,8 +97,9 @@ def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False
     tr = np.zeros((B, max(1, cfg.max_outer), 4)) if trace else None
     err = C.create_string_buffer(256)
     c = cfg.to_c()
-    code = oracle().orc_clomp_solve_batch(_p(A), m, n, _p(Y), B, C.byref(c), isa, mode, _p(s),
-                                          _p(mk), _p(it), _p(rn), _p(cv), _p(st), _p(tr), err, 256)
+    code = oracle().orc_clomp_solve_batch_basis(_p(A), m, n, _p(D), _p(Y), B, C.byref(c), isa,
+                                                mode, _p(s), _p(mk), _p(it), _p(rn), _p(cv),
+                                                _p(st), _p(tr), err, 256)
     return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
                 final_residual_norm=rn, converged=cv.astype(bool), status=st, trace=tr)
 
@@ -120,9 +128,11 @@ def orc_solve_sep(Ar, Ac, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2):
                 final_residual_norm=rn, converged=cv.astype(bool), status=st)
 
 
-def ref_solve_batch(A, Y, cfg: ClompConfig):
-    """The unmodified reference clomp_solve_batch."""
+def ref_solve_batch(A, Y, cfg: ClompConfig, basis=None):
+    """The unmodified reference clomp_solve_batch (basis: n x n synthesis
+    matrix, needed by the priors; None: the 1 x n dummy of SURVEY.md D8)."""
     A = np.ascontiguousarray(A, np.float64)
+    D = None if basis is None else np.ascontiguousarray(basis, np.float64)
     Y = np.ascontiguousarray(Y, np.float64)
     if Y.ndim == 1:
         Y = Y.reshape(-1, 1)
@@ -136,10 +146,12 @@ def ref_solve_batch(A, Y, cfg: ClompConfig):
     wall = np.zeros(1)
     err = C.create_string_buffer(256)
     c = cfg.to_c()
-    code = ref().ref_clomp_solve_batch(_p(A), m, n, _p(Y), B, C.byref(c), _p(s), _p(mk), _p(it),
-                                       _p(rn), _p(cv), _p(wall), err, 256)
+    xh = np.zeros((n, B)) if D is not None else None
+    code = ref().ref_clomp_solve_batch_b(_p(A), m, n, _p(D), _p(Y), B, C.byref(c), _p(s), _p(mk),
+                                         _p(it), _p(rn), _p(cv), _p(xh), _p(wall), err, 256)
     return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=int(it[0]),
-                final_residual_norm=float(rn[0]), converged=bool(cv[0]), wall_s=float(wall[0]))
+                final_residual_norm=float(rn[0]), converged=bool(cv[0]), wall_s=float(wall[0]),
+                x_hat=xh)
 
 
 def orc_inject(A, R, th, mask, isa=ISA_AVX2):

@@ -29,9 +29,11 @@ def test_oracle_matches_reference_golden(case):
     A = ARR[f"{name}/A"].astype(np.float64)
     Y = ARR[f"{name}/Y"].astype(np.float64)
     mode = refbind.MODE_JOINT if case["api"] == "batch" else refbind.MODE_PER_SIGNAL
-    r = refbind.orc_solve(A, Y, _cfg(case["cfg"]), mode=mode)
-    assert r["code"] == case["code"], r["err"]
-    if case["code"] != 0:
+    D = ARR[f"{name}/D"] if case.get("basis") else None
+    r = refbind.orc_solve(A, Y, _cfg(case["cfg"]), mode=mode, basis=D)
+    code = case.get("gpu_code", case["code"])  # multi-column priors: not restated
+    assert r["code"] == code, r["err"]
+    if code != 0:
         return
     assert np.array_equal(r["mask"], ARR[f"{name}/mask"])
     assert np.array_equal(r["s"], ARR[f"{name}/s"])  # bit-exact
@@ -73,10 +75,60 @@ def test_wrapper_equals_one_column_batch():
 
 
 def test_priors_are_rejected_not_faked():
+    """Priors need the synthesis basis; multi-column priors (TV-2D / LV) are
+    not restated and say so instead of running something else."""
     A = ARR["small_th1_plain_b1/A"].astype(np.float64)
     Y = ARR["small_th1_plain_b1/Y"].astype(np.float64)
-    r = refbind.orc_solve(A, Y, ClompConfig())  # defaults: auto priors on
+    r = refbind.orc_solve(A, Y, ClompConfig())  # defaults: auto priors on, no basis
     assert r["code"] == 5
+    D = ARR["prior_joint_b3_tv2d/D"]
+    r = refbind.orc_solve(ARR["prior_joint_b3_tv2d/A"], ARR["prior_joint_b3_tv2d/Y"],
+                          ClompConfig(max_outer=3), mode=refbind.MODE_JOINT, basis=D)
+    assert r["code"] == 5
+
+
+def test_tv_prior_is_a_quadratic_form_on_dct_coefficients():
+    """TV-1D of x = D s equals s^T H s with H = D^T Delta^T Delta D / n
+    (priors.cpp:11-26); for the DCT basis (sensing.cpp:13-29) H is diagonal
+    with entries (2 - 2 cos(pi k / n)) / n.  This is the identity the B200
+    learning kernels use to fold the prior into the support Gram matrix."""
+    n = 64
+    D = ARR["prior_default_single/D"]
+    Dl = np.diff(D, axis=0)  # rows x_{j+1} - x_j of Delta D
+    H = Dl.T @ Dl / n
+    lam = (2 - 2 * np.cos(np.pi * np.arange(n) / n)) / n
+    assert np.allclose(H, np.diag(lam), atol=1e-12)
+
+
+@pytest.mark.skipif(not refbind.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("isa", [refbind.ISA_AVX2, refbind.ISA_SCALAR])
+@pytest.mark.parametrize("opt,w_tv", [(ADAM, -1.0), (PLAIN, 0.05), (MOMENTUM, -1.0)])
+def test_oracle_priors_match_live_reference(isa, opt, w_tv):
+    """TV-1D prior chained through the DCT basis, per-signal and one-column
+    joint solves, both kernel ISAs, bit for bit."""
+    rng = np.random.default_rng(200 + 10 * isa + opt)
+    n, m, B, k = 48, 24, 3, 4
+    D = np.zeros((n, n))
+    refbind.ref().ref_dct_basis(n, refbind._p(D))
+    A = (rng.standard_normal((m, n)) / np.sqrt(m) @ D).astype(np.float32).astype(np.float64)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, k, replace=False), b] = rng.standard_normal(k)
+    Y = (A @ X + 0.02 * rng.standard_normal((m, B))).astype(np.float32).astype(np.float64)
+    cfg = ClompConfig(th=0.7 if opt == ADAM else 1.0, max_outer=8, inner_steps=30,
+                      lr=0.05 if opt != ADAM else 0.02, opt=opt, w_tv=w_tv)
+    assert refbind.ref().ref_force_isa(isa) == 0
+    try:
+        orc = refbind.orc_solve(A, Y, cfg, mode=refbind.MODE_PER_SIGNAL, isa=isa, basis=D)
+        for b in range(B):
+            ref = refbind.ref_solve_batch(A, Y[:, b:b + 1], cfg, basis=D)
+            assert ref["code"] == orc["status"][b] == 0
+            assert np.array_equal(ref["s"][:, 0], orc["s"][:, b])
+            assert np.array_equal(ref["mask"][:, 0], orc["mask"][:, b])
+            assert ref["iterations"] == orc["iterations"][b]
+            assert ref["final_residual_norm"] == orc["final_residual_norm"][b]
+    finally:
+        refbind.ref().ref_force_isa(refbind.ISA_AVX2)
 
 
 @pytest.mark.skipif(not refbind.ref_available(), reason="oracle/_ref not built")
