@@ -205,6 +205,15 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode);
  * semantics) run the whole solve in one persistent block per signal; 0
  * forces the batched kernel pipeline instead (tests compare the two). */
 int cl_set_fused(cl_ctx* ctx, int on);
+/* Synthesis basis D (n x n, x = D s; MeasurementSetup::basis, sensing.hpp:37-45)
+ * for the priors.  The TV prior (priors.cpp:11-26, chained through D^T,
+ * clomp.cpp:93-119) runs on single-column solves: CL_MODE_PER_SIGNAL (the
+ * CLI's 1D path, clomp_solve per column) or a one-column batch, folded into
+ * the support Gram system.  layout CL_LAYOUT_REF: basis[q * n + j] = D(q, j)
+ * (la::Mat row-major); CL_LAYOUT_T: the transpose.  NULL clears.
+ * Priors on multi-column joint batches (TV-2D + local variance) return
+ * CL_ERR_UNSUPPORTED; priors without a basis too. */
+int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram
  * matrix in registers (default 1); 0 keeps them on the block-per-signal
  * kernel (tests compare the two). */

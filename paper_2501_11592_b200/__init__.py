@@ -147,9 +147,9 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_basis",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
-    "cl_gen_problem_2d",
+    "cl_gen_problem_2d", "cl_dct_basis",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
 
@@ -183,6 +183,7 @@ def lib() -> C.CDLL:
         h.cl_set_gram_cache.argtypes = [vp, i32]
         h.cl_set_fused.argtypes = [vp, i32]
         h.cl_set_cluster_learn.argtypes = [vp, i32]
+        h.cl_set_basis.argtypes = [vp, vp, C.c_int64, i32]
         h.cl_nccl_unique_id.argtypes = [vp]
         h.cl_create_colshard.restype = vp
         h.cl_create_colshard.argtypes = [i32, vp, i64, i64, i32, i32, i32, vp, C.POINTER(C.c_int)]
@@ -190,6 +191,7 @@ def lib() -> C.CDLL:
         h.cl_create_sep.restype = vp
         h.cl_create_sep.argtypes = [i32, vp, i64, i64, vp, i64, i64, i32, C.POINTER(C.c_int)]
         h.cl_gen_problem_2d.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]
+        h.cl_dct_basis.argtypes = [i64, vp]
         h.cl_config_default.argtypes = [C.POINTER(CConfig)]
         h.cl_rng_draws.argtypes = [C.c_uint64, i32, C.c_uint64, i64, vp, vp]
         h.cl_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, i32, i32, C.c_double, vp, vp, vp, vp]
@@ -376,6 +378,17 @@ class ClompContext:
         """Allow (default) or forbid the one-block-per-signal latency path."""
         _raise(lib().cl_set_fused(self._h, int(bool(on))), self._h)
 
+    def set_basis(self, D):
+        """Synthesis basis D (n x n, x = D s; MeasurementSetup::basis) for the
+        TV prior of single-column solves; None clears it."""
+        if D is None:
+            _raise(lib().cl_set_basis(self._h, None, 0, 0), self._h)
+            return
+        D = np.ascontiguousarray(D, np.float64)
+        if D.ndim != 2 or D.shape[0] != D.shape[1]:
+            raise DimensionError("set_basis: D must be square")
+        _raise(lib().cl_set_basis(self._h, _ptr(D), D.shape[0], 0), self._h)
+
     def set_cluster_learn(self, on: bool):
         """Learn supports of 33..256 atoms on CTA clusters with register-resident
         Gram blocks (default) or on the block-per-signal kernel."""
@@ -526,6 +539,14 @@ def gen_problem_2d(seed: int, n_r: int, n_c: int, m_r: int, m_c: int, k: int, ba
 
 # BASELINE.json configs.  lr / epochs for configs 2-5 are not
 # stated there; config 1's are used and recorded.
+def dct_basis(n: int) -> np.ndarray:
+    """dct_basis (sensing.cpp:13-29): the orthonormal DCT-II synthesis matrix
+    D (n x n, x = D s) of make_setup problems, for ClompContext.set_basis."""
+    D = np.zeros((n, n), np.float64)
+    _raise(lib().cl_dct_basis(int(n), _ptr(D)))
+    return D
+
+
 CONFIGS = {
     1: dict(name="cfg1_1d_single", m=128, n=256, k=10, batch=1, value_law=0, snr_db=-1.0, seed=0),
     2: dict(name="cfg2_1d_batched", m=512, n=1024, k=32, batch=4096, value_law=0, snr_db=40.0, seed=1),

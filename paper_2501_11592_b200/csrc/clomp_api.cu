@@ -72,6 +72,11 @@ struct cl_ctx {
   __half* at_lo = nullptr;
   float a_scale = 1.0f;      // its power-of-two scale
   double* gfull = nullptr;  // A^T A fp64 [n][n], built once (k_gram.cu)
+  // synthesis basis for the priors (cl_set_basis): Delta D atom-major,
+  // ddt[j][q] = D[q][j] - D[q+1][j] (q < n - 1), fp64, row stride ldd
+  double* ddt = nullptr;
+  int64_t ldd = 0;
+  std::vector<double> prior_w;  // this call's per-signal TV weights (empty: off)
   // separable 2D contexts (cl_create_sep)
   bool sep = false;
   int64_t mr = 0, nr = 0, mc = 0, nc = 0, ldr = 0, ldc = 0;
@@ -151,6 +156,25 @@ int validate(cl_ctx* ctx, const cl_config* c) {
   return CL_OK;
 }
 
+// kern::sum_sq as the reference computes it on x86 (the AVX2 dot of
+// kernels_avx2.cpp:30-58: 4 x 4 accumulators over 16-wide blocks, a 4-wide
+// block loop, pairwise combination, FMA tail), so automatic prior weights
+// (resolve_weights, clomp.cpp:131-140) are the reference's bits.
+double ref_sum_sq(const double* v, int64_t n) {
+  double acc[4][4] = {};
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16)
+    for (int k = 0; k < 4; ++k)
+      for (int l = 0; l < 4; ++l) acc[k][l] = std::fma(v[i + 4 * k + l], v[i + 4 * k + l], acc[k][l]);
+  for (; i + 4 <= n; i += 4)
+    for (int l = 0; l < 4; ++l) acc[0][l] = std::fma(v[i + l], v[i + l], acc[0][l]);
+  double q[4];
+  for (int l = 0; l < 4; ++l) q[l] = (acc[0][l] + acc[1][l]) + (acc[2][l] + acc[3][l]);
+  double total = (q[0] + q[2]) + (q[1] + q[3]);
+  for (; i < n; ++i) total = std::fma(v[i], v[i], total);
+  return total;
+}
+
 // resolve_weights (clomp.cpp:131-140) and whether loss_impl would run a prior
 // (clomp.cpp:93-94: LV only when the batch fits its window).
 bool priors_active(const cl_config* c, double mean_sq, int64_t batch, int64_t n) {
@@ -170,7 +194,7 @@ int64_t support_cap(const cl_ctx* ctx, const cl_config* c) {
 
 // Carve the workspace for (B, cap); reallocate only when it grows.
 int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
-                     bool need_split, int64_t ntile) {
+                     bool need_split, int64_t ntile, bool need_prior = false) {
   const int64_t ldm = ctx->ldm;
   const int64_t mwords = (ctx->n + 31) / 32;
   auto carve = [&](Carver& cv, Work& w) {
@@ -213,6 +237,12 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.big_list = cv.take<int32_t>(B);
     w.counters = cv.take<int32_t>(kNumCounters);
     w.joint = cv.take<double>(kNumJoint);
+    if (need_prior) {
+      w.hgram = cv.take<double>(B * cap * cap);
+      w.wtv = cv.take<double>(B);
+      w.rloss = cv.take<double>(B);
+      w.best_R = cv.take<double>(B);
+    }
   };
   Carver probe{nullptr};
   Work tmp;
@@ -239,6 +269,8 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
   w.at_c64 = ctx->at_c64;
   w.gr = ctx->gr;
   w.gc = ctx->gc;
+  w.ddt = need_prior ? ctx->ddt : nullptr;
+  w.ldd = ctx->ldd;
   ctx->w = w;
   return CL_OK;
 }
@@ -287,7 +319,7 @@ void enqueue_count(const SolveParams& p, const cl_config* c, int mode, int64_t c
   if (p.sep)
     *per_iter = 3 + 2 + (cap > 8 ? 2 : 1) + 3 + (mode == CL_MODE_JOINT ? 2 : 0);
   else
-    *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0);
+    *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0) + (p.prior ? 3 : 0);
 }
 
 struct OutPtrs {
@@ -334,15 +366,19 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                 "supported (lower max_outer, or th < 1 with n > 2048)");
   // Latency path: the whole solve in one persistent block per signal when the
   // dictionary is small (config 1) and supports stay register-resident.
-  const bool fused = ctx->fused_ok && !ctx->sep && !colshard &&
+  const bool prior = !ctx->prior_w.empty();
+  const bool fused = ctx->fused_ok && !ctx->sep && !colshard && !prior &&
                      (mode == CL_MODE_PER_SIGNAL || B == 1) &&
                      cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
                      B <= 4 * (int64_t)ctx->sms;
   const int64_t tile_atoms =
       tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
-  int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile);
+  int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile, prior);
   if (st) return st;
+  if (prior)
+    CL_CUDA(ctx, cudaMemcpyAsync(ctx->w.wtv, ctx->prior_w.data(), (size_t)B * sizeof(double),
+                                 cudaMemcpyHostToDevice, ctx->stream));
   st = ensure_adam_tables(ctx, c);
   if (st) return st;
 
@@ -378,7 +414,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.max_outer = (int32_t)c->max_outer;
   // A one-column joint solve is exactly clomp_solve (clomp.cpp:294-311), so
   // the fused path runs everything with per-signal state.
-  p.mode = fused ? CL_MODE_PER_SIGNAL : mode;
+  p.mode = (fused || (prior && B == 1)) ? CL_MODE_PER_SIGNAL : mode;
+  p.prior = prior ? 1 : 0;
   p.bc1 = ctx->bc;
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
   p.delta_rel = delta_for(tensor, ctx->ldm);
@@ -393,7 +430,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.ldc = ctx->ldc;
   // th == 1: the selection (K1c, near-tie rescoring included) runs at the top
   // of the learning kernel, one warp per signal, instead of its own launch.
-  p.fuse_select = (!full_scores && !p.sep) ? 1 : 0;
+  p.fuse_select = (!full_scores && !p.sep && !prior) ? 1 : 0;
   p.cluster_learn = ctx->cluster_learn ? 1 : 0;
   p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
 
@@ -467,9 +504,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     else
       launch_corr_f64(p, w, full_scores, s);
     if (!p.fuse_select) launch_select(p, w, full_scores, s);
+    if (p.prior) launch_prior_ext(p, w, s);
     const int bound = c->th >= 1.0 ? outer : (int)cap;
     launch_learn(p, w, outer, bound, s);
-    *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
+    if (p.prior) launch_prior_control(p, w, outer, s);
+    *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
     if (mode == CL_MODE_JOINT) {
       launch_joint_control(p, w, outer, false, s);
       launch_joint_snapshot(p, w, s);
@@ -539,9 +578,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
           launch_corr_f64(p, w, full_scores, s);
         cudaEventRecord(e[1], s);
         if (!p.fuse_select) launch_select(p, w, full_scores, s);
+        if (p.prior) launch_prior_ext(p, w, s);
         cudaEventRecord(e[2], s);
         launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
-        launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2);
+        if (p.prior) launch_prior_control(p, w, o, s);
+        launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
         if (mode == CL_MODE_JOINT) {
           launch_joint_control(p, w, o, false, s);
           launch_joint_snapshot(p, w, s);
@@ -900,6 +941,7 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode) {
     if (ctx->gfull) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->gfull);
+  cudaFree(ctx->ddt);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);
@@ -931,6 +973,7 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->at_hi);
   cudaFree(ctx->at_lo);
   cudaFree(ctx->gfull);
+  cudaFree(ctx->ddt);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);
@@ -1013,6 +1056,36 @@ int cl_set_fused(cl_ctx* ctx, int on) {
   return CL_OK;
 }
 
+int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  cudaSetDevice(ctx->device);
+  if (ctx->sep)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "cl_set_basis: priors on separable contexts are not implemented");
+  if (layout != CL_LAYOUT_REF && layout != CL_LAYOUT_T)
+    return fail(ctx, CL_ERR_CONFIG, "cl_set_basis: unknown layout");
+  cudaFree(ctx->ddt);
+  ctx->ddt = nullptr;
+  ctx->ldd = 0;
+  if (!basis) return CL_OK;  // cleared
+  if (n != ctx->n)
+    return fail(ctx, CL_ERR_DIMENSION, "cl_set_basis: basis is " + std::to_string(n) + " x " +
+                                           std::to_string(n) + ", the dictionary has n = " +
+                                           std::to_string(ctx->n) + " atoms");
+  // Delta D atom-major: row j holds D[q][j] - D[q+1][j], q < n - 1 (fp64,
+  // exact differences of the caller's fp64 basis), zero padded to ldd.
+  const int64_t ldd = std::max<int64_t>(32, (n - 1 + 31) / 32 * 32);
+  std::vector<double> h((size_t)(n * ldd), 0.0);
+  auto at = [&](int64_t q, int64_t j) {  // D[q][j]
+    return layout == CL_LAYOUT_REF ? basis[q * n + j] : basis[j * n + q];
+  };
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t q = 0; q + 1 < n; ++q) h[(size_t)(j * ldd + q)] = at(q, j) - at(q + 1, j);
+  CL_CUDA(ctx, cudaMalloc(&ctx->ddt, h.size() * sizeof(double)));
+  CL_CUDA(ctx, cudaMemcpy(ctx->ddt, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  ctx->ldd = ldd;
+  return CL_OK;
+}
+
 int cl_set_cluster_learn(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
   ctx->cluster_learn = on != 0;
@@ -1038,23 +1111,56 @@ int cl_synchronize(cl_ctx* ctx) {
   return CL_OK;
 }
 
+// Priors the B200 path runs: TV-1D (priors.cpp:11-26) on single-column
+// solves — clomp_solve on every column (the CLI's 1D path) or a one-column
+// batch — folded into the support Gram system (k_prior_ext).  Multi-column
+// joint batches (TV-2D + local variance) and separable contexts are
+// rejected.  col_ms: mean(y^2) per column (automatic weights).
 static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode,
                       double mean_sq_all, const std::vector<double>* col_ms) {
+  ctx->prior_w.clear();
   int st = validate(ctx, cfg);
   if (st) return st;
   if (batch <= 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: empty batch");
   if (mode != CL_MODE_JOINT && mode != CL_MODE_PER_SIGNAL)
     return fail(ctx, CL_ERR_CONFIG, "clomp: unknown solve mode");
+  const bool single = mode == CL_MODE_PER_SIGNAL || batch == 1;
   bool pri = false;
-  if (mode == CL_MODE_JOINT) {
+  if (!single) {
     pri = priors_active(cfg, mean_sq_all, batch, ctx->n);
   } else if (col_ms) {
     for (double ms : *col_ms) pri = pri || priors_active(cfg, ms, 1, ctx->n);
+  } else {
+    pri = cfg->w_tv > 0.0 || (cfg->w_lv > 0.0 && cfg->lv_window <= 1);
   }
-  if (pri)
+  if (!pri) return CL_OK;
+  if (!single)
     return fail(ctx, CL_ERR_UNSUPPORTED,
-                "clomp: TV/LV priors are not implemented on the B200 path; set "
-                "w_tv = w_lv = 0");
+                "clomp: TV-2D / local-variance priors of multi-column joint batches are not "
+                "implemented on the B200 path (per-signal solves, or w_tv = w_lv = 0)");
+  if (ctx->sep)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: priors on separable contexts are not implemented");
+  if (ctx->world > 1 || ctx->vshards > 1)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: priors on column-sharded contexts are not implemented");
+  // local_variance runs on a single column only when its window is < 2,
+  // which it rejects (priors.cpp:77-79)
+  if (cfg->w_lv != 0.0 && cfg->lv_window <= 1 && (uint64_t)ctx->n >= cfg->lv_window) {
+    for (int64_t b = 0; b < batch; ++b) {
+      const double w_lv = cfg->w_lv < 0.0 ? 0.01 * (col_ms ? (*col_ms)[(size_t)b] : 0.0) : cfg->w_lv;
+      if (w_lv > 0.0) return fail(ctx, CL_ERR_CONFIG, "local_variance: window must be >= 2");
+    }
+  }
+  if (cfg->w_tv == 0.0) return CL_OK;  // only LV was configured: it never runs here
+  if (!ctx->ddt)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "clomp: the TV prior needs the synthesis basis (cl_set_basis)");
+  if (cfg->w_tv < 0.0 && !col_ms)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_solve_batch_device: automatic prior weights need y on the host; pass "
+                "an explicit w_tv");
+  ctx->prior_w.assign((size_t)batch, cfg->w_tv);
+  if (cfg->w_tv < 0.0)
+    for (int64_t b = 0; b < batch; ++b) ctx->prior_w[(size_t)b] = 0.01 * (*col_ms)[(size_t)b];
   return CL_OK;
 }
 
@@ -1092,16 +1198,19 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   double all = 0.0;
   if (batch > 0 && cfg && (cfg->w_tv < 0.0 || cfg->w_lv < 0.0)) {
     col_ms.assign((size_t)batch, 0.0);
-    for (int64_t i = 0; i < m; ++i)
-      for (int64_t b = 0; b < batch; ++b) {
-        const double v = y_layout == CL_LAYOUT_REF ? y[i * batch + b] : y[b * m + i];
-        col_ms[(size_t)b] += v * v;
-      }
-    for (double& v : col_ms) {
-      all += v;
-      v /= (double)m;
+    std::vector<double> col((size_t)m), rowmajor;
+    for (int64_t b = 0; b < batch; ++b) {
+      for (int64_t i = 0; i < m; ++i)
+        col[(size_t)i] = y_layout == CL_LAYOUT_REF ? y[i * batch + b] : y[b * m + i];
+      col_ms[(size_t)b] = ref_sum_sq(col.data(), m) / (double)m;
     }
-    all /= (double)(m * batch);
+    // the whole batch in the reference's row-major order (m x B)
+    rowmajor.resize((size_t)(m * batch));
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t b = 0; b < batch; ++b)
+        rowmajor[(size_t)(i * batch + b)] =
+            y_layout == CL_LAYOUT_REF ? y[i * batch + b] : y[b * m + i];
+    all = ref_sum_sq(rowmajor.data(), m * batch) / (double)(m * batch);
   }
   int st = check_call(ctx, batch, cfg, mode, all, col_ms.empty() ? nullptr : &col_ms);
   if (st) return st;
@@ -1196,11 +1305,8 @@ int cl_solve_batch_device(cl_ctx* ctx, const float* d_y, int64_t batch,
                           const cl_device_result* out) {
   if (!ctx) return CL_ERR_INTERNAL;
   cudaSetDevice(ctx->device);
-  // Prior weights need mean(y^2); the device path requires them off explicitly
-  // (w_tv == w_lv == 0), which is what every BASELINE config uses.
-  if (cfg && (cfg->w_tv != 0.0 || cfg->w_lv != 0.0))
-    return fail(ctx, CL_ERR_UNSUPPORTED,
-                "cl_solve_batch_device: set w_tv = w_lv = 0 (priors unsupported)");
+  // Automatic prior weights need mean(y^2) of host data: the device path
+  // takes explicit weights only (check_call).
   int st = check_call(ctx, batch, cfg, mode, 0.0, nullptr);
   if (st) return st;
   if (!out) return fail(ctx, CL_ERR_DIMENSION, "cl_solve_batch_device: null result");

@@ -111,6 +111,11 @@ struct SolveParams {
   // supports of 33..256 atoms learn on CTA clusters with register-resident
   // Gram blocks (k_learn_cluster); 0 keeps them on k_learn_block (tests)
   int32_t cluster_learn;
+  // TV-1D prior (single-column solves): the Gram system carries
+  // G + w_b H, H = (Delta D_S)^T (Delta D_S) / n, extended by k_prior_ext; the
+  // learning kernels store the residual loss and k_prior_control adds w_b c^T H c
+  // and runs the stopping rules (clomp.cpp:93-119, 253-273)
+  int32_t prior;
 };
 
 struct Work {
@@ -160,6 +165,13 @@ struct Work {
   int32_t* big_list = nullptr;     // [B] signals queued for the block learner
   int32_t* counters = nullptr;     // see Counter
   double* joint = nullptr;         // see Joint
+  // priors (SolveParams::prior)
+  const double* ddt = nullptr;     // [n][ldd] Delta D atom-major (fp64)
+  int64_t ldd = 0;
+  double* hgram = nullptr;         // [B][cap][cap] H of the support
+  double* wtv = nullptr;           // [B] resolved TV weight per signal
+  double* rloss = nullptr;         // [B] residual part of the current loss
+  double* best_R = nullptr;        // [B] residual part of the best snapshot's loss
 };
 
 enum Counter {
@@ -267,6 +279,11 @@ bool nccl_allgather_inplace(void* comm, void* buf, size_t count_per_rank, int by
 bool nccl_allreduce_sum_i32(void* comm, int32_t* buf, size_t count, cudaStream_t s);
 void launch_cand_exchange(const Cand* g, Cand* cand, int64_t B, int64_t ntl, int world,
                           int64_t atoms_per_rank, cudaStream_t s);
+
+// Priors: Gram + H extension for the atoms selected this iteration (before
+// the learning kernels), and loss / stopping rules after them.
+void launch_prior_ext(const SolveParams& p, const Work& w, cudaStream_t s);
+void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
 
 // Whole per-signal solve in one persistent block per signal (small problems).
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);

@@ -187,6 +187,15 @@ static void dct(int64_t n, std::vector<double>& d) {
   }
 }
 
+// The synthesis basis of make_setup problems (x = D s), for cl_set_basis.
+int cl_dct_basis(int64_t n, double* out) {
+  if (n <= 0 || !out) return 3;
+  std::vector<double> d;
+  dct(n, d);
+  std::memcpy(out, d.data(), sizeof(double) * d.size());
+  return 0;
+}
+
 // Separable 2D problem (BASELINE configs 4-5):
 //   Phi_r (m_r x n_r), Phi_c (m_c x n_c) i.i.d. normal()/sqrt(m), row-major;
 //   A_r = fp32(Phi_r D_r), A_c = fp32(Phi_c D_c) with D the orthonormal DCT;

@@ -83,7 +83,8 @@ __global__ void k_init(SolveParams p, Work w, const float* __restrict__ y_in,
   const double L = warp_sum(acc);
   if (w.r_hi) split_row(w, b, p.ldm, L, lane, 32);
   if (lane == 0) {
-    w.loss[b] = L;
+    w.loss[b] = L;  // s = 0: the prior terms vanish
+    if (w.rloss) w.rloss[b] = L;
     w.cnt[b] = 0;
     w.gcnt[b] = 0;
     w.best_cnt[b] = 0;
@@ -417,9 +418,13 @@ __device__ __forceinline__ CtlState load_ctl(const Work& w, int64_t b) {
   return c;
 }
 
+// L: the loss the reference's best / stall / divergence rules read (lb.total,
+// clomp.cpp:253-273); L_res: its residual part, which the eps test reads
+// (clomp.cpp:238-242).  They differ only with a prior.
 __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
-                               int outer, double L, const CtlState& st) {
+                               int outer, double L, const CtlState& st, double L_res) {
   w.loss[b] = L;
+  if (w.rloss) w.rloss[b] = L_res;
   if (!isfinite(L)) {
     w.status[b] = kStatusNumerical;
     w.active[b] = 0;
@@ -430,6 +435,7 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
   if (L < st.best_L) {
     w.best_L[b] = L;
     w.best_cnt[b] = st.cnt;
+    if (w.best_R) w.best_R[b] = L_res;
     snap = true;
   }
   const double prev = st.prev_L;
@@ -440,7 +446,7 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
   w.prev_L[b] = L;
   if (stall >= p.stall_patience || outer >= p.max_outer) {
     w.active[b] = 0;
-  } else if (sqrt(L) < p.eps) {
+  } else if (sqrt(L_res) < p.eps) {
     w.conv[b] = 1;
     w.active[b] = 0;
   } else {
@@ -450,8 +456,13 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
 }
 
 __device__ __forceinline__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
+                                               int outer, double L, const CtlState& st) {
+  return control_signal(p, w, b, outer, L, st, L);
+}
+
+__device__ __forceinline__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
                                                int outer, double L) {
-  return control_signal(p, w, b, outer, L, load_ctl(w, b));
+  return control_signal(p, w, b, outer, L, load_ctl(w, b), L);
 }
 
 // ----------------------------------------------------- optimizer steps
@@ -1079,7 +1090,9 @@ k_resid_w(SolveParams p, Work w, int outer) {
   const double L = warp_residual(p, w, b, cs, sups, t, lane);
   int snap = 0;
   if (lane == 0) {
-    if (p.mode == kModePerSignal)
+    if (p.prior)
+      w.rloss[b] = L;  // k_prior_control adds the prior and decides
+    else if (p.mode == kModePerSignal)
       snap = control_signal(p, w, b, outer, L, ctl);
     else
       w.loss[b] = L;
@@ -1549,7 +1562,9 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
       for (int q = 0; q < nw; ++q) L += red[q];
       s_L = L;
       snap_s = 0;
-      if (p.mode == kModePerSignal)
+      if (p.prior)
+        w.rloss[b] = L;  // k_prior_control adds the prior and decides
+      else if (p.mode == kModePerSignal)
         snap_s = control_signal(p, w, b, outer, L);
       else
         w.loss[b] = L;
@@ -1880,7 +1895,9 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       double L = 0.0;
       for (int r = 0; r < Q; ++r) L += lpart[r];
       int snap = 0;
-      if (p.mode == kModePerSignal)
+      if (p.prior)
+        w.rloss[b] = L;  // k_prior_control adds the prior and decides
+      else if (p.mode == kModePerSignal)
         snap = control_signal(p, w, b, outer, L);
       else
         w.loss[b] = L;
@@ -1895,6 +1912,109 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       for (int k = gt; k < t; k += GS) w.best_coef[b * cap + k] = cs[k];
     cl_sync<Q>();  // smem (sups, cbuf, lpart) free for the next signal
   }
+}
+
+// ------------------------------------------------------------- priors
+// TV-1D (priors.cpp:11-26) on x = D s of a single-column solve is the
+// quadratic form tv = s^T H s with H = (Delta D)^T (Delta D) / n, Delta the
+// forward difference; its chained gradient D^T (w dtv/dx) (clomp.cpp:93-117)
+// is 2 w H s.  On the support the learning system becomes
+// g = 2 ((G + w H) c - b), so every learning kernel runs unchanged on
+// G + w H, and the loss the stopping rules read is ||r||^2 + w c^T H c
+// (lb.total, clomp.cpp:126).  k_prior_ext builds the Gram and H rows of the
+// atoms selected this iteration (the learning kernels then find nothing to
+// extend); k_prior_control adds the prior to the residual loss the learning
+// kernels stored and runs the per-signal stopping rules.
+constexpr int kPriorThreads = 128;
+
+__global__ void __launch_bounds__(kPriorThreads)
+k_prior_ext(SolveParams p, Work w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nw = kPriorThreads / 32;
+  const int64_t cap = p.cap;
+  const double inv_n = 1.0 / (double)p.n;
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t b = p.sig_lo + blockIdx.x; b < p.sig_hi; b += gridDim.x) {
+    if (!w.active[b]) continue;
+    const int t = w.cnt[b], t0 = w.gcnt[b];
+    if (t0 >= t) continue;
+    const double wb = w.wtv[b];
+    double* G = w.gram + b * cap * cap;
+    double* H = w.hgram + b * cap * cap;
+    const int32_t* sup = w.sup + b * cap;
+    const float* y = w.y32 + b * p.ldm;
+    for (int k = t0; k < t; ++k) {
+      const int64_t sk = sup[k];
+      const float* ak = w.at32 + sk * p.ldm;
+      const double* dk = w.ddt + sk * w.ldd;
+      for (int i = warp; i <= k; i += nw) {
+        const int64_t si = sup[i];
+        double g = 0.0;
+        if (w.gfull) {
+          g = w.gfull[sk * p.n + si];
+        } else {
+          const float* ai = w.at32 + si * p.ldm;
+          for (int64_t q = lane; q < p.ldm; q += 32) g = fma(f2d(ak[q]), f2d(ai[q]), g);
+          g = warp_sum(g);
+        }
+        const double* di = w.ddt + si * w.ldd;
+        double h = 0.0;
+        for (int64_t q = lane; q < w.ldd; q += 32) h = fma(dk[q], di[q], h);
+        h = warp_sum(h) * inv_n;
+        if (lane == 0) {
+          const double v = g + wb * h;
+          G[(int64_t)k * cap + i] = v;
+          G[(int64_t)i * cap + k] = v;
+          H[(int64_t)k * cap + i] = h;
+          H[(int64_t)i * cap + k] = h;
+        }
+      }
+      if (warp == nw - 1) {
+        double acc = 0.0;
+        for (int64_t q = lane; q < p.ldm; q += 32) acc = fma(f2d(ak[q]), f2d(y[q]), acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          w.bvec[b * cap + k] = acc;
+          w.coef[b * cap + k] = 0.0;  // new atoms start at 0 (clomp.hpp:53-54)
+          w.mom1[b * cap + k] = 0.0;
+          w.mom2[b * cap + k] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) w.gcnt[b] = t;
+  }
+}
+
+// Warp per signal: tv = c^T H c, total = ||r||^2 + w tv, stopping rules and
+// the best snapshot (clomp.cpp:253-273).
+__global__ void __launch_bounds__(128)
+k_prior_control(SolveParams p, Work w, int outer) {
+  const int lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
+  const int64_t b = p.sig_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= p.sig_hi || !w.active[b]) return;
+  const int64_t cap = p.cap;
+  const int t = w.cnt[b];
+  const double* H = w.hgram + b * cap * cap;
+  const double* c = w.coef + b * cap;
+  double acc = 0.0;
+  for (int i = lane; i < t; i += 32) {
+    double row = 0.0;
+    for (int j = 0; j < t; ++j) row = fma(H[(int64_t)j * cap + i], c[j], row);
+    acc = fma(c[i], row, acc);
+  }
+  const double tv = warp_sum(acc);
+  int snap = 0;
+  if (lane == 0) {
+    const double Lr = w.rloss[b];
+    snap = control_signal(p, w, b, outer, Lr + w.wtv[b] * tv, load_ctl(w, b), Lr);
+  }
+  snap = __shfl_sync(kFull, snap, 0);
+  if (snap)
+    for (int i = lane; i < t; i += 32) w.best_coef[b * cap + i] = c[i];
 }
 
 // ------------------------------------------------------ fused small solve
@@ -2138,7 +2258,10 @@ __global__ void k_finalize(SolveParams p, Work w, int64_t out_cap,
     status = w.status[b];
     iters = w.iters[b];
     use_best = !w.conv[b] && isfinite(w.best_L[b]);
-    rn = use_best ? sqrt(w.best_L[b]) : sqrt(w.loss[b]);
+    if (p.prior)  // the losses carry the prior: the residual parts are kept apart
+      rn = use_best ? sqrt(w.best_R[b]) : sqrt(w.rloss[b]);
+    else
+      rn = use_best ? sqrt(w.best_L[b]) : sqrt(w.loss[b]);
   }
   const bool bad = status == kStatusNumerical;
   int t = bad ? 0 : (use_best ? w.best_cnt[b] : w.cnt[b]);
@@ -2336,6 +2459,17 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       default: launch_block_variant<2>(p, w, outer, big_list, grid, skip_le, s); break;
     }
   }
+}
+
+void launch_prior_ext(const SolveParams& p, const Work& w, cudaStream_t s) {
+  const int64_t nsig = p.sig_hi - p.sig_lo;
+  const unsigned grid = (unsigned)std::min<int64_t>(nsig, 4096);
+  launch_pdl(k_prior_ext, dim3(grid), dim3(kPriorThreads), 0, s, p, w);
+}
+
+void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
+  const int64_t nsig = p.sig_hi - p.sig_lo;
+  launch_pdl(k_prior_control, dim3((unsigned)((nsig + 3) / 4)), dim3(128), 0, s, p, w, outer);
 }
 
 void launch_joint_control(const SolveParams& p, const Work& w, int outer,

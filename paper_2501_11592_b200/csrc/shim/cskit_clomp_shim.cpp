@@ -13,8 +13,11 @@
 // * Inputs are rounded to fp32 (the GPU operand precision); results are fp64.
 // * x_hat = basis * (s .* mask) is computed on the host with the reference's
 //   la::matmul, as clomp.cpp:289 does.
-// * Priors (resolved w_tv / w_lv > 0) are not available on the GPU path: the
-//   call throws cskit::ConfigError instead of silently changing the problem.
+// * Priors: setup.basis (n x n) is handed to cl_set_basis, so the TV prior of
+//   single-column solves (clomp_solve, one-column batches: the CLI's 1D path)
+//   runs on the GPU.  Multi-column batches with priors (TV-2D + local
+//   variance) are not available there: the call throws cskit::ConfigError
+//   instead of silently changing the problem.
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -30,7 +33,7 @@ namespace {
 
 struct CachedCtx {
   cl_ctx* ctx = nullptr;
-  uint64_t hash = 0;
+  uint64_t hash = 0, basis_hash = 0;
   std::size_t m = 0, n = 0;
   ~CachedCtx() {
     if (ctx) cl_destroy(ctx);
@@ -61,10 +64,22 @@ uint64_t fnv1a(const double* p, std::size_t count) {
   }
 }
 
+void sync_basis(const cskit::MeasurementSetup& setup) {
+  const bool square = setup.basis.rows == setup.n && setup.basis.cols == setup.n;
+  const uint64_t bh = square ? fnv1a(setup.basis.data(), setup.basis.a.size()) : 0;
+  if (bh == g_cache->basis_hash) return;
+  const int st = cl_set_basis(g_cache->ctx, square ? setup.basis.data() : nullptr,
+                              static_cast<int64_t>(setup.n), CL_LAYOUT_REF);
+  if (st != CL_OK) rethrow(st, cl_last_error(g_cache->ctx));
+  g_cache->basis_hash = bh;
+}
+
 cl_ctx* context_for(const cskit::MeasurementSetup& setup) {
   const uint64_t h = fnv1a(setup.a.data(), setup.a.a.size());
-  if (g_cache && g_cache->hash == h && g_cache->m == setup.m && g_cache->n == setup.n)
+  if (g_cache && g_cache->hash == h && g_cache->m == setup.m && g_cache->n == setup.n) {
+    sync_basis(setup);
     return g_cache->ctx;
+  }
   std::vector<float> a32(setup.a.a.size());
   for (std::size_t i = 0; i < a32.size(); ++i) a32[i] = static_cast<float>(setup.a.a[i]);
   int st = 0;
@@ -76,6 +91,7 @@ cl_ctx* context_for(const cskit::MeasurementSetup& setup) {
   g_cache->hash = h;
   g_cache->m = setup.m;
   g_cache->n = setup.n;
+  sync_basis(setup);
   return ctx;
 }
 

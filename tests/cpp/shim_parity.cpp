@@ -82,6 +82,46 @@ int main() {
                 static_cast<long long>(it), err, xerr, ok ? "ok" : "FAIL");
     failures += ok ? 0 : 1;
   }
+  // The reference's default configuration (Adam, th = 0.7, automatic TV / LV
+  // weights): the TV prior runs on the GPU through the basis the shim hands
+  // over (LV never applies to one column).
+  for (int seed = 1; seed <= 3; ++seed) {
+    MeasurementSetup setup = make_setup(64, 0.5, 200 + seed);
+    setup.a = round32(setup.a);
+    Rng rng(static_cast<uint64_t>(seed + 50));
+    la::Vec x(setup.n, 0.0);
+    for (int k = 0; k < 4; ++k) x[rng.uniform_below(setup.n)] = rng.normal();
+    la::Vec y = la::matvec(setup.a, x);
+    for (double& v : y) v = static_cast<double>(static_cast<float>(v));
+    ClompConfig cfg;  // defaults: priors on
+    cfg.max_outer = 12;
+    const SolveResult got = clomp_solve(setup, y, cfg);
+    orc_config oc{cfg.th, cfg.max_outer, cfg.eps, cfg.inner_steps, cfg.lr, 2, 0, cfg.w_tv,
+                  cfg.w_lv, cfg.lv.window, cfg.lv.stride, cfg.stall_tol, cfg.stall_patience};
+    std::vector<double> s(setup.n);
+    std::vector<uint8_t> mk(setup.n);
+    int64_t it = 0;
+    double rn = 0.0;
+    uint8_t cv = 0;
+    int32_t st = 0;
+    orc_clomp_solve_batch_basis(setup.a.data(), setup.m, setup.n, setup.basis.data(), y.data(),
+                                1, &oc, ORC_ISA_AVX2, ORC_MODE_PER_SIGNAL, s.data(), mk.data(),
+                                &it, &rn, &cv, &st, nullptr, nullptr, 0);
+    double cmax = 0.0, err = 0.0;
+    bool same_mask = true;
+    for (std::size_t j = 0; j < setup.n; ++j) {
+      same_mask = same_mask && (got.s.mask[j] == mk[j]);
+      cmax = std::fmax(cmax, std::fabs(s[j]));
+      err = std::fmax(err, std::fabs(got.s.values[j] - s[j]));
+    }
+    const bool ok = st == 0 && same_mask && got.iterations == static_cast<std::size_t>(it) &&
+                    err <= 1e-9 * std::fmax(cmax, 1.0) &&
+                    std::fabs(got.final_residual_norm - rn) <= 1e-9 * std::fmax(rn, 1e-12);
+    std::printf("default config (priors) seed %d: mask %s iters %zu/%lld coef err %.2e %s\n",
+                seed, same_mask ? "same" : "DIFF", got.iterations, static_cast<long long>(it),
+                err, ok ? "ok" : "FAIL");
+    failures += ok ? 0 : 1;
+  }
   // Error mapping: a diverging lr raises cskit::NumericalError through the shim.
   try {
     MeasurementSetup setup = make_setup(32, 0.5, 7);

@@ -43,3 +43,11 @@ def test_value_law_pm_uniform(built_lib):
     _, X, _, _ = cl.gen_problem_1d(3, 32, 64, 8, 4, value_law=1)
     v = np.abs(X[X != 0])
     assert np.all((v >= 1.0) & (v < 2.0))
+
+
+def test_dct_basis_matches_reference_bit_for_bit(built_lib):
+    """cl_dct_basis restates dct_basis (sensing.cpp:13-29): equal to the
+    reference's own output (tests/golden dct8) and orthonormal."""
+    assert np.array_equal(cl.dct_basis(8), ARR["dct8"])
+    D = cl.dct_basis(64)
+    assert np.allclose(D.T @ D, np.eye(64), atol=1e-13)

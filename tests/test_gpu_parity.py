@@ -64,9 +64,13 @@ def test_solve_matches_reference_golden(case, corr_path):
     if corr_path == "gemv" and Y.shape[1] > 4:
         pytest.skip("the GEMV correlation serves batches of at most 4 signals")
     ctx = make_ctx(A, corr_path)
+    if case.get("basis"):
+        ctx.set_basis(ARR[f"{name}/D"])  # the priors chain through it
     mode = cl.MODE_JOINT if case["api"] == "batch" else cl.MODE_PER_SIGNAL
-    if case["code"] != 0:
-        exc = {2: cl.ConfigError, 3: cl.DimensionError, 4: cl.NumericalError}[case["code"]]
+    code = case.get("gpu_code", case["code"])
+    if code != 0:
+        exc = {2: cl.ConfigError, 3: cl.DimensionError, 4: cl.NumericalError,
+               5: cl.UnsupportedError}[code]
         with pytest.raises(exc):
             cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
         return
@@ -266,3 +270,71 @@ def test_cluster_learning_vs_oracle_and_block_kernel(gpu_available, K, opt):
     assert np.array_equal(r.mask, r0.mask)
     assert np.array_equal(r.iterations, r0.iterations)
     assert rel_coef_err(r.s, r0.s) <= 1e-9
+
+
+def test_priors_default_config_per_signal_vs_oracle(gpu_available):
+    """The reference's default configuration (Adam, th = 0.7, automatic TV / LV
+    weights) on a make_setup-style problem (A = Phi D, DCT synthesis basis),
+    one signal at a time: the TV prior is folded into the support Gram system
+    (k_prior_ext / k_prior_control) and matches the oracle, which is bit-exact
+    with the reference.  Config-2 sizes: N = 1024, M = 512, 32 signals."""
+    n, m, B, k = 1024, 512, 32, 12
+    D = cl.dct_basis(n)
+    rng = np.random.default_rng(5)
+    A = ((rng.standard_normal((m, n)) / np.sqrt(m)) @ D).astype(np.float32)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, k, replace=False), b] = rng.standard_normal(k)
+    Y = (A.astype(np.float64) @ X + 0.003 * rng.standard_normal((m, B))).astype(np.float32)
+    cfg = cl.ClompConfig(max_outer=16)
+    for path in ("tc", "f64"):
+        ctx = make_ctx(A, path)
+        ctx.set_basis(D)
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        assert np.all(r.status == 0)
+        idx = np.arange(0, B, 8)
+        ref = refbind.orc_solve(A.astype(np.float64), Y[:, idx].astype(np.float64), cfg,
+                                mode=refbind.MODE_PER_SIGNAL, basis=D)
+        for q, b in enumerate(idx):
+            assert np.array_equal(r.mask[:, b], ref["mask"][:, q]), f"signal {b}: support"
+            assert r.iterations[b] == ref["iterations"][q]
+            assert rel_coef_err(r.s[:, b], ref["s"][:, q]) <= 1e-7
+            np.testing.assert_allclose(r.final_residual_norm[b], ref["final_residual_norm"][q],
+                                       rtol=1e-7)
+
+
+def test_priors_th1_large_support_cluster_and_block(gpu_available):
+    """TV prior with supports past 32 atoms (cluster and block learning
+    kernels) against the oracle."""
+    n, m, B, K = 512, 256, 3, 48
+    D = cl.dct_basis(n)
+    rng = np.random.default_rng(9)
+    A = ((rng.standard_normal((m, n)) / np.sqrt(m)) @ D).astype(np.float32)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, K, replace=False), b] = rng.standard_normal(K)
+    Y = (A.astype(np.float64) @ X).astype(np.float32)
+    cfg = cl.ClompConfig(th=1.0, opt=cl.PLAIN, lr=0.1, max_outer=K, w_tv=0.5)
+    ref = refbind.orc_solve(A.astype(np.float64), Y.astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL, basis=D)
+    for cluster in (True, False):
+        ctx = make_ctx(A, "tc")
+        ctx.set_basis(D)
+        ctx.set_cluster_learn(cluster)
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        assert np.array_equal(r.mask, ref["mask"])
+        assert np.array_equal(r.iterations, ref["iterations"])
+        assert rel_coef_err(r.s, ref["s"]) <= 1e-7
+
+
+def test_priors_rejected_where_not_implemented(gpu_available):
+    A = ARR["prior_joint_b3_tv2d/A"]
+    Y = ARR["prior_joint_b3_tv2d/Y"]
+    ctx = make_ctx(A)
+    with pytest.raises(cl.UnsupportedError):  # no basis
+        cl.clomp_solve_batch(ctx, Y[:, :1], cl.ClompConfig(max_outer=3))
+    ctx.set_basis(ARR["prior_joint_b3_tv2d/D"])
+    with pytest.raises(cl.UnsupportedError):  # multi-column joint: TV-2D + LV
+        cl.clomp_solve_batch(ctx, Y, cl.ClompConfig(max_outer=3), mode=cl.MODE_JOINT)
+    r = cl.clomp_solve_batch(ctx, Y, cl.ClompConfig(max_outer=3), mode=cl.MODE_PER_SIGNAL)
+    assert np.all(r.status == 0)
