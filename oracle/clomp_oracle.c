@@ -7,9 +7,9 @@
  * What it restates, with the reference lines it follows:
  *   validate                 clomp.cpp:18-30
  *   inject_from_scores       clomp.cpp:41-53   (select_support twin, solvers.cpp:68-80)
- *   loss_impl                clomp.cpp:74-127 (priors: TV-1D on single-column
- *                            solves, the only prior a column of clomp_solve sees)
- *   tv_1d                    priors.cpp:11-26
+ *   loss_impl                clomp.cpp:74-127 (with the priors)
+ *   tv_1d / tv_2d            priors.cpp:11-26 / 28-59
+ *   local_variance           priors.cpp:61-116
  *   resolve_weights          clomp.cpp:131-140
  *   gradient_step            clomp.cpp:171-209
  *   clomp_solve_batch        clomp.cpp:211-292
@@ -162,6 +162,11 @@ typedef struct {
   const double* basis;
   const double* dt;
   double w_tv;
+  /* local variance (priors.cpp:74-116), evaluated when w_lv > 0 and the batch
+   * fits the window (clomp.cpp:93) */
+  double w_lv;
+  int lv_on;
+  int64_t lv_window, lv_stride;
 } problem_t;
 
 static inline double entry(const problem_t* p, int64_t q, int64_t j) {
@@ -187,18 +192,19 @@ static void residual(const problem_t* p, const double* s, const support_t* sup,
   }
 }
 
-/* x = basis * s_eff (clomp.cpp:95) for a single column, support-restricted
- * like residual() (exact zeros add nothing to the sequential sums). */
+/* x = basis * s_eff (clomp.cpp:95), n x B row-major, support-restricted like
+ * residual() (exact zeros add nothing to the sequential sums). */
 static void synth(const problem_t* p, const double* s, const support_t* sup, double* x) {
-  const int64_t n = p->n;
-  for (int64_t i = 0; i < n; ++i) {
-    double acc = 0.0;
-    for (int64_t q = 0; q < sup[0].count; ++q) {
-      const int64_t j = sup[0].idx[q];
-      acc = mac(acc, p->basis[i * n + j], s[j], p->isa);
+  const int64_t n = p->n, B = p->batch;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t b = 0; b < B; ++b) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < sup[b].count; ++q) {
+        const int64_t j = sup[b].idx[q];
+        acc = mac(acc, p->basis[i * n + j], s[j * B + b], p->isa);
+      }
+      x[i * B + b] = acc;
     }
-    x[i] = acc;
-  }
 }
 
 /* tv_1d (priors.cpp:11-26): mean squared forward difference and its gradient. */
@@ -219,24 +225,125 @@ static double tv_1d(const double* x, int64_t n, double* grad) {
   return acc * inv_n;
 }
 
-/* The TV-1D part of loss_impl (clomp.cpp:93-119) for a single column: returns
- * tv; with g != NULL adds the chained gradient D^T (w_tv * dtv/dx) to g on the
- * support (clomp.cpp:100-102, 114-117).  x, gv, gx: n-entry scratch. */
-static double prior_tv(const problem_t* p, const double* s, const support_t* sup, double* g,
-                       double* x, double* gv, double* gx) {
-  const int64_t n = p->n;
+/* tv_2d (priors.cpp:28-59) of an h x w image (row-major): vertical and
+ * horizontal squared differences, each averaged over its own extent. */
+static double tv_2d(const double* x, int64_t h, int64_t w, double* grad) {
+  if (grad)
+    for (int64_t e = 0; e < h * w; ++e) grad[e] = 0.0;
+  double acc = 0.0;
+  if (h >= 2) {
+    const double inv_h = 1.0 / (double)h;
+    for (int64_t i = 0; i + 1 < h; ++i)
+      for (int64_t j = 0; j < w; ++j) {
+        const double d = x[i * w + j] - x[(i + 1) * w + j];
+        acc += inv_h * d * d;
+        if (grad) {
+          grad[i * w + j] += 2.0 * inv_h * d;
+          grad[(i + 1) * w + j] -= 2.0 * inv_h * d;
+        }
+      }
+  }
+  if (w >= 2) {
+    const double inv_w = 1.0 / (double)w;
+    for (int64_t i = 0; i < h; ++i)
+      for (int64_t j = 0; j + 1 < w; ++j) {
+        const double d = x[i * w + j] - x[i * w + j + 1];
+        acc += inv_w * d * d;
+        if (grad) {
+          grad[i * w + j] += 2.0 * inv_w * d;
+          grad[i * w + j + 1] -= 2.0 * inv_w * d;
+        }
+      }
+  }
+  return acc;
+}
+
+/* Window origins along one axis (priors.cpp:63-70): every stride, plus the
+ * last full window if the stride missed it. */
+static int64_t block_starts(int64_t dim, int64_t window, int64_t stride, int64_t* out) {
+  int64_t cnt = 0;
+  for (int64_t s0 = 0; s0 + window <= dim; s0 += stride) out[cnt++] = s0;
+  const int64_t last = dim - window;
+  if (cnt == 0 || out[cnt - 1] != last) out[cnt++] = last;
+  return cnt;
+}
+
+/* local_variance (priors.cpp:74-116): mean over windows of the standard
+ * deviation, with its gradient.  Parameters are validated by the caller. */
+static double local_variance(const double* x, int64_t h, int64_t w, int64_t window,
+                             int64_t stride, double* grad) {
+  if (grad)
+    for (int64_t e = 0; e < h * w; ++e) grad[e] = 0.0;
+  int64_t* rows = malloc((size_t)(h + 2) * sizeof(int64_t));
+  int64_t* cols = malloc((size_t)(w + 2) * sizeof(int64_t));
+  const int64_t nr = block_starts(h, window, stride, rows);
+  const int64_t nc = block_starts(w, window, stride, cols);
+  const double count = (double)(window * window);
+  const double inv_blocks = 1.0 / (double)(nr * nc);
+  double acc = 0.0;
+  for (int64_t a = 0; a < nr; ++a)
+    for (int64_t bb = 0; bb < nc; ++bb) {
+      const int64_t r0 = rows[a], c0 = cols[bb];
+      double sum = 0.0, sum_sq = 0.0;
+      for (int64_t i = 0; i < window; ++i)
+        for (int64_t j = 0; j < window; ++j) {
+          const double v = x[(r0 + i) * w + c0 + j];
+          sum += v;
+          sum_sq += v * v;
+        }
+      const double mean = sum / count;
+      double var = sum_sq / count - mean * mean;
+      if (var < 0.0) var = 0.0; /* std::max(var, 0.0) */
+      const double sd = sqrt(var);
+      acc += inv_blocks * sd;
+      if (grad && sd > 0.0) {
+        const double scale = inv_blocks / (count * sd);
+        for (int64_t i = 0; i < window; ++i)
+          for (int64_t j = 0; j < window; ++j)
+            grad[(r0 + i) * w + c0 + j] += scale * (x[(r0 + i) * w + c0 + j] - mean);
+      }
+    }
+  free(rows);
+  free(cols);
+  return acc;
+}
+
+/* The prior part of loss_impl (clomp.cpp:93-119): returns w_tv tv + w_lv lv
+ * as the reference adds it to lb.total (tv, lv returned through *tv, *lv);
+ * with g != NULL adds the chained gradient D^T gx to g on the supports.
+ * x, gv, gx: n x B scratch each. */
+static void prior_eval(const problem_t* p, const double* s, const support_t* sup, double* g,
+                       double* x, double* gv, double* gx, double* tv, double* lv) {
+  const int64_t n = p->n, B = p->batch, nb = n * B;
   synth(p, s, sup, x);
-  const double tv = tv_1d(x, n, g ? gv : NULL);
-  if (g) {
-    for (int64_t i = 0; i < n; ++i) gx[i] = 0.0 + p->w_tv * gv[i];
-    for (int64_t q = 0; q < sup[0].count; ++q) {
-      const int64_t j = sup[0].idx[q];
-      double acc = 0.0;
-      for (int64_t i = 0; i < n; ++i) acc = mac(acc, p->dt[j * n + i], gx[i], p->isa);
-      g[j] += acc;
+  if (g)
+    for (int64_t e = 0; e < nb; ++e) gx[e] = 0.0;
+  *tv = 0.0;
+  *lv = 0.0;
+  if (p->w_tv > 0.0) {
+    if (B == 1) {
+      *tv = tv_1d(x, n, g ? gv : NULL);
+      if (g)
+        for (int64_t i = 0; i < n; ++i) gx[i] += p->w_tv * gv[i]; /* clomp.cpp:101 */
+    } else {
+      *tv = tv_2d(x, n, B, g ? gv : NULL);
+      if (g) /* kern::axpy (kernels_avx2.cpp:80-92: FMA; scalar: mul + add) */
+        for (int64_t e = 0; e < nb; ++e) gx[e] = mac(gx[e], p->w_tv, gv[e], p->isa);
     }
   }
-  return tv;
+  if (p->lv_on) {
+    *lv = local_variance(x, n, B, p->lv_window, p->lv_stride, g ? gv : NULL);
+    if (g)
+      for (int64_t e = 0; e < nb; ++e) gx[e] = mac(gx[e], p->w_lv, gv[e], p->isa);
+  }
+  if (g) /* chain = matmul(dt, gx) (clomp.cpp:114-117) on the supports */
+    for (int64_t b = 0; b < B; ++b)
+      for (int64_t q = 0; q < sup[b].count; ++q) {
+        const int64_t j = sup[b].idx[q];
+        double acc = 0.0;
+        for (int64_t i = 0; i < n; ++i) acc = mac(acc, p->dt[j * n + i], gx[i * B + b], p->isa);
+        g[j * B + b] += acc;
+      }
 }
 
 /* (A^T r)[j, b] for one atom j: la::matmul(ops.at, r) element (clomp.cpp:89, 245). */
@@ -364,8 +471,9 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
     sup[b].idx = sup_mem + b * n;
     best_sup[b].idx = sup_mem + nb + b * n;
   }
-  const int prior = p->w_tv > 0.0;  /* single-column solves only (solve_driver) */
-  double* px = prior ? calloc((size_t)(3 * n), sizeof(double)) : NULL;
+  const int prior = p->w_tv > 0.0 || p->lv_on;
+  double* px = prior ? calloc((size_t)(3 * nb), sizeof(double)) : NULL;
+  double tvv = 0.0, lvv = 0.0;
   uint64_t adam_steps = 0;
   double best_loss = INFINITY, prev_loss = INFINITY;
   uint64_t stall = 0;
@@ -391,13 +499,15 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
           const int64_t j = sup[b].idx[q];
           g[j * B + b] = corr(p, r, j, b) * 2.0;
         }
-      if (prior) prior_tv(p, s, sup, g, px, px + n, px + 2 * n);
+      if (prior) prior_eval(p, s, sup, g, px, px + nb, px + 2 * nb, &tvv, &lvv);
       step_support(s, m1, m2, g, sup, B, c, &adam_steps);
     }
     residual(p, s, sup, y, r);
     double loss = sum_sq(r, mb, p->isa);
-    if (prior) /* lb.total = residual + w_tv tv (+ w_lv * 0: no LV on one column) */
-      loss = loss + p->w_tv * prior_tv(p, s, sup, NULL, px, NULL, NULL);
+    if (prior) { /* lb.total = residual + w_tv tv + w_lv lv (clomp.cpp:126) */
+      prior_eval(p, s, sup, NULL, px, NULL, NULL, &tvv, &lvv);
+      loss = loss + p->w_tv * tvv + p->w_lv * lvv;
+    }
     if (!isfinite(loss)) {
       set_err(err, errlen, "clomp: loss diverged; reduce lr");
       status = ORC_ERR_NUMERICAL;
@@ -462,29 +572,36 @@ static double* transpose(const double* a, int64_t m, int64_t n) {
 }
 
 /* Which priors loss_impl evaluates for this solve (clomp.cpp:93-119): TV-1D
- * on single-column solves (clomp_solve, or a one-column batch); local
- * variance only when batch >= window (never for one column, except the
- * window < 2 configuration error local_variance raises, priors.cpp:77-79).
- * TV-2D / LV on multi-column batches are not restated. */
+ * on one column, TV-2D on a multi-column batch, local variance when the batch
+ * and n fit its window, with local_variance's parameter checks
+ * (priors.cpp:77-84), which the reference raises at its first loss
+ * evaluation (reported here before the solve). */
 static int prior_setup(problem_t* p, const orc_config* c, double w_tv, double w_lv,
                        int64_t batch, char* err, int errlen) {
   p->w_tv = 0.0;
+  p->w_lv = 0.0;
+  p->lv_on = 0;
   const int lv_fits = batch >= (int64_t)c->lv_window && p->n >= (int64_t)c->lv_window;
   if (!(w_tv > 0.0) && !(w_lv > 0.0 && lv_fits)) return ORC_OK;
-  if (batch > 1) {
-    set_err(err, errlen, "clomp oracle: TV-2D / local-variance priors on multi-column "
-                         "batches are not restated");
-    return ORC_ERR_UNSUPPORTED;
-  }
-  if (w_lv > 0.0 && lv_fits) {
-    set_err(err, errlen, "local_variance: window must be >= 2");
-    return ORC_ERR_CONFIG;
-  }
   if (!p->basis) {
     set_err(err, errlen, "clomp oracle: priors need the synthesis basis");
     return ORC_ERR_UNSUPPORTED;
   }
-  p->w_tv = w_tv;
+  if (w_lv > 0.0 && lv_fits) {
+    if (c->lv_window < 2) {
+      set_err(err, errlen, "local_variance: window must be >= 2");
+      return ORC_ERR_CONFIG;
+    }
+    if (c->lv_stride < 1 || c->lv_stride >= c->lv_window) {
+      set_err(err, errlen, "local_variance: stride must be in [1, window)");
+      return ORC_ERR_CONFIG;
+    }
+    p->lv_on = 1;
+    p->w_lv = w_lv;
+    p->lv_window = (int64_t)c->lv_window;
+    p->lv_stride = (int64_t)c->lv_stride;
+  }
+  p->w_tv = w_tv > 0.0 ? w_tv : 0.0;
   return ORC_OK;
 }
 
@@ -577,7 +694,7 @@ int orc_clomp_solve_batch_basis(const double* a, int64_t m, int64_t n,
   }
   double* at = transpose(a, m, n);
   double* dt = basis ? transpose(basis, n, n) : NULL;
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, basis, dt, 0.0};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, basis, dt, 0.0, 0.0, 0, 0, 0};
   const int st = solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations,
                               final_rn, converged, status, trace, err, errlen);
   free(at);
@@ -604,7 +721,7 @@ int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
                         int64_t* iterations, double* final_rn, uint8_t* converged,
                         int32_t* status, double* trace, char* err, int errlen) {
   problem_t p = {NULL, NULL, mr * mc, nr * nc, batch, isa, ar, ac, mr, nr, mc, nc,
-                 NULL, NULL, 0.0};
+                 NULL, NULL, 0.0, 0.0, 0, 0, 0};
   return solve_driver(p, y, batch, cfg, mode, s_out, mask_out, iterations, final_rn,
                       converged, status, trace, err, errlen);
 }
@@ -615,7 +732,7 @@ int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
                        int64_t batch, double th, int isa, uint8_t* mask) {
   if (!(th > 0.0) || th > 1.0) return ORC_ERR_CONFIG;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0, 0.0, 0, 0, 0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {
@@ -639,7 +756,7 @@ int orc_clomp_loss(const double* a, int64_t m, int64_t n, const double* y,
   resolve_weights(cfg, y, m * batch, isa, &w_tv, &w_lv);
   if (w_tv > 0.0 || w_lv > 0.0) return ORC_ERR_UNSUPPORTED;
   double* at = transpose(a, m, n);
-  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0};
+  problem_t p = {a, at, m, n, batch, isa, NULL, NULL, 0, 0, 0, 0, NULL, NULL, 0.0, 0.0, 0, 0, 0};
   support_t* sup = calloc((size_t)batch, sizeof(support_t));
   int64_t* mem = calloc((size_t)(n * batch), sizeof(int64_t));
   for (int64_t b = 0; b < batch; ++b) {

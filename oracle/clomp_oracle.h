@@ -43,7 +43,7 @@ enum {
   ORC_ERR_CONFIG = 2,      /* cskit::ConfigError    (errors.hpp:22) */
   ORC_ERR_DIMENSION = 3,   /* cskit::DimensionError (errors.hpp:16) */
   ORC_ERR_NUMERICAL = 4,   /* cskit::NumericalError (errors.hpp:28) */
-  ORC_ERR_UNSUPPORTED = 5  /* multi-column priors (TV-2D / LV), or priors without a basis */
+  ORC_ERR_UNSUPPORTED = 5  /* priors without a synthesis basis */
 };
 
 /* Kernel semantics to reproduce: 1 = kernels_avx2.cpp (FMA), 0 = kernels_scalar.cpp. */
@@ -74,8 +74,9 @@ int orc_clomp_solve_batch(const double* a, int64_t m, int64_t n,
                           char* err, int errlen);
 
 /* Same with the synthesis basis D (n x n row-major, x = D s; NULL = none), which
- * the priors need: TV-1D (priors.cpp:11-26) chained through D^T on
- * single-column solves (PER_SIGNAL, or JOINT with one column). */
+ * the priors need (clomp.cpp:93-119): TV-1D (priors.cpp:11-26) on one column,
+ * TV-2D (priors.cpp:28-59) and local variance (priors.cpp:74-116) on a
+ * multi-column batch, chained through D^T. */
 int orc_clomp_solve_batch_basis(const double* a, int64_t m, int64_t n,
                                 const double* basis, const double* y, int64_t batch,
                                 const orc_config* cfg, int isa, int mode,

@@ -31,9 +31,8 @@ def test_oracle_matches_reference_golden(case):
     mode = refbind.MODE_JOINT if case["api"] == "batch" else refbind.MODE_PER_SIGNAL
     D = ARR[f"{name}/D"] if case.get("basis") else None
     r = refbind.orc_solve(A, Y, _cfg(case["cfg"]), mode=mode, basis=D)
-    code = case.get("gpu_code", case["code"])  # multi-column priors: not restated
-    assert r["code"] == code, r["err"]
-    if code != 0:
+    assert r["code"] == case["code"], r["err"]
+    if case["code"] != 0:
         return
     assert np.array_equal(r["mask"], ARR[f"{name}/mask"])
     assert np.array_equal(r["s"], ARR[f"{name}/s"])  # bit-exact
@@ -74,16 +73,12 @@ def test_wrapper_equals_one_column_batch():
         assert np.array_equal(one[k], bat[k])
 
 
-def test_priors_are_rejected_not_faked():
-    """Priors need the synthesis basis; multi-column priors (TV-2D / LV) are
-    not restated and say so instead of running something else."""
+def test_priors_need_the_basis():
+    """Priors chain through the synthesis basis; without one the oracle says
+    so instead of running something else."""
     A = ARR["small_th1_plain_b1/A"].astype(np.float64)
     Y = ARR["small_th1_plain_b1/Y"].astype(np.float64)
     r = refbind.orc_solve(A, Y, ClompConfig())  # defaults: auto priors on, no basis
-    assert r["code"] == 5
-    D = ARR["prior_joint_b3_tv2d/D"]
-    r = refbind.orc_solve(ARR["prior_joint_b3_tv2d/A"], ARR["prior_joint_b3_tv2d/Y"],
-                          ClompConfig(max_outer=3), mode=refbind.MODE_JOINT, basis=D)
     assert r["code"] == 5
 
 
@@ -129,6 +124,43 @@ def test_oracle_priors_match_live_reference(isa, opt, w_tv):
             assert ref["final_residual_norm"] == orc["final_residual_norm"][b]
     finally:
         refbind.ref().ref_force_isa(refbind.ISA_AVX2)
+
+
+@pytest.mark.skipif(not refbind.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("isa", [refbind.ISA_AVX2, refbind.ISA_SCALAR])
+@pytest.mark.parametrize("cfgd", [dict(max_outer=8),  # defaults: TV-2D + LV, Adam, th 0.7
+                                  dict(th=1.0, opt=PLAIN, lr=0.05, max_outer=6, w_tv=0.05, w_lv=0.0),
+                                  dict(opt=MOMENTUM, lr=0.02, max_outer=6, w_tv=0.0, w_lv=0.1),
+                                  dict(max_outer=5, lv_window=4, lv_stride=3),
+                                  dict(max_outer=5, lv_stride=3)],  # ConfigError
+                         ids=["default", "tv2d_plain", "lv_momentum", "lv_w4s3", "bad_stride"])
+def test_oracle_image_mode_priors_match_live_reference(isa, cfgd):
+    """The reference's column-batch image mode (clomp_solve_batch on many
+    columns, cskit.cpp:620-652): TV-2D (priors.cpp:28-59) and local variance
+    (priors.cpp:74-116) on x = D S, joint stopping — bit for bit, both ISAs."""
+    rng = np.random.default_rng(300 + isa)
+    n, m, B, k = 48, 24, 7, 4
+    D = np.zeros((n, n))
+    refbind.ref().ref_dct_basis(n, refbind._p(D))
+    A = (rng.standard_normal((m, n)) / np.sqrt(m) @ D).astype(np.float32).astype(np.float64)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, k, replace=False), b] = rng.standard_normal(k)
+    Y = (A @ X + 0.01 * rng.standard_normal((m, B))).astype(np.float32).astype(np.float64)
+    cfg = ClompConfig(**cfgd)
+    assert refbind.ref().ref_force_isa(isa) == 0
+    try:
+        ref = refbind.ref_solve_batch(A, Y, cfg, basis=D)
+        orc = refbind.orc_solve(A, Y, cfg, mode=refbind.MODE_JOINT, isa=isa, basis=D)
+    finally:
+        refbind.ref().ref_force_isa(refbind.ISA_AVX2)
+    assert ref["code"] == orc["code"], orc["err"]
+    if ref["code"]:
+        return
+    assert np.array_equal(ref["s"], orc["s"])
+    assert np.array_equal(ref["mask"], orc["mask"])
+    assert ref["iterations"] == orc["iterations"][0]
+    assert ref["final_residual_norm"] == orc["final_residual_norm"][0]
 
 
 @pytest.mark.skipif(not refbind.ref_available(), reason="oracle/_ref not built")

@@ -1,6 +1,6 @@
 # Every BASELINE config through bench.py (ours + reference arm) -> gpurun_out/cfg_*.json
 mkdir -p gpurun_out
-for c in 1 2 3 4 5 6; do
+for c in 1 2 3 4 5 6 7; do
   extra=""
   case $c in 6) extra="--max-outer 16";; esac
   python bench.py --config $c --steps 3 --warmup 3 $extra 2>&1 | tail -1 > gpurun_out/cfg_${c}.json
