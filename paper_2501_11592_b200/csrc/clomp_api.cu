@@ -76,7 +76,17 @@ struct cl_ctx {
   // ddt[j][q] = D[q][j] - D[q+1][j] (q < n - 1), fp64, row stride ldd
   double* ddt = nullptr;
   int64_t ldd = 0;
+  double* dt = nullptr;         // the basis atom-major (dt[k][q] = D[q][k]), image mode
   std::vector<double> prior_w;  // this call's per-signal TV weights (empty: off)
+  // this call's image-mode priors (multi-column joint batch): batch-global
+  // weights and the local-variance window layout
+  bool img = false;
+  double img_wtv = 0.0, img_wlv = 0.0;
+  bool img_lv = false;
+  int img_window = 0, img_stride = 0;
+  std::vector<int32_t> lv_rows, lv_cols, lv_rowcov, lv_colcov;
+  int32_t* lv_tab = nullptr;  // device copy of the four tables
+  size_t lv_tab_bytes = 0;
   // separable 2D contexts (cl_create_sep)
   bool sep = false;
   int64_t mr = 0, nr = 0, mc = 0, nc = 0, ldr = 0, ldc = 0;
@@ -194,7 +204,8 @@ int64_t support_cap(const cl_ctx* ctx, const cl_config* c) {
 
 // Carve the workspace for (B, cap); reallocate only when it grows.
 int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
-                     bool need_split, int64_t ntile, bool need_prior = false) {
+                     bool need_split, int64_t ntile, bool need_prior = false,
+                     bool need_image = false) {
   const int64_t ldm = ctx->ldm;
   const int64_t mwords = (ctx->n + 31) / 32;
   auto carve = [&](Carver& cv, Work& w) {
@@ -243,6 +254,16 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
       w.rloss = cv.take<double>(B);
       w.best_R = cv.take<double>(B);
     }
+    if (need_image) {
+      const int64_t nwin = (int64_t)ctx->lv_rows.size() * (int64_t)ctx->lv_cols.size();
+      w.img_x = cv.take<double>(B * ctx->n);
+      w.img_gx = cv.take<double>(B * ctx->n);
+      w.img_gd = cv.take<double>(B * cap);
+      w.lv_mean = cv.take<double>(std::max<int64_t>(nwin, 1));
+      w.lv_scale = cv.take<double>(std::max<int64_t>(nwin, 1));
+      w.lv_sd = cv.take<double>(std::max<int64_t>(nwin, 1));
+      w.img_part = cv.take<double>(1024);
+    }
   };
   Carver probe{nullptr};
   Work tmp;
@@ -271,6 +292,14 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
   w.gc = ctx->gc;
   w.ddt = need_prior ? ctx->ddt : nullptr;
   w.ldd = ctx->ldd;
+  if (need_image) {
+    w.dt = ctx->dt;
+    const int32_t* t = ctx->lv_tab;
+    w.lv_rows = t;
+    w.lv_cols = t + ctx->lv_rows.size();
+    w.lv_rowcov = w.lv_cols + ctx->lv_cols.size();
+    w.lv_colcov = w.lv_rowcov + ctx->lv_rowcov.size();
+  }
   ctx->w = w;
   return CL_OK;
 }
@@ -366,7 +395,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                 "supported (lower max_outer, or th < 1 with n > 2048)");
   // Latency path: the whole solve in one persistent block per signal when the
   // dictionary is small (config 1) and supports stay register-resident.
-  const bool prior = !ctx->prior_w.empty();
+  const bool image = ctx->img;
+  const bool prior = !ctx->prior_w.empty() || image;
   const bool fused = ctx->fused_ok && !ctx->sep && !colshard && !prior &&
                      (mode == CL_MODE_PER_SIGNAL || B == 1) &&
                      cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
@@ -374,9 +404,25 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   const int64_t tile_atoms =
       tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
-  int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile, prior);
+  if (image) {  // local-variance window tables -> device
+    const size_t cnt = ctx->lv_rows.size() + ctx->lv_cols.size() + ctx->lv_rowcov.size() +
+                       ctx->lv_colcov.size();
+    if (cnt * 4 > ctx->lv_tab_bytes) {
+      cudaFree(ctx->lv_tab);
+      ctx->lv_tab = nullptr;
+      CL_CUDA(ctx, cudaMalloc(&ctx->lv_tab, std::max<size_t>(cnt, 1) * 4));
+      ctx->lv_tab_bytes = std::max<size_t>(cnt, 1) * 4;
+    }
+    std::vector<int32_t> all;
+    for (auto* v : {&ctx->lv_rows, &ctx->lv_cols, &ctx->lv_rowcov, &ctx->lv_colcov})
+      all.insert(all.end(), v->begin(), v->end());
+    if (!all.empty())
+      CL_CUDA(ctx, cudaMemcpy(ctx->lv_tab, all.data(), all.size() * 4, cudaMemcpyHostToDevice));
+  }
+  int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile,
+                            prior && !image, image);
   if (st) return st;
-  if (prior)
+  if (prior && !image)
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->w.wtv, ctx->prior_w.data(), (size_t)B * sizeof(double),
                                  cudaMemcpyHostToDevice, ctx->stream));
   st = ensure_adam_tables(ctx, c);
@@ -414,8 +460,15 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.max_outer = (int32_t)c->max_outer;
   // A one-column joint solve is exactly clomp_solve (clomp.cpp:294-311), so
   // the fused path runs everything with per-signal state.
-  p.mode = (fused || (prior && B == 1)) ? CL_MODE_PER_SIGNAL : mode;
-  p.prior = prior ? 1 : 0;
+  p.mode = (fused || (prior && !image && B == 1)) ? CL_MODE_PER_SIGNAL : mode;
+  p.prior = image ? 2 : prior ? 1 : 0;
+  p.w_tv_g = ctx->img_wtv;
+  p.w_lv_g = ctx->img_wlv;
+  p.lv_on = image && ctx->img_lv ? 1 : 0;
+  p.lv_window = ctx->img_window;
+  p.lv_stride = ctx->img_stride;
+  p.lv_nr = (int32_t)ctx->lv_rows.size();
+  p.lv_nc = (int32_t)ctx->lv_cols.size();
   p.bc1 = ctx->bc;
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
   p.delta_rel = delta_for(tensor, ctx->ldm);
@@ -506,9 +559,14 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     if (!p.fuse_select) launch_select(p, w, full_scores, s);
     if (p.prior) launch_prior_ext(p, w, s);
     const int bound = c->th >= 1.0 ? outer : (int)cap;
-    launch_learn(p, w, outer, bound, s);
-    if (p.prior) launch_prior_control(p, w, outer, s);
-    *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
+    if (p.prior == 2) {  // image mode: coupled epochs, residual, prior loss
+      launch_image_learn(p, w, outer, s);
+      *launches += 2 + (int64_t)p.inner * (p.lv_on ? 4 : 3) + 3 + p.lv_on;
+    } else {
+      launch_learn(p, w, outer, bound, s);
+      if (p.prior) launch_prior_control(p, w, outer, s);
+      *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
+    }
     if (mode == CL_MODE_JOINT) {
       launch_joint_control(p, w, outer, false, s);
       launch_joint_snapshot(p, w, s);
@@ -580,8 +638,12 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         if (!p.fuse_select) launch_select(p, w, full_scores, s);
         if (p.prior) launch_prior_ext(p, w, s);
         cudaEventRecord(e[2], s);
-        launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
-        if (p.prior) launch_prior_control(p, w, o, s);
+        if (p.prior == 2) {
+          launch_image_learn(p, w, o, s);
+        } else {
+          launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
+          if (p.prior) launch_prior_control(p, w, o, s);
+        }
         launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
         if (mode == CL_MODE_JOINT) {
           launch_joint_control(p, w, o, false, s);
@@ -942,6 +1004,8 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->gfull);
   cudaFree(ctx->ddt);
+  cudaFree(ctx->dt);
+  cudaFree(ctx->lv_tab);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);
@@ -974,6 +1038,8 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->at_lo);
   cudaFree(ctx->gfull);
   cudaFree(ctx->ddt);
+  cudaFree(ctx->dt);
+  cudaFree(ctx->lv_tab);
   cudaFree(ctx->at_r32);
   cudaFree(ctx->at_c32);
   cudaFree(ctx->at_r64);
@@ -1064,7 +1130,9 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
   if (layout != CL_LAYOUT_REF && layout != CL_LAYOUT_T)
     return fail(ctx, CL_ERR_CONFIG, "cl_set_basis: unknown layout");
   cudaFree(ctx->ddt);
+  cudaFree(ctx->dt);
   ctx->ddt = nullptr;
+  ctx->dt = nullptr;
   ctx->ldd = 0;
   if (!basis) return CL_OK;  // cleared
   if (n != ctx->n)
@@ -1083,6 +1151,13 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
   CL_CUDA(ctx, cudaMalloc(&ctx->ddt, h.size() * sizeof(double)));
   CL_CUDA(ctx, cudaMemcpy(ctx->ddt, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
   ctx->ldd = ldd;
+  // the basis itself, atom-major (synthesis x = D s and the chain D^T gx of
+  // the image mode)
+  h.assign((size_t)(n * n), 0.0);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t q = 0; q < n; ++q) h[(size_t)(k * n + q)] = at(q, k);
+  CL_CUDA(ctx, cudaMalloc(&ctx->dt, h.size() * sizeof(double)));
+  CL_CUDA(ctx, cudaMemcpy(ctx->dt, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
   return CL_OK;
 }
 
@@ -1116,11 +1191,79 @@ int cl_synchronize(cl_ctx* ctx) {
 // batch — folded into the support Gram system (k_prior_ext).  Multi-column
 // joint batches (TV-2D + local variance) and separable contexts are
 // rejected.  col_ms: mean(y^2) per column (automatic weights).
+// block_starts (priors.cpp:63-70): window origins along one axis.
+static std::vector<int32_t> block_starts(int64_t dim, int64_t window, int64_t stride) {
+  std::vector<int32_t> v;
+  for (int64_t s = 0; s + window <= dim; s += stride) v.push_back((int32_t)s);
+  const int64_t last = dim - window;
+  if (v.empty() || v.back() != last) v.push_back((int32_t)last);
+  return v;
+}
+
+// Image mode: the priors of a multi-column joint batch (TV-2D + local
+// variance on x = D S, batch-global weights; clomp.cpp:93-119, 131-140).
+static int setup_image_mode(cl_ctx* ctx, int64_t batch, const cl_config* cfg, double mean_sq,
+                            bool have_ms) {
+  if (ctx->sep)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: priors on separable contexts are not implemented");
+  if (ctx->world > 1 || ctx->vshards > 1)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: priors on column-sharded contexts are not implemented");
+  if (!ctx->dt)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: the priors need the synthesis basis (cl_set_basis)");
+  if ((cfg->w_tv < 0.0 || cfg->w_lv < 0.0) && !have_ms)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_solve_batch_device: automatic prior weights need y on the host; pass "
+                "explicit w_tv / w_lv");
+  const double auto_w = 0.01 * mean_sq;
+  const double w_tv = cfg->w_tv < 0.0 ? auto_w : cfg->w_tv;
+  const double w_lv = cfg->w_lv < 0.0 ? auto_w : cfg->w_lv;
+  const int64_t n = ctx->n, W = (int64_t)cfg->lv_window;
+  const bool lv_on = w_lv > 0.0 && batch >= W && n >= W;
+  ctx->lv_rows.clear();
+  ctx->lv_cols.clear();
+  ctx->lv_rowcov.clear();
+  ctx->lv_colcov.clear();
+  if (lv_on) {  // local_variance's own checks (priors.cpp:77-84)
+    if (W < 2) return fail(ctx, CL_ERR_CONFIG, "local_variance: window must be >= 2");
+    if (cfg->lv_stride < 1 || cfg->lv_stride >= cfg->lv_window)
+      return fail(ctx, CL_ERR_CONFIG, "local_variance: stride must be in [1, window)");
+    ctx->lv_rows = block_starts(n, W, (int64_t)cfg->lv_stride);
+    ctx->lv_cols = block_starts(batch, W, (int64_t)cfg->lv_stride);
+    auto cover = [&](const std::vector<int32_t>& starts, int64_t dim, std::vector<int32_t>& cov) {
+      cov.assign((size_t)(dim * kLvCover), -1);
+      for (size_t wi = 0; wi < starts.size(); ++wi)
+        for (int64_t q = starts[wi]; q < starts[wi] + W; ++q) {
+          int32_t* c = &cov[(size_t)(q * kLvCover)];
+          int a = 0;
+          while (a < kLvCover && c[a] >= 0) ++a;
+          if (a == kLvCover) return false;
+          c[a] = (int32_t)wi;
+        }
+      return true;
+    };
+    if (!cover(ctx->lv_rows, n, ctx->lv_rowcov) || !cover(ctx->lv_cols, batch, ctx->lv_colcov))
+      return fail(ctx, CL_ERR_UNSUPPORTED,
+                  "local_variance: more than 8 windows cover one pixel (window / stride)");
+  }
+  ctx->img = true;
+  ctx->img_wtv = w_tv > 0.0 ? w_tv : 0.0;
+  ctx->img_wlv = lv_on ? w_lv : 0.0;
+  ctx->img_lv = lv_on;
+  ctx->img_window = (int)W;
+  ctx->img_stride = (int)cfg->lv_stride;
+  return CL_OK;
+}
+
 static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode,
                       double mean_sq_all, const std::vector<double>* col_ms) {
   ctx->prior_w.clear();
+  ctx->img = false;
   int st = validate(ctx, cfg);
   if (st) return st;
+  if (!col_ms && (cfg->w_tv < 0.0 || cfg->w_lv < 0.0))
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_solve_batch_device: automatic prior weights (w < 0) need y on the host; "
+                "pass explicit w_tv / w_lv");
   if (batch <= 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: empty batch");
   if (mode != CL_MODE_JOINT && mode != CL_MODE_PER_SIGNAL)
     return fail(ctx, CL_ERR_CONFIG, "clomp: unknown solve mode");
@@ -1134,10 +1277,7 @@ static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode
     pri = cfg->w_tv > 0.0 || (cfg->w_lv > 0.0 && cfg->lv_window <= 1);
   }
   if (!pri) return CL_OK;
-  if (!single)
-    return fail(ctx, CL_ERR_UNSUPPORTED,
-                "clomp: TV-2D / local-variance priors of multi-column joint batches are not "
-                "implemented on the B200 path (per-signal solves, or w_tv = w_lv = 0)");
+  if (!single) return setup_image_mode(ctx, batch, cfg, mean_sq_all, col_ms != nullptr);
   if (ctx->sep)
     return fail(ctx, CL_ERR_UNSUPPORTED, "clomp: priors on separable contexts are not implemented");
   if (ctx->world > 1 || ctx->vshards > 1)

@@ -116,6 +116,10 @@ struct SolveParams {
   // learning kernels store the residual loss and k_prior_control adds w_b c^T H c
   // and runs the stopping rules (clomp.cpp:93-119, 253-273)
   int32_t prior;
+  // image mode (prior == 2): multi-column joint batch with TV-2D / local
+  // variance on x = D S (clomp.cpp:93-119), batch-global weights
+  double w_tv_g, w_lv_g;
+  int32_t lv_on, lv_window, lv_stride, lv_nr, lv_nc;
 };
 
 struct Work {
@@ -172,6 +176,19 @@ struct Work {
   double* wtv = nullptr;           // [B] resolved TV weight per signal
   double* rloss = nullptr;         // [B] residual part of the current loss
   double* best_R = nullptr;        // [B] residual part of the best snapshot's loss
+  // image mode
+  const double* dt = nullptr;      // [n][n] basis atom-major: dt[k][q] = D[q][k]
+  double* img_x = nullptr;         // [B][n] x = D S_eff, signal-major (pixel (q, b))
+  double* img_gx = nullptr;        // [B][n] prior gradient in x-space
+  double* img_gd = nullptr;        // [B][cap] data gradient 2 (G c - b)
+  double* lv_mean = nullptr;       // [nr * nc] window means
+  double* lv_scale = nullptr;      // [nr * nc] inv_blocks / (count sd), 0 when sd == 0
+  double* lv_sd = nullptr;         // [nr * nc] window standard deviations
+  const int32_t* lv_rows = nullptr;   // [nr] window row origins
+  const int32_t* lv_cols = nullptr;   // [nc] window column origins
+  const int32_t* lv_rowcov = nullptr; // [n][8] row-window indices covering row q (-1 pad)
+  const int32_t* lv_colcov = nullptr; // [B][8] column-window indices covering column b
+  double* img_part = nullptr;      // [1024] loss partials
 };
 
 enum Counter {
@@ -187,6 +204,9 @@ enum Counter {
 enum Joint {
   kJBest = 0, kJPrev = 1, kJTotal = 2, kJStall = 3, kJImproved = 4,
   kJStop = 5, kJConv = 6, kJStatus = 7, kJIters = 8, kJFinalRn = 9,
+  kJPrior = 10,   // image mode: w_tv tv + w_lv lv of the current coefficients
+  kJTotalR = 11,  // image mode: residual part of kJTotal
+  kJBestR = 12,   // image mode: residual part of kJBest
   kNumJoint = 16
 };
 
@@ -284,6 +304,10 @@ void launch_cand_exchange(const Cand* g, Cand* cand, int64_t B, int64_t ntl, int
 // the learning kernels), and loss / stopping rules after them.
 void launch_prior_ext(const SolveParams& p, const Work& w, cudaStream_t s);
 void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
+// Image mode: the coupled epochs of one outer iteration and the residual /
+// prior loss after them (joint control follows).
+void launch_image_learn(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
+constexpr int kLvCover = 8;  // max windows covering one row / column
 
 // Whole per-signal solve in one persistent block per signal (small problems).
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);

@@ -15,12 +15,13 @@
 // term is ~2^-22 |a||r|) at twice the tf32 tensor rate, and the epilogue
 // divides the scales back out exactly.
 //
-// Roles (128 threads): warp 0 lane 0 issues TMA into a 4-stage ring,
+// Roles (256 threads): warp 0 lane 0 issues TMA into a 4-stage ring,
 // warp 1 lane 0 issues tcgen05.mma (single thread per CTA), warp 2 owns the
-// TMEM allocation.  After the last commit all four warps drain TMEM with
-// tcgen05.ld: thread = signal (its TMEM lane), so the per-signal candidate
-// record over the tile's 256 atoms (top-2 atoms + third value, Cand) is a
-// register scan with no shuffles.  Only that record per (signal, atom tile)
+// TMEM allocation.  After the last commit all eight warps drain TMEM with
+// tcgen05.ld: thread = signal (its TMEM lane; warps w and w + 4 share lanes
+// and split the columns), so the per-signal candidate record over the tile's
+// 256 atoms (top-2 atoms + third value, Cand) is a register scan with no
+// shuffles and one shared-memory merge of the two halves.  Only that record per (signal, atom tile)
 // reaches HBM; the selection merges tiles and re-decides near-ties (gap inside
 // the split-fp16 error bound) from exact fp64 scores of the few atoms in the band.
 #include <cuda.h>
@@ -198,7 +199,7 @@ __device__ __forceinline__ void cand_scan32(const float (&v)[32], int ka, int li
 // CTA r loads rows [r*TN/CL, (r+1)*TN/CL) of A_hi/A_lo and multicasts them, and
 // a stage is refilled only after all CL MMA issuers released it.
 template <int CL>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(256, 1)
 k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
           const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
           int64_t n, int64_t B, int kblocks, int64_t ntile, const int32_t* __restrict__ active,
@@ -221,7 +222,7 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
   // Whole tile finished?  (uniform per CTA; a cluster must stay together)
   if (CL == 1) {
     int mine = 0;
-    const int64_t b = m0 + threadIdx.x;
+    const int64_t b = m0 + (threadIdx.x & (TM - 1));
     mine = (b < B) ? active[b] : 0;
     if (!__syncthreads_or(mine)) return;
   }
@@ -305,21 +306,25 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
     mma_commit(accum);        // accumulator complete
   }
 
-  // ---------------- epilogue: thread = signal, scan its 256 atom columns
+  // ---------------- epilogue: thread = signal (its TMEM lane), eight warps:
+  // warps w and w + 4 read the same 32 lanes, columns [0, TN/2) and
+  // [TN/2, TN); the upper half's records are merged into the lower's.
   __syncwarp();
   mbar_wait(accum, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int64_t b = m0 + warp * 32 + lane;
-  // Candidate record (Cand) of this signal over the tile's atoms, scanned in
-  // ascending order so strict comparisons give the lowest atom on ties.
+  const int half = warp >> 2, wl = warp & 3;
+  const int64_t b = m0 + wl * 32 + lane;
+  // Candidate record (Cand) of this signal over its half of the tile's atoms,
+  // scanned in ascending order so strict comparisons give the lowest atom on ties.
   float v1 = -1.f, v2 = -1.f, v3 = -1.f;
   int i1 = 0x7fffffff, i2 = 0x7fffffff;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t lane_base = (uint32_t)(wl * 32) << 16;
 #pragma unroll 1
-  for (int c = 0; c < TN / 32; ++c) {
+  for (int c = 0; c < TN / 64; ++c) {
+    const int col = half * (TN / 2) + c * 32;
     float v[32];
-    tmem_ld_32(tmem + lane_base + (uint32_t)(c * 32), v);
-    const int64_t a0 = n0 + c * 32;
+    tmem_ld_32(tmem + lane_base + (uint32_t)col, v);
+    const int64_t a0 = n0 + col;
     if (scores_dbg && b < B) {
       const double u = (double)r_scale[b] * a_inv_scale;
       for (int q = 0; q < 32; ++q)
@@ -330,7 +335,33 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
     else  // ragged last tile: atoms past n never enter
       cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
   }
-  if (b < B) {
+  // the stage ring is idle now (every MMA retired): reuse it for the merge
+  float* mv = reinterpret_cast<float*>(smem);
+  int* mi = reinterpret_cast<int*>(mv + 3 * TM);
+  const int row = wl * 32 + lane;
+  if (half == 1) {
+    mv[row] = v1;
+    mv[TM + row] = v2;
+    mv[2 * TM + row] = v3;
+    mi[row] = i1;
+    mi[TM + row] = i2;
+  }
+  __syncthreads();
+  if (half == 0 && b < B) {
+    // upper-half atoms are all larger: strict inserts keep the lower atom on ties
+    const float u1 = mv[row], u2 = mv[TM + row], u3 = mv[2 * TM + row];
+    const int j1 = mi[row], j2 = mi[TM + row];
+    auto ins = [&](float x, int k) {  // the cand_scan32 update
+      const bool g1 = x > v1, g2 = x > v2;
+      i2 = g1 ? i1 : (g2 ? k : i2);
+      i1 = g1 ? k : i1;
+      v3 = fmaxf(v3, fminf(x, v2));
+      v2 = fmaxf(v2, fminf(x, v1));
+      v1 = fmaxf(v1, x);
+    };
+    ins(u1, j1);
+    ins(u2, j2);
+    v3 = fmaxf(v3, u3);
     // back to true units: both operand scales are exact powers of two
     const double u = (double)r_scale[b] * a_inv_scale;
     Cand r;
@@ -451,7 +482,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   if (!clustered) {
     cudaFuncSetAttribute(k_corr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     dim3 grid((unsigned)((p.n_corr + TN - 1) / TN), (unsigned)mtiles);
-    return launch_pdl(k_corr_tc<1>, grid, dim3(128), (size_t)SMEM_BYTES, s, *rhi, *rlo, *ahi, *alo,
+    return launch_pdl(k_corr_tc<1>, grid, dim3(256), (size_t)SMEM_BYTES, s, *rhi, *rlo, *ahi, *alo,
                       p.n_corr, p.B, kblocks, p.ntl, (const int32_t*)w.active,
                       (const float*)w.r_scale, p.a_inv_scale, w.cand, scores_dbg) == cudaSuccess;
   }
@@ -460,7 +491,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)((p.n_corr + TN - 1) / TN),
                      (unsigned)((mtiles + kCluster - 1) / kCluster * kCluster));
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];

@@ -1939,15 +1939,15 @@ k_prior_ext(SolveParams p, Work w) {
     if (!w.active[b]) continue;
     const int t = w.cnt[b], t0 = w.gcnt[b];
     if (t0 >= t) continue;
-    const double wb = w.wtv[b];
+    const double wb = w.wtv ? w.wtv[b] : 0.0;  // image mode: data Gram only
     double* G = w.gram + b * cap * cap;
-    double* H = w.hgram + b * cap * cap;
+    double* H = w.hgram ? w.hgram + b * cap * cap : nullptr;
     const int32_t* sup = w.sup + b * cap;
     const float* y = w.y32 + b * p.ldm;
     for (int k = t0; k < t; ++k) {
       const int64_t sk = sup[k];
       const float* ak = w.at32 + sk * p.ldm;
-      const double* dk = w.ddt + sk * w.ldd;
+      const double* dk = w.hgram ? w.ddt + sk * w.ldd : nullptr;
       for (int i = warp; i <= k; i += nw) {
         const int64_t si = sup[i];
         double g = 0.0;
@@ -1958,16 +1958,20 @@ k_prior_ext(SolveParams p, Work w) {
           for (int64_t q = lane; q < p.ldm; q += 32) g = fma(f2d(ak[q]), f2d(ai[q]), g);
           g = warp_sum(g);
         }
-        const double* di = w.ddt + si * w.ldd;
         double h = 0.0;
-        for (int64_t q = lane; q < w.ldd; q += 32) h = fma(dk[q], di[q], h);
-        h = warp_sum(h) * inv_n;
+        if (H) {
+          const double* di = w.ddt + si * w.ldd;
+          for (int64_t q = lane; q < w.ldd; q += 32) h = fma(dk[q], di[q], h);
+          h = warp_sum(h) * inv_n;
+        }
         if (lane == 0) {
           const double v = g + wb * h;
           G[(int64_t)k * cap + i] = v;
           G[(int64_t)i * cap + k] = v;
-          H[(int64_t)k * cap + i] = h;
-          H[(int64_t)i * cap + k] = h;
+          if (H) {
+            H[(int64_t)k * cap + i] = h;
+            H[(int64_t)i * cap + k] = h;
+          }
         }
       }
       if (warp == nw - 1) {
@@ -2015,6 +2019,214 @@ k_prior_control(SolveParams p, Work w, int outer) {
   snap = __shfl_sync(kFull, snap, 0);
   if (snap)
     for (int i = lane; i < t; i += 32) w.best_coef[b * cap + i] = c[i];
+}
+
+// ------------------------------------------------------------ image mode
+// The reference's column-batch image path (cskit.cpp:620-652): one joint
+// clomp_solve_batch over the columns of an image, whose priors couple the
+// columns — TV-2D (priors.cpp:28-59) and local variance (priors.cpp:74-116) on
+// the n x B image x = D S_eff (clomp.cpp:93-119), batch-global weights and
+// stopping.  The data term stays in the per-column Gram form; every epoch is
+//   k_img_synth  per column: gd = 2 (G c - b) and x_b = D_S c_b
+//   k_img_lv     per LV window: mean, sd (stats of the current x)
+//   k_img_gx     per pixel: gx = w_tv dtv/dx + w_lv dlv/dx
+//   k_img_step   per column: g = gd + (D^T gx)_S, optimizer step (gradient_step)
+// and after the epochs the residual per column plus k_img_loss (tv, lv of the
+// final x) feed k_joint_control.  Pixel (q, b) of x is img_x[b * n + q].
+constexpr int kImgThreads = 256;
+
+__global__ void __launch_bounds__(kImgThreads)
+k_img_synth(SolveParams p, Work w, int grad) {
+  extern __shared__ __align__(16) unsigned char ism[];
+  double* cs = reinterpret_cast<double*>(ism);
+  int32_t* sups = reinterpret_cast<int32_t*>(cs + p.cap);
+  const int tid = threadIdx.x;
+  const int64_t cap = p.cap, n = p.n;
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+    if (!w.active[b]) continue;
+    const int t = w.cnt[b];
+    for (int k = tid; k < t; k += kImgThreads) {
+      cs[k] = w.coef[b * cap + k];
+      sups[k] = w.sup[b * cap + k];
+    }
+    __syncthreads();
+    if (grad) {
+      const double* G = w.gram + b * cap * cap;
+      for (int i = tid; i < t; i += kImgThreads) {
+        double acc = 0.0;
+        for (int j = 0; j < t; ++j) acc = fma(G[(int64_t)j * cap + i], cs[j], acc);
+        w.img_gd[b * cap + i] = 2.0 * (acc - w.bvec[b * cap + i]);
+      }
+    }
+    for (int64_t q = tid; q < n; q += kImgThreads) {
+      double acc = 0.0;
+      for (int k = 0; k < t; ++k) acc = fma(w.dt[(int64_t)sups[k] * n + q], cs[k], acc);
+      w.img_x[b * n + q] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Local-variance window statistics: mean, sd, and the gradient scale
+// inv_blocks / (count sd) (0 where sd == 0: no gradient, priors.cpp:106).
+__global__ void k_img_lv(SolveParams p, Work w) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t win = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nwin = (int64_t)p.lv_nr * p.lv_nc;
+  if (win >= nwin || !w.active[0]) return;
+  const int r0 = w.lv_rows[win / p.lv_nc], c0 = w.lv_cols[win % p.lv_nc];
+  const int W = p.lv_window;
+  double sum = 0.0, sum_sq = 0.0;
+  for (int j = 0; j < W; ++j)
+    for (int i = 0; i < W; ++i) {
+      const double v = w.img_x[(int64_t)(c0 + j) * p.n + r0 + i];
+      sum += v;
+      sum_sq = fma(v, v, sum_sq);
+    }
+  const double count = (double)(W * W);
+  const double mean = sum / count;
+  const double var = fmax(sum_sq / count - mean * mean, 0.0);
+  const double sd = sqrt(var);
+  const double inv_blocks = 1.0 / (double)nwin;
+  w.lv_mean[win] = mean;
+  w.lv_sd[win] = sd;
+  w.lv_scale[win] = sd > 0.0 ? inv_blocks / (count * sd) : 0.0;
+}
+
+__global__ void k_img_gx(SolveParams p, Work w) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n = p.n, B = p.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * B || !w.active[0]) return;
+  const int64_t b = e / n, q = e % n;
+  const double* x = w.img_x;
+  const double xv = x[e];
+  double g = 0.0;
+  if (p.w_tv_g > 0.0) {
+    const double ih = 2.0 / (double)n, iw = 2.0 / (double)B;
+    double gv = 0.0;
+    if (n >= 2) {
+      if (q + 1 < n) gv += ih * (xv - x[e + 1]);
+      if (q > 0) gv -= ih * (x[e - 1] - xv);
+    }
+    if (B >= 2) {
+      if (b + 1 < B) gv += iw * (xv - x[e + n]);
+      if (b > 0) gv -= iw * (x[e - n] - xv);
+    }
+    g = p.w_tv_g * gv;
+  }
+  if (p.lv_on) {
+    double gl = 0.0;
+    for (int a = 0; a < kLvCover; ++a) {
+      const int ri = w.lv_rowcov[q * kLvCover + a];
+      if (ri < 0) break;
+      for (int c = 0; c < kLvCover; ++c) {
+        const int ci = w.lv_colcov[b * kLvCover + c];
+        if (ci < 0) break;
+        const int64_t win = (int64_t)ri * p.lv_nc + ci;
+        gl = fma(w.lv_scale[win], xv - w.lv_mean[win], gl);
+      }
+    }
+    g = fma(p.w_lv_g, gl, g);
+  }
+  w.img_gx[e] = g;
+}
+
+template <int OPT>
+__global__ void __launch_bounds__(kImgThreads)
+k_img_step(SolveParams p, Work w, int outer, int e) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nw = kImgThreads / 32;
+  const int64_t cap = p.cap, n = p.n;
+  pdl_wait();
+  pdl_trigger();
+  double bc1 = 1.0, bc2 = 1.0;
+  if (OPT == 2) {
+    const int step = (outer - 1) * p.inner + e;
+    bc1 = p.bc1[step];
+    bc2 = p.bc2[step];
+  }
+  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+    if (!w.active[b]) continue;
+    const int t = w.cnt[b];
+    const double* gx = w.img_gx + b * n;
+    for (int k = warp; k < t; k += nw) {
+      const double* dk = w.dt + (int64_t)w.sup[b * cap + k] * n;
+      double acc = 0.0;
+      for (int64_t q = lane; q < n; q += 32) acc = fma(dk[q], gx[q], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const int64_t o = b * cap + k;
+        double c = w.coef[o], m1 = w.mom1[o], m2 = w.mom2[o];
+        opt_step<OPT>(c, w.img_gd[o] + acc, m1, m2, p.lr, bc1, bc2);
+        w.coef[o] = c;
+        w.mom1[o] = m1;
+        w.mom2[o] = m2;
+      }
+    }
+  }
+}
+
+// Residual of every column after the epochs (fp64, stored for the next
+// correlation with its split) into loss[b].
+__global__ void __launch_bounds__(128)
+k_img_resid(SolveParams p, Work w) {
+  const int lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
+  const int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= p.B || !w.active[b]) return;
+  const int t = w.cnt[b];
+  const double L = warp_residual(p, w, b, w.coef + b * p.cap, w.sup + b * p.cap, t, lane);
+  if (lane == 0) w.loss[b] = L;
+}
+
+// tv and lv of the final x (one block, fixed reduction order):
+// joint[kJPrior] = w_tv tv + w_lv lv (lb.total's prior part, clomp.cpp:126).
+__global__ void __launch_bounds__(1024)
+k_img_loss(SolveParams p, Work w) {
+  __shared__ double red_tv[1024], red_lv[1024];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  if (!w.active[0]) return;
+  const int64_t n = p.n, B = p.B;
+  double tv = 0.0, lv = 0.0;
+  if (p.w_tv_g > 0.0) {
+    const double ih = 1.0 / (double)n, iw = 1.0 / (double)B;
+    for (int64_t e = tid; e < n * B; e += 1024) {
+      const int64_t b = e / n, q = e % n;
+      const double xv = w.img_x[e];
+      if (q + 1 < n) {
+        const double d = xv - w.img_x[e + 1];
+        tv = fma(ih * d, d, tv);
+      }
+      if (b + 1 < B) {
+        const double d = xv - w.img_x[e + n];
+        tv = fma(iw * d, d, tv);
+      }
+    }
+  }
+  if (p.lv_on) {
+    const int64_t nwin = (int64_t)p.lv_nr * p.lv_nc;
+    const double inv_blocks = 1.0 / (double)nwin;
+    for (int64_t win = tid; win < nwin; win += 1024) lv = fma(inv_blocks, w.lv_sd[win], lv);
+  }
+  red_tv[tid] = tv;
+  red_lv[tid] = lv;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) {
+      red_tv[tid] += red_tv[tid + o];
+      red_lv[tid] += red_lv[tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) w.joint[kJPrior] = p.w_tv_g * red_tv[0] + p.w_lv_g * red_lv[0];
 }
 
 // ------------------------------------------------------ fused small solve
@@ -2172,7 +2384,10 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
   }
   __shared__ int stop_s;
   if (tid == 0) {
-    const double total = red[0];
+    // image mode: the stopping rules read lb.total (residual + priors), the
+    // eps test and the final norm the residual part (clomp.cpp:238-242, 253-288)
+    const double total_r = red[0];
+    const double total = (p.prior == 2 && !init) ? total_r + w.joint[kJPrior] : total_r;
     int changed = 0;
     for (int q = 0; q < (int)(blockDim.x / 32); ++q) changed |= chg[q];
     double* J = w.joint;
@@ -2186,12 +2401,16 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
       J[kJIters] = 0.0;
       J[kJConv] = 0.0;
       J[kJTotal] = total;
-      if (sqrt(total) < p.eps) {
+      J[kJTotalR] = total_r;
+      J[kJBestR] = CUDART_INF;
+      J[kJPrior] = 0.0;
+      if (sqrt(total_r) < p.eps) {
         J[kJConv] = 1.0;
         stop = 1;
       }
     } else {
       J[kJTotal] = total;
+      J[kJTotalR] = total_r;
       if (!isfinite(total)) {
         J[kJStatus] = (double)kStatusNumerical;
         stop = 1;
@@ -2199,6 +2418,7 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
         J[kJIters] = (double)outer;
         if (total < J[kJBest]) {
           J[kJBest] = total;
+          J[kJBestR] = total_r;
           J[kJImproved] = 1.0;
         }
         const double prev = J[kJPrev];
@@ -2210,7 +2430,7 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
         J[kJPrev] = total;
         if (st >= (double)p.stall_patience || outer >= p.max_outer) {
           stop = 1;
-        } else if (sqrt(total) < p.eps) {
+        } else if (sqrt(total_r) < p.eps) {
           J[kJConv] = 1.0;
           stop = 1;
         }
@@ -2253,7 +2473,10 @@ __global__ void k_finalize(SolveParams p, Work w, int64_t out_cap,
     iters = (int)J[kJIters];
     const bool conv = J[kJConv] != 0.0;
     use_best = !conv && isfinite(J[kJBest]);
-    rn = use_best ? sqrt(J[kJBest]) : sqrt(J[kJTotal]);
+    if (p.prior == 2)
+      rn = use_best ? sqrt(J[kJBestR]) : sqrt(J[kJTotalR]);
+    else
+      rn = use_best ? sqrt(J[kJBest]) : sqrt(J[kJTotal]);
   } else {
     status = w.status[b];
     iters = w.iters[b];
@@ -2470,6 +2693,35 @@ void launch_prior_ext(const SolveParams& p, const Work& w, cudaStream_t s) {
 void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
   const int64_t nsig = p.sig_hi - p.sig_lo;
   launch_pdl(k_prior_control, dim3((unsigned)((nsig + 3) / 4)), dim3(128), 0, s, p, w, outer);
+}
+
+void launch_image_learn(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
+  const unsigned cgrid = (unsigned)std::min<int64_t>(p.B, 2048);
+  const size_t smem = (size_t)p.cap * 12 + 16;
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaFuncSetAttribute(k_img_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  const int64_t npix = p.n * p.B;
+  const unsigned pgrid = (unsigned)((npix + 255) / 256);
+  const int64_t nwin = (int64_t)p.lv_nr * p.lv_nc;
+  for (int e = 0; e < p.inner; ++e) {
+    launch_pdl(k_img_synth, dim3(cgrid), dim3(kImgThreads), smem, s, p, w, 1);
+    if (p.lv_on)
+      launch_pdl(k_img_lv, dim3((unsigned)((nwin + 127) / 128)), dim3(128), 0, s, p, w);
+    launch_pdl(k_img_gx, dim3(pgrid), dim3(256), 0, s, p, w);
+    switch (p.opt) {
+      case 0: launch_pdl(k_img_step<0>, dim3(cgrid), dim3(kImgThreads), 0, s, p, w, outer, e); break;
+      case 1: launch_pdl(k_img_step<1>, dim3(cgrid), dim3(kImgThreads), 0, s, p, w, outer, e); break;
+      default: launch_pdl(k_img_step<2>, dim3(cgrid), dim3(kImgThreads), 0, s, p, w, outer, e); break;
+    }
+  }
+  launch_pdl(k_img_resid, dim3((unsigned)((p.B + 3) / 4)), dim3(128), 0, s, p, w);
+  launch_pdl(k_img_synth, dim3(cgrid), dim3(kImgThreads), smem, s, p, w, 0);
+  if (p.lv_on)
+    launch_pdl(k_img_lv, dim3((unsigned)((nwin + 127) / 128)), dim3(128), 0, s, p, w);
+  launch_pdl(k_img_loss, dim3(1), dim3(1024), 0, s, p, w);
 }
 
 void launch_joint_control(const SolveParams& p, const Work& w, int outer,

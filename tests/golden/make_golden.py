@@ -176,7 +176,7 @@ def main():
     # th = 0.7, auto TV / LV weights) on a make_setup-style problem A = Phi D
     # with the DCT synthesis basis (sensing.cpp:13-29, 60-79).  A column solved
     # alone sees TV-1D only (LV needs batch >= window); a multi-column batch
-    # runs TV-2D + LV, which the B200 library rejects (gpu_code 5).
+    # (the image mode) runs TV-2D + local variance.
     nP, mP = 64, 32
     DP = np.zeros((nP, nP))
     refbind.ref().ref_dct_basis(nP, refbind._p(DP))
@@ -193,8 +193,7 @@ def main():
                                                                 max_outer=6, inner_steps=40,
                                                                 w_tv=-1.0), "single", basis=DP)
     add_solve("prior_joint_b1", AP, YP[:, :1], ClompConfig(max_outer=12), "batch", basis=DP)
-    add_solve("prior_joint_b3_tv2d", AP, YP, ClompConfig(max_outer=8), "batch", basis=DP,
-              gpu_code=5)
+    add_solve("prior_joint_b3_tv2d", AP, YP, ClompConfig(max_outer=8), "batch", basis=DP)
     # identity basis: TV of the coefficients themselves
     Ai, Yi = rand_problem(8, 32, 64, 5, 2, snr_db=30)
     add_solve("prior_identity_basis_single", Ai, Yi, ClompConfig(th=1.0, opt=ADAM, lr=0.02,

@@ -327,14 +327,44 @@ def test_priors_th1_large_support_cluster_and_block(gpu_available):
         assert rel_coef_err(r.s, ref["s"]) <= 1e-7
 
 
-def test_priors_rejected_where_not_implemented(gpu_available):
+def test_priors_need_the_basis(gpu_available):
     A = ARR["prior_joint_b3_tv2d/A"]
     Y = ARR["prior_joint_b3_tv2d/Y"]
     ctx = make_ctx(A)
     with pytest.raises(cl.UnsupportedError):  # no basis
         cl.clomp_solve_batch(ctx, Y[:, :1], cl.ClompConfig(max_outer=3))
-    ctx.set_basis(ARR["prior_joint_b3_tv2d/D"])
-    with pytest.raises(cl.UnsupportedError):  # multi-column joint: TV-2D + LV
+    with pytest.raises(cl.UnsupportedError):
         cl.clomp_solve_batch(ctx, Y, cl.ClompConfig(max_outer=3), mode=cl.MODE_JOINT)
-    r = cl.clomp_solve_batch(ctx, Y, cl.ClompConfig(max_outer=3), mode=cl.MODE_PER_SIGNAL)
-    assert np.all(r.status == 0)
+
+
+@pytest.mark.parametrize("cfgd", [dict(max_outer=10),  # defaults: Adam, th 0.7, TV-2D + LV
+                                  dict(th=1.0, opt=cl.PLAIN, lr=0.05, max_outer=8, w_tv=0.05,
+                                       w_lv=0.0),
+                                  dict(opt=cl.MOMENTUM, lr=0.02, max_outer=6, w_tv=0.0,
+                                       w_lv=0.1, lv_window=4, lv_stride=3)],
+                         ids=["default", "tv2d_plain_th1", "lv_momentum"])
+def test_image_mode_priors_vs_oracle(gpu_available, cfgd):
+    """The reference's column-batch image mode (clomp_solve_batch over the
+    columns of an image, cskit.cpp:620-652): TV-2D and local variance couple
+    the columns through x = D S; joint stopping.  A 96-row image of 40
+    columns, against the oracle (bit-exact with the reference)."""
+    n, m, B, k = 96, 48, 40, 5
+    D = cl.dct_basis(n)
+    rng = np.random.default_rng(17)
+    A = ((rng.standard_normal((m, n)) / np.sqrt(m)) @ D).astype(np.float32)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, k, replace=False), b] = rng.standard_normal(k)
+    Y = (A.astype(np.float64) @ X + 0.01 * rng.standard_normal((m, B))).astype(np.float32)
+    cfg = cl.ClompConfig(**cfgd)
+    ref = refbind.orc_solve(A.astype(np.float64), Y.astype(np.float64), cfg,
+                            mode=refbind.MODE_JOINT, basis=D)
+    assert ref["code"] == 0
+    for path in ("tc", "f64"):
+        ctx = make_ctx(A, path)
+        ctx.set_basis(D)
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_JOINT)
+        assert np.array_equal(r.mask, ref["mask"])
+        assert np.array_equal(r.iterations, ref["iterations"])
+        assert rel_coef_err(r.s, ref["s"]) <= 1e-7
+        np.testing.assert_allclose(r.final_residual_norm, ref["final_residual_norm"], rtol=1e-7)
