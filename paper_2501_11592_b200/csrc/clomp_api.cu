@@ -1514,6 +1514,10 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
   return CL_OK;
 }
 
+int cl_debug_k1_trace(unsigned long long* out, int max_ctas) {
+  return corr_tc_trace(out, max_ctas);
+}
+
 int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
                     double* scores) {
   if (!ctx || !r || !scores || batch <= 0) return CL_ERR_INTERNAL;

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -194,6 +195,124 @@ __device__ __forceinline__ void cand_scan32(const float (&v)[32], int ka, int li
   }
 }
 
+#ifdef CL_K1_TRACE
+__device__ unsigned long long g_k1_trace[1024][16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K1_MARK(i) \
+  do { g_k1_trace[blockIdx.y * gridDim.x + blockIdx.x][i] = gtimer(); } while (0)
+#define K1_MARK_T(i, tid) do { if (threadIdx.x == (tid)) K1_MARK(i); } while (0)
+#else
+#define K1_MARK(i) do { } while (0)
+#define K1_MARK_T(i, tid) do { } while (0)
+#endif
+
+// TMEM -> registers without the wait (the caller batches loads, then waits once).
+__device__ __forceinline__ void tmem_ld_32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+
+// Epilogue: thread = signal (its TMEM lane); NW warps, warp w reads the 32
+// lanes of quarter w % 4 and column part w / 4 of P = NW / 4 equal parts
+// (TN / (32 P) chunks of 32 columns, loaded back to back, one wait).  Each
+// part's record is merged into part 0's through the (idle) stage ring in
+// ascending part order, so strict inserts keep the lowest atom on ties.
+template <int NW>
+__device__ __forceinline__ void tile_epilogue(uint8_t* smem, uint32_t tmem, uint64_t* accum,
+                                              int64_t m0, int64_t n0, int64_t n, int64_t B,
+                                              int64_t ntile, const float* __restrict__ r_scale,
+                                              double a_inv_scale, Cand* __restrict__ cand,
+                                              float* __restrict__ scores_dbg, int warp, int lane,
+                                              int64_t tile) {
+  constexpr int P = NW / 4;
+  constexpr int CH = TN / (32 * P);  // chunks of 32 columns per thread
+  __syncwarp();
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int part = warp >> 2, wl = warp & 3;
+  const int64_t b = m0 + wl * 32 + lane;
+  float v1 = -1.f, v2 = -1.f, v3 = -1.f;
+  int i1 = 0x7fffffff, i2 = 0x7fffffff;
+  const uint32_t lane_base = (uint32_t)(wl * 32) << 16;
+  uint32_t raw[CH][32];
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    tmem_ld_32_nowait(tmem + lane_base + (uint32_t)(part * (TN / P) + c * 32), raw[c]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  K1_MARK_T(7, 96);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = part * (TN / P) + c * 32;
+    float v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(raw[c][q]);
+    const int64_t a0 = n0 + col;
+    if (scores_dbg && b < B) {
+      const double u = (double)r_scale[b] * a_inv_scale;
+      for (int q = 0; q < 32; ++q)
+        if (a0 + q < n) scores_dbg[b * n + a0 + q] = (float)((double)v[q] * u);
+    }
+    if (a0 + 32 <= n)
+      cand_scan32<false>(v, (int)a0, 32, v1, i1, v2, i2, v3);
+    else  // ragged last tile: atoms past n never enter
+      cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
+  }
+  // the stage ring is idle now (every MMA retired): reuse it for the merge
+  float* mv = reinterpret_cast<float*>(smem);       // [P][3][TM]
+  int* mi = reinterpret_cast<int*>(mv + P * 3 * TM);  // [P][2][TM]
+  const int row = wl * 32 + lane;
+  K1_MARK_T(8, 96);
+  K1_MARK_T(9, 480);
+  if (part > 0) {
+    mv[(part * 3 + 0) * TM + row] = v1;
+    mv[(part * 3 + 1) * TM + row] = v2;
+    mv[(part * 3 + 2) * TM + row] = v3;
+    mi[(part * 2 + 0) * TM + row] = i1;
+    mi[(part * 2 + 1) * TM + row] = i2;
+  }
+  __syncthreads();
+  K1_MARK_T(10, 0);
+  if (part == 0 && b < B) {
+    auto ins = [&](float x, int k) {  // the cand_scan32 update
+      const bool g1 = x > v1, g2 = x > v2;
+      i2 = g1 ? i1 : (g2 ? k : i2);
+      i1 = g1 ? k : i1;
+      v3 = fmaxf(v3, fminf(x, v2));
+      v2 = fmaxf(v2, fminf(x, v1));
+      v1 = fmaxf(v1, x);
+    };
+#pragma unroll
+    for (int q = 1; q < P; ++q) {
+      ins(mv[(q * 3 + 0) * TM + row], mi[(q * 2 + 0) * TM + row]);
+      ins(mv[(q * 3 + 1) * TM + row], mi[(q * 2 + 1) * TM + row]);
+      v3 = fmaxf(v3, mv[(q * 3 + 2) * TM + row]);
+    }
+    // back to true units: both operand scales are exact powers of two
+    const double u = (double)r_scale[b] * a_inv_scale;
+    Cand r;
+    r.v1 = v1 >= 0.f ? (double)v1 * u : -1.0;
+    r.v2 = v2 >= 0.f ? (double)v2 * u : -1.0;
+    r.v3 = v3 >= 0.f ? (double)v3 * u : -1.0;
+    r.i1 = i1;
+    r.i2 = i2;
+    cand[b * ntile + tile] = r;
+    K1_MARK_T(11, 0);
+  }
+}
+
 // CL: CTAs per cluster along the signal dimension.  With CL > 1 the atom tile
 // (the operand every CTA of the cluster shares) is fetched once per cluster:
 // CTA r loads rows [r*TN/CL, (r+1)*TN/CL) of A_hi/A_lo and multicasts them, and
@@ -306,72 +425,8 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
     mma_commit(accum);        // accumulator complete
   }
 
-  // ---------------- epilogue: thread = signal (its TMEM lane), eight warps:
-  // warps w and w + 4 read the same 32 lanes, columns [0, TN/2) and
-  // [TN/2, TN); the upper half's records are merged into the lower's.
-  __syncwarp();
-  mbar_wait(accum, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int half = warp >> 2, wl = warp & 3;
-  const int64_t b = m0 + wl * 32 + lane;
-  // Candidate record (Cand) of this signal over its half of the tile's atoms,
-  // scanned in ascending order so strict comparisons give the lowest atom on ties.
-  float v1 = -1.f, v2 = -1.f, v3 = -1.f;
-  int i1 = 0x7fffffff, i2 = 0x7fffffff;
-  const uint32_t lane_base = (uint32_t)(wl * 32) << 16;
-#pragma unroll 1
-  for (int c = 0; c < TN / 64; ++c) {
-    const int col = half * (TN / 2) + c * 32;
-    float v[32];
-    tmem_ld_32(tmem + lane_base + (uint32_t)col, v);
-    const int64_t a0 = n0 + col;
-    if (scores_dbg && b < B) {
-      const double u = (double)r_scale[b] * a_inv_scale;
-      for (int q = 0; q < 32; ++q)
-        if (a0 + q < n) scores_dbg[b * n + a0 + q] = (float)((double)v[q] * u);
-    }
-    if (a0 + 32 <= n)
-      cand_scan32<false>(v, (int)a0, 32, v1, i1, v2, i2, v3);
-    else  // ragged last tile: atoms past n never enter
-      cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
-  }
-  // the stage ring is idle now (every MMA retired): reuse it for the merge
-  float* mv = reinterpret_cast<float*>(smem);
-  int* mi = reinterpret_cast<int*>(mv + 3 * TM);
-  const int row = wl * 32 + lane;
-  if (half == 1) {
-    mv[row] = v1;
-    mv[TM + row] = v2;
-    mv[2 * TM + row] = v3;
-    mi[row] = i1;
-    mi[TM + row] = i2;
-  }
-  __syncthreads();
-  if (half == 0 && b < B) {
-    // upper-half atoms are all larger: strict inserts keep the lower atom on ties
-    const float u1 = mv[row], u2 = mv[TM + row], u3 = mv[2 * TM + row];
-    const int j1 = mi[row], j2 = mi[TM + row];
-    auto ins = [&](float x, int k) {  // the cand_scan32 update
-      const bool g1 = x > v1, g2 = x > v2;
-      i2 = g1 ? i1 : (g2 ? k : i2);
-      i1 = g1 ? k : i1;
-      v3 = fmaxf(v3, fminf(x, v2));
-      v2 = fmaxf(v2, fminf(x, v1));
-      v1 = fmaxf(v1, x);
-    };
-    ins(u1, j1);
-    ins(u2, j2);
-    v3 = fmaxf(v3, u3);
-    // back to true units: both operand scales are exact powers of two
-    const double u = (double)r_scale[b] * a_inv_scale;
-    Cand r;
-    r.v1 = v1 >= 0.f ? (double)v1 * u : -1.0;
-    r.v2 = v2 >= 0.f ? (double)v2 * u : -1.0;
-    r.v3 = v3 >= 0.f ? (double)v3 * u : -1.0;
-    r.i1 = i1;
-    r.i2 = i2;
-    cand[b * ntile + blockIdx.x] = r;
-  }
+  tile_epilogue<8>(smem, tmem, accum, m0, n0, n, B, ntile, r_scale, a_inv_scale, cand, scores_dbg,
+                   warp, lane, blockIdx.x);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still write into it
@@ -379,6 +434,170 @@ k_corr_tc(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CU
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   }
+}
+
+// ------------------------------------------------ CTA-pair (cta_group::2)
+// Two SMs of a TPC share one 256-signal x 256-atom tile: UMMA M = 256
+// (each CTA's 128 signals in its own TMEM lanes), N = 256 atoms split over
+// the pair's shared memory (each CTA holds 128 atom rows of every stage).  The
+// leader (cluster rank 0) issues every tcgen05.mma.cta_group::2; both CTAs'
+// TMA loads complete on the leader's stage barrier (.cta_group::2), and the
+// leader's commits arrive on both CTAs' empty / accumulator barriers.  Each
+// SM now ingests 32 KB per stage (its R slice + half the atom slice) instead
+// of 48 KB for the same MMA work, which is what limits the one-SM kernel at
+// short K (config 2: K = 512, 16 k-blocks).
+constexpr int A2_BYTES = (TN / 2) * BK * 2;  // 8 KB: half the atom tile
+constexpr int STAGE2_BYTES = 2 * R_BYTES + 2 * A2_BYTES;
+constexpr int STAGES2 = 6;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr uint32_t kIdesc2 = (1u << 4) | ((TN >> 3) << 17) | ((2 * TM >> 4) << 24);
+constexpr int kPairWarps = 16;  // epilogue: four column parts per TMEM lane quarter
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kPairWarps, 1)
+k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
+           const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+           int64_t n, int64_t B, int kblocks, int64_t ntile, const float* __restrict__ r_scale,
+           double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* accum = empty + STAGES2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();  // 0 = leader
+  // the pair spans cluster x (cta_group::2 pairs along x): blockIdx.x = signal
+  // tile, blockIdx.y = atom tile
+  const int64_t m0 = (int64_t)blockIdx.x * TM;  // this CTA's 128 signals
+  const int64_t n0 = (int64_t)blockIdx.y * TN;  // the pair's 256 atoms
+  if (threadIdx.x == 0) K1_MARK(0);
+
+  // Setup that does not read the previous kernel's output runs before the
+  // dependency wait (PDL): barriers, TMEM, tensor-map prefetch.
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rhi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rlo)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)));
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers and TMEM exist before any cross-CTA traffic
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the residual split of the previous kernel
+  pdl_trigger();
+  if (threadIdx.x == 0) K1_MARK(1);
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs): own R slice + own half of the
+    // atom slice, completing on the leader's stage barrier
+    const uint32_t full0 = mapa_u32(smem_u32(&full[0]), 0);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES2;
+      const uint32_t ph = (kb / STAGES2) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+      uint8_t* st = smem + s * STAGE2_BYTES;
+      const uint32_t bar = full0 + (uint32_t)(s * 8);
+      const int k0 = kb * BK;
+      const int arow = (int)n0 + (int)rank * (TN / 2);
+      tma_load_2d_pair(st, &tm_rhi, bar, k0, (int)m0);
+      tma_load_2d_pair(st + R_BYTES, &tm_rlo, bar, k0, (int)m0);
+      tma_load_2d_pair(st + 2 * R_BYTES, &tm_ahi, bar, k0, arow);
+      tma_load_2d_pair(st + 2 * R_BYTES + A2_BYTES, &tm_alo, bar, k0, arow);
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer: the leader's single thread for the pair
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES2;
+      const uint32_t ph = (kb / STAGES2) & 1;
+      mbar_wait(&full[s], ph);
+      if (kb == 0) K1_MARK(2);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint8_t* st = smem + s * STAGE2_BYTES;
+      const uint64_t d_rhi = sw128_desc(smem_u32(st));
+      const uint64_t d_rlo = sw128_desc(smem_u32(st + R_BYTES));
+      const uint64_t d_ahi = sw128_desc(smem_u32(st + 2 * R_BYTES));
+      const uint64_t d_alo = sw128_desc(smem_u32(st + 2 * R_BYTES + A2_BYTES));
+#pragma unroll
+      for (int j = 0; j < BK / 16; ++j) {
+        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+        mma_f16_pair(tmem, d_rhi + adv, d_alo + adv, (kb | j) != 0);
+        mma_f16_pair(tmem, d_rlo + adv, d_ahi + adv, 1);
+        mma_f16_pair(tmem, d_rhi + adv, d_ahi + adv, 1);
+      }
+      if (kb < kblocks - STAGES2) mma_commit_pair(&empty[s]);  // stage free in both CTAs
+    }
+    K1_MARK(3);
+    mma_commit_pair(accum);  // accumulators complete in both CTAs
+  }
+
+#ifdef CL_K1_TRACE
+  if (threadIdx.x == 96) {
+    mbar_wait(accum, 0);
+    K1_MARK(4);
+  }
+#endif
+  tile_epilogue<kPairWarps>(smem, tmem, accum, m0, n0, n, B, ntile, r_scale, a_inv_scale, cand,
+                            scores_dbg, warp, lane, blockIdx.y);
+  if (threadIdx.x == 0) K1_MARK(5);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();  // the pair's MMAs / commits are done before TMEM goes
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+  if (threadIdx.x == 64) K1_MARK(6);
 }
 
 // fp16 split of the dictionary: scale*x = hi + lo with scale = 2^e chosen by
@@ -468,9 +687,40 @@ int64_t corr_tc_tile_atoms() { return TN; }
 
 constexpr int kCluster = 4;
 
+static int g_tc_mode = -1;  // -1 auto, 0 one-SM kernel, 1 CTA pair (CL_TC_PAIR)
+
 static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_dbg,
                            cudaStream_t s) {
   const int64_t mtiles = (p.B + TM - 1) / TM;
+  if (g_tc_mode < 0) {
+    const char* e = getenv("CL_TC_PAIR");
+    g_tc_mode = e ? atoi(e) : 1;
+  }
+  if (g_tc_mode == 1 && mtiles >= 2) {
+    const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
+    const CUtensorMap* rlo = cached_map(1, w.r_lo, p.B, p.ldm, TM);
+    const CUtensorMap* ahi = cached_map(2, w.at_hi + p.atom0 * p.ldm, p.n_corr, p.ldm, TN / 2);
+    const CUtensorMap* alo = cached_map(3, w.at_lo + p.atom0 * p.ldm, p.n_corr, p.ldm, TN / 2);
+    if (!rhi || !rlo || !ahi || !alo) return false;
+    cudaFuncSetAttribute(k_corr_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)((mtiles + 1) / 2 * 2), (unsigned)((p.n_corr + TN - 1) / TN));
+    cfg.blockDim = dim3(32 * kPairWarps);
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, k_corr_tc2, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
+                              (int)(p.ldm / BK), p.ntl, (const float*)w.r_scale, p.a_inv_scale,
+                              w.cand, scores_dbg) == cudaSuccess;
+  }
   const bool clustered = mtiles >= kCluster;
   const int arows = clustered ? TN / kCluster : TN;
   const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
@@ -506,6 +756,21 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
   return cudaLaunchKernelEx(&cfg, k_corr_tc<kCluster>, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
                             kblocks, p.ntl, w.active, w.r_scale, p.a_inv_scale, w.cand,
                             scores_dbg) == cudaSuccess;
+}
+
+// Debug: per-CTA globaltimer marks of the last pair-kernel launch (build with
+// CL_NVCC_EXTRA=-DCL_K1_TRACE): entry, after setup, first stage, last MMA,
+// accumulator ready, epilogue done, exit.  Returns CTAs written (0: not built in).
+int corr_tc_trace(unsigned long long* out, int max_ctas) {
+#ifdef CL_K1_TRACE
+  const int n = max_ctas < 1024 ? max_ctas : 1024;
+  cudaMemcpyFromSymbol(out, g_k1_trace, (size_t)n * 16 * sizeof(unsigned long long));
+  return n;
+#else
+  (void)out;
+  (void)max_ctas;
+  return 0;
+#endif
 }
 
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
