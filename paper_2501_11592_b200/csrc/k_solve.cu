@@ -1592,8 +1592,6 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
 // at the fp64 pipe's rate instead of 8 bytes of shared memory or L2 per FMA
 // (k_learn_block), the rest of the outer iteration (Gram extension, residual,
 // loss, stopping rules, snapshot) is split over the whole cluster.
-constexpr int kClThreads = 256;
-
 __device__ __forceinline__ double warp_reduce8_t(double (&v)[8], int lane) {
 #pragma unroll
   for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
@@ -1703,9 +1701,17 @@ __device__ __forceinline__ double resid_rows(const SolveParams& p, const Work& w
 // rb % Q, warp rb / Q), so every CTA owns rows whenever t > 8 (Q - 1): each
 // CTA then has a warp that waits on every exchange phase, which keeps the
 // phases of its barriers in order (see the epoch loop).
-template <int Q, int OPT>
-__global__ void __launch_bounds__(kClThreads, 1)
+// Q CTAs of NWC warps; lane l owns CW columns [CW l, CW l + CW) of its warp's
+// 8 rows: t <= min(8 NWC Q, 32 CW).  Variants: (1, 2, 8) t <= 64,
+// (1, 4, 16) t <= 128 (one CTA, no remote traffic), (4, 8, 8) t <= 256.
+template <int Q, int CW, int NWC>
+constexpr int cl_min_blocks() { return (Q == 1 && CW <= 2) ? 2 : 1; }
+
+template <int Q, int CW, int NWC, int OPT>
+__global__ void __launch_bounds__(32 * NWC, (cl_min_blocks<Q, CW, NWC>()))
 k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
+  constexpr int kClThreads = 32 * NWC;
+  constexpr int kTmax = (8 * NWC * Q < 32 * CW) ? 8 * NWC * Q : 32 * CW;
   __shared__ __align__(16) double cbuf[2][256];
   __shared__ __align__(8) uint64_t fullb[2];  // c buffer b complete (t * 8 bytes)
   __shared__ uint32_t s_phase[2];            // phases of fullb[] completed so far
@@ -1729,7 +1735,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   pdl_trigger();
   const int count = w.counters[kBigCount + (outer & 1)];
   const int64_t cap = p.cap;
-  const int R0 = 8 * (warp * Q + q), C0 = 8 * lane;
+  const int R0 = 8 * (warp * Q + q), C0 = CW * lane;
   const int my_row = R0 + (lane >> 2);
   // remote addresses: c buffers and their barriers in every CTA of the cluster
   uint32_t dst_c[Q], dst_b0[Q], dst_b1[Q];
@@ -1743,7 +1749,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   for (int li = blockIdx.y; li < count; li += gridDim.y) {
     const int64_t b = big_list[li];
     const int t = w.cnt[b];
-    if (t > 64 * Q) continue;  // uniform over the cluster: left to k_learn_block
+    if (t > kTmax) continue;  // uniform over the cluster: left to k_learn_block
     const int t0 = w.gcnt[b];
     double* G = w.gram + b * cap * cap;
     const float* y = w.y32 + b * p.ldm;
@@ -1790,11 +1796,11 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     __threadfence();
     cl_sync<Q>();  // G, b, fresh coefficients visible to the whole cluster
     if (q == 0 && tid == 0) w.gcnt[b] = t;
-    double g[8][8];
+    double g[8][CW];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < CW; ++j)
         g[i][j] = (R0 + i < t && C0 + j < t) ? G[(int64_t)(R0 + i) * cap + C0 + j] : 0.0;
     for (int k = tid; k < t; k += kClThreads) cbuf[0][k] = w.coef[b * cap + k];
     const bool producing = R0 < t;
@@ -1832,10 +1838,10 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
                            cl_smem_u32(&fullb[nxt])),
                        "r"((uint32_t)(t * 8))
                        : "memory");
-        double cv[8];
+        double cv[CW];
         const double2* cp2 = reinterpret_cast<const double2*>(&cbuf[cur][C0]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CW / 2; ++j) {
           const double2 x = cp2[j];
           cv[2 * j] = x.x;
           cv[2 * j + 1] = x.y;
@@ -1845,7 +1851,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
         for (int i = 0; i < 8; ++i) {
           double a = 0.0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) a = fma(g[i][j], cv[j], a);
+          for (int j = 0; j < CW; ++j) a = fma(g[i][j], cv[j], a);
           acc[i] = a;
         }
         const double gc = warp_reduce8_t(acc, lane);
@@ -2591,12 +2597,12 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
   }
 }
 
-template <int Q>
+template <int Q, int CW, int NWC>
 static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int32_t* big_list,
                              int nclusters, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Q, (unsigned)nclusters);
-  cfg.blockDim = dim3(kClThreads);
+  cfg.blockDim = dim3(32 * NWC);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -2614,26 +2620,31 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
   cfg.numAttrs = na;
   const int32_t* bl = big_list;
   switch (p.opt) {
-    case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 0>, p, w, outer, bl); break;
-    case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 1>, p, w, outer, bl); break;
-    default: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, 2>, p, w, outer, bl); break;
+    case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 0>, p, w, outer, bl); break;
+    case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 1>, p, w, outer, bl); break;
+    default: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 2>, p, w, outer, bl); break;
   }
 }
 
 // Cluster learning for supports of 33..256 atoms: returns the support size
-// up to which it learns this iteration (0 when not launched).
+// up to which it learns this iteration (0 when not launched).  One CTA per
+// signal up to 128 atoms (64: 8 warps x 2 columns per lane; 128: 16 warps x 4),
+// four-CTA clusters up to 256.
 static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                                 int64_t nsig, int sms, cudaStream_t s) {
   if (p.sep || max_cnt <= kWarpCap || p.cluster_learn == 0) return 0;
-  const int Q = max_cnt <= 64 ? 1 : max_cnt <= 128 ? 2 : 4;
-  const int nclusters = (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / Q));
-  if (Q == 1)
-    launch_cluster_q<1>(p, w, outer, w.big_list, nclusters, s);
-  else if (Q == 2)
-    launch_cluster_q<2>(p, w, outer, w.big_list, nclusters, s);
-  else
-    launch_cluster_q<4>(p, w, outer, w.big_list, nclusters, s);
-  return 64 * Q;
+  auto nc = [&](int q) { return (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / q)); };
+  if (max_cnt <= 64) {
+    launch_cluster_q<1, 2, 8>(p, w, outer, w.big_list,
+                              (int)std::min<int64_t>(nsig, 2 * (int64_t)sms), s);
+    return 64;
+  }
+  if (max_cnt <= 128) {
+    launch_cluster_q<1, 4, 16>(p, w, outer, w.big_list, nc(1), s);
+    return 128;
+  }
+  launch_cluster_q<4, 8, 8>(p, w, outer, w.big_list, nc(4), s);
+  return 256;
 }
 
 void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
