@@ -215,8 +215,9 @@ int cl_set_fused(cl_ctx* ctx, int on);
  * CL_ERR_UNSUPPORTED; priors without a basis too. */
 int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram
- * matrix in registers (default 1); 0 keeps them on the block-per-signal
- * kernel (tests compare the two). */
+ * matrix in registers (default 1; 2 = an eight-CTA variant above 128 atoms
+ * instead of four CTAs); 0 keeps them on the block-per-signal kernel (tests
+ * compare them). */
 int cl_set_cluster_learn(cl_ctx* ctx, int on);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);

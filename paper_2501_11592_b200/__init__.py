@@ -389,10 +389,11 @@ class ClompContext:
             raise DimensionError("set_basis: D must be square")
         _raise(lib().cl_set_basis(self._h, _ptr(D), D.shape[0], 0), self._h)
 
-    def set_cluster_learn(self, on: bool):
+    def set_cluster_learn(self, on):
         """Learn supports of 33..256 atoms on CTA clusters with register-resident
-        Gram blocks (default) or on the block-per-signal kernel."""
-        _raise(lib().cl_set_cluster_learn(self._h, int(bool(on))), self._h)
+        Gram blocks (True / 1, default; 2 = eight-CTA variant above 128 atoms) or
+        on the block-per-signal kernel (False / 0)."""
+        _raise(lib().cl_set_cluster_learn(self._h, int(on)), self._h)
 
     def set_profiling(self, on: bool):
         _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)

@@ -117,7 +117,7 @@ struct cl_ctx {
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool fused_ok = true;  // small problems: one persistent block per signal
-  bool cluster_learn = true;  // supports of 33..256 atoms on CTA clusters
+  int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (2: 4-CTA variant)
   // column sharding (cl_create_colshard); vshards emulates W shards on one GPU
   int rank = 0, world = 1, vshards = 1;
   void* comm = nullptr;
@@ -484,7 +484,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // th == 1: the selection (K1c, near-tie rescoring included) runs at the top
   // of the learning kernel, one warp per signal, instead of its own launch.
   p.fuse_select = (!full_scores && !p.sep && !prior) ? 1 : 0;
-  p.cluster_learn = ctx->cluster_learn ? 1 : 0;
+  p.cluster_learn = ctx->cluster_learn;
   p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
 
   const Work& w = ctx->w;
@@ -1163,7 +1163,7 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
 
 int cl_set_cluster_learn(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
-  ctx->cluster_learn = on != 0;
+  ctx->cluster_learn = on < 0 ? 0 : (on > 2 ? 1 : on);
   return CL_OK;
 }
 
@@ -1513,6 +1513,8 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
       mask[j * batch + b] = (bits[(size_t)(b * p.mwords + j / 32)] >> (j % 32)) & 1u;
   return CL_OK;
 }
+
+int cl_debug_cluster_trace(unsigned long long* out) { return cluster_trace(out); }
 
 int cl_debug_k1_trace(unsigned long long* out, int max_ctas) {
   return corr_tc_trace(out, max_ctas);

@@ -250,6 +250,7 @@ void launch_corr_gemv(const SolveParams& p, const Work& w, bool full_scores,
 // tcgen05 3xTF32 correlation with fused top-2 epilogue (th == 1).
 bool corr_tc_available();
 int corr_tc_trace(unsigned long long* out, int max_ctas);
+int cluster_trace(unsigned long long* out);
 int64_t corr_tc_tile_atoms();
 void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
 // Same kernel, additionally writing the signed fp32 scores [B][n] (tests).

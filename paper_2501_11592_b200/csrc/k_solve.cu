@@ -1592,6 +1592,27 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
 // at the fp64 pipe's rate instead of 8 bytes of shared memory or L2 per FMA
 // (k_learn_block), the rest of the outer iteration (Gram extension, residual,
 // loss, stopping rules, snapshot) is split over the whole cluster.
+// Generic transposed butterfly over RW row partials: lanes
+// (lane >> (5 - log2 RW)) == i end with row i's warp total.
+template <int RW>
+__device__ __forceinline__ double warp_reduce_rows_t(double (&v)[RW], int lane) {
+#pragma unroll
+  for (int h = RW / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  constexpr int kLog = RW >= 8 ? 3 : RW >= 4 ? 2 : RW >= 2 ? 1 : 0;
+  double x = v[0];
+#pragma unroll
+  for (int o = 16 >> kLog; o >= 1; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
 __device__ __forceinline__ double warp_reduce8_t(double (&v)[8], int lane) {
 #pragma unroll
   for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
@@ -1702,22 +1723,31 @@ __device__ __forceinline__ double resid_rows(const SolveParams& p, const Work& w
 // CTA then has a warp that waits on every exchange phase, which keeps the
 // phases of its barriers in order (see the epoch loop).
 // Q CTAs of NWC warps; lane l owns CW columns [CW l, CW l + CW) of its warp's
-// 8 rows: t <= min(8 NWC Q, 32 CW).  Variants: (1, 2, 8) t <= 64,
-// (1, 4, 16) t <= 128 (one CTA, no remote traffic), (4, 8, 8) t <= 256.
-template <int Q, int CW, int NWC>
-constexpr int cl_min_blocks() { return (Q == 1 && CW <= 2) ? 2 : 1; }
+// RW rows: t <= min(RW NWC Q, 32 CW).  Variants (Q, CW, NWC, RW):
+// (1, 2, 8, 8) t <= 64, (1, 4, 16, 8) t <= 128 (one CTA, no remote traffic),
+// (4, 8, 8, 8) t <= 256 ((8, 8, 8, 4), two CTAs per SM, for comparison).
+template <int Q, int CW, int NWC, int RW>
+constexpr int cl_min_blocks() { return ((Q == 1 && CW <= 2) || RW == 4) ? 2 : 1; }
 
-template <int Q, int CW, int NWC, int OPT>
-__global__ void __launch_bounds__(32 * NWC, (cl_min_blocks<Q, CW, NWC>()))
+#ifdef CL_CLUSTER_TRACE
+// Debug (CL_NVCC_EXTRA=-DCL_CLUSTER_TRACE): clock64 split of the epoch loop,
+// CTA 0 warp 0 lane 0 of every cluster launch accumulates
+// [wait, fma, reduce, step+store, epochs] cycles.
+__device__ unsigned long long g_cl_trace[8];
+#endif
+
+template <int Q, int CW, int NWC, int RW, int OPT>
+__global__ void __launch_bounds__(32 * NWC, (cl_min_blocks<Q, CW, NWC, RW>()))
 k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   constexpr int kClThreads = 32 * NWC;
-  constexpr int kTmax = (8 * NWC * Q < 32 * CW) ? 8 * NWC * Q : 32 * CW;
+  constexpr int kTmax = (RW * NWC * Q < 32 * CW) ? RW * NWC * Q : 32 * CW;
+  constexpr int kRowShift = RW == 8 ? 2 : 3;  // lanes per row = 32 / RW
   __shared__ __align__(16) double cbuf[2][256];
   __shared__ __align__(8) uint64_t fullb[2];  // c buffer b complete (t * 8 bytes)
   __shared__ uint32_t s_phase[2];            // phases of fullb[] completed so far
   __shared__ int32_t sups[256];
   __shared__ double red[kClThreads / 32];
-  __shared__ double lpart[4];  // rank 0: per-CTA loss partials
+  __shared__ double lpart[8];  // rank 0: per-CTA loss partials
   __shared__ double s_L;
   __shared__ int s_snap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1735,8 +1765,8 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   pdl_trigger();
   const int count = w.counters[kBigCount + (outer & 1)];
   const int64_t cap = p.cap;
-  const int R0 = 8 * (warp * Q + q), C0 = CW * lane;
-  const int my_row = R0 + (lane >> 2);
+  const int R0 = RW * (warp * Q + q), C0 = CW * lane;
+  const int my_row = R0 + (lane >> kRowShift);
   // remote addresses: c buffers and their barriers in every CTA of the cluster
   uint32_t dst_c[Q], dst_b0[Q], dst_b1[Q];
 #pragma unroll
@@ -1796,15 +1826,15 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     __threadfence();
     cl_sync<Q>();  // G, b, fresh coefficients visible to the whole cluster
     if (q == 0 && tid == 0) w.gcnt[b] = t;
-    double g[8][CW];
+    double g[RW][CW];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < RW; ++i)
 #pragma unroll
       for (int j = 0; j < CW; ++j)
         g[i][j] = (R0 + i < t && C0 + j < t) ? G[(int64_t)(R0 + i) * cap + C0 + j] : 0.0;
     for (int k = tid; k < t; k += kClThreads) cbuf[0][k] = w.coef[b * cap + k];
     const bool producing = R0 < t;
-    const bool owner = (lane & 3) == 0 && my_row < t;
+    const bool owner = (lane & ((1 << kRowShift) - 1)) == 0 && my_row < t;
     double cr = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
     if (my_row < t) {
       cr = w.coef[b * cap + my_row];
@@ -1821,6 +1851,13 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     // that CTA's barrier).  A sender has received every row of epoch e's
     // input, produced by warps that had themselves waited for the phase of
     // the buffer being overwritten, so a phase never receives bytes early.
+#ifdef CL_CLUSTER_TRACE
+    unsigned long long tw = 0, tf = 0, tr = 0, ts = 0, tcur = clock64();
+    const bool tracer = q == 0 && tid == 0;
+#define CLT(acc) do { if (tracer) { const unsigned long long x = clock64(); acc += x - tcur; tcur = x; } } while (0)
+#else
+#define CLT(acc) do { } while (0)
+#endif
     if (producing) {
       for (int e = 0; e < E; ++e) {
         const int cur = e & 1, nxt = cur ^ 1;
@@ -1846,15 +1883,24 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
           cv[2 * j] = x.x;
           cv[2 * j + 1] = x.y;
         }
-        double acc[8];
+        CLT(tw);
+        double acc[RW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < RW; ++i) {
           double a = 0.0;
 #pragma unroll
           for (int j = 0; j < CW; ++j) a = fma(g[i][j], cv[j], a);
           acc[i] = a;
         }
-        const double gc = warp_reduce8_t(acc, lane);
+#ifdef CL_CLUSTER_TRACE
+        if (tracer && acc[0] == 12345.678) tw += 1;  // consume the FMAs before the mark
+#endif
+        CLT(tf);
+        const double gc = warp_reduce_rows_t<RW>(acc, lane);
+#ifdef CL_CLUSTER_TRACE
+        if (tracer && gc == 12345.678) tw += 1;
+#endif
+        CLT(tr);
         if (owner) {
           double bc1 = 1.0, bc2 = 1.0;
           if (OPT == 2) {
@@ -1871,7 +1917,17 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
                 "d"(cr), "r"(nxt ? dst_b1[r] : dst_b0[r])
                 : "memory");
         }
+        CLT(ts);
       }
+#ifdef CL_CLUSTER_TRACE
+      if (tracer) {
+        atomicAdd(&g_cl_trace[0], tw);
+        atomicAdd(&g_cl_trace[1], tf);
+        atomicAdd(&g_cl_trace[2], tr);
+        atomicAdd(&g_cl_trace[3], ts);
+        atomicAdd(&g_cl_trace[4], (unsigned long long)E);
+      }
+#endif
       const int fin = E & 1;
       cl_mbar_wait(cl_smem_u32(&fullb[fin]), (fin ? pc1 : pc0) & 1);
     }
@@ -2597,7 +2653,7 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
   }
 }
 
-template <int Q, int CW, int NWC>
+template <int Q, int CW, int NWC, int RW>
 static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int32_t* big_list,
                              int nclusters, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
@@ -2620,9 +2676,9 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
   cfg.numAttrs = na;
   const int32_t* bl = big_list;
   switch (p.opt) {
-    case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 0>, p, w, outer, bl); break;
-    case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 1>, p, w, outer, bl); break;
-    default: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, 2>, p, w, outer, bl); break;
+    case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 0>, p, w, outer, bl); break;
+    case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 1>, p, w, outer, bl); break;
+    default: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 2>, p, w, outer, bl); break;
   }
 }
 
@@ -2635,15 +2691,24 @@ static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, 
   if (p.sep || max_cnt <= kWarpCap || p.cluster_learn == 0) return 0;
   auto nc = [&](int q) { return (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / q)); };
   if (max_cnt <= 64) {
-    launch_cluster_q<1, 2, 8>(p, w, outer, w.big_list,
-                              (int)std::min<int64_t>(nsig, 2 * (int64_t)sms), s);
+    launch_cluster_q<1, 2, 8, 8>(p, w, outer, w.big_list,
+                                 (int)std::min<int64_t>(nsig, 2 * (int64_t)sms), s);
     return 64;
   }
   if (max_cnt <= 128) {
-    launch_cluster_q<1, 4, 16>(p, w, outer, w.big_list, nc(1), s);
+    launch_cluster_q<1, 4, 16, 8>(p, w, outer, w.big_list, nc(1), s);
     return 128;
   }
-  launch_cluster_q<4, 8, 8>(p, w, outer, w.big_list, nc(4), s);
+  if (p.cluster_learn == 2) {
+    // eight CTAs of 4-row warps (half the registers per thread, two CTAs per
+    // SM, a four-partial reduction): measured slower than four 8-row CTAs
+    // (config 3: 414 vs 360 ms; config 7 equal) — kept for comparison
+    launch_cluster_q<8, 8, 8, 4>(p, w, outer, w.big_list,
+                                 (int)std::max<int64_t>(1, std::min<int64_t>(nsig, 2 * sms / 8)),
+                                 s);
+    return 256;
+  }
+  launch_cluster_q<4, 8, 8, 8>(p, w, outer, w.big_list, nc(4), s);
   return 256;
 }
 
@@ -2693,6 +2758,16 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
       default: launch_block_variant<2>(p, w, outer, big_list, grid, skip_le, s); break;
     }
   }
+}
+
+int cluster_trace(unsigned long long* out) {
+#ifdef CL_CLUSTER_TRACE
+  cudaMemcpyFromSymbol(out, g_cl_trace, 8 * sizeof(unsigned long long));
+  return 1;
+#else
+  (void)out;
+  return 0;
+#endif
 }
 
 void launch_prior_ext(const SolveParams& p, const Work& w, cudaStream_t s) {

@@ -265,11 +265,12 @@ def test_cluster_learning_vs_oracle_and_block_kernel(gpu_available, K, opt):
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
     assert np.all(r.status == 0)
     _subset_parity(A, Y, cfg, np.arange(min(B, 2)), r, X if opt == cl.PLAIN else None)
-    ctx.set_cluster_learn(False)
-    r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
-    assert np.array_equal(r.mask, r0.mask)
-    assert np.array_equal(r.iterations, r0.iterations)
-    assert rel_coef_err(r.s, r0.s) <= 1e-9
+    for variant in (0, 2):  # block kernel; eight-CTA cluster variant
+        ctx.set_cluster_learn(variant)
+        r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        assert np.array_equal(r.mask, r0.mask)
+        assert np.array_equal(r.iterations, r0.iterations)
+        assert rel_coef_err(r.s, r0.s) <= 1e-9
 
 
 def test_priors_default_config_per_signal_vs_oracle(gpu_available):
