@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--max-outer", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05, 3 GEMV")
+    ap.add_argument("--power-levels", type=int, default=-1,
+                    help="plain GD on cluster-sized supports: squaring levels (-1 auto, 0 off)")
     return ap.parse_args()
 
 
@@ -371,6 +373,8 @@ def run_ours(args, rank, world, local_rank):
         ctx = cl.ClompContext(A, device=local_rank)
     if args.corr_path:
         ctx.set_corr_path(args.corr_path)
+    if args.power_levels != -1 and not c["sep"]:
+        ctx.set_power_levels(args.power_levels)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)
     d_y = torch.from_numpy(np.ascontiguousarray(Y.T)).to(dev)  # signal-major B x m

@@ -219,6 +219,12 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
  * instead of four CTAs); 0 keeps them on the block-per-signal kernel (tests
  * compare them). */
 int cl_set_cluster_learn(cl_ctx* ctx, int on);
+/* Plain gradient descent on cluster-learned supports (33..256 atoms): run the
+ * E epochs as E mod 2^L plain steps, L batched squarings of T = I - 2 lr G on
+ * the fp64 tensor cores and E / 2^L steps of c <- T^(2^L) c + d (the same
+ * iterate in exact arithmetic).  levels: -1 auto (default, L = 3), 0 off (one
+ * cluster epoch per reference epoch), 1..8 explicit. */
+int cl_set_power_levels(cl_ctx* ctx, int levels);
 /* Enable per-kernel CUDA-event timing in cl_get_stats (adds syncs). */
 int cl_set_profiling(cl_ctx* ctx, int on);
 /* Run this context's work on a caller-owned cudaStream_t (NULL restores the

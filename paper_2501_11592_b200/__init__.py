@@ -147,7 +147,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_basis",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
     "cl_gen_problem_2d", "cl_dct_basis",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
@@ -183,6 +183,7 @@ def lib() -> C.CDLL:
         h.cl_set_gram_cache.argtypes = [vp, i32]
         h.cl_set_fused.argtypes = [vp, i32]
         h.cl_set_cluster_learn.argtypes = [vp, i32]
+        h.cl_set_power_levels.argtypes = [vp, i32]
         h.cl_set_basis.argtypes = [vp, vp, C.c_int64, i32]
         h.cl_nccl_unique_id.argtypes = [vp]
         h.cl_create_colshard.restype = vp
@@ -394,6 +395,11 @@ class ClompContext:
         Gram blocks (True / 1, default; 2 = eight-CTA variant above 128 atoms) or
         on the block-per-signal kernel (False / 0)."""
         _raise(lib().cl_set_cluster_learn(self._h, int(on)), self._h)
+
+    def set_power_levels(self, levels: int):
+        """Power form of plain GD on cluster-learned supports: -1 auto (L = 3),
+        0 off (one cluster epoch per reference epoch), L squaring levels."""
+        _raise(lib().cl_set_power_levels(self._h, int(levels)), self._h)
 
     def set_profiling(self, on: bool):
         _raise(lib().cl_set_profiling(self._h, int(bool(on))), self._h)

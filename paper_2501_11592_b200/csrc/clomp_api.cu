@@ -118,6 +118,9 @@ struct cl_ctx {
   int corr_force = 0;
   bool fused_ok = true;  // small problems: one persistent block per signal
   int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (2: 4-CTA variant)
+  int power_levels = -1;  // plain GD on cluster-sized supports: squaring levels (-1 auto, 0 off)
+  double* pw_buf = nullptr;  // power-form buffers (Work::pw_t / pw_d)
+  size_t pw_bytes = 0;
   // column sharding (cl_create_colshard); vshards emulates W shards on one GPU
   int rank = 0, world = 1, vshards = 1;
   void* comm = nullptr;
@@ -485,6 +488,43 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // of the learning kernel, one warp per signal, instead of its own launch.
   p.fuse_select = (!full_scores && !p.sep && !prior) ? 1 : 0;
   p.cluster_learn = ctx->cluster_learn;
+  // Power form for the cluster-learned supports (plain GD only: momentum and
+  // Adam are not affine in c).  Auto: L = 3 (E = 200 -> 25 steps of T^8).
+  {
+    const int64_t nsig = p.sig_hi - p.sig_lo;
+    int L = ctx->power_levels < 0 ? 3 : ctx->power_levels;
+    while (L > 0 && ((int64_t)1 << L) > (int64_t)c->inner_steps) --L;
+    const bool use = L > 0 && c->opt == CL_OPT_PLAIN && !prior && !ctx->sep &&
+                     ctx->cluster_learn == 1 && cap > kWarpCap;
+    if (use) {
+      const int64_t ld = std::min<int64_t>(256, (cap + 63) / 64 * 64);
+      const int64_t slots = std::min<int64_t>(nsig, 1024);
+      const int64_t nchunk = (ctx->ldm + 511) / 512;  // k_pw_resid row chunks
+      const size_t bytes =
+          (size_t)(2 * slots * (ld * ld + ld) + slots * nchunk) * sizeof(double) +
+          (size_t)slots * sizeof(int32_t);
+      if (bytes > ctx->pw_bytes) {
+        if (ctx->pw_buf) cudaFree(ctx->pw_buf);
+        ctx->pw_buf = nullptr;
+        ctx->pw_bytes = 0;
+        CL_CUDA(ctx, cudaMalloc(&ctx->pw_buf, bytes));
+        CL_CUDA(ctx, cudaMemset(ctx->pw_buf, 0, bytes));  // chunk counters start at 0
+        ctx->pw_bytes = bytes;
+      }
+      ctx->w.pw_t = ctx->pw_buf;
+      ctx->w.pw_d = ctx->pw_buf + 2 * slots * ld * ld;
+      ctx->w.pw_part = ctx->w.pw_d + 2 * slots * ld;
+      ctx->w.pw_cnt = reinterpret_cast<int32_t*>(ctx->w.pw_part + slots * nchunk);
+      p.pw_levels = L;
+      p.pw_q = (int32_t)(c->inner_steps >> L);
+      p.pw_r = (int32_t)(c->inner_steps & ((1u << L) - 1));
+      p.pw_slots = (int32_t)slots;
+      p.pw_ld = (int32_t)ld;
+    } else {
+      ctx->w.pw_t = ctx->w.pw_d = ctx->w.pw_part = nullptr;
+      ctx->w.pw_cnt = nullptr;
+    }
+  }
   p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
 
   const Work& w = ctx->w;
@@ -534,7 +574,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         nccl_allgather_inplace(ctx->comm, w.xg, cnt * sizeof(Cand), 1, ctx->rank, s);
       }
       launch_cand_exchange(w.xg, w.cand, B, p.ntl, W, p.n_corr, s);
-      launch_learn(p, w, outer, outer, s);  // selection fused (p.fuse_select)
+      *launches += launch_learn(p, w, outer, outer, s);  // selection fused (p.fuse_select)
       *launches += 1 + (cap > 8 ? 3 : 2);
       if (ctx->world > 1) {
         const size_t rows = (size_t)((p.sig_hi - p.sig_lo) * p.ldm);
@@ -563,7 +603,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       launch_image_learn(p, w, outer, s);
       *launches += 2 + (int64_t)p.inner * (p.lv_on ? 4 : 3) + 3 + p.lv_on;
     } else {
-      launch_learn(p, w, outer, bound, s);
+      *launches += launch_learn(p, w, outer, bound, s);
       if (p.prior) launch_prior_control(p, w, outer, s);
       *launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
     }
@@ -641,7 +681,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         if (p.prior == 2) {
           launch_image_learn(p, w, o, s);
         } else {
-          launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
+          launches += launch_learn(p, w, o, c->th >= 1.0 ? o : (int)cap, s);
           if (p.prior) launch_prior_control(p, w, o, s);
         }
         launches += (p.fuse_select ? 1 : 2) + (cap > 8 ? 3 : 2) + (p.prior ? 2 : 0);
@@ -1047,6 +1087,7 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->gr);
   cudaFree(ctx->gc);
   cudaFree(ctx->wbuf);
+  cudaFree(ctx->pw_buf);
   cudaFree(ctx->bc);
   cudaFree(ctx->stage);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -1112,6 +1153,7 @@ int cl_set_virtual_shards(cl_ctx* ctx, int shards) {
   ctx->vshards = shards;
   ctx->wbytes = 0;  // force a fresh workspace carve with the shard buffers
   cudaFree(ctx->wbuf);
+  cudaFree(ctx->pw_buf);
   ctx->wbuf = nullptr;
   return CL_OK;
 }
@@ -1164,6 +1206,12 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
 int cl_set_cluster_learn(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
   ctx->cluster_learn = on < 0 ? 0 : (on > 2 ? 1 : on);
+  return CL_OK;
+}
+
+int cl_set_power_levels(cl_ctx* ctx, int levels) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  ctx->power_levels = levels < 0 ? -1 : std::min(levels, 8);
   return CL_OK;
 }
 

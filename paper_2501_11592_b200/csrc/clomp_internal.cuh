@@ -111,6 +111,11 @@ struct SolveParams {
   // supports of 33..256 atoms learn on CTA clusters with register-resident
   // Gram blocks (k_learn_cluster); 0 keeps them on k_learn_block (tests)
   int32_t cluster_learn;
+  // power form of plain GD for cluster-sized supports (k_pow_sq): E = 2^L q + r
+  // epochs run as r plain steps, L batched squarings of T = I - 2 lr G on the
+  // fp64 tensor cores, then q steps of c <- T^(2^L) c + d_(2^L); the first
+  // pw_slots big-list signals use it (0 levels: per-epoch cluster learning)
+  int32_t pw_levels, pw_q, pw_r, pw_slots, pw_ld;
   // TV-1D prior (single-column solves): the Gram system carries
   // G + w_b H, H = (Delta D_S)^T (Delta D_S) / n, extended by k_prior_ext; the
   // learning kernels store the residual loss and k_prior_control adds w_b c^T H c
@@ -167,6 +172,10 @@ struct Work {
   int32_t* status = nullptr;
   int32_t* changed = nullptr;
   int32_t* big_list = nullptr;     // [B] signals queued for the block learner
+  double* pw_t = nullptr;          // [2][pw_slots][pw_ld][pw_ld] powers T^(2^l) (ping-pong)
+  double* pw_d = nullptr;          // [2][pw_slots][pw_ld] offsets d_(2^l)
+  double* pw_part = nullptr;       // [pw_slots][row chunks] residual sum-of-squares partials
+  int32_t* pw_cnt = nullptr;       // [pw_slots] finished row chunks (reset by the last one)
   int32_t* counters = nullptr;     // see Counter
   double* joint = nullptr;         // see Joint
   // priors (SolveParams::prior)
@@ -281,7 +290,7 @@ void launch_init(const SolveParams& p, const Work& w, const float* y_in,
                  int y_layout, bool y_on_device_signal_major, cudaStream_t s);
 void launch_select(const SolveParams& p, const Work& w, bool full_scores,
                    cudaStream_t s);
-void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
+int launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
                   cudaStream_t s);
 void launch_joint_control(const SolveParams& p, const Work& w, int outer,
                           bool init, cudaStream_t s);

@@ -1736,7 +1736,12 @@ constexpr int cl_min_blocks() { return ((Q == 1 && CW <= 2) || RW == 4) ? 2 : 1;
 __device__ unsigned long long g_cl_trace[8];
 #endif
 
-template <int Q, int CW, int NWC, int RW, int OPT>
+// PH (power form, plain GD, see k_pow_sq): 0 = every epoch here (E = inner);
+// 1 = Gram extension plus the r leftover plain epochs, no residual tail (the
+// squarings follow); 2 = q steps of c <- M c + d with M = T^(2^L), d = d_(2^L)
+// from the power buffers, then the residual tail.  Signals past pw_slots run
+// the PH 0 path inside the PH 1 launch.
+template <int Q, int CW, int NWC, int RW, int OPT, int PH = 0>
 __global__ void __launch_bounds__(32 * NWC, (cl_min_blocks<Q, CW, NWC, RW>()))
 k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
   constexpr int kClThreads = 32 * NWC;
@@ -1780,6 +1785,8 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     const int64_t b = big_list[li];
     const int t = w.cnt[b];
     if (t > kTmax) continue;  // uniform over the cluster: left to k_learn_block
+    const bool pw = PH != 0 && li < p.pw_slots;  // power form for this signal
+    if (PH == 2 && !pw) continue;                // learned by the PH 1 launch
     const int t0 = w.gcnt[b];
     double* G = w.gram + b * cap * cap;
     const float* y = w.y32 + b * p.ldm;
@@ -1826,26 +1833,31 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     __threadfence();
     cl_sync<Q>();  // G, b, fresh coefficients visible to the whole cluster
     if (q == 0 && tid == 0) w.gcnt[b] = t;
+    const int pwb = (p.pw_levels - 1) & 1;  // buffer holding T^(2^L), d_(2^L)
+    const double* gsrc =
+        PH == 2 ? w.pw_t + ((int64_t)pwb * p.pw_slots + li) * p.pw_ld * p.pw_ld : G;
+    const int64_t ldg = PH == 2 ? p.pw_ld : cap;
     double g[RW][CW];
 #pragma unroll
     for (int i = 0; i < RW; ++i)
 #pragma unroll
       for (int j = 0; j < CW; ++j)
-        g[i][j] = (R0 + i < t && C0 + j < t) ? G[(int64_t)(R0 + i) * cap + C0 + j] : 0.0;
+        g[i][j] = (R0 + i < t && C0 + j < t) ? gsrc[(int64_t)(R0 + i) * ldg + C0 + j] : 0.0;
     for (int k = tid; k < t; k += kClThreads) cbuf[0][k] = w.coef[b * cap + k];
     const bool producing = R0 < t;
     const bool owner = (lane & ((1 << kRowShift) - 1)) == 0 && my_row < t;
     double cr = 0.0, bi = 0.0, m1 = 0.0, m2 = 0.0;
     if (my_row < t) {
       cr = w.coef[b * cap + my_row];
-      bi = w.bvec[b * cap + my_row];
+      bi = PH == 2 ? w.pw_d[((int64_t)pwb * p.pw_slots + li) * p.pw_ld + my_row]
+                   : w.bvec[b * cap + my_row];
       m1 = w.mom1[b * cap + my_row];
       m2 = w.mom2[b * cap + my_row];
     }
     uint32_t pc0 = s_phase[0], pc1 = s_phase[1];
     __syncthreads();
     const int step0 = (outer - 1) * p.inner;
-    const int E = p.inner;
+    const int E = !pw ? p.inner : (PH == 1 ? p.pw_r : p.pw_q);
     // Epoch e reads buffer e & 1 and sends its rows' new coefficients into
     // buffer (e + 1) & 1 of every CTA (st.async, completing t * 8 bytes on
     // that CTA's barrier).  A sender has received every row of epoch e's
@@ -1858,7 +1870,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
 #else
 #define CLT(acc) do { } while (0)
 #endif
-    if (producing) {
+    if (producing && E > 0) {
       for (int e = 0; e < E; ++e) {
         const int cur = e & 1, nxt = cur ^ 1;
         if (e > 0) {
@@ -1907,7 +1919,10 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
             bc1 = p.bc1[step0 + e];
             bc2 = p.bc2[step0 + e];
           }
-          opt_step<OPT>(cr, 2.0 * (gc - bi), m1, m2, p.lr, bc1, bc2);
+          if (PH == 2)
+            cr = gc + bi;  // c <- T^(2^L) c + d_(2^L)
+          else
+            opt_step<OPT>(cr, 2.0 * (gc - bi), m1, m2, p.lr, bc1, bc2);
           const uint32_t off = (uint32_t)((nxt * 256 + my_row) * 8);
 #pragma unroll
           for (int r = 0; r < Q; ++r)
@@ -1941,6 +1956,10 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
       w.mom1[b * cap + my_row] = m1;
       w.mom2[b * cap + my_row] = m2;
     }
+    if (pw) {  // PH 1: squarings and PH 2 follow; PH 2: k_pw_resid finishes it
+      cl_sync<Q>();
+      continue;
+    }
     // Residual r = A_S c - y (fp64, rows over the cluster) and its loss.
     const double* cs = cbuf[E & 1];
     double lacc = resid_rows<4>(p, w, b, sups, cs, t, gt, GS);
@@ -1973,6 +1992,353 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     if (s_snap)
       for (int k = gt; k < t; k += GS) w.best_coef[b * cap + k] = cs[k];
     cl_sync<Q>();  // smem (sups, cbuf, lpart) free for the next signal
+  }
+}
+
+// ------------------------------- power form for cluster-sized supports
+// Plain GD is affine, c <- T c + d with T = I - 2 lr G, d = 2 lr b
+// (clomp.cpp:87-90, 178-181); E = 2^L q + r epochs equal r plain steps followed
+// by q steps of c <- T^(2^L) c + d_(2^L) in exact arithmetic (the maps commute:
+// both are c* + T^k (c - c*)).  k_learn_warp does this inside one warp for
+// t <= 32; here the squarings of the 33..256-atom systems of the whole big
+// list run as one batched fp64 tensor-core GEMM per level (mma.sync m8n8k4 f64
+// -> DMMA), so the cluster kernel's latency-bound epoch chain shrinks from E
+// to r + q steps.  Level l reads M_l (l = 0: T, built from G on load) and
+// d_l, writes M_(l+1) = M_l^2 (upper 64 x 64 block triangle, mirrored: the
+// powers of a symmetric T are symmetric) and d_(l+1) = d_l + M_l d_l.
+// CTA = one 64 x 64 output block of one signal, 4 warps of 32 x 32 (4 x 4
+// DMMA tiles each), k in chunks of 32 through padded shared memory (rows of
+// 36 doubles: every fragment load is two conflict-free wavefronts).
+constexpr int kPwTile = 64;
+constexpr int kPwKc = 32;
+constexpr int kPwThreads = 128;
+constexpr int kPwSmem = 4 * kPwTile * (kPwKc + 4) * 8;  // 2 stages x 2 panels
+
+// Gram extension of the power-form signals (the first pw_slots of the big
+// list with t <= tmax), one warp per signal: the new rows / columns of G and
+// b_k = a_k . y for the atoms injected this iteration, new coefficients 0
+// (clomp.hpp:53-54).  Same arithmetic as k_learn_cluster's extension.
+__global__ void __launch_bounds__(128)
+k_pw_extend(SolveParams p, Work w, int outer, const int32_t* big_list, int tmax) {
+  pdl_wait();
+  pdl_trigger();
+  const int count = min(w.counters[kBigCount + (outer & 1)], p.pw_slots);
+  const int lane = threadIdx.x & 31;
+  const int li = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (li >= count) return;
+  const int64_t b = big_list[li];
+  const int t = w.cnt[b];
+  if (t > tmax) return;
+  const int t0 = w.gcnt[b];
+  const int64_t cap = p.cap;
+  double* G = w.gram + b * cap * cap;
+  const int32_t* sup = w.sup + b * cap;
+  const float* y = w.y32 + b * p.ldm;
+  for (int k = t0; k < t; ++k) {
+    const int64_t jk = sup[k];
+    const float* ak = w.at32 + jk * p.ldm;
+    if (w.gfull) {
+      for (int i = lane; i <= k; i += 32) {
+        const double v = w.gfull[jk * p.n + sup[i]];
+        G[(int64_t)k * cap + i] = v;
+        G[(int64_t)i * cap + k] = v;
+      }
+    } else {
+      for (int i = 0; i <= k; ++i) {
+        const float* ai = w.at32 + (int64_t)sup[i] * p.ldm;
+        double acc = 0.0;
+        for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(ai[m]), acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          G[(int64_t)k * cap + i] = acc;
+          G[(int64_t)i * cap + k] = acc;
+        }
+      }
+    }
+    double acc = 0.0;
+    for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(y[m]), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      w.bvec[b * cap + k] = acc;
+      w.coef[b * cap + k] = 0.0;
+      w.mom1[b * cap + k] = 0.0;
+      w.mom2[b * cap + k] = 0.0;
+    }
+  }
+  if (lane == 0) w.gcnt[b] = t;
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kPwThreads, 3)
+k_pow_sq(SolveParams p, Work w, int outer, const int32_t* big_list, int level, int tmax,
+         int nt) {
+  // two k-chunk stages of both 64-row panels (cp.async ring), dynamic smem
+  extern __shared__ __align__(16) double pw_smem[];
+  typedef double Panel[kPwTile][kPwKc + 4];
+  Panel* As = reinterpret_cast<Panel*>(pw_smem);
+  Panel* Bs = As + 2;
+  pdl_wait();
+  pdl_trigger();
+  const int count = min(w.counters[kBigCount + (outer & 1)], p.pw_slots);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row / column
+  const double twolr = 2.0 * p.lr;
+  const int64_t ld = p.pw_ld;
+  // output block (I, J), J >= I, of the upper block triangle of an nt x nt grid
+  int I = 0, J = 0;
+  {
+    int x = blockIdx.x;
+    for (I = 0; I < nt; ++I) {
+      if (x < nt - I) {
+        J = I + x;
+        break;
+      }
+      x -= nt - I;
+    }
+  }
+  const bool from_g = level == 0;
+  for (int li = blockIdx.y; li < count; li += gridDim.y) {
+    const int64_t b = big_list[li];
+    const int t = w.cnt[b];
+    if (t > tmax || J * kPwTile >= t) continue;  // uniform per CTA
+    const double* src = from_g ? w.gram + b * p.cap * p.cap
+                               : w.pw_t + ((int64_t)((level - 1) & 1) * p.pw_slots + li) * ld * ld;
+    const int64_t lds = from_g ? p.cap : ld;
+    double* dst = w.pw_t + ((int64_t)(level & 1) * p.pw_slots + li) * ld * ld;
+    const bool aligned = !from_g || (p.cap & 1) == 0;
+    // stage chunk kc of rows I / J: 16-byte copies, zero-filled outside t x t
+    auto issue = [&](int chunk) {
+      const int st = chunk & 1, k0 = chunk * kPwKc;
+#pragma unroll
+      for (int e = tid; e < kPwTile * kPwKc / 2; e += kPwThreads) {
+        const int r = e / (kPwKc / 2), c = 2 * (e % (kPwKc / 2));
+        const int k = k0 + c;
+        const int kb = k < t ? (k + 1 < t ? 16 : 8) : 0;
+        const int ra = I * kPwTile + r, rb = J * kPwTile + r;
+        const double* pa = src + (int64_t)(ra < t ? ra : 0) * lds + (kb ? k : 0);
+        const double* pb = src + (int64_t)(rb < t ? rb : 0) * lds + (kb ? k : 0);
+        if (aligned) {
+          cp_async16_zfill(&As[st][r][c], pa, ra < t ? kb : 0);
+          cp_async16_zfill(&Bs[st][r][c], pb, rb < t ? kb : 0);
+        } else {  // odd row stride (G with odd cap): 8-byte copies
+          const int k1 = kb == 16 ? 8 : 0;
+          cp_async8_zfill(&As[st][r][c], pa, ra < t && kb ? 8 : 0);
+          cp_async8_zfill(&As[st][r][c + 1], pa + (k1 ? 1 : 0), ra < t ? k1 : 0);
+          cp_async8_zfill(&Bs[st][r][c], pb, rb < t && kb ? 8 : 0);
+          cp_async8_zfill(&Bs[st][r][c + 1], pb + (k1 ? 1 : 0), rb < t ? k1 : 0);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    const int nchunk = (t + kPwKc - 1) / kPwKc;
+    issue(0);
+    for (int ch = 0; ch < nchunk; ++ch) {
+      const int st = ch & 1;
+      if (ch + 1 < nchunk) {
+        issue(ch + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      if (from_g) {  // T = I - 2 lr G on the staged entries (zeros stay zero)
+        const int k0 = ch * kPwKc;
+        for (int e = tid; e < kPwTile * kPwKc; e += kPwThreads) {
+          const int r = e / kPwKc, c = e % kPwKc, k = k0 + c;
+          const int ra = I * kPwTile + r, rb = J * kPwTile + r;
+          if (k < t) {
+            if (ra < t) As[st][r][c] = ra == k ? 1.0 - twolr * As[st][r][c] : -(twolr * As[st][r][c]);
+            if (rb < t) Bs[st][r][c] = rb == k ? 1.0 - twolr * Bs[st][r][c] : -(twolr * Bs[st][r][c]);
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int ks = 0; ks < kPwKc / 4; ++ks) {
+        double fa[4], fb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          fa[i] = As[st][wm * 32 + i * 8 + fr][ks * 4 + fc];
+          fb[i] = Bs[st][wn * 32 + i * 8 + fr][ks * 4 + fc];
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+                : "d"(fa[mi]), "d"(fb[ni]));
+      }
+      __syncthreads();  // stage st is refilled by the next issue
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int row = I * kPwTile + wm * 32 + mi * 8 + fr;
+        const int col = J * kPwTile + wn * 32 + ni * 8 + 2 * fc;
+        if (row < t) {
+          if (col + 1 < t) {
+            *reinterpret_cast<double2*>(dst + (int64_t)row * ld + col) =
+                make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+          } else if (col < t) {
+            dst[(int64_t)row * ld + col] = acc[mi][ni][0];
+          }
+          if (I != J) {
+            if (col < t) dst[(int64_t)col * ld + row] = acc[mi][ni][0];
+            if (col + 1 < t) dst[(int64_t)(col + 1) * ld + row] = acc[mi][ni][1];
+          }
+        }
+      }
+    if (I == J) {
+      // d_(l+1) = d_l + M_l d_l on this block's rows (d_0 = 2 lr b)
+      const double* dsrc = from_g ? w.bvec + b * p.cap
+                                  : w.pw_d + ((int64_t)((level - 1) & 1) * p.pw_slots + li) * ld;
+      double* ddst = w.pw_d + ((int64_t)(level & 1) * p.pw_slots + li) * ld;
+      const double dscale = from_g ? twolr : 1.0;
+      for (int rr = 0; rr < kPwTile / 4; ++rr) {
+        const int i = I * kPwTile + warp * (kPwTile / 4) + rr;
+        if (i >= t) break;
+        const double* mrow = src + (int64_t)i * lds;
+        double a = 0.0;
+        for (int k = lane; k < t; k += 32) {
+          const double v = mrow[k];
+          const double mik = !from_g ? v : (i == k ? 1.0 - twolr * v : -(twolr * v));
+          a = fma(mik, dscale * dsrc[k], a);
+        }
+        a = warp_sum(a);
+        if (lane == 0) ddst[i] = dscale * dsrc[i] + a;
+      }
+    }
+  }
+}
+
+// Residual tail of the power-form signals after the PH 2 epochs (what
+// k_learn_cluster's tail does for the others): r = A_S c - y in fp64 over
+// row chunks of 512 — one CTA each, four consecutive rows per thread (float4
+// atom loads, eight atoms in flight), many CTAs per SM so the gathers of the
+// 33..256-atom supports overlap — and per-chunk loss partials.  The last CTA
+// of a signal sums them in chunk order, runs the stopping rules
+// (clomp.cpp:253-273, eps test :238-242), writes the fp16 split for the next
+// K1 and the best snapshot.
+constexpr int kPwResThreads = 128;
+constexpr int kPwResRows = 4 * kPwResThreads;
+
+__global__ void __launch_bounds__(kPwResThreads)
+k_pw_resid(SolveParams p, Work w, int outer, const int32_t* big_list, int tmax) {
+  __shared__ __align__(16) double cs[256];
+  __shared__ int32_t ss[256];
+  __shared__ double red[kPwResThreads / 32];
+  __shared__ double s_L;
+  __shared__ int s_last, s_snap;
+  pdl_wait();
+  pdl_trigger();
+  const int count = min(w.counters[kBigCount + (outer & 1)], p.pw_slots);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunk = (int)((p.ldm + kPwResRows - 1) / kPwResRows);
+  const int64_t cap = p.cap, ldm = p.ldm;
+  for (int li = blockIdx.y; li < count; li += gridDim.y) {
+    const int64_t b = big_list[li];
+    const int t = w.cnt[b];
+    if (t > tmax) continue;  // uniform per CTA
+    for (int k = tid; k < t; k += kPwResThreads) {
+      cs[k] = w.coef[b * cap + k];
+      ss[k] = w.sup[b * cap + k];
+    }
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * kPwResRows + 4 * tid;
+    double lacc = 0.0;
+    if (i0 < ldm) {  // ldm is a multiple of 128: rows i0 .. i0 + 3 all exist
+      double r[4] = {0.0, 0.0, 0.0, 0.0};
+      int k = 0;
+      for (; k + 8 <= t; k += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z)
+          v[z] = *reinterpret_cast<const float4*>(w.at32 + (int64_t)ss[k + z] * ldm + i0);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) {
+          const double c = cs[k + z];
+          r[0] = fma(f2d(v[z].x), c, r[0]);
+          r[1] = fma(f2d(v[z].y), c, r[1]);
+          r[2] = fma(f2d(v[z].z), c, r[2]);
+          r[3] = fma(f2d(v[z].w), c, r[3]);
+        }
+      }
+      for (; k < t; ++k) {
+        const float4 v = *reinterpret_cast<const float4*>(w.at32 + (int64_t)ss[k] * ldm + i0);
+        const double c = cs[k];
+        r[0] = fma(f2d(v.x), c, r[0]);
+        r[1] = fma(f2d(v.y), c, r[1]);
+        r[2] = fma(f2d(v.z), c, r[2]);
+        r[3] = fma(f2d(v.w), c, r[3]);
+      }
+      const float4 yv = *reinterpret_cast<const float4*>(w.y32 + b * ldm + i0);
+      r[0] -= f2d(yv.x);
+      r[1] -= f2d(yv.y);
+      r[2] -= f2d(yv.z);
+      r[3] -= f2d(yv.w);
+      *reinterpret_cast<double2*>(w.r64 + b * ldm + i0) = make_double2(r[0], r[1]);
+      *reinterpret_cast<double2*>(w.r64 + b * ldm + i0 + 2) = make_double2(r[2], r[3]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) lacc = fma(r[e], r[e], lacc);
+    }
+    lacc = warp_sum(lacc);
+    if (lane == 0) red[warp] = lacc;
+    __syncthreads();
+    if (tid == 0) {
+      double part = 0.0;
+      for (int q = 0; q < kPwResThreads / 32; ++q) part += red[q];
+      w.pw_part[(int64_t)li * nchunk + blockIdx.x] = part;
+      __threadfence();
+      s_last = atomicAdd(&w.pw_cnt[li], 1) == nchunk - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // every chunk's rows and partial are visible
+      __threadfence();
+      if (tid == 0) {
+        double L = 0.0;
+        for (int q = 0; q < nchunk; ++q) L += __ldcg(&w.pw_part[(int64_t)li * nchunk + q]);
+        w.pw_cnt[li] = 0;
+        int snap = 0;
+        if (p.mode == kModePerSignal)
+          snap = control_signal(p, w, b, outer, L);
+        else
+          w.loss[b] = L;
+        s_L = L;
+        s_snap = snap;
+      }
+      __syncthreads();
+      if (w.r_hi) {
+        const float sc = split_scale(s_L);
+        if (tid == 0) w.r_scale[b] = 1.0f / sc;
+        for (int64_t i = tid; i < ldm; i += kPwResThreads)
+          split_f16(__ldcg(&w.r64[b * ldm + i]), sc, w.r_hi[b * ldm + i], w.r_lo[b * ldm + i]);
+      }
+      if (s_snap)
+        for (int k = tid; k < t; k += kPwResThreads) w.best_coef[b * cap + k] = cs[k];
+    }
+    __syncthreads();  // cs / ss / flags reused by the next signal
   }
 }
 
@@ -2655,7 +3021,7 @@ static void launch_block_variant(const SolveParams& p, const Work& w, int outer,
 
 template <int Q, int CW, int NWC, int RW>
 static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int32_t* big_list,
-                             int nclusters, cudaStream_t s) {
+                             int nclusters, cudaStream_t s, int ph = 0) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Q, (unsigned)nclusters);
   cfg.blockDim = dim3(32 * NWC);
@@ -2675,6 +3041,14 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
   cfg.attrs = at;
   cfg.numAttrs = na;
   const int32_t* bl = big_list;
+  if (ph == 1) {
+    cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 0, 1>, p, w, outer, bl);
+    return;
+  }
+  if (ph == 2) {
+    cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 0, 2>, p, w, outer, bl);
+    return;
+  }
   switch (p.opt) {
     case 0: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 0>, p, w, outer, bl); break;
     case 1: cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 1>, p, w, outer, bl); break;
@@ -2685,18 +3059,47 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
 // Cluster learning for supports of 33..256 atoms: returns the support size
 // up to which it learns this iteration (0 when not launched).  One CTA per
 // signal up to 128 atoms (64: 8 warps x 2 columns per lane; 128: 16 warps x 4),
-// four-CTA clusters up to 256.
+// four-CTA clusters up to 256.  With the power form (plain GD, p.pw_levels >
+// 0) the variant runs twice around the batched squarings (PH 1 / PH 2); *extra
+// counts the additional launches.
 static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
-                                int64_t nsig, int sms, cudaStream_t s) {
+                                int64_t nsig, int sms, cudaStream_t s, int* extra) {
   if (p.sep || max_cnt <= kWarpCap || p.cluster_learn == 0) return 0;
   auto nc = [&](int q) { return (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / q)); };
+  const bool pw = p.pw_levels > 0 && p.opt == 0 && p.cluster_learn != 2;
+  auto run = [&](auto launch, int tmax) {
+    if (!pw) {
+      launch(0);
+      return;
+    }
+    const int64_t nbig = std::min<int64_t>(nsig, p.pw_slots);
+    launch_pdl(k_pw_extend, dim3((unsigned)((nbig + 3) / 4)), dim3(128), 0, s, p, w, outer,
+               (const int32_t*)w.big_list, tmax);
+    const bool ph1 = p.pw_r > 0 || nsig > p.pw_slots;  // leftover epochs / signals
+    if (ph1) launch(1);
+    const int nt = (tmax + kPwTile - 1) / kPwTile;
+    const int sig_grid = (int)std::min<int64_t>(std::min<int64_t>(nsig, p.pw_slots),
+                                                (int64_t)sms * 16);
+    cudaFuncSetAttribute(k_pow_sq, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
+    for (int l = 0; l < p.pw_levels; ++l)
+      launch_pdl(k_pow_sq, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)std::max(sig_grid, 1)),
+                 dim3(kPwThreads), kPwSmem, s, p, w, outer, (const int32_t*)w.big_list, l, tmax, nt);
+    launch(2);
+    const int nchunk = (int)((p.ldm + kPwResRows - 1) / kPwResRows);
+    launch_pdl(k_pw_resid, dim3((unsigned)nchunk, (unsigned)std::max<int64_t>(1, nbig)),
+               dim3(kPwResThreads), 0, s, p, w, outer, (const int32_t*)w.big_list, tmax);
+    *extra += 2 + (ph1 ? 1 : 0) + p.pw_levels;
+  };
   if (max_cnt <= 64) {
-    launch_cluster_q<1, 2, 8, 8>(p, w, outer, w.big_list,
-                                 (int)std::min<int64_t>(nsig, 2 * (int64_t)sms), s);
+    run([&](int ph) {
+      launch_cluster_q<1, 2, 8, 8>(p, w, outer, w.big_list,
+                                   (int)std::min<int64_t>(nsig, 2 * (int64_t)sms), s, ph);
+    }, 64);
     return 64;
   }
   if (max_cnt <= 128) {
-    launch_cluster_q<1, 4, 16, 8>(p, w, outer, w.big_list, nc(1), s);
+    run([&](int ph) { launch_cluster_q<1, 4, 16, 8>(p, w, outer, w.big_list, nc(1), s, ph); },
+        128);
     return 128;
   }
   if (p.cluster_learn == 2) {
@@ -2708,12 +3111,13 @@ static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, 
                                  s);
     return 256;
   }
-  launch_cluster_q<4, 8, 8, 8>(p, w, outer, w.big_list, nc(4), s);
+  run([&](int ph) { launch_cluster_q<4, 8, 8, 8>(p, w, outer, w.big_list, nc(4), s, ph); }, 256);
   return 256;
 }
 
-void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
-                  cudaStream_t s) {
+int launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
+                 cudaStream_t s) {
+  int extra = 0;  // launches beyond learn (+ residual) + cluster + block
   int32_t* big_list = w.big_list;
   // max_cnt: upper bound on the support size after this iteration's select
   // (ties can exceed it; those signals fall through to the block kernel).
@@ -2751,13 +3155,14 @@ void launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(nsig < 2 * sms ? nsig : 2 * sms);
-    const int skip_le = launch_cluster_learn(p, w, outer, max_cnt, nsig, sms, s);
+    const int skip_le = launch_cluster_learn(p, w, outer, max_cnt, nsig, sms, s, &extra);
     switch (p.opt) {
       case 0: launch_block_variant<0>(p, w, outer, big_list, grid, skip_le, s); break;
       case 1: launch_block_variant<1>(p, w, outer, big_list, grid, skip_le, s); break;
       default: launch_block_variant<2>(p, w, outer, big_list, grid, skip_le, s); break;
     }
   }
+  return extra;
 }
 
 int cluster_trace(unsigned long long* out) {

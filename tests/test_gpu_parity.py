@@ -271,6 +271,39 @@ def test_cluster_learning_vs_oracle_and_block_kernel(gpu_available, K, opt):
         assert np.array_equal(r.mask, r0.mask)
         assert np.array_equal(r.iterations, r0.iterations)
         assert rel_coef_err(r.s, r0.s) <= 1e-9
+    if opt == cl.PLAIN:  # power form (batched DMMA squarings) vs per-epoch cluster learning
+        ctx.set_cluster_learn(1)
+        for levels in (0, 1, 2, 4):
+            ctx.set_power_levels(levels)
+            r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+            assert np.array_equal(r.mask, r0.mask)
+            assert np.array_equal(r.iterations, r0.iterations)
+            assert rel_coef_err(r.s, r0.s) <= 1e-9
+
+
+@pytest.mark.parametrize("inner,mode", [(203, cl.MODE_PER_SIGNAL), (200, cl.MODE_JOINT),
+                                        (5, cl.MODE_PER_SIGNAL)])
+def test_power_form_cluster_vs_oracle(gpu_available, inner, mode):
+    """Power form on cluster-sized supports with leftover plain epochs
+    (E = 203 = 8 * 25 + 3), in joint mode, and with E < 2^L (levels
+    clamped): supports, iterations and coefficients against the oracle."""
+    m, n, B, K = 512, 1024, 4, 72
+    A, X, Y, _ = cl.gen_problem_1d(77 + inner, m, n, K, B, value_law=1)
+    cfg = cl.ClompConfig.baseline(K)
+    cfg.inner_steps = inner
+    ctx = make_ctx(A, "tc")
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
+    assert np.all(r.status == 0)
+    ref = refbind.orc_solve(A.astype(np.float64), Y.astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL if mode == cl.MODE_PER_SIGNAL
+                            else refbind.MODE_JOINT)
+    assert np.array_equal(r.mask, ref["mask"])
+    assert np.array_equal(r.iterations, ref["iterations"])
+    assert rel_coef_err(r.s, ref["s"]) <= 1e-9
+    ctx.set_power_levels(0)
+    r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
+    assert np.array_equal(r.mask, r0.mask)
+    assert rel_coef_err(r.s, r0.s) <= 1e-9
 
 
 def test_priors_default_config_per_signal_vs_oracle(gpu_available):
