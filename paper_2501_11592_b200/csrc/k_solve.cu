@@ -2009,45 +2009,54 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
 // CTA = one 64 x 64 output block of one signal, 4 warps of 32 x 32 (4 x 4
 // DMMA tiles each), k in chunks of 32 through padded shared memory (rows of
 // 36 doubles: every fragment load is two conflict-free wavefronts).
+#ifndef CL_PW_MINB
+#define CL_PW_MINB 4
+#endif
 constexpr int kPwTile = 64;
-constexpr int kPwKc = 32;
+#ifndef CL_PW_KC
+#define CL_PW_KC 16
+#endif
+constexpr int kPwKc = CL_PW_KC;
 constexpr int kPwThreads = 128;
 constexpr int kPwSmem = 4 * kPwTile * (kPwKc + 4) * 8;  // 2 stages x 2 panels
 
 // Gram extension of the power-form signals (the first pw_slots of the big
-// list with t <= tmax), one warp per signal: the new rows / columns of G and
+// list with t <= tmax), one CTA per signal: the new rows / columns of G and
 // b_k = a_k . y for the atoms injected this iteration, new coefficients 0
-// (clomp.hpp:53-54).  Same arithmetic as k_learn_cluster's extension.
-__global__ void __launch_bounds__(128)
+// (clomp.hpp:53-54).
+constexpr int kPwExtThreads = 128;
+
+__global__ void __launch_bounds__(kPwExtThreads)
 k_pw_extend(SolveParams p, Work w, int outer, const int32_t* big_list, int tmax) {
+  __shared__ double red[kPwExtThreads / 32];
   pdl_wait();
   pdl_trigger();
   const int count = min(w.counters[kBigCount + (outer & 1)], p.pw_slots);
-  const int lane = threadIdx.x & 31;
-  const int li = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int li = blockIdx.x;
   if (li >= count) return;
   const int64_t b = big_list[li];
   const int t = w.cnt[b];
   if (t > tmax) return;
   const int t0 = w.gcnt[b];
-  const int64_t cap = p.cap;
+  const int64_t cap = p.cap, ldm = p.ldm;
   double* G = w.gram + b * cap * cap;
   const int32_t* sup = w.sup + b * cap;
-  const float* y = w.y32 + b * p.ldm;
+  const float* y = w.y32 + b * ldm;
   for (int k = t0; k < t; ++k) {
     const int64_t jk = sup[k];
-    const float* ak = w.at32 + jk * p.ldm;
+    const float* ak = w.at32 + jk * ldm;
     if (w.gfull) {
-      for (int i = lane; i <= k; i += 32) {
+      for (int i = tid; i <= k; i += kPwExtThreads) {
         const double v = w.gfull[jk * p.n + sup[i]];
         G[(int64_t)k * cap + i] = v;
         G[(int64_t)i * cap + k] = v;
       }
     } else {
-      for (int i = 0; i <= k; ++i) {
-        const float* ai = w.at32 + (int64_t)sup[i] * p.ldm;
+      for (int i = warp; i <= k; i += kPwExtThreads / 32) {
+        const float* ai = w.at32 + (int64_t)sup[i] * ldm;
         double acc = 0.0;
-        for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(ai[m]), acc);
+        for (int64_t m = lane; m < ldm; m += 32) acc = fma(f2d(ak[m]), f2d(ai[m]), acc);
         acc = warp_sum(acc);
         if (lane == 0) {
           G[(int64_t)k * cap + i] = acc;
@@ -2056,16 +2065,28 @@ k_pw_extend(SolveParams p, Work w, int outer, const int32_t* big_list, int tmax)
       }
     }
     double acc = 0.0;
-    for (int64_t m = lane; m < p.ldm; m += 32) acc = fma(f2d(ak[m]), f2d(y[m]), acc);
+    for (int64_t m = 4 * tid; m < ldm; m += 4 * kPwExtThreads) {
+      const float4 a = *reinterpret_cast<const float4*>(ak + m);
+      const float4 v = *reinterpret_cast<const float4*>(y + m);
+      acc = fma(f2d(a.x), f2d(v.x), acc);
+      acc = fma(f2d(a.y), f2d(v.y), acc);
+      acc = fma(f2d(a.z), f2d(v.z), acc);
+      acc = fma(f2d(a.w), f2d(v.w), acc);
+    }
     acc = warp_sum(acc);
-    if (lane == 0) {
-      w.bvec[b * cap + k] = acc;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double bk = 0.0;
+      for (int q = 0; q < kPwExtThreads / 32; ++q) bk += red[q];
+      w.bvec[b * cap + k] = bk;
       w.coef[b * cap + k] = 0.0;
       w.mom1[b * cap + k] = 0.0;
       w.mom2[b * cap + k] = 0.0;
     }
+    __syncthreads();
   }
-  if (lane == 0) w.gcnt[b] = t;
+  if (tid == 0) w.gcnt[b] = t;
 }
 
 __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
@@ -2082,7 +2103,7 @@ __device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int 
                : "memory");
 }
 
-__global__ void __launch_bounds__(kPwThreads, 3)
+__global__ void __launch_bounds__(kPwThreads, CL_PW_MINB)
 k_pow_sq(SolveParams p, Work w, int outer, const int32_t* big_list, int level, int tmax,
          int nt) {
   // two k-chunk stages of both 64-row panels (cp.async ring), dynamic smem
@@ -3073,7 +3094,7 @@ static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, 
       return;
     }
     const int64_t nbig = std::min<int64_t>(nsig, p.pw_slots);
-    launch_pdl(k_pw_extend, dim3((unsigned)((nbig + 3) / 4)), dim3(128), 0, s, p, w, outer,
+    launch_pdl(k_pw_extend, dim3((unsigned)std::max<int64_t>(1, nbig)), dim3(kPwExtThreads), 0, s, p, w, outer,
                (const int32_t*)w.big_list, tmax);
     const bool ph1 = p.pw_r > 0 || nsig > p.pw_slots;  // leftover epochs / signals
     if (ph1) launch(1);
