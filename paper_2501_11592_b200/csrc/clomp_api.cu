@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -498,7 +499,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                      ctx->cluster_learn == 1 && cap > kWarpCap;
     if (use) {
       const int64_t ld = std::min<int64_t>(256, (cap + 63) / 64 * 64);
-      const int64_t slots = std::min<int64_t>(nsig, 1024);
+      // big-list slots with power buffers (signals past them learn per epoch);
+      // CL_PW_MAX_SLOTS lowers the cap (tests exercise the overflow path)
+      const char* env_slots = getenv("CL_PW_MAX_SLOTS");
+      const int64_t max_slots = env_slots ? std::max<int64_t>(1, atoll(env_slots)) : 1024;
+      const int64_t slots = std::min<int64_t>(nsig, max_slots);
       const int64_t nchunk = (ctx->ldm + 511) / 512;  // k_pw_resid row chunks
       const size_t bytes =
           (size_t)(2 * slots * (ld * ld + ld) + slots * nchunk) * sizeof(double) +

@@ -3175,7 +3175,11 @@ int launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)(nsig < 2 * sms ? nsig : 2 * sms);
+#ifndef CL_BLOCK_GRID_DIV
+#define CL_BLOCK_GRID_DIV 1
+#endif
+    const int gmax = std::max(1, 2 * sms / CL_BLOCK_GRID_DIV);
+    const int grid = (int)(nsig < gmax ? nsig : gmax);
     const int skip_le = launch_cluster_learn(p, w, outer, max_cnt, nsig, sms, s, &extra);
     switch (p.opt) {
       case 0: launch_block_variant<0>(p, w, outer, big_list, grid, skip_le, s); break;

@@ -306,6 +306,32 @@ def test_power_form_cluster_vs_oracle(gpu_available, inner, mode):
     assert rel_coef_err(r.s, r0.s) <= 1e-9
 
 
+def test_power_form_slot_overflow(gpu_available, monkeypatch):
+    """Big-list signals past the power-buffer slots learn per epoch inside
+    the same iteration (CL_PW_MAX_SLOTS = 2 of 5 signals): same supports,
+    iterations and coefficients as the all-power and all-per-epoch runs."""
+    m, n, B, K = 512, 1024, 5, 48
+    A, X, Y, _ = cl.gen_problem_1d(91, m, n, K, B, value_law=1)
+    cfg = cl.ClompConfig.baseline(K)
+    cfg.inner_steps = 203
+    ctx = make_ctx(A, "tc")
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    monkeypatch.setenv("CL_PW_MAX_SLOTS", "2")
+    ctx2 = make_ctx(A, "tc")
+    r2 = cl.clomp_solve_batch(ctx2, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    monkeypatch.delenv("CL_PW_MAX_SLOTS")
+    ctx2.set_power_levels(0)
+    r0 = cl.clomp_solve_batch(ctx2, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    for other in (r2, r0):
+        assert np.array_equal(r.mask, other.mask)
+        assert np.array_equal(r.iterations, other.iterations)
+        assert rel_coef_err(r.s, other.s) <= 1e-9
+    ref = refbind.orc_solve(A.astype(np.float64), Y[:, :2].astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL)
+    assert np.array_equal(r.mask[:, :2], ref["mask"])
+    assert rel_coef_err(r.s[:, :2], ref["s"]) <= 1e-9
+
+
 def test_priors_default_config_per_signal_vs_oracle(gpu_available):
     """The reference's default configuration (Adam, th = 0.7, automatic TV / LV
     weights) on a make_setup-style problem (A = Phi D, DCT synthesis basis),
