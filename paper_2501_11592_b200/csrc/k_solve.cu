@@ -1787,6 +1787,9 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     if (t > kTmax) continue;  // uniform over the cluster: left to k_learn_block
     const bool pw = PH != 0 && li < p.pw_slots;  // power form for this signal
     if (PH == 2 && !pw) continue;                // learned by the PH 1 launch
+#ifdef CL_CLUSTER_TRACE
+    const unsigned long long tsig0 = clock64();
+#endif
     const int t0 = w.gcnt[b];
     double* G = w.gram + b * cap * cap;
     const float* y = w.y32 + b * p.ldm;
@@ -1866,6 +1869,7 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
 #ifdef CL_CLUSTER_TRACE
     unsigned long long tw = 0, tf = 0, tr = 0, ts = 0, tcur = clock64();
     const bool tracer = q == 0 && tid == 0;
+    const unsigned long long tpro = tcur - tsig0;  // prologue: loads, extension, syncs
 #define CLT(acc) do { if (tracer) { const unsigned long long x = clock64(); acc += x - tcur; tcur = x; } } while (0)
 #else
 #define CLT(acc) do { } while (0)
@@ -1941,6 +1945,8 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
         atomicAdd(&g_cl_trace[2], tr);
         atomicAdd(&g_cl_trace[3], ts);
         atomicAdd(&g_cl_trace[4], (unsigned long long)E);
+        atomicAdd(&g_cl_trace[5], tpro);
+        atomicAdd(&g_cl_trace[7], 1ull);
       }
 #endif
       const int fin = E & 1;
@@ -1958,6 +1964,9 @@ k_learn_cluster(SolveParams p, Work w, int outer, const int32_t* big_list) {
     }
     if (pw) {  // PH 1: squarings and PH 2 follow; PH 2: k_pw_resid finishes it
       cl_sync<Q>();
+#ifdef CL_CLUSTER_TRACE
+      if (tracer) atomicAdd(&g_cl_trace[6], clock64() - tcur);  // after the epochs
+#endif
       continue;
     }
     // Residual r = A_S c - y (fp64, rows over the cluster) and its loss.
@@ -3061,6 +3070,26 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
   ++na;
   cfg.attrs = at;
   cfg.numAttrs = na;
+  if (Q > 1) {
+    // Clusters must fit inside a GPC: not every SM can host one.  A grid of
+    // more clusters than can be co-resident runs its last clusters in a second
+    // wave (each cluster loops over signals), so cap it at the occupancy.
+    static int max_active = 0;
+    if (max_active == 0) {
+      int nmax = 0;
+      if (cudaOccupancyMaxActiveClusters(&nmax, k_learn_cluster<Q, CW, NWC, RW, 0>, &cfg) !=
+              cudaSuccess ||
+          nmax <= 0) {
+        cudaGetLastError();
+        nmax = -1;
+      }
+      max_active = nmax;
+    }
+    if (max_active > 0 && nclusters > max_active) {
+      nclusters = max_active;
+      cfg.gridDim = dim3(Q, (unsigned)nclusters);
+    }
+  }
   const int32_t* bl = big_list;
   if (ph == 1) {
     cudaLaunchKernelEx(&cfg, k_learn_cluster<Q, CW, NWC, RW, 0, 1>, p, w, outer, bl);

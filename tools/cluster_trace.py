@@ -21,3 +21,6 @@ E = max(int(buf[4]), 1)
 for nm, v in zip(["wait", "fma", "reduce", "step+store"], buf[:4]):
     print(f"{nm:12s} {int(v) / E:8.1f} cycles/epoch")
 print("epochs traced", E)
+S = max(int(buf[7]), 1)
+print(f"per signal: prologue {int(buf[5]) / S:.0f} cycles, after-epochs {int(buf[6]) / S:.0f} cycles, "
+      f"epochs {E / S:.1f}, signals traced {S}")
