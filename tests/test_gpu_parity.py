@@ -428,3 +428,32 @@ def test_image_mode_priors_vs_oracle(gpu_available, cfgd):
         assert np.array_equal(r.iterations, ref["iterations"])
         assert rel_coef_err(r.s, ref["s"]) <= 1e-7
         np.testing.assert_allclose(r.final_residual_norm, ref["final_residual_norm"], rtol=1e-7)
+
+
+def test_tie_grown_supports_fast_path(gpu_available):
+    """Exact ties (duplicated atoms are selected together, clomp.cpp:49-51) grow
+    supports past the 32-atom fast-kernel bucket at config-2 sizes; the fast
+    kernel queues those signals for the block kernel.  Supports, iterations
+    and coefficients match the oracle."""
+    m, n, B, K = 512, 1024, 64, 30
+    A, X, Y, _ = cl.gen_problem_1d(123, m, n, K, B, snr_db=40.0)
+    A = np.array(A)
+    A[:, 1:128:2] = A[:, 0:128:2]  # 64 duplicated atom pairs
+    X = np.zeros((n, B))
+    rng = np.random.default_rng(4)
+    for b in range(B):  # each signal uses 10 duplicated atoms plus 14 others
+        X[rng.choice(np.arange(0, 128, 2), 10, replace=False), b] = rng.standard_normal(10)
+        X[rng.choice(np.arange(128, n), 14, replace=False), b] = rng.standard_normal(14)
+    Y = (A.astype(np.float64) @ X).astype(np.float32)
+    cfg = cl.ClompConfig.baseline(K)
+    ctx = make_ctx(A, "tc")
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.all(r.status == 0)
+    assert int(r.mask.sum(axis=0).max()) > 32  # the tie path ran
+    idx = np.arange(0, B, 4)
+    ref = refbind.orc_solve(A.astype(np.float64), Y[:, idx].astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL)
+    for q, b in enumerate(idx):
+        assert np.array_equal(r.mask[:, b], ref["mask"][:, q]), f"signal {b}: support"
+        assert r.iterations[b] == ref["iterations"][q]
+        assert rel_coef_err(r.s[:, b], ref["s"][:, q]) <= 1e-9
