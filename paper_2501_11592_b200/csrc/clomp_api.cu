@@ -368,8 +368,12 @@ struct OutPtrs {
 
 // The outer loop shared by the host-buffer and device-buffer entry points.
 // y_dev: device pointer, layout_ref ? m x B : B x m.
+// host_sync = false (cl_solve_batch): the fused and graph paths return with
+// the work queued; the caller's one synchronise after its D2H of the results
+// completes them (one host round trip per call instead of two), and it then
+// reads the rescan counter (stats.rescans) from the pinned counter copy.
 int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
-               const cl_config* c, int mode, const OutPtrs& out) {
+               const cl_config* c, int mode, const OutPtrs& out, bool host_sync = true) {
   // K1b: a handful of residuals (the CLI's one-signal-at-a-time path) makes
   // the correlation an HBM-bound GEMV; auto below 9 signals, or forced (3).
   const bool gemv_fit = !ctx->sep && corr_gemv_supported(ctx->ldm, B);
@@ -623,7 +627,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   std::memset(ctx->h_counters, 0, kNumCounters * sizeof(int32_t));
   int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
-  ++launches;
+  launches += (layout_ref && p.B > 1) ? 2 : 1;  // + the tiled transpose of m x B y
   if (p.sep) {  // b values of every atom: Z = A_r^T Y A_c
     launch_sep_corr(p, w, w.y64, w.zb, false, s);
     launches += 2;
@@ -641,7 +645,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     CL_CUDA(ctx, cudaGetLastError());
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, s));
-    CL_CUDA(ctx, cudaStreamSynchronize(s));
+    if (host_sync) CL_CUDA(ctx, cudaStreamSynchronize(s));
     stats.kernel_launches = launches;
     stats.rescans = 0;
     stats.outer_iterations = p.max_outer;
@@ -803,10 +807,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     CL_CUDA(ctx, cudaGetLastError());
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, s));
-    CL_CUDA(ctx, cudaStreamSynchronize(s));
+    if (host_sync) CL_CUDA(ctx, cudaStreamSynchronize(s));
   }
   stats.kernel_launches = launches;
-  stats.rescans = ctx->h_counters[kRescanTotal];
+  stats.rescans = ctx->h_counters[kRescanTotal];  // refreshed by the caller if !host_sync
   stats.outer_iterations = outer_done;
   ctx->stats = stats;
   return CL_OK;
@@ -1442,11 +1446,12 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
     std::memcpy(hy, y, ybytes);
     CL_CUDA(ctx, cudaMemcpyAsync(d_y, hy, ybytes, cudaMemcpyHostToDevice, s));
   }
-  st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o);
+  st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o, false);
   if (st) return st;
   CL_CUDA(ctx, cudaMemcpyAsync(hio, stg + align_up(ybytes, 256), out_bytes,
                                cudaMemcpyDeviceToHost, s));
   CL_CUDA(ctx, cudaStreamSynchronize(s));
+  if (ctx->stats.corr_path != 2) ctx->stats.rescans = ctx->h_counters[kRescanTotal];
   // host views of the compact results (same carving as the device side)
   Carver hv{hio};
   const int32_t* h_sup = hv.take<int32_t>(batch * cap);

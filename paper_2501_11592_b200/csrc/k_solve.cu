@@ -62,17 +62,36 @@ __device__ __forceinline__ void split_row(const Work& w, int64_t b, int64_t ldm,
 }
 
 // ------------------------------------------------------------------ init
+// The reference's m x B layout (element (i, b) at i B + b, linalg.hpp:21-24)
+// to signal-major rows of y32 through a 32 x 32 shared-memory tile, so both
+// the reads and the writes are coalesced (a warp-per-signal strided read of
+// the m x B array cost ~0.2 ms at config 2).
+__global__ void k_transpose_y(const float* __restrict__ y_in, int64_t m, int64_t B,
+                              float* __restrict__ out, int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int64_t b0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, b = b0 + threadIdx.x;
+    if (i < m && b < B) tile[r][threadIdx.x] = y_in[i * B + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t b = b0 + r, i = i0 + threadIdx.x;
+    if (i < m && b < B) out[b * ldo + i] = tile[threadIdx.x][r];
+  }
+}
+
 // One warp per signal: stage y, r = 0 - y = -y (clomp.cpp:236-237 at s = 0),
 // ||y||^2, fresh state, and the outer-1 eps test in per-signal mode.
-__global__ void k_init(SolveParams p, Work w, const float* __restrict__ y_in,
-                       int layout_ref) {
+__global__ void k_init(SolveParams p, Work w, const float* y_in,
+                       int64_t in_ld) {
   const int lane = threadIdx.x & 31;
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= p.B) return;
   double acc = 0.0;
   for (int64_t i = lane; i < p.ldm; i += 32) {
     float v = 0.f;
-    if (i < p.m) v = layout_ref ? y_in[i * p.B + b] : y_in[b * p.m + i];
+    if (i < p.m) v = y_in[b * in_ld + i];
     const int64_t o = b * p.ldm + i;
     w.y32[o] = v;
     w.y64[o] = (double)v;
@@ -3006,7 +3025,14 @@ void launch_init(const SolveParams& p, const Work& w, const float* y_in,
                  int y_layout, bool, cudaStream_t s) {
   const int threads = 256;
   const int64_t blocks = (p.B * 32 + threads - 1) / threads;
-  k_init<<<(unsigned)blocks, threads, 0, s>>>(p, w, y_in, y_layout == 0);
+  int64_t in_ld = p.m;
+  if (y_layout == 0 && p.B > 1) {  // reference m x B: tiled transpose into y32 first
+    const dim3 tg((unsigned)((p.B + 31) / 32), (unsigned)((p.m + 31) / 32));
+    k_transpose_y<<<tg, dim3(32, 8), 0, s>>>(y_in, p.m, p.B, w.y32, p.ldm);
+    y_in = w.y32;
+    in_ld = p.ldm;
+  }
+  k_init<<<(unsigned)blocks, threads, 0, s>>>(p, w, y_in, in_ld);
 }
 
 void launch_split_resid(const SolveParams& p, const Work& w, cudaStream_t s) {
