@@ -559,7 +559,12 @@ def run_ours(args, rank, world, local_rank):
             "kernel": "learning phase (k_learn_fast / k_learn_warp / k_learn_cluster + residual)",
             "bound": "fp64", "achieved": learn_flops / (learn_ms / 1e3) / 1e12,
             "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": learn_flops / (learn_ms / 1e3) / 1e12 / fp64_peak, "traffic": None,
+            "frac": learn_flops / (learn_ms / 1e3) / 1e12 / fp64_peak,
+            "traffic": 42.39e6 if args.config == 2 and prof["corr_path"] == 1 else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch of k_learn_fast<32,0> (the "
+                             "largest learning launch, t = 17..32: 41.1 MB read, 1.3 MB written; "
+                             "the support Gram / state rows and y, the residual halves stay in "
+                             "L2), profiles/r1_cfg2_ncu_full_summary_final.txt"),
             "peak_source": "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x SM clock under load",
             "algorithmic_per_step": (f"B * sum_t (2 E t^2 + 2 m t), t = 1..{outers}, E = {E} "
                                      f"= {learn_flops:.4e} FLOP"),

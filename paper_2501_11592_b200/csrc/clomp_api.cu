@@ -251,6 +251,7 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.changed = cv.take<int32_t>(B);
     w.big_list = cv.take<int32_t>(B);
     w.counters = cv.take<int32_t>(kNumCounters);
+    w.tile_done = cv.take<int32_t>((B + 127) / 128 + 2);
     w.joint = cv.take<double>(kNumJoint);
     if (need_prior) {
       w.hgram = cv.take<double>(B * cap * cap);
@@ -535,6 +536,21 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     }
   }
   p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
+  // CL_TILE_OVERLAP=1: K1 of iteration o + 1 starts a signal tile as soon as
+  // the learning kernels have finished that tile's signals (per-signal th == 1
+  // on the fast learning kernel, supports within one warp).  Correct (GPU suite
+  // green with it) but measured slower at config 2 (2.21 vs 2.07 ms per step:
+  // the early pair CTAs wait on SMs the learning tail still needs), so off by
+  // default.
+  {
+    const bool fast_learn = p.fuse_select && ctx->w.gfull && !p.sep && cap >= 32 && (cap & 1) == 0;
+    const char* env_ov = getenv("CL_TILE_OVERLAP");
+    const bool want = env_ov ? atoi(env_ov) != 0 : false;
+    p.tile_flags = (want && tensor && !colshard && p.mode == CL_MODE_PER_SIGNAL && !prior &&
+                    fast_learn && c->th >= 1.0 && p.max_outer <= kWarpCap && ctx->w.tile_done)
+                       ? 1 : 0;
+    p.tile_wait = 0;
+  }
 
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
@@ -599,9 +615,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       }
       return;
     }
-    if (tensor)
-      launch_corr_tc(p, w, s);
-    else if (gemv)
+    if (tensor) {
+      SolveParams pk = p;
+      pk.tile_wait = p.tile_flags && outer > 1 ? outer - 1 : 0;
+      launch_corr_tc(pk, w, s);
+    } else if (gemv)
       launch_corr_gemv(p, w, full_scores, s);
     else
       launch_corr_f64(p, w, full_scores, s);
@@ -624,6 +642,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   };
 
   CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
+  if (p.tile_flags)
+    CL_CUDA(ctx, cudaMemsetAsync(w.tile_done, 0, (size_t)((B + 127) / 128 + 2) * sizeof(int32_t), s));
   std::memset(ctx->h_counters, 0, kNumCounters * sizeof(int32_t));
   int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);

@@ -125,6 +125,11 @@ struct SolveParams {
   // variance on x = D S (clomp.cpp:93-119), batch-global weights
   double w_tv_g, w_lv_g;
   int32_t lv_on, lv_window, lv_stride, lv_nr, lv_nc;
+  // K1 overlaps the learning tail (per-signal th == 1 fast path): the learning
+  // kernels count finished signals per 128-signal tile in Work::tile_done and
+  // the next K1 starts a tile once its count reaches tile_wait x its signals
+  // (tile_wait = outer - 1; 0 = the plain programmatic wait)
+  int32_t tile_flags, tile_wait;
 };
 
 struct Work {
@@ -177,6 +182,7 @@ struct Work {
   double* pw_part = nullptr;       // [pw_slots][row chunks] residual sum-of-squares partials
   int32_t* pw_cnt = nullptr;       // [pw_slots] finished row chunks (reset by the last one)
   int32_t* counters = nullptr;     // see Counter
+  int32_t* tile_done = nullptr;    // [B/128 + 2] signals finished per K1 signal tile (monotonic per solve)
   double* joint = nullptr;         // see Joint
   // priors (SolveParams::prior)
   const double* ddt = nullptr;     // [n][ldd] Delta D atom-major (fp64)

@@ -487,11 +487,30 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+// K1 may start a signal tile before the learning kernels of the previous
+// iteration have exited (SolveParams::tile_flags): thread 0 waits until the
+// tile's finished-signal count reaches `target` (acquire), then orders the
+// async proxy (TMA) after it.  A bounded spin: past it the plain programmatic
+// wait (predecessor grid complete) is used instead, so a count that never
+// arrives costs time, never correctness.
+__device__ __forceinline__ void wait_tile_ready(const int32_t* flag, int target) {
+  bool ok = target <= 0;
+  for (int i = 0; !ok && i < (1 << 16); ++i) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    ok = v >= target;
+    if (!ok) __nanosleep(64);
+  }
+  if (!ok) pdl_wait();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(32 * kPairWarps, 1)
 k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
            const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
            int64_t n, int64_t B, int kblocks, int64_t ntile, const float* __restrict__ r_scale,
-           double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg) {
+           double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg,
+           const int32_t* tile_done, int tile_wait) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -533,8 +552,17 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
   cluster_sync();  // both CTAs' barriers and TMEM exist before any cross-CTA traffic
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // the residual split of the previous kernel
-  pdl_trigger();
+  if (tile_wait > 0) {  // this tile's residual split, counted by the learners
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+      const int64_t cnt = B - m0 < TM ? (B - m0 > 0 ? B - m0 : 0) : TM;
+      wait_tile_ready(tile_done + blockIdx.x, (int)(tile_wait * cnt));
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();  // the residual split of the previous kernel
+    pdl_trigger();
+  }
   if (threadIdx.x == 0) K1_MARK(1);
 
   if (warp == 0 && lane == 0) {
@@ -589,6 +617,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
 #endif
   tile_epilogue<kPairWarps>(smem, tmem, accum, m0, n0, n, B, ntile, r_scale, a_inv_scale, cand,
                             scores_dbg, warp, lane, blockIdx.y);
+  // early start: this grid completes only after its predecessor (the block
+  // learner), so every later kernel still sees the whole iteration finished
+  if (tile_wait > 0) pdl_wait();
   if (threadIdx.x == 0) K1_MARK(5);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -939,7 +970,8 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, k_corr_tc2, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
                               (int)(p.ldm / BK), p.ntl, (const float*)w.r_scale, p.a_inv_scale,
-                              w.cand, scores_dbg) == cudaSuccess;
+                              w.cand, scores_dbg, (const int32_t*)w.tile_done,
+                              p.tile_flags && p.atom0 == 0 ? (int)p.tile_wait : 0) == cudaSuccess;
   }
   const bool clustered = mtiles >= kCluster;
   const int arows = clustered ? TN / kCluster : TN;

@@ -1168,8 +1168,22 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
 // works on registers (support membership by ballot instead of the mask), the
 // new Gram row comes from gfull and b_k = a_k . y (round trip 2), and the
 // epochs start with everything in registers / shared memory.
+// Signal b is finished for this iteration (residual split, scale, records read):
+// count it for its K1 signal tile (SolveParams::tile_flags).  Every lane's
+// writes are ordered before lane 0's release by the fences and the warp barrier.
+__device__ __forceinline__ void tile_done_warp(const SolveParams& p, const Work& w, int64_t b,
+                                               int lane) {
+  if (!p.tile_flags) return;
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(&w.tile_done[b >> 7], 1);
+  }
+}
+
 template <int TB, int OPT>
-__device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, int64_t b,
+__device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, int64_t b,
                                            int outer, int32_t* big_list, double* cs,
                                            int32_t* sups, double* s1, uint64_t* bar, int lane) {
   const int64_t cap = p.cap;  // >= 32
@@ -1194,7 +1208,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
     ctl.prev_L = w.prev_L[b];
     ctl.stall = w.stall[b];
   }
-  if (!act) return;
+  if (!act) return false;
   const bool staged = t0 <= TB;
   if (staged) stage_gram_bulk(p, w, b, t0, s1, LDS, bar, lane);
 
@@ -1208,7 +1222,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
     select_top_warp(p, w, b, lane);
     if (!w.active[b]) {
       if (staged) mbar_wait0(bar);
-      return;
+      return false;
     }
     t = w.cnt[b];
     chg = w.changed[b];
@@ -1224,7 +1238,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
             w.changed[b] = 0;
           }
           if (staged) mbar_wait0(bar);
-          return;
+          return false;
         }
         if (lane == t_old) sup_l = i1;
         if (lane == 0) {
@@ -1241,7 +1255,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
       select_near_tie(p, w, b, v1, delta, t_old, lane);
       if (!w.active[b]) {
         if (staged) mbar_wait0(bar);
-        return;
+        return false;
       }
       t = w.cnt[b];
       chg = w.changed[b];
@@ -1256,7 +1270,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
       big_list[slot] = (int32_t)b;
     }
     if (staged) mbar_wait0(bar);
-    return;
+    return true;  // k_learn_block finishes it (and counts it for K1)
   }
 
   // round trip 2: Gram row / column of the new atoms from gfull, b_k = a_k . y
@@ -1321,6 +1335,7 @@ __device__ __forceinline__ void learn_fast(const SolveParams& p, const Work& w, 
   }
   snap = __shfl_sync(kFull, snap, 0);
   if (snap && lane < t) w.best_coef[b * p.cap + lane] = c;
+  return false;
 }
 
 template <int TB>
@@ -1402,8 +1417,9 @@ k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi) return;
-  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp], sq_all[warp],
-                      &bar_all[warp], lane);
+  const bool queued = learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp],
+                                         sq_all[warp], &bar_all[warp], lane);
+  if (!queued) tile_done_warp(p, w, b, lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -1425,8 +1441,15 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
   __shared__ double s_L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kBlockThreads / 32;
-  pdl_wait();
-  pdl_trigger();
+  // tile_flags: trigger first, so the next K1 may start the tiles whose signals
+  // are done while this kernel still waits for the learner
+  if (p.tile_flags) {
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
   const int count = w.counters[kBigCount + (outer & 1)];
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kBigCount + ((outer + 1) & 1)] = 0;
   const int64_t cap = p.cap;
@@ -1592,7 +1615,12 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
     if (w.r_hi) split_row(w, b, p.ldm, s_L, tid, kBlockThreads);  // own r64 entries
     if (snap_s)
       for (int i = tid; i < t; i += kBlockThreads) w.best_coef[b * cap + i] = cs[i];
+    if (p.tile_flags) __threadfence();
     __syncthreads();
+    if (p.tile_flags && tid == 0) {  // this big signal is done: count it for K1
+      __threadfence();
+      atomicAdd(&w.tile_done[b >> 7], 1);
+    }
   }
 }
 
