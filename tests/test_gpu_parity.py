@@ -467,9 +467,16 @@ def test_tile_overlap_mode_identical(gpu_available, monkeypatch):
     m, n, B, K = 512, 1024, 512, 30
     A, X, Y, _ = cl.gen_problem_1d(77, m, n, K, B, snr_db=40.0)
     A = np.array(A)
-    A[:, 1:64:2] = A[:, 0:64:2]  # duplicated atom pairs -> tie-grown supports
-    Y = np.array(Y)
-    Y[:, :64] += A[:, 0:64:2].sum(axis=1, keepdims=True).astype(np.float32) * 0.5
+    A[:, 1:128:2] = A[:, 0:128:2]  # duplicated atom pairs -> tie-grown supports
+    X = np.zeros((n, B))
+    rng = np.random.default_rng(5)
+    for b in range(B):
+        if b % 8 == 0:  # every 8th signal: 10 duplicated atoms plus 14 others
+            X[rng.choice(np.arange(0, 128, 2), 10, replace=False), b] = rng.standard_normal(10)
+            X[rng.choice(np.arange(128, n), 14, replace=False), b] = rng.standard_normal(14)
+        else:
+            X[rng.choice(np.arange(128, n), 24, replace=False), b] = rng.standard_normal(24)
+    Y = (A.astype(np.float64) @ X).astype(np.float32)
     cfg = cl.ClompConfig.baseline(K)
     outs = []
     for flag in ("0", "1"):
