@@ -151,8 +151,9 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
 /* Device-resident variant for throughput: d_y is a device pointer, signal-major
  * B x m fp32 (leading dimension m).  Results are written to device buffers
  * (any may be NULL): support/coef [B][cap], count/iterations(int32)/
- * final_rn/converged/status [B].  Asynchronous on the context stream; call
- * cl_synchronize before reading. */
+ * final_rn/converged/status [B].  Runs on the context stream; the host reads
+ * the active-signal count between graph chunks, so the call returns with the
+ * results written (cl_synchronize afterwards is harmless). */
 typedef struct cl_device_result {
   int64_t cap;
   int32_t* support;
