@@ -369,6 +369,28 @@ struct OutPtrs {
 
 // The outer loop shared by the host-buffer and device-buffer entry points.
 // y_dev: device pointer, layout_ref ? m x B : B x m.
+// Power levels of the warp learners' affine form (k_solve.cu epochs_plain):
+// E = 2^L q + r epochs cost popcount(r) + q matvec steps, L offset doublings
+// and L squarings of T = I - 2 lr G; a squaring on the fp64 tensor cores costs
+// about sq[b] matvec steps for a support bucket of 8 (b + 1) atoms (one 8 x 8
+// output block at 8 atoms, ten at 32).  CL_SQ_COSTS="c8,c16,c24,c32" overrides.
+static void warp_power_levels(int E, int32_t out[4]) {
+  int sq[4] = {5, 5, 5, 5};
+  if (const char* e = getenv("CL_SQ_COSTS"))
+    sscanf(e, "%d,%d,%d,%d", &sq[0], &sq[1], &sq[2], &sq[3]);
+  for (int b = 0; b < 4; ++b) {
+    int best_l = 0, best = E;
+    for (int l = 1; l <= 8; ++l) {
+      const int cost = __builtin_popcount((unsigned)(E & ((1 << l) - 1))) + (1 + sq[b]) * l + (E >> l);
+      if ((E >> l) >= 1 && cost < best) {
+        best = cost;
+        best_l = l;
+      }
+    }
+    out[b] = best_l;
+  }
+}
+
 // host_sync = false (cl_solve_batch): the fused and graph paths return with
 // the work queued; the caller's one synchronise after its D2H of the results
 // completes them (one host round trip per call instead of two), and it then
@@ -466,6 +488,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.stall_patience = (int32_t)std::min<uint64_t>(c->stall_patience, 1u << 30);
   p.opt = c->opt;
   p.inner = (int32_t)c->inner_steps;
+  warp_power_levels(p.inner, p.warp_L);
   p.max_outer = (int32_t)c->max_outer;
   // A one-column joint solve is exactly clomp_solve (clomp.cpp:294-311), so
   // the fused path runs everything with per-signal state.

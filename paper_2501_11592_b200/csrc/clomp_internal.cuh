@@ -130,6 +130,9 @@ struct SolveParams {
   // the next K1 starts a tile once its count reaches tile_wait x its signals
   // (tile_wait = outer - 1; 0 = the plain programmatic wait)
   int32_t tile_flags, tile_wait;
+  // warp learners (plain GD): power levels L for support buckets of 8 / 16 /
+  // 24 / 32 atoms (E = 2^L q + r epochs as L squarings + q + popcount(r) steps)
+  int32_t warp_L[4];
 };
 
 struct Work {

@@ -679,26 +679,11 @@ __device__ __forceinline__ void square_dmma(double* buf, int lane) {
 // c <- T^P c + d_P finish — the same iterate as E single steps in exact
 // arithmetic (c_{k+a} = T^a c_k + d_a composes in any order).  L minimises
 // popcount(r) + L + q dependent matvecs plus L squarings.
-#ifndef CL_SQ_COST
-#define CL_SQ_COST 5
-#endif
-__device__ __forceinline__ int power_levels(int E) {
-  int best_l = 0, best = E;
-  for (int l = 1; l <= 8; ++l) {
-    const int cost = __popc(E & ((1 << l) - 1)) + (1 + CL_SQ_COST) * l + (E >> l);
-    if ((E >> l) >= 1 && cost < best) {
-      best = cost;
-      best_l = l;
-    }
-  }
-  return best_l;
-}
-
 template <int T, int TB>
 __device__ void epochs_plain(double (&g)[TB], double& c, double d, double* cs,
                              double* s1, const SolveParams& p, int lane) {
   const int E = p.inner;
-  const int L = power_levels(E);
+  const int L = p.warp_L[T / 8 - 1];  // host: warp_power_levels (clomp_api.cu)
   int ep = 0;
   if (L == 0) {
     affine_steps<T, TB>(g, c, d, cs, E, &ep);
