@@ -2727,6 +2727,10 @@ k_img_loss(SolveParams p, Work w) {
 // warp learning routine of the batched path, the fp64 residual and the
 // stopping rules, with no kernel boundary between outer iterations.
 constexpr int kFusedThreads = 256;
+#ifndef CL_FUSED_ATOMS
+#define CL_FUSED_ATOMS 32
+#endif
+constexpr int kFusedAtoms = CL_FUSED_ATOMS;  // atoms per warp pass of the correlation (was 8)
 
 template <int OPT>
 __global__ void __launch_bounds__(kFusedThreads)
@@ -2746,17 +2750,19 @@ k_solve_fused(SolveParams p, Work w) {
   __syncthreads();
   double* sc = w.scores + b * p.n;
   for (int outer = 1; outer <= p.max_outer; ++outer) {
-    // K1: exact fp64 scores |a_j . r|, 8 atoms per warp pass (8 independent
-    // dot products keep enough loads in flight to hide L2 latency).
+    // K1: exact fp64 scores |a_j . r|, kFusedAtoms atoms per warp pass (as many
+    // independent dot products as registers allow keep the L2 loads in flight;
+    // config 1's 256 atoms take one pass of the 8 warps).  Each score's
+    // summation order does not depend on the pass width.
     double cmax = 0.0;
-    for (int64_t j0 = warp * 8; j0 < p.n; j0 += nw * 8) {
-      double acc[8];
+    for (int64_t j0 = warp * kFusedAtoms; j0 < p.n; j0 += nw * kFusedAtoms) {
+      double acc[kFusedAtoms];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+      for (int u = 0; u < kFusedAtoms; ++u) acc[u] = 0.0;
       for (int64_t i = 2 * lane; i < p.ldm; i += 64) {
         const double2 r01 = *reinterpret_cast<const double2*>(rs + i);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kFusedAtoms; ++u) {
           if (j0 + u < p.n) {
             const float2 a = *reinterpret_cast<const float2*>(w.at32 + (j0 + u) * p.ldm + i);
             acc[u] = fma(f2d(a.x), r01.x, acc[u]);
@@ -2765,7 +2771,7 @@ k_solve_fused(SolveParams p, Work w) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kFusedAtoms; ++u) {
         const double v = fabs(warp_sum(acc[u]));
         if (j0 + u < p.n) {
           if (lane == 0) sc[j0 + u] = v;
