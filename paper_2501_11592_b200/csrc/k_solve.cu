@@ -2731,12 +2731,19 @@ constexpr int kFusedThreads = 256;
 #define CL_FUSED_ATOMS 32
 #endif
 constexpr int kFusedAtoms = CL_FUSED_ATOMS;  // atoms per warp pass of the correlation (was 8)
+#ifndef CL_FUSED_STAGE_MAX
+#define CL_FUSED_STAGE_MAX (200 * 1024)
+#endif
+constexpr int kFusedStageMax = CL_FUSED_STAGE_MAX;  // dynamic smem cap for the staged dictionary
 
 template <int OPT>
 __global__ void __launch_bounds__(kFusedThreads)
-k_solve_fused(SolveParams p, Work w) {
+k_solve_fused(SolveParams p, Work w, int stage_a) {
   extern __shared__ __align__(16) unsigned char fsm[];
   double* rs = reinterpret_cast<double*>(fsm);                 // [ldm] residual
+  // stage_a: the whole fp32 dictionary (atom-major, n x ldm) staged once into
+  // shared memory behind rs, so the per-iteration correlation and residual
+  // gathers read shared memory instead of L2 (config 1: 128 KB)
   __shared__ __align__(16) double cs[2 * kWarpCap];
   __shared__ int32_t sups[kWarpCap];
   __shared__ __align__(16) double sq[kWarpCap * (kWarpCap + 4)];
@@ -2747,6 +2754,14 @@ k_solve_fused(SolveParams p, Work w) {
   const int64_t b = blockIdx.x;
   if (!w.active[b]) return;
   for (int64_t i = tid; i < p.ldm; i += kFusedThreads) rs[i] = w.r64[b * p.ldm + i];
+  const float* At = w.at32;
+  if (stage_a) {
+    float* As = reinterpret_cast<float*>(rs + p.ldm);
+    const int64_t n4 = p.n * p.ldm / 4;
+    for (int64_t i = tid; i < n4; i += kFusedThreads)
+      reinterpret_cast<float4*>(As)[i] = reinterpret_cast<const float4*>(w.at32)[i];
+    At = As;
+  }
   __syncthreads();
   double* sc = w.scores + b * p.n;
   for (int outer = 1; outer <= p.max_outer; ++outer) {
@@ -2764,7 +2779,7 @@ k_solve_fused(SolveParams p, Work w) {
 #pragma unroll
         for (int u = 0; u < kFusedAtoms; ++u) {
           if (j0 + u < p.n) {
-            const float2 a = *reinterpret_cast<const float2*>(w.at32 + (j0 + u) * p.ldm + i);
+            const float2 a = *reinterpret_cast<const float2*>(At + (j0 + u) * p.ldm + i);
             acc[u] = fma(f2d(a.x), r01.x, acc[u]);
             acc[u] = fma(f2d(a.y), r01.y, acc[u]);
           }
@@ -2808,7 +2823,7 @@ k_solve_fused(SolveParams p, Work w) {
     double lacc = 0.0;
     for (int64_t i = tid; i < p.ldm; i += kFusedThreads) {
       double acc = 0.0;
-      for (int k = 0; k < t; ++k) acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
+      for (int k = 0; k < t; ++k) acc = fma((double)At[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
       const double rv = acc - w.y64[b * p.ldm + i];
       rs[i] = rv;
       lacc = fma(rv, rv, lacc);
@@ -3341,11 +3356,17 @@ void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStre
 }
 
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s) {
-  const size_t smem = (size_t)p.ldm * 8;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // stage A in shared memory when it fits and every signal still gets its own SM
+  const size_t a_bytes = (size_t)(p.n * p.ldm) * 4;
+  const int stage_a = (p.ldm * 8 + a_bytes <= (size_t)kFusedStageMax && p.B <= sms) ? 1 : 0;
+  const size_t smem = (size_t)p.ldm * 8 + (stage_a ? a_bytes : 0);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w);
+    kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w, stage_a);
   };
   switch (p.opt) {
     case 0: go(k_solve_fused<0>); break;

@@ -1,7 +1,7 @@
 L=paper_2501_11592_b200/_build/libclomp_b200.so
 cp $L /tmp/base.so
 for rep in 1 2; do
-for v in base variants/fa8.so variants/fa16.so; do
+for v in base variants/*.so; do
   if [ "$v" = base ]; then cp /tmp/base.so $L; else cp $v $L; fi
   echo "CFG 1 VAR $v $(timeout 300 python bench.py --config 1 --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],1), round(d["ms_per_step"],4), round(d["e2e"]["value"],1))' 2>&1 | tail -1)"
 done
