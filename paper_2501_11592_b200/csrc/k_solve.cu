@@ -2731,6 +2731,9 @@ constexpr int kFusedThreads = 256;
 #define CL_FUSED_ATOMS 32
 #endif
 constexpr int kFusedAtoms = CL_FUSED_ATOMS;  // atoms per warp pass of the correlation (was 8)
+#ifndef CL_FUSED_WL
+#define CL_FUSED_WL 0  // 1: learner reads the staged copy too (measured neutral at config 1)
+#endif
 #ifndef CL_FUSED_STAGE_MAX
 #define CL_FUSED_STAGE_MAX (200 * 1024)
 #endif
@@ -2806,7 +2809,13 @@ k_solve_fused(SolveParams p, Work w, int stage_a) {
       __syncwarp();
       if (w.active[b] && w.cnt[b] <= kWarpCap) {
         stage_gram_async(p, w, b, w.gcnt[b], sq, kWarpCap + 4, lane);
+#if CL_FUSED_WL
+        Work wl = w;  // the learner's atom reads (Gram extension, b_k) from the staged copy
+        wl.at32 = At;
+        learn_warp_body<kWarpCap, OPT>(p, wl, b, outer, cs, sups, sq, nullptr, lane);
+#else
         learn_warp_body<kWarpCap, OPT>(p, w, b, outer, cs, sups, sq, nullptr, lane);
+#endif
       }
       else if (lane == 0 && w.active[b])
         w.status[b] = 7, w.active[b] = 0;  // capacity: larger supports use the batched path
