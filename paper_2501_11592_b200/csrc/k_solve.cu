@@ -3365,16 +3365,25 @@ void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStre
 }
 
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s) {
-  int dev = 0, sms = 148;
+  // latency-bound path: the SM count and the smem attribute are queried / set
+  // once per device (the attribute only grows), not per call
+  static int sms_of[64] = {0};
+  static size_t smem_set[64][3] = {};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  dev &= 63;
+  if (sms_of[dev] == 0) cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sms_of[dev];
   // stage A in shared memory when it fits and every signal still gets its own SM
   const size_t a_bytes = (size_t)(p.n * p.ldm) * 4;
   const int stage_a = (p.ldm * 8 + a_bytes <= (size_t)kFusedStageMax && p.B <= sms) ? 1 : 0;
   const size_t smem = (size_t)p.ldm * 8 + (stage_a ? a_bytes : 0);
   auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
+    size_t& set = smem_set[dev][p.opt < 0 ? 0 : (p.opt > 2 ? 2 : p.opt)];
+    if (smem > 48 * 1024 && smem > set) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set = smem;
+    }
     kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w, stage_a);
   };
   switch (p.opt) {
