@@ -15,8 +15,8 @@ for i in range(6):
     t1 = time.perf_counter()
     print(i, "public wall ms %.3f" % ((t1 - t0) * 1e3), "lib e2e ms %.3f" % ctx.stats()["e2e_ms"])
 dev = torch.device("cuda:0")
-for lay, d_y in (("signal-major", torch.from_numpy(np.ascontiguousarray(Y.T)).to(dev)),
-                 ("ref m x B", torch.from_numpy(np.ascontiguousarray(Y)).to(dev))):
+# (cl_solve_batch_device takes signal-major B x m y only)
+for lay, d_y in (("signal-major", torch.from_numpy(np.ascontiguousarray(Y.T)).to(dev)),):
     cap = min(c["n"], c["k"] + 16)
     o = [torch.zeros((B, cap), dtype=torch.int32, device=dev), torch.zeros((B, cap), dtype=torch.float64, device=dev)]
     o += [torch.zeros(B, dtype=t, device=dev) for t in (torch.int32, torch.int32, torch.float64, torch.uint8, torch.int32)]
