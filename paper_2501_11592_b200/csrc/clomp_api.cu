@@ -46,7 +46,10 @@ struct Carver {
   }
 };
 
-constexpr int kChunkIters = 8;
+#ifndef CL_CHUNK_ITERS
+#define CL_CHUNK_ITERS 8
+#endif
+constexpr int kChunkIters = CL_CHUNK_ITERS;  // outer iterations per captured graph
 
 struct GraphKey {
   SolveParams p{};
