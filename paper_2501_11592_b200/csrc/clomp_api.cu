@@ -47,7 +47,7 @@ struct Carver {
 };
 
 #ifndef CL_CHUNK_ITERS
-#define CL_CHUNK_ITERS 8
+#define CL_CHUNK_ITERS 16
 #endif
 constexpr int kChunkIters = CL_CHUNK_ITERS;  // outer iterations per captured graph
 

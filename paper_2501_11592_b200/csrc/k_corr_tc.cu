@@ -510,7 +510,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
            const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
            int64_t n, int64_t B, int kblocks, int64_t ntile, const float* __restrict__ r_scale,
            double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg,
-           const int32_t* tile_done, int tile_wait) {
+           const int32_t* tile_done, int tile_wait, const int32_t* __restrict__ active) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -564,6 +564,15 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
     pdl_trigger();
   }
   if (threadIdx.x == 0) K1_MARK(1);
+  // A pair whose 256 signals have all stopped has no reader for its records:
+  // both CTAs read the same flags and skip to the teardown together (batches
+  // that finish early replay the rest of their graph chunk nearly for free).
+  int live_sig = 0;
+  if (threadIdx.x < 2 * TM) {
+    const int64_t sb = (int64_t)(blockIdx.x & ~1u) * TM + threadIdx.x;
+    live_sig = sb < B && active[sb] != 0;
+  }
+  if (__syncthreads_or(live_sig)) {
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs): own R slice + own half of the
@@ -617,6 +626,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
 #endif
   tile_epilogue<kPairWarps>(smem, tmem, accum, m0, n0, n, B, ntile, r_scale, a_inv_scale, cand,
                             scores_dbg, warp, lane, blockIdx.y);
+  }  // live pair
   // early start: this grid completes only after its predecessor (the block
   // learner), so every later kernel still sees the whole iteration finished
   if (tile_wait > 0) pdl_wait();
@@ -971,7 +981,8 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
     return cudaLaunchKernelEx(&cfg, k_corr_tc2, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
                               (int)(p.ldm / BK), p.ntl, (const float*)w.r_scale, p.a_inv_scale,
                               w.cand, scores_dbg, (const int32_t*)w.tile_done,
-                              p.tile_flags && p.atom0 == 0 ? (int)p.tile_wait : 0) == cudaSuccess;
+                              p.tile_flags && p.atom0 == 0 ? (int)p.tile_wait : 0,
+                              (const int32_t*)w.active) == cudaSuccess;
   }
   const bool clustered = mtiles >= kCluster;
   const int arows = clustered ? TN / kCluster : TN;
