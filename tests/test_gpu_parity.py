@@ -457,36 +457,3 @@ def test_tie_grown_supports_fast_path(gpu_available):
         assert np.array_equal(r.mask[:, b], ref["mask"][:, q]), f"signal {b}: support"
         assert r.iterations[b] == ref["iterations"][q]
         assert rel_coef_err(r.s[:, b], ref["s"][:, q]) <= 1e-9
-
-
-def test_tile_overlap_mode_identical(gpu_available, monkeypatch):
-    """CL_TILE_OVERLAP=1 (K1 starts a signal tile once the learners have counted
-    its signals done, instead of waiting for the whole learning grid; off by
-    default, measured slower) gives bit-identical results on a config-2-size
-    batch with exact ties, so the block kernel's count path runs too."""
-    m, n, B, K = 512, 1024, 512, 30
-    A, X, Y, _ = cl.gen_problem_1d(77, m, n, K, B, snr_db=40.0)
-    A = np.array(A)
-    A[:, 1:128:2] = A[:, 0:128:2]  # duplicated atom pairs -> tie-grown supports
-    X = np.zeros((n, B))
-    rng = np.random.default_rng(5)
-    for b in range(B):
-        if b % 8 == 0:  # every 8th signal: 10 duplicated atoms plus 14 others
-            X[rng.choice(np.arange(0, 128, 2), 10, replace=False), b] = rng.standard_normal(10)
-            X[rng.choice(np.arange(128, n), 14, replace=False), b] = rng.standard_normal(14)
-        else:
-            X[rng.choice(np.arange(128, n), 24, replace=False), b] = rng.standard_normal(24)
-    Y = (A.astype(np.float64) @ X).astype(np.float32)
-    cfg = cl.ClompConfig.baseline(K)
-    outs = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("CL_TILE_OVERLAP", flag)
-        ctx = make_ctx(A, "tc")
-        outs.append(cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL))
-    a, b = outs
-    assert np.all(a.status == 0)
-    assert int(a.mask.sum(axis=0).max()) > 32  # the tie path (block kernel) ran
-    assert np.array_equal(a.mask, b.mask)
-    assert np.array_equal(a.s, b.s)
-    assert np.array_equal(a.iterations, b.iterations)
-    assert np.array_equal(a.final_residual_norm, b.final_residual_norm)
