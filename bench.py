@@ -46,6 +46,11 @@ sys.path.insert(0, str(ROOT))
 METRIC = "signals reconstructed/sec at fixed (N,M,K)"
 UNIT = "signals/s"
 CHUNK = 8  # signals per reference worker call (AVX2 tile width)
+# the arithmetic the path computes in: fp32 operands (A, y), the batched
+# correlation as a split-fp16 tcgen05 GEMM (three f16 MMAs, fp32 TMEM
+# accumulation) with fp64 rescoring of near-tied selections, every learning
+# product, residual and reduction in fp64
+DTYPE = "f32 operands; 3xf16 tcgen05 correlation + f64 rescoring; f64 learning"
 
 
 def parse():
@@ -56,6 +61,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--colshard", action="store_true")
+    ap.add_argument("--vshards", type=int, default=4,
+                    help="--colshard on one GPU: virtual column shards (the NCCL path's kernels "
+                         "and exchanges, one device)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank solves its own batch of the config's size; strong: "
+                         "the config's batch is split across the ranks")
     ap.add_argument("--max-outer", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05, 3 GEMV")
@@ -64,17 +75,26 @@ def parse():
     return ap.parse_args()
 
 
-def workload(args, rank: int):
-    import paper_2501_11592_b200 as cl
+def workload(args, rank: int, world: int = 1):
+    from paper_2501_11592_b200.configs import CONFIGS
 
-    c = dict(cl.CONFIGS[args.config])
+    c = dict(CONFIGS[args.config])
     c["sep"] = "n_r" in c
     if c["sep"]:
         c["n"], c["m"] = c["n_r"] * c["n_c"], c["m_r"] * c["m_c"]
         c["max_outer"] = args.max_outer or 64
     else:
         c["max_outer"] = args.max_outer or c["k"]
-    if not args.colshard:
+    c["sig_lo"], c["sig_hi"] = 0, c["batch"]
+    if args.colshard:
+        pass  # one batch solved together by all ranks
+    elif args.scaling == "strong":
+        # strong scaling: the config's batch is the GLOBAL batch (config 5:
+        # "batch 1024 sharded by image across 1/2/4/8 GPUs"); every rank draws
+        # the same problem and solves its contiguous slice of the signals
+        per = -(-c["batch"] // world)
+        c["sig_lo"], c["sig_hi"] = min(rank * per, c["batch"]), min((rank + 1) * per, c["batch"])
+    else:
         c["seed"] = c["seed"] + 1000 * rank  # weak scaling: each rank its own batch
     return c
 
@@ -92,73 +112,121 @@ def make_problem(c):
 
 
 def solver_config(c):
-    import paper_2501_11592_b200 as cl
+    from paper_2501_11592_b200.configs import ClompConfig
 
-    cfg = cl.ClompConfig.baseline(c["k"])
+    cfg = ClompConfig.baseline(c["k"])
     cfg.max_outer = c["max_outer"]
     return cfg
 
 
-def config_block(c, n_gpus, colshard):
+def config_block(c, n_gpus, mode):
+    """mode: "weak" (a batch per GPU), "strong" (the batch split by signal),
+    "colshard" (one batch, the dictionary split by atoms)."""
     if c["sep"]:
         shape = (f"{c['n_r']}x{c['n_c']} coefficients, {c['m_r']}x{c['m_c']} measurements, "
                  f"K={c['k']} (prefix: {c['max_outer']} outer iterations)")
     else:
         shape = f"N={c['n']} M={c['m']} K={c['k']}"
     noise = "" if c["sep"] or c["snr_db"] < 0 else f" {c['snr_db']} dB"
+    weak = mode == "weak"
     return {
-        "workload": f"{c['name']}: {shape} batch={c['batch']}{'' if colshard else '/GPU'}{noise}",
-        "n": c["n"], "m": c["m"], "k": c["k"], "batch_per_gpu": c["batch"] // (n_gpus if colshard else 1),
-        "global_batch": c["batch"] * (1 if colshard else n_gpus), "lr": 0.1, "epochs": 200,
+        "workload": f"{c['name']}: {shape} batch={c['batch']}{'/GPU' if weak else ''}{noise}",
+        "n": c["n"], "m": c["m"], "k": c["k"],
+        "batch_per_gpu": c["batch"] if weak else -(-c["batch"] // n_gpus),
+        "global_batch": c["batch"] * (n_gpus if weak else 1), "lr": 0.1, "epochs": 200,
         "th": 1.0, "max_outer": c["max_outer"], "optimizer": "plain", "priors": "off",
         "mode": "per_signal (clomp_solve per column)", "seed": c["seed"],
-        "parallelism": (f"column-shard x{n_gpus} (NCCL all-gathers)" if colshard
-                        else f"signal-shard x{n_gpus}, no collectives"),
+        "parallelism": {"weak": f"signal-shard x{n_gpus} (a batch per GPU), no collectives",
+                        "strong": f"signal-shard x{n_gpus} (one batch split), no collectives",
+                        "colshard": f"column-shard x{n_gpus} (NCCL all-gathers)"}[mode],
         "l2": "flushed between timed steps (256 MiB write)",
     }
 
 
 # ----------------------------------------------------------- reference arm
-def _ref_worker(args):
-    core, A, Ychunk, cfgd = args
+# The reference arm and the cpu_baseline leg run the UNMODIFIED reference
+# library (oracle/_ref/libcskit_ref.so) in P spawned single-threaded worker
+# processes, one pinned per host core.  Each worker draws the workload itself
+# with the reference's own cskit::Rng (refbind.ref_gen_problem_1d, the same
+# bits as the product's generator: tests/test_datagen.py), so no process of
+# this arm loads the B200 library.
+_W = {}
+
+
+def _ref_init(core_counter, gen_args):
+    import multiprocessing as mp  # noqa: F401
+
+    with core_counter.get_lock():
+        idx = core_counter.value
+        core_counter.value += 1
     try:
-        os.sched_setaffinity(0, {core})
+        cores = sorted(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, {cores[idx % len(cores)]})
     except Exception:
         pass
     sys.path.insert(0, str(ROOT / "tests"))
     import refbind
-    from paper_2501_11592_b200 import ClompConfig
 
-    cfg = ClompConfig(**cfgd)
+    seed, m, n, k, batch, law, snr = gen_args
+    A, _, Y = refbind.ref_gen_problem_1d(seed, m, n, k, batch, value_law=law, snr_db=snr,
+                                         want_x=False)
+    _W["A"] = A.astype(np.float64)
+    _W["Y"] = Y.astype(np.float64)
+    _W["refbind"] = refbind
+
+
+def _ref_task(job):
+    lo, cfgd = job
+    from paper_2501_11592_b200.configs import ClompConfig
+
+    refbind = _W["refbind"]
+    Y = _W["Y"]
+    B = Y.shape[1]
+    chunk = np.ascontiguousarray(Y[:, lo % B:lo % B + CHUNK])
     t0 = time.perf_counter()
-    r = refbind.ref_solve_batch(A, Ychunk, cfg)
-    return time.perf_counter() - t0, r["code"], Ychunk.shape[1]
+    r = refbind.ref_solve_batch(_W["A"], chunk, ClompConfig(**cfgd))
+    return time.perf_counter() - t0, r["code"], chunk.shape[1]
 
 
-def reference_round(A64, Y64, cfg, workers: int, scale: float = 0.0):
-    """One bounded sample: `workers` processes x CHUNK signals in parallel.
-    With scale, the sample is a truncated solve (reference_plan) and its wall
-    time is multiplied by scale to extrapolate to the full one."""
-    import dataclasses
-    import multiprocessing as mp
+class ReferencePool:
+    """P spawned reference workers holding the workload (generated once)."""
 
-    cfgd = dataclasses.asdict(cfg)
-    B = Y64.shape[1]
-    jobs = []
-    for w in range(workers):
-        lo = (w * CHUNK) % B
-        jobs.append((w % (os.cpu_count() or 1), A64, np.ascontiguousarray(Y64[:, lo:lo + CHUNK]), cfgd))
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_ref_worker, jobs)
-    wall = time.perf_counter() - t0
-    if any(code != 0 for _, code, _ in res):
-        raise RuntimeError("reference solve failed")
-    sig = sum(n for _, _, n in res)
-    if scale:
-        wall = wall * scale
-    return sig / wall, wall, sig
+    def __init__(self, c, workers: int):
+        import multiprocessing as mp
+
+        ctx = mp.get_context("spawn")
+        self.workers = workers
+        counter = ctx.Value("i", 0)
+        gen = (c["seed"], c["m"], c["n"], c["k"], c["batch"], c["value_law"], c["snr_db"])
+        self.pool = ctx.Pool(workers, initializer=_ref_init, initargs=(counter, gen))
+        # every worker has generated its inputs before the first timed round
+        self.pool.map(_ref_noop, range(4 * workers), chunksize=1)
+
+    def round(self, cfg, workers: int, scale: float = 0.0):
+        """One bounded sample: `workers` tasks x CHUNK signals in parallel.
+        With scale, the sample is a truncated solve (reference_plan) and its
+        wall time is multiplied by scale to extrapolate to the full one."""
+        import dataclasses
+
+        cfgd = dataclasses.asdict(cfg)
+        jobs = [(w * CHUNK, cfgd) for w in range(workers)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_ref_task, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+        if any(code != 0 for _, code, _ in res):
+            raise RuntimeError("reference solve failed")
+        sig = sum(n for _, _, n in res)
+        if scale:
+            wall = wall * scale
+        return sig / wall, wall, sig
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def _ref_noop(_):
+    return os.getpid()
 
 
 def cpu_info():
@@ -204,7 +272,7 @@ def reference_plan(c):
 
 def run_reference(args, rank, world):
     if rank != 0:
-        return
+        return  # torchrun: rank 0 alone times the host cores
     sys.path.insert(0, str(ROOT / "tests"))
     import refbind
 
@@ -217,18 +285,18 @@ def run_reference(args, rank, world):
     if not refbind.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcskit_ref.so not built"}))
         return
-    A, X, Y = make_problem(c)
-    A64, Y64 = A.astype(np.float64), Y.astype(np.float64)
     cfg, extra, note = reference_plan(c)
     P = host_workers()
+    pool = ReferencePool(c, P)
     for _ in range(args.warmup):
-        reference_round(A64, Y64, cfg, min(P, 2), extra)
+        pool.round(cfg, min(P, 2), extra)
     vals, walls = [], []
     sig = 0
     for _ in range(args.steps):
-        v, wall, sig = reference_round(A64, Y64, cfg, P, extra)
+        v, wall, sig = pool.round(cfg, P, extra)
         vals.append(v)
         walls.append(wall)
+    pool.close()
     value = statistics.mean(vals)
     sample = (f"{P} workers x {CHUNK} signals per step (clomp_solve_batch, AVX2), {sig} "
               f"signals/step, {note}")
@@ -236,8 +304,10 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True,
-        "scaling": "strong" if args.colshard else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_block(c, 1, False),
+        "scaling": "strong" if args.colshard or args.scaling == "strong" else "weak",
+        "vs_baseline": None, "dtype": "f64 (the reference computes in double)",
+        "data": "synthetic (seeded cskit::Rng, BASELINE config laws)",
+        "config": config_block(c, world, "colshard" if args.colshard else args.scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "reference",
                          "sample": sample, "cpu": cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -359,9 +429,13 @@ def run_ours(args, rank, world, local_rank):
     dist = world > 1
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    c = workload(args, rank)
+    c = workload(args, rank, world)
     A, X, Y = make_problem(c)
-    B, m, n = c["batch"], c["m"], c["n"]
+    if (c["sig_lo"], c["sig_hi"]) != (0, c["batch"]):
+        Y = np.ascontiguousarray(Y[:, c["sig_lo"]:c["sig_hi"]])
+    B, m, n = Y.shape[1], c["m"], c["n"]
+    if B == 0:
+        raise SystemExit("strong scaling: more ranks than signals")
     cfg = solver_config(c)
     if c["sep"]:
         ctx = cl.ClompContext.separable(A[0], A[1], device=local_rank)
@@ -371,6 +445,8 @@ def run_ours(args, rank, world, local_rank):
         ctx = cl.ClompContext.colshard(A, rank, world, nid[0], device=local_rank)
     else:
         ctx = cl.ClompContext(A, device=local_rank)
+        if args.colshard:  # one GPU: the column-shard code path with virtual shards
+            ctx.set_virtual_shards(args.vshards)
     if args.corr_path:
         ctx.set_corr_path(args.corr_path)
     if args.power_levels != -1 and not c["sep"]:
@@ -430,7 +506,8 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_signals = B if args.colshard else B * world
+    strong = args.colshard or args.scaling == "strong"
+    total_signals = c["batch"] if strong else B * world
     value = total_signals / (ms_max / 1000.0)
 
     # Per-phase breakdown of one solve (profiling events, outside the timed region).
@@ -475,10 +552,10 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "strong" if args.colshard else "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic (seeded cskit::Rng restatement, BASELINE config laws)",
-        "config": config_block(c, world, args.colshard),
+        "config": config_block(c, world, "colshard" if args.colshard else args.scaling),
     }
     if prof and prof["corr_path"] == 3 and not c["sep"]:
         # K1b GEMV: HBM-bound; algorithmic bytes per launch = the fp32
@@ -591,7 +668,9 @@ def run_ours(args, rank, world, local_rank):
         if refbind.ref_available():
             P = host_workers()
             rcfg, extra, note = reference_plan(c)
-            v, wall, sig = reference_round(A.astype(np.float64), Y.astype(np.float64), rcfg, P, extra)
+            pool = ReferencePool(c, P)
+            v, wall, sig = pool.round(rcfg, P, extra)
+            pool.close()
             out["cpu_baseline"] = {
                 "value": v, "unit": UNIT, "cores": P, "kind": "reference",
                 "sample": f"{P} workers x {CHUNK} signals of this workload, one round ({note})",
@@ -599,8 +678,25 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(out))
 
 
+def self_launch(args) -> bool:
+    """`bench.py --gpus N` outside torchrun: start the N ranks ourselves (one
+    process per GPU, the same torchrun command line the driver uses)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -10,13 +10,21 @@
  *
  * Numeric contract
  *   * Operands A and y are fp32 (north star).  Every product and reduction on
- *     the learning path is carried in fp64; correlations run on the tensor
- *     cores (3xTF32) and every selection whose top-2 gap is inside the error
- *     bound of that GEMM is re-decided from fp64 scores.  Supports therefore
- *     match the fp64 reference (clomp.cpp:211-292) and coefficients agree to
- *     ~1e-12 relative.
- *   * Priors (w_tv/w_lv > 0 after resolve_weights, clomp.cpp:131-140) are not
- *     implemented: CL_ERR_UNSUPPORTED, never a CPU fallback.
+ *     the learning path is carried in fp64.  At th == 1 the batched
+ *     correlation runs on the tcgen05 tensor cores as a split-fp16 GEMM
+ *     (s*x = hi + lo, three kind::f16 MMAs hi.lo + lo.hi + hi.hi accumulated
+ *     in fp32 TMEM, ~fp32 accuracy), and every selection whose top-2 gap lies
+ *     inside that GEMM's error bound (delta_for in clomp_api.cu: (1e-5 +
+ *     ldm/8 * 1.2e-7) * max||a|| * ||r||) is re-decided from exact fp64
+ *     scores of the atoms in the band.  th < 1, B <= 4 (GEMV) and the fused
+ *     small-problem path score in fp64 directly.  Supports therefore match
+ *     the fp64 reference (clomp.cpp:211-292); coefficients agree to ~1e-12
+ *     relative on the golden cases.
+ *   * Priors (w_tv/w_lv > 0 after resolve_weights, clomp.cpp:131-140): TV-1D
+ *     on single-column solves and TV-2D + local variance on multi-column
+ *     joint batches (the reference's image mode) run on the GPU once a
+ *     synthesis basis is set (cl_set_basis); separable and column-sharded
+ *     contexts return CL_ERR_UNSUPPORTED.  Never a CPU fallback.
  *
  * Threading: one context per host thread; calls on distinct contexts may run
  * concurrently.  A context owns one device, one stream and its workspace.
@@ -192,10 +200,10 @@ typedef struct cl_stats {
 } cl_stats;
 int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 
-/* Tuning / test knobs: 0 = auto (GEMV for B <= 8, else tcgen05 at th == 1,
+/* Tuning / test knobs: 0 = auto (GEMV for B <= 4, else tcgen05 at th == 1,
  * else fp64 SIMT), 1 = force fp64 SIMT correlation, 2 = force the tcgen05
  * split-fp16 correlation (th == 1 only), 3 = force the HBM-bound GEMV
- * (1 <= B <= 8). */
+ * (1 <= B <= 4). */
 int cl_set_corr_path(cl_ctx* ctx, int path);
 /* Dictionary Gram cache G = A^T A (fp64, n x n) used to extend each signal's
  * support Gram matrix by a gather instead of re-streaming atoms:
@@ -216,9 +224,8 @@ int cl_set_fused(cl_ctx* ctx, int on);
  * CL_ERR_UNSUPPORTED; priors without a basis too. */
 int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram
- * matrix in registers (default 1; 2 = an eight-CTA variant above 128 atoms
- * instead of four CTAs); 0 keeps them on the block-per-signal kernel (tests
- * compare them). */
+ * matrix in registers (default 1); 0 keeps them on the block-per-signal
+ * kernel (tests compare them). */
 int cl_set_cluster_learn(cl_ctx* ctx, int on);
 /* Plain gradient descent on cluster-learned supports (33..256 atoms): run the
  * E epochs as E mod 2^L plain steps, L batched squarings of T = I - 2 lr G on

@@ -7,10 +7,12 @@
 // and the unit-level entry points through ctypes.  Nothing here computes; it
 // marshals plain arrays into cskit types and maps the reference exceptions
 // (errors.hpp:10-37) onto the status codes of include/clomp_b200.h.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "cskit/clomp.hpp"
@@ -246,6 +248,78 @@ void ref_rng_draws(uint64_t seed, int kind, uint64_t bound, int64_t count,
       default: out_u64[i] = rng.uniform_below(bound); break;
     }
   }
+}
+
+// The harness's seeded 1D problem drawn from the reference's
+// own cskit::Rng (rng.hpp:13-79), so bench.py's reference arm generates its
+// inputs without loading the B200 library.  Same draw order as the product's
+// cl_gen_problem_1d (tests/test_datagen.py pins the two bit for bit): A
+// entries normal()/sqrt(m) row-major, columns normalised in fp64, rounded to
+// fp32; per signal a partial Fisher-Yates support (uniform_below) then k
+// values (normal(), or sign from uniform() < 0.5 times 1 + uniform());
+// y = A x in fp64; per-signal noise sd = rms(A x_b) 10^(-snr/20) drawn after
+// every signal; y rounded to fp32.  A m x n fp32, X n x B fp64 (may be NULL),
+// Y m x B fp32, all row-major.
+int ref_gen_problem_1d(uint64_t seed, int64_t m, int64_t n, int64_t k, int64_t batch,
+                       int normalize, int value_law, double snr_db, float* A, double* X,
+                       float* Y) {
+  if (m <= 0 || n <= 0 || batch <= 0 || k < 0 || k > n) return 3;
+  cskit::Rng rng(seed);
+  std::vector<double> a(static_cast<size_t>(m * n));
+  const double scale = 1.0 / std::sqrt(static_cast<double>(m));
+  for (auto& e : a) e = scale * rng.normal();
+  if (normalize) {
+    for (int64_t j = 0; j < n; ++j) {
+      double ss = 0.0;
+      for (int64_t i = 0; i < m; ++i) ss += a[i * n + j] * a[i * n + j];
+      const double nrm = std::sqrt(ss);
+      if (nrm > 0.0)
+        for (int64_t i = 0; i < m; ++i) a[i * n + j] /= nrm;
+    }
+  }
+  for (int64_t e = 0; e < m * n; ++e) A[e] = static_cast<float>(a[e]);
+  std::vector<int64_t> perm(static_cast<size_t>(n)), sup(static_cast<size_t>(k * batch));
+  std::vector<double> vals(static_cast<size_t>(k * batch));
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t j = 0; j < n; ++j) perm[j] = j;
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t r = q + static_cast<int64_t>(rng.uniform_below(static_cast<uint64_t>(n - q)));
+      std::swap(perm[q], perm[r]);
+    }
+    for (int64_t q = 0; q < k; ++q) {
+      double v;
+      if (value_law == 1) {
+        const double sgn = rng.uniform() < 0.5 ? -1.0 : 1.0;
+        v = sgn * (1.0 + rng.uniform());
+      } else {
+        v = rng.normal();
+      }
+      sup[b * k + q] = perm[q];
+      vals[b * k + q] = v;
+    }
+  }
+  if (X) std::memset(X, 0, sizeof(double) * n * batch);
+  std::vector<double> yall(static_cast<size_t>(m * batch)), rms(static_cast<size_t>(batch));
+  for (int64_t b = 0; b < batch; ++b) {
+    if (X)
+      for (int64_t q = 0; q < k; ++q) X[sup[b * k + q] * batch + b] = vals[b * k + q];
+    double ss = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < k; ++q)
+        acc += static_cast<double>(A[i * n + sup[b * k + q]]) * vals[b * k + q];
+      yall[i * batch + b] = acc;
+      ss += acc * acc;
+    }
+    rms[b] = std::sqrt(ss / static_cast<double>(m));
+  }
+  if (snr_db >= 0.0 && std::isfinite(snr_db)) {
+    const double f = std::pow(10.0, -snr_db / 20.0);
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t i = 0; i < m; ++i) yall[i * batch + b] += rms[b] * f * rng.normal();
+  }
+  for (int64_t e = 0; e < m * batch; ++e) Y[e] = static_cast<float>(yall[e]);
+  return 0;
 }
 
 // dct_basis (sensing.cpp:13-29), n x n row-major.

@@ -121,7 +121,7 @@ struct cl_ctx {
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool fused_ok = true;  // small problems: one persistent block per signal
-  int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (2: 4-CTA variant)
+  int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (0: block kernel)
   int power_levels = -1;  // plain GD on cluster-sized supports: squaring levels (-1 auto, 0 off)
   double* pw_buf = nullptr;  // power-form buffers (Work::pw_t / pw_d)
   size_t pw_bytes = 0;
@@ -254,7 +254,6 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.changed = cv.take<int32_t>(B);
     w.big_list = cv.take<int32_t>(B);
     w.counters = cv.take<int32_t>(kNumCounters);
-    w.tile_done = cv.take<int32_t>((B + 127) / 128 + 2);
     w.joint = cv.take<double>(kNumJoint);
     if (need_prior) {
       w.hgram = cv.take<double>(B * cap * cap);
@@ -561,29 +560,6 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       ctx->w.pw_cnt = nullptr;
     }
   }
-  p.lazy_r64 = 0;  // measured slower: the rescoring warp becomes the tail
-  // CL_TILE_OVERLAP=1: K1 of iteration o + 1 starts a signal tile as soon as
-  // the learning kernels have finished that tile's signals (per-signal th == 1
-  // on the fast learning kernel, supports within one warp).  Correct (GPU suite
-  // green with it) but measured slower at config 2 (2.21 vs 2.07 ms per step:
-  // the early pair CTAs wait on SMs the learning tail still needs), so off by
-  // default.
-  {
-    const bool fast_learn = p.fuse_select && ctx->w.gfull && !p.sep && cap >= 32 && (cap & 1) == 0;
-#ifdef CL_TILE_OVERLAP_EXPERIMENT
-    const char* env_ov = getenv("CL_TILE_OVERLAP");
-    const bool want = env_ov ? atoi(env_ov) != 0 : false;
-#else
-    // compiled out: one GPU-suite run of the overlap test stalled (the run
-    // hit its time limit), so the mode is not reachable in normal builds
-    const bool want = false;
-#endif
-    p.tile_flags = (want && tensor && !colshard && p.mode == CL_MODE_PER_SIGNAL && !prior &&
-                    fast_learn && c->th >= 1.0 && p.max_outer <= kWarpCap && ctx->w.tile_done)
-                       ? 1 : 0;
-    p.tile_wait = 0;
-  }
-
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
   cl_stats stats{};
@@ -594,6 +570,9 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   // th == 1), learning + residual + stopping rules.  th == 1 adds one atom per
   // iteration, so the learning kernel's support bucket follows `outer`
   // (signals grown past it by ties are finished by the block kernel).
+  // false once a launch or collective could not be enqueued (tensor-map
+  // encode, cudaLaunchKernelEx, NCCL): the call fails with CL_ERR_CUDA.
+  bool enq_ok = true;
   auto enqueue_iteration = [&](int outer, int64_t* launches) {
     // (the active count is cleared by the learning kernel, see k_learn_warp)
     if (p.sep) {
@@ -619,7 +598,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         Work wk = w;
         wk.cand = w.xg + (int64_t)r * B * p.ntl;
         if (tensor)
-          launch_corr_tc(pk, wk, s);
+          enq_ok &= launch_corr_tc(pk, wk, s);
         else if (gemv)
           launch_corr_gemv(pk, wk, false, s);
         else
@@ -628,7 +607,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       }
       if (ctx->world > 1) {
         const size_t cnt = (size_t)(B * p.ntl);
-        nccl_allgather_inplace(ctx->comm, w.xg, cnt * sizeof(Cand), 1, ctx->rank, s);
+        enq_ok &= nccl_allgather_inplace(ctx->comm, w.xg, cnt * sizeof(Cand), 1, ctx->rank, s);
       }
       launch_cand_exchange(w.xg, w.cand, B, p.ntl, W, p.n_corr, s);
       *launches += launch_learn(p, w, outer, outer, s);  // selection fused (p.fuse_select)
@@ -636,21 +615,19 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       if (ctx->world > 1) {
         const size_t rows = (size_t)((p.sig_hi - p.sig_lo) * p.ldm);
         if (w.r_hi) {
-          nccl_allgather_inplace(ctx->comm, w.r_hi, rows * sizeof(__half), 1, ctx->rank, s);
-          nccl_allgather_inplace(ctx->comm, w.r_lo, rows * sizeof(__half), 1, ctx->rank, s);
-          nccl_allgather_inplace(ctx->comm, w.r_scale, (size_t)(p.sig_hi - p.sig_lo), 4,
-                                 ctx->rank, s);
+          enq_ok &= nccl_allgather_inplace(ctx->comm, w.r_hi, rows * sizeof(__half), 1, ctx->rank, s);
+          enq_ok &= nccl_allgather_inplace(ctx->comm, w.r_lo, rows * sizeof(__half), 1, ctx->rank, s);
+          enq_ok &= nccl_allgather_inplace(ctx->comm, w.r_scale, (size_t)(p.sig_hi - p.sig_lo), 4,
+                                           ctx->rank, s);
         } else {
-          nccl_allgather_inplace(ctx->comm, w.r64, rows, 8, ctx->rank, s);
+          enq_ok &= nccl_allgather_inplace(ctx->comm, w.r64, rows, 8, ctx->rank, s);
         }
-        nccl_allreduce_sum_i32(ctx->comm, &w.counters[kActiveCount], 1, s);
+        enq_ok &= nccl_allreduce_sum_i32(ctx->comm, &w.counters[active_slot(outer)], 1, s);
       }
       return;
     }
     if (tensor) {
-      SolveParams pk = p;
-      pk.tile_wait = p.tile_flags && outer > 1 ? outer - 1 : 0;
-      launch_corr_tc(pk, w, s);
+      enq_ok &= launch_corr_tc(p, w, s);
     } else if (gemv)
       launch_corr_gemv(p, w, full_scores, s);
     else
@@ -674,8 +651,6 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   };
 
   CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
-  if (p.tile_flags)
-    CL_CUDA(ctx, cudaMemsetAsync(w.tile_done, 0, (size_t)((B + 127) / 128 + 2) * sizeof(int32_t), s));
   std::memset(ctx->h_counters, 0, kNumCounters * sizeof(int32_t));
   int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
@@ -717,7 +692,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                                      cudaMemcpyDeviceToHost, s));
         CL_CUDA(ctx, cudaStreamSynchronize(s));
         outer_done = outer;
-        if (ctx->h_counters[kActiveCount] == 0) break;
+        if (ctx->h_counters[active_slot(outer)] == 0) break;
         continue;
       }
       // 1D: events around every phase, the stream synchronised once per
@@ -730,7 +705,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         cudaEvent_t* e = &pe[(size_t)(4 * (o - outer))];
         cudaEventRecord(e[0], s);
         if (tensor)
-          launch_corr_tc(p, w, s);
+          enq_ok &= launch_corr_tc(p, w, s);
         else if (gemv)
           launch_corr_gemv(p, w, full_scores, s);
         else
@@ -754,6 +729,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         cudaEventRecord(e[3], s);
       }
       CL_CUDA(ctx, cudaGetLastError());
+      if (!enq_ok) return fail(ctx, CL_ERR_CUDA, "clomp: correlation kernel launch failed");
       CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
                                    cudaMemcpyDeviceToHost, s));
       CL_CUDA(ctx, cudaStreamSynchronize(s));
@@ -770,7 +746,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       for (auto& e : pe) cudaEventDestroy(e);
       outer_done = o1;
       outer = o1;
-      if (ctx->h_counters[kActiveCount] == 0) break;
+      if (ctx->h_counters[active_slot(o1)] == 0) break;
     }
     launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
                     out.conv, out.status, s);
@@ -815,6 +791,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         cudaMemcpyAsync(ctx->h_chunk + (ch & 1) * kNumCounters, w.counters,
                         kNumCounters * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
         CL_CUDA(ctx, cudaStreamEndCapture(s, &g));
+        if (!enq_ok) {
+          cudaGraphDestroy(g);
+          return fail(ctx, CL_ERR_CUDA, "clomp: correlation kernel launch failed (capture)");
+        }
         cudaGraphExec_t ge = nullptr;
         CL_CUDA(ctx, cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
@@ -829,6 +809,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         const int o1c = std::min(p.max_outer, o0 + kChunkIters - 1);
         int64_t dummy = 0;
         for (int o = o0; o <= o1c; ++o) enqueue_iteration(o, &dummy);
+        if (!enq_ok) return fail(ctx, CL_ERR_CUDA, "clomp: column-shard launch or collective failed");
         cudaMemcpyAsync(ctx->h_chunk + (ch & 1) * kNumCounters, w.counters,
                         kNumCounters * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
       } else {
@@ -840,7 +821,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       outer_done = o1;
       if (ch >= 1) {
         CL_CUDA(ctx, cudaEventSynchronize(ctx->chunk_ev[(ch - 1) & 1]));
-        if (ctx->h_chunk[((ch - 1) & 1) * kNumCounters + kActiveCount] == 0) break;
+        const int o_prev = std::min(p.max_outer, ch * kChunkIters);  // last iteration of chunk ch - 1
+        if (ctx->h_chunk[((ch - 1) & 1) * kNumCounters + active_slot(o_prev)] == 0) break;
       }
     }
     launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
@@ -848,13 +830,15 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     ++launches;
     if (colshard && ctx->world > 1) {  // every rank returns the whole batch
       const size_t ns = (size_t)(p.sig_hi - p.sig_lo);
-      if (out.sup) nccl_allgather_inplace(ctx->comm, out.sup, ns * out.cap, 4, ctx->rank, s);
-      if (out.coef) nccl_allgather_inplace(ctx->comm, out.coef, ns * out.cap, 8, ctx->rank, s);
-      if (out.cnt) nccl_allgather_inplace(ctx->comm, out.cnt, ns, 4, ctx->rank, s);
-      if (out.iters) nccl_allgather_inplace(ctx->comm, out.iters, ns, 4, ctx->rank, s);
-      if (out.rn) nccl_allgather_inplace(ctx->comm, out.rn, ns, 8, ctx->rank, s);
-      if (out.conv) nccl_allgather_inplace(ctx->comm, out.conv, ns, 1, ctx->rank, s);
-      if (out.status) nccl_allgather_inplace(ctx->comm, out.status, ns, 4, ctx->rank, s);
+      bool ok = true;
+      if (out.sup) ok &= nccl_allgather_inplace(ctx->comm, out.sup, ns * out.cap, 4, ctx->rank, s);
+      if (out.coef) ok &= nccl_allgather_inplace(ctx->comm, out.coef, ns * out.cap, 8, ctx->rank, s);
+      if (out.cnt) ok &= nccl_allgather_inplace(ctx->comm, out.cnt, ns, 4, ctx->rank, s);
+      if (out.iters) ok &= nccl_allgather_inplace(ctx->comm, out.iters, ns, 4, ctx->rank, s);
+      if (out.rn) ok &= nccl_allgather_inplace(ctx->comm, out.rn, ns, 8, ctx->rank, s);
+      if (out.conv) ok &= nccl_allgather_inplace(ctx->comm, out.conv, ns, 1, ctx->rank, s);
+      if (out.status) ok &= nccl_allgather_inplace(ctx->comm, out.status, ns, 4, ctx->rank, s);
+      if (!ok) return fail(ctx, CL_ERR_CUDA, "clomp: result all-gather failed");
     }
     CL_CUDA(ctx, cudaGetLastError());
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
@@ -1104,15 +1088,6 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode) {
     if (ctx->gfull) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->gfull);
-  cudaFree(ctx->ddt);
-  cudaFree(ctx->dt);
-  cudaFree(ctx->lv_tab);
-  cudaFree(ctx->at_r32);
-  cudaFree(ctx->at_c32);
-  cudaFree(ctx->at_r64);
-  cudaFree(ctx->at_c64);
-  cudaFree(ctx->gr);
-  cudaFree(ctx->gc);
       ctx->gfull = nullptr;
     }
     ctx->w.gfull = nullptr;
@@ -1266,7 +1241,7 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
 
 int cl_set_cluster_learn(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
-  ctx->cluster_learn = on < 0 ? 0 : (on > 2 ? 1 : on);
+  ctx->cluster_learn = on <= 0 ? 0 : 1;
   return CL_OK;
 }
 
@@ -1676,7 +1651,10 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
   if (tc) {
     float* d = nullptr;
     CL_CUDA(ctx, cudaMalloc(&d, (size_t)(batch * n) * 4));
-    launch_corr_tc_debug(p, w, d, s);
+    if (!launch_corr_tc_debug(p, w, d, s)) {
+      cudaFree(d);
+      return fail(ctx, CL_ERR_CUDA, "cl_debug_scores: tcgen05 launch failed");
+    }
     std::vector<float> h((size_t)(batch * n));
     CL_CUDA(ctx, cudaMemcpyAsync(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost, s));
     CL_CUDA(ctx, cudaStreamSynchronize(s));

@@ -15,10 +15,53 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <utility>
 
 namespace clb {
+
+// ---- per-device host caches
+// One slot per device for a host-computed value of one call site (SM count,
+// co-resident clusters, the dynamic shared-memory limit already raised).
+// Racing initialisers compute the same value and the slots are atomics, so
+// concurrent calls on distinct contexts (clomp_b200.h threading rule) are
+// data-race free, and a second device never reuses the first one's value.
+constexpr int kMaxDevices = 64;
+struct DevSlots {
+  std::atomic<long long> v[kMaxDevices];
+  long long get(int dev) const { return v[dev & (kMaxDevices - 1)].load(std::memory_order_relaxed); }
+  void set(int dev, long long x) { v[dev & (kMaxDevices - 1)].store(x, std::memory_order_relaxed); }
+};
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline int device_sms(int dev) {
+  static DevSlots cache;
+  long long v = cache.get(dev);
+  if (v <= 0) {
+    int s = 0;
+    if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || s <= 0) {
+      cudaGetLastError();
+      s = 148;
+    }
+    cache.set(dev, s);
+    v = s;
+  }
+  return (int)v;
+}
+// Raise kern's dynamic shared-memory limit on the current device to at least
+// `bytes` (once per device and size).
+template <class K>
+inline void ensure_smem_limit(DevSlots& slot, K kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  const int dev = current_device();
+  if ((long long)bytes <= slot.get(dev)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  slot.set(dev, (long long)bytes);
+}
 
 constexpr int kCorrTileAtoms = 64;    // fp64 SIMT correlation tile (atoms)
 constexpr int kCorrTileSignals = 64;  // fp64 SIMT correlation tile (signals)
@@ -104,9 +147,6 @@ struct SolveParams {
   int64_t nr, nc, mr, mc, ldr, ldc;
   // th == 1 selection runs inside the learning kernel (warp per signal)
   int32_t fuse_select;
-  // r64 is not stored by the residual kernel; the rare near-tie rescoring
-  // recomputes the row it needs (tensor path, th == 1, ldm <= 512)
-  int32_t lazy_r64;
   double a_inv_scale;       // 1 / (power-of-two scale of the fp16 dictionary split)
   // supports of 33..256 atoms learn on CTA clusters with register-resident
   // Gram blocks (k_learn_cluster); 0 keeps them on k_learn_block (tests)
@@ -125,11 +165,6 @@ struct SolveParams {
   // variance on x = D S (clomp.cpp:93-119), batch-global weights
   double w_tv_g, w_lv_g;
   int32_t lv_on, lv_window, lv_stride, lv_nr, lv_nc;
-  // K1 overlaps the learning tail (per-signal th == 1 fast path): the learning
-  // kernels count finished signals per 128-signal tile in Work::tile_done and
-  // the next K1 starts a tile once its count reaches tile_wait x its signals
-  // (tile_wait = outer - 1; 0 = the plain programmatic wait)
-  int32_t tile_flags, tile_wait;
   // warp learners (plain GD): power levels L for support buckets of 8 / 16 /
   // 24 / 32 atoms (E = 2^L q + r epochs as L squarings + q + popcount(r) steps)
   int32_t warp_L[4];
@@ -185,7 +220,6 @@ struct Work {
   double* pw_part = nullptr;       // [pw_slots][row chunks] residual sum-of-squares partials
   int32_t* pw_cnt = nullptr;       // [pw_slots] finished row chunks (reset by the last one)
   int32_t* counters = nullptr;     // see Counter
-  int32_t* tile_done = nullptr;    // [B/128 + 2] signals finished per K1 signal tile (monotonic per solve)
   double* joint = nullptr;         // see Joint
   // priors (SolveParams::prior)
   const double* ddt = nullptr;     // [n][ldd] Delta D atom-major (fp64)
@@ -211,13 +245,20 @@ struct Work {
 
 enum Counter {
   kCounter0 = 0,      // (unused)
-  kActiveCount = 1,   // signals still iterating after this outer iteration
+  kCounter1 = 1,      // (unused)
   kMaxCount = 2,      // max support size over the batch
   kRescanTotal = 3,   // rescans over the whole solve
   kBigCount = 4,      // signals queued for the block learning kernel; slots
                       // 4 + (outer & 1), the block kernel clears the other one
+  kActive0 = 6,       // signals still iterating after outer iteration o: slot
+                      // 6 + (o & 1) (active_slot), incremented by the stopping
+                      // rules of iteration o and cleared by the learning kernel
+                      // of iteration o - 1, i.e. one whole kernel boundary
+                      // before any increment (no in-grid store/atomic race)
   kNumCounters = 8
 };
+
+__host__ __device__ __forceinline__ int active_slot(int outer) { return kActive0 + (outer & 1); }
 
 enum Joint {
   kJBest = 0, kJPrev = 1, kJTotal = 2, kJStall = 3, kJImproved = 4,
@@ -270,9 +311,11 @@ bool corr_tc_available();
 int corr_tc_trace(unsigned long long* out, int max_ctas);
 int cluster_trace(unsigned long long* out);
 int64_t corr_tc_tile_atoms();
-void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
+// false: the tensor maps could not be encoded or the launch failed (the
+// caller reports CL_ERR_CUDA; stale candidate records are never consumed).
+bool launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
 // Same kernel, additionally writing the signed fp32 scores [B][n] (tests).
-void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
+bool launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
                           cudaStream_t s);
 void launch_split_dict(const float* src, __half* hi, __half* lo, int64_t count, float scale,
                        cudaStream_t s);

@@ -268,16 +268,7 @@ k_corr_gemv(const float* __restrict__ at, const double* __restrict__ r,
   }
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+int num_sms() { return device_sms(current_device()); }
 
 template <int NB, int V>
 void launch_nb(const SolveParams& p, const Work& w, bool full_scores, cudaStream_t s) {
@@ -296,12 +287,8 @@ void launch_nb(const SolveParams& p, const Work& w, bool full_scores, cudaStream
                                     kRingBytes / (sa * (row_bytes + (int64_t)NB * G * 8)));
   }
   const size_t smem = (size_t)stages * sa * (row_bytes + (size_t)NB * G * 8);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_corr_gemv<NB, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRingBytes);
-    attr_set = true;
-  }
+  static DevSlots attr_set;
+  ensure_smem_limit(attr_set, k_corr_gemv<NB, V>, kRingBytes);
   const int grid = (int)std::min<int64_t>(p.ntl, num_sms());
   k_corr_gemv<NB, V><<<grid, 32 * (G + 2), smem, s>>>(
       w.at32 + p.atom0 * p.ldm, w.r64, w.active, p.n_corr, p.B, p.ldm, p.ntl, sa, stages,

@@ -487,30 +487,12 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-// K1 may start a signal tile before the learning kernels of the previous
-// iteration have exited (SolveParams::tile_flags): thread 0 waits until the
-// tile's finished-signal count reaches `target` (acquire), then orders the
-// async proxy (TMA) after it.  A bounded spin: past it the plain programmatic
-// wait (predecessor grid complete) is used instead, so a count that never
-// arrives costs time, never correctness.
-__device__ __forceinline__ void wait_tile_ready(const int32_t* flag, int target) {
-  bool ok = target <= 0;
-  for (int i = 0; !ok && i < (1 << 16); ++i) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    ok = v >= target;
-    if (!ok) __nanosleep(64);
-  }
-  if (!ok) pdl_wait();
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
 __global__ void __launch_bounds__(32 * kPairWarps, 1)
 k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
            const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
            int64_t n, int64_t B, int kblocks, int64_t ntile, const float* __restrict__ r_scale,
            double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg,
-           const int32_t* tile_done, int tile_wait, const int32_t* __restrict__ active) {
+           const int32_t* __restrict__ active) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -552,17 +534,8 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
   cluster_sync();  // both CTAs' barriers and TMEM exist before any cross-CTA traffic
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (tile_wait > 0) {  // this tile's residual split, counted by the learners
-    pdl_trigger();
-    if (threadIdx.x == 0) {
-      const int64_t cnt = B - m0 < TM ? (B - m0 > 0 ? B - m0 : 0) : TM;
-      wait_tile_ready(tile_done + blockIdx.x, (int)(tile_wait * cnt));
-    }
-    __syncthreads();
-  } else {
-    pdl_wait();  // the residual split of the previous kernel
-    pdl_trigger();
-  }
+  pdl_wait();  // the residual split of the previous kernel
+  pdl_trigger();
   if (threadIdx.x == 0) K1_MARK(1);
   // A pair whose 256 signals have all stopped has no reader for its records:
   // both CTAs read the same flags and skip to the teardown together (batches
@@ -627,9 +600,6 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
   tile_epilogue<kPairWarps>(smem, tmem, accum, m0, n0, n, B, ntile, r_scale, a_inv_scale, cand,
                             scores_dbg, warp, lane, blockIdx.y);
   }  // live pair
-  // early start: this grid completes only after its predecessor (the block
-  // learner), so every later kernel still sees the whole iteration finished
-  if (tile_wait > 0) pdl_wait();
   if (threadIdx.x == 0) K1_MARK(5);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -639,201 +609,6 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ C
                  "r"(TMEM_COLS));
   }
   if (threadIdx.x == 64) K1_MARK(6);
-}
-
-// ------------------------------------- CTA pair, two accumulator halves
-// The pair tile's 256 atoms as two N = 128 halves accumulated in TMEM
-// columns [0, 128) and [128, 256): all k-blocks of half 0, commit, then all
-// k-blocks of half 1 (the residual slice is streamed twice, from L2), so the
-// epilogue of half 0 runs under the MMAs of half 1 and only half 1's drain
-// (32 columns per thread) follows the last MMA.  Warps 0 / 1 only produce /
-// issue; warps 2..17 drain TMEM (lane quarter = warp % 4, column part =
-// (warp - 2) / 4).  A part's columns are not contiguous across the halves, so
-// the part merge breaks exact ties by the lower atom explicitly.
-constexpr int A2S_BYTES = (TN / 4) * BK * 2;  // 4 KB: a CTA's 64 atoms of a half
-constexpr int STAGE2S_BYTES = 2 * R_BYTES + 2 * A2S_BYTES;
-constexpr int STAGES2S = 8;
-constexpr int SMEM2S_BYTES = STAGES2S * STAGE2S_BYTES + 1024 + 256;
-constexpr uint32_t kIdesc2s = (1u << 4) | (((TN / 2) >> 3) << 17) | ((2 * TM >> 4) << 24);
-constexpr int kSplitWarps = 18;
-
-__device__ __forceinline__ void mma_f16_pair_s(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc2s), "r"(accumulate));
-}
-
-__global__ void __launch_bounds__(32 * kSplitWarps, 1)
-k_corr_tc2s(const __grid_constant__ CUtensorMap tm_rhi, const __grid_constant__ CUtensorMap tm_rlo,
-            const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-            int64_t n, int64_t B, int kblocks, int64_t ntile, const float* __restrict__ r_scale,
-            double a_inv_scale, Cand* __restrict__ cand, float* __restrict__ scores_dbg) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2S * STAGE2S_BYTES);
-  uint64_t* empty = full + STAGES2S;
-  uint64_t* accum = empty + STAGES2S;  // [2]: one per half
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();  // 0 = leader
-  const int64_t m0 = (int64_t)blockIdx.x * TM;  // this CTA's 128 signals
-  const int64_t n0 = (int64_t)blockIdx.y * TN;  // the pair's 256 atoms
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(&accum[0], 1);
-    mbar_init(&accum[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rhi)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rlo)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)));
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  cluster_sync();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // the residual split of the previous kernel
-  pdl_trigger();
-  const int total = 2 * kblocks;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer (both CTAs)
-      const uint32_t full0 = mapa_u32(smem_u32(&full[0]), 0);
-      for (int it = 0; it < total; ++it) {
-        const int h = it / kblocks, kb = it - h * kblocks;
-        const int s = it % STAGES2S;
-        const uint32_t ph = (it / STAGES2S) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2S_BYTES);
-        uint8_t* st = smem + s * STAGE2S_BYTES;
-        const uint32_t bar = full0 + (uint32_t)(s * 8);
-        const int k0 = kb * BK;
-        const int arow = (int)n0 + h * (TN / 2) + (int)rank * (TN / 4);
-        tma_load_2d_pair(st, &tm_rhi, bar, k0, (int)m0);
-        tma_load_2d_pair(st + R_BYTES, &tm_rlo, bar, k0, (int)m0);
-        tma_load_2d_pair(st + 2 * R_BYTES, &tm_ahi, bar, k0, arow);
-        tma_load_2d_pair(st + 2 * R_BYTES + A2S_BYTES, &tm_alo, bar, k0, arow);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer: the leader's single thread for the pair
-      for (int it = 0; it < total; ++it) {
-        const int h = it / kblocks, kb = it - h * kblocks;
-        const int s = it % STAGES2S;
-        const uint32_t ph = (it / STAGES2S) & 1;
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint8_t* st = smem + s * STAGE2S_BYTES;
-        const uint64_t d_rhi = sw128_desc(smem_u32(st));
-        const uint64_t d_rlo = sw128_desc(smem_u32(st + R_BYTES));
-        const uint64_t d_ahi = sw128_desc(smem_u32(st + 2 * R_BYTES));
-        const uint64_t d_alo = sw128_desc(smem_u32(st + 2 * R_BYTES + A2S_BYTES));
-        const uint32_t td = tmem + (uint32_t)(h * (TN / 2));
-#pragma unroll
-        for (int j = 0; j < BK / 16; ++j) {
-          const uint64_t adv = (uint64_t)(j * 32) >> 4;
-          mma_f16_pair_s(td, d_rhi + adv, d_alo + adv, (kb | j) != 0);
-          mma_f16_pair_s(td, d_rlo + adv, d_ahi + adv, 1);
-          mma_f16_pair_s(td, d_rhi + adv, d_ahi + adv, 1);
-        }
-        if (it < total - STAGES2S) mma_commit_pair(&empty[s]);
-        if (kb == kblocks - 1) mma_commit_pair(&accum[h]);  // half h complete in both CTAs
-      }
-    }
-  } else {
-    // ---------------- epilogue: 16 warps, thread = signal, 32 columns per half
-    const int wl = warp & 3, part = (warp - 2) >> 2;
-    const int64_t b = m0 + wl * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(wl * 32) << 16;
-    float v1 = -1.f, v2 = -1.f, v3 = -1.f;
-    int i1 = 0x7fffffff, i2 = 0x7fffffff;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      mbar_wait(&accum[h], 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int col = h * (TN / 2) + part * 32;
-      uint32_t raw[32];
-      tmem_ld_32_nowait(tmem + lane_base + (uint32_t)col, raw);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float v[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(raw[q]);
-      const int64_t a0 = n0 + col;
-      if (scores_dbg && b < B) {
-        const double u = (double)r_scale[b] * a_inv_scale;
-        for (int q = 0; q < 32; ++q)
-          if (a0 + q < n) scores_dbg[b * n + a0 + q] = (float)((double)v[q] * u);
-      }
-      if (a0 + 32 <= n)
-        cand_scan32<false>(v, (int)a0, 32, v1, i1, v2, i2, v3);
-      else if (a0 < n)
-        cand_scan32<true>(v, (int)a0, (int)(n - a0), v1, i1, v2, i2, v3);
-    }
-    // every MMA retired: the stage ring holds the part records for the merge
-    float* mv = reinterpret_cast<float*>(smem);       // [4][3][TM]
-    int* mi = reinterpret_cast<int*>(mv + 4 * 3 * TM);  // [4][2][TM]
-    const int row = wl * 32 + lane;
-    if (part > 0) {
-      mv[(part * 3 + 0) * TM + row] = v1;
-      mv[(part * 3 + 1) * TM + row] = v2;
-      mv[(part * 3 + 2) * TM + row] = v3;
-      mi[(part * 2 + 0) * TM + row] = i1;
-      mi[(part * 2 + 1) * TM + row] = i2;
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * (kSplitWarps - 2)) : "memory");
-    if (part == 0 && b < B) {
-      auto ins = [&](float x, int k) {  // lexicographic: larger score, then lower atom
-        const bool g1 = x > v1 || (x == v1 && k < i1);
-        const bool g2 = x > v2 || (x == v2 && k < i2);
-        i2 = g1 ? i1 : (g2 ? k : i2);
-        i1 = g1 ? k : i1;
-        v3 = fmaxf(v3, fminf(x, v2));
-        v2 = fmaxf(v2, fminf(x, v1));
-        v1 = fmaxf(v1, x);
-      };
-#pragma unroll
-      for (int q = 1; q < 4; ++q) {
-        ins(mv[(q * 3 + 0) * TM + row], mi[(q * 2 + 0) * TM + row]);
-        ins(mv[(q * 3 + 1) * TM + row], mi[(q * 2 + 1) * TM + row]);
-        v3 = fmaxf(v3, mv[(q * 3 + 2) * TM + row]);
-      }
-      const double u = (double)r_scale[b] * a_inv_scale;
-      Cand r;
-      r.v1 = v1 >= 0.f ? (double)v1 * u : -1.0;
-      r.v2 = v2 >= 0.f ? (double)v2 * u : -1.0;
-      r.v3 = v3 >= 0.f ? (double)v3 * u : -1.0;
-      r.i1 = i1;
-      r.i2 = i2;
-      cand[b * ntile + blockIdx.y] = r;
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  cluster_sync();  // the pair's MMAs / commits are done before TMEM goes
-  if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
 }
 
 // fp16 split of the dictionary: scale*x = hi + lo with scale = 2^e chosen by
@@ -923,39 +698,14 @@ int64_t corr_tc_tile_atoms() { return TN; }
 
 constexpr int kCluster = 4;
 
-static int g_tc_mode = -1;  // -1 auto, 0 one-SM kernel, 1 CTA pair (CL_TC_PAIR)
+static std::atomic<int> g_tc_mode{-1};  // -1 auto, 0 one-SM kernel, 1 CTA pair (CL_TC_PAIR)
 
 static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_dbg,
                            cudaStream_t s) {
   const int64_t mtiles = (p.B + TM - 1) / TM;
   if (g_tc_mode < 0) {
     const char* e = getenv("CL_TC_PAIR");
-    g_tc_mode = e ? atoi(e) : 1;
-  }
-  if (g_tc_mode == 2 && mtiles >= 2) {  // pair kernel with two accumulator halves
-    const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
-    const CUtensorMap* rlo = cached_map(1, w.r_lo, p.B, p.ldm, TM);
-    const CUtensorMap* ahi = cached_map(2, w.at_hi + p.atom0 * p.ldm, p.n_corr, p.ldm, TN / 4);
-    const CUtensorMap* alo = cached_map(3, w.at_lo + p.atom0 * p.ldm, p.n_corr, p.ldm, TN / 4);
-    if (!rhi || !rlo || !ahi || !alo) return false;
-    cudaFuncSetAttribute(k_corr_tc2s, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2S_BYTES);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)((mtiles + 1) / 2 * 2), (unsigned)((p.n_corr + TN - 1) / TN));
-    cfg.blockDim = dim3(32 * kSplitWarps);
-    cfg.dynamicSmemBytes = SMEM2S_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, k_corr_tc2s, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
-                              (int)(p.ldm / BK), p.ntl, (const float*)w.r_scale, p.a_inv_scale,
-                              w.cand, scores_dbg) == cudaSuccess;
+    g_tc_mode.store(e ? atoi(e) : 1);
   }
   if (g_tc_mode >= 1 && mtiles >= 2) {
     const CUtensorMap* rhi = cached_map(0, w.r_hi, p.B, p.ldm, TM);
@@ -980,9 +730,7 @@ static bool launch_tc_impl(const SolveParams& p, const Work& w, float* scores_db
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, k_corr_tc2, *rhi, *rlo, *ahi, *alo, p.n_corr, p.B,
                               (int)(p.ldm / BK), p.ntl, (const float*)w.r_scale, p.a_inv_scale,
-                              w.cand, scores_dbg, (const int32_t*)w.tile_done,
-                              p.tile_flags && p.atom0 == 0 ? (int)p.tile_wait : 0,
-                              (const int32_t*)w.active) == cudaSuccess;
+                              w.cand, scores_dbg, (const int32_t*)w.active) == cudaSuccess;
   }
   const bool clustered = mtiles >= kCluster;
   const int arows = clustered ? TN / kCluster : TN;
@@ -1036,13 +784,13 @@ int corr_tc_trace(unsigned long long* out, int max_ctas) {
 #endif
 }
 
-void launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
-  launch_tc_impl(p, w, nullptr, s);
+bool launch_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
+  return launch_tc_impl(p, w, nullptr, s);
 }
 
-void launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
+bool launch_corr_tc_debug(const SolveParams& p, const Work& w, float* scores,
                           cudaStream_t s) {
-  launch_tc_impl(p, w, scores, s);
+  return launch_tc_impl(p, w, scores, s);
 }
 
 void launch_split_dict(const float* src, __half* hi, __half* lo, int64_t count, float scale,

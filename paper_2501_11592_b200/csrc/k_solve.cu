@@ -253,42 +253,8 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
 
 // Near-tied th == 1 selection: exact rescoring of the band, every tie with the
 // exact maximum injected (see above).  Updates sup / cnt / mask / changed.
-// r64 row of signal b from its current support and coefficients (same
-// per-element operation order as warp_residual), for lazy_r64 contexts.
-__device__ void recompute_r64_row(const SolveParams& p, const Work& w, int64_t b, int t,
-                                  int lane) {
-  const int64_t cap = p.cap;
-  const float* y = w.y32 + b * p.ldm;
-  for (int64_t i0 = 0; i0 < p.ldm; i0 += 128) {  // lane owns rows i0 + lane + 32 q
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k0 = 0; k0 < t; k0 += 32) {  // support in warp-sized pieces
-      const int kk = k0 + lane;
-      const int32_t sk = kk < t ? w.sup[b * cap + kk] : 0;
-      const double ck = kk < t ? w.coef[b * cap + kk] : 0.0;
-      const int kn = t - k0 < 32 ? t - k0 : 32;
-#pragma unroll 4
-      for (int k = 0; k < kn; ++k) {
-        const int64_t a = (int64_t)__shfl_sync(kFull, sk, k) * p.ldm;
-        const double c = __shfl_sync(kFull, ck, k);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t i = i0 + lane + 32 * q;
-          if (i < p.ldm) acc[q] = fma(f2d(w.at32[a + i]), c, acc[q]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t i = i0 + lane + 32 * q;
-      if (i < p.ldm) w.r64[b * p.ldm + i] = acc[q] - f2d(y[i]);
-    }
-  }
-  __syncwarp();
-}
-
 __device__ void select_near_tie(const SolveParams& p, const Work& w, int64_t b, double v1,
                                 double delta, int t_old, int lane) {
-  if (p.lazy_r64) recompute_r64_row(p, w, b, t_old, lane);
   PickState ps{t_old, 0, 0};
   if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
   const double cut = v1 - 2.0 * delta;
@@ -469,7 +435,7 @@ __device__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
     w.conv[b] = 1;
     w.active[b] = 0;
   } else {
-    atomicAdd(&w.counters[kActiveCount], 1);
+    atomicAdd(&w.counters[active_slot(outer)], 1);
   }
   return snap;
 }
@@ -597,9 +563,6 @@ __device__ __forceinline__ void affine_steps(const double (&m)[TB], double& c, d
 // of P once (A-layout fragments F(I, K) = P[8I + lane/4][4K + lane%4]) and the
 // whole product runs from registers; the shared-memory broadcast traffic of
 // the SIMT squaring disappears.
-#ifndef CL_SQ_ILP
-#define CL_SQ_ILP 0
-#endif
 template <int T>
 __device__ __forceinline__ void square_dmma(double* buf, int lane) {
   constexpr int NI = T / 8, NK = T / 4, LD = T + 4;
@@ -610,36 +573,6 @@ __device__ __forceinline__ void square_dmma(double* buf, int lane) {
 #pragma unroll
     for (int K = 0; K < NK; ++K) f[I][K] = buf[(8 * I + r) * LD + 4 * K + c];
   __syncwarp();
-#if CL_SQ_ILP
-  // Upper block triangle only (J >= I), all blocks' accumulators live at once
-  // (independent DMMA chains); off-diagonal blocks also written transposed.
-  double acc[NI][NI][2];
-#pragma unroll
-  for (int I = 0; I < NI; ++I)
-#pragma unroll
-    for (int J = I; J < NI; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
-#pragma unroll
-  for (int K = 0; K < NK; ++K)
-#pragma unroll
-    for (int I = 0; I < NI; ++I)
-#pragma unroll
-      for (int J = I; J < NI; ++J)
-        asm volatile(
-            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-            : "+d"(acc[I][J][0]), "+d"(acc[I][J][1])
-            : "d"(f[I][K]), "d"(f[J][K]));
-#pragma unroll
-  for (int I = 0; I < NI; ++I)
-#pragma unroll
-    for (int J = I; J < NI; ++J) {
-      *reinterpret_cast<double2*>(buf + (8 * I + r) * LD + 8 * J + 2 * c) =
-          make_double2(acc[I][J][0], acc[I][J][1]);
-      if (J != I) {
-        buf[(8 * J + 2 * c) * LD + 8 * I + r] = acc[I][J][0];
-        buf[(8 * J + 2 * c + 1) * LD + 8 * I + r] = acc[I][J][1];
-      }
-    }
-#else
   // Upper block triangle only (J >= I): the product is symmetric, so each
   // off-diagonal 8x8 block is also written transposed (NI(NI+1)/2 of NI^2
   // blocks computed: 10 of 16 at T = 32).
@@ -666,7 +599,6 @@ __device__ __forceinline__ void square_dmma(double* buf, int lane) {
       }
     }
   }
-#endif
   __syncwarp();
 }
 
@@ -926,10 +858,8 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
         r[4 * q + 1] -= y01.y;
         r[4 * q + 2] -= y23.x;
         r[4 * q + 3] -= y23.y;
-        if (!p.lazy_r64) {
-          *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
-          *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
-        }
+        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
+        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) lacc = fma(r[4 * q + e], r[4 * q + e], lacc);
       }
@@ -1153,20 +1083,6 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
 // works on registers (support membership by ballot instead of the mask), the
 // new Gram row comes from gfull and b_k = a_k . y (round trip 2), and the
 // epochs start with everything in registers / shared memory.
-// Signal b is finished for this iteration (residual split, scale, records read):
-// count it for its K1 signal tile (SolveParams::tile_flags).  Every lane's
-// writes are ordered before lane 0's release by the fences and the warp barrier.
-__device__ __forceinline__ void tile_done_warp(const SolveParams& p, const Work& w, int64_t b,
-                                               int lane) {
-  if (!p.tile_flags) return;
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    atomicAdd(&w.tile_done[b >> 7], 1);
-  }
-}
-
 template <int TB, int OPT>
 __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, int64_t b,
                                            int outer, int32_t* big_list, double* cs,
@@ -1350,9 +1266,10 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();
   pdl_trigger();
-  // this iteration's active count starts here (incremented by the stopping
-  // rules after learning; read by the host one graph chunk later)
-  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
+  // the NEXT iteration's active count starts here (this iteration's slot was
+  // cleared by the previous iteration's learning kernel; the stopping rules
+  // increment it after learning, the host reads it one graph chunk later)
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[active_slot(outer + 1)] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi) return;
   double* s1 = sq_all[warp];
@@ -1399,12 +1316,11 @@ k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   __syncwarp();
   pdl_wait();
   pdl_trigger();
-  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kActiveCount] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[active_slot(outer + 1)] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi) return;
-  const bool queued = learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp],
-                                         sq_all[warp], &bar_all[warp], lane);
-  if (!queued) tile_done_warp(p, w, b, lane);
+  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp], sq_all[warp],
+                     &bar_all[warp], lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -1426,15 +1342,8 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
   __shared__ double s_L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kBlockThreads / 32;
-  // tile_flags: trigger first, so the next K1 may start the tiles whose signals
-  // are done while this kernel still waits for the learner
-  if (p.tile_flags) {
-    pdl_trigger();
-    pdl_wait();
-  } else {
-    pdl_wait();
-    pdl_trigger();
-  }
+  pdl_wait();
+  pdl_trigger();
   const int count = w.counters[kBigCount + (outer & 1)];
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[kBigCount + ((outer + 1) & 1)] = 0;
   const int64_t cap = p.cap;
@@ -1600,12 +1509,7 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
     if (w.r_hi) split_row(w, b, p.ldm, s_L, tid, kBlockThreads);  // own r64 entries
     if (snap_s)
       for (int i = tid; i < t; i += kBlockThreads) w.best_coef[b * cap + i] = cs[i];
-    if (p.tile_flags) __threadfence();
     __syncthreads();
-    if (p.tile_flags && tid == 0) {  // this big signal is done: count it for K1
-      __threadfence();
-      atomicAdd(&w.tile_done[b >> 7], 1);
-    }
   }
 }
 
@@ -2731,9 +2635,6 @@ constexpr int kFusedThreads = 256;
 #define CL_FUSED_ATOMS 32
 #endif
 constexpr int kFusedAtoms = CL_FUSED_ATOMS;  // atoms per warp pass of the correlation (was 8)
-#ifndef CL_FUSED_WL
-#define CL_FUSED_WL 0  // 1: learner reads the staged copy too (measured neutral at config 1)
-#endif
 #ifndef CL_FUSED_STAGE_MAX
 #define CL_FUSED_STAGE_MAX (200 * 1024)
 #endif
@@ -2809,13 +2710,7 @@ k_solve_fused(SolveParams p, Work w, int stage_a) {
       __syncwarp();
       if (w.active[b] && w.cnt[b] <= kWarpCap) {
         stage_gram_async(p, w, b, w.gcnt[b], sq, kWarpCap + 4, lane);
-#if CL_FUSED_WL
-        Work wl = w;  // the learner's atom reads (Gram extension, b_k) from the staged copy
-        wl.at32 = At;
-        learn_warp_body<kWarpCap, OPT>(p, wl, b, outer, cs, sups, sq, nullptr, lane);
-#else
         learn_warp_body<kWarpCap, OPT>(p, w, b, outer, cs, sups, sq, nullptr, lane);
-#endif
       }
       else if (lane == 0 && w.active[b])
         w.status[b] = 7, w.active[b] = 0;  // capacity: larger supports use the batched path
@@ -2882,20 +2777,25 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
   if (!init && w.joint[kJStop] != 0.0) {
     if (threadIdx.x == 0) {
       w.joint[kJImproved] = 0.0;
-      w.counters[kActiveCount] = 0;
+      w.counters[active_slot(outer)] = 0;
     }
     return;
   }
   __shared__ int chg[32];
   const int tid = threadIdx.x;
   double s = 0.0;
-  int any = 0;
+  int any = 0, full = 0;
   for (int64_t b = tid; b < p.B; b += blockDim.x) {
     s += w.loss[b];
     any |= w.changed[b];
+    // a signal whose support outgrew the per-signal capacity stopped learning
+    // (pick_finish / warp_threshold_append): the batch cannot continue with
+    // the reference's semantics, so it stops with the capacity status
+    if (!init) full |= w.status[b] == kStatusCapacity;
   }
   red[tid] = s;
   any = __any_sync(kFull, any);
+  full = __syncthreads_or(full);
   if ((tid & 31) == 0) chg[tid >> 5] = any;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
@@ -2931,7 +2831,10 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
     } else {
       J[kJTotal] = total;
       J[kJTotalR] = total_r;
-      if (!isfinite(total)) {
+      if (full) {
+        J[kJStatus] = (double)kStatusCapacity;
+        stop = 1;
+      } else if (!isfinite(total)) {
         J[kJStatus] = (double)kStatusNumerical;
         stop = 1;
       } else {
@@ -2957,7 +2860,7 @@ k_joint_control(SolveParams p, Work w, int outer, int init) {
       }
     }
     J[kJStop] = stop;
-    w.counters[kActiveCount] = stop ? 0 : (int)p.B;
+    w.counters[active_slot(outer)] = stop ? 0 : (int)p.B;
     stop_s = stop;
   }
   __syncthreads();
@@ -3143,7 +3046,9 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
     // Clusters must fit inside a GPC: not every SM can host one.  A grid of
     // more clusters than can be co-resident runs its last clusters in a second
     // wave (each cluster loops over signals), so cap it at the occupancy.
-    static int max_active = 0;
+    static DevSlots active_cache;
+    const int dev = current_device();
+    int max_active = (int)active_cache.get(dev);
     if (max_active == 0) {
       int nmax = 0;
       if (cudaOccupancyMaxActiveClusters(&nmax, k_learn_cluster<Q, CW, NWC, RW, 0>, &cfg) !=
@@ -3153,6 +3058,7 @@ static void launch_cluster_q(const SolveParams& p, const Work& w, int outer, int
         nmax = -1;
       }
       max_active = nmax;
+      active_cache.set(dev, nmax);
     }
     if (max_active > 0 && nclusters > max_active) {
       nclusters = max_active;
@@ -3185,7 +3091,7 @@ static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, 
                                 int64_t nsig, int sms, cudaStream_t s, int* extra) {
   if (p.sep || max_cnt <= kWarpCap || p.cluster_learn == 0) return 0;
   auto nc = [&](int q) { return (int)std::max<int64_t>(1, std::min<int64_t>(nsig, sms / q)); };
-  const bool pw = p.pw_levels > 0 && p.opt == 0 && p.cluster_learn != 2;
+  const bool pw = p.pw_levels > 0 && p.opt == 0;
   auto run = [&](auto launch, int tmax) {
     if (!pw) {
       launch(0);
@@ -3220,15 +3126,6 @@ static int launch_cluster_learn(const SolveParams& p, const Work& w, int outer, 
     run([&](int ph) { launch_cluster_q<1, 4, 16, 8>(p, w, outer, w.big_list, nc(1), s, ph); },
         128);
     return 128;
-  }
-  if (p.cluster_learn == 2) {
-    // eight CTAs of 4-row warps (half the registers per thread, two CTAs per
-    // SM, a four-partial reduction): measured slower than four 8-row CTAs
-    // (config 3: 414 vs 360 ms; config 7 equal) — kept for comparison
-    launch_cluster_q<8, 8, 8, 4>(p, w, outer, w.big_list,
-                                 (int)std::max<int64_t>(1, std::min<int64_t>(nsig, 2 * sms / 8)),
-                                 s);
-    return 256;
   }
   run([&](int ph) { launch_cluster_q<4, 8, 8, 8>(p, w, outer, w.big_list, nc(4), s, ph); }, 256);
   return 256;
@@ -3312,11 +3209,8 @@ void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaSt
 void launch_image_learn(const SolveParams& p, const Work& w, int outer, cudaStream_t s) {
   const unsigned cgrid = (unsigned)std::min<int64_t>(p.B, 2048);
   const size_t smem = (size_t)p.cap * 12 + 16;
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaFuncSetAttribute(k_img_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = smem;
-  }
+  static DevSlots smem_set;
+  ensure_smem_limit(smem_set, k_img_synth, smem);
   const int64_t npix = p.n * p.B;
   const unsigned pgrid = (unsigned)((npix + 255) / 256);
   const int64_t nwin = (int64_t)p.lv_nr * p.lv_nc;
@@ -3367,23 +3261,14 @@ void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStre
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s) {
   // latency-bound path: the SM count and the smem attribute are queried / set
   // once per device (the attribute only grows), not per call
-  static int sms_of[64] = {0};
-  static size_t smem_set[64][3] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  dev &= 63;
-  if (sms_of[dev] == 0) cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int sms = sms_of[dev];
+  static DevSlots smem_set[3];
+  const int sms = device_sms(current_device());
   // stage A in shared memory when it fits and every signal still gets its own SM
   const size_t a_bytes = (size_t)(p.n * p.ldm) * 4;
   const int stage_a = (p.ldm * 8 + a_bytes <= (size_t)kFusedStageMax && p.B <= sms) ? 1 : 0;
   const size_t smem = (size_t)p.ldm * 8 + (stage_a ? a_bytes : 0);
   auto go = [&](auto kern) {
-    size_t& set = smem_set[dev][p.opt < 0 ? 0 : (p.opt > 2 ? 2 : p.opt)];
-    if (smem > 48 * 1024 && smem > set) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = smem;
-    }
+    ensure_smem_limit(smem_set[p.opt < 0 ? 0 : (p.opt > 2 ? 2 : p.opt)], kern, smem);
     kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w, stage_a);
   };
   switch (p.opt) {

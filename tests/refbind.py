@@ -11,7 +11,7 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_2501_11592_b200 import CConfig, ClompConfig
+from paper_2501_11592_b200.configs import CConfig, ClompConfig
 
 ROOT = Path(__file__).resolve().parents[1]
 ORACLE_SO = ROOT / "oracle" / "_build" / "libclomp_oracle.so"
@@ -73,9 +73,25 @@ def ref() -> C.CDLL:
         h.ref_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, vp]
         h.ref_rng_draws.argtypes = [C.c_uint64, C.c_int, C.c_uint64, i64, vp, vp]
         h.ref_dct_basis.argtypes = [i64, vp]
+        h.ref_gen_problem_1d.argtypes = [C.c_uint64, i64, i64, i64, i64, C.c_int, C.c_int,
+                                         C.c_double, vp, vp, vp]
         h.ref_force_isa.argtypes = [C.c_int]
         _ref = h
     return _ref
+
+
+def ref_gen_problem_1d(seed, m, n, k, batch, normalize=True, value_law=0, snr_db=-1.0,
+                       want_x=True):
+    """The harness's seeded problem drawn with the reference's cskit::Rng
+    (oracle/ref_harness.cpp): (A m x n fp32, X n x B fp64 or None, Y m x B fp32)."""
+    A = np.zeros((m, n), np.float32)
+    X = np.zeros((n, batch)) if want_x else None
+    Y = np.zeros((m, batch), np.float32)
+    code = ref().ref_gen_problem_1d(seed, m, n, k, batch, int(normalize), int(value_law),
+                                    float(snr_db), _p(A), _p(X), _p(Y))
+    if code:
+        raise ValueError("ref_gen_problem_1d: bad sizes")
+    return A, X, Y
 
 
 def orc_solve(A, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2, trace=False, basis=None):

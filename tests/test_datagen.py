@@ -51,3 +51,21 @@ def test_dct_basis_matches_reference_bit_for_bit(built_lib):
     assert np.array_equal(cl.dct_basis(8), ARR["dct8"])
     D = cl.dct_basis(64)
     assert np.allclose(D.T @ D, np.eye(64), atol=1e-13)
+
+
+@pytest.mark.parametrize("args", [(7, 64, 128, 5, 3, 0, 40.0), (2, 96, 300, 12, 5, 1, -1.0),
+                                  (1, 128, 256, 10, 9, 0, 40.0)])
+def test_reference_side_generator_matches_product(built_lib, args):
+    """bench.py's reference arm draws its inputs with the reference's own
+    cskit::Rng (oracle/ref_harness.cpp) instead of the product library; both
+    generators must produce the same bits."""
+    import refbind
+
+    if not refbind.ref_available():
+        pytest.skip("oracle/_ref not built")
+    seed, m, n, k, B, law, snr = args
+    A, X, Y, _ = cl.gen_problem_1d(seed, m, n, k, B, value_law=law, snr_db=snr)
+    A2, X2, Y2 = refbind.ref_gen_problem_1d(seed, m, n, k, B, value_law=law, snr_db=snr)
+    assert np.array_equal(A, A2)
+    assert np.array_equal(X, X2)
+    assert np.array_equal(Y, Y2)
