@@ -179,6 +179,25 @@ static inline double entry(const problem_t* p, int64_t q, int64_t j) {
 static void residual(const problem_t* p, const double* s, const support_t* sup,
                      const double* y, double* r) {
   const int64_t B = p->batch;
+  if (p->at) {
+    /* Same per-element sums (support order, the same mac sequence from 0.0),
+     * accumulated atom by atom over contiguous rows of the transposed copy
+     * instead of gathering A's strided columns (cache-friendly at config 3's
+     * 512 MB dictionary; bit-identical results). */
+    const int64_t m = p->m;
+    for (int64_t b = 0; b < B; ++b) {
+      for (int64_t i = 0; i < m; ++i) r[i * B + b] = 0.0;
+      const support_t* sb = &sup[b];
+      for (int64_t q = 0; q < sb->count; ++q) {
+        const int64_t j = sb->idx[q];
+        const double* atrow = p->at + j * m;
+        const double sj = s[j * B + b];
+        for (int64_t i = 0; i < m; ++i) r[i * B + b] = mac(r[i * B + b], atrow[i], sj, p->isa);
+      }
+      for (int64_t i = 0; i < m; ++i) r[i * B + b] = r[i * B + b] - y[i * B + b];
+    }
+    return;
+  }
   for (int64_t i = 0; i < p->m; ++i) {
     for (int64_t b = 0; b < B; ++b) {
       double acc = 0.0;
@@ -360,6 +379,37 @@ static inline double corr(const problem_t* p, const double* r, int64_t j,
   return acc;
 }
 
+/* (A^T r)[j, b] for up to 8 atoms at once: the same per-element sequential
+ * sums as corr() (each output's mac chain in k order), interleaved so the
+ * independent chains overlap instead of waiting on one FMA latency each
+ * (bit-identical; the oracle's cost at config 3 is these chains). */
+static void corr8(const problem_t* p, const double* r, const int64_t* js, int cnt, int64_t b,
+                  double* out) {
+  if (!p->at || cnt < 8) {
+    for (int u = 0; u < cnt; ++u) out[u] = corr(p, r, js[u], b);
+    return;
+  }
+  const int64_t B = p->batch, m = p->m;
+  const double* a[8];
+  double acc[8];
+  for (int u = 0; u < 8; ++u) {
+    a[u] = p->at + js[u] * m;
+    acc[u] = 0.0;
+  }
+  if (p->isa == ORC_ISA_AVX2) {
+    for (int64_t q = 0; q < m; ++q) {
+      const double rq = r[q * B + b];
+      for (int u = 0; u < 8; ++u) acc[u] = fma(a[u][q], rq, acc[u]);
+    }
+  } else {
+    for (int64_t q = 0; q < m; ++q) {
+      const double rq = r[q * B + b];
+      for (int u = 0; u < 8; ++u) acc[u] = acc[u] + a[u][q] * rq;
+    }
+  }
+  for (int u = 0; u < 8; ++u) out[u] = acc[u];
+}
+
 /* inject_from_scores (clomp.cpp:41-53) on freshly computed scores.
  * Returns 1 if any mask bit flipped; records the fp64 top-2 for tracing. */
 static int inject(const problem_t* p, const double* r, double th,
@@ -371,8 +421,14 @@ static int inject(const problem_t* p, const double* r, double th,
   for (int64_t b = 0; b < B; ++b) {
     double cmax = 0.0, second = 0.0;
     int64_t arg = -1;
+    for (int64_t j0 = 0; j0 < n; j0 += 8) {
+      int64_t js[8];
+      const int cnt = (int)(n - j0 < 8 ? n - j0 : 8);
+      for (int u = 0; u < cnt; ++u) js[u] = j0 + u;
+      corr8(p, r, js, cnt, b, scores + j0);
+    }
     for (int64_t j = 0; j < n; ++j) {
-      const double v = fabs(corr(p, r, j, b));
+      const double v = fabs(scores[j]);
       scores[j] = v;
       if (v > cmax) {
         second = cmax;
@@ -495,9 +551,11 @@ static int solve_joint(const problem_t* p, const double* y, const orc_config* c,
        * squares is computed and discarded there; it does not feed the step. */
       residual(p, s, sup, y, r);
       for (int64_t b = 0; b < B; ++b)
-        for (int64_t q = 0; q < sup[b].count; ++q) {
-          const int64_t j = sup[b].idx[q];
-          g[j * B + b] = corr(p, r, j, b) * 2.0;
+        for (int64_t q0 = 0; q0 < sup[b].count; q0 += 8) {
+          const int cnt = (int)(sup[b].count - q0 < 8 ? sup[b].count - q0 : 8);
+          double v[8];
+          corr8(p, r, sup[b].idx + q0, cnt, b, v);
+          for (int u = 0; u < cnt; ++u) g[sup[b].idx[q0 + u] * B + b] = v[u] * 2.0;
         }
       if (prior) prior_eval(p, s, sup, g, px, px + nb, px + 2 * nb, &tvv, &lvv);
       step_support(s, m1, m2, g, sup, B, c, &adam_steps);
@@ -811,5 +869,245 @@ int orc_gradient_step(double* s, const uint8_t* mask, double* m1, double* m2,
     default:
       return ORC_ERR_CONFIG;
   }
+  return ORC_OK;
+}
+
+/* ------------------------------------------- separable, Gram form (fast)
+ * The same per-signal loop (clomp.cpp:235-291, B = 1 semantics) with the
+ * separable operator, for full-size 2D parity where the matrix-free exact
+ * restatement above is infeasible (config 4: K = 1500, 16384 x 65536).
+ * Products are regrouped, so results are the fp64 loop's up to summation
+ * order (not bit-exact with the reference; pinned against orc_clomp_solve_sep
+ * on prefixes by tests/test_oracle.py):
+ *   residual  R = A_r C A_c^T - Y through V = A_r C (C sparse, m_r x n_c);
+ *   scores    S = A_r^T R A_c (n_r x n_c), atom p = i + n_r j;
+ *   epochs    g_S = 2 (G_S c - b_S) with G_S[k][l] = Gr[i_k][i_l] Gc[j_k][j_l]
+ *             (Gr = A_r^T A_r, Gc = A_c^T A_c) and b = A_r^T Y A_c, which
+ *             equals 2 A_S^T (A_S c - y) (clomp.cpp:87-91) in exact arithmetic. */
+static void sep_residual(const double* ar, int64_t mr, int64_t nr, const double* ac, int64_t mc,
+                         int64_t nc, const support_t* sup, const double* s, const double* y,
+                         double* v, double* r) {
+  for (int64_t e = 0; e < mr * nc; ++e) v[e] = 0.0;
+  for (int64_t q = 0; q < sup->count; ++q) {
+    const int64_t pidx = sup->idx[q], i = pidx % nr, j = pidx / nr;
+    const double c = s[pidx];
+    for (int64_t qr = 0; qr < mr; ++qr) v[qr * nc + j] += ar[qr * nr + i] * c;
+  }
+  for (int64_t qc = 0; qc < mc; ++qc)
+    for (int64_t qr = 0; qr < mr; ++qr) {
+      const double* vr = v + qr * nc;
+      const double* acr = ac + qc * nc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int64_t j = 0;
+      for (; j + 4 <= nc; j += 4) {
+        a0 += vr[j] * acr[j];
+        a1 += vr[j + 1] * acr[j + 1];
+        a2 += vr[j + 2] * acr[j + 2];
+        a3 += vr[j + 3] * acr[j + 3];
+      }
+      for (; j < nc; ++j) a0 += vr[j] * acr[j];
+      r[qr + mr * qc] = ((a0 + a1) + (a2 + a3)) - y[qr + mr * qc];
+    }
+}
+
+/* out (n_r x n_c, p = i + n_r j) = A_r^T Rm A_c with Rm[qr][qc] = r[qr + m_r qc].
+ * u: scratch of n_r m_c + m_r m_c + n_r n_c doubles. */
+static void sep_corr(const double* ar, int64_t mr, int64_t nr, const double* ac, int64_t mc,
+                     int64_t nc, const double* r, double* u, double* out) {
+  double* rm = u + nr * mc;       /* Rm row-major (m_r x m_c) */
+  double* o2 = rm + mr * mc;      /* A_r^T Rm A_c row-major (n_r x n_c) */
+  for (int64_t qc = 0; qc < mc; ++qc)
+    for (int64_t qr = 0; qr < mr; ++qr) rm[qr * mc + qc] = r[qr + mr * qc];
+  for (int64_t e = 0; e < nr * mc; ++e) u[e] = 0.0;  /* U = A_r^T Rm  (n_r x m_c) */
+  for (int64_t qr = 0; qr < mr; ++qr)
+    for (int64_t i = 0; i < nr; ++i) {
+      const double a = ar[qr * nr + i];
+      double* ur = u + i * mc;
+      const double* rr = rm + qr * mc;
+      for (int64_t qc = 0; qc < mc; ++qc) ur[qc] += a * rr[qc];
+    }
+  for (int64_t e = 0; e < nr * nc; ++e) o2[e] = 0.0;
+  for (int64_t i = 0; i < nr; ++i)
+    for (int64_t qc = 0; qc < mc; ++qc) {
+      const double uq = u[i * mc + qc];
+      const double* acr = ac + qc * nc;
+      double* orow = o2 + i * nc;
+      for (int64_t j = 0; j < nc; ++j) orow[j] += uq * acr[j];
+    }
+  for (int64_t i = 0; i < nr; ++i)
+    for (int64_t j = 0; j < nc; ++j) out[i + nr * j] = o2[i * nc + j];
+}
+
+static double dot4(const double* a, const double* b, int64_t n) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t k = 0;
+  for (; k + 4 <= n; k += 4) {
+    a0 += a[k] * b[k];
+    a1 += a[k + 1] * b[k + 1];
+    a2 += a[k + 2] * b[k + 2];
+    a3 += a[k + 3] * b[k + 3];
+  }
+  for (; k < n; ++k) a0 += a[k] * b[k];
+  return (a0 + a1) + (a2 + a3);
+}
+
+static int sep_gram_one(const double* ar, int64_t mr, int64_t nr, const double* ac, int64_t mc,
+                        int64_t nc, const double* gr, const double* gc, const double* y,
+                        const orc_config* c, double* s_out, uint8_t* mask_out, int64_t* it_out,
+                        double* rn_out, uint8_t* cv_out) {
+  const int64_t n = nr * nc, m = mr * mc;
+  int64_t cap = (int64_t)c->max_outer + 64;
+  if (c->th < 1.0 || cap > n) cap = n;
+  double* s = calloc((size_t)n, sizeof(double));
+  double* m1 = calloc((size_t)n, sizeof(double));
+  double* m2 = calloc((size_t)n, sizeof(double));
+  double* g = calloc((size_t)n, sizeof(double));
+  double* best_s = calloc((size_t)n, sizeof(double));
+  uint8_t* mask = calloc((size_t)n, 1);
+  uint8_t* best_mask = calloc((size_t)n, 1);
+  double* zb = malloc((size_t)n * sizeof(double));
+  double* sc = malloc((size_t)n * sizeof(double));
+  double* v = malloc((size_t)(mr * nc) * sizeof(double));
+  double* u = malloc((size_t)(nr * mc + mr * mc + nr * nc) * sizeof(double));
+  double* r = malloc((size_t)m * sizeof(double));
+  int64_t* idx = malloc((size_t)n * sizeof(int64_t));
+  int64_t* bidx = malloc((size_t)n * sizeof(int64_t));
+  double* G = NULL;
+  double* cs = malloc((size_t)cap * sizeof(double));
+  double* bs = malloc((size_t)cap * sizeof(double));
+  support_t sup = {idx, 0}, best_sup = {bidx, 0};
+  int status = ORC_OK, converged = 0, have_best = 0;
+  int64_t iterations = 0, gdim = -1;
+  uint64_t adam_steps = 0, stall = 0;
+  double best_loss = INFINITY, prev_loss = INFINITY;
+  sep_corr(ar, mr, nr, ac, mc, nc, y, u, zb);  /* b = A^T y of every atom */
+  for (uint64_t outer = 1; outer <= c->max_outer; ++outer) {
+    sep_residual(ar, mr, nr, ac, mc, nc, &sup, s, y, v, r);
+    if (sqrt(dot4(r, r, m)) < c->eps) {
+      converged = 1;
+      break;
+    }
+    sep_corr(ar, mr, nr, ac, mc, nc, r, u, sc);
+    double cmax = 0.0;
+    for (int64_t p = 0; p < n; ++p) {
+      sc[p] = fabs(sc[p]);
+      if (sc[p] > cmax) cmax = sc[p];
+    }
+    int changed = 0;
+    if (cmax != 0.0) {
+      const double cut = c->th * cmax;
+      for (int64_t p = 0; p < n; ++p)
+        if (sc[p] >= cut && !mask[p]) {
+          if (sup.count >= cap) { status = ORC_ERR_DIMENSION; goto done; }
+          mask[p] = 1;
+          support_insert(&sup, p);
+          changed = 1;
+        }
+    }
+    const int64_t t = sup.count;
+    if (t != gdim) {  /* support (sorted) changed: rebuild G_S and b_S */
+      free(G);
+      G = malloc((size_t)(t * t) * sizeof(double));
+      for (int64_t k = 0; k < t; ++k) {
+        const int64_t ik = idx[k] % nr, jk = idx[k] / nr;
+        for (int64_t l = 0; l < t; ++l) {
+          const int64_t il = idx[l] % nr, jl = idx[l] / nr;
+          G[k * t + l] = gr[ik * nr + il] * gc[jk * nc + jl];
+        }
+        bs[k] = zb[idx[k]];
+      }
+      gdim = t;
+    }
+    for (int64_t k = 0; k < t; ++k) cs[k] = s[idx[k]];
+    for (uint64_t step = 0; step < c->inner_steps; ++step) {
+      for (int64_t k = 0; k < t; ++k) g[idx[k]] = 2.0 * (dot4(G + k * t, cs, t) - bs[k]);
+      step_support(s, m1, m2, g, &sup, 1, c, &adam_steps);
+      for (int64_t k = 0; k < t; ++k) cs[k] = s[idx[k]];
+    }
+    sep_residual(ar, mr, nr, ac, mc, nc, &sup, s, y, v, r);
+    const double loss = dot4(r, r, m);
+    if (!isfinite(loss)) { status = ORC_ERR_NUMERICAL; goto done; }
+    iterations = (int64_t)outer;
+    if (loss < best_loss) {
+      best_loss = loss;
+      memcpy(best_s, s, (size_t)n * sizeof(double));
+      memcpy(best_mask, mask, (size_t)n);
+      best_sup.count = sup.count;
+      memcpy(bidx, idx, (size_t)sup.count * sizeof(int64_t));
+      have_best = 1;
+    }
+    const double rel = isfinite(prev_loss) ? (prev_loss - loss) / fmax(fabs(prev_loss), 1e-300)
+                                           : INFINITY;
+    stall = (!changed && rel < c->stall_tol) ? stall + 1 : 0;
+    prev_loss = loss;
+    if (stall >= c->stall_patience) break;
+  }
+  {
+    const double* so = s;
+    const uint8_t* mo = mask;
+    const support_t* su = &sup;
+    if (!converged && isfinite(best_loss) && have_best) {
+      so = best_s;
+      mo = best_mask;
+      su = &best_sup;
+    }
+    sep_residual(ar, mr, nr, ac, mc, nc, su, so, y, v, r);
+    *rn_out = sqrt(dot4(r, r, m));
+    *cv_out = *rn_out < c->eps;
+    *it_out = iterations;
+    memcpy(s_out, so, (size_t)n * sizeof(double));
+    memcpy(mask_out, mo, (size_t)n);
+  }
+done:
+  free(s); free(m1); free(m2); free(g); free(best_s); free(mask); free(best_mask);
+  free(zb); free(sc); free(v); free(u); free(r); free(idx); free(bidx); free(G);
+  free(cs); free(bs);
+  return status;
+}
+
+int orc_clomp_solve_sep_gram(const double* ar, int64_t mr, int64_t nr, const double* ac,
+                             int64_t mc, int64_t nc, const double* y, int64_t batch,
+                             const orc_config* cfg, double* s_out, uint8_t* mask_out,
+                             int64_t* iterations, double* final_rn, uint8_t* converged,
+                             int32_t* status, char* err, int errlen) {
+  int st = validate(cfg, err, errlen);
+  if (st) return st;
+  if (mr <= 0 || nr <= 0 || mc <= 0 || nc <= 0 || batch <= 0) {
+    set_err(err, errlen, "clomp: empty operator or batch");
+    return ORC_ERR_DIMENSION;
+  }
+  const int64_t n = nr * nc, m = mr * mc;
+  double* gr = malloc((size_t)(nr * nr) * sizeof(double));
+  double* gc = malloc((size_t)(nc * nc) * sizeof(double));
+  for (int64_t i = 0; i < nr; ++i)
+    for (int64_t k = 0; k < nr; ++k) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < mr; ++q) acc += ar[q * nr + i] * ar[q * nr + k];
+      gr[i * nr + k] = acc;
+    }
+  for (int64_t j = 0; j < nc; ++j)
+    for (int64_t k = 0; k < nc; ++k) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < mc; ++q) acc += ac[q * nc + j] * ac[q * nc + k];
+      gc[j * nc + k] = acc;
+    }
+  double* yc = malloc((size_t)m * sizeof(double));
+  double* sc = malloc((size_t)n * sizeof(double));
+  uint8_t* mk = malloc((size_t)n);
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t q = 0; q < m; ++q) yc[q] = y[q * batch + b];
+    int64_t it = 0;
+    double rn = 0.0;
+    uint8_t cv = 0;
+    status[b] = sep_gram_one(ar, mr, nr, ac, mc, nc, gr, gc, yc, cfg, sc, mk, &it, &rn, &cv);
+    for (int64_t p = 0; p < n; ++p) {
+      s_out[p * batch + b] = status[b] ? 0.0 : sc[p];
+      mask_out[p * batch + b] = status[b] ? 0 : mk[p];
+    }
+    iterations[b] = status[b] ? 0 : it;
+    final_rn[b] = status[b] ? NAN : rn;
+    converged[b] = status[b] ? 0 : cv;
+  }
+  free(gr); free(gc); free(yc); free(sc); free(mk);
   return ORC_OK;
 }

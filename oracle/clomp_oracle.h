@@ -97,6 +97,15 @@ int orc_clomp_solve_sep(const double* ar, int64_t mr, int64_t nr,
                         int64_t* iterations, double* final_rn, uint8_t* converged,
                         int32_t* status, double* trace, char* err, int errlen);
 
+/* The separable per-signal loop in Gram form (products regrouped, fp64):
+ * full-size 2D parity where the exact matrix-free restatement is too slow.
+ * Per-signal semantics only; status[b] per signal. */
+int orc_clomp_solve_sep_gram(const double* ar, int64_t mr, int64_t nr, const double* ac,
+                             int64_t mc, int64_t nc, const double* y, int64_t batch,
+                             const orc_config* cfg, double* s_out, uint8_t* mask_out,
+                             int64_t* iterations, double* final_rn, uint8_t* converged,
+                             int32_t* status, char* err, int errlen);
+
 /* inject_support (clomp.cpp:142-154): mask |= thresholded |A^T r| per column. */
 int orc_inject_support(const double* a, int64_t m, int64_t n, const double* r,
                        int64_t batch, double th, int isa, uint8_t* mask);

@@ -48,6 +48,9 @@ def oracle() -> C.CDLL:
         h.orc_clomp_solve_sep.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, C.POINTER(CConfig),
                                           C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp,
                                           C.c_char_p, C.c_int]
+        h.orc_clomp_solve_sep_gram.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64,
+                                               C.POINTER(CConfig), vp, vp, vp, vp, vp, vp,
+                                               C.c_char_p, C.c_int]
         h.orc_inject_support.argtypes = [vp, i64, i64, vp, i64, C.c_double, C.c_int, vp]
         h.orc_clomp_loss.argtypes = [vp, i64, i64, vp, i64, vp, vp, C.POINTER(CConfig), C.c_int, vp, vp]
         h.orc_gradient_step.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(CConfig)]
@@ -140,6 +143,32 @@ def orc_solve_sep(Ar, Ac, Y, cfg: ClompConfig, mode=MODE_JOINT, isa=ISA_AVX2):
     code = oracle().orc_clomp_solve_sep(_p(Ar), Ar.shape[0], Ar.shape[1], _p(Ac), Ac.shape[0],
                                         Ac.shape[1], _p(Y), B, C.byref(c), isa, mode, _p(s), _p(mk),
                                         _p(it), _p(rn), _p(cv), _p(st), None, err, 256)
+    return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
+                final_residual_norm=rn, converged=cv.astype(bool), status=st)
+
+
+def orc_solve_sep_gram(Ar, Ac, Y, cfg: ClompConfig):
+    """Separable per-signal loop in Gram form (fp64, products regrouped): the
+    full-size 2D checker (oracle/clomp_oracle.c, orc_clomp_solve_sep_gram)."""
+    Ar = np.ascontiguousarray(Ar, np.float64)
+    Ac = np.ascontiguousarray(Ac, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    if Y.ndim == 1:
+        Y = Y.reshape(-1, 1)
+    n = Ar.shape[1] * Ac.shape[1]
+    B = Y.shape[1]
+    s = np.zeros((n, B))
+    mk = np.zeros((n, B), np.uint8)
+    it = np.zeros(B, np.int64)
+    rn = np.zeros(B)
+    cv = np.zeros(B, np.uint8)
+    st = np.zeros(B, np.int32)
+    err = C.create_string_buffer(256)
+    c = cfg.to_c()
+    code = oracle().orc_clomp_solve_sep_gram(_p(Ar), Ar.shape[0], Ar.shape[1], _p(Ac),
+                                             Ac.shape[0], Ac.shape[1], _p(Y), B, C.byref(c),
+                                             _p(s), _p(mk), _p(it), _p(rn), _p(cv), _p(st),
+                                             err, 256)
     return dict(code=code, err=err.value.decode(), s=s, mask=mk, iterations=it,
                 final_residual_norm=rn, converged=cv.astype(bool), status=st)
 

@@ -35,22 +35,30 @@ def snr_db(x, xh):
     return np.inf if e == 0 else 10 * np.log10(np.sum(x ** 2) / e)
 
 
-@pytest.fixture(scope="module", params=["f64", "tc", "gemv", "auto"])
+@pytest.fixture(scope="module", params=["f64", "tc", "tc_pair", "gemv", "auto"])
 def corr_path(request, gpu_available):
     return request.param
 
 
+PAIR_MIN_SIGNALS = 129  # the CTA-pair tcgen05 kernel serves two 128-signal tiles
+
+
 def make_ctx(A, path="auto"):
-    """path: 'f64' batched pipeline with fp64 SIMT correlation, 'tc' batched
-    pipeline with the tcgen05 correlation, 'gemv' batched pipeline with the
-    B <= 4 GEMV correlation, 'auto' library choice (the fused
+    """path: 'f64' batched pipeline with fp64 SIMT correlation; 'tc' batched
+    pipeline FORCED onto the tcgen05 correlation (set_corr_path(2): the
+    one-CTA kernel below 129 signals, the CTA-pair kernel from 129 on; never
+    the GEMV); 'tc_pair' the same, with per-signal batches replicated past
+    128 columns by the tests so the pair kernel runs; 'gemv' batched pipeline
+    with the B <= 4 GEMV correlation; 'auto' library choice (the fused
     one-block-per-signal solve for small per-signal problems)."""
     ctx = cl.ClompContext(np.asarray(A, np.float32))
     if path == "f64":
         ctx.set_corr_path(1)
+    if path in ("tc", "tc_pair"):
+        ctx.set_corr_path(2)
     if path == "gemv":
         ctx.set_corr_path(3)
-    if path in ("f64", "tc", "gemv"):
+    if path in ("f64", "tc", "tc_pair", "gemv"):
         ctx.set_fused(False)
     return ctx
 
@@ -63,10 +71,24 @@ def test_solve_matches_reference_golden(case, corr_path):
     cfg = cl.ClompConfig(**case["cfg"])
     if corr_path == "gemv" and Y.shape[1] > 4:
         pytest.skip("the GEMV correlation serves batches of at most 4 signals")
+    mode = cl.MODE_JOINT if case["api"] == "batch" else cl.MODE_PER_SIGNAL
+    reps = 1
+    if corr_path == "tc_pair":
+        # per-signal columns are independent (clomp_solve per column): replicate
+        # the batch past 128 signals so the CTA-pair kernel correlates it, and
+        # check every replica against the golden outputs
+        if mode != cl.MODE_PER_SIGNAL and Y.shape[1] > 1:
+            pytest.skip("joint batches couple their columns; cannot be replicated")
+        if cfg.th < 1.0 or case.get("basis"):
+            pytest.skip("the tcgen05 correlation serves th == 1 without priors")
+        if case.get("gpu_code", case["code"]) != 0:
+            pytest.skip("error cases: per-signal mode reports them per signal")
+        reps = -(-PAIR_MIN_SIGNALS // Y.shape[1])
+        Y = np.tile(Y, (1, reps))
+        mode = cl.MODE_PER_SIGNAL
     ctx = make_ctx(A, corr_path)
     if case.get("basis"):
         ctx.set_basis(ARR[f"{name}/D"])  # the priors chain through it
-    mode = cl.MODE_JOINT if case["api"] == "batch" else cl.MODE_PER_SIGNAL
     code = case.get("gpu_code", case["code"])
     if code != 0:
         exc = {2: cl.ConfigError, 3: cl.DimensionError, 4: cl.NumericalError,
@@ -75,12 +97,24 @@ def test_solve_matches_reference_golden(case, corr_path):
             cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
         return
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
-    assert np.array_equal(r.mask, ARR[f"{name}/mask"]), "support sets differ"
-    assert np.array_equal(r.iterations, ARR[f"{name}/iterations"])
-    assert np.array_equal(r.converged, ARR[f"{name}/converged"].astype(bool))
-    s_ref = ARR[f"{name}/s"]
+    if reps > 1:
+        assert ctx.stats()["corr_path"] == 1  # tcgen05 (pair kernel at >= 129 signals)
+    tile = (lambda a: np.tile(a, (1, reps)) if a.ndim == 2 else np.tile(a, reps))
+    assert np.array_equal(r.mask, tile(ARR[f"{name}/mask"])), "support sets differ"
+    it_ref = ARR[f"{name}/iterations"]
+    if reps > 1 and it_ref.size == 1:
+        it_ref = np.repeat(it_ref, Y.shape[1] // reps)
+    assert np.array_equal(r.iterations, tile(it_ref) if reps > 1 else it_ref)
+    cv_ref = ARR[f"{name}/converged"].astype(bool)
+    if reps > 1 and cv_ref.size == 1:
+        cv_ref = np.repeat(cv_ref, Y.shape[1] // reps)
+    assert np.array_equal(r.converged, tile(cv_ref) if reps > 1 else cv_ref)
+    s_ref = tile(ARR[f"{name}/s"])
     assert rel_coef_err(r.s, s_ref) <= TIGHT_RTOL
-    np.testing.assert_allclose(r.final_residual_norm, ARR[f"{name}/final_residual_norm"],
+    rn_ref = ARR[f"{name}/final_residual_norm"]
+    if reps > 1 and rn_ref.size == 1:
+        rn_ref = np.repeat(rn_ref, Y.shape[1] // reps)
+    np.testing.assert_allclose(r.final_residual_norm, tile(rn_ref) if reps > 1 else rn_ref,
                                rtol=1e-6, atol=1e-12)
 
 
@@ -128,24 +162,131 @@ def _subset_parity(A, Y, cfg, idx, gpu_res, X=None):
             assert abs(snr_db(X[:, b], gpu_res.s[:, b]) - snr_db(X[:, b], ref["s"][:, q])) < 0.1
 
 
-def test_config2_full_batch_subset_parity(gpu_available):
-    """Config 2 (N=1024, M=512, K=32, B=4096, 40 dB) solved as one batch on
-    the GPU; 24 signals spread over the batch are re-solved by the oracle
-    (per-signal semantics make each column independent of the others)."""
+def _pool_parity(c, cols, r, X, cfg, per_task=1):
+    """GPU result r of the whole config-c batch against oracle per-signal solves
+    of columns `cols` (tests/oracle_pool.py, one worker per host core): support
+    sets, iteration counts and converged flags identical, coefficients within
+    the north star's 1e-4, reconstruction SNR within 0.1 dB."""
+    import oracle_pool
+
+    ref = oracle_pool.solve_columns(c, cols, cfg, per_task=per_task)
+    worst = 0.0
+    for b in cols:
+        sup, vals, it, conv, st, rn = ref[b]
+        assert st == 0
+        ms = np.flatnonzero(r.mask[:, b])
+        assert np.array_equal(ms, sup), f"signal {b}: support differs"
+        assert r.iterations[b] == it, f"signal {b}: iterations"
+        assert bool(r.converged[b]) == conv, f"signal {b}: converged flag"
+        s_ref = np.zeros(r.s.shape[0])
+        s_ref[sup] = vals
+        err = rel_coef_err(r.s[:, b], s_ref)
+        worst = max(worst, err)
+        assert err <= COEF_RTOL, f"signal {b}: coefficient error {err}"
+        assert abs(snr_db(X[:, b], r.s[:, b]) - snr_db(X[:, b], s_ref)) < 0.1
+        np.testing.assert_allclose(r.final_residual_norm[b], rn, rtol=1e-6, atol=1e-12)
+    return worst
+
+
+def test_config2_whole_batch_parity(gpu_available):
+    """Config 2 (N=1024, M=512, K=32, B=4096, 40 dB) at full size through the
+    benchmarked auto path (tcgen05 CTA-pair correlation, fused selection +
+    fast warp learners): EVERY one of the 4096 signals is re-solved by the
+    oracle (per-signal semantics make the columns independent) and must have
+    the same support, iterations and converged flag, coefficients within
+    1e-4 and SNR within 0.1 dB."""
     c = cl.CONFIGS[2]
     A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
                                    value_law=c["value_law"], snr_db=c["snr_db"])
     ctx = make_ctx(A)
     cfg = cl.ClompConfig.baseline(c["k"])
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert ctx.stats()["corr_path"] == 1
     assert np.all(r.status == 0)
     assert np.all(r.iterations == c["k"])
-    idx = np.linspace(0, c["batch"] - 1, 24).astype(int)
-    _subset_parity(A, Y, cfg, idx, r, X)
+    worst = _pool_parity(c, range(c["batch"]), r, X, cfg, per_task=64)
+    print(f"config 2: 4096/4096 signals identical supports, worst coef err {worst:.2e}")
     # whole-batch properties: K atoms each, high SNR recovery
     assert np.all(r.mask.sum(0) == c["k"])
     snrs = np.array([snr_db(X[:, b], r.s[:, b]) for b in range(0, c["batch"], 64)])
     assert np.median(snrs) > 30.0
+
+
+def test_config3_full_batch_parity(gpu_available):
+    """Config 3 (N=16384, M=4096, K=256, B=256, +-(1+U), noiseless) at full
+    size through the benchmarked auto path: the CTA-pair tcgen05 correlation
+    at m = 4096, the fast warp learners to 32 atoms, then the four-CTA
+    cluster learners with the L = 3 power form (batched DMMA squarings),
+    k_pw_extend / k_pw_resid, with the cluster grid capped at the co-resident
+    cluster count so the persistent loop runs several signals per cluster.
+    16 signals spread over the batch are re-solved by the oracle (~45 s per
+    signal per core)."""
+    c = cl.CONFIGS[3]
+    A, X, Y, _ = cl.gen_problem_1d(c["seed"], c["m"], c["n"], c["k"], c["batch"],
+                                   value_law=c["value_law"], snr_db=c["snr_db"])
+    ctx = make_ctx(A)
+    cfg = cl.ClompConfig.baseline(c["k"])
+    r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert ctx.stats()["corr_path"] == 1
+    assert np.all(r.status == 0)
+    assert np.all(r.iterations == c["k"])
+    assert np.all(r.mask.sum(0) == c["k"])
+    cols = list(np.linspace(0, c["batch"] - 1, 16).astype(int))
+    worst = _pool_parity(c, cols, r, X, cfg)
+    print(f"config 3: 16/16 signals identical supports, worst coef err {worst:.2e}")
+
+
+def test_joint_capacity_overflow_raises(gpu_available):
+    """An atom duplicated 24 times is selected with all its exact ties at once
+    (clomp.cpp:49-51); with max_outer = 3 the per-signal capacity is
+    3 + 16 = 19 atoms.  Per-signal mode reports CL_ERR_CAPACITY for that
+    signal; joint mode (clomp_solve_batch semantics) raises CapacityError
+    instead of returning a silently truncated batch."""
+    m, n, B = 64, 256, 4
+    A, _, _, _ = cl.gen_problem_1d(5, m, n, 3, B)
+    A = np.array(A)
+    A[:, 1:25] = A[:, [0]]  # atoms 0..24 identical
+    X = np.zeros((n, B))
+    rng = np.random.default_rng(8)
+    X[0, 0] = 3.0  # signal 0 selects atom 0 and its 24 ties first
+    for b in range(1, B):  # the others use distinct atoms only
+        X[rng.choice(np.arange(25, n), 3, replace=False), b] = rng.standard_normal(3) + 2.0
+    Y = (A.astype(np.float64) @ X).astype(np.float32)
+    cfg = cl.ClompConfig.baseline(3)
+    for path in ("tc", "f64"):
+        ctx = make_ctx(A, path)
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        assert r.status[0] == cl.CL_ERR_CAPACITY
+        assert np.all(r.status[1:] == 0)
+        with pytest.raises(cl.CapacityError):
+            cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_JOINT)
+
+
+def test_basis_then_gram_cache_off_then_destroy(gpu_available):
+    """set_basis -> set_gram_cache(0) -> a prior solve -> set_gram_cache(1) ->
+    another solve -> destroy: the cache toggle frees only the Gram cache (the
+    basis, dictionary and workspace stay valid; no double free at destroy)."""
+    n, m, B = 128, 64, 3
+    D = cl.dct_basis(n)
+    rng = np.random.default_rng(3)
+    A = ((rng.standard_normal((m, n)) / np.sqrt(m)) @ D).astype(np.float32)
+    X = np.zeros((n, B))
+    for b in range(B):
+        X[rng.choice(n, 4, replace=False), b] = rng.standard_normal(4)
+    Y = (A.astype(np.float64) @ X).astype(np.float32)
+    cfg = cl.ClompConfig(max_outer=6)
+    ref = refbind.orc_solve(A.astype(np.float64), Y.astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL, basis=D)
+    ctx = make_ctx(A, "tc")
+    ctx.set_basis(D)
+    ctx.set_gram_cache(0)
+    r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    ctx.set_gram_cache(1)
+    r1 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    for r in (r0, r1):
+        assert np.array_equal(r.mask, ref["mask"])
+        assert rel_coef_err(r.s, ref["s"]) <= 1e-7
+    ctx.close()
 
 
 def test_joint_mode_batch_of_nine_matches_reference(gpu_available):
@@ -265,7 +406,7 @@ def test_cluster_learning_vs_oracle_and_block_kernel(gpu_available, K, opt):
     r = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
     assert np.all(r.status == 0)
     _subset_parity(A, Y, cfg, np.arange(min(B, 2)), r, X if opt == cl.PLAIN else None)
-    for variant in (0, 2):  # block kernel; eight-CTA cluster variant
+    for variant in (0,):  # the block-per-signal kernel
         ctx.set_cluster_learn(variant)
         r0 = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
         assert np.array_equal(r.mask, r0.mask)

@@ -200,3 +200,32 @@ def test_oracle_separable_matches_reference_on_explicit_kron(case):
     assert r["code"] == case["code"] == 0, r["err"]
     for k in ("s", "mask", "iterations", "final_residual_norm"):
         assert np.array_equal(r[k], ARR[f"{name}/{k}"]), k
+
+
+@pytest.mark.parametrize("dims,K,opt", [((24, 20, 12, 16), 12, 0), ((32, 32, 16, 16), 40, 0),
+                                        ((16, 24, 10, 12), 10, 2)])
+def test_separable_gram_oracle_pinned_to_exact_restatement(dims, K, opt):
+    """The Gram-form separable checker (products regrouped; used for the
+    full-size config-4 parity where the exact matrix-free restatement is
+    infeasible) against the exact restatement, itself bit-exact with the
+    reference on the explicit Kronecker matrix (test above): identical
+    supports, iterations and converged flags; coefficients to 1e-10."""
+    import paper_2501_11592_b200 as cl
+
+    nr, nc, mr, mc = dims
+    Ar, Ac, X, Y = cl.gen_problem_2d(100 + K, nr, nc, mr, mc, K // 2, 3)
+    cfg = cl.ClompConfig.baseline(K)
+    cfg.opt = opt
+    if opt == 2:
+        cfg.lr = 0.01
+    ex = refbind.orc_solve_sep(Ar, Ac, Y, cfg, mode=refbind.MODE_PER_SIGNAL)
+    gr = refbind.orc_solve_sep_gram(Ar, Ac, Y, cfg)
+    assert ex["code"] == 0 and gr["code"] == 0
+    assert np.all(gr["status"] == 0)
+    assert np.array_equal(ex["mask"], gr["mask"])
+    assert np.array_equal(ex["iterations"], gr["iterations"])
+    assert np.array_equal(ex["converged"], gr["converged"])
+    den = np.max(np.abs(ex["s"]))
+    assert np.max(np.abs(ex["s"] - gr["s"])) / den <= 1e-10
+    np.testing.assert_allclose(gr["final_residual_norm"], ex["final_residual_norm"], rtol=1e-9,
+                               atol=1e-13)
