@@ -156,6 +156,22 @@ const char* cl_last_error(const cl_ctx* ctx);
 int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
                    const cl_config* cfg, int mode, cl_result* out);
 
+/* Pipelined form of cl_solve_batch for streams of batches (throughput):
+ * cl_submit validates, starts the host->device copy of y on a copy stream and
+ * queues the whole solve and the device->host copy of its compact results
+ * behind it; cl_wait blocks until the OLDEST submitted batch's results are in
+ * host memory and expands them into `out` exactly as cl_solve_batch does.  Up
+ * to two batches may be in flight per context, so batch i + 1's upload and
+ * batch i's download overlap the other's solve (cl_solve_batch = cl_submit +
+ * cl_wait).  y must stay valid until the matching cl_wait returns when it is
+ * page-locked (it is read by the DMA engine); a pageable y is copied to the
+ * context's pinned staging before cl_submit returns.  Errors of the call
+ * itself (config, dimensions, allocation) are returned by cl_submit and leave
+ * nothing in flight; solve results and JOINT-mode failures by cl_wait. */
+int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
+              const cl_config* cfg, int mode);
+int cl_wait(cl_ctx* ctx, cl_result* out);
+
 /* Device-resident variant for throughput: d_y is a device pointer, signal-major
  * B x m fp32 (leading dimension m).  Results are written to device buffers
  * (any may be NULL): support/coef [B][cap], count/iterations(int32)/

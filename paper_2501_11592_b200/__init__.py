@@ -125,7 +125,7 @@ class CStats(C.Structure):
 # Every symbol include/clomp_b200.h declares (tests check the .so exports them).
 EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
-    "cl_solve_batch", "cl_solve_batch_device", "cl_synchronize",
+    "cl_solve_batch", "cl_submit", "cl_wait", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
     "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
@@ -152,6 +152,8 @@ def lib() -> C.CDLL:
         h.cl_last_error.restype = C.c_char_p
         h.cl_last_error.argtypes = [vp]
         h.cl_solve_batch.argtypes = [vp, vp, i64, i32, C.POINTER(CConfig), i32, C.POINTER(CResult)]
+        h.cl_submit.argtypes = [vp, vp, i64, i32, C.POINTER(CConfig), i32]
+        h.cl_wait.argtypes = [vp, C.POINTER(CResult)]
         h.cl_solve_batch_device.argtypes = [vp, vp, i64, C.POINTER(CConfig), i32, C.POINTER(CDeviceResult)]
         h.cl_synchronize.argtypes = [vp]
         h.cl_inject_support.argtypes = [vp, vp, i64, C.c_double, vp]
@@ -302,6 +304,14 @@ class ClompContext:
     def handle(self):
         return self._h
 
+    @property
+    def _pending(self) -> list:
+        # result buffers of batches submitted with clomp_submit (oldest first)
+        p = self.__dict__.get("_pend_list")
+        if p is None:
+            p = self.__dict__["_pend_list"] = []
+        return p
+
     def close(self):
         if getattr(self, "_h", None):
             lib().cl_destroy(self._h)
@@ -376,6 +386,77 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _prep_y(ctx: ClompContext, y_cols, layout: str):
+    y = np.ascontiguousarray(y_cols, dtype=np.float32)
+    if y.ndim == 1:
+        y = y.reshape(-1, 1) if layout == "ref" else y.reshape(1, -1)
+    if layout == "ref":
+        if y.shape[0] != ctx.m:
+            raise DimensionError(f"clomp: y rows {y.shape[0]} vs m={ctx.m}")
+        return y, y.shape[1], LAYOUT_REF
+    if y.shape[1] != ctx.m:
+        raise DimensionError(f"clomp: y cols {y.shape[1]} vs m={ctx.m}")
+    return y, y.shape[0], LAYOUT_T
+
+
+class _Pending:
+    """Result buffers of one submitted batch (filled by cl_wait)."""
+
+    def __init__(self, ctx: ClompContext, y, B: int, cfg: ClompConfig, dense: bool):
+        n = ctx.n
+        cap = max(1, n if cfg.th < 1.0 else min(n, max(1, int(cfg.max_outer)) + 16))
+        self.y, self.B, self.cap, self.dense = y, B, cap, dense  # y kept alive for the DMA
+        # uninitialised: cl_wait writes every entry of the compact rows (zeros
+        # past each count), which saves zeroing ~2 MB per config-2 call
+        self.sup = np.empty((max(B, 1), cap), np.int32)
+        self.coef = np.empty((max(B, 1), cap), np.float64)
+        if B == 0:
+            self.sup.fill(0)
+            self.coef.fill(0.0)
+        self.cnt = np.zeros(max(B, 1), np.int32)
+        self.s = np.zeros((n, max(B, 1)), np.float64) if dense else None
+        self.mask = np.zeros((n, max(B, 1)), np.uint8) if dense else None
+        self.it = np.zeros(max(B, 1), np.int64)
+        self.rn = np.zeros(max(B, 1), np.float64)
+        self.cv = np.zeros(max(B, 1), np.uint8)
+        self.st = np.zeros(max(B, 1), np.int32)
+        self.res = CResult(cap, _ptr(self.sup), _ptr(self.coef), _ptr(self.cnt), _ptr(self.s),
+                           _ptr(self.mask), _ptr(self.it), _ptr(self.rn), _ptr(self.cv),
+                           _ptr(self.st))
+
+    def result(self) -> BatchSolveResult:
+        B, cap, dense = self.B, self.cap, self.dense
+        counts = np.minimum(self.cnt[:B], cap)
+        return BatchSolveResult(self.s[:, :B] if dense else None,
+                                self.mask[:, :B] if dense else None, self.it[:B], self.rn[:B],
+                                self.cv[:B].astype(bool), self.st[:B], Ragged(self.sup, counts),
+                                Ragged(self.coef, counts))
+
+
+def clomp_submit(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
+                 mode: int = MODE_JOINT, layout: str = "ref", dense: bool = True) -> None:
+    """First half of a pipelined clomp_solve_batch (cl_submit): starts the
+    upload of y and queues the solve and the download of its results; returns
+    at once.  Up to two batches may be in flight per context; clomp_wait
+    returns them in submission order.  Streams of batches overlap batch i + 1's
+    upload and batch i's download with the other's solve."""
+    cfg = cfg or ClompConfig()
+    y, B, lay = _prep_y(ctx, y_cols, layout)
+    pend = _Pending(ctx, y, B, cfg, dense)
+    c = cfg.to_c()
+    _raise(lib().cl_submit(ctx.handle, _ptr(y), B, lay, C.byref(c), int(mode)), ctx.handle)
+    ctx._pending.append(pend)
+
+
+def clomp_wait(ctx: ClompContext) -> BatchSolveResult:
+    """Second half (cl_wait): the oldest submitted batch's result."""
+    if not ctx._pending:
+        raise ConfigError("clomp_wait: nothing in flight")
+    pend = ctx._pending.pop(0)
+    _raise(lib().cl_wait(ctx.handle, C.byref(pend.res)), ctx.handle)
+    return pend.result()
+
+
 def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
                       mode: int = MODE_JOINT, layout: str = "ref",
                       dense: bool = True) -> BatchSolveResult:
@@ -386,45 +467,13 @@ def clomp_solve_batch(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,
     in page-locked memory (e.g. a pinned torch tensor's numpy view) is copied
     to the GPU directly, pageable y through the context's pinned staging."""
     cfg = cfg or ClompConfig()
-    y = np.ascontiguousarray(y_cols, dtype=np.float32)
-    if y.ndim == 1:
-        y = y.reshape(-1, 1) if layout == "ref" else y.reshape(1, -1)
-    if layout == "ref":
-        if y.shape[0] != ctx.m:
-            raise DimensionError(f"clomp: y rows {y.shape[0]} vs m={ctx.m}")
-        B = y.shape[1]
-        lay = LAYOUT_REF
-    else:
-        if y.shape[1] != ctx.m:
-            raise DimensionError(f"clomp: y cols {y.shape[1]} vs m={ctx.m}")
-        B = y.shape[0]
-        lay = LAYOUT_T
-    n = ctx.n
-    cap = max(1, n if cfg.th < 1.0 else min(n, max(1, int(cfg.max_outer)) + 16))
-    # uninitialised: cl_solve_batch writes every entry of the compact rows
-    # (zeros past each count), which saves zeroing ~2 MB per config-2 call
-    sup = np.empty((max(B, 1), cap), np.int32)
-    coef = np.empty((max(B, 1), cap), np.float64)
-    if B == 0:
-        sup.fill(0)
-        coef.fill(0.0)
-    cnt = np.zeros(max(B, 1), np.int32)
-    s = np.zeros((n, max(B, 1)), np.float64) if dense else None
-    mask = np.zeros((n, max(B, 1)), np.uint8) if dense else None
-    it = np.zeros(max(B, 1), np.int64)
-    rn = np.zeros(max(B, 1), np.float64)
-    cv = np.zeros(max(B, 1), np.uint8)
-    st = np.zeros(max(B, 1), np.int32)
-    res = CResult(cap, _ptr(sup), _ptr(coef), _ptr(cnt), _ptr(s), _ptr(mask),
-                  _ptr(it), _ptr(rn), _ptr(cv), _ptr(st))
+    y, B, lay = _prep_y(ctx, y_cols, layout)
+    pend = _Pending(ctx, y, B, cfg, dense)
     c = cfg.to_c()
-    code = lib().cl_solve_batch(ctx.handle, _ptr(y), B, lay, C.byref(c), int(mode), C.byref(res))
+    code = lib().cl_solve_batch(ctx.handle, _ptr(y), B, lay, C.byref(c), int(mode),
+                                C.byref(pend.res))
     _raise(code, ctx.handle)
-    counts = np.minimum(cnt[:B], cap)
-    supports = Ragged(sup, counts)
-    coefs = Ragged(coef, counts)
-    return BatchSolveResult(s[:, :B] if dense else None, mask[:, :B] if dense else None,
-                            it[:B], rn[:B], cv[:B].astype(bool), st[:B], supports, coefs)
+    return pend.result()
 
 
 def clomp_solve(ctx: ClompContext, y, cfg: ClompConfig | None = None) -> SolveResult:

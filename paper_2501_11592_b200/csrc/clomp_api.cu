@@ -109,12 +109,26 @@ struct cl_ctx {
   // Adam bias-correction tables
   double* bc = nullptr;
   size_t bc_len = 0;
-  // host-call staging
-  void* stage = nullptr;
-  size_t stage_bytes = 0;
+  // host-call staging: two slots, so cl_submit of batch i + 1 can copy its y
+  // in while batch i solves and batch i's results copy out while i + 1 solves
+  struct Slot {
+    char* d_stage = nullptr;   // device: y, then the compact results
+    size_t d_bytes = 0;
+    char* h_io = nullptr;      // pinned host: compact results (+ a pageable y staged)
+    size_t h_bytes = 0;
+    cudaEvent_t ev_in = nullptr, ev_solve = nullptr, ev_out = nullptr;
+    bool busy = false;
+    int64_t batch = 0, cap = 0;
+    size_t ybytes = 0, out_bytes = 0;
+    int mode = 0;
+    bool fused = false;
+    std::chrono::steady_clock::time_point t_start;
+  };
+  Slot slot[2];
+  int slot_head = 0;     // next slot cl_submit fills
+  int slot_inflight = 0; // submitted and not yet waited (0..2)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
   int32_t* h_counters = nullptr;  // pinned
-  char* h_io = nullptr;           // pinned host staging (pageable y in, results out)
-  size_t h_io_bytes = 0;
   int32_t* h_chunk = nullptr;     // pinned, 2 x kNumCounters (graph chunks)
   cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
   GraphKey gkey;
@@ -438,6 +452,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
   if (image) {  // local-variance window tables -> device
+    // (a batch submitted earlier may still read the tables: cl_submit pipelining)
+    CL_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     const size_t cnt = ctx->lv_rows.size() + ctx->lv_cols.size() + ctx->lv_rowcov.size() +
                        ctx->lv_colcov.size();
     if (cnt * 4 > ctx->lv_tab_bytes) {
@@ -852,15 +868,46 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   return CL_OK;
 }
 
-void* stage_bytes(cl_ctx* ctx, size_t bytes) {
-  if (bytes > ctx->stage_bytes) {
-    if (ctx->stage) cudaFree(ctx->stage);
-    ctx->stage = nullptr;
-    ctx->stage_bytes = 0;
-    if (cudaMalloc(&ctx->stage, bytes) != cudaSuccess) return nullptr;
-    ctx->stage_bytes = bytes;
+char* slot_device(cl_ctx* ctx, cl_ctx::Slot& sl, size_t bytes) {
+  if (bytes > sl.d_bytes) {
+    if (sl.d_stage) {
+      cudaStreamSynchronize(ctx->stream);  // the previous solve may still read it
+      cudaFree(sl.d_stage);
+    }
+    sl.d_stage = nullptr;
+    sl.d_bytes = 0;
+    if (cudaMalloc(&sl.d_stage, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    sl.d_bytes = bytes;
   }
-  return ctx->stage;
+  return sl.d_stage;
+}
+
+char* slot_host(cl_ctx::Slot& sl, size_t bytes) {
+  if (bytes > sl.h_bytes) {
+    if (sl.h_io) cudaFreeHost(sl.h_io);
+    sl.h_io = nullptr;
+    sl.h_bytes = 0;
+    if (cudaMallocHost(&sl.h_io, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    sl.h_bytes = bytes;
+  }
+  return sl.h_io;
+}
+
+bool slot_events(cl_ctx* ctx, cl_ctx::Slot& sl) {
+  if (!ctx->copy_in &&
+      (cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking) != cudaSuccess))
+    return false;
+  if (sl.ev_in) return true;
+  return cudaEventCreateWithFlags(&sl.ev_in, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&sl.ev_solve, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&sl.ev_out, cudaEventDisableTiming) == cudaSuccess;
 }
 
 }  // namespace
@@ -1109,6 +1156,8 @@ void cl_destroy(cl_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_in) cudaStreamSynchronize(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamSynchronize(ctx->copy_out);
   cudaFree(ctx->at32);
   cudaFree(ctx->at_hi);
   cudaFree(ctx->at_lo);
@@ -1125,9 +1174,15 @@ void cl_destroy(cl_ctx* ctx) {
   cudaFree(ctx->wbuf);
   cudaFree(ctx->pw_buf);
   cudaFree(ctx->bc);
-  cudaFree(ctx->stage);
+  for (auto& sl : ctx->slot) {
+    cudaFree(sl.d_stage);
+    if (sl.h_io) cudaFreeHost(sl.h_io);
+    for (cudaEvent_t e : {sl.ev_in, sl.ev_solve, sl.ev_out})
+      if (e) cudaEventDestroy(e);
+  }
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
-  if (ctx->h_io) cudaFreeHost(ctx->h_io);
   if (ctx->h_chunk) cudaFreeHost(ctx->h_chunk);
   if (ctx->comm) nccl_comm_destroy(ctx->comm);
   for (auto& e : ctx->chunk_ev)
@@ -1388,20 +1443,6 @@ static int check_call(cl_ctx* ctx, int64_t batch, const cl_config* cfg, int mode
   return CL_OK;
 }
 
-static char* host_io(cl_ctx* ctx, size_t bytes) {
-  if (bytes > ctx->h_io_bytes) {
-    if (ctx->h_io) cudaFreeHost(ctx->h_io);
-    ctx->h_io = nullptr;
-    ctx->h_io_bytes = 0;
-    if (cudaMallocHost(&ctx->h_io, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
-    }
-    ctx->h_io_bytes = bytes;
-  }
-  return ctx->h_io;
-}
-
 static bool is_pinned(const void* p) {
   cudaPointerAttributes at{};
   const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess;
@@ -1409,13 +1450,22 @@ static bool is_pinned(const void* p) {
   return ok && at.type == cudaMemoryTypeHost;
 }
 
-int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
-                   const cl_config* cfg, int mode, cl_result* out) {
+// Pipelined host-buffer solve, first half: validate, copy y to the device on
+// the copy-in stream (it overlaps the previous batch still solving), enqueue
+// the whole solve on the context stream behind that copy, and the copy of the
+// compact results to pinned host memory on the copy-out stream behind the
+// solve.  Returns with everything queued (the host only waited for graph
+// chunks one behind, see solve_core).
+int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
+              const cl_config* cfg, int mode) {
   if (!ctx) return CL_ERR_INTERNAL;
   if (!y && batch > 0) return fail(ctx, CL_ERR_DIMENSION, "clomp: null y");
-  const auto t_start = std::chrono::steady_clock::now();
+  if (ctx->slot_inflight >= 2)
+    return fail(ctx, CL_ERR_CONFIG, "cl_submit: two batches already in flight; call cl_wait");
   cudaSetDevice(ctx->device);
-  const int64_t m = ctx->m, n = ctx->n;
+  cl_ctx::Slot& sl = ctx->slot[ctx->slot_head];
+  sl.t_start = std::chrono::steady_clock::now();
+  const int64_t m = ctx->m;
   // mean(y^2) for resolve_weights (clomp.cpp:134-136), per batch and per
   // column; only automatic prior weights (w < 0) depend on it.
   std::vector<double> col_ms;
@@ -1444,7 +1494,8 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   const size_t obytes = align_up((size_t)(batch * cap) * 4, 256) +
                         align_up((size_t)(batch * cap) * 8, 256) +
                         4 * align_up((size_t)batch * 8, 256) + 256;
-  char* stg = static_cast<char*>(stage_bytes(ctx, align_up(ybytes, 256) + obytes));
+  if (!slot_events(ctx, sl)) return fail(ctx, CL_ERR_CUDA, "clomp: stream / event creation failed");
+  char* stg = slot_device(ctx, sl, align_up(ybytes, 256) + obytes);
   if (!stg) return fail(ctx, CL_ERR_CUDA, "clomp: staging allocation failed");
   float* d_y = reinterpret_cast<float*>(stg);
   Carver cv{stg + align_up(ybytes, 256)};
@@ -1460,27 +1511,58 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   const size_t out_bytes = cv.off;  // the compact results, one D2H copy
 
   // Host side: pinned caller buffers go straight to the DMA engine; pageable
-  // ones are staged through the context's pinned buffer, which also receives
-  // the compact results.
+  // ones are staged through the slot's pinned buffer, which also receives the
+  // compact results.
   const bool y_pinned = is_pinned(y);
-  char* hio = host_io(ctx, out_bytes + (y_pinned ? 0 : align_up(ybytes, 256)));
+  char* hio = slot_host(sl, out_bytes + (y_pinned ? 0 : align_up(ybytes, 256)));
   if (!hio) return fail(ctx, CL_ERR_CUDA, "clomp: pinned host staging allocation failed");
   cudaStream_t s = ctx->stream;
   if (y_pinned) {
-    CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, s));
+    CL_CUDA(ctx, cudaMemcpyAsync(d_y, y, ybytes, cudaMemcpyHostToDevice, ctx->copy_in));
   } else {
     char* hy = hio + out_bytes;
     std::memcpy(hy, y, ybytes);
-    CL_CUDA(ctx, cudaMemcpyAsync(d_y, hy, ybytes, cudaMemcpyHostToDevice, s));
+    CL_CUDA(ctx, cudaMemcpyAsync(d_y, hy, ybytes, cudaMemcpyHostToDevice, ctx->copy_in));
   }
+  CL_CUDA(ctx, cudaEventRecord(sl.ev_in, ctx->copy_in));
+  CL_CUDA(ctx, cudaStreamWaitEvent(s, sl.ev_in, 0));
   st = solve_core(ctx, d_y, y_layout == CL_LAYOUT_REF, batch, cfg, mode, o, false);
-  if (st) return st;
+  if (st) {
+    cudaStreamSynchronize(ctx->copy_in);
+    cudaStreamSynchronize(s);
+    return st;
+  }
+  CL_CUDA(ctx, cudaEventRecord(sl.ev_solve, s));
+  CL_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_out, sl.ev_solve, 0));
   CL_CUDA(ctx, cudaMemcpyAsync(hio, stg + align_up(ybytes, 256), out_bytes,
-                               cudaMemcpyDeviceToHost, s));
-  CL_CUDA(ctx, cudaStreamSynchronize(s));
-  if (ctx->stats.corr_path != 2) ctx->stats.rescans = ctx->h_counters[kRescanTotal];
+                               cudaMemcpyDeviceToHost, ctx->copy_out));
+  CL_CUDA(ctx, cudaEventRecord(sl.ev_out, ctx->copy_out));
+  sl.busy = true;
+  sl.batch = batch;
+  sl.cap = cap;
+  sl.ybytes = ybytes;
+  sl.out_bytes = out_bytes;
+  sl.mode = mode;
+  sl.fused = ctx->stats.corr_path == 2;
+  ctx->slot_head ^= 1;
+  ++ctx->slot_inflight;
+  return CL_OK;
+}
+
+// Second half: block until the oldest submitted batch's results are in host
+// memory and expand them into the caller's buffers.
+int cl_wait(cl_ctx* ctx, cl_result* out) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (ctx->slot_inflight <= 0) return fail(ctx, CL_ERR_CONFIG, "cl_wait: nothing in flight");
+  cudaSetDevice(ctx->device);
+  cl_ctx::Slot& sl = ctx->slot[(ctx->slot_head + 2 - ctx->slot_inflight) & 1];
+  --ctx->slot_inflight;
+  sl.busy = false;
+  CL_CUDA(ctx, cudaEventSynchronize(sl.ev_out));
+  const int64_t batch = sl.batch, cap = sl.cap, n = ctx->n;
+  if (!sl.fused) ctx->stats.rescans = ctx->h_counters[kRescanTotal];
   // host views of the compact results (same carving as the device side)
-  Carver hv{hio};
+  Carver hv{sl.h_io};
   const int32_t* h_sup = hv.take<int32_t>(batch * cap);
   const double* h_coef = hv.take<double>(batch * cap);
   const int32_t* h_cnt = hv.take<int32_t>(batch);
@@ -1517,18 +1599,29 @@ int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
       if (out->status) out->status[b] = h_st[b];
     }
   }
-  // End to end through this call: host y in, host results out (wall clock).
+  // End to end through submit + wait: host y in, host results out (wall clock;
+  // with two batches in flight it includes the time queued behind the other).
   ctx->stats.e2e_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start)
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - sl.t_start)
           .count();
-  ctx->stats.h2d_bytes = (int64_t)ybytes;
-  ctx->stats.d2h_bytes = (int64_t)out_bytes;
-  if (mode == CL_MODE_JOINT && batch > 0 && h_st[0] != CL_OK) {
+  ctx->stats.h2d_bytes = (int64_t)sl.ybytes;
+  ctx->stats.d2h_bytes = (int64_t)sl.out_bytes;
+  if (sl.mode == CL_MODE_JOINT && batch > 0 && h_st[0] != CL_OK) {
     return fail(ctx, h_st[0],
                 h_st[0] == CL_ERR_NUMERICAL ? "clomp: loss diverged; reduce lr"
                                             : "clomp: support capacity exceeded");
   }
   return CL_OK;
+}
+
+int cl_solve_batch(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
+                   const cl_config* cfg, int mode, cl_result* out) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (ctx->slot_inflight != 0)
+    return fail(ctx, CL_ERR_CONFIG, "cl_solve_batch: batches submitted with cl_submit are still in flight");
+  const int st = cl_submit(ctx, y, batch, y_layout, cfg, mode);
+  if (st) return st;
+  return cl_wait(ctx, out);
 }
 
 int cl_solve_batch_device(cl_ctx* ctx, const float* d_y, int64_t batch,

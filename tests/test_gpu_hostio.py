@@ -31,3 +31,70 @@ def test_pinned_pageable_dense_compact_agree(gpu_available):
             assert np.array_equal(r.support[b], ref.support[b])
             assert np.array_equal(r.coef[b], ref.coef[b])
             assert np.array_equal(np.flatnonzero(ref.mask[:, b]), np.sort(ref.support[b]))
+
+
+def _same(r, ref, B):
+    assert np.array_equal(r.iterations, ref.iterations)
+    assert np.array_equal(r.final_residual_norm, ref.final_residual_norm)
+    assert np.array_equal(r.status, ref.status)
+    for b in range(B):
+        assert np.array_equal(r.support[b], ref.support[b])
+        assert np.array_equal(r.coef[b], ref.coef[b])
+
+
+@pytest.mark.parametrize("shape", [(96, 256, 6, 40), (512, 1024, 12, 300)])
+def test_submit_wait_pipeline_equals_blocking_calls(gpu_available, shape):
+    """cl_submit / cl_wait with two batches in flight return, in submission
+    order, exactly what blocking cl_solve_batch calls return (pinned and
+    pageable y, different batch sizes back to back)."""
+    m, n, k, B = shape
+    A, _, Y, _ = cl.gen_problem_1d(11, m, n, k, B, snr_db=40.0)
+    ctx = cl.ClompContext(A)
+    cfg = cl.ClompConfig.baseline(k)
+    batches = []
+    for i, lo in enumerate((0, B // 3, B // 2, 1)):
+        y = np.ascontiguousarray(Y[:, lo:])
+        if i % 2 == 0:
+            yp = torch.empty(y.shape, dtype=torch.float32, pin_memory=True).numpy()
+            yp[...] = y
+            y = yp
+        batches.append(y)
+    refs = [cl.clomp_solve_batch(ctx, y, cfg, mode=cl.MODE_PER_SIGNAL, dense=False) for y in batches]
+    got = []
+    cl.clomp_submit(ctx, batches[0], cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+    for y in batches[1:]:
+        cl.clomp_submit(ctx, y, cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+        got.append(cl.clomp_wait(ctx))
+    got.append(cl.clomp_wait(ctx))
+    for y, r, ref in zip(batches, got, refs):
+        _same(r, ref, y.shape[1])
+    st = ctx.stats()
+    assert st["h2d_bytes"] == batches[-1].size * 4 and st["e2e_ms"] > 0
+
+
+def test_submit_limits_and_errors(gpu_available):
+    A, _, Y, _ = cl.gen_problem_1d(3, 64, 128, 4, 8)
+    ctx = cl.ClompContext(A)
+    cfg = cl.ClompConfig.baseline(4)
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_wait(ctx)  # nothing in flight
+    bad = cl.ClompConfig.baseline(4)
+    bad.lr = 0.0
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_submit(ctx, Y, bad, mode=cl.MODE_PER_SIGNAL)  # leaves nothing in flight
+    assert not ctx._pending
+    cl.clomp_submit(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    cl.clomp_submit(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_submit(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)  # third in flight
+    assert len(ctx._pending) == 2
+    with pytest.raises(cl.ConfigError):
+        cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)  # blocking call while in flight
+    a, b = cl.clomp_wait(ctx), cl.clomp_wait(ctx)
+    _same(a, b, Y.shape[1])
+    # a diverging joint batch reports through cl_wait
+    div = cl.ClompConfig.baseline(4)
+    div.lr = 1e6
+    cl.clomp_submit(ctx, Y, div, mode=cl.MODE_JOINT)
+    with pytest.raises(cl.NumericalError):
+        cl.clomp_wait(ctx)
