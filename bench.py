@@ -521,27 +521,66 @@ def run_ours(args, rank, world, local_rank):
         prof = ctx.stats()
         ctx.set_profiling(False)
 
-    # End to end through the public API: y from pinned host memory in, the
-    # compact per-signal results (supports, coefficients, norms, flags) back in
-    # host memory; wall clock of the whole library call (ctx.stats e2e_ms).
-    Y_pin = torch.empty(Y.shape, dtype=torch.float32, pin_memory=True).numpy()
-    Y_pin[...] = Y
+    # End to end through the public API: every step's y comes from pinned host
+    # memory and its compact per-signal results (supports, coefficients, norms,
+    # flags) land back in host memory.  Pipelined (clomp_submit / clomp_wait,
+    # two batches in flight): step i + 1's upload and step i's download run on
+    # copy streams under the other step's solve; the L2 flush is queued on the
+    # solve stream before every step, inside the timed region.  Host wall clock
+    # over the whole K-step region / K.  The blocking single call is reported
+    # beside it (e2e.blocking_call).
+    n_rot = 3
+    Y_pins = []
+    for i in range(n_rot):
+        yp = torch.empty(Y.shape, dtype=torch.float32, pin_memory=True).numpy()
+        yp[...] = Y
+        Y_pins.append(yp)
     for _ in range(max(args.warmup, 3)):  # warm-up (graphs, pinned staging, host pages)
-        cl.clomp_solve_batch(ctx, Y_pin, cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+        cl.clomp_solve_batch(ctx, Y_pins[0], cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
     e2e_ms = []
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(3)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = cl.clomp_solve_batch(ctx, Y_pin, cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+        r = cl.clomp_solve_batch(ctx, Y_pins[0], cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         st = ctx.stats()
     assert np.all(r.status == 0)
-    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    blocking_ms = statistics.mean(e2e_ms)
+
+    def flush_step(i):
+        with torch.cuda.stream(stream):
+            flush.fill_(3)
+        cl.clomp_submit(ctx, Y_pins[i % n_rot], cfg, mode=cl.MODE_PER_SIGNAL, dense=False)
+
+    for rep in range(2):  # rep 0: warm-up of the pipelined loop
+        if dist:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        flush_step(0)
+        for i in range(1, args.steps):
+            flush_step(i)
+            r = cl.clomp_wait(ctx)
+            assert r.status.max() == 0
+        r = cl.clomp_wait(ctx)
+        assert r.status.max() == 0
+        pipe_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    te = torch.tensor([pipe_ms, blocking_ms], dtype=torch.float64, device=dev)
     if dist:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = total_signals / (float(te.item()) / 1000.0)
+    e2e_val = total_signals / (float(te[0].item()) / 1000.0)
+    e2e_blocking = total_signals / (float(te[1].item()) / 1000.0)
+
+    # One-off context cost (dictionary transpose + upload, fp16 split, A^T A).
+    t0 = time.perf_counter()
+    if c["sep"]:
+        ctx2 = cl.ClompContext.separable(A[0], A[1], device=local_rank)
+    else:
+        ctx2 = cl.ClompContext(A, device=local_rank)
+    create_ms = (time.perf_counter() - t0) * 1e3
+    ctx2.close()
 
     if rank != 0:
         return
@@ -658,8 +697,29 @@ def run_ours(args, rank, world, local_rank):
             out["roofline_learn"] = learn_roof
     out["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
                   "d2h_bytes_per_step": st["d2h_bytes"],
-                  "path": ("clomp_solve_batch(dense=False): y from pinned host memory, compact "
-                           "results (supports, coefficients, norms, flags) to host; host wall clock around the Python call")}
+                  "path": ("clomp_submit / clomp_wait (dense=False), two batches in flight: every "
+                           "step's y from pinned host memory, compact results (supports, "
+                           "coefficients, norms, flags) to host, L2 flush queued before every "
+                           "step; host wall clock over the K-step region / K"),
+                  "blocking_call": {"value": e2e_blocking, "unit": UNIT,
+                                    "path": "one clomp_solve_batch call at a time, host wall clock around it"}}
+    out["setup"] = {"cl_create_ms": create_ms,
+                    "note": "one-off per dictionary (host transpose, upload, fp16 split, A^T A); outside every timed region"}
+    # The drop-in boundary itself: cskit::clomp_solve_batch (the reference's C++
+    # signature, joint semantics, fp64 host buffers, dense s / mask / x_hat back)
+    # served by the C++ shim, timed by a prebuilt binary at this config's shape.
+    shim_bin = ROOT / "paper_2501_11592_b200" / "_build" / "shim_bench"
+    if world == 1 and shim_bin.exists() and args.config in (1, 2) and not args.colshard:
+        try:
+            ctx.close()  # free this process's copy before the binary runs on the same GPU
+            lines = []
+            for ident in (0, 1):
+                rr = subprocess.run([str(shim_bin), str(n), str(c["batch"]), str(c["k"]), "5", str(ident)],
+                                    capture_output=True, text=True, timeout=300)
+                lines.append(json.loads(rr.stdout.strip().splitlines()[-1]))
+            out["shim"] = lines
+        except Exception as exc:  # the boundary timing is supplementary
+            out["shim"] = {"unavailable": repr(exc)[:200]}
     out["gpu_launches"] = int(launches_per_step * args.steps)
     out["clocks"] = clocks
     if world == 1 and not args.no_cpu_baseline and not c["sep"]:

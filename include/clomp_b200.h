@@ -92,6 +92,7 @@ void cl_config_default(cl_config* cfg);
 /* Results, caller-owned host buffers.  NULL pointers are skipped.
  * `cap` is the per-signal length of support/coef.  The support of signal b is
  * support[b*cap .. b*cap+count[b]) in ascending atom order with coef aligned. */
+#define CL_RESULT_PREZEROED 1  /* cl_result::flags: s and mask are already all zero */
 typedef struct cl_result {
   int64_t cap;
   int32_t* support;             /* [B][cap]                                */
@@ -103,6 +104,11 @@ typedef struct cl_result {
   double* final_residual_norm;  /* [B]  (JOINT: the batch Frobenius norm)  */
   uint8_t* converged;           /* [B]                                     */
   int32_t* status;              /* [B]  cl_status per signal               */
+  double* x_hat;                /* dense n x B, REF layout: basis * (s .* mask)
+                                 * (BatchSolveResult::x_hat, clomp.cpp:289); needs
+                                 * cl_set_basis + cl_set_synthesis(ctx, 1)          */
+  int32_t flags;                /* CL_RESULT_* (0: the library zero-fills s / mask) */
+  int32_t pad0;
 } cl_result;
 
 typedef struct cl_ctx cl_ctx;
@@ -142,6 +148,27 @@ cl_ctx* cl_create_colshard(int device, const float* a, int64_t m, int64_t n,
 /* Test hook: run the column-sharded algorithm with `shards` virtual shards on
  * this one GPU (the exchange is a local copy instead of NCCL). */
 int cl_set_virtual_shards(cl_ctx* ctx, int shards);
+
+/* Multi-GPU context group in ONE process: one context per
+ * listed device, driven by one host thread per device inside each call.
+ *   CL_GROUP_SIGNAL_SHARD: the batch's independent signals (CL_MODE_PER_SIGNAL,
+ *     the CLI's per-signal loop cskit.cpp:543-551) are split into contiguous
+ *     ranges, one per device, with no data-path communication; every device
+ *     holds the whole dictionary.  A device may be listed more than once.
+ *   CL_GROUP_COLUMN_SHARD: one large dictionary sharded by atoms
+ *     (cl_create_colshard over NCCL, distinct devices): every device solves
+ *     the whole batch together; rank 0's results are returned.
+ * cl_group_solve_batch has cl_solve_batch's arguments and result layout. */
+enum { CL_GROUP_SIGNAL_SHARD = 0, CL_GROUP_COLUMN_SHARD = 1 };
+typedef struct cl_group cl_group;
+cl_group* cl_create_group(const int* devices, int ndev, const float* a, int64_t m, int64_t n,
+                          int a_layout, int mode, int* status);
+void cl_destroy_group(cl_group* g);
+int cl_group_size(const cl_group* g);
+cl_ctx* cl_group_context(cl_group* g, int index);   /* borrowed: knobs, stats */
+const char* cl_group_last_error(const cl_group* g); /* NULL: last failing cl_create_group */
+int cl_group_solve_batch(cl_group* g, const float* y, int64_t batch, int y_layout,
+                         const cl_config* cfg, int mode, cl_result* out);
 
 /* Message of the last failing call on ctx (or of the last failing cl_create
  * on this thread when ctx is NULL). */
@@ -239,6 +266,13 @@ int cl_set_fused(cl_ctx* ctx, int on);
  * Priors on multi-column joint batches (TV-2D + local variance) return
  * CL_ERR_UNSUPPORTED; priors without a basis too. */
 int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
+/* Synthesis x_hat = D (s .* mask) (clomp.cpp:289) on the GPU: when on, every
+ * host-buffer solve of a context with a basis also forms x_hat from the
+ * compact supports (n x count multiply-adds per signal instead of the
+ * reference's dense n x n x B product) and returns it in cl_result::x_hat
+ * (n x B fp64 more per download).  Off by default; a non-NULL x_hat without
+ * it (or without a basis) fails with CL_ERR_UNSUPPORTED. */
+int cl_set_synthesis(cl_ctx* ctx, int on);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram
  * matrix in registers (default 1); 0 keeps them on the block-per-signal
  * kernel (tests compare them). */

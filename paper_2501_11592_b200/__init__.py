@@ -89,6 +89,9 @@ class CResult(C.Structure):
         ("final_residual_norm", C.c_void_p),
         ("converged", C.c_void_p),
         ("status", C.c_void_p),
+        ("x_hat", C.c_void_p),
+        ("flags", C.c_int32),
+        ("pad0", C.c_int32),
     ]
 
 
@@ -127,8 +130,10 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_submit", "cl_wait", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis", "cl_set_synthesis",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
+    "cl_create_group", "cl_destroy_group", "cl_group_size", "cl_group_context",
+    "cl_group_last_error", "cl_group_solve_batch",
     "cl_gen_problem_2d", "cl_dct_basis",
     "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
 ]
@@ -167,10 +172,20 @@ def lib() -> C.CDLL:
         h.cl_set_cluster_learn.argtypes = [vp, i32]
         h.cl_set_power_levels.argtypes = [vp, i32]
         h.cl_set_basis.argtypes = [vp, vp, C.c_int64, i32]
+        h.cl_set_synthesis.argtypes = [vp, i32]
         h.cl_nccl_unique_id.argtypes = [vp]
         h.cl_create_colshard.restype = vp
         h.cl_create_colshard.argtypes = [i32, vp, i64, i64, i32, i32, i32, vp, C.POINTER(C.c_int)]
         h.cl_set_virtual_shards.argtypes = [vp, i32]
+        h.cl_create_group.restype = vp
+        h.cl_create_group.argtypes = [vp, i32, vp, i64, i64, i32, i32, C.POINTER(C.c_int)]
+        h.cl_destroy_group.argtypes = [vp]
+        h.cl_group_size.argtypes = [vp]
+        h.cl_group_context.restype = vp
+        h.cl_group_context.argtypes = [vp, i32]
+        h.cl_group_last_error.restype = C.c_char_p
+        h.cl_group_last_error.argtypes = [vp]
+        h.cl_group_solve_batch.argtypes = [vp, vp, i64, i32, C.POINTER(CConfig), i32, C.POINTER(CResult)]
         h.cl_create_sep.restype = vp
         h.cl_create_sep.argtypes = [i32, vp, i64, i64, vp, i64, i64, i32, C.POINTER(C.c_int)]
         h.cl_gen_problem_2d.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]
@@ -215,6 +230,7 @@ class BatchSolveResult:
     status: np.ndarray
     support: Ragged               # per signal, ascending atom indices
     coef: Ragged                  # per signal, aligned with support
+    x_hat: np.ndarray | None = None   # n x B fp64, basis @ (s * mask) (set_synthesis)
 
 
 @dataclasses.dataclass
@@ -345,6 +361,16 @@ class ClompContext:
             raise DimensionError("set_basis: D must be square")
         _raise(lib().cl_set_basis(self._h, _ptr(D), D.shape[0], 0), self._h)
 
+    def set_synthesis(self, on: bool):
+        """Also return x_hat = D (s * mask) (BatchSolveResult.x_hat, clomp.cpp:289),
+        formed on the GPU from the compact supports; needs set_basis."""
+        _raise(lib().cl_set_synthesis(self._h, int(bool(on))), self._h)
+        self.__dict__["_synth_on"] = bool(on)
+
+    @property
+    def _synthesis(self) -> bool:
+        return self.__dict__.get("_synth_on", False)
+
     def set_cluster_learn(self, on):
         """Learn supports of 33..256 atoms on CTA clusters with register-resident
         Gram blocks (True / 1, default; 2 = eight-CTA variant above 128 atoms) or
@@ -377,6 +403,58 @@ class ClompContext:
         s = CStats()
         _raise(lib().cl_get_stats(self._h, C.byref(s)), self._h)
         return {f: getattr(s, f) for f, _ in CStats._fields_ if f != "pad0"}
+
+
+GROUP_SIGNAL_SHARD, GROUP_COLUMN_SHARD = 0, 1
+
+
+class ClompGroup:
+    """One dictionary on several GPUs of this process (cl_create_group):
+    mode GROUP_SIGNAL_SHARD splits a batch's independent signals across the
+    devices, GROUP_COLUMN_SHARD splits one large dictionary by atoms (NCCL)."""
+
+    def __init__(self, a, devices, mode: int = GROUP_SIGNAL_SHARD, layout: str = "ref"):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        if a.ndim != 2:
+            raise DimensionError("dictionary must be 2-D")
+        self.m, self.n = a.shape if layout == "ref" else a.shape[::-1]
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        st = C.c_int(0)
+        h = lib().cl_create_group(devs, len(devices), _ptr(a), self.m, self.n,
+                                  LAYOUT_REF if layout == "ref" else LAYOUT_T, int(mode), C.byref(st))
+        if not h:
+            msg = lib().cl_group_last_error(None)
+            raise _ERRORS.get(st.value or CL_ERR_CUDA, Error)(msg.decode() if msg else "cl_create_group")
+        self._g = h
+        self.devices = list(devices)
+        self._synthesis = False
+
+    def close(self):
+        if getattr(self, "_g", None):
+            lib().cl_destroy_group(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self) -> int:
+        return lib().cl_group_size(self._g)
+
+    def solve_batch(self, y_cols, cfg: ClompConfig | None = None, mode: int = MODE_PER_SIGNAL,
+                    layout: str = "ref", dense: bool = True) -> BatchSolveResult:
+        cfg = cfg or ClompConfig()
+        y, B, lay = _prep_y(self, y_cols, layout)
+        pend = _Pending(self, y, B, cfg, dense)
+        c = cfg.to_c()
+        code = lib().cl_group_solve_batch(self._g, _ptr(y), B, lay, C.byref(c), int(mode),
+                                          C.byref(pend.res))
+        if code:
+            msg = lib().cl_group_last_error(self._g)
+            raise _ERRORS.get(code, Error)(msg.decode() if msg else f"status {code}")
+        return pend.result()
 
 
 def nccl_unique_id() -> bytes:
@@ -420,9 +498,10 @@ class _Pending:
         self.rn = np.zeros(max(B, 1), np.float64)
         self.cv = np.zeros(max(B, 1), np.uint8)
         self.st = np.zeros(max(B, 1), np.int32)
+        self.xh = np.zeros((n, max(B, 1)), np.float64) if ctx._synthesis else None
         self.res = CResult(cap, _ptr(self.sup), _ptr(self.coef), _ptr(self.cnt), _ptr(self.s),
                            _ptr(self.mask), _ptr(self.it), _ptr(self.rn), _ptr(self.cv),
-                           _ptr(self.st))
+                           _ptr(self.st), _ptr(self.xh), 1, 0)  # s / mask are np.zeros: PREZEROED
 
     def result(self) -> BatchSolveResult:
         B, cap, dense = self.B, self.cap, self.dense
@@ -430,7 +509,8 @@ class _Pending:
         return BatchSolveResult(self.s[:, :B] if dense else None,
                                 self.mask[:, :B] if dense else None, self.it[:B], self.rn[:B],
                                 self.cv[:B].astype(bool), self.st[:B], Ragged(self.sup, counts),
-                                Ragged(self.coef, counts))
+                                Ragged(self.coef, counts),
+                                self.xh[:, :B] if self.xh is not None else None)
 
 
 def clomp_submit(ctx: ClompContext, y_cols, cfg: ClompConfig | None = None,

@@ -122,6 +122,7 @@ struct cl_ctx {
     size_t ybytes = 0, out_bytes = 0;
     int mode = 0;
     bool fused = false;
+    bool xhat = false;  // x_hat = D s was formed and downloaded with the results
     std::chrono::steady_clock::time_point t_start;
   };
   Slot slot[2];
@@ -134,6 +135,7 @@ struct cl_ctx {
   GraphKey gkey;
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
+  bool want_xhat = false;  // cl_set_synthesis
   bool fused_ok = true;  // small problems: one persistent block per signal
   int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (0: block kernel)
   int power_levels = -1;  // plain GD on cluster-sized supports: squaring levels (-1 auto, 0 off)
@@ -1294,6 +1296,14 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout) {
   return CL_OK;
 }
 
+int cl_set_synthesis(cl_ctx* ctx, int on) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (ctx->slot_inflight != 0)
+    return fail(ctx, CL_ERR_CONFIG, "cl_set_synthesis: batches are in flight");
+  ctx->want_xhat = on != 0;
+  return CL_OK;
+}
+
 int cl_set_cluster_learn(cl_ctx* ctx, int on) {
   if (!ctx) return CL_ERR_INTERNAL;
   ctx->cluster_learn = on <= 0 ? 0 : 1;
@@ -1491,9 +1501,11 @@ int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
 
   const int64_t cap = support_cap(ctx, cfg);
   const size_t ybytes = (size_t)(m * batch) * sizeof(float);
+  const bool xhat = ctx->want_xhat && ctx->dt != nullptr;
   const size_t obytes = align_up((size_t)(batch * cap) * 4, 256) +
                         align_up((size_t)(batch * cap) * 8, 256) +
-                        4 * align_up((size_t)batch * 8, 256) + 256;
+                        4 * align_up((size_t)batch * 8, 256) + 256 +
+                        (xhat ? align_up((size_t)(batch * ctx->n) * 8, 256) + 256 : 0);
   if (!slot_events(ctx, sl)) return fail(ctx, CL_ERR_CUDA, "clomp: stream / event creation failed");
   char* stg = slot_device(ctx, sl, align_up(ybytes, 256) + obytes);
   if (!stg) return fail(ctx, CL_ERR_CUDA, "clomp: staging allocation failed");
@@ -1508,7 +1520,8 @@ int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   o.rn = cv.take<double>(batch);
   o.conv = cv.take<uint8_t>(batch);
   o.status = cv.take<int32_t>(batch);
-  const size_t out_bytes = cv.off;  // the compact results, one D2H copy
+  double* d_xhat = xhat ? cv.take<double>(batch * ctx->n) : nullptr;
+  const size_t out_bytes = cv.off;  // the compact results (+ x_hat), one D2H copy
 
   // Host side: pinned caller buffers go straight to the DMA engine; pageable
   // ones are staged through the slot's pinned buffer, which also receives the
@@ -1532,6 +1545,10 @@ int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
     cudaStreamSynchronize(s);
     return st;
   }
+  if (xhat) {  // x_hat = D (s .* mask) from the compact results (clomp.cpp:289)
+    launch_synth(ctx->dt, ctx->n, batch, cap, o.sup, o.coef, o.cnt, d_xhat, s);
+    ++ctx->stats.kernel_launches;
+  }
   CL_CUDA(ctx, cudaEventRecord(sl.ev_solve, s));
   CL_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_out, sl.ev_solve, 0));
   CL_CUDA(ctx, cudaMemcpyAsync(hio, stg + align_up(ybytes, 256), out_bytes,
@@ -1544,6 +1561,7 @@ int cl_submit(cl_ctx* ctx, const float* y, int64_t batch, int y_layout,
   sl.out_bytes = out_bytes;
   sl.mode = mode;
   sl.fused = ctx->stats.corr_path == 2;
+  sl.xhat = xhat;
   ctx->slot_head ^= 1;
   ++ctx->slot_inflight;
   return CL_OK;
@@ -1570,10 +1588,24 @@ int cl_wait(cl_ctx* ctx, cl_result* out) {
   const double* h_rn = hv.take<double>(batch);
   const uint8_t* h_cv = hv.take<uint8_t>(batch);
   const int32_t* h_st = hv.take<int32_t>(batch);
+  const double* h_xh = sl.xhat ? hv.take<double>(batch * n) : nullptr;
 
   if (out) {
-    if (out->s) std::memset(out->s, 0, sizeof(double) * (size_t)(n * batch));
-    if (out->mask) std::memset(out->mask, 0, (size_t)(n * batch));
+    if (out->x_hat && h_xh) {  // device result is signal-major [B][n]
+      if (batch == 1) {
+        std::memcpy(out->x_hat, h_xh, sizeof(double) * (size_t)n);
+      } else {
+        constexpr int64_t T = 32;
+        for (int64_t q0 = 0; q0 < n; q0 += T)
+          for (int64_t b0 = 0; b0 < batch; b0 += T)
+            for (int64_t q = q0; q < std::min(n, q0 + T); ++q)
+              for (int64_t b = b0; b < std::min(batch, b0 + T); ++b)
+                out->x_hat[q * batch + b] = h_xh[b * n + q];
+      }
+    }
+    const bool prezeroed = (out->flags & CL_RESULT_PREZEROED) != 0;
+    if (out->s && !prezeroed) std::memset(out->s, 0, sizeof(double) * (size_t)(n * batch));
+    if (out->mask && !prezeroed) std::memset(out->mask, 0, (size_t)(n * batch));
     for (int64_t b = 0; b < batch; ++b) {
       const int cnt = h_cnt[b];
       for (int k = 0; k < cnt; ++k) {
@@ -1606,6 +1638,9 @@ int cl_wait(cl_ctx* ctx, cl_result* out) {
           .count();
   ctx->stats.h2d_bytes = (int64_t)sl.ybytes;
   ctx->stats.d2h_bytes = (int64_t)sl.out_bytes;
+  if (out && out->x_hat && !h_xh)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "clomp: x_hat needs a synthesis basis (cl_set_basis) and cl_set_synthesis(ctx, 1)");
   if (sl.mode == CL_MODE_JOINT && batch > 0 && h_st[0] != CL_OK) {
     return fail(ctx, h_st[0],
                 h_st[0] == CL_ERR_NUMERICAL ? "clomp: loss diverged; reduce lr"

@@ -372,6 +372,10 @@ void launch_prior_control(const SolveParams& p, const Work& w, int outer, cudaSt
 void launch_image_learn(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
 constexpr int kLvCover = 8;  // max windows covering one row / column
 
+// ---- k_synth.cu: x_hat[b][q] = sum_k D[q][sup_k] coef_k from the compact results
+void launch_synth(const double* dt, int64_t n, int64_t B, int64_t out_cap, const int32_t* sup,
+                  const double* coef, const int32_t* cnt, double* xhat, cudaStream_t s);
+
 // Whole per-signal solve in one persistent block per signal (small problems).
 void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);
 // inject_support unit path: residual already in w.r64 (and split), mask in

@@ -98,3 +98,26 @@ def test_submit_limits_and_errors(gpu_available):
     cl.clomp_submit(ctx, Y, div, mode=cl.MODE_JOINT)
     with pytest.raises(cl.NumericalError):
         cl.clomp_wait(ctx)
+
+
+def test_synthesis_x_hat_on_gpu(gpu_available):
+    """x_hat = D (s * mask) (clomp.cpp:289) formed on the GPU from the compact
+    supports equals the dense host product; it needs a basis and the switch."""
+    n, m, k, B = 128, 64, 5, 9
+    A, _, Y, _ = cl.gen_problem_1d(5, m, n, k, B)
+    D = cl.dct_basis(n)
+    ctx = cl.ClompContext(A)
+    cfg = cl.ClompConfig.baseline(k)
+    ctx.set_synthesis(True)
+    with pytest.raises(cl.UnsupportedError):  # no basis yet
+        cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    ctx.set_basis(D)
+    for mode in (cl.MODE_PER_SIGNAL, cl.MODE_JOINT):
+        r = cl.clomp_solve_batch(ctx, Y, cfg, mode=mode)
+        want = D @ (r.s * r.mask)
+        assert r.x_hat.shape == (n, B)
+        assert np.max(np.abs(r.x_hat - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    r1 = cl.clomp_solve_batch(ctx, Y[:, :1], cfg, mode=cl.MODE_JOINT)
+    assert np.max(np.abs(r1.x_hat - D @ (r1.s * r1.mask))) <= 1e-12
+    ctx.set_synthesis(False)
+    assert cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL).x_hat is None
