@@ -67,7 +67,11 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank solves its own batch of the config's size; strong: "
                          "the config's batch is split across the ranks")
-    ap.add_argument("--max-outer", type=int, default=0)
+    ap.add_argument("--max-outer", type=int, default=0,
+                    help="outer iterations (0: K for the 1D configs, a 64-iteration prefix for the "
+                         "2D ones; -1: the config's full K)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="time-box a heavy config on fewer signals / images than it names")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corr-path", type=int, default=0, help="0 auto, 1 fp64 SIMT, 2 tcgen05, 3 GEMV")
     ap.add_argument("--power-levels", type=int, default=-1,
@@ -80,11 +84,13 @@ def workload(args, rank: int, world: int = 1):
 
     c = dict(CONFIGS[args.config])
     c["sep"] = "n_r" in c
+    if args.batch:
+        c["batch"] = args.batch
     if c["sep"]:
         c["n"], c["m"] = c["n_r"] * c["n_c"], c["m_r"] * c["m_c"]
-        c["max_outer"] = args.max_outer or 64
+        c["max_outer"] = c["k"] if args.max_outer < 0 else (args.max_outer or 64)
     else:
-        c["max_outer"] = args.max_outer or c["k"]
+        c["max_outer"] = c["k"] if args.max_outer < 0 else (args.max_outer or c["k"])
     c["sig_lo"], c["sig_hi"] = 0, c["batch"]
     if args.colshard:
         pass  # one batch solved together by all ranks
@@ -124,7 +130,8 @@ def config_block(c, n_gpus, mode):
     "colshard" (one batch, the dictionary split by atoms)."""
     if c["sep"]:
         shape = (f"{c['n_r']}x{c['n_c']} coefficients, {c['m_r']}x{c['m_c']} measurements, "
-                 f"K={c['k']} (prefix: {c['max_outer']} outer iterations)")
+                 f"K={c['k']} (" + ("full solve" if c["max_outer"] >= c["k"] else
+                                   f"prefix: {c['max_outer']} outer iterations") + ")")
     else:
         shape = f"N={c['n']} M={c['m']} K={c['k']}"
     noise = "" if c["sep"] or c["snr_db"] < 0 else f" {c['snr_db']} dB"

@@ -273,6 +273,16 @@ int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
  * (n x B fp64 more per download).  Off by default; a non-NULL x_hat without
  * it (or without a basis) fails with CL_ERR_UNSUPPORTED. */
 int cl_set_synthesis(cl_ctx* ctx, int on);
+/* Separable contexts, large supports: learn in DIRECT form — the reference's
+ * epoch (clomp.cpp:83-91, 120-123) applied through the factors, V = A_r C
+ * (column-sorted sparse), R = V A_c^T - Y and U = R A_c as fp64 GEMMs, the
+ * gradient 2 a_r,i . U_j on the support entries only — instead of the Gram
+ * form, whose t x t matrix per image stops fitting (above 2048 atoms: config
+ * 5's K = 13107) or costs more to stream than the operator costs to apply.
+ * from_outer: -1 auto (every iteration without a Gram buffer; otherwise from
+ * t^2 > m_r n_c m_c / 8 on), 0 never (supports above 2048 atoms then fail
+ * with CL_ERR_UNSUPPORTED), k > 0 from outer iteration k on (tests). */
+int cl_set_direct_form(cl_ctx* ctx, int from_outer);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram
  * matrix in registers (default 1); 0 keeps them on the block-per-signal
  * kernel (tests compare them). */

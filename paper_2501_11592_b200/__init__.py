@@ -130,7 +130,7 @@ EXPORTED = [
     "cl_config_default", "cl_create", "cl_destroy", "cl_last_error",
     "cl_solve_batch", "cl_submit", "cl_wait", "cl_solve_batch_device", "cl_synchronize",
     "cl_inject_support", "cl_get_stats", "cl_set_corr_path", "cl_set_profiling",
-    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis", "cl_set_synthesis",
+    "cl_set_stream", "cl_debug_scores", "cl_set_gram_cache", "cl_create_sep", "cl_set_fused", "cl_set_cluster_learn", "cl_set_power_levels", "cl_set_basis", "cl_set_synthesis", "cl_set_direct_form",
     "cl_nccl_unique_id", "cl_create_colshard", "cl_set_virtual_shards",
     "cl_create_group", "cl_destroy_group", "cl_group_size", "cl_group_context",
     "cl_group_last_error", "cl_group_solve_batch",
@@ -173,6 +173,7 @@ def lib() -> C.CDLL:
         h.cl_set_power_levels.argtypes = [vp, i32]
         h.cl_set_basis.argtypes = [vp, vp, C.c_int64, i32]
         h.cl_set_synthesis.argtypes = [vp, i32]
+        h.cl_set_direct_form.argtypes = [vp, i32]
         h.cl_nccl_unique_id.argtypes = [vp]
         h.cl_create_colshard.restype = vp
         h.cl_create_colshard.argtypes = [i32, vp, i64, i64, i32, i32, i32, vp, C.POINTER(C.c_int)]
@@ -341,6 +342,11 @@ class ClompContext:
 
     def set_corr_path(self, path: int):
         _raise(lib().cl_set_corr_path(self._h, int(path)), self._h)
+
+    def set_direct_form(self, from_outer: int):
+        """Separable contexts: learn in direct form (no support Gram matrix) from
+        outer iteration `from_outer` on; -1 auto, 0 never."""
+        _raise(lib().cl_set_direct_form(self._h, int(from_outer)), self._h)
 
     def set_gram_cache(self, mode: int):
         """1 build / 0 drop / -1 auto the fp64 A^T A cache."""

@@ -136,6 +136,7 @@ struct cl_ctx {
   std::vector<cudaGraphExec_t> graphs;
   int corr_force = 0;
   bool want_xhat = false;  // cl_set_synthesis
+  int direct_mode = -1;  // separable direct-form learning: -1 auto, 0 off, k > 0 from iteration k
   bool fused_ok = true;  // small problems: one persistent block per signal
   int cluster_learn = 1;  // supports of 33..256 atoms on CTA clusters (0: block kernel)
   int power_levels = -1;  // plain GD on cluster-sized supports: squaring levels (-1 auto, 0 off)
@@ -220,15 +221,39 @@ bool priors_active(const cl_config* c, double mean_sq, int64_t batch, int64_t n)
 
 // Per-signal support capacity.  th == 1 adds one atom per outer iteration
 // except on exact ties (clomp.cpp:49-51 injects every tie), hence the slack.
+constexpr int64_t kGramCapMax = 2048;  // largest support with a Gram matrix per signal
+
 int64_t support_cap(const cl_ctx* ctx, const cl_config* c) {
   if (c->th >= 1.0) return std::min<int64_t>(ctx->n, (int64_t)c->max_outer + kTieSlack);
-  return ctx->n;
+  // th < 1 can select any number of atoms per iteration.  Separable contexts
+  // switch to direct-form learning (no Gram matrix), so every atom fits; 1D
+  // contexts keep a Gram matrix per signal and stop a signal that outgrows it
+  // with CL_ERR_CAPACITY.
+  if (ctx->sep) return ctx->n;
+  return std::min<int64_t>(ctx->n, kGramCapMax);
+}
+
+// First outer iteration that learns in direct form on a separable context
+// (launch_sep_direct_learn), 0 = never.  Without a Gram buffer (capacity above
+// kGramCapMax) every iteration does; otherwise the Gram form runs while
+// streaming G (8 t^2 bytes per epoch) is cheaper than applying the operator
+// (two mr x nc x mc fp64 GEMMs per epoch): t^2 < mr nc mc / 16 from the measured
+// costs at config 4 (Gram form ~5.3e-12 t^2 s, direct form ~3.4e-13 mr nc mc s
+// per image and epoch).  th < 1 has no per-iteration bound on t.
+int64_t direct_from(const cl_ctx* ctx, const cl_config* c, int64_t cap) {
+  if (!ctx->sep || ctx->direct_mode == 0) return 0;
+  if (cap > kGramCapMax) return 1;
+  if (ctx->direct_mode > 0) return ctx->direct_mode;
+  if (c->th < 1.0) return 0;
+  const double tstar = std::sqrt((double)ctx->mr * (double)ctx->nc * (double)ctx->mc / 16.0);
+  const int64_t from = std::max<int64_t>(257, (int64_t)tstar + 1);
+  return from <= (int64_t)c->max_outer ? from : 0;
 }
 
 // Carve the workspace for (B, cap); reallocate only when it grows.
 int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
                      bool need_split, int64_t ntile, bool need_prior = false,
-                     bool need_image = false) {
+                     bool need_image = false, bool sep_tc = false, bool with_direct = false) {
   const int64_t ldm = ctx->ldm;
   const int64_t mwords = (ctx->n + 31) / 32;
   auto carve = [&](Carver& cv, Work& w) {
@@ -244,6 +269,17 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
       w.zb = cv.take<double>(B * ctx->n);
       w.sep_scratch = cv.take<double>(B * ctx->nc * ctx->mr);
       w.lpart = cv.take<double>(B * (((ctx->mr + 63) / 64) * ((ctx->mc + 63) / 64)));
+      if (with_direct) {
+        w.sep_scratch2 = cv.take<double>(B * ctx->nc * ctx->mr);
+        w.csc_ptr = cv.take<int32_t>(B * (ctx->nc + 1));
+        w.csc_perm = cv.take<int32_t>(B * cap);
+      }
+      if (sep_tc) {
+        w.u_hi = cv.take<__half>(B * ctx->nc * ctx->ldr);
+        w.u_lo = cv.take<__half>(B * ctx->nc * ctx->ldr);
+        w.u_scale = cv.take<float>(B * ctx->nc);
+        w.u_active = cv.take<int32_t>(B * ctx->nc);
+      }
     }
     if (ctx->world > 1 || ctx->vshards > 1) {
       w.xg = cv.take<Cand>(B * ntile);
@@ -254,7 +290,7 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
     w.coef = cv.take<double>(B * cap);
     w.mom1 = cv.take<double>(B * cap);
     w.mom2 = cv.take<double>(B * cap);
-    w.gram = cv.take<double>(B * cap * cap);
+    w.gram = cap <= kGramCapMax ? cv.take<double>(B * cap * cap) : nullptr;
     w.bvec = cv.take<double>(B * cap);
     w.maskbits = cv.take<uint32_t>(B * mwords);
     w.best_coef = cv.take<double>(B * cap);
@@ -369,7 +405,8 @@ void enqueue_count(const SolveParams& p, const cl_config* c, int mode, int64_t c
                    int64_t* per_iter) {
   (void)c;
   if (p.sep)
-    *per_iter = 3 + 2 + (cap > 8 ? 2 : 1) + 3 + (mode == CL_MODE_JOINT ? 2 : 0);
+    *per_iter = 3 + 2 + (cap > 8 ? 2 : 1) + 3 + (mode == CL_MODE_JOINT ? 2 : 0) +
+                (p.tile_atoms == corr_tc_tile_atoms() ? 2 : 0);
   else
     *per_iter = 3 + (cap > 8 ? 3 : 2) + (mode == CL_MODE_JOINT ? 2 : 0) + (p.prior ? 3 : 0);
 }
@@ -423,7 +460,14 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                 "cl_set_corr_path(3): the GEMV correlation needs 1 <= B <= 8 on a 1D dictionary");
   const bool gemv = gemv_fit && (ctx->corr_force == 0 || ctx->corr_force == 3);
   const bool tensor = !ctx->sep && !gemv && use_tensor_path(ctx, c);
-  const bool full_scores = c->th < 1.0 || ctx->sep;
+  // separable contexts: stage 2 of the correlation on the tensor cores (K1 on
+  // the rows of U = R A_c) with candidate records instead of B x n fp64 scores
+  const bool sep_tc = ctx->sep && use_tensor_path(ctx, c);
+  if (ctx->sep && ctx->corr_force == 2 && !sep_tc)
+    return fail(ctx, CL_ERR_UNSUPPORTED,
+                "cl_set_corr_path(2): the separable tcgen05 correlation needs th = 1 and n_r a "
+                "multiple of 256");
+  const bool full_scores = c->th < 1.0 || (ctx->sep && !sep_tc);
   const int64_t cap = support_cap(ctx, c);
   const int W = ctx->world > 1 ? ctx->world : ctx->vshards;
   const bool colshard = W > 1;
@@ -438,10 +482,11 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     if (ctx->world > 1 && B % ctx->world != 0)
       return fail(ctx, CL_ERR_DIMENSION, "column sharding: batch must divide by the world size");
   }
-  if (cap > 2048)
+  const int64_t dfrom = direct_from(ctx, c, cap);
+  if (cap > kGramCapMax && dfrom != 1)
     return fail(ctx, CL_ERR_UNSUPPORTED,
-                "clomp: support capacity above 2048 atoms per signal is not "
-                "supported (lower max_outer, or th < 1 with n > 2048)");
+                "clomp: more than 2048 atoms per signal (max_outer) needs the direct-form "
+                "learner (separable contexts; cl_set_direct_form)");
   // Latency path: the whole solve in one persistent block per signal when the
   // dictionary is small (config 1) and supports stay register-resident.
   const bool image = ctx->img;
@@ -451,7 +496,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
                      cap <= kWarpCap && ctx->n * ctx->ldm <= (int64_t)1 << 22 &&
                      B <= 4 * (int64_t)ctx->sms;
   const int64_t tile_atoms =
-      tensor ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
+      (tensor || sep_tc) ? corr_tc_tile_atoms() : gemv ? corr_gemv_tile_atoms() : kCorrTileAtoms;
   const int64_t ntile = (ctx->n + tile_atoms - 1) / tile_atoms;
   if (image) {  // local-variance window tables -> device
     // (a batch submitted earlier may still read the tables: cl_submit pipelining)
@@ -471,7 +516,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       CL_CUDA(ctx, cudaMemcpy(ctx->lv_tab, all.data(), all.size() * 4, cudaMemcpyHostToDevice));
   }
   int st = ensure_workspace(ctx, B, cap, full_scores || fused, tensor && !fused, ntile,
-                            prior && !image, image);
+                            prior && !image, image, sep_tc, dfrom > 0);
   if (st) return st;
   if (prior && !image)
     CL_CUDA(ctx, cudaMemcpyAsync(ctx->w.wtv, ctx->prior_w.data(), (size_t)B * sizeof(double),
@@ -523,7 +568,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   p.lv_nc = (int32_t)ctx->lv_cols.size();
   p.bc1 = ctx->bc;
   p.bc2 = ctx->bc ? ctx->bc + ctx->bc_len : nullptr;
-  p.delta_rel = delta_for(tensor, ctx->ldm);
+  p.delta_rel = delta_for(tensor || sep_tc, sep_tc ? ctx->ldr : ctx->ldm);
   p.colnorm_max = ctx->colnorm_max;
   p.a_inv_scale = 1.0 / (double)ctx->a_scale;
   p.sep = ctx->sep ? 1 : 0;
@@ -581,7 +626,7 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
   cl_stats stats{};
-  stats.corr_path = tensor ? 1 : gemv ? 3 : 0;
+  stats.corr_path = (tensor || sep_tc) ? 1 : gemv ? 3 : 0;
 
   // One outer iteration (clomp.cpp:235-274): counters reset, K1, K1c (with
   // exact fp64 rescoring of near-ties; fused into the learning kernel when
@@ -594,12 +639,26 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   auto enqueue_iteration = [&](int outer, int64_t* launches) {
     // (the active count is cleared by the learning kernel, see k_learn_warp)
     if (p.sep) {
-      launch_sep_corr(p, w, w.r64, w.scores, true, s);
-      launch_select(p, w, true, s);
-      const int bound = c->th >= 1.0 ? outer : (int)cap;
-      launch_learn(p, w, outer, bound, s);
-      launch_sep_resid(p, w, outer, bound, s);
-      *launches += 3 + 2 + (cap > 8 ? 2 : 1) + 3;
+      if (sep_tc) {
+        enq_ok &= launch_sep_corr_tc(p, w, s);
+        launch_select(p, w, false, s);
+        *launches += 2;  // + the row split and the record index fix-up
+      } else {
+        launch_sep_corr(p, w, w.r64, w.scores, true, s);
+        launch_select(p, w, true, s);
+      }
+      const int bound = c->th >= 1.0 ? (int)std::min<int64_t>(cap, outer + kTieSlack) : (int)cap;
+      if (dfrom > 0 && outer >= dfrom) {
+        SolveParams pd = p;
+        pd.direct = 1;
+        *launches += launch_sep_direct_learn(pd, w, outer, bound, s);
+        launch_sep_resid(pd, w, outer, bound, s);
+        *launches += 3 + 2 + 3;
+      } else {
+        launch_learn(p, w, outer, c->th >= 1.0 ? outer : (int)cap, s);
+        launch_sep_resid(p, w, outer, bound, s);
+        *launches += 3 + 2 + (cap > 8 ? 2 : 1) + 3;
+      }
       if (mode == CL_MODE_JOINT) {
         launch_joint_control(p, w, outer, false, s);
         launch_joint_snapshot(p, w, s);
@@ -798,7 +857,13 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     }
     const int nchunks = (p.max_outer + kChunkIters - 1) / kChunkIters;
     if ((int)ctx->graphs.size() < nchunks) ctx->graphs.resize((size_t)nchunks, nullptr);
+    // chunks whose iterations learn in direct form launch ~4 kernels per epoch:
+    // they are enqueued directly (like the NCCL chunks), not captured
+    auto chunk_direct = [&](int ch) {
+      return dfrom > 0 && std::min(p.max_outer, (ch + 1) * kChunkIters) >= dfrom;
+    };
     for (int ch = 0; ch < nchunks && !colshard; ++ch) {
+      if (chunk_direct(ch)) continue;
       if (!ctx->graphs[(size_t)ch]) {
         const int o0 = ch * kChunkIters + 1;
         const int o1 = std::min(p.max_outer, o0 + kChunkIters - 1);
@@ -822,12 +887,13 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     int64_t per_iter = 0;
     enqueue_count(p, c, mode, cap, &per_iter);
     for (int ch = 0; ch < nchunks; ++ch) {
-      if (colshard) {  // NCCL inside: enqueue directly (not captured)
+      if (colshard || chunk_direct(ch)) {  // NCCL / direct-form epochs inside: not captured
         const int o0 = ch * kChunkIters + 1;
         const int o1c = std::min(p.max_outer, o0 + kChunkIters - 1);
         int64_t dummy = 0;
         for (int o = o0; o <= o1c; ++o) enqueue_iteration(o, &dummy);
-        if (!enq_ok) return fail(ctx, CL_ERR_CUDA, "clomp: column-shard launch or collective failed");
+        if (!enq_ok) return fail(ctx, CL_ERR_CUDA, "clomp: launch or collective failed");
+        if (!colshard) launches += dummy - per_iter * (o1c - o0 + 1);  // counted below at per_iter
         cudaMemcpyAsync(ctx->h_chunk + (ch & 1) * kNumCounters, w.counters,
                         kNumCounters * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
       } else {
@@ -1069,7 +1135,9 @@ cl_ctx* cl_create_sep(int device, const float* a_r, int64_t m_r, int64_t n_r,
   ctx->ldr = (m_r + 127) / 128 * 128;
   ctx->ldc = (m_c + 127) / 128 * 128;
   ctx->sms = prop.multiProcessorCount;
-  ctx->tc_ok = false;
+  // stage 2 of the correlation (A_r^T U) runs on the K1 kernel when its 256-atom
+  // tiles line up with the coefficient columns
+  ctx->tc_ok = corr_tc_available() && n_r % corr_tc_tile_atoms() == 0;
   auto atom_major = [&](const float* a, int64_t m, int64_t n, int64_t ld,
                         std::vector<float>& f, std::vector<double>& d, double& cmax) {
     f.assign((size_t)(n * ld), 0.f);
@@ -1107,6 +1175,15 @@ cl_ctx* cl_create_sep(int device, const float* a_r, int64_t m_r, int64_t n_r,
        cudaMallocHost(&ctx->h_chunk, 2 * kNumCounters * sizeof(int32_t)) == cudaSuccess &&
        cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming) == cudaSuccess &&
        cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming) == cudaSuccess;
+  if (ok && ctx->tc_ok) {  // fp16 split of A_r (the K1 dictionary operand)
+    ok = cudaMalloc(&ctx->at_hi, fr.size() * sizeof(__half)) == cudaSuccess &&
+         cudaMalloc(&ctx->at_lo, fr.size() * sizeof(__half)) == cudaSuccess;
+    if (ok) {
+      ctx->a_scale = split_scale(cr * cr);
+      launch_split_dict(ctx->at_r32, ctx->at_hi, ctx->at_lo, (int64_t)fr.size(), ctx->a_scale,
+                        ctx->stream);
+    }
+  }
   if (ok) {
     // Factor Grams in fp64 on the device (k_gram.cu): Gr = A_r^T A_r, Gc = A_c^T A_c.
     launch_gram_full(ctx->at_r32, n_r, ctx->ldr, ctx->gr, ctx->stream);
@@ -1301,6 +1378,14 @@ int cl_set_synthesis(cl_ctx* ctx, int on) {
   if (ctx->slot_inflight != 0)
     return fail(ctx, CL_ERR_CONFIG, "cl_set_synthesis: batches are in flight");
   ctx->want_xhat = on != 0;
+  return CL_OK;
+}
+
+int cl_set_direct_form(cl_ctx* ctx, int from_outer) {
+  if (!ctx) return CL_ERR_INTERNAL;
+  if (!ctx->sep)
+    return fail(ctx, CL_ERR_UNSUPPORTED, "cl_set_direct_form: separable contexts only");
+  ctx->direct_mode = from_outer < 0 ? -1 : from_outer;
   return CL_OK;
 }
 
@@ -1734,6 +1819,10 @@ int cl_inject_support(cl_ctx* ctx, const double* r, int64_t batch, double th,
 }
 
 int cl_debug_cluster_trace(unsigned long long* out) { return cluster_trace(out); }
+
+int cl_debug_learn_trace(unsigned long long* out, int max_signals) {
+  return learn_trace(out, max_signals);
+}
 
 int cl_debug_k1_trace(unsigned long long* out, int max_ctas) {
   return corr_tc_trace(out, max_ctas);

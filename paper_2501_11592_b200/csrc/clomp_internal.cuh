@@ -145,6 +145,8 @@ struct SolveParams {
   // separable 2D operator A = A_c (x) A_r (atom p = i + nr*j, row q = qr + mr*qc)
   int32_t sep;
   int64_t nr, nc, mr, mc, ldr, ldc;
+  // separable contexts: this iteration learns in direct form (k_sep.cu)
+  int32_t direct;
   // th == 1 selection runs inside the learning kernel (warp per signal)
   int32_t fuse_select;
   double a_inv_scale;       // 1 / (power-of-two scale of the fp16 dictionary split)
@@ -190,6 +192,17 @@ struct Work {
   double* zb = nullptr;            // [B][n] A_r^T Y A_c (b values of every atom)
   double* sep_scratch = nullptr;   // [B][nc][mr] U = R A_c  /  V = A_r C
   double* lpart = nullptr;         // [B][tiles] residual sum-of-squares partials
+  // separable correlation on the tensor cores: stage 2 (A_r^T U) is the K1
+  // kernel on B nc pseudo-signals (the rows U_b[j][:] of U = R A_c)
+  __half* u_hi = nullptr;          // [B nc][ldr] scaled fp16 split of U
+  __half* u_lo = nullptr;
+  float* u_scale = nullptr;        // [B nc] 1 / scale
+  int32_t* u_active = nullptr;     // [B nc] the image's active flag per row
+  // direct-form learning (large supports): second scratch for U = R A_c and the
+  // support sorted by coefficient column
+  double* sep_scratch2 = nullptr;  // [B][nc][mr]
+  int32_t* csc_ptr = nullptr;      // [B][nc + 1]
+  int32_t* csc_perm = nullptr;     // [B][cap] support entries by column
   Cand* xg = nullptr;            // column sharding: per-shard candidates [W][B][ntl]
   Cand* cand = nullptr;          // correlation candidates [B][ntile]
   double* scores = nullptr;      // [B][n] |A^T r| (th < 1 path)
@@ -310,6 +323,7 @@ void launch_corr_gemv(const SolveParams& p, const Work& w, bool full_scores,
 bool corr_tc_available();
 int corr_tc_trace(unsigned long long* out, int max_ctas);
 int cluster_trace(unsigned long long* out);
+int learn_trace(unsigned long long* out, int max_signals);
 int64_t corr_tc_tile_atoms();
 // false: the tensor maps could not be encoded or the launch failed (the
 // caller reports CL_ERR_CUDA; stale candidate records are never consumed).
@@ -324,8 +338,16 @@ void launch_split_resid(const SolveParams& p, const Work& w, cudaStream_t s);
 // ---- launchers (k_sep.cu) ----
 void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
                      double* dst, bool abs_scores, cudaStream_t s);
+// Tensor-core variant (th == 1, nr a multiple of the K1 atom tile): stage 1 in
+// fp64, its rows split to fp16, stage 2 = K1 with the fused candidate
+// records (global atom indices); false when a launch could not be enqueued.
+bool launch_sep_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s);
 void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
                       cudaStream_t s);
+// All epochs of one outer iteration in direct form (no support Gram matrix);
+// bound: upper bound on the support sizes.  Returns the kernels launched.
+int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int bound,
+                            cudaStream_t s);
 int64_t sep_resid_tiles(const SolveParams& p);
 
 // ---- launchers (k_gram.cu) ----
@@ -336,6 +358,26 @@ void launch_gram_full(const float* at, int64_t n, int64_t ldm, double* g,
 // sm_100a (tools/micro/cvt.cu: ~61 conversions per SM-cycle); integer
 // bit-assembly with special-case selects measured 10x slower.
 __device__ __forceinline__ double f2d(float f) { return (double)f; }
+
+// ---- optimizer steps (gradient_step, clomp.cpp:171-209), shared by k_solve.cu / k_sep.cu
+template <int OPT>
+__device__ __forceinline__ void opt_step(double& c, double g, double& m1,
+                                         double& m2, double lr, double bc1,
+                                         double bc2) {
+  if (OPT == 0) {  // plain: s -= lr * g (clomp.cpp:178-181)
+    c = __dsub_rn(c, __dmul_rn(lr, g));
+  } else if (OPT == 1) {  // momentum (clomp.cpp:182-188)
+    m1 = __dadd_rn(__dmul_rn(0.9, m1), g);
+    c = __dsub_rn(c, __dmul_rn(lr, m1));
+  } else {  // Adam (clomp.cpp:189-206)
+    const double b1 = 0.9, b2 = 0.999, tiny = 1e-8;
+    m1 = __dadd_rn(__dmul_rn(b1, m1), __dmul_rn(1.0 - b1, g));
+    m2 = __dadd_rn(__dmul_rn(b2, m2), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+    const double mhat = __ddiv_rn(m1, bc1);
+    const double vhat = __ddiv_rn(m2, bc2);
+    c = __dsub_rn(c, __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(sqrt(vhat), tiny)));
+  }
+}
 
 // ---- launchers (k_solve.cu) ----
 void launch_init(const SolveParams& p, const Work& w, const float* y_in,

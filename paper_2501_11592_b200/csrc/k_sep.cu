@@ -39,75 +39,116 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(256) k_gemm_sep(Gemm g) {
+// 64 x 64 output tile per CTA on the fp64 tensor cores (mma.sync m8n8k4 f64 ->
+// DMMA): four warps, each a 32 x 32 quadrant as 4 x 4 accumulator blocks of
+// 8 x 8.  K runs in 16-wide chunks through two shared-memory buffers; the next
+// chunk's global loads are issued into registers before the current chunk's
+// MMAs and stored after them, so the ~1 us load latency hides under ~64 DMMAs
+// per warp (the SIMT 4 x 4 register tile this replaces waited for every chunk
+// and ran at a fifth of the pipe with the 1-2 CTAs per SM these shapes give).
+// Operands with arbitrary strides; tiles are staged as Ps[k][x] with row stride
+// 68 doubles, for which the A / B fragment reads (lane -> k = lane % 4,
+// x = lane / 4) hit 16 distinct 8-byte slots per half warp: conflict-free.
+constexpr int GLD = GT + 4;
+constexpr int kGemmThreads = 128;
+
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
   const int64_t b = blockIdx.y;
   if (g.active && !g.active[b]) return;
-  __shared__ double Ps[GK][GT + 2];
-  __shared__ double Qs[GK][GT + 2];
-  __shared__ double red[8];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  __shared__ __align__(16) double Ps[2][GK][GLD];
+  __shared__ __align__(16) double Qs[2][GK][GLD];
+  __shared__ double red[kGemmThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wx = (warp & 1) * 32, wy = (warp >> 1) * 32;  // quadrant origin (x, y)
   const int64_t tiles_x = (g.X + GT - 1) / GT;
   const int64_t x0 = (blockIdx.x % tiles_x) * GT, y0 = (blockIdx.x / tiles_x) * GT;
   const double* P = g.P + b * g.psb;
   const double* Q = g.Q + b * g.qsb;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
   const bool p_kfast = g.psk == 1, q_kfast = g.qsk == 1;
-  for (int64_t k0 = 0; k0 < g.K; k0 += GK) {
+  constexpr int PER = GT * GK / kGemmThreads;  // 8 elements of each operand per thread
+  double pv[PER], qv[PER];
+  auto fetch = [&](int64_t k0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + 256 * u;
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + kGemmThreads * u;
       const int xx = p_kfast ? e / GK : e % GT, kk = p_kfast ? e % GK : e / GT;
       const int64_t x = x0 + xx, k = k0 + kk;
-      Ps[kk][xx] = (x < g.X && k < g.K) ? P[x * g.psx + k * g.psk] : 0.0;
+      pv[u] = (x < g.X && k < g.K) ? P[x * g.psx + k * g.psk] : 0.0;
       const int yy = q_kfast ? e / GK : e % GT, kq = q_kfast ? e % GK : e / GT;
-      const int64_t y = y0 + yy, kq2 = k0 + kq;
-      Qs[kq][yy] = (y < g.Y && kq2 < g.K) ? Q[y * g.qsy + kq2 * g.qsk] : 0.0;
+      const int64_t y = y0 + yy, k2 = k0 + kq;
+      qv[u] = (y < g.Y && k2 < g.K) ? Q[y * g.qsy + k2 * g.qsk] : 0.0;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int k = 0; k < GK; ++k) {
-      double a[4], c[4];
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + kGemmThreads * u;
+      const int xx = p_kfast ? e / GK : e % GT, kk = p_kfast ? e % GK : e / GT;
+      Ps[buf][kk][xx] = pv[u];
+      const int yy = q_kfast ? e / GK : e % GT, kq = q_kfast ? e % GK : e / GT;
+      Qs[buf][kq][yy] = qv[u];
+    }
+  };
+  double acc[4][4][2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = Ps[k][ty * 4 + q];
-        c[q] = Qs[k][tx * 4 + q];
-      }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int fk = lane & 3, fr = lane >> 2;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += GK, buf ^= 1) {
+    const bool more = k0 + GK < g.K;
+    if (more) fetch(k0 + GK);
+#pragma unroll
+    for (int ks = 0; ks < GK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ps[buf][ks + fk][wx + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Qs[buf][ks + fk][wy + 8 * j + fr];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], c[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+              : "d"(af[i]), "d"(bf[j]));
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
   }
+  // accumulator block (i, j): element (row = fr, cols 2 fk, 2 fk + 1)
   double* C = g.C + b * g.csb;
   double ss = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t x = x0 + ty * 4 + i, y = y0 + tx * 4 + j;
-      if (x >= g.X || y >= g.Y) continue;
-      const int64_t o = x * g.csx + y * g.csy;
-      double v = acc[i][j];
-      if (g.mode == 1) {
-        v = fabs(v);
-      } else if (g.mode == 2) {
-        v -= g.yref[b * g.csb + o];
-        ss = fma(v, v, ss);
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t x = x0 + wx + 8 * i + fr, y = y0 + wy + 8 * j + 2 * fk + h;
+        if (x >= g.X || y >= g.Y) continue;
+        const int64_t o = x * g.csx + y * g.csy;
+        double v = acc[i][j][h];
+        if (g.mode == 1) {
+          v = fabs(v);
+        } else if (g.mode == 2) {
+          v -= g.yref[b * g.csb + o];
+          ss = fma(v, v, ss);
+        }
+        C[o] = v;
       }
-      C[o] = v;
-    }
   if (g.mode == 2) {
     ss = warp_sum_d(ss);
-    if ((tid & 31) == 0) red[tid >> 5] = ss;
+    if (lane == 0) red[warp] = ss;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int q = 0; q < 8; ++q) t += red[q];
+      for (int q = 0; q < kGemmThreads / 32; ++q) t += red[q];
       g.lpart[b * g.tiles + blockIdx.x] = t;
     }
   }
@@ -131,11 +172,192 @@ __global__ void __launch_bounds__(256) k_sep_scatter(SolveParams p, Work w) {
   }
 }
 
+// Rows of U (one per image b and coefficient column j, mr doubles) to the K1
+// residual operand: per-row power-of-two scale from the row norm, fp16 hi / lo
+// halves (zero padded to ldr), and the image's active flag per row.  One warp
+// per row.
+__global__ void __launch_bounds__(256) k_sep_split_u(SolveParams p, Work w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= p.B * p.nc) return;
+  const int64_t b = row / p.nc;
+  const int act = w.active[b];
+  if (lane == 0) w.u_active[row] = act;
+  if (!act) return;
+  const double* u = w.sep_scratch + row * p.mr;
+  double ss = 0.0;
+  for (int64_t q = lane; q < p.mr; q += 32) ss = fma(u[q], u[q], ss);
+  ss = warp_sum_d(ss);
+  const float sc = split_scale(ss);
+  if (lane == 0) w.u_scale[row] = 1.0f / sc;
+  for (int64_t q = lane; q < p.ldr; q += 32) {
+    __half h = __float2half_rn(0.f), l = h;
+    if (q < p.mr) split_f16(u[q], sc, h, l);
+    w.u_hi[row * p.ldr + q] = h;
+    w.u_lo[row * p.ldr + q] = l;
+  }
+}
+
+// K1 wrote atom indices local to its pseudo-signal (i in [0, nr)); record
+// (b, tile) belongs to coefficient column j = tile / (nr / tile_atoms), so the
+// global atom is i + nr j.
+__global__ void k_sep_fix_cand(SolveParams p, Work w) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.B * p.ntile) return;
+  const int64_t tile = e % p.ntile;
+  const int32_t base = (int32_t)((tile / (p.nr / p.tile_atoms)) * p.nr);
+  Cand c = w.cand[e];
+  if (c.i1 != 0x7fffffff) c.i1 += base;
+  if (c.i2 != 0x7fffffff) c.i2 += base;
+  w.cand[e] = c;
+}
+
+// ------------------------------------------------ direct-form learning
+// Supports too large for the Gram form (G is t x t fp64 per image: 1.4 GB at
+// config 5's K = 13107) or past the point where streaming G costs more than
+// applying the operator (t^2 > ~ mr nc mc / 8) learn with the reference's own
+// epoch (clomp.cpp:83-91, 120-123, 171-209) applied through the factors:
+//   V = A_r C        sparse: per coefficient column j, sum_k c_k a_r,i_k
+//   R = V A_c^T - Y  dense fp64 GEMM (mr x nc x mc)
+//   U = R A_c        dense fp64 GEMM (mr x mc x nc)
+//   g_k = 2 a_r,i_k . U_j_k   for the t support entries only, optimizer step
+// The support is kept column-sorted (CSC) so V needs no atomics and its
+// summation order is fixed.
+
+// One block per image: zero the coefficients of the atoms selected since the
+// last call (clomp.hpp:53-54), then sort the support by coefficient column
+// (stable: insertion order inside a column).
+__global__ void __launch_bounds__(256) k_dir_csc(SolveParams p, Work w) {
+  extern __shared__ int32_t s_cnt[];  // [nc + 1]
+  const int64_t b = blockIdx.x;
+  if (!w.active[b]) return;
+  const int t = w.cnt[b], t0 = w.gcnt[b];
+  const int tid = threadIdx.x;
+  for (int k = t0 + tid; k < t; k += blockDim.x) {
+    w.coef[b * p.cap + k] = 0.0;
+    w.mom1[b * p.cap + k] = 0.0;
+    w.mom2[b * p.cap + k] = 0.0;
+  }
+  for (int64_t j = tid; j <= p.nc; j += blockDim.x) s_cnt[j] = 0;
+  __syncthreads();
+  const int32_t* sup = w.sup + b * p.cap;
+  for (int k = tid; k < t; k += blockDim.x) atomicAdd(&s_cnt[sup[k] / p.nr + 1], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int64_t j = 0; j <= p.nc; ++j) {
+      run += s_cnt[j];
+      s_cnt[j] = run;
+    }
+  }
+  __syncthreads();
+  int32_t* ptr = w.csc_ptr + b * (p.nc + 1);
+  for (int64_t j = tid; j <= p.nc; j += blockDim.x) ptr[j] = s_cnt[j];
+  // column j's entries in insertion order: one thread per column scans the
+  // support (t <= a few thousand per image; once per outer iteration)
+  int32_t* perm = w.csc_perm + b * p.cap;
+  for (int64_t j = tid; j < p.nc; j += blockDim.x) {
+    int pos = s_cnt[j];
+    const int end = s_cnt[j + 1];
+    for (int k = 0; k < t && pos < end; ++k)
+      if (sup[k] / p.nr == j) perm[pos++] = k;
+  }
+  if (tid == 0) w.gcnt[b] = t;
+}
+
+// One epoch's sparse half, one WARP per coefficient column j of image b (the
+// entries of a column share U_j and V_j and nothing else): with STEP, every
+// entry's gradient g_k = 2 a_r,i_k . U_j and gradient_step on c_k (the lanes
+// update the column's entries in parallel); then V_b^T[j][:] = sum over the
+// column's entries of c_k a_r,i_k with the new coefficients, which the next
+// epoch's residual GEMM (or the iteration's final residual) reads.  Entries in
+// chunks of 32 (one per lane), rows in chunks of 32 kDirRows per lane.
+constexpr int kDirWarps = 8;
+constexpr int kDirRows = 8;  // rows per lane per pass (256-row passes)
+
+template <int OPT, bool STEP>
+__global__ void __launch_bounds__(32 * kDirWarps) k_dir_colstep(SolveParams p, Work w,
+                                                               const double* __restrict__ u,
+                                                               double* __restrict__ vt, int step) {
+  const int64_t b = blockIdx.y;
+  if (!w.active[b]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kDirWarps + warp;
+  if (j >= p.nc) return;
+  const int32_t* ptr = w.csc_ptr + b * (p.nc + 1);
+  const int e0 = ptr[j], e1 = ptr[j + 1];
+  const int32_t* perm = w.csc_perm + b * p.cap;
+  const int32_t* sup = w.sup + b * p.cap;
+  double* coef = w.coef + b * p.cap;
+  const double* uj = u + (b * p.nc + j) * p.mr;
+  double* out = vt + (b * p.nc + j) * p.mr;
+  for (int64_t q0 = 0; q0 < p.mr; q0 += 32 * kDirRows) {
+    double vacc[kDirRows];
+#pragma unroll
+    for (int r = 0; r < kDirRows; ++r) vacc[r] = 0.0;
+    for (int ec = e0; ec < e1; ec += 32) {
+      const int ne = min(32, e1 - ec);
+      int k_l = 0;
+      int64_t row_l = 0;
+      double c_l = 0.0;
+      if (lane < ne) {
+        k_l = perm[ec + lane];
+        row_l = (int64_t)(sup[k_l] % p.nr) * p.ldr;
+        c_l = coef[k_l];
+      }
+      if (STEP && q0 == 0) {  // gradients of this chunk's entries (full-length dots)
+        double g_l = 0.0;
+        for (int idx = 0; idx < ne; ++idx) {
+          const double* ar = w.at_r64 + __shfl_sync(0xffffffffu, row_l, idx);
+          double acc = 0.0;
+          for (int64_t q = lane; q < p.mr; q += 32) acc = fma(ar[q], uj[q], acc);
+          acc = warp_sum_d(acc);
+          if (lane == idx) g_l = acc;
+        }
+        if (lane < ne) {
+          const int64_t o = b * p.cap + k_l;
+          double m1 = 0.0, m2 = 0.0, bc1 = 1.0, bc2 = 1.0;
+          if (OPT != 0) {
+            m1 = w.mom1[o];
+            m2 = w.mom2[o];
+          }
+          if (OPT == 2) {
+            bc1 = p.bc1[step];
+            bc2 = p.bc2[step];
+          }
+          opt_step<OPT>(c_l, 2.0 * g_l, m1, m2, p.lr, bc1, bc2);
+          coef[k_l] = c_l;
+          if (OPT != 0) {
+            w.mom1[o] = m1;
+            w.mom2[o] = m2;
+          }
+        }
+      }
+      for (int idx = 0; idx < ne; ++idx) {
+        const double* ar = w.at_r64 + __shfl_sync(0xffffffffu, row_l, idx);
+        const double c = __shfl_sync(0xffffffffu, c_l, idx);
+#pragma unroll
+        for (int r = 0; r < kDirRows; ++r) {
+          const int64_t q = q0 + lane + 32 * r;
+          if (q < p.mr) vacc[r] = fma(c, ar[q], vacc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kDirRows; ++r) {
+      const int64_t q = q0 + lane + 32 * r;
+      if (q < p.mr) out[q] = vacc[r];
+    }
+  }
+}
+
 unsigned tiles2(int64_t X, int64_t Y) {
   return (unsigned)(((X + GT - 1) / GT) * ((Y + GT - 1) / GT));
 }
 
 }  // namespace
+
+void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
 
 // dst_b = A_r^T Src_b A_c (vec'd), Src_b = vec(r_src_b) with leading dim ldm.
 // abs_scores: |.| into the full-score buffer; else signed (Z = A_r^T Y A_c).
@@ -160,7 +382,7 @@ void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
   g1.K = p.mc;
   g1.mode = 0;
   g1.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), 256, 0, s>>>(g1);
+  k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
   // stage 2: S_b[i][j] = sum_qr A_r[qr][i] U_b[j][qr], stored at p = i + nr*j
   Gemm g2{};
   g2.P = w.at_r64;
@@ -180,17 +402,133 @@ void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
   g2.K = p.mr;
   g2.mode = abs_scores ? 1 : 0;
   g2.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g2.X, g2.Y), (unsigned)p.B), 256, 0, s>>>(g2);
+  k_gemm_sep<<<dim3(tiles2(g2.X, g2.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g2);
+}
+
+bool launch_sep_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
+  // stage 1 (fp64): U_b[j][qr] = sum_qc A_c[qc][j] R_b[qr][qc]
+  Gemm g1{};
+  g1.P = w.at_c64;
+  g1.psx = p.ldc;
+  g1.psk = 1;
+  g1.psb = 0;
+  g1.Q = w.r64;
+  g1.qsy = 1;
+  g1.qsk = p.mr;
+  g1.qsb = p.ldm;
+  g1.C = w.sep_scratch;
+  g1.csx = p.mr;
+  g1.csy = 1;
+  g1.csb = p.nc * p.mr;
+  g1.X = p.nc;
+  g1.Y = p.mr;
+  g1.K = p.mc;
+  g1.mode = 0;
+  g1.active = w.active;
+  k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
+  const int64_t rows = p.B * p.nc;
+  k_sep_split_u<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(p, w);
+  // stage 2 on tcgen05: scores(i, j) = a_r,i . U_j for every row as its own
+  // "signal" against the dictionary A_r; the epilogue keeps the candidate
+  // records per (row, 256-atom tile), which is the image's (b, tile) layout.
+  SolveParams q = p;
+  q.B = rows;
+  q.ldm = p.ldr;
+  q.m = p.mr;
+  q.n = p.nr;
+  q.n_corr = p.nr;
+  q.atom0 = 0;
+  q.ntile = p.nr / p.tile_atoms;
+  q.ntl = q.ntile;
+  Work v = w;
+  v.r_hi = w.u_hi;
+  v.r_lo = w.u_lo;
+  v.r_scale = w.u_scale;
+  v.active = w.u_active;
+  if (!launch_corr_tc(q, v, s)) return false;
+  const int64_t recs = p.B * p.ntile;
+  k_sep_fix_cand<<<(unsigned)((recs + 255) / 256), 256, 0, s>>>(p, w);
+  return true;
+}
+
+// R = V A_c^T - Y from V^T in `vt` (mode 2: also the loss partials).
+static void launch_dir_resid_gemm(const SolveParams& p, const Work& w, const double* vt,
+                                  cudaStream_t s) {
+  Gemm g{};
+  g.P = vt;  // VT[j][qr]
+  g.psx = 1;
+  g.psk = p.mr;
+  g.psb = p.nc * p.mr;
+  g.Q = w.at_c64;  // A_c[qc][j] = at_c64[j][qc]
+  g.qsy = 1;
+  g.qsk = p.ldc;
+  g.qsb = 0;
+  g.C = w.r64;
+  g.csx = 1;
+  g.csy = p.mr;
+  g.csb = p.ldm;
+  g.X = p.mr;
+  g.Y = p.mc;
+  g.K = p.nc;
+  g.mode = 2;
+  g.yref = w.y64;
+  g.lpart = w.lpart;
+  g.tiles = tiles2(p.mr, p.mc);
+  g.active = w.active;
+  k_gemm_sep<<<dim3(tiles2(g.X, g.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g);
+}
+
+int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int bound,
+                            cudaStream_t s) {
+  (void)bound;
+  k_dir_csc<<<(unsigned)p.B, 256, (size_t)(p.nc + 1) * sizeof(int32_t), s>>>(p, w);
+  const dim3 cgrid((unsigned)((p.nc + kDirWarps - 1) / kDirWarps), (unsigned)p.B);
+  double* vt = w.sep_scratch;
+  double* u = w.sep_scratch2;
+  k_dir_colstep<0, false><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, 0);  // V of the current c
+  for (int e = 0; e < p.inner; ++e) {
+    launch_dir_resid_gemm(p, w, vt, s);
+    // U_b[j][qr] = sum_qc A_c[qc][j] R_b[qr][qc]
+    Gemm g1{};
+    g1.P = w.at_c64;
+    g1.psx = p.ldc;
+    g1.psk = 1;
+    g1.psb = 0;
+    g1.Q = w.r64;
+    g1.qsy = 1;
+    g1.qsk = p.mr;
+    g1.qsb = p.ldm;
+    g1.C = u;
+    g1.csx = p.mr;
+    g1.csy = 1;
+    g1.csb = p.nc * p.mr;
+    g1.X = p.nc;
+    g1.Y = p.mr;
+    g1.K = p.mc;
+    g1.mode = 0;
+    g1.active = w.active;
+    k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
+    const int step = (outer - 1) * p.inner + e;
+    switch (p.opt) {  // the step and the next V in one pass over the columns
+      case 0: k_dir_colstep<0, true><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, step); break;
+      case 1: k_dir_colstep<1, true><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, step); break;
+      default: k_dir_colstep<2, true><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, step); break;
+    }
+  }
+  return 2 + 3 * p.inner;
 }
 
 int64_t sep_resid_tiles(const SolveParams& p) { return tiles2(p.mr, p.mc); }
-
-void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
 
 // r_b = vec(A_r C_b A_c^T) - y_b, its tf32 split, ||r_b||^2, stopping rules.
 void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
                       cudaStream_t s) {
   (void)tb;
+  if (p.direct && w.csc_ptr) {  // V of the learned coefficients is in sep_scratch already
+    launch_dir_resid_gemm(p, w, w.sep_scratch, s);
+    launch_sep_control(p, w, outer, s);
+    return;
+  }
   k_sep_scatter<<<(unsigned)p.B, 256, 0, s>>>(p, w);
   Gemm g{};
   g.P = w.sep_scratch;  // VT[j][qr]
@@ -213,7 +551,7 @@ void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
   g.lpart = w.lpart;
   g.tiles = sep_resid_tiles(p);
   g.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g.X, g.Y), (unsigned)p.B), 256, 0, s>>>(g);
+  k_gemm_sep<<<dim3(tiles2(g.X, g.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g);
   launch_sep_control(p, w, outer, s);
 }
 

@@ -145,6 +145,24 @@ __device__ __forceinline__ void exact_scores8(const SolveParams& p, const Work& 
   double acc[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  if (p.sep) {
+    // Separable atom (i, j): a_r,i^T R a_c,j = a_r,i . U_j with U = R A_c in fp64
+    // (stage 1 of this iteration's correlation, still in sep_scratch).
+    const int64_t b = (r - w.r64) / p.ldm;
+    const double* U = w.sep_scratch + b * p.nc * p.mr;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (u < cnt) {
+        const int64_t atom = j0 + u, ia = atom % p.nr, ja = atom / p.nr;
+        const double* ar = w.at_r64 + ia * p.ldr;
+        const double* uj = U + ja * p.mr;
+        for (int64_t q = lane; q < p.mr; q += 32) acc[u] = fma(ar[q], uj[q], acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) out[u] = u < cnt ? fabs(warp_sum(acc[u])) : -1.0;
+    return;
+  }
 #pragma unroll 2
   for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
     const double2 r01 = *reinterpret_cast<const double2*>(r + i);
@@ -448,26 +466,6 @@ __device__ __forceinline__ bool control_signal(const SolveParams& p, const Work&
 __device__ __forceinline__ bool control_signal(const SolveParams& p, const Work& w, int64_t b,
                                                int outer, double L) {
   return control_signal(p, w, b, outer, L, load_ctl(w, b), L);
-}
-
-// ----------------------------------------------------- optimizer steps
-template <int OPT>
-__device__ __forceinline__ void opt_step(double& c, double g, double& m1,
-                                         double& m2, double lr, double bc1,
-                                         double bc2) {
-  if (OPT == 0) {  // plain: s -= lr * g (clomp.cpp:178-181)
-    c = __dsub_rn(c, __dmul_rn(lr, g));
-  } else if (OPT == 1) {  // momentum (clomp.cpp:182-188)
-    m1 = __dadd_rn(__dmul_rn(0.9, m1), g);
-    c = __dsub_rn(c, __dmul_rn(lr, m1));
-  } else {  // Adam (clomp.cpp:189-206)
-    const double b1 = 0.9, b2 = 0.999, tiny = 1e-8;
-    m1 = __dadd_rn(__dmul_rn(b1, m1), __dmul_rn(1.0 - b1, g));
-    m2 = __dadd_rn(__dmul_rn(b2, m2), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
-    const double mhat = __ddiv_rn(m1, bc1);
-    const double vhat = __ddiv_rn(m2, bc2);
-    c = __dsub_rn(c, __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(sqrt(vhat), tiny)));
-  }
 }
 
 // ------------------------------------------ learning, warp per signal
@@ -1083,12 +1081,30 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
 // works on registers (support membership by ballot instead of the mask), the
 // new Gram row comes from gfull and b_k = a_k . y (round trip 2), and the
 // epochs start with everything in registers / shared memory.
+#ifdef CL_LEARN_TRACE
+// Debug (CL_NVCC_EXTRA=-DCL_LEARN_TRACE): per-signal phase timestamps of the
+// last k_learn_fast launch: globaltimer at entry, clock64 at entry / after the
+// state loads + record merge / selection / Gram extension / staged rows /
+// epochs / residual + control.
+__device__ unsigned long long g_lt[8192][8];
+__device__ __forceinline__ unsigned long long lt_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LT_MARK(i) do { if (lane == 0 && b < 8192) g_lt[b][i] = (i) == 0 ? lt_gtimer() : (unsigned long long)clock64(); } while (0)
+#else
+#define LT_MARK(i) do { } while (0)
+#endif
+
 template <int TB, int OPT>
 __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, int64_t b,
                                            int outer, int32_t* big_list, double* cs,
                                            int32_t* sups, double* s1, uint64_t* bar, int lane) {
   const int64_t cap = p.cap;  // >= 32
   constexpr int LDS = TB + 4;
+  LT_MARK(0);
+  LT_MARK(1);
   // round trip 1: all independent loads (garbage beyond cnt is never used)
   const int act = w.active[b];
   const int t_old = w.cnt[b];
@@ -1117,6 +1133,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   double v1, v2;
   int i1;
   cand_merge_warp(p, w, b, first, v1, i1, v2, lane);
+  LT_MARK(2);
   int t = t_old;
   int chg = 0;  // mask changed this iteration (stall rule)
   if (t_old >= 32) {  // support wider than the warp: mask-based general path
@@ -1174,6 +1191,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
     return true;  // k_learn_block finishes it (and counts it for K1)
   }
 
+  LT_MARK(3);
   // round trip 2: Gram row / column of the new atoms from gfull, b_k = a_k . y
   double* G = w.gram + b * cap * cap;
   const float* y = w.y32 + b * p.ldm;  // fp32 data, exact in fp64
@@ -1207,9 +1225,12 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
     if (lane == 0) w.bvec[b * cap + k] = accb;
   }
   if (lane == 0) w.gcnt[b] = t;
+  LT_MARK(4);
   mbar_wait0(bar);
   __syncwarp();
+  LT_MARK(5);
   const double c = learn_epochs<TB, OPT>(p, w, b, outer, cs, s1, lane, t, c_l, b_l, m1, m2);
+  LT_MARK(6);
 
   // residual r = A_S c - y, its fp16 split for the next K1, the loss and the
   // stopping rules (clomp.cpp:236-242, 253-273) in the same warp: the L2-bound
@@ -1236,6 +1257,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   }
   snap = __shfl_sync(kFull, snap, 0);
   if (snap && lane < t) w.best_coef[b * p.cap + lane] = c;
+  LT_MARK(7);
   return false;
 }
 
@@ -3183,6 +3205,18 @@ int launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     }
   }
   return extra;
+}
+
+int learn_trace(unsigned long long* out, int max_signals) {
+#ifdef CL_LEARN_TRACE
+  const int n = max_signals < 8192 ? max_signals : 8192;
+  cudaMemcpyFromSymbol(out, g_lt, (size_t)n * 8 * sizeof(unsigned long long));
+  return n;
+#else
+  (void)out;
+  (void)max_signals;
+  return 0;
+#endif
 }
 
 int cluster_trace(unsigned long long* out) {
