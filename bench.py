@@ -98,8 +98,9 @@ def workload(args, rank: int, world: int = 1):
         # strong scaling: the config's batch is the GLOBAL batch (config 5:
         # "batch 1024 sharded by image across 1/2/4/8 GPUs"); every rank draws
         # the same problem and solves its contiguous slice of the signals
-        per = -(-c["batch"] // world)
-        c["sig_lo"], c["sig_hi"] = min(rank * per, c["batch"]), min((rank + 1) * per, c["batch"])
+        from paper_2501_11592_b200.sharding import shard_range
+
+        c["sig_lo"], c["sig_hi"] = shard_range(c["batch"], rank, world)
     else:
         c["seed"] = c["seed"] + 1000 * rank  # weak scaling: each rank its own batch
     return c
@@ -427,6 +428,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(values, device, dist_on: bool):
+    """Element-wise maximum of per-rank timings (ms) over the process group
+    (NCCL on the GPUs, gloo in the CPU tests): the job is as slow as its
+    slowest rank."""
+    import torch
+
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist_on:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
+
+
+def job_throughput(c, batch_local: int, world: int, strong: bool, ms_max: float) -> float:
+    """Whole-job signals/s: all ranks' signals over the slowest rank's time."""
+    total = c["batch"] if strong else batch_local * world
+    return total / (ms_max / 1000.0)
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
@@ -509,13 +528,10 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop(t_region0, t_region1)
     times = [a.elapsed_time(b) for a, b in evs]
     ms = statistics.mean(times)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks([ms], dev, dist)[0]
     strong = args.colshard or args.scaling == "strong"
     total_signals = c["batch"] if strong else B * world
-    value = total_signals / (ms_max / 1000.0)
+    value = job_throughput(c, B, world, strong, ms_max)
 
     # Per-phase breakdown of one solve (profiling events, outside the timed region).
     prof = None
@@ -574,11 +590,9 @@ def run_ours(args, rank, world, local_rank):
         r = cl.clomp_wait(ctx)
         assert r.status.max() == 0
         pipe_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    te = torch.tensor([pipe_ms, blocking_ms], dtype=torch.float64, device=dev)
-    if dist:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = total_signals / (float(te[0].item()) / 1000.0)
-    e2e_blocking = total_signals / (float(te[1].item()) / 1000.0)
+    te = max_over_ranks([pipe_ms, blocking_ms], dev, dist)
+    e2e_val = total_signals / (te[0] / 1000.0)
+    e2e_blocking = total_signals / (te[1] / 1000.0)
 
     # One-off context cost (dictionary transpose + upload, fp16 split, A^T A).
     t0 = time.perf_counter()
@@ -632,14 +646,13 @@ def run_ours(args, rank, world, local_rank):
         if prof["corr_path"] == 1:
             # split fp16 (3 f16 MMAs per product, fp32 accumulation): the useful
             # rate is compared with the measured dense bf16/f16 peak / 3.
-            # K1 is timed inside a long step: the sustained figure applies.
-            dense = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+            # A K1 launch is ~20 us inside a ~2 ms step (config 2), far too
+            # short to heat the part: the burst figure applies.
+            dense = peaks.get("bf16_tflops", 1590.0)
             peak = dense / 3.0
             bound, punit = "tensor", "TFLOP/s (fp32-equivalent, 3 x f16 MMA)"
-            peak_src = ("MEASURED_PEAKS.json bf16_tflops_sustained (= dense f16 rate) / 3, derived"
-                        if "bf16_tflops_sustained" in peaks else
-                        "MEASURED_PEAKS.json bf16_tflops / 3" if "bf16_tflops" in peaks
-                        else "fallback 1590 TFLOP/s / 3")
+            peak_src = ("MEASURED_PEAKS.json bf16_tflops (burst dense bf16 = f16 rate) / 3, derived"
+                        if "bf16_tflops" in peaks else "fallback 1590 TFLOP/s / 3")
         else:
             clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
             peak = 148 * 64 * 2 * clk / 1e12
@@ -650,8 +663,9 @@ def run_ours(args, rank, world, local_rank):
             "kernel": "K1 correlation A^T R + top-2 epilogue (k_corr_tc)",
             "bound": bound, "achieved": achieved, "peak": peak, "unit": punit,
             "frac": achieved / peak,
-            "traffic": 10.54e6 if prof["corr_path"] == 1 and args.config == 2 else None,
-            "traffic_note": ("ncu dram__bytes_read+write per launch, profiles/r1_cfg2_ncu_full_summary.txt"
+            "traffic": 10.57e6 if prof["corr_path"] == 1 and args.config == 2 else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch (10.57 MB read, 0 written; "
+                             "algorithmic 10.49 MB), profiles/r2/r2_k1.summary.txt"
                              if prof["corr_path"] == 1 and args.config == 2 else None),
             "peak_source": peak_src,
             "algorithmic_per_launch": f"2*N*M*B = {corr_flops:.3e} FLOP",
@@ -683,18 +697,19 @@ def run_ours(args, rank, world, local_rank):
             "bound": "fp64", "achieved": learn_flops / (learn_ms / 1e3) / 1e12,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": learn_flops / (learn_ms / 1e3) / 1e12 / fp64_peak,
-            "traffic": 42.39e6 if args.config == 2 and prof["corr_path"] == 1 else None,
-            "traffic_note": ("ncu dram__bytes_read+write per launch of k_learn_fast<32,0> (the "
-                             "largest learning launch, t = 17..32: 41.1 MB read, 1.3 MB written; "
-                             "the support Gram / state rows and y, the residual halves stay in "
-                             "L2), profiles/r1_cfg2_ncu_full_summary_final.txt"),
+            "traffic": 53.96e6 if args.config == 2 and prof["corr_path"] == 1 else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch of k_learn_fast<32,0> at t = 30 "
+                             "(the largest learning launches, t = 17..32: 51.4 MB read, 2.5 MB "
+                             "written: the support Gram rows, per-signal state and y; the atom "
+                             "gathers of the residual are L2 hits), profiles/r2/r2_learn32.summary.txt"),
             "peak_source": "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x SM clock under load",
             "algorithmic_per_step": (f"B * sum_t (2 E t^2 + 2 m t), t = 1..{outers}, E = {E} "
                                      f"= {learn_flops:.4e} FLOP"),
             "ms_per_step": learn_ms,
             "share_of_profiled_step": learn_ms / max(prof["total_ms"], 1e-9),
             "note": ("Gram-form work (what the reference's dense epochs reduce to); the kernels "
-                     "run a power form with more fp64 tensor-core FLOPs, not counted"),
+                     "run the power form, which executes about half of these FLOPs at t = 32 "
+                     "(4 DMMA squarings + 21 matvecs), so the executed-FLOP pipe use is lower"),
         }
         corr_ms = prof["corr_ms"]
         if learn_ms > corr_ms:

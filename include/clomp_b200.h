@@ -26,6 +26,12 @@
  *     synthesis basis is set (cl_set_basis); separable and column-sharded
  *     contexts return CL_ERR_UNSUPPORTED.  Never a CPU fallback.
  *
+ *   * Support capacity per signal: th == 1 adds one atom per outer iteration
+ *     (plus exact ties), so the capacity is max_outer + 16.  1D contexts keep a
+ *     Gram matrix per signal and serve up to 2048 atoms (th < 1: a signal that
+ *     outgrows it ends with CL_ERR_CAPACITY); separable contexts switch to
+ *     direct-form learning (cl_set_direct_form) and have no limit below n.
+ *
  * Threading: one context per host thread; calls on distinct contexts may run
  * concurrently.  A context owns one device, one stream and its workspace.
  */
@@ -48,7 +54,7 @@ typedef enum cl_status {
   CL_ERR_CONFIG = 2,       /* cskit::ConfigError    (clomp.cpp:18-30)          */
   CL_ERR_DIMENSION = 3,    /* cskit::DimensionError (clomp.cpp:215-218)        */
   CL_ERR_NUMERICAL = 4,    /* cskit::NumericalError (clomp.cpp:255-256)        */
-  CL_ERR_UNSUPPORTED = 5,  /* priors on                                        */
+  CL_ERR_UNSUPPORTED = 5,  /* a combination this build does not serve (message says which) */
   CL_ERR_CUDA = 6,         /* CUDA runtime / no device / extension missing     */
   CL_ERR_CAPACITY = 7      /* support grew past the per-signal capacity        */
 } cl_status;
@@ -244,9 +250,10 @@ typedef struct cl_stats {
 int cl_get_stats(const cl_ctx* ctx, cl_stats* out);
 
 /* Tuning / test knobs: 0 = auto (GEMV for B <= 4, else tcgen05 at th == 1,
- * else fp64 SIMT), 1 = force fp64 SIMT correlation, 2 = force the tcgen05
- * split-fp16 correlation (th == 1 only), 3 = force the HBM-bound GEMV
- * (1 <= B <= 4). */
+ * else fp64 SIMT), 1 = force the fp64 correlation, 2 = force the tcgen05
+ * split-fp16 correlation (th == 1 only; separable contexts: stage 2 of
+ * A_r^T R A_c as K1 on the rows of R A_c, needs n_r a multiple of 256),
+ * 3 = force the HBM-bound GEMV (1 <= B <= 4, 1D). */
 int cl_set_corr_path(cl_ctx* ctx, int path);
 /* Dictionary Gram cache G = A^T A (fp64, n x n) used to extend each signal's
  * support Gram matrix by a gather instead of re-streaming atoms:
@@ -258,13 +265,15 @@ int cl_set_gram_cache(cl_ctx* ctx, int mode);
  * forces the batched kernel pipeline instead (tests compare the two). */
 int cl_set_fused(cl_ctx* ctx, int on);
 /* Synthesis basis D (n x n, x = D s; MeasurementSetup::basis, sensing.hpp:37-45)
- * for the priors.  The TV prior (priors.cpp:11-26, chained through D^T,
- * clomp.cpp:93-119) runs on single-column solves: CL_MODE_PER_SIGNAL (the
- * CLI's 1D path, clomp_solve per column) or a one-column batch, folded into
- * the support Gram system.  layout CL_LAYOUT_REF: basis[q * n + j] = D(q, j)
- * (la::Mat row-major); CL_LAYOUT_T: the transpose.  NULL clears.
- * Priors on multi-column joint batches (TV-2D + local variance) return
- * CL_ERR_UNSUPPORTED; priors without a basis too. */
+ * for the priors and the synthesis x_hat = D s.  Single-column solves
+ * (CL_MODE_PER_SIGNAL — the CLI's 1D path, clomp_solve per column — or a
+ * one-column batch) run the TV prior (priors.cpp:11-26, chained through D^T,
+ * clomp.cpp:93-119) folded into the support Gram system; multi-column joint
+ * batches (the reference's image mode, cskit.cpp:620-652) run TV-2D + local
+ * variance per epoch.  layout CL_LAYOUT_REF: basis[q * n + j] = D(q, j)
+ * (la::Mat row-major); CL_LAYOUT_T: the transpose.  NULL clears.  Priors
+ * without a basis, or on separable / column-sharded contexts, return
+ * CL_ERR_UNSUPPORTED. */
 int cl_set_basis(cl_ctx* ctx, const double* basis, int64_t n, int layout);
 /* Synthesis x_hat = D (s .* mask) (clomp.cpp:289) on the GPU: when on, every
  * host-buffer solve of a context with a basis also forms x_hat from the
@@ -280,7 +289,7 @@ int cl_set_synthesis(cl_ctx* ctx, int on);
  * form, whose t x t matrix per image stops fitting (above 2048 atoms: config
  * 5's K = 13107) or costs more to stream than the operator costs to apply.
  * from_outer: -1 auto (every iteration without a Gram buffer; otherwise from
- * t^2 > m_r n_c m_c / 8 on), 0 never (supports above 2048 atoms then fail
+ * t^2 > m_r n_c m_c / 16 on), 0 never (supports above 2048 atoms then fail
  * with CL_ERR_UNSUPPORTED), k > 0 from outer iteration k on (tests). */
 int cl_set_direct_form(cl_ctx* ctx, int from_outer);
 /* Supports of 33..256 atoms learn on CTA clusters with the support Gram

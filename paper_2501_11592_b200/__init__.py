@@ -28,7 +28,9 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_build" / "libclomp_b200.so"
+# CLOMP_B200_LIB selects another build of the same library (the debug build
+# with device-side index checks, _build/libclomp_b200_dbg.so); never a fallback
+LIB_PATH = Path(os.environ.get("CLOMP_B200_LIB") or _PKG / "_build" / "libclomp_b200.so")
 
 from .configs import ADAM, CONFIGS, MOMENTUM, PLAIN, CConfig, ClompConfig  # noqa: F401
 MODE_JOINT, MODE_PER_SIGNAL = 0, 1

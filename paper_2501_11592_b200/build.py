@@ -67,6 +67,38 @@ def _compile(src: Path) -> tuple[Path, str]:
     return obj, res.stderr
 
 
+def build_debug() -> Path:
+    """libclomp_b200_dbg.so: the same sources with -DCL_DEBUG_CHECKS (device-side
+    asserts on data-derived indices, clomp_internal.cuh), objects kept apart."""
+    dbg = OUT / "dbg"
+    dbg.mkdir(parents=True, exist_ok=True)
+    lib = OUT / "libclomp_b200_dbg.so"
+    srcs = _sources()
+    headers = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
+    stamp = dbg / "build.stamp"
+    digest = _digest(srcs + headers)
+    if lib.exists() and stamp.exists() and stamp.read_text() == digest:
+        return lib
+
+    def comp(src: Path) -> Path:
+        obj = dbg / (src.stem + ".o")
+        flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")] + ["-DCL_DEBUG_CHECKS"]
+        cmd = [nvcc()] + (["-x", "cu"] if src.suffix == ".cpp" else []) + flags + ["-c", str(src), "-o", str(obj)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc (debug) failed on {src.name}:\n{res.stdout}\n{res.stderr}")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = [str(o) for o in ex.map(comp, srcs)]
+    cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", str(lib)] + objs + ["-lpthread", "-ldl", "-lrt"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link (debug) failed:\n{res.stdout}\n{res.stderr}")
+    stamp.write_text(digest)
+    return lib
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     OUT.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
@@ -92,3 +124,5 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--debug" in sys.argv:
+        print(build_debug())

@@ -1320,11 +1320,18 @@ cl_ctx* cl_create_colshard(int device, const float* a, int64_t m, int64_t n, int
 int cl_set_virtual_shards(cl_ctx* ctx, int shards) {
   if (!ctx || shards < 1) return CL_ERR_INTERNAL;
   if (ctx->world > 1) return fail(ctx, CL_ERR_CONFIG, "context is already column-sharded");
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
   ctx->vshards = shards;
-  ctx->wbytes = 0;  // force a fresh workspace carve with the shard buffers
+  // force a fresh workspace carve with the shard buffers (and fresh power-form
+  // buffers: their slot count follows the per-rank signal range)
   cudaFree(ctx->wbuf);
   cudaFree(ctx->pw_buf);
   ctx->wbuf = nullptr;
+  ctx->wbytes = 0;
+  ctx->pw_buf = nullptr;
+  ctx->pw_bytes = 0;
+  ctx->w = Work{};
   return CL_OK;
 }
 

@@ -19,6 +19,18 @@
 #include <string>
 #include <utility>
 
+// Debug build (python -m paper_2501_11592_b200.build --debug ->
+// _build/libclomp_b200_dbg.so, -DCL_DEBUG_CHECKS): device-side assert on every
+// index the kernels form from data (atoms, support slots, list slots, tiles),
+// standing in for compute-sanitizer where the tool is not available.  A failed
+// check traps the kernel; the call returns CL_ERR_CUDA ("device-side assert").
+#ifdef CL_DEBUG_CHECKS
+#include <cassert>
+#define CL_CHECK(cond) assert(cond)
+#else
+#define CL_CHECK(cond) ((void)0)
+#endif
+
 namespace clb {
 
 // ---- per-device host caches

@@ -308,6 +308,8 @@ __device__ __forceinline__ void tile_epilogue(uint8_t* smem, uint32_t tmem, uint
     r.v3 = v3 >= 0.f ? (double)v3 * u : -1.0;
     r.i1 = i1;
     r.i2 = i2;
+    CL_CHECK(tile >= 0 && tile < ntile && (i1 == 0x7fffffff || (i1 >= n0 && i1 < n0 + TN && i1 < n)) &&
+             (i2 == 0x7fffffff || (i2 >= n0 && i2 < n0 + TN && i2 < n)));
     cand[b * ntile + tile] = r;
     K1_MARK_T(11, 0);
   }

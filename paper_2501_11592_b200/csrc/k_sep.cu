@@ -207,6 +207,8 @@ __global__ void k_sep_fix_cand(SolveParams p, Work w) {
   const int64_t tile = e % p.ntile;
   const int32_t base = (int32_t)((tile / (p.nr / p.tile_atoms)) * p.nr);
   Cand c = w.cand[e];
+  CL_CHECK((c.i1 == 0x7fffffff || (c.i1 >= 0 && c.i1 < p.nr)) &&
+           (c.i2 == 0x7fffffff || (c.i2 >= 0 && c.i2 < p.nr)));
   if (c.i1 != 0x7fffffff) c.i1 += base;
   if (c.i2 != 0x7fffffff) c.i2 += base;
   w.cand[e] = c;
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(256) k_dir_csc(SolveParams p, Work w) {
   // column j's entries in insertion order: one thread per column scans the
   // support (t <= a few thousand per image; once per outer iteration)
   int32_t* perm = w.csc_perm + b * p.cap;
+  CL_CHECK(t >= 0 && t <= p.cap && t0 >= 0 && t0 <= t);
   for (int64_t j = tid; j < p.nc; j += blockDim.x) {
     int pos = s_cnt[j];
     const int end = s_cnt[j + 1];
@@ -302,6 +305,8 @@ __global__ void __launch_bounds__(32 * kDirWarps) k_dir_colstep(SolveParams p, W
       double c_l = 0.0;
       if (lane < ne) {
         k_l = perm[ec + lane];
+        CL_CHECK(k_l >= 0 && k_l < w.cnt[b] && sup[k_l] >= 0 && sup[k_l] < p.n &&
+                 sup[k_l] / p.nr == j);
         row_l = (int64_t)(sup[k_l] % p.nr) * p.ldr;
         c_l = coef[k_l];
       }

@@ -143,6 +143,7 @@ __device__ __forceinline__ void exact_scores8(const SolveParams& p, const Work& 
                                               const double* r, int64_t j0, int cnt,
                                               double (&out)[8], int lane) {
   double acc[8];
+  CL_CHECK(j0 >= 0 && cnt >= 1 && cnt <= 8 && j0 + cnt <= p.n);
 #pragma unroll
   for (int u = 0; u < 8; ++u) acc[u] = 0.0;
   if (p.sep) {
@@ -198,6 +199,7 @@ struct PickState {
 __device__ __forceinline__ void pick_atom(const SolveParams& p, const Work& w, int64_t b,
                                           int32_t j, PickState& ps) {
   uint32_t* mb = w.maskbits + b * p.mwords;
+  CL_CHECK(j >= 0 && j < p.n && b >= 0 && b < p.B && ps.t >= 0 && ps.t <= p.cap);
   if (mask_test(mb, j)) return;  // already in the support: mask unchanged
   if (ps.t < p.cap) {
     w.sup[b * p.cap + ps.t] = j;
@@ -364,6 +366,7 @@ __device__ void warp_threshold_append(const SolveParams& p, const Work& w,
     const unsigned bal = __ballot_sync(kFull, pick);
     if (pick) {
       const int pos = t + __popc(bal & ((1u << lane) - 1u));
+      CL_CHECK(pos >= 0 && j < p.n);
       if (pos < p.cap) {
         w.sup[b * p.cap + pos] = (int32_t)j;
         atomicOr(&mb[j >> 5], 1u << (j & 31));
@@ -832,6 +835,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
 #pragma unroll kResidUnroll
     for (int k = 0; k < t; ++k) {
       const double ck = cs[k];
+      CL_CHECK(sups[k] >= 0 && sups[k] < p.n && t <= kWarpCap);
       const float* row = w.at32 + (int64_t)sups[k] * ldm + base + 4 * lane;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1126,6 +1130,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
     ctl.stall = w.stall[b];
   }
   if (!act) return false;
+  CL_CHECK(t_old >= 0 && t_old <= cap && t0 >= 0 && t0 <= t_old);
   const bool staged = t0 <= TB;
   if (staged) stage_gram_bulk(p, w, b, t0, s1, LDS, bar, lane);
 
@@ -1185,6 +1190,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   if (t > TB || t0 > TB) {  // outgrew this bucket: the block kernel learns it
     if (lane == 0) {
       const int slot = atomicAdd(&w.counters[kBigCount + (outer & 1)], 1);
+      CL_CHECK(slot >= 0 && slot < p.B);
       big_list[slot] = (int32_t)b;
     }
     if (staged) mbar_wait0(bar);
@@ -1197,6 +1203,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   const float* y = w.y32 + b * p.ldm;  // fp32 data, exact in fp64
   for (int k = t0; k < t; ++k) {
     const int64_t jk = __shfl_sync(kFull, sup_l, k);
+    CL_CHECK(jk >= 0 && jk < p.n && t <= TB && (lane > k || (sup_l >= 0 && sup_l < p.n)));
     if (lane <= k) {
       const double v = w.gfull[jk * p.n + sup_l];
       G[(int64_t)k * cap + lane] = v;
@@ -1308,6 +1315,7 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
   if (w.cnt[b] > TB) {
     if (lane == 0) {
       const int slot = atomicAdd(&w.counters[kBigCount + (outer & 1)], 1);
+      CL_CHECK(slot >= 0 && slot < p.B);
       big_list[slot] = (int32_t)b;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1371,7 +1379,9 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
   const int64_t cap = p.cap;
   for (int li = blockIdx.x; li < count; li += gridDim.x) {
     const int64_t b = big_list[li];
+    CL_CHECK(b >= p.sig_lo && b < p.sig_hi && count <= p.B);
     const int t = w.cnt[b];
+    CL_CHECK(t >= 0 && t <= cap && t <= kBlockRows * kBlockThreads);
     if (t <= skip_le) continue;  // learned by k_learn_cluster this iteration
     const int t0 = w.gcnt[b];
     double* G = w.gram + b * cap * cap;
@@ -2940,6 +2950,7 @@ __global__ void k_finalize(SolveParams p, Work w, int64_t out_cap,
     const int32_t jk = sv[k];
     int rank = 0;
     for (int q = 0; q < t; ++q) rank += sv[q] < jk;
+    CL_CHECK(jk >= 0 && jk < p.n && rank < t && t <= cap);
     if (rank < out_cap) {
       if (sup_out) sup_out[b * out_cap + rank] = jk;
       if (coef_out) coef_out[b * out_cap + rank] = cv[k];

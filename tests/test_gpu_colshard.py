@@ -40,3 +40,17 @@ def test_colshard_rejects_unsupported(gpu_available):
         cl.clomp_solve_batch(ctx, Y, cl.ClompConfig.baseline(4), mode=cl.MODE_PER_SIGNAL)
     with pytest.raises(cl.UnsupportedError):
         cl.clomp_solve_batch(ctx, Y, cl.ClompConfig.baseline(4), mode=cl.MODE_JOINT)
+
+
+def test_virtual_shards_switched_on_a_used_context(gpu_available):
+    """cl_set_virtual_shards on a context that already solved (workspace and
+    power-form buffers allocated) re-carves both; round 2's debug-build probe
+    found the power-form buffer freed but still referenced here."""
+    A, X, Y, _ = cl.gen_problem_1d(33, 512, 1024, 72, 6, value_law=1)
+    cfg = cl.ClompConfig.baseline(72)
+    ctx = cl.ClompContext(A)
+    ref = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)  # cluster learners + power form
+    for shards in (2, 1, 4):
+        ctx.set_virtual_shards(shards)
+        got = cl.clomp_solve_batch(ctx, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+        assert np.array_equal(got.mask, ref.mask) and np.array_equal(got.s, ref.s)
