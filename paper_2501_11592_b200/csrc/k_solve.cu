@@ -1278,7 +1278,7 @@ constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
 #define CL_LEARN16_MINB 4
 #endif
 #ifndef CL_LEARN8_MINB
-#define CL_LEARN8_MINB 4
+#define CL_LEARN8_MINB 7
 #endif
 template <int TB>
 constexpr int learn_min_blocks() {
