@@ -51,6 +51,19 @@ struct Carver {
 #endif
 constexpr int kChunkIters = CL_CHUNK_ITERS;  // outer iterations per captured graph
 
+// The fused small solve is one kernel (init, iterations, result compaction),
+// launched as a cached one-node graph.  Keyed by everything the node reads.
+struct FusedGraphKey {
+  unsigned char p[sizeof(SolveParams)];
+  unsigned char w[sizeof(Work)];
+  const void* y = nullptr;
+  int layout_ref = 0;
+  const void* out[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t out_cap = 0;
+  cudaStream_t stream = nullptr;
+  bool operator==(const FusedGraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
 struct GraphKey {
   SolveParams p{};
   Work w{};  // every device pointer a captured kernel reads
@@ -134,6 +147,7 @@ struct cl_ctx {
   cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
   GraphKey gkey;
   std::vector<cudaGraphExec_t> graphs;
+  std::vector<std::pair<FusedGraphKey, cudaGraphExec_t>> fused_graphs;  // a few (two staging slots)
   int corr_force = 0;
   bool want_xhat = false;  // cl_set_synthesis
   int direct_mode = -1;  // separable direct-form learning: -1 auto, 0 off, k > 0 from iteration k
@@ -727,9 +741,48 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     }
   };
 
+  int64_t launches = 0;
+  if (fused) {
+    FusedGraphKey key;
+    std::memset(&key, 0, sizeof(key));
+    std::memcpy(key.p, &p, sizeof(p));
+    std::memcpy(key.w, &w, sizeof(w));
+    key.y = y_dev;
+    key.layout_ref = layout_ref;
+    const void* optr[7] = {out.sup, out.coef, out.cnt, out.iters, out.rn, out.conv, out.status};
+    std::memcpy(key.out, optr, sizeof(optr));
+    key.out_cap = out.cap;
+    key.stream = s;
+    cudaGraphExec_t ge = nullptr;
+    for (auto& kv : ctx->fused_graphs)
+      if (kv.first == key) ge = kv.second;
+    if (!ge) {
+      cudaGraph_t g = nullptr;
+      CL_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+      launch_solve_fused(p, w, y_dev, layout_ref ? 1 : 0, out.cap, out.sup, out.coef, out.cnt,
+                         out.iters, out.rn, out.conv, out.status, s);
+      CL_CUDA(ctx, cudaStreamEndCapture(s, &g));
+      CL_CUDA(ctx, cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      if (ctx->fused_graphs.size() >= 8) {  // callers cycling through many buffers
+        cudaGraphExecDestroy(ctx->fused_graphs.front().second);
+        ctx->fused_graphs.erase(ctx->fused_graphs.begin());
+      }
+      ctx->fused_graphs.emplace_back(key, ge);
+    }
+    CL_CUDA(ctx, cudaGraphLaunch(ge, s));
+    launches += 1;
+    CL_CUDA(ctx, cudaGetLastError());
+    if (host_sync) CL_CUDA(ctx, cudaStreamSynchronize(s));
+    stats.kernel_launches = launches;
+    stats.rescans = 0;
+    stats.outer_iterations = p.max_outer;
+    stats.corr_path = 2;
+    ctx->stats = stats;
+    return CL_OK;
+  }
   CL_CUDA(ctx, cudaMemsetAsync(w.counters, 0, kNumCounters * sizeof(int32_t), s));
   std::memset(ctx->h_counters, 0, kNumCounters * sizeof(int32_t));
-  int64_t launches = 0;
   launch_init(p, w, y_dev, layout_ref ? 0 : 1, false, s);
   launches += (layout_ref && p.B > 1) ? 2 : 1;  // + the tiled transpose of m x B y
   if (p.sep) {  // b values of every atom: Z = A_r^T Y A_c
@@ -741,22 +794,6 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     ++launches;
   }
   int outer_done = 0;
-  if (fused) {
-    launch_solve_fused(p, w, s);
-    launch_finalize(p, w, out.cap, out.sup, out.coef, out.cnt, out.iters, out.rn,
-                    out.conv, out.status, s);
-    launches += 2;
-    CL_CUDA(ctx, cudaGetLastError());
-    CL_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, w.counters, kNumCounters * sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost, s));
-    if (host_sync) CL_CUDA(ctx, cudaStreamSynchronize(s));
-    stats.kernel_launches = launches;
-    stats.rescans = 0;
-    stats.outer_iterations = p.max_outer;
-    stats.corr_path = 2;
-    ctx->stats = stats;
-    return CL_OK;
-  }
   if (ctx->profiling) {
     // Per-phase CUDA-event timing (outside the graph path).
     cudaEvent_t ev[5];
@@ -1285,6 +1322,8 @@ void cl_destroy(cl_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& g : ctx->graphs)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& kv : ctx->fused_graphs)
+    if (kv.second) cudaGraphExecDestroy(kv.second);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

@@ -430,8 +430,13 @@ constexpr int kLvCover = 8;  // max windows covering one row / column
 void launch_synth(const double* dt, int64_t n, int64_t B, int64_t out_cap, const int32_t* sup,
                   const double* coef, const int32_t* cnt, double* xhat, cudaStream_t s);
 
-// Whole per-signal solve in one persistent block per signal (small problems).
-void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s);
+// Whole per-signal solve in one persistent block per signal (small problems):
+// init, every outer iteration and the result compaction in one kernel.
+// y_in: m x B (y_ref) or signal-major B x m.
+void launch_solve_fused(const SolveParams& p, const Work& w, const float* y_in, int y_ref,
+                        int64_t out_cap, int32_t* sup_out, double* coef_out, int32_t* cnt_out,
+                        int32_t* iters_out, double* rn_out, uint8_t* conv_out, int32_t* status_out,
+                        cudaStream_t s);
 // inject_support unit path: residual already in w.r64 (and split), mask in
 // w.maskbits; appends nothing to the learning state.
 void launch_inject_finish(const SolveParams& p, const Work& w, cudaStream_t s);

@@ -918,7 +918,7 @@ __device__ __forceinline__ void stage_gram_async(const SolveParams& p, const Wor
 template <int TB, int OPT>
 __device__ __forceinline__ double learn_epochs(const SolveParams& p, const Work& w, int64_t b,
                                                int outer, double* cs, double* s1, int lane, int t,
-                                               double c, double bi, double m1, double m2) {
+                                               double c, double bi, double& m1, double& m2) {
   constexpr int LDS = TB + 4;
   double g[TB];
   const double twolr = 2.0 * p.lr;
@@ -945,7 +945,11 @@ __device__ __forceinline__ double learn_epochs(const SolveParams& p, const Work&
       else
         epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
     } else {
-      if (t <= 16)
+      // (zero padding is exact, so the narrower instantiations compute the
+      // same bits; t <= 8 reaches a 32-atom bucket only on the fused path)
+      if (t <= 8)
+        epochs_plain<8, TB>(g, c, bi, cs, s1, p, lane);
+      else if (t <= 16)
         epochs_plain<16, TB>(g, c, bi, cs, s1, p, lane);
       else if (t <= 24)
         epochs_plain<24, TB>(g, c, bi, cs, s1, p, lane);
@@ -2672,40 +2676,161 @@ constexpr int kFusedAtoms = CL_FUSED_ATOMS;  // atoms per warp pass of the corre
 #endif
 constexpr int kFusedStageMax = CL_FUSED_STAGE_MAX;  // dynamic smem cap for the staged dictionary
 
-template <int OPT>
+// Everything a signal's solve touches between outer iterations stays on chip:
+// the residual, y, the scores, the support / coefficients / b / moments, the
+// support Gram matrix, the mask and the stopping-rule state live in shared
+// memory (round 1 kept them in global memory and paid ~8 dependent round trips
+// per outer iteration: 18.6 us each at config 1).  What still leaves the SM per
+// iteration is the gather of the new Gram row from A^T A (one L2 round trip)
+// and fire-and-forget stores.  The state k_finalize reads is written once at
+// the end.
+#ifdef CL_LEARN_TRACE
+// phase marks of signal 0's outer iterations in the fused kernel (row = outer)
+#define FT_MARK(i) do { if (tid == 0 && b == 0 && outer < 8192) g_lt[outer][i] = (unsigned long long)clock64(); } while (0)
+#else
+#define FT_MARK(i) do { } while (0)
+#endif
+
+struct FusedCtl {
+  double best_L, prev_L, loss;
+  int t, t0, stall, iters, status, conv, active, best_cnt, changed;
+};
+
+// STAGED: the dictionary lives in shared memory MEASUREMENT-major, AT[i][j] with
+// an odd row stride n + 1 floats, so that (a) the correlation runs one thread
+// per atom, serial over the measurements with r[i] broadcast — consecutive
+// atoms are consecutive words, no shuffles, 4 partial sums per atom in a fixed
+// order — and (b) column reads (b_k, the residual's A[i][sup_k]) hit distinct
+// banks.  Round 1 staged it atom-major and reduced 32 dot products per warp
+// with 160 shuffles: 13.6 k of the 26.5 k cycles of a config-1 outer iteration
+// (tools/fused_trace.py).  !STAGED (dictionary too large for shared memory, or
+// more signals than SMs) keeps the atom-major global reads.
+// The kernel also does what k_init and k_finalize do for the batched path (y in,
+// r = -y, the eps test at s = 0; the snapshot rule, support sorted ascending,
+// final norm and flags out), so a whole solve is one kernel node.
+struct FusedIo {
+  const float* y;       // m x B (y_ref) or B x y_ld
+  int64_t y_ld;
+  int32_t y_ref;
+  int64_t out_cap;
+  int32_t* sup;
+  double* coef;
+  int32_t* cnt;
+  int32_t* iters;
+  double* rn;
+  uint8_t* conv;
+  int32_t* status;
+};
+
+template <int OPT, bool STAGED>
 __global__ void __launch_bounds__(kFusedThreads)
-k_solve_fused(SolveParams p, Work w, int stage_a) {
+k_solve_fused(SolveParams p, Work w, int sc_smem, FusedIo io) {
   extern __shared__ __align__(16) unsigned char fsm[];
   double* rs = reinterpret_cast<double*>(fsm);                 // [ldm] residual
-  // stage_a: the whole fp32 dictionary (atom-major, n x ldm) staged once into
-  // shared memory behind rs, so the per-iteration correlation and residual
-  // gathers read shared memory instead of L2 (config 1: 128 KB)
+  double* ys = rs + p.ldm;                                     // [ldm] y (fp32 values, exact)
+  double* sc_s = ys + p.ldm;                                   // [n] |scores| (sc_smem)
+  uint32_t* mask = reinterpret_cast<uint32_t*>(sc_s + (sc_smem ? p.n : 0));  // [mwords, padded]
+  float* As = reinterpret_cast<float*>(mask + 2 * ((p.mwords + 3) & ~3LL));  // [m][n + 1] (STAGED)
+  const int64_t lda = p.n + 1;
   __shared__ __align__(16) double cs[2 * kWarpCap];
+  __shared__ __align__(16) double sq[kWarpCap * (kWarpCap + 4)];   // learn_epochs work buffer
+  __shared__ __align__(16) double Gs[kWarpCap * (kWarpCap + 4)];   // support Gram, persistent
+  __shared__ double s_c[kWarpCap], s_b[kWarpCap], s_m1[kWarpCap], s_m2[kWarpCap], s_best[kWarpCap];
   __shared__ int32_t sups[kWarpCap];
-  __shared__ __align__(16) double sq[kWarpCap * (kWarpCap + 4)];
   __shared__ double red[kFusedThreads / 32];
-  __shared__ int s_active;
+  __shared__ FusedCtl ctl;
+  uint32_t* pickw = mask + ((p.mwords + 3) & ~3LL);  // [mwords] this iteration's picks
+  constexpr int LDS = kWarpCap + 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kFusedThreads / 32;
   const int64_t b = blockIdx.x;
-  if (!w.active[b]) return;
-  for (int64_t i = tid; i < p.ldm; i += kFusedThreads) rs[i] = w.r64[b * p.ldm + i];
-  const float* At = w.at32;
-  if (stage_a) {
-    float* As = reinterpret_cast<float*>(rs + p.ldm);
-    const int64_t n4 = p.n * p.ldm / 4;
-    for (int64_t i = tid; i < n4; i += kFusedThreads)
-      reinterpret_cast<float4*>(As)[i] = reinterpret_cast<const float4*>(w.at32)[i];
-    At = As;
+  // k_init: y, r = A*0 - y = -y (clomp.cpp:236-237 at s = 0), ||y||^2
+  for (int64_t i = tid; i < p.ldm; i += kFusedThreads) {
+    float v = 0.f;
+    if (i < p.m) v = io.y_ref ? io.y[i * p.B + b] : io.y[b * io.y_ld + i];
+    ys[i] = (double)v;
+    rs[i] = -(double)v;
+  }
+  for (int64_t q = tid; q < p.mwords; q += kFusedThreads) mask[q] = 0u;
+  if (tid < kWarpCap) s_c[tid] = s_b[tid] = s_m1[tid] = s_m2[tid] = s_best[tid] = 0.0;
+  __syncthreads();
+  if (warp == 0) {
+    double yy = 0.0;  // k_init's summation order: lanes stride the row, then the butterfly
+    for (int64_t i = lane; i < p.ldm; i += 32) yy = fma(ys[i], ys[i], yy);
+    yy = warp_sum(yy);
+    if (lane == 0) red[0] = yy;
   }
   __syncthreads();
-  double* sc = w.scores + b * p.n;
-  for (int outer = 1; outer <= p.max_outer; ++outer) {
-    // K1: exact fp64 scores |a_j . r|, kFusedAtoms atoms per warp pass (as many
-    // independent dot products as registers allow keep the L2 loads in flight;
-    // config 1's 256 atoms take one pass of the 8 warps).  Each score's
-    // summation order does not depend on the pass width.
+  if (tid == 0) {
+    const double L = red[0];
+    ctl.best_L = CUDART_INF;
+    ctl.prev_L = CUDART_INF;
+    ctl.loss = L;
+    ctl.t = ctl.t0 = ctl.stall = ctl.iters = ctl.status = ctl.conv = ctl.best_cnt = ctl.changed = 0;
+    ctl.active = 1;
+    if (sqrt(L) < p.eps) {  // the outer-1 eps test (clomp.cpp:238-242)
+      ctl.active = 0;
+      ctl.conv = 1;
+    }
+  }
+  const float* At = w.at32;
+  if (STAGED) {
+    // coalesced float4 reads of the atom-major dictionary (eight in flight per
+    // thread), scattered to the measurement-major copy
+    const int64_t n4 = p.n * p.ldm / 4, l4 = p.ldm / 4;
+    for (int64_t e0 = tid; e0 < n4; e0 += 8 * kFusedThreads) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t e = e0 + u * kFusedThreads;
+        if (e < n4) v[u] = reinterpret_cast<const float4*>(w.at32)[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t e = e0 + u * kFusedThreads;
+        if (e < n4) {
+          const int64_t j = e / l4, i = 4 * (e % l4);
+          if (i < p.m) As[i * lda + j] = v[u].x;
+          if (i + 1 < p.m) As[(i + 1) * lda + j] = v[u].y;
+          if (i + 2 < p.m) As[(i + 2) * lda + j] = v[u].z;
+          if (i + 3 < p.m) As[(i + 3) * lda + j] = v[u].w;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* sc = sc_smem ? sc_s : w.scores + b * p.n;
+  const int cap = (int)p.cap;  // <= kWarpCap on this path
+  for (int outer = 1; outer <= p.max_outer && ctl.active; ++outer) {
+    // K1: exact fp64 scores |a_j . r|, kFusedAtoms atoms per warp pass (config
+    // 1's 256 atoms take one pass of the 8 warps).  Each score's summation
+    // order does not depend on the pass width.
     double cmax = 0.0;
+    FT_MARK(0);
+    if (STAGED) {
+      // K1: exact fp64 scores |a_j . r|, one thread per atom
+      for (int64_t j = tid; j < p.n; j += kFusedThreads) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const float* col = As + j;
+        int64_t i = 0;
+#pragma unroll 4
+        for (; i + 4 <= p.m; i += 4) {  // r as two 16-byte broadcasts per four rows
+          const double2 r01 = *reinterpret_cast<const double2*>(rs + i);
+          const double2 r23 = *reinterpret_cast<const double2*>(rs + i + 2);
+          a0 = fma(f2d(col[i * lda]), r01.x, a0);
+          a1 = fma(f2d(col[(i + 1) * lda]), r01.y, a1);
+          a2 = fma(f2d(col[(i + 2) * lda]), r23.x, a2);
+          a3 = fma(f2d(col[(i + 3) * lda]), r23.y, a3);
+        }
+        for (; i < p.m; ++i) a0 = fma(f2d(col[i * lda]), rs[i], a0);
+        const double v = fabs((a0 + a1) + (a2 + a3));
+        sc[j] = v;
+        cmax = fmax(cmax, v);
+      }
+      cmax = warp_max(cmax);
+    } else {
+    // K1: exact fp64 scores |a_j . r|, kFusedAtoms atoms per warp pass.  Each
+    // score's summation order does not depend on the pass width.
     for (int64_t j0 = warp * kFusedAtoms; j0 < p.n; j0 += nw * kFusedAtoms) {
       double acc[kFusedAtoms];
 #pragma unroll
@@ -2730,54 +2855,219 @@ k_solve_fused(SolveParams p, Work w, int stage_a) {
         }
       }
     }
+    }
     if (lane == 0) red[warp] = cmax;
     __syncthreads();
-    // K1c: inject_from_scores (clomp.cpp:41-53), ties included; K2 learning.
-    if (warp == 0) {
-      double m = 0.0;
-      for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
-      if (lane == 0) w.changed[b] = 0;
-      if (m > 0.0)
-        warp_threshold_append(p, w, b, p.th * m, [&](int64_t j) { return sc[j]; }, lane);
-      __syncwarp();
-      if (w.active[b] && w.cnt[b] <= kWarpCap) {
-        stage_gram_async(p, w, b, w.gcnt[b], sq, kWarpCap + 4, lane);
-        learn_warp_body<kWarpCap, OPT>(p, w, b, outer, cs, sups, sq, nullptr, lane);
+    FT_MARK(1);
+    // K1c: inject_from_scores (clomp.cpp:41-53), ties included, ascending j.
+    // Every warp marks its atoms (one ballot word per 32 atoms); warp 0 then
+    // places the picks by a prefix over the words.
+    double m = 0.0;
+    for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
+    {
+      const double cut = p.th * m;
+      for (int64_t j0 = (int64_t)warp * 32; j0 < p.n; j0 += kFusedThreads) {
+        const int64_t j = j0 + lane;
+        const bool pick = m > 0.0 && j < p.n && sc[j] >= cut && !((mask[j >> 5] >> (j & 31)) & 1u);
+        const unsigned bal = __ballot_sync(kFull, pick);
+        if (lane == 0) pickw[j0 >> 5] = bal;
       }
-      else if (lane == 0 && w.active[b])
-        w.status[b] = 7, w.active[b] = 0;  // capacity: larger supports use the batched path
     }
     __syncthreads();
-    if (!w.active[b]) break;
+    if (warp == 0) {
+      int t = ctl.t;
+      const int t0 = ctl.t0;
+      int added = 0, overflow = 0;
+      for (int64_t w0 = 0; w0 < p.mwords; w0 += 32) {
+        const int64_t wi = w0 + lane;
+        unsigned bits = wi < p.mwords ? pickw[wi] : 0u;
+        const int cntw = __popc(bits);
+        int pre = cntw;  // inclusive prefix over the 32 words
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(kFull, pre, o);
+          if (lane >= o) pre += v;
+        }
+        const int tot = __shfl_sync(kFull, pre, 31);
+        int pos = t + pre - cntw;
+        if (bits) mask[wi] |= bits;
+        while (bits) {
+          const int bit = __ffs(bits) - 1;
+          bits &= bits - 1;
+          CL_CHECK(pos >= 0 && wi * 32 + bit < p.n);
+          if (pos < cap) sups[pos] = (int32_t)(wi * 32 + bit);
+          ++pos;
+        }
+        t += tot;
+        added += tot;
+        if (t > cap) overflow = 1;
+      }
+      __syncwarp();
+      FT_MARK(2);
+      if (overflow) {  // larger supports use the batched path
+        if (lane == 0) {
+          ctl.status = kStatusCapacity;
+          ctl.active = 0;
+          ctl.t = cap;
+          ctl.changed = added > 0;
+        }
+      } else {
+        // Gram row / column and b_k = a_k . y of the atoms added this iteration
+        // (new atoms start at c = 0, clomp.hpp:53-54)
+        for (int k = t0; k < t; ++k) {
+          const int64_t jk = sups[k];
+          double gk = 0.0;
+          if (w.gfull) {
+            if (lane <= k) gk = w.gfull[jk * p.n + sups[lane]];
+          } else {
+            for (int i = 0; i <= k; ++i) {  // fp64 dot of the fp32 atoms, lanes over m
+              double acc = 0.0;
+              if (STAGED) {
+                for (int64_t q = lane; q < p.m; q += 32)
+                  acc = fma(f2d(As[q * lda + jk]), f2d(As[q * lda + sups[i]]), acc);
+              } else {
+                const float* ai = At + (int64_t)sups[i] * p.ldm;
+                const float* ak = At + jk * p.ldm;
+                for (int64_t q = lane; q < p.ldm; q += 32) acc = fma(f2d(ak[q]), f2d(ai[q]), acc);
+              }
+              acc = warp_sum(acc);
+              if (lane == i) gk = acc;
+            }
+          }
+          if (lane <= k) {
+            Gs[k * LDS + lane] = gk;
+            Gs[lane * LDS + k] = gk;
+          }
+          double accb = 0.0;
+          if (STAGED) {  // the same element order as the atom-major float4 walk
+            for (int64_t i0 = 4 * lane; i0 < p.m; i0 += 128)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (i0 + e < p.m) accb = fma(f2d(As[(i0 + e) * lda + jk]), ys[i0 + e], accb);
+          } else {
+            const float* ak = At + jk * p.ldm;
+#pragma unroll 4
+            for (int64_t i0 = 4 * lane; i0 < p.ldm; i0 += 128) {
+              const float4 a = *reinterpret_cast<const float4*>(ak + i0);
+              accb = fma(f2d(a.x), ys[i0], accb);
+              accb = fma(f2d(a.y), ys[i0 + 1], accb);
+              accb = fma(f2d(a.z), ys[i0 + 2], accb);
+              accb = fma(f2d(a.w), ys[i0 + 3], accb);
+            }
+          }
+          accb = warp_sum(accb);
+          if (lane == k) {
+            s_b[k] = accb;
+            s_c[k] = s_m1[k] = s_m2[k] = 0.0;
+          }
+        }
+        __syncwarp();
+        FT_MARK(3);
+        // K2: all epochs; learn_epochs squares in place, so it works on a copy
+        for (int e = lane; e < t * LDS; e += 32) sq[e] = Gs[e];
+        __syncwarp();
+        double m1 = lane < t ? s_m1[lane] : 0.0, m2 = lane < t ? s_m2[lane] : 0.0;
+        const double c = learn_epochs<kWarpCap, OPT>(p, w, b, outer, cs, sq, lane, t,
+                                                      lane < t ? s_c[lane] : 0.0,
+                                                      lane < t ? s_b[lane] : 0.0, m1, m2);
+        if (lane < t) {
+          s_c[lane] = c;
+          s_m1[lane] = m1;
+          s_m2[lane] = m2;
+        }
+        if (lane == 0) {
+          ctl.t = t;
+          ctl.t0 = t;
+          ctl.changed = added > 0;
+        }
+      }
+    }
+    FT_MARK(4);
+    __syncthreads();
+    if (!ctl.active) break;
     // residual r = A_S c - y (fp64) and the stopping rules
-    const int t = w.cnt[b];
-    if (tid < t) {
-      cs[tid] = w.coef[b * p.cap + tid];
-      sups[tid] = w.sup[b * p.cap + tid];
-    }
-    __syncthreads();
+    const int t = ctl.t;
     double lacc = 0.0;
     for (int64_t i = tid; i < p.ldm; i += kFusedThreads) {
       double acc = 0.0;
-      for (int k = 0; k < t; ++k) acc = fma((double)At[(int64_t)sups[k] * p.ldm + i], cs[k], acc);
-      const double rv = acc - w.y64[b * p.ldm + i];
+      if (STAGED) {
+        if (i < p.m)
+          for (int k = 0; k < t; ++k) acc = fma((double)As[i * lda + sups[k]], s_c[k], acc);
+      } else {
+        for (int k = 0; k < t; ++k) acc = fma((double)At[(int64_t)sups[k] * p.ldm + i], s_c[k], acc);
+      }
+      const double rv = acc - ys[i];
       rs[i] = rv;
       lacc = fma(rv, rv, lacc);
     }
     lacc = warp_sum(lacc);
     if (lane == 0) red[warp] = lacc;
     __syncthreads();
-    if (tid == 0) {
+    FT_MARK(5);
+    if (warp == 0) {
+      // clomp.cpp:253-273 on the on-chip state (control_signal's rules)
       double L = 0.0;
       for (int q = 0; q < nw; ++q) L += red[q];
-      s_active = 0;
-      if (control_signal(p, w, b, outer, L)) {
-        for (int k = 0; k < t; ++k) w.best_coef[b * p.cap + k] = cs[k];
+      int snap = 0;
+      if (lane == 0) {
+        ctl.loss = L;
+        if (!isfinite(L)) {
+          ctl.status = kStatusNumerical;
+          ctl.active = 0;
+        } else {
+          ctl.iters = outer;
+          if (L < ctl.best_L) {
+            ctl.best_L = L;
+            ctl.best_cnt = t;
+            snap = 1;
+          }
+          const double prev = ctl.prev_L;
+          const double rel = isfinite(prev) ? (prev - L) / fmax(fabs(prev), 1e-300) : CUDART_INF;
+          const int stall = (!ctl.changed && rel < p.stall_tol) ? ctl.stall + 1 : 0;
+          ctl.stall = stall;
+          ctl.prev_L = L;
+          if (stall >= p.stall_patience || outer >= p.max_outer) {
+            ctl.active = 0;
+          } else if (sqrt(L) < p.eps) {
+            ctl.conv = 1;
+            ctl.active = 0;
+          }
+        }
       }
-      s_active = w.active[b];
+      snap = __shfl_sync(kFull, snap, 0);
+      if (snap && lane < t) s_best[lane] = s_c[lane];
     }
+    FT_MARK(6);
     __syncthreads();
-    if (!s_active) break;
+    if (!ctl.active) break;
+  }
+  // k_finalize: the best snapshot unless converged (clomp.cpp:276-288), the
+  // support in ascending atom order, final norm and flags
+  __syncthreads();
+  if (warp == 0) {
+    const bool bad = ctl.status == kStatusNumerical;
+    const bool use_best = !ctl.conv && isfinite(ctl.best_L);
+    int t = bad ? 0 : (use_best ? ctl.best_cnt : ctl.t);
+    if (ctl.status == kStatusCapacity) t = ctl.t < cap ? ctl.t : cap;
+    const double* cv = use_best ? s_best : s_c;
+    if (lane < t) {
+      const int32_t jk = sups[lane];
+      int rank = 0;
+      for (int q = 0; q < t; ++q) rank += sups[q] < jk;
+      CL_CHECK(rank < t && jk >= 0 && jk < p.n);
+      if (rank < io.out_cap) {
+        if (io.sup) io.sup[b * io.out_cap + rank] = jk;
+        if (io.coef) io.coef[b * io.out_cap + rank] = cv[lane];
+      }
+    }
+    if (lane == 0) {
+      const double rn = use_best ? sqrt(ctl.best_L) : sqrt(ctl.loss);
+      if (io.cnt) io.cnt[b] = t < io.out_cap ? t : (int)io.out_cap;
+      if (io.iters) io.iters[b] = ctl.iters;
+      if (io.rn) io.rn[b] = bad ? CUDART_NAN : rn;
+      if (io.conv) io.conv[b] = (!bad && rn < p.eps) ? 1 : 0;
+      if (io.status) io.status[b] = ctl.status;
+    }
   }
 }
 
@@ -3303,23 +3593,50 @@ void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStre
   k_sep_control<<<(unsigned)blocks, 128, 0, s>>>(p, w, outer, sep_resid_tiles(p));
 }
 
-void launch_solve_fused(const SolveParams& p, const Work& w, cudaStream_t s) {
+void launch_solve_fused(const SolveParams& p, const Work& w, const float* y_in, int y_ref,
+                        int64_t out_cap, int32_t* sup_out, double* coef_out, int32_t* cnt_out,
+                        int32_t* iters_out, double* rn_out, uint8_t* conv_out, int32_t* status_out,
+                        cudaStream_t s) {
+  FusedIo io{y_in, p.m, y_ref, out_cap, sup_out, coef_out, cnt_out, iters_out, rn_out, conv_out, status_out};
   // latency-bound path: the SM count and the smem attribute are queried / set
   // once per device (the attribute only grows), not per call
-  static DevSlots smem_set[3];
+  static DevSlots smem_set[6];
   const int sms = device_sms(current_device());
-  // stage A in shared memory when it fits and every signal still gets its own SM
-  const size_t a_bytes = (size_t)(p.n * p.ldm) * 4;
-  const int stage_a = (p.ldm * 8 + a_bytes <= (size_t)kFusedStageMax && p.B <= sms) ? 1 : 0;
-  const size_t smem = (size_t)p.ldm * 8 + (stage_a ? a_bytes : 0);
-  auto go = [&](auto kern) {
-    ensure_smem_limit(smem_set[p.opt < 0 ? 0 : (p.opt > 2 ? 2 : p.opt)], kern, smem);
-    kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w, stage_a);
+  // dynamic shared memory: residual, y, the mask, then (when they fit) the
+  // scores and the whole dictionary (measurement-major, m x (n + 1) floats); A
+  // is staged only while every signal still gets its own SM
+  const size_t base = (size_t)p.ldm * 16 + (size_t)((p.mwords + 3) & ~3LL) * 8;  // mask + picks
+  const size_t sc_bytes = (size_t)p.n * 8;
+  const size_t a_bytes = (size_t)(p.m * (p.n + 1)) * 4 + 16;
+  const int sc_smem = base + sc_bytes <= (size_t)kFusedStageMax ? 1 : 0;
+  const size_t with_sc = base + (sc_smem ? sc_bytes : 0);
+  const bool stage_a = with_sc + a_bytes <= (size_t)kFusedStageMax && p.B <= sms;
+  const size_t smem = with_sc + (stage_a ? a_bytes : 0);
+  auto go = [&](auto kern, int slot) {
+    // static shared memory (~21 KB) counts against the 48 KB default too: opt
+    // in to the large carve-out as soon as the sum could pass it
+    if (smem + 24 * 1024 > 48 * 1024) {
+      const int dev = current_device();
+      if ((long long)smem > smem_set[slot].get(dev)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set[slot].set(dev, (long long)smem);
+      }
+    }
+    kern<<<(unsigned)p.B, kFusedThreads, smem, s>>>(p, w, sc_smem, io);
   };
-  switch (p.opt) {
-    case 0: go(k_solve_fused<0>); break;
-    case 1: go(k_solve_fused<1>); break;
-    default: go(k_solve_fused<2>); break;
+  const int o = p.opt < 0 ? 0 : (p.opt > 2 ? 2 : p.opt);
+  if (stage_a) {
+    switch (o) {
+      case 0: go(k_solve_fused<0, true>, 0); break;
+      case 1: go(k_solve_fused<1, true>, 1); break;
+      default: go(k_solve_fused<2, true>, 2); break;
+    }
+  } else {
+    switch (o) {
+      case 0: go(k_solve_fused<0, false>, 3); break;
+      case 1: go(k_solve_fused<1, false>, 4); break;
+      default: go(k_solve_fused<2, false>, 5); break;
+    }
   }
 }
 
