@@ -285,6 +285,7 @@ int ensure_workspace(cl_ctx* ctx, int64_t B, int64_t cap, bool need_scores,
       w.lpart = cv.take<double>(B * (((ctx->mr + 63) / 64) * ((ctx->mc + 63) / 64)));
       if (with_direct) {
         w.sep_scratch2 = cv.take<double>(B * ctx->nc * ctx->mr);
+        w.sep_z2 = cv.take<double>(B * ctx->nc * ctx->mr);
         w.csc_ptr = cv.take<int32_t>(B * (ctx->nc + 1));
         w.csc_perm = cv.take<int32_t>(B * cap);
       }
@@ -788,6 +789,10 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   if (p.sep) {  // b values of every atom: Z = A_r^T Y A_c
     launch_sep_corr(p, w, w.y64, w.zb, false, s);
     launches += 2;
+    if (dfrom > 0) {  // direct form: the constant part of U = R A_c
+      launch_sep_direct_prepare(p, w, s);
+      ++launches;
+    }
   }
   if (p.mode == CL_MODE_JOINT) {
     launch_joint_control(p, w, 0, true, s);

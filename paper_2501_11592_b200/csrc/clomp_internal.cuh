@@ -213,6 +213,7 @@ struct Work {
   // direct-form learning (large supports): second scratch for U = R A_c and the
   // support sorted by coefficient column
   double* sep_scratch2 = nullptr;  // [B][nc][mr]
+  double* sep_z2 = nullptr;        // [B][nc][mr] Y A_c (constant part of U = R A_c)
   int32_t* csc_ptr = nullptr;      // [B][nc + 1]
   int32_t* csc_perm = nullptr;     // [B][cap] support entries by column
   Cand* xg = nullptr;            // column sharding: per-shard candidates [W][B][ntl]
@@ -360,6 +361,8 @@ void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
 // bound: upper bound on the support sizes.  Returns the kernels launched.
 int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int bound,
                             cudaStream_t s);
+// Once per solve, before the first direct-form iteration: Z2 = Y A_c.
+void launch_sep_direct_prepare(const SolveParams& p, const Work& w, cudaStream_t s);
 int64_t sep_resid_tiles(const SolveParams& p);
 
 // ---- launchers (k_gram.cu) ----

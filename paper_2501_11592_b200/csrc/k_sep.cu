@@ -26,7 +26,7 @@ struct Gemm {
   double* C;
   int64_t csx, csy, csb;
   int64_t X, Y, K;
-  int mode;  // 0 store, 1 |.|, 2 residual (acc - yref), split + sum of squares
+  int mode;  // 0 store, 1 |.|, 2 residual (acc - yref) + sum of squares, 3 acc - yref
   const double* yref;
   double* lpart;
   int64_t tiles;  // tiles per batch entry (lpart stride)
@@ -49,31 +49,44 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Operands with arbitrary strides; tiles are staged as Ps[k][x] with row stride
 // 68 doubles, for which the A / B fragment reads (lane -> k = lane % 4,
 // x = lane / 4) hit 16 distinct 8-byte slots per half warp: conflict-free.
-constexpr int GLD = GT + 4;
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 256;
 
+// TX x 64 output tile (TX = 64 or 128 rows of X): eight warps as TX/32 x 256/TX,
+// each a 32 x (64 TX / 256 ... ) sub-tile of 8 x 8 accumulator blocks.  At these
+// shapes (K = 128..512, operands L2-resident) the kernel is bound by the bytes
+// a CTA pulls from L2 per FLOP, so the 128-row tile (10.7 FLOP/B instead of 8)
+// is used wherever the output has 128 rows to give.
+template <int TX>
 __global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
   const int64_t b = blockIdx.y;
   if (g.active && !g.active[b]) return;
-  __shared__ __align__(16) double Ps[2][GK][GLD];
-  __shared__ __align__(16) double Qs[2][GK][GLD];
+  constexpr int PLD = TX + 4, QLD = GT + 4;
+  extern __shared__ __align__(16) double gsm[];
+  double* Ps = gsm;                      // [2][GK][PLD]
+  double* Qs = gsm + 2 * GK * PLD;       // [2][GK][QLD]
   __shared__ double red[kGemmThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wx = (warp & 1) * 32, wy = (warp >> 1) * 32;  // quadrant origin (x, y)
-  const int64_t tiles_x = (g.X + GT - 1) / GT;
-  const int64_t x0 = (blockIdx.x % tiles_x) * GT, y0 = (blockIdx.x / tiles_x) * GT;
+  constexpr int WX = TX / 32;            // warps along x
+  constexpr int NJ = GT / (8 / WX) / 8;  // 8-wide accumulator blocks along y per warp
+  const int wx = (warp % WX) * 32, wy = (warp / WX) * (8 * NJ);
+  const int64_t tiles_x = (g.X + TX - 1) / TX;
+  const int64_t x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * GT;
   const double* P = g.P + b * g.psb;
   const double* Q = g.Q + b * g.qsb;
   const bool p_kfast = g.psk == 1, q_kfast = g.qsk == 1;
-  constexpr int PER = GT * GK / kGemmThreads;  // 8 elements of each operand per thread
-  double pv[PER], qv[PER];
+  constexpr int PPER = TX * GK / kGemmThreads, QPER = GT * GK / kGemmThreads;
+  double pv[PPER], qv[QPER];
   auto fetch = [&](int64_t k0) {
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
+    for (int u = 0; u < PPER; ++u) {
       const int e = tid + kGemmThreads * u;
-      const int xx = p_kfast ? e / GK : e % GT, kk = p_kfast ? e % GK : e / GT;
+      const int xx = p_kfast ? e / GK : e % TX, kk = p_kfast ? e % GK : e / TX;
       const int64_t x = x0 + xx, k = k0 + kk;
       pv[u] = (x < g.X && k < g.K) ? P[x * g.psx + k * g.psk] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < QPER; ++u) {
+      const int e = tid + kGemmThreads * u;
       const int yy = q_kfast ? e / GK : e % GT, kq = q_kfast ? e % GK : e / GT;
       const int64_t y = y0 + yy, k2 = k0 + kq;
       qv[u] = (y < g.Y && k2 < g.K) ? Q[y * g.qsy + k2 * g.qsk] : 0.0;
@@ -81,19 +94,23 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
+    for (int u = 0; u < PPER; ++u) {
       const int e = tid + kGemmThreads * u;
-      const int xx = p_kfast ? e / GK : e % GT, kk = p_kfast ? e % GK : e / GT;
-      Ps[buf][kk][xx] = pv[u];
+      const int xx = p_kfast ? e / GK : e % TX, kk = p_kfast ? e % GK : e / TX;
+      Ps[(buf * GK + kk) * PLD + xx] = pv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < QPER; ++u) {
+      const int e = tid + kGemmThreads * u;
       const int yy = q_kfast ? e / GK : e % GT, kq = q_kfast ? e % GK : e / GT;
-      Qs[buf][kq][yy] = qv[u];
+      Qs[(buf * GK + kq) * QLD + yy] = qv[u];
     }
   };
-  double acc[4][4][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int fk = lane & 3, fr = lane >> 2;
   fetch(0);
   stash(0);
@@ -104,15 +121,15 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
     if (more) fetch(k0 + GK);
 #pragma unroll
     for (int ks = 0; ks < GK; ks += 4) {
-      double af[4], bf[4];
+      double af[4], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = Ps[buf][ks + fk][wx + 8 * i + fr];
+      for (int i = 0; i < 4; ++i) af[i] = Ps[(buf * GK + ks + fk) * PLD + wx + 8 * i + fr];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Qs[buf][ks + fk][wy + 8 * j + fr];
+      for (int j = 0; j < NJ; ++j) bf[j] = Qs[(buf * GK + ks + fk) * QLD + wy + 8 * j + fr];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
           asm volatile(
               "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
               : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
@@ -124,10 +141,35 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
   // accumulator block (i, j): element (row = fr, cols 2 fk, 2 fk + 1)
   double* C = g.C + b * g.csb;
   double ss = 0.0;
+  // Outputs contiguous along y (the MMA's column pair c0, c1 of a lane is two
+  // adjacent doubles): one 16-byte access per pair, so four lanes cover 64
+  // contiguous bytes instead of half of each 32-byte sector (the scalar
+  // epilogue's yref reads were 37 % of this kernel's stall samples).
+  const bool pair_ok = g.csy == 1 && (g.csx & 1) == 0 && (g.csb & 1) == 0 && (g.Y & 1) == 0 &&
+                       (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && g.mode != 1 &&
+                       (g.mode == 0 || (reinterpret_cast<uintptr_t>(g.yref) & 15) == 0);
+  if (pair_ok) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int64_t x = x0 + wx + 8 * i + fr, y = y0 + wy + 8 * j + 2 * fk;
+        if (x >= g.X || y >= g.Y) continue;
+        const int64_t o = x * g.csx + y;
+        double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (g.mode >= 2) {
+          const double2 r = *reinterpret_cast<const double2*>(g.yref + b * g.csb + o);
+          v.x -= r.x;
+          v.y -= r.y;
+          if (g.mode == 2) ss = fma(v.y, v.y, fma(v.x, v.x, ss));
+        }
+        *reinterpret_cast<double2*>(C + o) = v;
+      }
+  } else
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t x = x0 + wx + 8 * i + fr, y = y0 + wy + 8 * j + 2 * fk + h;
@@ -139,6 +181,8 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_sep(Gemm g) {
         } else if (g.mode == 2) {
           v -= g.yref[b * g.csb + o];
           ss = fma(v, v, ss);
+        } else if (g.mode == 3) {
+          v -= g.yref[b * g.csb + o];
         }
         C[o] = v;
       }
@@ -360,6 +404,25 @@ unsigned tiles2(int64_t X, int64_t Y) {
   return (unsigned)(((X + GT - 1) / GT) * ((Y + GT - 1) / GT));
 }
 
+// 128-row tiles wherever the output has them to give; the residual GEMM (mode
+// 2) keeps 64 x 64 so its loss partials stay tiles2(m_r, m_c) per image.
+void launch_gemm(const Gemm& g, int64_t B, cudaStream_t s) {
+  static DevSlots attr_set[2];
+  const int dev = current_device();
+  if (g.mode != 2 && g.X >= 128) {
+    constexpr size_t smem = (size_t)2 * GK * (128 + 4 + GT + 4) * sizeof(double);
+    if (attr_set[1].get(dev) == 0) {
+      cudaFuncSetAttribute(k_gemm_sep<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set[1].set(dev, 1);
+    }
+    const unsigned tiles = (unsigned)(((g.X + 127) / 128) * ((g.Y + GT - 1) / GT));
+    k_gemm_sep<128><<<dim3(tiles, (unsigned)B), kGemmThreads, smem, s>>>(g);
+  } else {
+    constexpr size_t smem = (size_t)2 * GK * (64 + 4 + GT + 4) * sizeof(double);
+    k_gemm_sep<64><<<dim3(tiles2(g.X, g.Y), (unsigned)B), kGemmThreads, smem, s>>>(g);
+  }
+}
+
 }  // namespace
 
 void launch_sep_control(const SolveParams& p, const Work& w, int outer, cudaStream_t s);
@@ -387,7 +450,7 @@ void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
   g1.K = p.mc;
   g1.mode = 0;
   g1.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
+  launch_gemm(g1, p.B, s);
   // stage 2: S_b[i][j] = sum_qr A_r[qr][i] U_b[j][qr], stored at p = i + nr*j
   Gemm g2{};
   g2.P = w.at_r64;
@@ -407,7 +470,7 @@ void launch_sep_corr(const SolveParams& p, const Work& w, const double* r_src,
   g2.K = p.mr;
   g2.mode = abs_scores ? 1 : 0;
   g2.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g2.X, g2.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g2);
+  launch_gemm(g2, p.B, s);
 }
 
 bool launch_sep_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
@@ -430,7 +493,7 @@ bool launch_sep_corr_tc(const SolveParams& p, const Work& w, cudaStream_t s) {
   g1.K = p.mc;
   g1.mode = 0;
   g1.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
+  launch_gemm(g1, p.B, s);
   const int64_t rows = p.B * p.nc;
   k_sep_split_u<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(p, w);
   // stage 2 on tcgen05: scores(i, j) = a_r,i . U_j for every row as its own
@@ -480,9 +543,39 @@ static void launch_dir_resid_gemm(const SolveParams& p, const Work& w, const dou
   g.lpart = w.lpart;
   g.tiles = tiles2(p.mr, p.mc);
   g.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g.X, g.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g);
+  launch_gemm(g, p.B, s);
 }
 
+// Z2_b = Y_b A_c (once per solve): the constant part of U = R A_c.
+void launch_sep_direct_prepare(const SolveParams& p, const Work& w, cudaStream_t s) {
+  Gemm g1{};
+  g1.P = w.at_c64;
+  g1.psx = p.ldc;
+  g1.psk = 1;
+  g1.psb = 0;
+  g1.Q = w.y64;
+  g1.qsy = 1;
+  g1.qsk = p.mr;
+  g1.qsb = p.ldm;
+  g1.C = w.sep_z2;
+  g1.csx = p.mr;
+  g1.csy = 1;
+  g1.csb = p.nc * p.mr;
+  g1.X = p.nc;
+  g1.Y = p.mr;
+  g1.K = p.mc;
+  g1.mode = 0;
+  g1.active = nullptr;
+  launch_gemm(g1, p.B, s);
+}
+
+// One epoch = the product(s) forming U = R A_c and one column kernel.  With
+// R = V A_c^T - Y,
+//   U = R A_c = V (A_c^T A_c) - Y A_c = V Gc - Z2,
+// so when n_c <= 2 m_c the two m_r x n_c x m_c products collapse into one
+// m_r x n_c x n_c product with the factor Gram Gc the context already holds (the
+// same regrouping as the 1D Gram form's G c - b; the residual itself is then
+// only formed at the end of the iteration, launch_sep_resid).
 int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int bound,
                             cudaStream_t s) {
   (void)bound;
@@ -491,28 +584,54 @@ int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int 
   double* vt = w.sep_scratch;
   double* u = w.sep_scratch2;
   k_dir_colstep<0, false><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, 0);  // V of the current c
+  // n_c <= 2 m_c: the regrouped product is no more work than the two it
+  // replaces (m_r n_c^2 against 2 m_r m_c n_c) and saves a launch per epoch
+  const bool regroup = p.nc <= 2 * p.mc;
   for (int e = 0; e < p.inner; ++e) {
-    launch_dir_resid_gemm(p, w, vt, s);
-    // U_b[j][qr] = sum_qc A_c[qc][j] R_b[qr][qc]
-    Gemm g1{};
-    g1.P = w.at_c64;
-    g1.psx = p.ldc;
-    g1.psk = 1;
-    g1.psb = 0;
-    g1.Q = w.r64;
-    g1.qsy = 1;
-    g1.qsk = p.mr;
-    g1.qsb = p.ldm;
-    g1.C = u;
-    g1.csx = p.mr;
-    g1.csy = 1;
-    g1.csb = p.nc * p.mr;
-    g1.X = p.nc;
-    g1.Y = p.mr;
-    g1.K = p.mc;
-    g1.mode = 0;
-    g1.active = w.active;
-    k_gemm_sep<<<dim3(tiles2(g1.X, g1.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g1);
+    if (regroup) {
+      // U_b[j][qr] = sum_j' Gc[j][j'] V_b[j'][qr] - Z2_b[j][qr]
+      Gemm g{};
+      g.P = w.gc;
+      g.psx = p.nc;
+      g.psk = 1;
+      g.psb = 0;
+      g.Q = vt;
+      g.qsy = 1;
+      g.qsk = p.mr;
+      g.qsb = p.nc * p.mr;
+      g.C = u;
+      g.csx = p.mr;
+      g.csy = 1;
+      g.csb = p.nc * p.mr;
+      g.X = p.nc;
+      g.Y = p.mr;
+      g.K = p.nc;
+      g.mode = 3;
+      g.yref = w.sep_z2;
+      g.active = w.active;
+      launch_gemm(g, p.B, s);
+    } else {
+      launch_dir_resid_gemm(p, w, vt, s);  // R = V A_c^T - Y
+      Gemm g1{};                           // U_b[j][qr] = sum_qc A_c[qc][j] R_b[qr][qc]
+      g1.P = w.at_c64;
+      g1.psx = p.ldc;
+      g1.psk = 1;
+      g1.psb = 0;
+      g1.Q = w.r64;
+      g1.qsy = 1;
+      g1.qsk = p.mr;
+      g1.qsb = p.ldm;
+      g1.C = u;
+      g1.csx = p.mr;
+      g1.csy = 1;
+      g1.csb = p.nc * p.mr;
+      g1.X = p.nc;
+      g1.Y = p.mr;
+      g1.K = p.mc;
+      g1.mode = 0;
+      g1.active = w.active;
+      launch_gemm(g1, p.B, s);
+    }
     const int step = (outer - 1) * p.inner + e;
     switch (p.opt) {  // the step and the next V in one pass over the columns
       case 0: k_dir_colstep<0, true><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, step); break;
@@ -520,7 +639,7 @@ int launch_sep_direct_learn(const SolveParams& p, const Work& w, int outer, int 
       default: k_dir_colstep<2, true><<<cgrid, 32 * kDirWarps, 0, s>>>(p, w, u, vt, step); break;
     }
   }
-  return 2 + 3 * p.inner;
+  return 2 + (regroup ? 2 : 3) * p.inner;
 }
 
 int64_t sep_resid_tiles(const SolveParams& p) { return tiles2(p.mr, p.mc); }
@@ -556,7 +675,7 @@ void launch_sep_resid(const SolveParams& p, const Work& w, int outer, int tb,
   g.lpart = w.lpart;
   g.tiles = sep_resid_tiles(p);
   g.active = w.active;
-  k_gemm_sep<<<dim3(tiles2(g.X, g.Y), (unsigned)p.B), kGemmThreads, 0, s>>>(g);
+  launch_gemm(g, p.B, s);
   launch_sep_control(p, w, outer, s);
 }
 
