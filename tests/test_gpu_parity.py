@@ -598,3 +598,43 @@ def test_tie_grown_supports_fast_path(gpu_available):
         assert np.array_equal(r.mask[:, b], ref["mask"][:, q]), f"signal {b}: support"
         assert r.iterations[b] == ref["iterations"][q]
         assert rel_coef_err(r.s[:, b], ref["s"][:, q]) <= 1e-9
+
+
+@pytest.mark.parametrize("B", [3, 200, 500])
+@pytest.mark.parametrize("opt,th,m,n", [(cl.PLAIN, 1.0, 48, 160), (cl.ADAM, 1.0, 48, 160),
+                                        (cl.MOMENTUM, 1.0, 48, 160), (cl.ADAM, 0.7, 24, 32)])
+def test_fused_small_solve_staged_and_global_dictionary(gpu_available, B, opt, th, m, n):
+    """The one-kernel small solve (init, iterations and result compaction on
+    chip) against the oracle and the batched pipeline: B = 3 stages the
+    dictionary measurement-major in shared memory, B = 200 / 500 (more signals
+    than SMs) read it atom-major from L2; exact ties (a duplicated atom), th < 1
+    multi-atom injections, Adam / momentum moments kept on chip."""
+    # n = 160 / m = 48: ragged ballot words and row chunks; th < 1 needs a
+    # capacity (= n) within the 32-atom learners, hence the 32-atom dictionary
+    k = 7 if n > 32 else 4
+    A, X, Y, _ = cl.gen_problem_1d(77, m, n, k, B, snr_db=30.0)
+    A[:, n - 5] = A[:, 12]  # exact tie whenever atom 12 wins
+    cfg = cl.ClompConfig.baseline(k)
+    cfg.opt, cfg.th = opt, th
+    if opt != cl.PLAIN:
+        cfg.lr, cfg.inner_steps = 0.02, 60
+    if th < 1.0:
+        cfg.max_outer = 4
+    fused = cl.ClompContext(A)
+    r = cl.clomp_solve_batch(fused, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert fused.stats()["corr_path"] == 2 and fused.stats()["kernel_launches"] == 1
+    batched = cl.ClompContext(A)
+    batched.set_fused(False)
+    q = cl.clomp_solve_batch(batched, Y, cfg, mode=cl.MODE_PER_SIGNAL)
+    assert np.array_equal(r.mask, q.mask)
+    assert np.array_equal(r.iterations, q.iterations)
+    assert np.array_equal(r.converged, q.converged)
+    assert np.array_equal(r.status, q.status)
+    assert rel_coef_err(r.s, q.s) <= 1e-9
+    np.testing.assert_allclose(r.final_residual_norm, q.final_residual_norm, rtol=1e-7, atol=1e-12)
+    idx = list(range(min(B, 6)))
+    ref = refbind.orc_solve(A.astype(np.float64), Y[:, idx].astype(np.float64), cfg,
+                            mode=refbind.MODE_PER_SIGNAL)
+    assert np.array_equal(r.mask[:, idx], ref["mask"])
+    assert np.array_equal(r.iterations[idx], ref["iterations"])
+    assert rel_coef_err(r.s[:, idx], ref["s"]) <= 1e-9
