@@ -318,6 +318,9 @@ int cl_debug_scores(cl_ctx* ctx, const float* r, int64_t batch, int path,
 
 int cl_abi_version(void);
 int cl_device_count(void);
+/* sizeof cl_config, cl_result, cl_device_result, cl_stats as this library was
+ * compiled: bindings in other languages check their struct mirrors against it. */
+void cl_abi_struct_sizes(int64_t out[4]);
 
 #ifdef __cplusplus
 }

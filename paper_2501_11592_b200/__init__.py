@@ -137,7 +137,7 @@ EXPORTED = [
     "cl_create_group", "cl_destroy_group", "cl_group_size", "cl_group_context",
     "cl_group_last_error", "cl_group_solve_batch",
     "cl_gen_problem_2d", "cl_dct_basis",
-    "cl_abi_version", "cl_device_count", "cl_rng_draws", "cl_gen_problem_1d",
+    "cl_abi_version", "cl_device_count", "cl_abi_struct_sizes", "cl_rng_draws", "cl_gen_problem_1d",
 ]
 
 _lib_handle = None

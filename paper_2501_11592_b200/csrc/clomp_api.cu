@@ -1026,6 +1026,14 @@ extern "C" {
 
 int cl_abi_version(void) { return CL_ABI_VERSION; }
 
+void cl_abi_struct_sizes(int64_t out[4]) {
+  if (!out) return;
+  out[0] = (int64_t)sizeof(cl_config);
+  out[1] = (int64_t)sizeof(cl_result);
+  out[2] = (int64_t)sizeof(cl_device_result);
+  out[3] = (int64_t)sizeof(cl_stats);
+}
+
 int cl_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {

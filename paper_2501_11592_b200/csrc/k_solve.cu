@@ -860,8 +860,10 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
         r[4 * q + 1] -= y01.y;
         r[4 * q + 2] -= y23.x;
         r[4 * q + 3] -= y23.y;
+#ifndef CL_EXP_NO_R64  // timing experiment: skip the fp64 residual store
         *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
         *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
+#endif
 #pragma unroll
         for (int e = 0; e < 4; ++e) lacc = fma(r[4 * q + e], r[4 * q + e], lacc);
       }

@@ -31,6 +31,16 @@ def test_library_exports_every_declared_symbol(built_lib):
     assert h.cl_abi_version() == 1
 
 
+def test_python_struct_mirrors_match_the_library(built_lib):
+    """The ctypes mirrors have the library's struct sizes (a field added on one
+    side only would shift every later pointer)."""
+    h = C.CDLL(str(built_lib))
+    out = (C.c_int64 * 4)()
+    h.cl_abi_struct_sizes(out)
+    assert list(out) == [C.sizeof(cl.CConfig), C.sizeof(cl.CResult), C.sizeof(cl.CDeviceResult),
+                         C.sizeof(cl.CStats)]
+
+
 def test_default_config_matches_reference(built_lib):
     c = cl.CConfig()
     cl.lib().cl_config_default(C.byref(c))
