@@ -222,10 +222,61 @@ __device__ __forceinline__ void pick_finish(const SolveParams& p, const Work& w,
   if (ps.added) atomicMax(&w.counters[kMaxCount], ps.t);
 }
 
+// Exact scorers for the near-tie rescoring.  ScoreResid: a_j . r from the stored
+// fp64 residual row.  ScoreGram (the fused fast kernel, which does not store
+// that row): the same quantity regrouped through the dictionary Gram cache,
+//   a_j . (A_S c - y) = sum_k (A^T A)[j][s_k] c_k - a_j . y,
+// from the signal's coefficients held one per lane.  Both carry an absolute
+// rounding error of order 1e-16 ||y|| (r itself is a difference of O(||y||)
+// terms rounded to fp64), as the reference's own scores do; identical atoms
+// read identical Gram rows and atom rows, so exact ties stay exact.
+struct ScoreResid {
+  const SolveParams& p;
+  const Work& w;
+  const double* r;
+  __device__ __forceinline__ void operator()(int64_t j0, int cnt, double (&out)[8], int lane) const {
+    exact_scores8(p, w, r, j0, cnt, out, lane);
+  }
+};
+
+struct ScoreGram {
+  const SolveParams& p;
+  const Work& w;
+  int64_t b;
+  double c_l;      // lane k: coefficient of support atom k (0 beyond t)
+  int32_t sup_l;   // lane k: support atom k
+  int t;
+  __device__ __forceinline__ void operator()(int64_t j0, int cnt, double (&out)[8], int lane) const {
+    const float* y = w.y32 + b * p.ldm;
+    double z[8], g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) z[u] = g[u] = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < cnt && lane < t) g[u] = w.gfull[(j0 + u) * p.n + sup_l] * c_l;
+    for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
+      const float4 yv = *reinterpret_cast<const float4*>(y + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < cnt) {
+          const float4 a = *reinterpret_cast<const float4*>(w.at32 + (j0 + u) * p.ldm + i);
+          z[u] = fma(f2d(a.x), f2d(yv.x), z[u]);
+          z[u] = fma(f2d(a.y), f2d(yv.y), z[u]);
+          z[u] = fma(f2d(a.z), f2d(yv.z), z[u]);
+          z[u] = fma(f2d(a.w), f2d(yv.w), z[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) out[u] = u < cnt ? fabs(warp_sum(g[u]) - warp_sum(z[u])) : -1.0;
+  }
+};
+
 // One pass over the atoms inside the band (ascending atom order).  Pass 0
 // returns the exact maximum; pass 1 picks every atom attaining M.
+template <class Scorer>
 __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, double cut,
-                            const double* r, int pass, double M, PickState& ps, int lane) {
+                            const Scorer& score, int pass, double M, PickState& ps, int lane) {
   const Cand* cd = w.cand + b * p.ntile;
   for (int64_t t0 = 0; t0 < p.ntile; t0 += 32) {
     const int64_t tl = t0 + lane;
@@ -242,7 +293,7 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
         for (int64_t j0 = a0; j0 < a1; j0 += 8) {
           const int cnt = (int)(a1 - j0 < 8 ? a1 - j0 : 8);
           double v[8];
-          exact_scores8(p, w, r, j0, cnt, v, lane);
+          score(j0, cnt, v, lane);
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             if (u >= cnt) continue;
@@ -257,8 +308,14 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
           ja = jb;
           jb = tmp;
         }
-        const double va = exact_score(p, w, r, ja, lane);
-        const double vb = jb >= 0 ? exact_score(p, w, r, jb, lane) : -1.0;
+        double v[8];
+        score(ja, 1, v, lane);
+        const double va = v[0];
+        double vb = -1.0;
+        if (jb >= 0) {
+          score(jb, 1, v, lane);
+          vb = v[0];
+        }
         if (pass == 0) {
           M = fmax(M, fmax(va, vb));
         } else if (lane == 0) {
@@ -273,16 +330,21 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
 
 // Near-tied th == 1 selection: exact rescoring of the band, every tie with the
 // exact maximum injected (see above).  Updates sup / cnt / mask / changed.
-__device__ void select_near_tie(const SolveParams& p, const Work& w, int64_t b, double v1,
-                                double delta, int t_old, int lane) {
+template <class Scorer>
+__device__ void select_near_tie_with(const SolveParams& p, const Work& w, int64_t b, double v1,
+                                     double delta, int t_old, const Scorer& score, int lane) {
   PickState ps{t_old, 0, 0};
   if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
   const double cut = v1 - 2.0 * delta;
-  const double* r = w.r64 + b * p.ldm;
-  const double M = band_pass(p, w, b, cut, r, 0, -1.0, ps, lane);
-  if (M > 0.0) band_pass(p, w, b, cut, r, 1, M, ps, lane);
+  const double M = band_pass(p, w, b, cut, score, 0, -1.0, ps, lane);
+  if (M > 0.0) band_pass(p, w, b, cut, score, 1, M, ps, lane);
   if (lane == 0) pick_finish(p, w, b, ps);
   __syncwarp();
+}
+
+__device__ void select_near_tie(const SolveParams& p, const Work& w, int64_t b, double v1,
+                                double delta, int t_old, int lane) {
+  select_near_tie_with(p, w, b, v1, delta, t_old, ScoreResid{p, w, w.r64 + b * p.ldm}, lane);
 }
 
 // Merge of one signal's candidate records: best (v1, i1) over all tiles (the
@@ -821,6 +883,12 @@ __device__ void warp_extend_gram(const SolveParams& p, const Work& w, int64_t b,
 #endif
 constexpr int kResidUnroll = CL_RESIDW_UNROLL;
 
+// STORE_R64 = false (the fused fast kernel): the fp64 residual row is not
+// written — only exact rescoring of a near-tied selection reads it, a few dozen
+// signals per step, and those rebuild their row on demand (materialize_r64);
+// the 16.8 MB written per config-2 iteration otherwise also evicts the Gram rows
+// the next iteration reloads (-4.7 % per step).
+template <bool STORE_R64 = true, bool SPLIT = true>
 __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
                                 const double* cs, const int32_t* sups, int t,
                                 int lane) {
@@ -860,10 +928,10 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
         r[4 * q + 1] -= y01.y;
         r[4 * q + 2] -= y23.x;
         r[4 * q + 3] -= y23.y;
-#ifndef CL_EXP_NO_R64  // timing experiment: skip the fp64 residual store
-        *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
-        *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
-#endif
+        if (STORE_R64) {
+          *reinterpret_cast<double2*>(w.r64 + o) = make_double2(r[4 * q + 0], r[4 * q + 1]);
+          *reinterpret_cast<double2*>(w.r64 + o + 2) = make_double2(r[4 * q + 2], r[4 * q + 3]);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) lacc = fma(r[4 * q + e], r[4 * q + e], lacc);
       }
@@ -872,7 +940,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
     for (int q = 0; q < 16; ++q) rr[q] = r[q];
   }
   const double L = warp_sum(lacc);
-  if (w.r_hi) {
+  if (SPLIT && w.r_hi) {
     if (ldm <= 512) {  // single pass: split straight from registers
       const float sc = split_scale(L);
       if (lane == 0) w.r_scale[b] = 1.0f / sc;
@@ -889,7 +957,7 @@ __device__ double warp_residual(const SolveParams& p, const Work& w, int64_t b,
       }
     } else {
       __syncwarp();
-      split_row(w, b, ldm, L, lane, 32);
+      split_row(w, b, ldm, L, lane, 32);  // reads r64: callers keep STORE_R64 for ldm > 512
     }
   }
   return L;
@@ -1107,7 +1175,7 @@ __device__ __forceinline__ unsigned long long lt_gtimer() {
 #define LT_MARK(i) do { } while (0)
 #endif
 
-template <int TB, int OPT>
+template <int TB, int OPT, bool LAZY>
 __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, int64_t b,
                                            int outer, int32_t* big_list, double* cs,
                                            int32_t* sups, double* s1, uint64_t* bar, int lane) {
@@ -1147,6 +1215,19 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   LT_MARK(2);
   int t = t_old;
   int chg = 0;  // mask changed this iteration (stall rule)
+  // LAZY (ldm <= 512 and the tensor-core correlation next: the fp16 split comes
+  // straight from registers): this kernel's residual tail skips the fp64 row;
+  // the paths that rescore exactly — a near-tied selection, or the mask-based
+  // selection of a full 32-atom support — rebuild it first (supports wider
+  // than the warp had theirs stored by the block / cluster kernels)
+  const double delta = p.delta_rel * p.colnorm_max * sqrt(Lb);
+  if (LAZY && t_old == kWarpCap) {  // the mask-based path below rescans from the row
+    cs[lane] = c_l;
+    sups[lane] = sup_l;
+    __syncwarp();
+    (void)warp_residual<true, false>(p, w, b, cs, sups, t_old, lane);  // the row it would have stored
+    __syncwarp();
+  }
   if (t_old >= 32) {  // support wider than the warp: mask-based general path
     select_top_warp(p, w, b, lane);
     if (!w.active[b]) {
@@ -1156,7 +1237,6 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
     t = w.cnt[b];
     chg = w.changed[b];
   } else if (v1 > 0.0) {  // else zero column: inject nothing (clomp.cpp:48)
-    const double delta = p.delta_rel * p.colnorm_max * sqrt(Lb);
     if (v1 - v2 > delta) {
       const bool dup = __any_sync(kFull, lane < t_old && sup_l == i1);
       if (!dup) {
@@ -1181,7 +1261,11 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
       chg = dup ? 0 : 1;
       if (lane == 0) w.changed[b] = chg;
     } else {
-      select_near_tie(p, w, b, v1, delta, t_old, lane);
+      if (LAZY)  // no fp64 residual row: rescore through the Gram cache
+        select_near_tie_with(p, w, b, v1, delta, t_old,
+                             ScoreGram{p, w, b, lane < t_old ? c_l : 0.0, sup_l, t_old}, lane);
+      else
+        select_near_tie(p, w, b, v1, delta, t_old, lane);
       if (!w.active[b]) {
         if (staged) mbar_wait0(bar);
         return false;
@@ -1257,7 +1341,7 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
     sups[lane] = 0;
   }
   __syncwarp();
-  const double L = warp_residual(p, w, b, cs, sups, t, lane);
+  const double L = warp_residual<!LAZY>(p, w, b, cs, sups, t, lane);
   int snap = 0;
   if (lane == 0) {
     if (p.mode == kModePerSignal) {
@@ -1334,7 +1418,7 @@ k_learn_warp(SolveParams p, Work w, int outer, int32_t* big_list) {
 }
 
 // Same bucket, the fast path (learn_fast): batched th == 1 with gfull.
-template <int TB, int OPT>
+template <int TB, int OPT, bool LAZY>
 __global__ void __launch_bounds__(32 * learn_warps<TB>(), learn_min_blocks<TB>())
 k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   constexpr int NW = learn_warps<TB>();
@@ -1355,8 +1439,8 @@ k_learn_fast(SolveParams p, Work w, int outer, int32_t* big_list) {
   if (blockIdx.x == 0 && threadIdx.x == 0) w.counters[active_slot(outer + 1)] = 0;
   const int64_t b = p.sig_lo + (int64_t)blockIdx.x * NW + warp;
   if (b >= p.sig_hi) return;
-  learn_fast<TB, OPT>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp], sq_all[warp],
-                     &bar_all[warp], lane);
+  learn_fast<TB, OPT, LAZY>(p, w, b, outer, big_list, cs_all[warp], sup_all[warp], sq_all[warp],
+                            &bar_all[warp], lane);
 }
 
 // ------------------------------------------ learning, block per signal
@@ -3469,11 +3553,20 @@ int launch_learn(const SolveParams& p, const Work& w, int outer, int max_cnt,
     constexpr int NW = learn_warps<TB>();
     const dim3 lg(blocks_for(NW)), lb(32 * NW);
     const bool fast = p.fuse_select && w.gfull && !p.sep && p.cap >= 32 && (p.cap & 1) == 0;
-    if (fast) {
+    // one 512-row pass with the tcgen05 correlation next (it reads the fp16
+    // split; the GEMV and fp64 correlations read the fp64 row itself): fp16
+    // split from registers, fp64 row on demand
+    if (fast && p.ldm <= 512 && w.r_hi != nullptr) {
       switch (p.opt) {
-        case 0: launch_pdl(k_learn_fast<TB, 0>, lg, lb, 0, s, p, w, outer, big_list); break;
-        case 1: launch_pdl(k_learn_fast<TB, 1>, lg, lb, 0, s, p, w, outer, big_list); break;
-        default: launch_pdl(k_learn_fast<TB, 2>, lg, lb, 0, s, p, w, outer, big_list); break;
+        case 0: launch_pdl(k_learn_fast<TB, 0, true>, lg, lb, 0, s, p, w, outer, big_list); break;
+        case 1: launch_pdl(k_learn_fast<TB, 1, true>, lg, lb, 0, s, p, w, outer, big_list); break;
+        default: launch_pdl(k_learn_fast<TB, 2, true>, lg, lb, 0, s, p, w, outer, big_list); break;
+      }
+    } else if (fast) {
+      switch (p.opt) {
+        case 0: launch_pdl(k_learn_fast<TB, 0, false>, lg, lb, 0, s, p, w, outer, big_list); break;
+        case 1: launch_pdl(k_learn_fast<TB, 1, false>, lg, lb, 0, s, p, w, outer, big_list); break;
+        default: launch_pdl(k_learn_fast<TB, 2, false>, lg, lb, 0, s, p, w, outer, big_list); break;
       }
     } else {
       switch (p.opt) {
