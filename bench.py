@@ -665,7 +665,7 @@ def run_ours(args, rank, world, local_rank):
             "frac": achieved / peak,
             "traffic": 10.57e6 if prof["corr_path"] == 1 and args.config == 2 else None,
             "traffic_note": ("ncu dram__bytes_read+write per launch (10.57 MB read, 0 written; "
-                             "algorithmic 10.49 MB), profiles/r2/r2_k1.summary.txt"
+                             "algorithmic 10.49 MB), profiles/r2/final/k1.summary.txt"
                              if prof["corr_path"] == 1 and args.config == 2 else None),
             "peak_source": peak_src,
             "algorithmic_per_launch": f"2*N*M*B = {corr_flops:.3e} FLOP",
@@ -697,11 +697,11 @@ def run_ours(args, rank, world, local_rank):
             "bound": "fp64", "achieved": learn_flops / (learn_ms / 1e3) / 1e12,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": learn_flops / (learn_ms / 1e3) / 1e12 / fp64_peak,
-            "traffic": 53.96e6 if args.config == 2 and prof["corr_path"] == 1 else None,
-            "traffic_note": ("ncu dram__bytes_read+write per launch of k_learn_fast<32,0> at t = 30 "
-                             "(the largest learning launches, t = 17..32: 51.4 MB read, 2.5 MB "
+            "traffic": 52.82e6 if args.config == 2 and prof["corr_path"] == 1 else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch of k_learn_fast<32,0,1> at t = 30 "
+                             "(the largest learning launches, t = 17..32: 51.5 MB read, 1.4 MB "
                              "written: the support Gram rows, per-signal state and y; the atom "
-                             "gathers of the residual are L2 hits), profiles/r2/r2_learn32.summary.txt"),
+                             "gathers of the residual are L2 hits), profiles/r2/final/learn32.summary.txt"),
             "peak_source": "derived fp64 pipe: 148 SM x 64 DFMA/clk x 2 x SM clock under load",
             "algorithmic_per_step": (f"B * sum_t (2 E t^2 + 2 m t), t = 1..{outers}, E = {E} "
                                      f"= {learn_flops:.4e} FLOP"),

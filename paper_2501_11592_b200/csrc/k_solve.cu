@@ -1358,8 +1358,17 @@ __device__ __forceinline__ bool learn_fast(const SolveParams& p, const Work& w, 
   return false;
 }
 
+#ifndef CL_LEARN_NW32
+#define CL_LEARN_NW32 2
+#endif
+#ifndef CL_LEARN_NW16
+#define CL_LEARN_NW16 4
+#endif
+#ifndef CL_LEARN_NW8
+#define CL_LEARN_NW8 4
+#endif
 template <int TB>
-constexpr int learn_warps() { return TB == 32 ? 2 : 4; }
+constexpr int learn_warps() { return TB == 32 ? CL_LEARN_NW32 : (TB == 16 ? CL_LEARN_NW16 : CL_LEARN_NW8); }
 
 #ifndef CL_LEARN32_MINB
 #define CL_LEARN32_MINB 8
@@ -1507,9 +1516,9 @@ k_learn_block(SolveParams p, Work w, int outer, const int32_t* big_list, int ski
       } else {
         for (int i = warp; i <= k; i += nw) {
           const float* ai = w.at32 + (int64_t)sups[i] * p.ldm;
+          const float* ak = w.at32 + (int64_t)sups[k] * p.ldm;
           double acc = 0.0;
-          for (int64_t q = lane; q < p.ldm; q += 32)
-            acc = fma((double)w.at32[(int64_t)sups[k] * p.ldm + q], (double)w.at32[(int64_t)sups[i] * p.ldm + q], acc);
+          for (int64_t q = lane; q < p.ldm; q += 32) acc = fma((double)ak[q], (double)ai[q], acc);
           acc = warp_sum(acc);
           if (lane == 0) {
             G[(int64_t)k * cap + i] = acc;
@@ -1669,23 +1678,6 @@ __device__ __forceinline__ double warp_reduce_rows_t(double (&v)[RW], int lane) 
 #pragma unroll
   for (int o = 16 >> kLog; o >= 1; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
   return x;
-}
-
-__device__ __forceinline__ double warp_reduce8_t(double (&v)[8], int lane) {
-#pragma unroll
-  for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      const double send = up ? v[i] : v[i + h];
-      const double keep = up ? v[i + h] : v[i];
-      v[i] = keep + __shfl_xor_sync(kFull, send, o);
-    }
-  }
-  double x = v[0];
-  x += __shfl_xor_sync(kFull, x, 2);
-  x += __shfl_xor_sync(kFull, x, 1);
-  return x;  // lanes 4i..4i+3: row i of the warp's 8 rows
 }
 
 template <int Q>

@@ -20,5 +20,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file
 python tools/launches.py gpurun_out/final/cfg1_launches.csv > gpurun_out/final/cfg1_launches.txt
 ncu --set full --clock-control none --import-source on -k regex:"k_solve_fused" --launch-skip 2 --launch-count 1 -o gpurun_out/final/fused -f python tools/prof_solve.py --config 1 --reps 2 > /dev/null 2>&1
 python tools/ncu_sum.py gpurun_out/final/fused.ncu-rep > gpurun_out/final/fused.summary.txt 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_learn_fast" --launch-skip 29 --launch-count 1 -o gpurun_out/final/learn32 -f python tools/prof_solve.py --config 2 --reps 0 > /dev/null 2>&1
+python tools/ncu_sum.py gpurun_out/final/learn32.ncu-rep > gpurun_out/final/learn32.summary.txt 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_corr_tc2" --launch-skip 20 --launch-count 1 -o gpurun_out/final/k1 -f python tools/prof_solve.py --config 2 --reps 0 > /dev/null 2>&1
+python tools/ncu_sum.py gpurun_out/final/k1.ncu-rep > gpurun_out/final/k1.summary.txt 2>&1
 python tools/time_defaults.py 4096 > gpurun_out/final/other_configs.txt 2>&1
+python tools/ncu_lines.py gpurun_out/final/learn32.ncu-rep 25 > gpurun_out/final/learn32.source_lines.txt 2>&1
+rm -f gpurun_out/final/*.ncu-rep   # gpurun merges at most 64 MiB back
 nvidia-smi --query-gpu=name,clocks.max.sm,clocks.max.mem --format=csv > gpurun_out/final/smi.txt
