@@ -640,30 +640,6 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
   }
   const Work& w = ctx->w;
   cudaStream_t s = ctx->stream;
-#ifdef CL_EXP_L2_PERSIST  // experiment: keep the per-signal Gram matrices resident in L2
-  {
-    static bool once = false;
-    int maxp = 0, maxw = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
-    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
-    const size_t gbytes = (size_t)(B * cap * cap) * sizeof(double);
-    if (w.gram && maxp > 0) {
-      if (!once) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
-        fprintf(stderr, "[l2] persisting max %d MB window max %d MB gram %zu MB\n", maxp >> 20, maxw >> 20, gbytes >> 20);
-        once = true;
-      }
-      cudaStreamAttrValue av{};
-      av.accessPolicyWindow.base_ptr = w.gram;
-      av.accessPolicyWindow.num_bytes = std::min<size_t>(gbytes, (size_t)maxw);
-      av.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)CL_EXP_L2_PERSIST / 100.0);
-      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
-      cudaGetLastError();
-    }
-  }
-#endif
   cl_stats stats{};
   stats.corr_path = (tensor || sep_tc) ? 1 : gemv ? 3 : 0;
 
