@@ -74,3 +74,34 @@ def test_ragged_rows_view_counts():
     res = cl.BatchSolveResult(None, None, np.zeros(3), np.zeros(3), np.zeros(3, bool),
                               np.zeros(3, np.int32), r, r)
     assert res.support[1].tolist() == [4, 5, 6, 7]
+
+
+def test_header_is_plain_c_and_links(built_lib, tmp_path):
+    """include/clomp_b200.h compiles as C99 (pedantic) and as C++, and a C
+    program using it links against the library (no CUDA, torch or C++ types in
+    the boundary)."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    inc = HEADER.parent
+    src = tmp_path / "use_abi.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "clomp_b200.h"\n'
+        "int main(void) {\n"
+        "  cl_config c; int64_t sz[4]; cl_config_default(&c); cl_abi_struct_sizes(sz);\n"
+        "  cl_result r = {0}; (void)r;\n"
+        '  printf("%d %d %lld %lld\\n", cl_abi_version(), (int)(c.th * 10), (long long)sz[0], (long long)sizeof(cl_config));\n'
+        "  return sz[0] == (int64_t)sizeof(cl_config) && sz[1] == (int64_t)sizeof(cl_result) ? 0 : 1;\n}\n")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", f"-I{inc}",
+                    "-fsyntax-only", str(src)], check=True)
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", f"-I{inc}", "-fsyntax-only", "-x", "c++",
+                    str(src)], check=True)
+    exe = tmp_path / "use_abi"
+    lib = Path(built_lib)
+    subprocess.run(["gcc", "-std=c99", f"-I{inc}", str(src), "-o", str(exe), f"-L{lib.parent}",
+                    "-lclomp_b200", f"-Wl,-rpath,{lib.parent}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.split()[:2] == ["1", "7"]
