@@ -183,11 +183,31 @@ __device__ __forceinline__ void exact_scores8(const SolveParams& p, const Work& 
   for (int u = 0; u < 8; ++u) out[u] = u < cnt ? fabs(warp_sum(acc[u])) : -1.0;
 }
 
+// One atom: the same per-lane summation order as exact_scores8 (so an atom
+// scores bitwise the same either way), with the row loads of eight 128-float
+// chunks issued ahead of the dependent FMA chain — a rescoring warp is alone on
+// its scheduler, and two chunks in flight fetched a 4096-row atom at ~10 GB/s.
 __device__ __forceinline__ double exact_score(const SolveParams& p, const Work& w,
                                               const double* r, int64_t j, int lane) {
-  double v[8];
-  exact_scores8(p, w, r, j, 1, v, lane);
-  return v[0];
+  if (p.sep) {
+    double v[8];
+    exact_scores8(p, w, r, j, 1, v, lane);
+    return v[0];
+  }
+  CL_CHECK(j >= 0 && j < p.n);
+  const float* a = w.at32 + j * p.ldm;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int64_t i = 4 * lane; i < p.ldm; i += 128) {
+    const float4 av = *reinterpret_cast<const float4*>(a + i);
+    const double2 r01 = *reinterpret_cast<const double2*>(r + i);
+    const double2 r23 = *reinterpret_cast<const double2*>(r + i + 2);
+    acc = fma(f2d(av.x), r01.x, acc);
+    acc = fma(f2d(av.y), r01.y, acc);
+    acc = fma(f2d(av.z), r23.x, acc);
+    acc = fma(f2d(av.w), r23.y, acc);
+  }
+  return fabs(warp_sum(acc));
 }
 
 // Support update of one picked atom (lane 0): skip atoms already selected,
@@ -235,7 +255,10 @@ struct ScoreResid {
   const Work& w;
   const double* r;
   __device__ __forceinline__ void operator()(int64_t j0, int cnt, double (&out)[8], int lane) const {
-    exact_scores8(p, w, r, j0, cnt, out, lane);
+    if (cnt == 1)
+      out[0] = exact_score(p, w, r, j0, lane);
+    else
+      exact_scores8(p, w, r, j0, cnt, out, lane);
   }
 };
 
@@ -274,9 +297,19 @@ struct ScoreGram {
 
 // One pass over the atoms inside the band (ascending atom order).  Pass 0
 // returns the exact maximum; pass 1 picks every atom attaining M.
+// Pass 0 also records what it scored — lane k keeps the k-th atom and its exact
+// score (atoms are visited in ascending order) — so a band of up to 32 atoms,
+// i.e. practically every one, is decided without scoring anything twice.
+struct BandRec {
+  int n = 0;        // atoms scored so far
+  int atom = -1;    // lane k: the k-th of them ...
+  double val = -1;  // ... and its score
+};
+
 template <class Scorer>
 __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, double cut,
-                            const Scorer& score, int pass, double M, PickState& ps, int lane) {
+                            const Scorer& score, int pass, double M, PickState& ps, int lane,
+                            BandRec& rec) {
   const Cand* cd = w.cand + b * p.ntile;
   for (int64_t t0 = 0; t0 < p.ntile; t0 += 32) {
     const int64_t tl = t0 + lane;
@@ -297,8 +330,16 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             if (u >= cnt) continue;
-            if (pass == 0) M = fmax(M, v[u]);
-            else if (v[u] == M && lane == 0) pick_atom(p, w, b, (int32_t)(j0 + u), ps);
+            if (pass == 0) {
+              M = fmax(M, v[u]);
+              if (lane == (rec.n & 31)) {
+                rec.atom = (int)(j0 + u);
+                rec.val = v[u];
+              }
+              ++rec.n;
+            } else if (v[u] == M && lane == 0) {
+              pick_atom(p, w, b, (int32_t)(j0 + u), ps);
+            }
           }
         }
       } else {
@@ -318,6 +359,18 @@ __device__ double band_pass(const SolveParams& p, const Work& w, int64_t b, doub
         }
         if (pass == 0) {
           M = fmax(M, fmax(va, vb));
+          if (lane == (rec.n & 31)) {
+            rec.atom = ja;
+            rec.val = va;
+          }
+          ++rec.n;
+          if (jb >= 0) {
+            if (lane == (rec.n & 31)) {
+              rec.atom = jb;
+              rec.val = vb;
+            }
+            ++rec.n;
+          }
         } else if (lane == 0) {
           if (va == M) pick_atom(p, w, b, ja, ps);
           if (jb >= 0 && vb == M) pick_atom(p, w, b, jb, ps);
@@ -336,8 +389,19 @@ __device__ void select_near_tie_with(const SolveParams& p, const Work& w, int64_
   PickState ps{t_old, 0, 0};
   if (lane == 0) atomicAdd(&w.counters[kRescanTotal], 1);
   const double cut = v1 - 2.0 * delta;
-  const double M = band_pass(p, w, b, cut, score, 0, -1.0, ps, lane);
-  if (M > 0.0) band_pass(p, w, b, cut, score, 1, M, ps, lane);
+  BandRec rec;
+  const double M = band_pass(p, w, b, cut, score, 0, -1.0, ps, lane, rec);
+  if (M > 0.0) {
+    if (rec.n <= 32) {  // every scored atom is on a lane, in ascending atom order
+      for (int k = 0; k < rec.n; ++k) {
+        const int a = __shfl_sync(kFull, rec.atom, k);
+        const double v = __shfl_sync(kFull, rec.val, k);
+        if (v == M && lane == 0) pick_atom(p, w, b, a, ps);
+      }
+    } else {
+      band_pass(p, w, b, cut, score, 1, M, ps, lane, rec);
+    }
+  }
   if (lane == 0) pick_finish(p, w, b, ps);
   __syncwarp();
 }
