@@ -879,10 +879,14 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     stats.total_ms = t;
     for (auto& e : ev) cudaEventDestroy(e);
   } else {
-    // Graph path: the iterations are captured in chunks of kChunkIters into
+    // Graph path: the iterations are captured in chunks of chunk_iters into
     // CUDA graphs (cached per launch configuration) and replayed back to back.
     // After each chunk the active-signal count is copied to pinned memory; the
     // host checks it one chunk behind, so the GPU never waits for the host.
+    // The host sees a finished batch one chunk late, so a solve of at most two
+    // chunks runs every iteration anyway: it is captured as ONE graph (no
+    // mid-solve counter copy breaking the programmatic-launch chain).
+    const int chunk_iters = p.max_outer <= 2 * kChunkIters ? p.max_outer : kChunkIters;
     GraphKey key{};
     key.p = p;
     key.w = w;
@@ -897,18 +901,18 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
       ctx->graphs.assign(0, nullptr);
       ctx->gkey = key;
     }
-    const int nchunks = (p.max_outer + kChunkIters - 1) / kChunkIters;
+    const int nchunks = (p.max_outer + chunk_iters - 1) / chunk_iters;
     if ((int)ctx->graphs.size() < nchunks) ctx->graphs.resize((size_t)nchunks, nullptr);
     // chunks whose iterations learn in direct form launch ~4 kernels per epoch:
     // they are enqueued directly (like the NCCL chunks), not captured
     auto chunk_direct = [&](int ch) {
-      return dfrom > 0 && std::min(p.max_outer, (ch + 1) * kChunkIters) >= dfrom;
+      return dfrom > 0 && std::min(p.max_outer, (ch + 1) * chunk_iters) >= dfrom;
     };
     for (int ch = 0; ch < nchunks && !colshard; ++ch) {
       if (chunk_direct(ch)) continue;
       if (!ctx->graphs[(size_t)ch]) {
-        const int o0 = ch * kChunkIters + 1;
-        const int o1 = std::min(p.max_outer, o0 + kChunkIters - 1);
+        const int o0 = ch * chunk_iters + 1;
+        const int o1 = std::min(p.max_outer, o0 + chunk_iters - 1);
         int64_t dummy = 0;
         cudaGraph_t g = nullptr;
         CL_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
@@ -930,8 +934,8 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
     enqueue_count(p, c, mode, cap, &per_iter);
     for (int ch = 0; ch < nchunks; ++ch) {
       if (colshard || chunk_direct(ch)) {  // NCCL / direct-form epochs inside: not captured
-        const int o0 = ch * kChunkIters + 1;
-        const int o1c = std::min(p.max_outer, o0 + kChunkIters - 1);
+        const int o0 = ch * chunk_iters + 1;
+        const int o1c = std::min(p.max_outer, o0 + chunk_iters - 1);
         int64_t dummy = 0;
         for (int o = o0; o <= o1c; ++o) enqueue_iteration(o, &dummy);
         if (!enq_ok) return fail(ctx, CL_ERR_CUDA, "clomp: launch or collective failed");
@@ -942,12 +946,12 @@ int solve_core(cl_ctx* ctx, const float* y_dev, int layout_ref, int64_t B,
         CL_CUDA(ctx, cudaGraphLaunch(ctx->graphs[(size_t)ch], s));
       }
       cudaEventRecord(ctx->chunk_ev[ch & 1], s);
-      const int o1 = std::min(p.max_outer, (ch + 1) * kChunkIters);
-      launches += per_iter * (o1 - ch * kChunkIters);
+      const int o1 = std::min(p.max_outer, (ch + 1) * chunk_iters);
+      launches += per_iter * (o1 - ch * chunk_iters);
       outer_done = o1;
       if (ch >= 1) {
         CL_CUDA(ctx, cudaEventSynchronize(ctx->chunk_ev[(ch - 1) & 1]));
-        const int o_prev = std::min(p.max_outer, ch * kChunkIters);  // last iteration of chunk ch - 1
+        const int o_prev = std::min(p.max_outer, ch * chunk_iters);  // last iteration of chunk ch - 1
         if (ctx->h_chunk[((ch - 1) & 1) * kNumCounters + active_slot(o_prev)] == 0) break;
       }
     }
